@@ -1,0 +1,36 @@
+# Builds the B200 product library (sm_100a) and the CPU oracle.
+#   make            -> paper_2304_12745_b200/lib/libufpgd_gpu.so + oracle/_build/libufpgd_oracle.so
+NVCC     ?= nvcc
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC -Xcompiler -Wall -Iinclude -Ipaper_2304_12745_b200/csrc
+PKG      := paper_2304_12745_b200
+LIBDIR   := $(PKG)/lib
+OBJDIR   := build/obj
+SRCS_CU  := $(PKG)/csrc/kernels.cu
+SRCS_CPP := $(PKG)/csrc/capi.cpp $(PKG)/csrc/host_gen.cpp
+CXX      ?= g++
+CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -Iinclude -I$(PKG)/csrc -I/usr/local/cuda/include
+OBJS     := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(SRCS_CU)) $(patsubst $(PKG)/csrc/%.cpp,$(OBJDIR)/%.o,$(SRCS_CPP))
+HDRS     := include/ufpgd_gpu.h $(PKG)/csrc/ufpgd_internal.h
+
+all: $(LIBDIR)/libufpgd_gpu.so oracle
+
+$(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; exit 1)
+
+$(OBJDIR)/%.o: $(PKG)/csrc/%.cpp $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(LIBDIR)/libufpgd_gpu.so: $(OBJS)
+	@mkdir -p $(LIBDIR)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl -lpthread
+
+oracle:
+	$(MAKE) -s -C oracle
+
+clean:
+	rm -rf build $(LIBDIR) oracle/_build
+
+.PHONY: all oracle clean

@@ -1,0 +1,202 @@
+/*
+ * ufpgd_gpu.h — C ABI of the B200-native batched PA-aware precoder solver.
+ *
+ * This is the drop-in boundary for the reference's hot path: the precoder
+ * entry points of /root/reference/proj/core (namespace ufpgd). Each function
+ * below names the reference interface it replaces. The C++ API in
+ * include/ufpgd/ (C++ headers) restores the reference signatures, validation and
+ * exception types on top of this ABI; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *  - Matrices are batches of K x M complex matrices in the reference's storage
+ *    (Eigen col-major, column m = antenna m, types.hpp:14-20), i.e. row-major
+ *    [B][M][K] arrays of ufpgd_c64 (layout-identical to CUDA float2 and to
+ *    std::complex<float>).
+ *  - Functions without a _host suffix take DEVICE pointers for the batch
+ *    arrays, enqueue work on `stream` (a cudaStream_t, NULL = legacy default
+ *    stream) of `device`, and return without synchronising. Small parameter
+ *    arrays (lambda, eta, c, v0) are HOST pointers and are copied at the call.
+ *  - _host functions take HOST pointers (pinned or pageable), run
+ *    synchronously and pipeline the host<->device copies with the kernels.
+ *  - No exceptions cross the ABI: 0 on success or a negative UFPGD_E* status,
+ *    with ufpgd_gpu_last_error() giving the message of the calling thread's
+ *    last failure.
+ *  - One CUDA context per device; calls on a given device are serialised by
+ *    the caller (the reference API is reentrant per realization; batches are
+ *    the unit here).
+ */
+#ifndef UFPGD_GPU_H
+#define UFPGD_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UFPGD_GPU_ABI_VERSION 1
+
+typedef struct {
+  float re, im;
+} ufpgd_c64;
+
+typedef void* ufpgd_stream_t; /* cudaStream_t */
+
+enum ufpgd_status {
+  UFPGD_OK = 0,
+  UFPGD_EINVAL_SHAPE = -1, /* std::invalid_argument on shapes (pgd.cpp:19-24) */
+  UFPGD_EINVAL_PARAM = -2, /* std::invalid_argument on lambda/eta/etc. */
+  UFPGD_EDIVERGED = -3,    /* DivergenceError (errors.hpp:18-25) */
+  UFPGD_ECONVERGENCE = -4, /* ConvergenceError (errors.hpp:27-31) */
+  UFPGD_ECUDA = -5,
+  UFPGD_ENCCL = -6,
+  UFPGD_ENOTSUP = -7
+};
+
+enum ufpgd_w0_mode {
+  UFPGD_W0_ZERO = 0,   /* W0 = 0 (BASELINE configs 1, 2, 4, 5) */
+  UFPGD_W0_CONJ_H = 1, /* W0 = H^* — the reference default (pgd.cpp:184, unfolded.cpp:96) */
+  UFPGD_W0_GIVEN = 2   /* W0 from the caller (the `start` argument) */
+};
+
+/* Largest supported layer count of one unfolded launch and user count. */
+#define UFPGD_MAX_LAYERS 256
+#define UFPGD_MAX_USERS 64
+
+int ufpgd_gpu_abi_version(void);
+const char* ufpgd_gpu_last_error(void);
+int ufpgd_gpu_device_count(int* count);
+
+/*
+ * Batched unfolded forward pass — replaces ufpgd::forward / forward_infer
+ * (unfolded.hpp:64-74, unfolded.cpp:83-156) applied to B independent
+ * channels. Layer i uses step eta[i] and threshold lambda[i]*eta[i]
+ * (computed in FP64 here, then rounded to FP32). c[k] = sigma_nu*sqrt(gamma_k)
+ * (SystemConfig::constraint_diag, system_config.cpp:45-47). Parameters are NOT
+ * projected or checked against the box here (the C++ layer does that exactly
+ * like unfolded.cpp:19-35); only lambda >= 0 and eta > 0 are required.
+ *
+ * Outputs (device, any may be NULL):
+ *   W[B][M][K]        final precoders
+ *   diverged_at[B]    first 0-based layer whose step image was non-finite, -1 if none
+ *                     (DivergenceError index semantics of unfolded.cpp:120-125)
+ *   l21[B]            ||W_b||_{2,1} (metrics.cpp:10-16), NaN when diverged
+ *   active[B]         #{m : ||w_m||^2 > 0} (pgd.cpp:23-29), -1 when diverged
+ *   stats[3] (double) {sum_b alpha*||W_b||_{2,1}, sum_b active_b, #diverged},
+ *                     sums over non-diverged realizations, deterministic order.
+ */
+int ufpgd_gpu_unfolded_forward(const ufpgd_c64* H, int64_t B, int K, int M,
+                               const double* lambda, const double* eta, int L,
+                               const double* c, int w0_mode, const ufpgd_c64* W0,
+                               ufpgd_c64* W, int32_t* diverged_at, float* l21,
+                               int32_t* active, double* stats, double alpha,
+                               int device, ufpgd_stream_t stream);
+
+/*
+ * Batched fixed-step power iteration on H^T H^* — replaces
+ * ufpgd::lipschitz_bound's `exact` (pgd.hpp:85-89, pgd.cpp:120-169) with the
+ * BASELINE rule: exactly `steps` applications from the reference's shared
+ * start vector (Rng(0x1F2E3D4C5B6A7988), pgd.cpp:131-134; pass v0 = NULL) or
+ * from a caller v0[M] (host). Lout[b] = Re(v^H w) of the last application;
+ * 0 for an all-zero channel (pgd.cpp:150-153).
+ */
+int ufpgd_gpu_power_iteration(const ufpgd_c64* H, int64_t B, int K, int M,
+                              const ufpgd_c64* v0, int steps, float* Lout, int device,
+                              ufpgd_stream_t stream);
+
+/*
+ * Batched plain PGD at a fixed step per realization — replaces
+ * ufpgd::solve_pgd (pgd.hpp:102-110, pgd.cpp:178-268) with trace_every = 0 and
+ * residual_tol = 0 over B channels. eta_in[B] (device) gives each
+ * realization's step; with eta_in == NULL the kernel first runs `power_steps`
+ * power iterations on its own channel and uses eta = 1/L (BASELINE config 3),
+ * writing the step it used to eta_out[B] (nullable). Threshold = lambda*eta.
+ * diverged_at holds the 1-based iteration of the first non-finite step image
+ * (pgd.cpp:231-235 semantics), -1 if none. Other outputs as for
+ * ufpgd_gpu_unfolded_forward.
+ */
+int ufpgd_gpu_pgd_fixed(const ufpgd_c64* H, int64_t B, int K, int M, const float* eta_in,
+                        int power_steps, double lambda, int64_t iters, const double* c,
+                        int w0_mode, const ufpgd_c64* W0, ufpgd_c64* W, int32_t* diverged_at,
+                        float* l21, int32_t* active, float* eta_out, double* stats,
+                        double alpha, int device, ufpgd_stream_t stream);
+
+/*
+ * General layer sweep on any (K <= 64, M) shape — the per-realization
+ * building blocks of pgd.hpp:41-72 (grad_f, prox_l21, pgd_step) and the taped
+ * forward (ForwardOptions::with_tape / with_iterates, unfolded.hpp:40-62).
+ * Runs L layers with raw per-layer (eta[i], thr[i]) — NO box check, thr given
+ * directly (prox_l21 is eta = 0, thr = t; pgd_step is eta, lambda*eta).
+ * mode 0: layers; mode 1: write grad_f(W0) to W and stop (W0 via w0_mode).
+ * residual_tol > 0 enables solve_pgd's relative-change stop
+ * (pgd.cpp:246-260) with iterations[B] receiving the steps taken.
+ * Optional tapes (device, NULL skips): iterates[(L+1)][B][M][K],
+ * tape_v[L][B][M][K] (step images), tape_norms / tape_shrink [L][B][M].
+ * diverged_at: 0-based layer (index_base = 0) or 1-based iteration (1).
+ */
+int ufpgd_gpu_layers_general(const ufpgd_c64* H, int64_t B, int K, int M, const double* eta,
+                             const double* thr, int L, const double* c, int w0_mode,
+                             const ufpgd_c64* W0, int mode, double residual_tol, int index_base,
+                             ufpgd_c64* W, int32_t* diverged_at, int64_t* iterations,
+                             ufpgd_c64* iterates, ufpgd_c64* tape_v, float* tape_norms,
+                             float* tape_shrink, int device, ufpgd_stream_t stream);
+
+/*
+ * Host-buffer (end-to-end) unfolded forward: H, W0, W, diverged_at and stats
+ * are HOST pointers. The batch is streamed through the device in chunks with
+ * H2D copy, kernel and D2H copy overlapped on separate streams; pageable
+ * buffers are staged through pinned memory. Returns UFPGD_EDIVERGED (after
+ * finishing the whole batch) when any realization diverged.
+ */
+int ufpgd_gpu_unfolded_forward_host(const ufpgd_c64* H, int64_t B, int K, int M,
+                                    const double* lambda, const double* eta, int L,
+                                    const double* c, int w0_mode, const ufpgd_c64* W0,
+                                    ufpgd_c64* W, int32_t* diverged_at, double* stats,
+                                    double alpha, int device);
+
+/* Same for plain PGD with the in-kernel 1/L step (config 3 end to end). */
+int ufpgd_gpu_pgd_fixed_host(const ufpgd_c64* H, int64_t B, int K, int M, int power_steps,
+                             double lambda, int64_t iters, const double* c, int w0_mode,
+                             const ufpgd_c64* W0, ufpgd_c64* W, int32_t* diverged_at,
+                             float* eta_out, double* stats, double alpha, int device);
+
+/*
+ * Single-process multi-GPU: shard the batch contiguously over devices
+ * 0..ngpus-1 (one host thread and stream per device) and reduce the three
+ * summary statistics with one ncclAllReduce over an NCCL communicator built by
+ * ufpgd_gpu_init (ncclCommInitAll). Host buffers, synchronous.
+ */
+int ufpgd_gpu_init(int ngpus);
+int ufpgd_gpu_shutdown(void);
+int ufpgd_gpu_unfolded_forward_sharded(const ufpgd_c64* H, int64_t B, int K, int M,
+                                       const double* lambda, const double* eta, int L,
+                                       const double* c, ufpgd_c64* W, int32_t* diverged_at,
+                                       double* stats, double alpha);
+
+/*
+ * Seeded synthetic input generation (harness side of SURVEY §8d, not timed):
+ * realization i = first_index + b is generate_channel(Rng::stream(seed_h, i))
+ * (channel.cpp:7-16, rng.cpp:19-40), row k scaled in FP64 by
+ * 10^(-u_k * gain_range_db / 20) with u_k = Rng::stream(seed_g, i).uniform()
+ * (gain_range_db = 0 disables), then rounded once to complex64. Host output
+ * [B][M][K]; `threads` host threads (<= 0: all).
+ */
+int ufpgd_generate_channels(uint64_t seed_h, uint64_t seed_g, double gain_range_db,
+                            int64_t first_index, int64_t B, int K, int M, ufpgd_c64* H,
+                            int threads);
+
+/* The reference's power-iteration start vector (pgd.cpp:131-134), FP64 -> c64. */
+int ufpgd_power_v0(int M, ufpgd_c64* v0);
+
+/*
+ * BASELINE layer parameters: Rng::stream(seed_p, 0) draws in pack order
+ * (lambda_0, mu_0, lambda_1, mu_1, ...) with lambda = 0.01 + 0.09u and
+ * mu = (0.5 + u) / mp_bound(K, M). Raw (unprojected) FP64 values.
+ */
+int ufpgd_layer_params(uint64_t seed_p, int L, int K, int M, double* lambda, double* eta);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* UFPGD_GPU_H */

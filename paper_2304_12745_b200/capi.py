@@ -1,0 +1,288 @@
+"""ctypes bindings of the C ABI (include/ufpgd_gpu.h).
+
+Every entry point here maps one-to-one onto an ``extern "C"`` function of
+``libufpgd_gpu.so``; status codes become the reference's exception types
+(errors.hpp:8-39): ``ValueError`` for ``std::invalid_argument``,
+``DivergenceError(index)`` and ``ConvergenceError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "lib", "libufpgd_gpu.so")
+
+OK, EINVAL_SHAPE, EINVAL_PARAM, EDIVERGED, ECONVERGENCE, ECUDA, ENCCL, ENOTSUP = 0, -1, -2, -3, -4, -5, -6, -7
+W0_ZERO, W0_CONJ_H, W0_GIVEN = 0, 1, 2
+
+
+class UfpgdError(RuntimeError):
+    """A CUDA / NCCL / unsupported-shape failure of the product library."""
+
+
+class DivergenceError(RuntimeError):
+    """errors.hpp:18-25 — non-finite iterate; ``index`` is the 0-based layer
+    (forward) or 1-based iteration (solve_pgd) of the first failure."""
+
+    def __init__(self, what: str, index: int, per_realization=None):
+        super().__init__(what)
+        self.index = index
+        self.diverged_at = per_realization
+
+
+class ConvergenceError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _LIB
+
+
+def lib():
+    """Loads the CUDA library; raises (never falls back) when it is absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB):
+            raise ImportError(f"{_LIB} is missing: run `make` (or __graft_entry__.build()) first; "
+                              "there is no CPU fallback for the ufpgd hot path")
+        L = C.CDLL(_LIB)
+        i, d, i64, u64, P = C.c_int, C.c_double, C.c_int64, C.c_uint64, C.c_void_p
+        sigs = {
+            "ufpgd_gpu_abi_version": (i, []),
+            "ufpgd_gpu_last_error": (C.c_char_p, []),
+            "ufpgd_gpu_device_count": (i, [P]),
+            "ufpgd_gpu_unfolded_forward": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, P, P, P, d, i, P]),
+            "ufpgd_gpu_power_iteration": (i, [P, i64, i, i, P, i, P, i, P]),
+            "ufpgd_gpu_pgd_fixed": (i, [P, i64, i, i, P, i, d, i64, P, i, P, P, P, P, P, P, P, d, i, P]),
+            "ufpgd_gpu_layers_general": (i, [P, i64, i, i, P, P, i, P, i, P, i, d, i, P, P, P, P, P, P, P, i, P]),
+            "ufpgd_gpu_unfolded_forward_host": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, P, d, i]),
+            "ufpgd_gpu_pgd_fixed_host": (i, [P, i64, i, i, i, d, i64, P, i, P, P, P, P, P, d, i]),
+            "ufpgd_gpu_init": (i, [i]),
+            "ufpgd_gpu_shutdown": (i, []),
+            "ufpgd_gpu_unfolded_forward_sharded": (i, [P, i64, i, i, P, P, i, P, P, P, P, d]),
+            "ufpgd_generate_channels": (i, [u64, u64, d, i64, i64, i, i, P, i]),
+            "ufpgd_power_v0": (i, [i, P]),
+            "ufpgd_layer_params": (i, [u64, i, i, i, P, P]),
+        }
+        for name, (res, args) in sigs.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def abi_version() -> int:
+    return lib().ufpgd_gpu_abi_version()
+
+
+def _check(rc: int, diverged=None, index_base: int = 0):
+    if rc == OK:
+        return
+    msg = lib().ufpgd_gpu_last_error().decode()
+    if rc in (EINVAL_SHAPE, EINVAL_PARAM):
+        raise ValueError(msg)
+    if rc == EDIVERGED:
+        idx = -1
+        if diverged is not None:
+            d = np.asarray(diverged)
+            bad = d[d >= 0]
+            idx = int(bad.min()) if bad.size else -1
+        raise DivergenceError(msg, idx, diverged)
+    if rc == ECONVERGENCE:
+        raise ConvergenceError(msg)
+    raise UfpgdError(f"ufpgd status {rc}: {msg}")
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(-1))
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _check_batch(H):
+    import torch
+
+    if not (isinstance(H, torch.Tensor) and H.is_cuda and H.dtype == torch.complex64 and H.dim() == 3
+            and H.is_contiguous()):
+        raise ValueError("H must be a contiguous CUDA complex64 tensor [B, M, K]")
+    B, M, K = H.shape
+    return B, K, M
+
+
+def unfolded_forward(H, lambda_, eta, c, *, w0_mode: int = W0_ZERO, W0=None, alpha: float = 1.0,
+                     want_stats: bool = True, want_per_realization: bool = False, out=None,
+                     stream=None):
+    """Batched ufpgd::forward (unfolded.cpp:83-156) on device tensors.
+
+    Returns dict(W=[B,M,K] complex64, diverged_at=int32[B], l21, active,
+    stats=float64[3]) with the optional entries None when not requested.
+    Asynchronous on ``stream``; divergence is reported in ``diverged_at`` /
+    ``stats[2]`` rather than raised (the caller decides, as with the reference's
+    per-index slots)."""
+    import torch
+
+    B, K, M = _check_batch(H)
+    lam, et, cc = _f64(lambda_), _f64(eta), _f64(c)
+    if lam.size != et.size:
+        raise ValueError("lambda and eta must have one entry per layer")
+    dev = H.device
+    W = out if out is not None else torch.empty_like(H)
+    div = torch.empty(B, dtype=torch.int32, device=dev)
+    l21 = torch.empty(B, dtype=torch.float32, device=dev) if want_per_realization else None
+    act = torch.empty(B, dtype=torch.int32, device=dev) if want_per_realization else None
+    stats = torch.empty(3, dtype=torch.float64, device=dev) if want_stats else None
+    rc = lib().ufpgd_gpu_unfolded_forward(
+        _ptr(H), B, K, M, _ptr(lam), _ptr(et), lam.size, _ptr(cc), w0_mode, _ptr(W0), _ptr(W), _ptr(div),
+        _ptr(l21), _ptr(act), _ptr(stats), float(alpha), dev.index or 0, _stream_ptr(stream))
+    _check(rc)
+    return dict(W=W, diverged_at=div, l21=l21, active=act, stats=stats)
+
+
+def power_iteration(H, steps: int = 30, v0=None, stream=None):
+    """Batched fixed-step lipschitz_bound (pgd.cpp:120-169, BASELINE 30-step rule)."""
+    import torch
+
+    B, K, M = _check_batch(H)
+    Lout = torch.empty(B, dtype=torch.float32, device=H.device)
+    v = None if v0 is None else np.ascontiguousarray(v0, dtype=np.complex64)
+    rc = lib().ufpgd_gpu_power_iteration(_ptr(H), B, K, M, _ptr(v), steps, _ptr(Lout), H.device.index or 0,
+                                         _stream_ptr(stream))
+    _check(rc)
+    return Lout
+
+
+def pgd_fixed(H, lambda_: float, iters: int, c, *, eta=None, power_steps: int = 30,
+              w0_mode: int = W0_CONJ_H, W0=None, alpha: float = 1.0, want_per_realization=False,
+              stream=None):
+    """Batched ufpgd::solve_pgd at a fixed step (pgd.cpp:178-268, trace off,
+    residual_tol 0). ``eta`` (device float32 [B]) or the in-kernel 1/L."""
+    import torch
+
+    B, K, M = _check_batch(H)
+    cc = _f64(c)
+    dev = H.device
+    W = torch.empty_like(H)
+    div = torch.empty(B, dtype=torch.int32, device=dev)
+    eta_out = torch.empty(B, dtype=torch.float32, device=dev)
+    l21 = torch.empty(B, dtype=torch.float32, device=dev) if want_per_realization else None
+    act = torch.empty(B, dtype=torch.int32, device=dev) if want_per_realization else None
+    stats = torch.empty(3, dtype=torch.float64, device=dev)
+    rc = lib().ufpgd_gpu_pgd_fixed(_ptr(H), B, K, M, _ptr(eta), power_steps, float(lambda_), int(iters),
+                                   _ptr(cc), w0_mode, _ptr(W0), _ptr(W), _ptr(div), _ptr(l21), _ptr(act),
+                                   _ptr(eta_out), _ptr(stats), float(alpha), dev.index or 0,
+                                   _stream_ptr(stream))
+    _check(rc)
+    return dict(W=W, diverged_at=div, eta=eta_out, l21=l21, active=act, stats=stats)
+
+
+def layers_general(H, eta, thr, c, *, w0_mode: int = W0_CONJ_H, W0=None, mode: int = 0,
+                   residual_tol: float = 0.0, index_base: int = 0, iterates: bool = False,
+                   tape: bool = False, stream=None):
+    """General-shape layer sweep with raw (eta, thr) per layer and optional
+    tapes (unfolded.hpp:40-62); mode 1 returns grad_f(W0) (pgd.cpp:68-83)."""
+    import torch
+
+    B, K, M = _check_batch(H)
+    et, th, cc = _f64(eta), _f64(thr), _f64(c)
+    L = 1 if mode == 1 else et.size
+    dev = H.device
+    W = torch.empty_like(H)
+    div = torch.empty(B, dtype=torch.int32, device=dev)
+    its = torch.empty(B, dtype=torch.int64, device=dev)
+    itr = torch.empty((L + 1, B, M, K), dtype=torch.complex64, device=dev) if iterates else None
+    tv = torch.empty((L, B, M, K), dtype=torch.complex64, device=dev) if tape else None
+    tn = torch.empty((L, B, M), dtype=torch.float32, device=dev) if tape else None
+    ts = torch.empty((L, B, M), dtype=torch.float32, device=dev) if tape else None
+    rc = lib().ufpgd_gpu_layers_general(
+        _ptr(H), B, K, M, _ptr(et), _ptr(th), L, _ptr(cc), w0_mode, _ptr(W0), mode, float(residual_tol),
+        index_base, _ptr(W), _ptr(div), _ptr(its), _ptr(itr), _ptr(tv), _ptr(tn), _ptr(ts),
+        dev.index or 0, _stream_ptr(stream))
+    _check(rc)
+    return dict(W=W, diverged_at=div, iterations=its, iterates=itr, tape_v=tv, tape_norms=tn,
+                tape_shrink=ts)
+
+
+def unfolded_forward_host(H: np.ndarray, lambda_, eta, c, *, w0_mode: int = W0_ZERO, W0=None,
+                          alpha: float = 1.0, out: Optional[np.ndarray] = None, device: int = 0,
+                          raise_on_divergence: bool = True):
+    """End-to-end host-buffer forward (pipelined H2D / kernel / D2H)."""
+    H = np.asarray(H)
+    if H.dtype != np.complex64 or H.ndim != 3 or not H.flags.c_contiguous:
+        raise ValueError("H must be a C-contiguous complex64 array [B, M, K]")
+    B, M, K = H.shape
+    lam, et, cc = _f64(lambda_), _f64(eta), _f64(c)
+    W = out if out is not None else np.empty_like(H)
+    div = np.empty(B, dtype=np.int32)
+    stats = np.zeros(3)
+    rc = lib().ufpgd_gpu_unfolded_forward_host(_ptr(H), B, K, M, _ptr(lam), _ptr(et), lam.size, _ptr(cc),
+                                               w0_mode, _ptr(W0), _ptr(W), _ptr(div), _ptr(stats),
+                                               float(alpha), device)
+    if rc == EDIVERGED and not raise_on_divergence:
+        rc = OK
+    _check(rc, div)
+    return dict(W=W, diverged_at=div, stats=stats)
+
+
+def pgd_fixed_host(H: np.ndarray, lambda_: float, iters: int, c, *, power_steps: int = 30,
+                   w0_mode: int = W0_CONJ_H, W0=None, alpha: float = 1.0, device: int = 0,
+                   raise_on_divergence: bool = True):
+    H = np.asarray(H)
+    if H.dtype != np.complex64 or H.ndim != 3 or not H.flags.c_contiguous:
+        raise ValueError("H must be a C-contiguous complex64 array [B, M, K]")
+    B, M, K = H.shape
+    cc = _f64(c)
+    W = np.empty_like(H)
+    div = np.empty(B, dtype=np.int32)
+    eta = np.empty(B, dtype=np.float32)
+    stats = np.zeros(3)
+    rc = lib().ufpgd_gpu_pgd_fixed_host(_ptr(H), B, K, M, power_steps, float(lambda_), int(iters), _ptr(cc),
+                                        w0_mode, _ptr(W0), _ptr(W), _ptr(div), _ptr(eta), _ptr(stats),
+                                        float(alpha), device)
+    if rc == EDIVERGED and not raise_on_divergence:
+        rc = OK
+    _check(rc, div, 1)
+    return dict(W=W, diverged_at=div, eta=eta, stats=stats)
+
+
+def generate_channels(seed_h: int, seed_g: int, gain_range_db: float, first_index: int, B: int, K: int,
+                      M: int, threads: int = 0, out: Optional[np.ndarray] = None) -> np.ndarray:
+    """Seeded complex64 channels [B, M, K] (host; harness input, not timed)."""
+    H = out if out is not None else np.empty((B, M, K), dtype=np.complex64)
+    rc = lib().ufpgd_generate_channels(seed_h, seed_g, float(gain_range_db), first_index, B, K, M, _ptr(H),
+                                       threads)
+    _check(rc)
+    return H
+
+
+def power_v0(M: int) -> np.ndarray:
+    v = np.empty(M, dtype=np.complex64)
+    _check(lib().ufpgd_power_v0(M, _ptr(v)))
+    return v
+
+
+def layer_params(seed_p: int, L: int, K: int, M: int):
+    lam = np.empty(L)
+    eta = np.empty(L)
+    _check(lib().ufpgd_layer_params(seed_p, L, K, M, _ptr(lam), _ptr(eta)))
+    return lam, eta

@@ -1,0 +1,676 @@
+// C ABI of the B200 batched precoder solver (include/ufpgd_gpu.h).
+// Validation, dispatch to the fused team kernel or the general-shape kernel,
+// deterministic statistics, the pipelined host-buffer path and the
+// single-process multi-GPU path with an NCCL all-reduce of the statistics.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "ufpgd_gpu.h"
+#include "ufpgd_internal.h"
+
+using namespace ufpgd_gpu_impl;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(UFPGD_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define UFPGD_CUDA(call)                                      \
+  do {                                                        \
+    cudaError_t _e = (call);                                  \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);       \
+  } while (0)
+
+// Sets the device for the duration of a call and restores the previous one.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int check_shape(int64_t B, int K, int M) {
+  if (B < 0) return fail(UFPGD_EINVAL_SHAPE, "batch size must be >= 0");
+  if (K < 1 || M < K) return fail(UFPGD_EINVAL_SHAPE, "need 1 <= K <= M (system_config.cpp:23-27)");
+  if (K > UFPGD_MAX_USERS) return fail(UFPGD_ENOTSUP, "K exceeds UFPGD_MAX_USERS");
+  return UFPGD_OK;
+}
+
+int check_c(const double* c, int K) {
+  if (!c) return fail(UFPGD_EINVAL_PARAM, "c (constraint diagonal) is required");
+  for (int k = 0; k < K; ++k)
+    if (!std::isfinite(c[k])) return fail(UFPGD_EINVAL_PARAM, "c must be finite");
+  return UFPGD_OK;
+}
+
+bool general_fits(int K, int M) {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (optin <= 0) optin = 227 * 1024;
+  return general_smem_bytes(K, M) + 1024 <= static_cast<size_t>(optin);
+}
+
+// Finalises block partials into stats (or just frees them).
+int finish_stats(double* partials, long long n, double* stats, cudaStream_t s) {
+  if (stats && partials) {
+    cudaError_t e = launch_stats_finalize(partials, n, stats, s);
+    if (e != cudaSuccess) return cuda_fail(e, "stats_finalize");
+  }
+  if (partials) cudaFreeAsync(partials, s);
+  return UFPGD_OK;
+}
+
+// Enqueues an unfolded forward on `s` (device buffers). Used by the public
+// device API and by the chunked host path.
+int enqueue_unfolded(const float2* H, int64_t B, int K, int M, const double* lambda,
+                     const double* eta, int L, const double* c, int w0_mode, const float2* W0,
+                     float2* W, int32_t* diverged_at, float* l21, int32_t* active,
+                     double* partials, double alpha, cudaStream_t s, long long* nparts) {
+  *nparts = B;
+  if (fused_supported(K, M) && L >= 1) {
+    FusedArgs a{};
+    a.H = H;
+    a.W = W;
+    a.W0 = W0;
+    a.diverged_at = diverged_at;
+    a.l21 = l21;
+    a.active = active;
+    a.block_partials = partials;
+    a.B = B;
+    a.L = L;
+    a.w0_mode = w0_mode;
+    a.alpha = static_cast<float>(alpha);
+    for (int k = 0; k < K; ++k) a.c[k] = static_cast<float>(c[k]);
+    for (int l = 0; l < L; ++l) {
+      a.eta[l] = static_cast<float>(eta[l]);
+      a.thr[l] = static_cast<float>(lambda[l] * eta[l]);
+    }
+    cudaError_t e = launch_fused(a, false, K, M, s, nparts);
+    if (e != cudaSuccess) return cuda_fail(e, "fused unfolded kernel");
+    return UFPGD_OK;
+  }
+  if (!general_fits(K, M)) return fail(UFPGD_ENOTSUP, "(K, M) too large for the general kernel");
+  GeneralArgs g{};
+  g.H = H;
+  g.W = W;
+  g.W0 = W0;
+  g.diverged_at = diverged_at;
+  g.l21 = l21;
+  g.active = active;
+  g.block_partials = partials;
+  g.B = B;
+  g.K = K;
+  g.M = M;
+  g.L = L;
+  g.w0_mode = w0_mode;
+  g.alpha = static_cast<float>(alpha);
+  for (int k = 0; k < K; ++k) g.c[k] = static_cast<float>(c[k]);
+  for (int l = 0; l < L; ++l) {
+    g.eta[l] = static_cast<float>(eta[l]);
+    g.thr[l] = static_cast<float>(lambda[l] * eta[l]);
+  }
+  cudaError_t e = launch_general(g, s);
+  if (e != cudaSuccess) return cuda_fail(e, "general kernel");
+  return UFPGD_OK;
+}
+
+long long partial_count(int64_t B, int K, int M, bool fused_path) {
+  if (fused_path) {
+    const int rpb = fused_realizations_per_block(K, M);
+    return (B + rpb - 1) / rpb;
+  }
+  return B;
+}
+
+int check_layers(const double* lambda, const double* eta, int L) {
+  if (L < 0 || L > UFPGD_MAX_LAYERS) return fail(UFPGD_EINVAL_PARAM, "layer count out of range");
+  if (L > 0 && (!lambda || !eta)) return fail(UFPGD_EINVAL_PARAM, "lambda/eta required");
+  for (int l = 0; l < L; ++l) {
+    if (!(lambda[l] >= 0.0) || !std::isfinite(lambda[l]))
+      return fail(UFPGD_EINVAL_PARAM, "layer " + std::to_string(l) + " lambda_i < 0");
+    if (!(eta[l] > 0.0) || !std::isfinite(eta[l]))
+      return fail(UFPGD_EINVAL_PARAM, "layer " + std::to_string(l) + " eta_i <= 0");
+  }
+  return UFPGD_OK;
+}
+
+int check_w0(int w0_mode, const void* W0) {
+  if (w0_mode < 0 || w0_mode > 2) return fail(UFPGD_EINVAL_PARAM, "bad w0_mode");
+  if (w0_mode == UFPGD_W0_GIVEN && !W0) return fail(UFPGD_EINVAL_PARAM, "W0 required");
+  return UFPGD_OK;
+}
+
+// ---- NCCL, loaded lazily so the library never pins an NCCL build -----------
+typedef struct ncclComm* ncclComm_t;
+typedef int ncclResult_t;
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+std::mutex g_nccl_mu;
+Nccl g_nccl;
+std::vector<ncclComm_t> g_comms;
+constexpr int kNcclDouble = 8;  // ncclFloat64
+constexpr int kNcclSum = 0;     // ncclSum
+
+bool load_nccl() {
+  if (g_nccl.h) return true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return false;
+  g_nccl.h = h;
+  g_nccl.CommInitAll = reinterpret_cast<decltype(g_nccl.CommInitAll)>(dlsym(h, "ncclCommInitAll"));
+  g_nccl.AllReduce = reinterpret_cast<decltype(g_nccl.AllReduce)>(dlsym(h, "ncclAllReduce"));
+  g_nccl.GroupStart = reinterpret_cast<decltype(g_nccl.GroupStart)>(dlsym(h, "ncclGroupStart"));
+  g_nccl.GroupEnd = reinterpret_cast<decltype(g_nccl.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+  g_nccl.CommDestroy = reinterpret_cast<decltype(g_nccl.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+  g_nccl.GetErrorString =
+      reinterpret_cast<decltype(g_nccl.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+  return g_nccl.CommInitAll && g_nccl.AllReduce && g_nccl.GroupStart && g_nccl.GroupEnd &&
+         g_nccl.CommDestroy;
+}
+
+// Chunked host pipeline shared by the unfolded and PGD host entry points.
+// `run` enqueues the kernel for one chunk on stream s given device buffers.
+template <class Run>
+int host_pipeline(const ufpgd_c64* H, int64_t B, int K, int M, const ufpgd_c64* W0, ufpgd_c64* W,
+                  int32_t* diverged_at, float* eta_out, long long parts_per_chunk_max,
+                  int64_t chunk, double* stats, Run run) {
+  const size_t per = static_cast<size_t>(K) * M * sizeof(float2);
+  constexpr int NS = 3;
+  cudaStream_t st[NS];
+  for (int i = 0; i < NS; ++i) UFPGD_CUDA(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
+  struct Buf {
+    float2 *h = nullptr, *w = nullptr, *w0 = nullptr;
+    int32_t* div = nullptr;
+    float* eta = nullptr;
+  } buf[NS];
+  const int64_t nchunks = B == 0 ? 0 : (B + chunk - 1) / chunk;
+  double* partials = nullptr;
+  double* dstats = nullptr;
+  int rc = UFPGD_OK;
+  auto cleanup = [&] {
+    for (int i = 0; i < NS; ++i) {
+      cudaStreamSynchronize(st[i]);
+      cudaFree(buf[i].h);
+      cudaFree(buf[i].w);
+      cudaFree(buf[i].w0);
+      cudaFree(buf[i].div);
+      cudaFree(buf[i].eta);
+      cudaStreamDestroy(st[i]);
+    }
+    cudaFree(partials);
+    cudaFree(dstats);
+  };
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; i < NS && e == cudaSuccess; ++i) {
+    e = cudaMalloc(&buf[i].h, per * chunk);
+    if (e == cudaSuccess) e = cudaMalloc(&buf[i].w, per * chunk);
+    if (e == cudaSuccess && W0) e = cudaMalloc(&buf[i].w0, per * chunk);
+    if (e == cudaSuccess) e = cudaMalloc(&buf[i].div, sizeof(int32_t) * chunk);
+    if (e == cudaSuccess && eta_out) e = cudaMalloc(&buf[i].eta, sizeof(float) * chunk);
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&partials, sizeof(double) * 3 * std::max<long long>(1, parts_per_chunk_max * nchunks));
+  if (e == cudaSuccess) e = cudaMalloc(&dstats, sizeof(double) * 3);
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "host pipeline allocation");
+  }
+  std::vector<long long> part_off(nchunks + 1, 0);
+  for (int64_t ci = 0; ci < nchunks && rc == UFPGD_OK; ++ci) {
+    const int i = static_cast<int>(ci % NS);
+    const int64_t b0 = ci * chunk, nb = std::min<int64_t>(chunk, B - b0);
+    cudaStream_t s = st[i];
+    e = cudaMemcpyAsync(buf[i].h, H + b0 * K * M, per * nb, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && W0)
+      e = cudaMemcpyAsync(buf[i].w0, W0 + b0 * K * M, per * nb, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) {
+      rc = cuda_fail(e, "H2D");
+      break;
+    }
+    long long np = 0;
+    rc = run(buf[i].h, nb, buf[i].w0, buf[i].w, buf[i].div, buf[i].eta, partials + 3 * part_off[ci], &np, s);
+    if (rc != UFPGD_OK) break;
+    part_off[ci + 1] = part_off[ci] + np;
+    e = cudaMemcpyAsync(W + b0 * K * M, buf[i].w, per * nb, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && diverged_at)
+      e = cudaMemcpyAsync(diverged_at + b0, buf[i].div, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && eta_out)
+      e = cudaMemcpyAsync(eta_out + b0, buf[i].eta, sizeof(float) * nb, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "D2H");
+  }
+  double host_stats[3] = {0.0, 0.0, 0.0};
+  if (rc == UFPGD_OK) {
+    for (int i = 1; i < NS; ++i) {
+      cudaEvent_t ev;
+      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      cudaEventRecord(ev, st[i]);
+      cudaStreamWaitEvent(st[0], ev, 0);
+      cudaEventDestroy(ev);
+    }
+    e = launch_stats_finalize(partials, part_off[nchunks], dstats, st[0]);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(host_stats, dstats, sizeof(host_stats), cudaMemcpyDeviceToHost, st[0]);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st[0]);
+    if (e != cudaSuccess) rc = cuda_fail(e, "host pipeline finalize");
+  }
+  cleanup();
+  if (rc != UFPGD_OK) return rc;
+  if (stats) std::memcpy(stats, host_stats, sizeof(host_stats));
+  if (host_stats[2] > 0.0) return fail(UFPGD_EDIVERGED, "non-finite iterate in at least one realization");
+  return UFPGD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ufpgd_gpu_abi_version(void) { return UFPGD_GPU_ABI_VERSION; }
+
+const char* ufpgd_gpu_last_error(void) { return g_last_error.c_str(); }
+
+int ufpgd_gpu_device_count(int* count) {
+  if (!count) return fail(UFPGD_EINVAL_PARAM, "count is null");
+  UFPGD_CUDA(cudaGetDeviceCount(count));
+  return UFPGD_OK;
+}
+
+int ufpgd_gpu_unfolded_forward(const ufpgd_c64* H, int64_t B, int K, int M, const double* lambda,
+                               const double* eta, int L, const double* c, int w0_mode,
+                               const ufpgd_c64* W0, ufpgd_c64* W, int32_t* diverged_at, float* l21,
+                               int32_t* active, double* stats, double alpha, int device,
+                               ufpgd_stream_t stream) {
+  int rc;
+  if ((rc = check_shape(B, K, M)) || (rc = check_layers(lambda, eta, L)) || (rc = check_c(c, K)) ||
+      (rc = check_w0(w0_mode, W0)))
+    return rc;
+  if (!(alpha > 0.0)) return fail(UFPGD_EINVAL_PARAM, "alpha must be > 0");
+  if (B > 0 && (!H || !W)) return fail(UFPGD_EINVAL_PARAM, "H and W are required");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (B == 0) {
+    if (stats) UFPGD_CUDA(cudaMemsetAsync(stats, 0, 3 * sizeof(double), s));
+    return UFPGD_OK;
+  }
+  const bool fused = fused_supported(K, M) && L >= 1;
+  const long long np = partial_count(B, K, M, fused);
+  double* partials = nullptr;
+  if (stats) UFPGD_CUDA(cudaMallocAsync(&partials, sizeof(double) * 3 * np, s));
+  long long used = 0;
+  rc = enqueue_unfolded(reinterpret_cast<const float2*>(H), B, K, M, lambda, eta, L, c, w0_mode,
+                        reinterpret_cast<const float2*>(W0), reinterpret_cast<float2*>(W),
+                        diverged_at, l21, active, partials, alpha, s, &used);
+  int rc2 = finish_stats(partials, rc == UFPGD_OK ? used : 0, stats, s);
+  return rc != UFPGD_OK ? rc : rc2;
+}
+
+int ufpgd_gpu_power_iteration(const ufpgd_c64* H, int64_t B, int K, int M, const ufpgd_c64* v0,
+                              int steps, float* Lout, int device, ufpgd_stream_t stream) {
+  int rc;
+  if ((rc = check_shape(B, K, M))) return rc;
+  if (M > 1024) return fail(UFPGD_ENOTSUP, "power iteration supports M <= 1024");
+  if (steps < 1) return fail(UFPGD_EINVAL_PARAM, "steps must be >= 1");
+  if (B > 0 && (!H || !Lout)) return fail(UFPGD_EINVAL_PARAM, "H and Lout are required");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
+  if (B == 0) return UFPGD_OK;
+  PowerArgs a{};
+  a.H = reinterpret_cast<const float2*>(H);
+  a.Lout = Lout;
+  a.B = B;
+  a.K = K;
+  a.M = M;
+  a.steps = steps;
+  if (v0) {
+    std::memcpy(a.v0, v0, sizeof(float2) * M);
+  } else {
+    std::vector<ufpgd_c64> tmp(M);
+    ufpgd_power_v0(M, tmp.data());
+    std::memcpy(a.v0, tmp.data(), sizeof(float2) * M);
+  }
+  cudaError_t e = launch_power(a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "power kernel");
+  return UFPGD_OK;
+}
+
+int ufpgd_gpu_pgd_fixed(const ufpgd_c64* H, int64_t B, int K, int M, const float* eta_in,
+                        int power_steps, double lambda, int64_t iters, const double* c, int w0_mode,
+                        const ufpgd_c64* W0, ufpgd_c64* W, int32_t* diverged_at, float* l21,
+                        int32_t* active, float* eta_out, double* stats, double alpha, int device,
+                        ufpgd_stream_t stream) {
+  int rc;
+  if ((rc = check_shape(B, K, M)) || (rc = check_c(c, K)) || (rc = check_w0(w0_mode, W0))) return rc;
+  if (!(lambda >= 0.0) || !std::isfinite(lambda)) return fail(UFPGD_EINVAL_PARAM, "PgdParams: lambda must be >= 0");
+  if (iters < 0) return fail(UFPGD_EINVAL_PARAM, "PgdParams: max_iters must be >= 0");
+  if (!eta_in && power_steps < 1) return fail(UFPGD_EINVAL_PARAM, "need eta_in or power_steps >= 1");
+  if (!(alpha > 0.0)) return fail(UFPGD_EINVAL_PARAM, "alpha must be > 0");
+  if (B > 0 && (!H || !W)) return fail(UFPGD_EINVAL_PARAM, "H and W are required");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (B == 0) {
+    if (stats) UFPGD_CUDA(cudaMemsetAsync(stats, 0, 3 * sizeof(double), s));
+    return UFPGD_OK;
+  }
+  const bool fused = fused_supported(K, M) && iters >= 1;
+  const long long np = partial_count(B, K, M, fused);
+  long long used = B;
+  double* partials = nullptr;
+  if (stats) UFPGD_CUDA(cudaMallocAsync(&partials, sizeof(double) * 3 * np, s));
+  std::vector<ufpgd_c64> v0(M);
+  ufpgd_power_v0(M, v0.data());
+  if (fused) {
+    FusedArgs a{};
+    a.H = reinterpret_cast<const float2*>(H);
+    a.W = reinterpret_cast<float2*>(W);
+    a.W0 = reinterpret_cast<const float2*>(W0);
+    a.eta_in = eta_in;
+    a.eta_out = eta_out;
+    a.diverged_at = diverged_at;
+    a.l21 = l21;
+    a.active = active;
+    a.block_partials = partials;
+    a.B = B;
+    a.L = iters;
+    a.w0_mode = w0_mode;
+    a.power_steps = power_steps;
+    a.lambda = static_cast<float>(lambda);
+    a.alpha = static_cast<float>(alpha);
+    for (int k = 0; k < K; ++k) a.c[k] = static_cast<float>(c[k]);
+    std::memcpy(a.v0, v0.data(), sizeof(float2) * M);
+    cudaError_t e = launch_fused(a, true, K, M, s, &used);
+    if (e != cudaSuccess) rc = cuda_fail(e, "fused PGD kernel");
+  } else {
+    if (!general_fits(K, M)) rc = fail(UFPGD_ENOTSUP, "(K, M) too large for the general kernel");
+    float* lip = nullptr;
+    if (rc == UFPGD_OK && !eta_in) {
+      cudaError_t e = cudaMallocAsync(&lip, sizeof(float) * B, s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "alloc");
+      if (rc == UFPGD_OK) rc = ufpgd_gpu_power_iteration(H, B, K, M, v0.data(), power_steps, lip, device, stream);
+    }
+    if (rc == UFPGD_OK) {
+      GeneralArgs gA{};
+      gA.H = reinterpret_cast<const float2*>(H);
+      gA.W = reinterpret_cast<float2*>(W);
+      gA.W0 = reinterpret_cast<const float2*>(W0);
+      gA.diverged_at = diverged_at;
+      gA.l21 = l21;
+      gA.active = active;
+      gA.block_partials = partials;
+      gA.B = B;
+      gA.K = K;
+      gA.M = M;
+      gA.w0_mode = w0_mode;
+      gA.pgd = 1;
+      gA.iters = iters;
+      gA.eta_b = eta_in;
+      gA.lip_b = lip;
+      gA.eta_out = eta_out;
+      gA.lambda = static_cast<float>(lambda);
+      gA.index_base = 1;
+      gA.alpha = static_cast<float>(alpha);
+      for (int k = 0; k < K; ++k) gA.c[k] = static_cast<float>(c[k]);
+      cudaError_t e = launch_general(gA, s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "general PGD kernel");
+    }
+    if (lip) cudaFreeAsync(lip, s);
+  }
+  int rc2 = finish_stats(partials, rc == UFPGD_OK ? used : 0, stats, s);
+  return rc != UFPGD_OK ? rc : rc2;
+}
+
+int ufpgd_gpu_layers_general(const ufpgd_c64* H, int64_t B, int K, int M, const double* eta,
+                             const double* thr, int L, const double* c, int w0_mode,
+                             const ufpgd_c64* W0, int mode, double residual_tol, int index_base,
+                             ufpgd_c64* W, int32_t* diverged_at, int64_t* iterations,
+                             ufpgd_c64* iterates, ufpgd_c64* tape_v, float* tape_norms,
+                             float* tape_shrink, int device, ufpgd_stream_t stream) {
+  int rc;
+  if ((rc = check_shape(B, K, M)) || (rc = check_c(c, K)) || (rc = check_w0(w0_mode, W0))) return rc;
+  if (mode != 0 && mode != 1) return fail(UFPGD_EINVAL_PARAM, "bad mode");
+  if (L < 0 || L > UFPGD_MAX_LAYERS) return fail(UFPGD_EINVAL_PARAM, "layer count out of range");
+  if (mode == 1) L = 1;
+  if (L > 0 && (!eta || !thr)) return fail(UFPGD_EINVAL_PARAM, "eta/thr required");
+  for (int l = 0; l < L; ++l)
+    if (!(eta[l] >= 0.0) || !(thr[l] >= 0.0)) return fail(UFPGD_EINVAL_PARAM, "need eta >= 0, thr >= 0");
+  if (!(residual_tol >= 0.0)) return fail(UFPGD_EINVAL_PARAM, "residual_tol must be >= 0");
+  if (B > 0 && (!H || !W)) return fail(UFPGD_EINVAL_PARAM, "H and W are required");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
+  if (B == 0) return UFPGD_OK;
+  if (!general_fits(K, M)) return fail(UFPGD_ENOTSUP, "(K, M) too large for the general kernel");
+  GeneralArgs a{};
+  a.H = reinterpret_cast<const float2*>(H);
+  a.W = reinterpret_cast<float2*>(W);
+  a.W0 = reinterpret_cast<const float2*>(W0);
+  a.diverged_at = diverged_at;
+  a.iterations = iterations;
+  a.iterates = reinterpret_cast<float2*>(iterates);
+  a.tape_v = reinterpret_cast<float2*>(tape_v);
+  a.tape_norms = tape_norms;
+  a.tape_shrink = tape_shrink;
+  a.B = B;
+  a.K = K;
+  a.M = M;
+  a.L = L;
+  a.w0_mode = w0_mode;
+  a.mode = mode;
+  a.index_base = index_base;
+  a.residual_tol = static_cast<float>(residual_tol);
+  a.alpha = 1.f;
+  for (int k = 0; k < K; ++k) a.c[k] = static_cast<float>(c[k]);
+  for (int l = 0; l < L; ++l) {
+    a.eta[l] = static_cast<float>(eta[l]);
+    a.thr[l] = static_cast<float>(thr[l]);
+  }
+  cudaError_t e = launch_general(a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "general kernel");
+  return UFPGD_OK;
+}
+
+int ufpgd_gpu_unfolded_forward_host(const ufpgd_c64* H, int64_t B, int K, int M,
+                                    const double* lambda, const double* eta, int L, const double* c,
+                                    int w0_mode, const ufpgd_c64* W0, ufpgd_c64* W,
+                                    int32_t* diverged_at, double* stats, double alpha, int device) {
+  int rc;
+  if ((rc = check_shape(B, K, M)) || (rc = check_layers(lambda, eta, L)) || (rc = check_c(c, K)) ||
+      (rc = check_w0(w0_mode, W0)))
+    return rc;
+  if (!(alpha > 0.0)) return fail(UFPGD_EINVAL_PARAM, "alpha must be > 0");
+  if (B > 0 && (!H || !W)) return fail(UFPGD_EINVAL_PARAM, "H and W are required");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
+  const bool fused = fused_supported(K, M) && L >= 1;
+  // ~32 MiB of H per chunk keeps three chunks in flight well inside HBM.
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, (32ll << 20) / (8ll * K * M)));
+  const long long ppc = partial_count(chunk, K, M, fused);
+  return host_pipeline(
+      H, B, K, M, w0_mode == UFPGD_W0_GIVEN ? W0 : nullptr, W, diverged_at, nullptr, ppc, chunk, stats,
+      [&](float2* h, int64_t nb, float2* w0, float2* w, int32_t* div, float*, double* parts,
+          long long* np, cudaStream_t s) {
+        return enqueue_unfolded(h, nb, K, M, lambda, eta, L, c, w0_mode, w0, w, div, nullptr, nullptr,
+                                parts, alpha, s, np);
+      });
+}
+
+int ufpgd_gpu_pgd_fixed_host(const ufpgd_c64* H, int64_t B, int K, int M, int power_steps,
+                             double lambda, int64_t iters, const double* c, int w0_mode,
+                             const ufpgd_c64* W0, ufpgd_c64* W, int32_t* diverged_at,
+                             float* eta_out, double* stats, double alpha, int device) {
+  int rc;
+  if ((rc = check_shape(B, K, M)) || (rc = check_c(c, K)) || (rc = check_w0(w0_mode, W0))) return rc;
+  DeviceGuard g(device);
+  if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
+  const bool fused = fused_supported(K, M) && iters >= 1;
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, (8ll << 20) / (8ll * K * M)));
+  const long long ppc = partial_count(chunk, K, M, fused);
+  // The device entry point finalises its own stats per chunk; here the
+  // pipeline collects block partials, so call the kernels with partials only.
+  return host_pipeline(
+      H, B, K, M, w0_mode == UFPGD_W0_GIVEN ? W0 : nullptr, W, diverged_at, eta_out, ppc, chunk,
+      stats,
+      [&](float2* h, int64_t nb, float2* w0, float2* w, int32_t* div, float* eo, double* parts,
+          long long* np, cudaStream_t s) -> int {
+        *np = nb;
+        std::vector<ufpgd_c64> v0(M);
+        ufpgd_power_v0(M, v0.data());
+        if (fused) {
+          FusedArgs a{};
+          a.H = h;
+          a.W = w;
+          a.W0 = w0;
+          a.eta_out = eo;
+          a.diverged_at = div;
+          a.block_partials = parts;
+          a.B = nb;
+          a.L = iters;
+          a.w0_mode = w0_mode;
+          a.power_steps = power_steps;
+          a.lambda = static_cast<float>(lambda);
+          a.alpha = static_cast<float>(alpha);
+          for (int k = 0; k < K; ++k) a.c[k] = static_cast<float>(c[k]);
+          std::memcpy(a.v0, v0.data(), sizeof(float2) * M);
+          cudaError_t e = launch_fused(a, true, K, M, s, np);
+          return e == cudaSuccess ? UFPGD_OK : cuda_fail(e, "fused PGD kernel");
+        }
+        // General shapes: power iteration then the general kernel, all on s.
+        float* lip = nullptr;
+        cudaError_t e = cudaMallocAsync(&lip, sizeof(float) * nb, s);
+        if (e != cudaSuccess) return cuda_fail(e, "alloc");
+        int r = ufpgd_gpu_power_iteration(reinterpret_cast<const ufpgd_c64*>(h), nb, K, M, v0.data(),
+                                          power_steps, lip, device, s);
+        if (r == UFPGD_OK) {
+          GeneralArgs gA{};
+          gA.H = h;
+          gA.W = w;
+          gA.W0 = w0;
+          gA.diverged_at = div;
+          gA.block_partials = parts;
+          gA.B = nb;
+          gA.K = K;
+          gA.M = M;
+          gA.w0_mode = w0_mode;
+          gA.pgd = 1;
+          gA.iters = iters;
+          gA.lip_b = lip;
+          gA.eta_out = eo;
+          gA.lambda = static_cast<float>(lambda);
+          gA.index_base = 1;
+          gA.alpha = static_cast<float>(alpha);
+          for (int k = 0; k < K; ++k) gA.c[k] = static_cast<float>(c[k]);
+          e = launch_general(gA, s);
+          r = e == cudaSuccess ? UFPGD_OK : cuda_fail(e, "general PGD kernel");
+        }
+        cudaFreeAsync(lip, s);
+        return r;
+      });
+}
+
+int ufpgd_gpu_init(int ngpus) {
+  std::lock_guard<std::mutex> lock(g_nccl_mu);
+  int count = 0;
+  UFPGD_CUDA(cudaGetDeviceCount(&count));
+  if (ngpus < 1 || ngpus > count) return fail(UFPGD_EINVAL_PARAM, "ngpus out of range");
+  if (!g_comms.empty()) return UFPGD_OK;
+  if (!load_nccl()) return fail(UFPGD_ENCCL, "libnccl.so.2 not loadable");
+  std::vector<int> devs(ngpus);
+  for (int i = 0; i < ngpus; ++i) devs[i] = i;
+  g_comms.assign(ngpus, nullptr);
+  ncclResult_t r = g_nccl.CommInitAll(g_comms.data(), ngpus, devs.data());
+  if (r != 0) {
+    g_comms.clear();
+    return fail(UFPGD_ENCCL, std::string("ncclCommInitAll: ") + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
+  }
+  return UFPGD_OK;
+}
+
+int ufpgd_gpu_shutdown(void) {
+  std::lock_guard<std::mutex> lock(g_nccl_mu);
+  for (ncclComm_t c : g_comms)
+    if (c) g_nccl.CommDestroy(c);
+  g_comms.clear();
+  return UFPGD_OK;
+}
+
+int ufpgd_gpu_unfolded_forward_sharded(const ufpgd_c64* H, int64_t B, int K, int M,
+                                       const double* lambda, const double* eta, int L,
+                                       const double* c, ufpgd_c64* W, int32_t* diverged_at,
+                                       double* stats, double alpha) {
+  int rc;
+  if ((rc = check_shape(B, K, M)) || (rc = check_layers(lambda, eta, L)) || (rc = check_c(c, K))) return rc;
+  std::lock_guard<std::mutex> lock(g_nccl_mu);
+  const int G = static_cast<int>(g_comms.size());
+  if (G == 0) return fail(UFPGD_ENCCL, "call ufpgd_gpu_init first");
+  // Contiguous shards [g*B/G, (g+1)*B/G); one host thread and stream per GPU.
+  std::vector<int> rcs(G, UFPGD_OK);
+  std::vector<std::string> errs(G);
+  std::vector<double*> dstats(G, nullptr);
+  std::vector<cudaStream_t> streams(G, nullptr);
+  std::vector<std::thread> th;
+  for (int gi = 0; gi < G; ++gi) {
+    th.emplace_back([&, gi] {
+      const int64_t b0 = B * gi / G, b1 = B * (gi + 1) / G, nb = b1 - b0;
+      cudaSetDevice(gi);
+      cudaStreamCreateWithFlags(&streams[gi], cudaStreamNonBlocking);
+      cudaMalloc(&dstats[gi], 3 * sizeof(double));
+      double part[3] = {0, 0, 0};
+      int r = ufpgd_gpu_unfolded_forward_host(H + b0 * K * M, nb, K, M, lambda, eta, L, c,
+                                              UFPGD_W0_ZERO, nullptr, W + b0 * K * M,
+                                              diverged_at ? diverged_at + b0 : nullptr, part, alpha, gi);
+      if (r != UFPGD_OK && r != UFPGD_EDIVERGED) errs[gi] = g_last_error;
+      rcs[gi] = r;
+      cudaMemcpyAsync(dstats[gi], part, sizeof(part), cudaMemcpyHostToDevice, streams[gi]);
+      cudaStreamSynchronize(streams[gi]);
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int gi = 0; gi < G; ++gi)
+    if (rcs[gi] != UFPGD_OK && rcs[gi] != UFPGD_EDIVERGED) return fail(rcs[gi], errs[gi]);
+  // The only collective: sum of the 3 statistics across GPUs.
+  g_nccl.GroupStart();
+  for (int gi = 0; gi < G; ++gi) {
+    cudaSetDevice(gi);
+    g_nccl.AllReduce(dstats[gi], dstats[gi], 3, kNcclDouble, kNcclSum, g_comms[gi], streams[gi]);
+  }
+  ncclResult_t nr = g_nccl.GroupEnd();
+  double out[3] = {0, 0, 0};
+  for (int gi = 0; gi < G; ++gi) {
+    cudaSetDevice(gi);
+    cudaStreamSynchronize(streams[gi]);
+    if (gi == 0) cudaMemcpy(out, dstats[0], sizeof(out), cudaMemcpyDeviceToHost);
+    cudaFree(dstats[gi]);
+    cudaStreamDestroy(streams[gi]);
+  }
+  if (nr != 0) return fail(UFPGD_ENCCL, "ncclAllReduce failed");
+  if (stats) std::memcpy(stats, out, sizeof(out));
+  if (out[2] > 0.0) return fail(UFPGD_EDIVERGED, "non-finite iterate in at least one realization");
+  return UFPGD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,775 @@
+// sm_100a kernels for the batched PA-aware precoder solver.
+//
+// Hot path: per realization
+// and per layer
+//     X' = W H^T - diag(c)            (K x K, contraction over the M antennas)
+//     V  = W - eta X' H^*             (K x M, contraction over the K users)
+//     w_m = max(0, 1 - t/||v_m||) v_m  (per-antenna group soft threshold)
+// which is unfolded.cpp:112-146 / pgd.cpp:226-244 with the constraint term
+// folded into X' (diag(c) H^* = (diag(c)) H^*, so X' H^* = grad_f(W),
+// pgd.hpp:41-47). The fold is exact algebra; it removes the K x M offset
+// matrix of SmoothGradient (pgd.cpp:51-59) and keeps FP32 error small over
+// thousands of iterations.
+//
+// Fused team kernel (fused_kernel): a team of T = TK*TM threads owns one
+// realization for ALL layers. Thread (a, b) of the team holds, in registers,
+//   w[i][kk] = W(k = a*KA + kk, m = i*TM + b)     (KA users x MB antennas)
+//   x[kk][j] = X'(a*KA + kk, j)                   (its KA rows of X')
+// and H lives in shared memory (row stride padded so the quarter-warp LDS.128
+// phases are bank-conflict free). One pass over the thread's antennas per
+// layer does stage 2 + prox for antenna m and, with the same H column still in
+// registers, accumulates antenna m's contribution to the NEXT layer's X'
+// (stage 1). Warp shuffles do the two reductions: the per-antenna norm across
+// the TK threads sharing an antenna, and the X' all-reduce across the TM
+// threads sharing rows (once per layer). H is read from HBM once
+// (ld.global.nc, streaming) and W written once (st.global.cs).
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+#include <cstdlib>
+#include <cmath>
+#include <algorithm>
+
+#include "ufpgd_internal.h"
+
+namespace ufpgd_gpu_impl {
+namespace {
+
+constexpr int kFusedMaxWarps = 8;  // fused blocks have 1..8 warps (chosen per launch)
+constexpr int kGenThreads = 256;
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void stg_stream(float4* p, float4 v) {
+  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
+// acc += a * b
+__device__ __forceinline__ void cmac(float2& acc, float2 a, float2 b) {
+  acc.x = fmaf(a.x, b.x, acc.x);
+  acc.x = fmaf(-a.y, b.y, acc.x);
+  acc.y = fmaf(a.x, b.y, acc.y);
+  acc.y = fmaf(a.y, b.x, acc.y);
+}
+
+// acc += a * conj(b)
+__device__ __forceinline__ void cmac_conj(float2& acc, float2 a, float2 b) {
+  acc.x = fmaf(a.x, b.x, acc.x);
+  acc.x = fmaf(a.y, b.y, acc.x);
+  acc.y = fmaf(a.y, b.x, acc.y);
+  acc.y = fmaf(-a.x, b.y, acc.y);
+}
+
+template <int K_, int M_, int TK_, int TM_>
+struct Team {
+  static constexpr int K = K_, M = M_, TK = TK_, TM = TM_;
+  static constexpr int T = TK * TM;     // threads per realization
+  static constexpr int R = 32 / T;      // realizations per warp
+  static constexpr int KA = K / TK;     // users per thread
+  static constexpr int P = KA / 2;      // user pairs per thread (FFMA2 lanes)
+  static constexpr int MB = M / TM;     // antennas per thread
+  static constexpr int HS = 2 * K + 4;  // padded H row stride in floats
+  static constexpr int SMEM_PER_WARP = R * M * HS * 4;
+  static_assert(32 % T == 0, "a team must divide the warp");
+  static_assert(K % TK == 0 && M % TM == 0, "team must tile (K, M)");
+  static_assert(KA % 2 == 0 && K % 2 == 0, "users are processed in FFMA2 pairs");
+};
+
+// Packed FP32x2 arithmetic (sm_100a FFMA2 / FMUL2 / FADD2). A complex matrix
+// is held split into real and imaginary parts, each packed over the thread's
+// user PAIR (rows k, k+1): re = (Re W(k,m), Re W(k+1,m)), im likewise. A
+// complex MAC with a broadcast scalar complex h then costs two FFMA2 per part
+// and ptxas folds the broadcast (and its negation) into the scalar operand of
+// FFMA2, so no shuffled or rotated copies are ever materialised.
+__device__ __forceinline__ float2 bc(float s) { return make_float2(s, s); }
+__device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) { return __ffma2_rn(bc(a), b, c); }
+__device__ __forceinline__ float2 fmul2(float a, float2 b) { return __fmul2_rn(bc(a), b); }
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 zero2() { return make_float2(0.f, 0.f); }
+
+// Loads row m of H (all K users, complex) from shared memory.
+template <class S>
+__device__ __forceinline__ void load_col(const float* hs, int m, float2 (&h)[S::K]) {
+  const float4* hp = reinterpret_cast<const float4*>(hs + m * S::HS);
+#pragma unroll
+  for (int q = 0; q < S::K / 2; ++q) {
+    const float4 t = hp[q];
+    h[2 * q] = make_float2(t.x, t.y);
+    h[2 * q + 1] = make_float2(t.z, t.w);
+  }
+}
+
+// Split-complex accumulators of the thread's rows of X' (stage 1 output).
+template <class S>
+struct XAcc {
+  float2 re[S::P][S::K], im[S::P][S::K];
+};
+
+// Stage 1 contribution of antenna m: X'(k, j) += W(k, m) H(j, m).
+template <class S>
+__device__ __forceinline__ void stage1_accumulate(XAcc<S>& xn, const float2 (&wr)[S::P],
+                                                  const float2 (&wi)[S::P], const float2 (&h)[S::K]) {
+#pragma unroll
+  for (int p = 0; p < S::P; ++p)
+#pragma unroll
+    for (int j = 0; j < S::K; ++j) {
+      xn.re[p][j] = ffma2(h[j].x, wr[p], xn.re[p][j]);
+      xn.re[p][j] = ffma2(-h[j].y, wi[p], xn.re[p][j]);
+      xn.im[p][j] = ffma2(h[j].x, wi[p], xn.im[p][j]);
+      xn.im[p][j] = ffma2(h[j].y, wr[p], xn.im[p][j]);
+    }
+}
+
+// All-reduce of the stage-1 partials across the TM threads sharing rows. The
+// constraint fold X'(k, k) -= c_k is already in the partials: the b == 0
+// thread of each row group starts its accumulation from -diag(c) (xacc_init).
+template <class S>
+__device__ __forceinline__ void allreduce(XAcc<S>& xn, XAcc<S>& x) {
+#pragma unroll
+  for (int p = 0; p < S::P; ++p)
+#pragma unroll
+    for (int j = 0; j < S::K; ++j) {
+      float2 r = xn.re[p][j], i = xn.im[p][j];
+#pragma unroll
+      for (int off = 1; off < S::TM; off <<= 1) {
+        const float2 ro = make_float2(__shfl_xor_sync(kFull, r.x, off), __shfl_xor_sync(kFull, r.y, off));
+        const float2 io = make_float2(__shfl_xor_sync(kFull, i.x, off), __shfl_xor_sync(kFull, i.y, off));
+        r = fadd2(r, ro);
+        i = fadd2(i, io);
+      }
+      x.re[p][j] = r;
+      x.im[p][j] = i;
+    }
+}
+
+// Start value of the stage-1 accumulators: -diag(c) on the thread's rows for
+// the b == 0 thread (so the all-reduce applies the fold exactly once), zero
+// elsewhere. cdiag[p] = (-c_k0, -c_k0+1) or zero, precomputed per thread.
+template <class S>
+__device__ __forceinline__ void xacc_init(XAcc<S>& x, const float2 (&cdiag)[S::P], int a) {
+#pragma unroll
+  for (int p = 0; p < S::P; ++p)
+#pragma unroll
+    for (int j = 0; j < S::K; ++j) {
+      // j is compile-time; the row pair (k0, k0+1) = (a*KA + 2p, +1) is not:
+      // only j in that pair gets a non-zero start, selected with one compare.
+      const int k0 = a * S::KA + 2 * p;
+      x.re[p][j] = make_float2(j == k0 ? cdiag[p].x : 0.f, j == k0 + 1 ? cdiag[p].y : 0.f);
+      x.im[p][j] = zero2();
+    }
+}
+
+template <class S>
+__device__ __forceinline__ void team_stage1(const float2 (&wr)[S::MB][S::P], const float2 (&wi)[S::MB][S::P],
+                                            XAcc<S>& x, const float* hs, int a, int b,
+                                            const float2 (&cdiag)[S::P]) {
+  XAcc<S> xn;
+  xacc_init<S>(xn, cdiag, a);
+#pragma unroll
+  for (int i = 0; i < S::MB; ++i) {
+    float2 h[S::K];
+    load_col<S>(hs, i * S::TM + b, h);
+    stage1_accumulate<S>(xn, wr[i], wi[i], h);
+  }
+  allreduce<S>(xn, x);
+}
+
+// One layer (or PGD iteration). STAGE1: also build X' for the next layer.
+// STATS: accumulate ||W||_{2,1} and the active count for this thread's
+// antennas (counted on the a == 0 threads only).
+template <class S, bool STAGE1, bool STATS>
+__device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&wi)[S::MB][S::P], XAcc<S>& x,
+                                           const float* hs, int a, int b, float eta, float thr,
+                                           const float2 (&cdiag)[S::P], bool& nonfinite, float& l21,
+                                           int& act) {
+  XAcc<S> xn;
+  if (STAGE1) xacc_init<S>(xn, cdiag, a);
+  const float thr2 = thr * thr;
+#pragma unroll
+  for (int i = 0; i < S::MB; ++i) {
+    float2 h[S::K];
+    load_col<S>(hs, i * S::TM + b, h);
+    // stage 2: G(k, m) = sum_j X'(k, j) conj(H(j, m)); V = W - eta G
+    float2 vr[S::P], vi[S::P];
+    float2 s2 = zero2();
+#pragma unroll
+    for (int p = 0; p < S::P; ++p) {
+      float2 gr0 = zero2(), gr1 = zero2(), gi0 = zero2(), gi1 = zero2();
+#pragma unroll
+      for (int j = 0; j < S::K; j += 2) {
+        gr0 = ffma2(h[j].x, x.re[p][j], gr0);
+        gr0 = ffma2(h[j].y, x.im[p][j], gr0);
+        gi0 = ffma2(h[j].x, x.im[p][j], gi0);
+        gi0 = ffma2(-h[j].y, x.re[p][j], gi0);
+        gr1 = ffma2(h[j + 1].x, x.re[p][j + 1], gr1);
+        gr1 = ffma2(h[j + 1].y, x.im[p][j + 1], gr1);
+        gi1 = ffma2(h[j + 1].x, x.im[p][j + 1], gi1);
+        gi1 = ffma2(-h[j + 1].y, x.re[p][j + 1], gi1);
+      }
+      vr[p] = ffma2(-eta, fadd2(gr0, gr1), wr[i][p]);
+      vi[p] = ffma2(-eta, fadd2(gi0, gi1), wi[i][p]);
+      s2 = __ffma2_rn(vr[p], vr[p], s2);
+      s2 = __ffma2_rn(vi[p], vi[p], s2);
+    }
+    float s = s2.x + s2.y;
+    // ||v_m||^2 across the TK threads holding antenna m
+#pragma unroll
+    for (int off = S::TM; off < S::T; off <<= 1) s += __shfl_xor_sync(kFull, s, off);
+    // Non-finite step image (unfolded.cpp:120-125): any NaN/Inf entry of
+    // v_m makes its squared column norm NaN/Inf. (A finite column whose
+    // squared norm overflows FP32, |v| > ~6e18, is flagged too.)
+    nonfinite |= !(s <= FLT_MAX);
+    // prox (pgd.cpp:85-99): strict ||v|| > t, i.e. s > t^2
+    const bool on = s > thr2;
+    const float r = rsqrtf(s);
+    const float scale = on ? fmaf(-thr, r, 1.f) : 0.f;
+#pragma unroll
+    for (int p = 0; p < S::P; ++p) {
+      wr[i][p] = fmul2(scale, vr[p]);
+      wi[i][p] = fmul2(scale, vi[p]);
+    }
+    if (STATS) {
+      if (a == 0 && on) {
+        l21 += fmaf(s, r, -thr);  // ||w_m|| = ||v_m|| - t
+        act += 1;
+      }
+    }
+    if (STAGE1) stage1_accumulate<S>(xn, wr[i], wi[i], h);
+  }
+  if (STAGE1) allreduce<S>(xn, x);
+}
+
+// Fixed-step power iteration on H^T H^* (pgd.cpp:146-162 with the BASELINE
+// 30-step rule) for the team's realization; every team thread returns the
+// Rayleigh quotient Re(v^H w) of the last step. Control flow is uniform
+// across the warp (all teams run `steps` steps) so the shuffles stay legal.
+template <class S>
+__device__ float team_power(const float* hs, const float2* v0, int steps, int a, int b) {
+  float2 v[S::MB];
+#pragma unroll
+  for (int i = 0; i < S::MB; ++i) v[i] = v0[i * S::TM + b];
+  float est = 0.f;
+  bool zero = false;
+  for (int st = 0; st < steps; ++st) {
+    float2 u[S::KA];
+#pragma unroll
+    for (int jj = 0; jj < S::KA; ++jj) u[jj] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < S::MB; ++i) {
+      const float2* hrow = reinterpret_cast<const float2*>(hs + (i * S::TM + b) * S::HS) + a * S::KA;
+#pragma unroll
+      for (int jj = 0; jj < S::KA; ++jj) cmac(u[jj], v[i], make_float2(hrow[jj].x, -hrow[jj].y));
+    }
+#pragma unroll
+    for (int jj = 0; jj < S::KA; ++jj)
+#pragma unroll
+      for (int off = 1; off < S::TM; off <<= 1) {
+        u[jj].x += __shfl_xor_sync(kFull, u[jj].x, off);
+        u[jj].y += __shfl_xor_sync(kFull, u[jj].y, off);
+      }
+    float dot = 0.f, wn2 = 0.f;
+    float2 wv[S::MB];
+#pragma unroll
+    for (int i = 0; i < S::MB; ++i) {
+      const float2* hrow = reinterpret_cast<const float2*>(hs + (i * S::TM + b) * S::HS) + a * S::KA;
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int jj = 0; jj < S::KA; ++jj) cmac(acc, hrow[jj], u[jj]);
+#pragma unroll
+      for (int off = S::TM; off < S::T; off <<= 1) {
+        acc.x += __shfl_xor_sync(kFull, acc.x, off);
+        acc.y += __shfl_xor_sync(kFull, acc.y, off);
+      }
+      wv[i] = acc;
+      dot = fmaf(v[i].x, acc.x, fmaf(v[i].y, acc.y, dot));
+      wn2 = fmaf(acc.x, acc.x, fmaf(acc.y, acc.y, wn2));
+    }
+#pragma unroll
+    for (int off = 1; off < S::TM; off <<= 1) {
+      dot += __shfl_xor_sync(kFull, dot, off);
+      wn2 += __shfl_xor_sync(kFull, wn2, off);
+    }
+    if (!zero) {
+      if (wn2 == 0.f) {
+        zero = true;  // pgd.cpp:150-153: an all-zero channel has L = 0
+        est = 0.f;
+      } else {
+        est = dot;
+        const float inv = 1.f / sqrtf(wn2);
+#pragma unroll
+        for (int i = 0; i < S::MB; ++i) v[i] = make_float2(wv[i].x * inv, wv[i].y * inv);
+      }
+    }
+  }
+  return est;
+}
+
+template <class S, bool PGD, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant__ FusedArgs p) {
+  extern __shared__ __align__(16) float smem[];
+  __shared__ double red[kFusedMaxWarps][3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int team = lane / S::T, tl = lane % S::T, a = tl / S::TM, b = tl % S::TM;
+  const long long rid = (static_cast<long long>(blockIdx.x) * nwarps + warp) * S::R + team;
+  const bool valid = rid < p.B;
+  float* hs = smem + (warp * S::R + team) * (S::M * S::HS);
+
+  // Stage H once: coalesced streaming float4 loads into the padded tile.
+  {
+    constexpr int NV = S::M * S::K / 2;
+    const float4* hg = reinterpret_cast<const float4*>(p.H) + (valid ? rid : 0LL) * NV;
+    float4 buf[NV / S::T];
+#pragma unroll
+    for (int q = 0; q < NV / S::T; ++q)
+      buf[q] = valid ? ldg_stream(hg + tl + q * S::T) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < NV / S::T; ++q) {
+      const int e = 2 * (tl + q * S::T);
+      *reinterpret_cast<float4*>(hs + (e / S::K) * S::HS + 2 * (e % S::K)) = buf[q];
+    }
+    __syncwarp();
+  }
+
+  // W(a*KA + 2p + {0,1}, i*TM + b), split into real / imaginary user pairs.
+  float2 wr[S::MB][S::P], wi[S::MB][S::P];
+  XAcc<S> x;
+  float2 cdiag[S::P];
+#pragma unroll
+  for (int q = 0; q < S::P; ++q) {
+    const int k0 = a * S::KA + 2 * q;
+    cdiag[q] = b == 0 ? make_float2(-p.c[k0], -p.c[k0 + 1]) : zero2();
+  }
+  if (p.w0_mode == UFPGD_W0_ZERO) {
+#pragma unroll
+    for (int i = 0; i < S::MB; ++i)
+#pragma unroll
+      for (int q = 0; q < S::P; ++q) {
+        wr[i][q] = zero2();
+        wi[i][q] = zero2();
+      }
+    // X' = 0 H^T - diag(c): the layer-0 product is identically zero.
+#pragma unroll
+    for (int q = 0; q < S::P; ++q)
+#pragma unroll
+      for (int j = 0; j < S::K; ++j) {
+        const int k0 = a * S::KA + 2 * q;
+        x.re[q][j] = make_float2(j == k0 ? -p.c[j] : 0.f, j == k0 + 1 ? -p.c[j] : 0.f);
+        x.im[q][j] = zero2();
+      }
+  } else {
+    if (p.w0_mode == UFPGD_W0_CONJ_H) {
+#pragma unroll
+      for (int i = 0; i < S::MB; ++i) {
+        const float4* hrow = reinterpret_cast<const float4*>(hs + (i * S::TM + b) * S::HS + 2 * a * S::KA);
+#pragma unroll
+        for (int q = 0; q < S::P; ++q) {
+          const float4 t = hrow[q];
+          wr[i][q] = make_float2(t.x, t.z);
+          wi[i][q] = make_float2(-t.y, -t.w);
+        }
+      }
+    } else {
+      const float2* w0 = p.W0 + (valid ? rid : 0LL) * (S::M * S::K);
+#pragma unroll
+      for (int i = 0; i < S::MB; ++i)
+#pragma unroll
+        for (int q = 0; q < S::P; ++q) {
+          const float4 t = valid ? ldg_stream(reinterpret_cast<const float4*>(
+                                       w0 + (i * S::TM + b) * S::K + a * S::KA + 2 * q))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+          wr[i][q] = make_float2(t.x, t.z);
+          wi[i][q] = make_float2(t.y, t.w);
+        }
+    }
+    team_stage1<S>(wr, wi, x, hs, a, b, cdiag);
+  }
+
+  float eta_b = 0.f, thr_b = 0.f;
+  if (PGD) {
+    if (p.eta_in) {
+      eta_b = valid ? p.eta_in[rid] : 1.f;
+    } else {
+      const float Lb = team_power<S>(hs, p.v0, p.power_steps, a, b);
+      eta_b = 1.f / Lb;
+    }
+    thr_b = p.lambda * eta_b;
+    if (p.eta_out && valid && tl == 0) p.eta_out[rid] = eta_b;
+  }
+
+  bool nonfinite = false;
+  long long first_bad = -1;
+  float l21 = 0.f;
+  int act = 0;
+  const long long L = p.L;
+  for (long long l = 0; l + 1 < L; ++l) {
+    const float eta = PGD ? eta_b : p.eta[l];
+    const float thr = PGD ? thr_b : p.thr[l];
+    team_layer<S, true, false>(wr, wi, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
+    if (nonfinite && first_bad < 0) first_bad = l;
+  }
+  if (L >= 1) {
+    const float eta = PGD ? eta_b : p.eta[L - 1];
+    const float thr = PGD ? thr_b : p.thr[L - 1];
+    team_layer<S, false, true>(wr, wi, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
+    if (nonfinite && first_bad < 0) first_bad = L - 1;
+  }
+
+  // Team-wide first divergence (min over the team, -1 = none).
+  long long fb = first_bad < 0 ? LLONG_MAX : first_bad;
+#pragma unroll
+  for (int off = 1; off < S::T; off <<= 1) fb = min(fb, __shfl_xor_sync(kFull, fb, off));
+#pragma unroll
+  for (int off = 1; off < S::TM; off <<= 1) {
+    l21 += __shfl_xor_sync(kFull, l21, off);
+    act += __shfl_xor_sync(kFull, act, off);
+  }
+  const bool diverged = fb != LLONG_MAX;
+
+  if (valid) {
+    float2* wg = p.W + rid * (S::M * S::K);
+#pragma unroll
+    for (int i = 0; i < S::MB; ++i)
+#pragma unroll
+      for (int q = 0; q < S::P; ++q)
+        stg_stream(reinterpret_cast<float4*>(wg + (i * S::TM + b) * S::K + a * S::KA + 2 * q),
+                   make_float4(wr[i][q].x, wi[i][q].x, wr[i][q].y, wi[i][q].y));
+    if (tl == 0) {
+      if (p.diverged_at) p.diverged_at[rid] = diverged ? static_cast<int32_t>(fb + (PGD ? 1 : 0)) : -1;
+      if (p.l21) p.l21[rid] = diverged ? __int_as_float(0x7fc00000) : l21;
+      if (p.active) p.active[rid] = diverged ? -1 : act;
+    }
+  }
+
+  if (p.block_partials) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    if (valid && tl == 0) {
+      if (diverged) {
+        s2 = 1.0;
+      } else {
+        s0 = static_cast<double>(p.alpha) * static_cast<double>(l21);
+        s1 = static_cast<double>(act);
+      }
+    }
+#pragma unroll
+    for (int off = S::T; off < 32; off <<= 1) {
+      s0 += __shfl_xor_sync(kFull, s0, off);
+      s1 += __shfl_xor_sync(kFull, s1, off);
+      s2 += __shfl_xor_sync(kFull, s2, off);
+    }
+    if (lane == 0) {
+      red[warp][0] = s0;
+      red[warp][1] = s1;
+      red[warp][2] = s2;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+      double t = 0.0;
+      for (int q = 0; q < nwarps; ++q) t += red[q][threadIdx.x];
+      p.block_partials[blockIdx.x * 3LL + threadIdx.x] = t;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// General-shape kernel: one CTA per realization, H / W / V / X' in shared
+// memory. Serves every (K, M) without a fused team specialisation, the
+// reference's per-realization helpers (grad_f, prox_l21, pgd_step) and the
+// taped forward (unfolded.cpp:127-143). Exact FP32 sqrt/div in the prox.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float block_sum(float v, float* scratch) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += scratch[q];
+  return t;
+}
+
+__global__ void __launch_bounds__(kGenThreads) general_kernel(const __grid_constant__ GeneralArgs p) {
+  extern __shared__ __align__(16) float2 gsm[];
+  __shared__ float scratch[kGenThreads / 32];
+  const int K = p.K, M = p.M, n = K * M, tid = threadIdx.x, nt = blockDim.x;
+  const long long rid = blockIdx.x;
+  float2* hs = gsm;
+  float2* ws = hs + n;
+  float2* vs = ws + n;
+  float2* xs = vs + n;
+  const float2* hg = p.H + rid * n;
+  for (int e = tid; e < n; e += nt) {
+    const float2 h = hg[e];
+    hs[e] = h;
+    ws[e] = p.w0_mode == UFPGD_W0_ZERO ? make_float2(0.f, 0.f)
+            : p.w0_mode == UFPGD_W0_CONJ_H ? make_float2(h.x, -h.y)
+                                           : p.W0[rid * n + e];
+  }
+  __syncthreads();
+  if (p.iterates)
+    for (int e = tid; e < n; e += nt) p.iterates[rid * n + e] = ws[e];
+
+  int first_bad = -1;
+  long long taken = 0;
+  float eta_r = 0.f, thr_r = 0.f;
+  if (p.pgd) {
+    eta_r = p.eta_b ? p.eta_b[rid] : 1.f / p.lip_b[rid];
+    thr_r = p.lambda * eta_r;
+    if (p.eta_out && tid == 0) p.eta_out[rid] = eta_r;
+  }
+  const long long layers = p.mode == 1 ? 1 : (p.pgd ? p.iters : p.L);
+  for (long long l = 0; l < layers; ++l) {
+    // stage 1: X'(k, j) = sum_m W(k, m) H(j, m) - c_k [k == j]
+    for (int o = tid; o < K * K; o += nt) {
+      const int k = o % K, j = o / K;
+      float2 acc = make_float2(0.f, 0.f);
+      for (int m = 0; m < M; ++m) cmac(acc, ws[m * K + k], hs[m * K + j]);
+      if (k == j) acc.x -= p.c[k];
+      xs[o] = acc;
+    }
+    __syncthreads();
+    // stage 2: G = X' H^*, V = W - eta G
+    const float eta = p.pgd ? eta_r : p.eta[l], thr = p.pgd ? thr_r : p.thr[l];
+    for (int e = tid; e < n; e += nt) {
+      const int m = e / K, k = e % K;
+      float2 g = make_float2(0.f, 0.f);
+      for (int j = 0; j < K; ++j) cmac_conj(g, xs[j * K + k], hs[m * K + j]);
+      if (p.mode == 1) {
+        p.W[rid * n + e] = g;
+      } else {
+        vs[e] = make_float2(fmaf(-eta, g.x, ws[e].x), fmaf(-eta, g.y, ws[e].y));
+      }
+    }
+    if (p.mode == 1) return;
+    __syncthreads();
+    // prox per antenna (pgd.cpp:85-99, exact sqrt and division)
+    float bad = 0.f, d2 = 0.f, s2 = 0.f;
+    for (int m = tid; m < M; m += nt) {
+      float s = 0.f;
+      for (int k = 0; k < K; ++k) {
+        const float2 v = vs[m * K + k];
+        if (!isfinite(v.x) || !isfinite(v.y)) bad = 1.f;
+        s = fmaf(v.x, v.x, fmaf(v.y, v.y, s));
+      }
+      const float nrm = sqrtf(s);
+      const bool on = nrm > thr;
+      const float sh = on ? 1.f - thr / nrm : 0.f;
+      for (int k = 0; k < K; ++k) {
+        const float2 v = vs[m * K + k];
+        const float2 wn = on ? make_float2(sh * v.x, sh * v.y) : make_float2(0.f, 0.f);
+        if (p.residual_tol > 0.f) {
+          const float2 wo = ws[m * K + k];
+          d2 += (wn.x - wo.x) * (wn.x - wo.x) + (wn.y - wo.y) * (wn.y - wo.y);
+          s2 += wo.x * wo.x + wo.y * wo.y;
+        }
+        ws[m * K + k] = wn;
+      }
+      if (p.tape_norms) p.tape_norms[(l * p.B + rid) * M + m] = nrm;
+      if (p.tape_shrink) p.tape_shrink[(l * p.B + rid) * M + m] = sh;
+    }
+    if (p.tape_v)
+      for (int e = tid; e < n; e += nt) p.tape_v[(l * p.B + rid) * n + e] = vs[e];
+    bad = block_sum(bad, scratch);
+    if (bad > 0.f && first_bad < 0) first_bad = static_cast<int>(l);
+    taken = l + 1;
+    if (p.iterates)
+      for (int e = tid; e < n; e += nt) p.iterates[((l + 1) * p.B + rid) * n + e] = ws[e];
+    if (p.residual_tol > 0.f) {
+      d2 = block_sum(d2, scratch);
+      s2 = block_sum(s2, scratch);
+      if (sqrtf(d2) / fmaxf(sqrtf(s2), 1e-12f) < p.residual_tol) break;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  for (int e = tid; e < n; e += nt) p.W[rid * n + e] = ws[e];
+  // statistics
+  float l21 = 0.f, act = 0.f;
+  for (int m = tid; m < M; m += nt) {
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s = fmaf(ws[m * K + k].x, ws[m * K + k].x, fmaf(ws[m * K + k].y, ws[m * K + k].y, s));
+    l21 += sqrtf(s);
+    act += s > 0.f ? 1.f : 0.f;
+  }
+  l21 = block_sum(l21, scratch);
+  act = block_sum(act, scratch);
+  if (tid == 0) {
+    const bool diverged = first_bad >= 0;
+    if (p.diverged_at) p.diverged_at[rid] = diverged ? first_bad + p.index_base : -1;
+    if (p.iterations) p.iterations[rid] = taken;
+    if (p.l21) p.l21[rid] = diverged ? __int_as_float(0x7fc00000) : l21;
+    if (p.active) p.active[rid] = diverged ? -1 : static_cast<int32_t>(act);
+    if (p.block_partials) {
+      p.block_partials[rid * 3 + 0] = diverged ? 0.0 : static_cast<double>(p.alpha) * l21;
+      p.block_partials[rid * 3 + 1] = diverged ? 0.0 : static_cast<double>(act);
+      p.block_partials[rid * 3 + 2] = diverged ? 1.0 : 0.0;
+    }
+  }
+}
+
+// Standalone fixed-step power iteration, one warp per realization, any shape
+// (H read straight from global memory; it is tiny next to the PGD loop).
+__global__ void __launch_bounds__(128) power_kernel(const __grid_constant__ PowerArgs p) {
+  const int lane = threadIdx.x & 31;
+  const long long rid = static_cast<long long>(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  if (rid >= p.B) return;  // warp-uniform
+  const int K = p.K, M = p.M;
+  const float2* h = p.H + rid * static_cast<long long>(K) * M;
+  extern __shared__ float2 psm[];
+  float2* v = psm + (threadIdx.x >> 5) * (M + UFPGD_MAX_USERS);
+  float2* u = v + M;
+  for (int m = lane; m < M; m += 32) v[m] = p.v0[m];
+  __syncwarp();
+  float est = 0.f;
+  for (int st = 0; st < p.steps; ++st) {
+    // u = H^* v
+    for (int j = 0; j < K; ++j) {
+      float2 acc = make_float2(0.f, 0.f);
+      for (int m = lane; m < M; m += 32) {
+        const float2 hv = h[m * K + j];
+        cmac(acc, make_float2(hv.x, -hv.y), v[m]);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        acc.x += __shfl_xor_sync(kFull, acc.x, off);
+        acc.y += __shfl_xor_sync(kFull, acc.y, off);
+      }
+      if (lane == 0) u[j] = acc;
+    }
+    __syncwarp();
+    float dot = 0.f, wn2 = 0.f;
+    for (int m = lane; m < M; m += 32) {
+      float2 acc = make_float2(0.f, 0.f);
+      for (int j = 0; j < K; ++j) cmac(acc, h[m * K + j], u[j]);
+      dot = fmaf(v[m].x, acc.x, fmaf(v[m].y, acc.y, dot));
+      wn2 = fmaf(acc.x, acc.x, fmaf(acc.y, acc.y, wn2));
+      v[m] = acc;  // unnormalised; scaled below
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      dot += __shfl_xor_sync(kFull, dot, off);
+      wn2 += __shfl_xor_sync(kFull, wn2, off);
+    }
+    if (wn2 == 0.f) {
+      est = 0.f;
+      break;  // warp-uniform
+    }
+    est = dot;
+    const float inv = 1.f / sqrtf(wn2);
+    __syncwarp();
+    for (int m = lane; m < M; m += 32) v[m] = make_float2(v[m].x * inv, v[m].y * inv);
+    __syncwarp();
+  }
+  if (lane == 0) p.Lout[rid] = est;
+}
+
+// Deterministic sum of per-block partials [n][3] -> stats[3].
+__global__ void __launch_bounds__(256) stats_finalize_kernel(const double* __restrict__ part, long long n,
+                                                             double* __restrict__ stats) {
+  __shared__ double acc[3][256];
+  double s[3] = {0.0, 0.0, 0.0};
+  for (long long i = threadIdx.x; i < n; i += 256)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) s[c] += part[i * 3 + c];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) acc[c][threadIdx.x] = s[c];
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[c][threadIdx.x] += acc[c][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x < 3) stats[threadIdx.x] = acc[threadIdx.x][0];
+}
+
+// Block geometry. A realization stays resident for all its layers and each
+// warp runs close to its own dependency-latency limit, so the kernel wants the
+// register-limited maximum of 8 resident warps per SM and every SM busy. A
+// sweep of 1..8 warps per block on B200 (tools/sweep_warps.sh)
+// found 1, 2 and 8 equally fast when the grid covers the SMs, so: the largest
+// of {8, 4, 2, 1} whose grid still has at least one block per SM.
+int pick_warps(int rpw, long long B) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  for (int nw = 8; nw > 1; nw >>= 1)
+    if ((B + static_cast<long long>(nw) * rpw - 1) / (static_cast<long long>(nw) * rpw) >= sms) return nw;
+  return 1;
+}
+
+template <class S>
+cudaError_t launch_team(const FusedArgs& a, bool pgd, cudaStream_t s, long long* nblocks) {
+  auto kern = pgd ? fused_kernel<S, true, 256, 1> : fused_kernel<S, false, 256, 1>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kFusedMaxWarps * S::SMEM_PER_WARP);
+  if (e != cudaSuccess) return e;
+  int nw = pick_warps(S::R, a.B);
+  if (const char* f = std::getenv("UFPGD_FUSED_WARPS")) nw = std::max(1, std::min(8, std::atoi(f)));
+  const long long rpb = static_cast<long long>(nw) * S::R;
+  const long long blocks = (a.B + rpb - 1) / rpb;
+  if (nblocks) *nblocks = blocks;
+  kern<<<static_cast<unsigned>(blocks), nw * 32, nw * S::SMEM_PER_WARP, s>>>(a);
+  return cudaGetLastError();
+}
+
+// Team shapes (K, M) -> (TK, TM): KA = K/TK = 2 users and MB = M/TM antennas
+// per thread keep W, X' and the next X' in registers.
+using Team_4_32 = Team<4, 32, 2, 4>;
+using Team_8_64 = Team<8, 64, 4, 4>;
+
+}  // namespace
+
+bool fused_supported(int K, int M) { return (K == 4 && M == 32) || (K == 8 && M == 64); }
+
+// Upper bound on realizations per block (partials are sized with the smallest
+// block the geometry chooser can pick: one warp).
+int fused_realizations_per_block(int K, int M) {
+  if (K == 4 && M == 32) return Team_4_32::R;
+  if (K == 8 && M == 64) return Team_8_64::R;
+  return 0;
+}
+
+cudaError_t launch_fused(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s, long long* nblocks) {
+  if (K == 4 && M == 32) return launch_team<Team_4_32>(a, pgd, s, nblocks);
+  if (K == 8 && M == 64) return launch_team<Team_8_64>(a, pgd, s, nblocks);
+  return cudaErrorInvalidValue;
+}
+
+size_t general_smem_bytes(int K, int M) {
+  return (3ull * K * M + static_cast<size_t>(K) * K) * sizeof(float2);
+}
+
+cudaError_t launch_general(const GeneralArgs& a, cudaStream_t s) {
+  const size_t smem = general_smem_bytes(a.K, a.M);
+  cudaError_t e = cudaFuncSetAttribute(general_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  general_kernel<<<static_cast<unsigned>(a.B), kGenThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_power(const PowerArgs& a, cudaStream_t s) {
+  const size_t smem = 4 * (a.M + UFPGD_MAX_USERS) * sizeof(float2);
+  cudaError_t e = cudaFuncSetAttribute(power_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  power_kernel<<<static_cast<unsigned>((a.B + 3) / 4), 128, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stats_finalize(const double* partials, long long n, double* stats, cudaStream_t s) {
+  stats_finalize_kernel<<<1, 256, 0, s>>>(partials, n, stats);
+  return cudaGetLastError();
+}
+
+}  // namespace ufpgd_gpu_impl

@@ -1,0 +1,88 @@
+// Internal interface between the C ABI (capi.cu) and the kernels (kernels.cu).
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "ufpgd_gpu.h"
+
+namespace ufpgd_gpu_impl {
+
+// Arguments of the fused team kernel (one team of TK*TM threads per
+// realization; see kernels.cu). Passed by value as a __grid_constant__.
+struct FusedArgs {
+  const float2* H;
+  float2* W;
+  const float2* W0;
+  const float* eta_in;    // PGD: per-realization step (nullable -> power iteration)
+  float* eta_out;         // PGD: step used (nullable)
+  int32_t* diverged_at;   // nullable
+  float* l21;             // nullable
+  int32_t* active;        // nullable
+  double* block_partials; // [gridDim.x][3], nullable
+  long long B;
+  long long L;            // layers (unfolded) or iterations (PGD)
+  int w0_mode;
+  int power_steps;        // PGD with eta_in == nullptr
+  float lambda;           // PGD threshold factor (thr = lambda * eta)
+  float alpha;            // PA constant for the consumed-power statistic
+  float c[UFPGD_MAX_USERS];
+  float eta[UFPGD_MAX_LAYERS];
+  float thr[UFPGD_MAX_LAYERS];
+  float2 v0[256];         // power-iteration start vector (PGD)
+};
+
+// Arguments of the general-shape kernel (one CTA per realization).
+struct GeneralArgs {
+  const float2* H;
+  float2* W;
+  const float2* W0;
+  int32_t* diverged_at;
+  int64_t* iterations;
+  float* l21;
+  int32_t* active;
+  double* block_partials;  // [B][3]
+  float2* iterates;
+  float2* tape_v;
+  float* tape_norms;
+  float* tape_shrink;
+  long long B;
+  int K, M, L;
+  int w0_mode;
+  int mode;         // 0 layers, 1 gradient only
+  int pgd;          // 1: every layer uses the realization's own step (below)
+  long long iters;  // layer / iteration count when pgd == 1
+  const float* eta_b;  // pgd: per-realization step (nullable -> 1 / lip_b)
+  const float* lip_b;  // pgd: per-realization Lipschitz estimate
+  float* eta_out;      // pgd: step used (nullable)
+  float lambda;        // pgd: thr = lambda * eta
+  int index_base;   // 0: layer index, 1: 1-based iteration
+  float residual_tol;
+  float alpha;
+  float c[UFPGD_MAX_USERS];
+  float eta[UFPGD_MAX_LAYERS];
+  float thr[UFPGD_MAX_LAYERS];
+};
+
+struct PowerArgs {
+  const float2* H;
+  float* Lout;
+  long long B;
+  int K, M, steps;
+  float2 v0[1024];
+};
+
+// Fused team kernel availability for (K, M); fills the launch geometry.
+bool fused_supported(int K, int M);
+int fused_realizations_per_block(int K, int M);
+// *nblocks receives the grid size (= number of block partials written).
+cudaError_t launch_fused(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s,
+                         long long* nblocks);
+size_t general_smem_bytes(int K, int M);
+cudaError_t launch_general(const GeneralArgs& a, cudaStream_t s);
+cudaError_t launch_power(const PowerArgs& a, cudaStream_t s);
+cudaError_t launch_stats_finalize(const double* partials, long long n, double* stats,
+                                  cudaStream_t s);
+
+}  // namespace ufpgd_gpu_impl

@@ -1,0 +1,35 @@
+"""Quick CUDA-event timing of the fused kernels (development aid, not the bench)."""
+import sys, time, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2304_12745_b200 as U
+
+def t_uf(cfg, reps=10):
+    w = U.CONFIGS[cfg]
+    t0 = time.time(); H = U.make_inputs(w); tg = time.time() - t0
+    lam, eta = w.layer_params()
+    Hd = torch.from_numpy(H).cuda(); W = torch.empty_like(Hd)
+    for _ in range(3): U.unfolded_forward(Hd, lam, eta, w.c, out=W)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps): U.unfolded_forward(Hd, lam, eta, w.c, out=W)
+    e.record(); torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / reps
+    fl = w.flops_per_realization() * w.B
+    print(f"cfg{cfg} B={w.B}: {ms:.3f} ms/batch  {w.B/ms*1e3/1e6:.2f} M precoders/s  {fl/ms/1e9:.2f} TFLOP/s  (gen {tg:.1f}s)", flush=True)
+
+def t_pgd(n=4096):
+    w = U.CONFIGS[3]
+    H = U.make_inputs(w, 0, n); Hd = torch.from_numpy(H).cuda()
+    U.pgd_fixed(Hd, w.lambda_pgd, 100, w.c); torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(); U.pgd_fixed(Hd, w.lambda_pgd, w.L, w.c); e.record(); torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    fl = w.flops_per_realization() * n
+    print(f"cfg3 B={n}: {ms:.3f} ms  {n/ms*1e3/1e3:.2f} k precoders/s  {fl/ms/1e9:.2f} TFLOP/s", flush=True)
+
+if __name__ == "__main__":
+    for c in [int(x) for x in (sys.argv[1:] or ["1", "2", "4"])]:
+        if c == 3: t_pgd()
+        else: t_uf(c, reps=10 if c != 4 else 2)
