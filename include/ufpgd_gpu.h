@@ -174,6 +174,13 @@ int ufpgd_gpu_unfolded_forward_sharded(const ufpgd_c64* H, int64_t B, int K, int
                                        double* stats, double alpha);
 
 /*
+ * Measurement helper (not a reference interface): FP32 FMA throughput of the
+ * device with the kernel's own FFMA2 instruction form, and the SM clock read
+ * in-kernel during the probe. The roofline denominator of bench.py.
+ */
+int ufpgd_gpu_fp32_peak(int device, double* tflops, double* sm_ghz);
+
+/*
  * Seeded synthetic input generation (harness side of SURVEY §8d, not timed):
  * realization i = first_index + b is generate_channel(Rng::stream(seed_h, i))
  * (channel.cpp:7-16, rng.cpp:19-40), row k scaled in FP64 by

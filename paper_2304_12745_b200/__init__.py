@@ -21,6 +21,10 @@ from .capi import (  # noqa: F401
     W0_GIVEN,
     W0_ZERO,
     abi_version,
+    fp32_peak,
+    init_multi_gpu,
+    shutdown_multi_gpu,
+    unfolded_forward_sharded,
     generate_channels,
     layer_params,
     layers_general,

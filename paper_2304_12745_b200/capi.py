@@ -64,6 +64,7 @@ def lib():
             "ufpgd_gpu_layers_general": (i, [P, i64, i, i, P, P, i, P, i, P, i, d, i, P, P, P, P, P, P, P, i, P]),
             "ufpgd_gpu_unfolded_forward_host": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, P, d, i]),
             "ufpgd_gpu_pgd_fixed_host": (i, [P, i64, i, i, i, d, i64, P, i, P, P, P, P, P, d, i]),
+            "ufpgd_gpu_fp32_peak": (i, [i, P, P]),
             "ufpgd_gpu_init": (i, [i]),
             "ufpgd_gpu_shutdown": (i, []),
             "ufpgd_gpu_unfolded_forward_sharded": (i, [P, i64, i, i, P, P, i, P, P, P, P, d]),
@@ -263,6 +264,42 @@ def pgd_fixed_host(H: np.ndarray, lambda_: float, iters: int, c, *, power_steps:
         rc = OK
     _check(rc, div, 1)
     return dict(W=W, diverged_at=div, eta=eta, stats=stats)
+
+
+def fp32_peak(device: int = 0):
+    """Measured FP32 FMA peak (TFLOP/s) with the fused kernel's FFMA2 form and
+    the SM clock (GHz) observed during the probe."""
+    t, g = C.c_double(), C.c_double()
+    _check(lib().ufpgd_gpu_fp32_peak(device, C.byref(t), C.byref(g)))
+    return t.value, g.value
+
+
+def init_multi_gpu(ngpus: int):
+    _check(lib().ufpgd_gpu_init(ngpus))
+
+
+def shutdown_multi_gpu():
+    _check(lib().ufpgd_gpu_shutdown())
+
+
+def unfolded_forward_sharded(H: np.ndarray, lambda_, eta, c, *, alpha: float = 1.0,
+                             raise_on_divergence: bool = True):
+    """Single-process multi-GPU forward over the devices given to
+    init_multi_gpu: contiguous shards, one NCCL all-reduce of the statistics."""
+    H = np.asarray(H)
+    if H.dtype != np.complex64 or H.ndim != 3 or not H.flags.c_contiguous:
+        raise ValueError("H must be a C-contiguous complex64 array [B, M, K]")
+    B, M, K = H.shape
+    lam, et, cc = _f64(lambda_), _f64(eta), _f64(c)
+    W = np.empty_like(H)
+    div = np.empty(B, dtype=np.int32)
+    stats = np.zeros(3)
+    rc = lib().ufpgd_gpu_unfolded_forward_sharded(_ptr(H), B, K, M, _ptr(lam), _ptr(et), lam.size, _ptr(cc),
+                                                  _ptr(W), _ptr(div), _ptr(stats), float(alpha))
+    if rc == EDIVERGED and not raise_on_divergence:
+        rc = OK
+    _check(rc, div)
+    return dict(W=W, diverged_at=div, stats=stats)
 
 
 def generate_channels(seed_h: int, seed_g: int, gain_range_db: float, first_index: int, B: int, K: int,

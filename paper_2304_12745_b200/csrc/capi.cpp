@@ -196,73 +196,86 @@ bool load_nccl() {
          g_nccl.CommDestroy;
 }
 
+// Per-device workspace of the host-buffer path: three streams and grow-only
+// device buffers, kept across calls so an end-to-end call costs only its
+// copies and kernels. Host calls on one device are serialised by its mutex.
+struct HostWorkspace {
+  std::mutex mu;
+  bool init = false;
+  static constexpr int NS = 3;
+  cudaStream_t st[NS] = {};
+  void* buf[NS][5] = {};
+  size_t cap[NS][5] = {};
+  double* partials = nullptr;
+  size_t partials_cap = 0;
+  double* dstats = nullptr;
+};
+HostWorkspace g_ws[64];
+
+cudaError_t ensure(void*& p, size_t& cap, size_t need) {
+  if (need <= cap) return cudaSuccess;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  cudaError_t e = cudaMalloc(&p, need);
+  if (e == cudaSuccess) cap = need;
+  return e;
+}
+
 // Chunked host pipeline shared by the unfolded and PGD host entry points.
 // `run` enqueues the kernel for one chunk on stream s given device buffers.
 template <class Run>
-int host_pipeline(const ufpgd_c64* H, int64_t B, int K, int M, const ufpgd_c64* W0, ufpgd_c64* W,
-                  int32_t* diverged_at, float* eta_out, long long parts_per_chunk_max,
+int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const ufpgd_c64* W0,
+                  ufpgd_c64* W, int32_t* diverged_at, float* eta_out, long long parts_per_chunk_max,
                   int64_t chunk, double* stats, Run run) {
+  if (device < 0 || device >= 64) return fail(UFPGD_EINVAL_PARAM, "device out of range");
+  HostWorkspace& ws = g_ws[device];
+  std::lock_guard<std::mutex> lock(ws.mu);
+  constexpr int NS = HostWorkspace::NS;
+  if (!ws.init) {
+    for (int i = 0; i < NS; ++i) UFPGD_CUDA(cudaStreamCreateWithFlags(&ws.st[i], cudaStreamNonBlocking));
+    UFPGD_CUDA(cudaMalloc(&ws.dstats, sizeof(double) * 3));
+    ws.init = true;
+  }
   const size_t per = static_cast<size_t>(K) * M * sizeof(float2);
-  constexpr int NS = 3;
-  cudaStream_t st[NS];
-  for (int i = 0; i < NS; ++i) UFPGD_CUDA(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
-  struct Buf {
-    float2 *h = nullptr, *w = nullptr, *w0 = nullptr;
-    int32_t* div = nullptr;
-    float* eta = nullptr;
-  } buf[NS];
   const int64_t nchunks = B == 0 ? 0 : (B + chunk - 1) / chunk;
-  double* partials = nullptr;
-  double* dstats = nullptr;
-  int rc = UFPGD_OK;
-  auto cleanup = [&] {
-    for (int i = 0; i < NS; ++i) {
-      cudaStreamSynchronize(st[i]);
-      cudaFree(buf[i].h);
-      cudaFree(buf[i].w);
-      cudaFree(buf[i].w0);
-      cudaFree(buf[i].div);
-      cudaFree(buf[i].eta);
-      cudaStreamDestroy(st[i]);
-    }
-    cudaFree(partials);
-    cudaFree(dstats);
-  };
+  const size_t need[5] = {per * chunk, per * chunk, W0 ? per * chunk : 0, sizeof(int32_t) * chunk,
+                          eta_out ? sizeof(float) * chunk : 0};
   cudaError_t e = cudaSuccess;
-  for (int i = 0; i < NS && e == cudaSuccess; ++i) {
-    e = cudaMalloc(&buf[i].h, per * chunk);
-    if (e == cudaSuccess) e = cudaMalloc(&buf[i].w, per * chunk);
-    if (e == cudaSuccess && W0) e = cudaMalloc(&buf[i].w0, per * chunk);
-    if (e == cudaSuccess) e = cudaMalloc(&buf[i].div, sizeof(int32_t) * chunk);
-    if (e == cudaSuccess && eta_out) e = cudaMalloc(&buf[i].eta, sizeof(float) * chunk);
+  for (int i = 0; i < NS && e == cudaSuccess; ++i)
+    for (int q = 0; q < 5 && e == cudaSuccess; ++q) e = ensure(ws.buf[i][q], ws.cap[i][q], need[q]);
+  if (e == cudaSuccess) {
+    void* pp = ws.partials;
+    e = ensure(pp, ws.partials_cap, sizeof(double) * 3 * std::max<long long>(1, parts_per_chunk_max * nchunks));
+    ws.partials = static_cast<double*>(pp);
   }
-  if (e == cudaSuccess) e = cudaMalloc(&partials, sizeof(double) * 3 * std::max<long long>(1, parts_per_chunk_max * nchunks));
-  if (e == cudaSuccess) e = cudaMalloc(&dstats, sizeof(double) * 3);
-  if (e != cudaSuccess) {
-    cleanup();
-    return cuda_fail(e, "host pipeline allocation");
-  }
+  if (e != cudaSuccess) return cuda_fail(e, "host pipeline allocation");
+  int rc = UFPGD_OK;
   std::vector<long long> part_off(nchunks + 1, 0);
   for (int64_t ci = 0; ci < nchunks && rc == UFPGD_OK; ++ci) {
     const int i = static_cast<int>(ci % NS);
     const int64_t b0 = ci * chunk, nb = std::min<int64_t>(chunk, B - b0);
-    cudaStream_t s = st[i];
-    e = cudaMemcpyAsync(buf[i].h, H + b0 * K * M, per * nb, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess && W0)
-      e = cudaMemcpyAsync(buf[i].w0, W0 + b0 * K * M, per * nb, cudaMemcpyHostToDevice, s);
+    cudaStream_t s = ws.st[i];
+    float2* dh = static_cast<float2*>(ws.buf[i][0]);
+    float2* dw = static_cast<float2*>(ws.buf[i][1]);
+    float2* dw0 = static_cast<float2*>(ws.buf[i][2]);
+    int32_t* ddiv = static_cast<int32_t*>(ws.buf[i][3]);
+    float* deta = static_cast<float*>(ws.buf[i][4]);
+    e = cudaMemcpyAsync(dh, H + b0 * K * M, per * nb, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && W0) e = cudaMemcpyAsync(dw0, W0 + b0 * K * M, per * nb, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) {
       rc = cuda_fail(e, "H2D");
       break;
     }
     long long np = 0;
-    rc = run(buf[i].h, nb, buf[i].w0, buf[i].w, buf[i].div, buf[i].eta, partials + 3 * part_off[ci], &np, s);
+    rc = run(dh, nb, W0 ? dw0 : nullptr, dw, ddiv, eta_out ? deta : nullptr, ws.partials + 3 * part_off[ci], &np, s);
     if (rc != UFPGD_OK) break;
     part_off[ci + 1] = part_off[ci] + np;
-    e = cudaMemcpyAsync(W + b0 * K * M, buf[i].w, per * nb, cudaMemcpyDeviceToHost, s);
+    e = cudaMemcpyAsync(W + b0 * K * M, dw, per * nb, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && diverged_at)
-      e = cudaMemcpyAsync(diverged_at + b0, buf[i].div, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, s);
+      e = cudaMemcpyAsync(diverged_at + b0, ddiv, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && eta_out)
-      e = cudaMemcpyAsync(eta_out + b0, buf[i].eta, sizeof(float) * nb, cudaMemcpyDeviceToHost, s);
+      e = cudaMemcpyAsync(eta_out + b0, deta, sizeof(float) * nb, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) rc = cuda_fail(e, "D2H");
   }
   double host_stats[3] = {0.0, 0.0, 0.0};
@@ -270,16 +283,17 @@ int host_pipeline(const ufpgd_c64* H, int64_t B, int K, int M, const ufpgd_c64* 
     for (int i = 1; i < NS; ++i) {
       cudaEvent_t ev;
       cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-      cudaEventRecord(ev, st[i]);
-      cudaStreamWaitEvent(st[0], ev, 0);
+      cudaEventRecord(ev, ws.st[i]);
+      cudaStreamWaitEvent(ws.st[0], ev, 0);
       cudaEventDestroy(ev);
     }
-    e = launch_stats_finalize(partials, part_off[nchunks], dstats, st[0]);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(host_stats, dstats, sizeof(host_stats), cudaMemcpyDeviceToHost, st[0]);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st[0]);
+    e = launch_stats_finalize(ws.partials, part_off[nchunks], ws.dstats, ws.st[0]);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(host_stats, ws.dstats, sizeof(host_stats), cudaMemcpyDeviceToHost, ws.st[0]);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ws.st[0]);
     if (e != cudaSuccess) rc = cuda_fail(e, "host pipeline finalize");
   }
-  cleanup();
+  for (int i = 0; i < NS; ++i) cudaStreamSynchronize(ws.st[i]);
   if (rc != UFPGD_OK) return rc;
   if (stats) std::memcpy(stats, host_stats, sizeof(host_stats));
   if (host_stats[2] > 0.0) return fail(UFPGD_EDIVERGED, "non-finite iterate in at least one realization");
@@ -511,7 +525,7 @@ int ufpgd_gpu_unfolded_forward_host(const ufpgd_c64* H, int64_t B, int K, int M,
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, (32ll << 20) / (8ll * K * M)));
   const long long ppc = partial_count(chunk, K, M, fused);
   return host_pipeline(
-      H, B, K, M, w0_mode == UFPGD_W0_GIVEN ? W0 : nullptr, W, diverged_at, nullptr, ppc, chunk, stats,
+      device, H, B, K, M, w0_mode == UFPGD_W0_GIVEN ? W0 : nullptr, W, diverged_at, nullptr, ppc, chunk, stats,
       [&](float2* h, int64_t nb, float2* w0, float2* w, int32_t* div, float*, double* parts,
           long long* np, cudaStream_t s) {
         return enqueue_unfolded(h, nb, K, M, lambda, eta, L, c, w0_mode, w0, w, div, nullptr, nullptr,
@@ -533,7 +547,7 @@ int ufpgd_gpu_pgd_fixed_host(const ufpgd_c64* H, int64_t B, int K, int M, int po
   // The device entry point finalises its own stats per chunk; here the
   // pipeline collects block partials, so call the kernels with partials only.
   return host_pipeline(
-      H, B, K, M, w0_mode == UFPGD_W0_GIVEN ? W0 : nullptr, W, diverged_at, eta_out, ppc, chunk,
+      device, H, B, K, M, w0_mode == UFPGD_W0_GIVEN ? W0 : nullptr, W, diverged_at, eta_out, ppc, chunk,
       stats,
       [&](float2* h, int64_t nb, float2* w0, float2* w, int32_t* div, float* eo, double* parts,
           long long* np, cudaStream_t s) -> int {
@@ -590,6 +604,15 @@ int ufpgd_gpu_pgd_fixed_host(const ufpgd_c64* H, int64_t B, int K, int M, int po
         cudaFreeAsync(lip, s);
         return r;
       });
+}
+
+int ufpgd_gpu_fp32_peak(int device, double* tflops, double* sm_ghz) {
+  if (!tflops || !sm_ghz) return fail(UFPGD_EINVAL_PARAM, "null output");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
+  cudaError_t e = measure_fp32_peak(tflops, sm_ghz);
+  if (e != cudaSuccess) return cuda_fail(e, "fp32 peak probe");
+  return UFPGD_OK;
 }
 
 int ufpgd_gpu_init(int ngpus) {
