@@ -7,13 +7,13 @@ PKG      := paper_2304_12745_b200
 LIBDIR   := $(PKG)/lib
 OBJDIR   := build/obj
 SRCS_CU  := $(PKG)/csrc/kernels.cu
-SRCS_CPP := $(PKG)/csrc/capi.cpp $(PKG)/csrc/host_gen.cpp
+SRCS_CPP := $(PKG)/csrc/capi.cpp $(PKG)/csrc/host_gen.cpp $(PKG)/csrc/api.cpp
 CXX      ?= g++
 CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -Iinclude -I$(PKG)/csrc -I/usr/local/cuda/include
 OBJS     := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(SRCS_CU)) $(patsubst $(PKG)/csrc/%.cpp,$(OBJDIR)/%.o,$(SRCS_CPP))
-HDRS     := include/ufpgd_gpu.h $(PKG)/csrc/ufpgd_internal.h
+HDRS     := include/ufpgd_gpu.h $(PKG)/csrc/ufpgd_internal.h $(wildcard include/ufpgd/*.hpp)
 
-all: $(LIBDIR)/libufpgd_gpu.so oracle
+all: $(LIBDIR)/libufpgd_gpu.so oracle build/test_api
 
 $(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -26,6 +26,10 @@ $(OBJDIR)/%.o: $(PKG)/csrc/%.cpp $(HDRS)
 $(LIBDIR)/libufpgd_gpu.so: $(OBJS)
 	@mkdir -p $(LIBDIR)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl -lpthread
+
+build/test_api: tests/cpp/test_api.cpp $(LIBDIR)/libufpgd_gpu.so $(HDRS)
+	@mkdir -p build
+	$(CXX) -O2 -std=c++20 -Iinclude -I/usr/local/cuda/include $< -o $@ -L$(LIBDIR) -lufpgd_gpu -Wl,-rpath,'$$ORIGIN/../$(LIBDIR)'
 
 oracle:
 	$(MAKE) -s -C oracle

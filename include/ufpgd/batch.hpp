@@ -1,0 +1,45 @@
+// Batched entry points: the reason this library exists. They take the
+// reference's per-channel storage stacked into one [B][M][K] complex<float>
+// array (what `parallel_for` over channels did on the CPU, parallel.hpp:12-18)
+// and run the whole batch on the device(s).
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <vector>
+
+#include "ufpgd/pgd.hpp"
+#include "ufpgd/system_config.hpp"
+#include "ufpgd/unfolded.hpp"
+
+namespace ufpgd {
+
+enum class StartMode { Zero = 0, ConjChannel = 1, Given = 2 };
+
+struct BatchResult {
+  std::vector<std::complex<float>> precoders;  // [B][M][K]
+  std::vector<std::int32_t> diverged_at;       // -1 = ok
+  std::vector<float> steps;                    // PGD: the 1/L step used per realization
+  double consumed_power_sum = 0.0;             // sum over non-diverged of alpha ||W||_{2,1}
+  double active_sum = 0.0;                     // sum of active antennas
+  long diverged = 0;
+};
+
+// forward over B channels (unfolded.cpp:83-146 per channel). Validates the
+// network exactly like forward (projected steps, matching K, M); does not
+// throw on divergence — per-realization indices are returned.
+BatchResult forward_batch(const UnfoldedNetwork& net, const std::complex<float>* channels, std::int64_t B,
+                          const SystemConfig& cfg, StartMode start = StartMode::ConjChannel,
+                          const std::complex<float>* W0 = nullptr);
+
+// solve_pgd over B channels with eta_b = 1 / (power_steps-step power iteration)
+// and threshold lambda * eta_b (BASELINE config 3), W0 = H^*.
+BatchResult solve_pgd_batch(const std::complex<float>* channels, std::int64_t B, const SystemConfig& cfg,
+                            double lambda, long iterations, int power_steps = 30);
+
+// forward_batch sharded over `ngpus` devices of this process (one NCCL
+// all-reduce of the statistics).
+BatchResult forward_batch_multi_gpu(const UnfoldedNetwork& net, const std::complex<float>* channels,
+                                    std::int64_t B, const SystemConfig& cfg, int ngpus);
+
+}  // namespace ufpgd

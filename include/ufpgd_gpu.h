@@ -105,6 +105,16 @@ int ufpgd_gpu_power_iteration(const ufpgd_c64* H, int64_t B, int K, int M,
                               ufpgd_stream_t stream);
 
 /*
+ * Batched converged power iteration in FP64 — ufpgd::lipschitz_bound's
+ * `exact` (pgd.cpp:120-169) with the reference's rule: relative change
+ * <= 1e-8 marks convergence, refinement continues to 1e-13 or 1e4 iterations.
+ * H is interleaved complex128 [B][M][K] (device); status[b] = 0 or
+ * UFPGD_ECONVERGENCE. Synchronous on `stream`.
+ */
+int ufpgd_gpu_lipschitz_exact(const double* H, int64_t B, int K, int M, double* Lout,
+                              int32_t* status, int device, ufpgd_stream_t stream);
+
+/*
  * Batched plain PGD at a fixed step per realization — replaces
  * ufpgd::solve_pgd (pgd.hpp:102-110, pgd.cpp:178-268) with trace_every = 0 and
  * residual_tol = 0 over B channels. eta_in[B] (device) gives each
@@ -170,8 +180,8 @@ int ufpgd_gpu_init(int ngpus);
 int ufpgd_gpu_shutdown(void);
 int ufpgd_gpu_unfolded_forward_sharded(const ufpgd_c64* H, int64_t B, int K, int M,
                                        const double* lambda, const double* eta, int L,
-                                       const double* c, ufpgd_c64* W, int32_t* diverged_at,
-                                       double* stats, double alpha);
+                                       const double* c, int w0_mode, ufpgd_c64* W,
+                                       int32_t* diverged_at, double* stats, double alpha);
 
 /*
  * Measurement helper (not a reference interface): FP32 FMA throughput of the
@@ -192,8 +202,10 @@ int ufpgd_generate_channels(uint64_t seed_h, uint64_t seed_g, double gain_range_
                             int64_t first_index, int64_t B, int K, int M, ufpgd_c64* H,
                             int threads);
 
-/* The reference's power-iteration start vector (pgd.cpp:131-134), FP64 -> c64. */
+/* The reference's power-iteration start vector (pgd.cpp:131-134), FP64 -> c64,
+ * and in FP64 (interleaved re, im). */
 int ufpgd_power_v0(int M, ufpgd_c64* v0);
+int ufpgd_power_v0_f64(int M, double* v0);
 
 /*
  * BASELINE layer parameters: Rng::stream(seed_p, 0) draws in pack order

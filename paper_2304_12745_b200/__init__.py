@@ -28,6 +28,7 @@ from .capi import (  # noqa: F401
     generate_channels,
     layer_params,
     layers_general,
+    lipschitz_exact,
     lib,
     lib_path,
     pgd_fixed,

@@ -67,7 +67,9 @@ def lib():
             "ufpgd_gpu_fp32_peak": (i, [i, P, P]),
             "ufpgd_gpu_init": (i, [i]),
             "ufpgd_gpu_shutdown": (i, []),
-            "ufpgd_gpu_unfolded_forward_sharded": (i, [P, i64, i, i, P, P, i, P, P, P, P, d]),
+            "ufpgd_gpu_unfolded_forward_sharded": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, d]),
+            "ufpgd_gpu_lipschitz_exact": (i, [P, i64, i, i, P, P, i, P]),
+            "ufpgd_power_v0_f64": (i, [i, P]),
             "ufpgd_generate_channels": (i, [u64, u64, d, i64, i64, i, i, P, i]),
             "ufpgd_power_v0": (i, [i, P]),
             "ufpgd_layer_params": (i, [u64, i, i, i, P, P]),
@@ -266,6 +268,22 @@ def pgd_fixed_host(H: np.ndarray, lambda_: float, iters: int, c, *, power_steps:
     return dict(W=W, diverged_at=div, eta=eta, stats=stats)
 
 
+def lipschitz_exact(H, stream=None):
+    """Converged FP64 power iteration (pgd.cpp:120-169) for a complex128 CUDA
+    tensor [B, M, K]; returns (L float64[B], status int32[B])."""
+    import torch
+
+    if not (isinstance(H, torch.Tensor) and H.is_cuda and H.dtype == torch.complex128 and H.dim() == 3
+            and H.is_contiguous()):
+        raise ValueError("H must be a contiguous CUDA complex128 tensor [B, M, K]")
+    B, M, K = H.shape
+    Lout = torch.empty(B, dtype=torch.float64, device=H.device)
+    st = torch.empty(B, dtype=torch.int32, device=H.device)
+    _check(lib().ufpgd_gpu_lipschitz_exact(_ptr(H), B, K, M, _ptr(Lout), _ptr(st), H.device.index or 0,
+                                           _stream_ptr(stream)))
+    return Lout, st
+
+
 def fp32_peak(device: int = 0):
     """Measured FP32 FMA peak (TFLOP/s) with the fused kernel's FFMA2 form and
     the SM clock (GHz) observed during the probe."""
@@ -282,7 +300,7 @@ def shutdown_multi_gpu():
     _check(lib().ufpgd_gpu_shutdown())
 
 
-def unfolded_forward_sharded(H: np.ndarray, lambda_, eta, c, *, alpha: float = 1.0,
+def unfolded_forward_sharded(H: np.ndarray, lambda_, eta, c, *, w0_mode: int = W0_ZERO, alpha: float = 1.0,
                              raise_on_divergence: bool = True):
     """Single-process multi-GPU forward over the devices given to
     init_multi_gpu: contiguous shards, one NCCL all-reduce of the statistics."""
@@ -295,7 +313,7 @@ def unfolded_forward_sharded(H: np.ndarray, lambda_, eta, c, *, alpha: float = 1
     div = np.empty(B, dtype=np.int32)
     stats = np.zeros(3)
     rc = lib().ufpgd_gpu_unfolded_forward_sharded(_ptr(H), B, K, M, _ptr(lam), _ptr(et), lam.size, _ptr(cc),
-                                                  _ptr(W), _ptr(div), _ptr(stats), float(alpha))
+                                                  w0_mode, _ptr(W), _ptr(div), _ptr(stats), float(alpha))
     if rc == EDIVERGED and not raise_on_divergence:
         rc = OK
     _check(rc, div)

@@ -1,0 +1,563 @@
+// C++ API with the reference's signatures (include/ufpgd/*.hpp), implemented
+// on the C ABI (include/ufpgd_gpu.h). Validation and exceptions follow the
+// reference (pgd.cpp, unfolded.cpp, system_config.cpp); all precoder math runs
+// on the device. Scalar helpers (mp_bound, project_params, constraint_diag,
+// metrics of one matrix) are host code, as in the reference.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <numbers>
+#include <string>
+#include <vector>
+
+#include "ufpgd/batch.hpp"
+#include "ufpgd/errors.hpp"
+#include "ufpgd/metrics.hpp"
+#include "ufpgd/pgd.hpp"
+#include "ufpgd/rng.hpp"
+#include "ufpgd/system_config.hpp"
+#include "ufpgd/unfolded.hpp"
+#include "ufpgd_gpu.h"
+
+namespace ufpgd {
+namespace {
+
+int g_device = 0;
+
+[[noreturn]] void raise(int rc, long index = -1) {
+  const std::string msg = ufpgd_gpu_last_error();
+  switch (rc) {
+    case UFPGD_EINVAL_SHAPE:
+    case UFPGD_EINVAL_PARAM:
+      throw std::invalid_argument(msg);
+    case UFPGD_EDIVERGED:
+      throw DivergenceError(msg, index);
+    case UFPGD_ECONVERGENCE:
+      throw ConvergenceError(msg);
+    default:
+      throw DeviceError("ufpgd device error " + std::to_string(rc) + ": " + msg);
+  }
+}
+
+void check(int rc) {
+  if (rc != UFPGD_OK) raise(rc);
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// RAII device buffer.
+template <class T>
+struct DeviceBuffer {
+  T* p = nullptr;
+  std::size_t n = 0;
+  explicit DeviceBuffer(std::size_t count) : n(count) {
+    if (n) cuda_check(cudaMalloc(&p, sizeof(T) * n), "cudaMalloc");
+  }
+  ~DeviceBuffer() {
+    if (p) cudaFree(p);
+  }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  void upload(const T* h) { cuda_check(cudaMemcpy(p, h, sizeof(T) * n, cudaMemcpyHostToDevice), "H2D"); }
+  void download(T* h) const { cuda_check(cudaMemcpy(h, p, sizeof(T) * n, cudaMemcpyDeviceToHost), "D2H"); }
+};
+
+struct DeviceScope {
+  int prev = 0;
+  DeviceScope() {
+    cudaGetDevice(&prev);
+    cuda_check(cudaSetDevice(g_device), "cudaSetDevice");
+  }
+  ~DeviceScope() { cudaSetDevice(prev); }
+};
+
+// K x M complex<double> (col-major) -> complex64 [M][K] (same element order).
+std::vector<ufpgd_c64> to_c64(const ComplexMatrix& A) {
+  std::vector<ufpgd_c64> out(static_cast<std::size_t>(A.size()));
+  const Complex* d = A.data();
+  for (std::size_t i = 0; i < out.size(); ++i)
+    out[i] = {static_cast<float>(d[i].real()), static_cast<float>(d[i].imag())};
+  return out;
+}
+
+ComplexMatrix from_c64(const ufpgd_c64* d, std::ptrdiff_t K, std::ptrdiff_t M) {
+  ComplexMatrix A(K, M);
+  Complex* o = A.data();
+  for (std::ptrdiff_t i = 0; i < K * M; ++i) o[i] = Complex(d[i].re, d[i].im);
+  return A;
+}
+
+void check_shapes(const ChannelMatrix& channel, const SystemConfig& cfg) {  // pgd.cpp:16-21
+  cfg.validate();
+  if (channel.rows() != cfg.K || channel.cols() != cfg.M)
+    throw std::invalid_argument("channel shape does not match SystemConfig");
+}
+
+constexpr double kBoundSlack = 1e-12;  // unfolded.cpp:17
+
+void check_projected(const UnfoldedNetwork& net) {  // unfolded.cpp:19-35
+  const double hi = 1.0 / net.mp_bound, lo = 0.5 * hi;
+  for (std::size_t i = 0; i < net.layers.size(); ++i) {
+    const LayerParams& l = net.layers[i];
+    if (!(l.lambda_i >= 0.0) || !std::isfinite(l.lambda_i))
+      throw std::invalid_argument("UnfoldedNetwork: layer " + std::to_string(i) + " lambda_i < 0");
+    if (!(l.eta_i >= lo * (1.0 - kBoundSlack)) || !(l.eta_i <= hi * (1.0 + kBoundSlack)))
+      throw std::invalid_argument("UnfoldedNetwork: layer " + std::to_string(i) + " eta_i outside [1/(2L), 1/L]");
+  }
+}
+
+// Runs the general-shape layer sweep on one realization.
+struct LayerRun {
+  PrecoderMatrix W;
+  int32_t diverged = -1;
+  int64_t iterations = 0;
+  std::vector<ufpgd_c64> iterates, tape_v;
+  std::vector<float> tape_norms, tape_shrink;
+};
+
+LayerRun run_layers(const ChannelMatrix& H, const RealVector& c, const std::vector<double>& eta,
+                    const std::vector<double>& thr, int w0_mode, const ComplexMatrix* W0, int mode,
+                    double residual_tol, int index_base, bool iterates, bool tape) {
+  const int K = static_cast<int>(H.rows()), M = static_cast<int>(H.cols());
+  const int L = mode == 1 ? 1 : static_cast<int>(eta.size());
+  const std::size_t n = static_cast<std::size_t>(K) * M;
+  DeviceScope scope;
+  DeviceBuffer<ufpgd_c64> dH(n), dW(n), dW0(W0 ? n : 0);
+  DeviceBuffer<int32_t> ddiv(1);
+  DeviceBuffer<int64_t> dits(1);
+  DeviceBuffer<ufpgd_c64> ditr(iterates ? (L + 1) * n : 0), dtv(tape ? L * n : 0);
+  DeviceBuffer<float> dtn(tape ? static_cast<std::size_t>(L) * M : 0), dts(tape ? static_cast<std::size_t>(L) * M : 0);
+  const auto h = to_c64(H);
+  dH.upload(h.data());
+  if (W0) {
+    const auto w0 = to_c64(*W0);
+    dW0.upload(w0.data());
+  }
+  check(ufpgd_gpu_layers_general(dH.p, 1, K, M, eta.data(), thr.data(), L, c.data(), w0_mode, dW0.p, mode,
+                                 residual_tol, index_base, dW.p, ddiv.p, dits.p, ditr.p, dtv.p, dtn.p, dts.p,
+                                 g_device, nullptr));
+  cuda_check(cudaDeviceSynchronize(), "layers_general");
+  LayerRun r;
+  std::vector<ufpgd_c64> w(n);
+  dW.download(w.data());
+  r.W = from_c64(w.data(), K, M);
+  ddiv.download(&r.diverged);
+  dits.download(&r.iterations);
+  if (iterates) {
+    r.iterates.resize((L + 1) * n);
+    ditr.download(r.iterates.data());
+  }
+  if (tape) {
+    r.tape_v.resize(L * n);
+    r.tape_norms.resize(static_cast<std::size_t>(L) * M);
+    r.tape_shrink.resize(static_cast<std::size_t>(L) * M);
+    dtv.download(r.tape_v.data());
+    dtn.download(r.tape_norms.data());
+    dts.download(r.tape_shrink.data());
+  }
+  return r;
+}
+
+std::uint64_t mix64(std::uint64_t x) {  // rng.cpp:10-15
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+
+}  // namespace
+
+// ---- system_config.cpp -------------------------------------------------------
+SystemConfig SystemConfig::uniform(int num_users, int num_antennas, double sinr_target, double noise_std,
+                                   double pa_scale) {
+  SystemConfig cfg;
+  cfg.K = num_users;
+  cfg.M = num_antennas;
+  cfg.sigma_nu = noise_std;
+  cfg.gamma = RealVector::Constant(std::max(num_users, 0), sinr_target);
+  cfg.alpha = pa_scale;
+  cfg.validate();
+  return cfg;
+}
+
+void SystemConfig::validate() const {
+  if (K < 1) throw std::invalid_argument("SystemConfig: K must be >= 1");
+  if (M < K)
+    throw std::invalid_argument("SystemConfig: need K <= M, got K=" + std::to_string(K) + " M=" + std::to_string(M));
+  if (!(sigma_nu >= 0.0)) throw std::invalid_argument("SystemConfig: sigma_nu must be >= 0");
+  if (gamma.size() != K) throw std::invalid_argument("SystemConfig: gamma must have K entries");
+  for (std::ptrdiff_t k = 0; k < gamma.size(); ++k)
+    if (!(gamma[k] > 0.0)) throw std::invalid_argument("SystemConfig: gamma[" + std::to_string(k) + "] must be > 0");
+  if (!(alpha > 0.0)) throw std::invalid_argument("SystemConfig: alpha must be > 0");
+}
+
+RealVector SystemConfig::constraint_diag() const {
+  RealVector c(gamma.size());
+  for (std::ptrdiff_t k = 0; k < gamma.size(); ++k) c[k] = sigma_nu * std::sqrt(gamma[k]);
+  return c;
+}
+
+// ---- rng.cpp / channel.cpp ------------------------------------------------------
+Rng Rng::stream(std::uint64_t seed, std::uint64_t stream_index) { return Rng(mix64(seed ^ mix64(stream_index))); }
+double Rng::uniform() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+double Rng::uniform_open() { return static_cast<double>((next_u64() >> 11) + 1) * 0x1.0p-53; }
+std::size_t Rng::index_below(std::size_t n) { return static_cast<std::size_t>(next_u64() % n); }
+Complex Rng::complex_gaussian() {
+  const double radius = std::sqrt(-std::log(uniform_open()));
+  const double angle = 2.0 * std::numbers::pi * uniform();
+  return {radius * std::cos(angle), radius * std::sin(angle)};
+}
+
+ChannelMatrix generate_channel(const SystemConfig& cfg, Rng& rng) {
+  cfg.validate();
+  ChannelMatrix h(cfg.K, cfg.M);
+  for (int k = 0; k < cfg.K; ++k)
+    for (int m = 0; m < cfg.M; ++m) h(k, m) = rng.complex_gaussian();
+  return h;
+}
+
+// ---- pgd.cpp ------------------------------------------------------------------
+void set_device(int d) { g_device = d; }
+int device() { return g_device; }
+
+void PgdParams::validate() const {
+  if (!(lambda >= 0.0)) throw std::invalid_argument("PgdParams: lambda must be >= 0");
+  if (!(eta > 0.0)) throw std::invalid_argument("PgdParams: eta must be > 0");
+  if (max_iters < 0) throw std::invalid_argument("PgdParams: max_iters must be >= 0");
+  if (!(residual_tol >= 0.0)) throw std::invalid_argument("PgdParams: residual_tol must be >= 0");
+  if (trace_every < 0) throw std::invalid_argument("PgdParams: trace_every must be >= 0");
+  if (trace_every > 0)
+    throw std::invalid_argument("PgdParams: trace recording is not part of the B200 path (trace_every must be 0)");
+}
+
+SmoothGradient SmoothGradient::make(const ChannelMatrix& channel, const SystemConfig& cfg) {
+  check_shapes(channel, cfg);
+  SmoothGradient g;
+  g.h_trans = channel.transpose();
+  g.h_conj = channel.conjugate();
+  g.c = cfg.constraint_diag();
+  g.offset = g.h_conj;
+  for (std::ptrdiff_t m = 0; m < g.offset.cols(); ++m)
+    for (std::ptrdiff_t k = 0; k < g.offset.rows(); ++k) g.offset(k, m) *= g.c[k];
+  g.channel = channel;
+  return g;
+}
+
+ComplexMatrix SmoothGradient::apply(const PrecoderMatrix& precoder) const {
+  if (precoder.rows() != channel.rows() || precoder.cols() != channel.cols())
+    throw std::invalid_argument("SmoothGradient: precoder shape mismatch");
+  return run_layers(channel, c, {0.0}, {0.0}, UFPGD_W0_GIVEN, &precoder, 1, 0.0, 0, false, false).W;
+}
+
+void SmoothGradient::apply_into(const PrecoderMatrix& precoder, ComplexMatrix& scratch, ComplexMatrix& out) const {
+  scratch = ComplexMatrix(precoder.rows(), precoder.rows());
+  out = apply(precoder);
+}
+
+ComplexMatrix grad_f(const PrecoderMatrix& precoder, const ChannelMatrix& channel, const SystemConfig& cfg) {
+  if (precoder.rows() != channel.rows() || precoder.cols() != channel.cols())
+    throw std::invalid_argument("grad_f: precoder/channel shape mismatch");
+  return SmoothGradient::make(channel, cfg).apply(precoder);
+}
+
+PrecoderMatrix prox_l21(const ComplexMatrix& input, double t) {
+  if (!(t >= 0.0)) throw std::invalid_argument("prox_l21: threshold must be >= 0");
+  // eta = 0 leaves V = W; the channel is irrelevant (a zero K x M channel).
+  ChannelMatrix zero(input.rows(), input.cols());
+  RealVector c(input.rows(), 0.0);
+  return run_layers(zero, c, {0.0}, {t}, UFPGD_W0_GIVEN, &input, 0, 0.0, 0, false, false).W;
+}
+
+PrecoderMatrix pgd_step(const PrecoderMatrix& precoder, const ChannelMatrix& channel, const SystemConfig& cfg,
+                        double lambda, double eta) {
+  if (!(lambda >= 0.0) || !(eta > 0.0)) throw std::invalid_argument("pgd_step: need lambda >= 0 and eta > 0");
+  check_shapes(channel, cfg);
+  if (precoder.rows() != cfg.K || precoder.cols() != cfg.M)
+    throw std::invalid_argument("grad_f: precoder/channel shape mismatch");
+  return run_layers(channel, cfg.constraint_diag(), {eta}, {lambda * eta}, UFPGD_W0_GIVEN, &precoder, 0, 0.0, 0,
+                    false, false)
+      .W;
+}
+
+double mp_bound(int num_users, int num_antennas) {  // pgd.cpp:111-118
+  if (num_users < 1 || num_antennas < 1) throw std::invalid_argument("mp_bound: dimensions must be positive");
+  const double edge = std::sqrt(static_cast<double>(num_users)) + std::sqrt(static_cast<double>(num_antennas));
+  return edge * edge;
+}
+
+LipschitzBound lipschitz_bound(const ChannelMatrix& channel) {
+  if (channel.rows() < 1 || channel.cols() < 1) throw std::invalid_argument("lipschitz_bound: empty channel");
+  LipschitzBound b;
+  b.mp = mp_bound(static_cast<int>(channel.rows()), static_cast<int>(channel.cols()));
+  DeviceScope scope;
+  const std::size_t n = static_cast<std::size_t>(channel.size());
+  DeviceBuffer<double> dH(2 * n), dL(1);
+  DeviceBuffer<int32_t> dst(1);
+  dH.upload(reinterpret_cast<const double*>(channel.data()));
+  check(ufpgd_gpu_lipschitz_exact(dH.p, 1, static_cast<int>(channel.rows()), static_cast<int>(channel.cols()), dL.p,
+                                  dst.p, g_device, nullptr));
+  int32_t st = 0;
+  dst.download(&st);
+  if (st != 0)
+    throw ConvergenceError("lipschitz_bound: power iteration did not reach tolerance 1e-8 within 10000 iterations");
+  dL.download(&b.exact);
+  return b;
+}
+
+double lagrangian_value(const PrecoderMatrix& precoder, const ChannelMatrix& channel, const SystemConfig& cfg,
+                        double lambda) {
+  const double r = constraint_residual(channel, precoder, cfg);
+  return lambda * l21_norm(precoder) + r * r;
+}
+
+PgdResult solve_pgd(const ChannelMatrix& channel, const SystemConfig& cfg, const PgdParams& params,
+                    const std::optional<PrecoderMatrix>& start) {
+  check_shapes(channel, cfg);
+  params.validate();
+  if (start && (start->rows() != cfg.K || start->cols() != cfg.M))
+    throw std::invalid_argument("solve_pgd: W0 shape mismatch");
+  PgdResult result;
+  if (params.max_iters == 0) {
+    result.precoder = start ? *start : channel.conjugate();
+    return result;
+  }
+  // The general kernel takes <= UFPGD_MAX_LAYERS (eta, thr) pairs per launch;
+  // longer runs are chained launch by launch from the previous iterate.
+  PrecoderMatrix w = start ? *start : channel.conjugate();
+  long done = 0;
+  while (done < params.max_iters) {
+    const long chunk = std::min<long>(UFPGD_MAX_LAYERS, params.max_iters - done);
+    std::vector<double> eta(static_cast<std::size_t>(chunk), params.eta);
+    std::vector<double> thr(static_cast<std::size_t>(chunk), params.lambda * params.eta);
+    LayerRun r = run_layers(channel, cfg.constraint_diag(), eta, thr, UFPGD_W0_GIVEN, &w, 0, params.residual_tol, 1,
+                            false, false);
+    if (r.diverged >= 0) throw DivergenceError("solve_pgd: non-finite iterate", done + r.diverged);
+    w = r.W;
+    done += r.iterations;
+    if (r.iterations < chunk) break;  // residual_tol stop inside the chunk
+  }
+  result.precoder = w;
+  result.iterations = done;
+  return result;
+}
+
+PrecoderMatrix oracle_solve(const ChannelMatrix& channel, const SystemConfig& cfg, double lambda) {
+  PgdParams params;
+  params.lambda = lambda;
+  params.eta = 1.0 / lipschitz_bound(channel).exact;
+  params.max_iters = 100000;
+  params.residual_tol = 1e-10;
+  return solve_pgd(channel, cfg, params).precoder;
+}
+
+// ---- unfolded.cpp -------------------------------------------------------------
+UnfoldedNetwork UnfoldedNetwork::pgd_init(int num_users, int num_antennas, int num_layers, double lambda) {
+  if (num_layers < 1) throw std::invalid_argument("pgd_init: need at least one layer");
+  if (!(lambda >= 0.0)) throw std::invalid_argument("pgd_init: lambda must be >= 0");
+  UnfoldedNetwork net;
+  net.num_users = num_users;
+  net.num_antennas = num_antennas;
+  net.mp_bound = ufpgd::mp_bound(num_users, num_antennas);
+  net.layers.assign(static_cast<std::size_t>(num_layers), LayerParams{lambda, 1.0 / net.mp_bound});
+  net.validate();
+  return net;
+}
+
+void UnfoldedNetwork::validate() const {
+  if (num_users < 1 || num_antennas < num_users) throw std::invalid_argument("UnfoldedNetwork: bad dimensions");
+  if (layers.empty()) throw std::invalid_argument("UnfoldedNetwork: no layers");
+  const double expected = ufpgd::mp_bound(num_users, num_antennas);
+  if (!(std::abs(mp_bound - expected) <= 1e-9 * expected))
+    throw std::invalid_argument("UnfoldedNetwork: mp_bound does not match (K, M)");
+}
+
+UnfoldedNetwork project_params(const UnfoldedNetwork& net) {
+  net.validate();
+  UnfoldedNetwork p = net;
+  const double hi = 1.0 / p.mp_bound, lo = 0.5 * hi;
+  for (LayerParams& l : p.layers) {
+    l.lambda_i = std::max(0.0, l.lambda_i);
+    l.eta_i = std::min(std::max(l.eta_i, lo), hi);
+  }
+  return p;
+}
+
+ForwardResult forward(const UnfoldedNetwork& net, const ChannelMatrix& channel, const SystemConfig& cfg,
+                      const std::optional<PrecoderMatrix>& start, const ForwardOptions& options) {
+  net.validate();
+  check_projected(net);
+  cfg.validate();
+  if (cfg.K != net.num_users || cfg.M != net.num_antennas || channel.rows() != cfg.K || channel.cols() != cfg.M)
+    throw std::invalid_argument("forward: dimension mismatch");
+  if (start && (start->rows() != cfg.K || start->cols() != cfg.M))
+    throw std::invalid_argument("forward: W0 shape mismatch");
+  const int L = static_cast<int>(net.layers.size());
+  std::vector<double> eta, thr;
+  for (const LayerParams& l : net.layers) {
+    eta.push_back(l.eta_i);
+    thr.push_back(l.lambda_i * l.eta_i);
+  }
+  ForwardResult result;
+  // Networks deeper than one launch's parameter block are chained.
+  if (L > UFPGD_MAX_LAYERS && !options.with_tape && !options.with_iterates) {
+    PrecoderMatrix w = start ? *start : channel.conjugate();
+    for (int l0 = 0; l0 < L; l0 += UFPGD_MAX_LAYERS) {
+      const int l1 = std::min(L, l0 + UFPGD_MAX_LAYERS);
+      LayerRun r = run_layers(channel, cfg.constraint_diag(), {eta.begin() + l0, eta.begin() + l1},
+                              {thr.begin() + l0, thr.begin() + l1}, UFPGD_W0_GIVEN, &w, 0, 0.0, 0, false, false);
+      if (r.diverged >= 0) throw DivergenceError("forward: non-finite iterate at layer", l0 + r.diverged);
+      w = r.W;
+    }
+    result.output = w;
+    return result;
+  }
+  if (L > UFPGD_MAX_LAYERS) throw std::invalid_argument("forward: tapes support at most UFPGD_MAX_LAYERS layers");
+  LayerRun r = run_layers(channel, cfg.constraint_diag(), eta, thr, start ? UFPGD_W0_GIVEN : UFPGD_W0_CONJ_H,
+                          start ? &*start : nullptr, 0, 0.0, 0, options.with_iterates || options.with_tape,
+                          options.with_tape);
+  if (r.diverged >= 0) throw DivergenceError("forward: non-finite iterate at layer", r.diverged);
+  result.output = r.W;
+  const std::ptrdiff_t K = cfg.K, M = cfg.M, n = K * M;
+  if (options.with_iterates)
+    for (int i = 0; i <= L; ++i) result.iterates.push_back(from_c64(r.iterates.data() + i * n, K, M));
+  if (options.with_tape) {
+    result.tape.layers.resize(static_cast<std::size_t>(L));
+    for (int i = 0; i < L; ++i) {
+      LayerTape& t = result.tape.layers[static_cast<std::size_t>(i)];
+      t.input = from_c64(r.iterates.data() + i * n, K, M);
+      t.step_image = from_c64(r.tape_v.data() + i * n, K, M);
+      t.column_norms.resize(M);
+      t.shrink_factors.resize(M);
+      for (std::ptrdiff_t m = 0; m < M; ++m) {
+        t.column_norms[m] = r.tape_norms[static_cast<std::size_t>(i * M + m)];
+        t.shrink_factors[m] = r.tape_shrink[static_cast<std::size_t>(i * M + m)];
+      }
+    }
+  }
+  return result;
+}
+
+PrecoderMatrix forward_infer(const UnfoldedNetwork& net, const ChannelMatrix& channel, const SystemConfig& cfg) {
+  return forward(net, channel, cfg).output;
+}
+
+// ---- metrics.cpp ----------------------------------------------------------------
+double l21_norm(const PrecoderMatrix& precoder) {
+  double total = 0.0;
+  for (std::ptrdiff_t m = 0; m < precoder.cols(); ++m) total += precoder.colNorm(m);
+  return total;
+}
+
+double tx_power(const PrecoderMatrix& precoder) { return precoder.squaredNorm(); }
+
+double consumed_power(const PrecoderMatrix& precoder, double alpha) {
+  if (!(alpha > 0.0)) throw std::invalid_argument("consumed_power: alpha must be > 0");
+  return alpha * l21_norm(precoder);
+}
+
+double constraint_residual(const ChannelMatrix& channel, const PrecoderMatrix& precoder, const SystemConfig& cfg) {
+  const RealVector c = cfg.constraint_diag();
+  double s = 0.0;
+  for (std::ptrdiff_t k = 0; k < channel.rows(); ++k)
+    for (std::ptrdiff_t j = 0; j < precoder.rows(); ++j) {
+      Complex acc = 0.0;
+      for (std::ptrdiff_t m = 0; m < channel.cols(); ++m) acc += channel(k, m) * precoder(j, m);
+      if (k == j) acc -= c[k];
+      s += std::norm(acc);
+    }
+  return std::sqrt(s);
+}
+
+int count_active_columns(const PrecoderMatrix& precoder) {
+  int a = 0;
+  for (std::ptrdiff_t m = 0; m < precoder.cols(); ++m)
+    if (precoder.colNorm(m) > 0.0) ++a;
+  return a;
+}
+
+// ---- batch.hpp ------------------------------------------------------------------
+BatchResult forward_batch(const UnfoldedNetwork& net, const std::complex<float>* channels, std::int64_t B,
+                          const SystemConfig& cfg, StartMode start, const std::complex<float>* W0) {
+  net.validate();
+  check_projected(net);
+  cfg.validate();
+  if (cfg.K != net.num_users || cfg.M != net.num_antennas) throw std::invalid_argument("forward: dimension mismatch");
+  if (start == StartMode::Given && !W0) throw std::invalid_argument("forward_batch: W0 required");
+  std::vector<double> lam, eta;
+  for (const LayerParams& l : net.layers) {
+    lam.push_back(l.lambda_i);
+    eta.push_back(l.eta_i);
+  }
+  BatchResult r;
+  const std::size_t n = static_cast<std::size_t>(B) * cfg.K * cfg.M;
+  r.precoders.resize(n);
+  r.diverged_at.resize(static_cast<std::size_t>(B));
+  double stats[3] = {0, 0, 0};
+  const RealVector c = cfg.constraint_diag();
+  const int rc = ufpgd_gpu_unfolded_forward_host(
+      reinterpret_cast<const ufpgd_c64*>(channels), B, cfg.K, cfg.M, lam.data(), eta.data(),
+      static_cast<int>(lam.size()), c.data(), static_cast<int>(start), reinterpret_cast<const ufpgd_c64*>(W0),
+      reinterpret_cast<ufpgd_c64*>(r.precoders.data()), r.diverged_at.data(), stats, cfg.alpha, g_device);
+  if (rc != UFPGD_OK && rc != UFPGD_EDIVERGED) raise(rc);
+  r.consumed_power_sum = stats[0];
+  r.active_sum = stats[1];
+  r.diverged = static_cast<long>(stats[2]);
+  return r;
+}
+
+BatchResult solve_pgd_batch(const std::complex<float>* channels, std::int64_t B, const SystemConfig& cfg,
+                            double lambda, long iterations, int power_steps) {
+  cfg.validate();
+  if (!(lambda >= 0.0)) throw std::invalid_argument("PgdParams: lambda must be >= 0");
+  if (iterations < 0) throw std::invalid_argument("PgdParams: max_iters must be >= 0");
+  BatchResult r;
+  const std::size_t n = static_cast<std::size_t>(B) * cfg.K * cfg.M;
+  r.precoders.resize(n);
+  r.diverged_at.resize(static_cast<std::size_t>(B));
+  r.steps.resize(static_cast<std::size_t>(B));
+  double stats[3] = {0, 0, 0};
+  const RealVector c = cfg.constraint_diag();
+  const int rc = ufpgd_gpu_pgd_fixed_host(reinterpret_cast<const ufpgd_c64*>(channels), B, cfg.K, cfg.M, power_steps,
+                                          lambda, iterations, c.data(), UFPGD_W0_CONJ_H, nullptr,
+                                          reinterpret_cast<ufpgd_c64*>(r.precoders.data()), r.diverged_at.data(),
+                                          r.steps.data(), stats, cfg.alpha, g_device);
+  if (rc != UFPGD_OK && rc != UFPGD_EDIVERGED) raise(rc);
+  r.consumed_power_sum = stats[0];
+  r.active_sum = stats[1];
+  r.diverged = static_cast<long>(stats[2]);
+  return r;
+}
+
+BatchResult forward_batch_multi_gpu(const UnfoldedNetwork& net, const std::complex<float>* channels, std::int64_t B,
+                                    const SystemConfig& cfg, int ngpus) {
+  net.validate();
+  check_projected(net);
+  cfg.validate();
+  if (cfg.K != net.num_users || cfg.M != net.num_antennas) throw std::invalid_argument("forward: dimension mismatch");
+  check(ufpgd_gpu_init(ngpus));
+  std::vector<double> lam, eta;
+  for (const LayerParams& l : net.layers) {
+    lam.push_back(l.lambda_i);
+    eta.push_back(l.eta_i);
+  }
+  BatchResult r;
+  r.precoders.resize(static_cast<std::size_t>(B) * cfg.K * cfg.M);
+  r.diverged_at.resize(static_cast<std::size_t>(B));
+  double stats[3] = {0, 0, 0};
+  const RealVector c = cfg.constraint_diag();
+  const int rc = ufpgd_gpu_unfolded_forward_sharded(
+      reinterpret_cast<const ufpgd_c64*>(channels), B, cfg.K, cfg.M, lam.data(), eta.data(),
+      static_cast<int>(lam.size()), c.data(), UFPGD_W0_CONJ_H, reinterpret_cast<ufpgd_c64*>(r.precoders.data()),
+      r.diverged_at.data(), stats, cfg.alpha);
+  if (rc != UFPGD_OK && rc != UFPGD_EDIVERGED) raise(rc);
+  r.consumed_power_sum = stats[0];
+  r.active_sum = stats[1];
+  r.diverged = static_cast<long>(stats[2]);
+  return r;
+}
+
+}  // namespace ufpgd

@@ -373,6 +373,27 @@ int ufpgd_gpu_power_iteration(const ufpgd_c64* H, int64_t B, int K, int M, const
   return UFPGD_OK;
 }
 
+int ufpgd_gpu_lipschitz_exact(const double* H, int64_t B, int K, int M, double* Lout, int32_t* status,
+                              int device, ufpgd_stream_t stream) {
+  if (B < 0 || K < 1 || M < 1) return fail(UFPGD_EINVAL_SHAPE, "lipschitz_bound: empty channel");
+  if (B > 0 && (!H || !Lout)) return fail(UFPGD_EINVAL_PARAM, "H and Lout are required");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
+  if (B == 0) return UFPGD_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // Start vector Rng(0x1F2E3D4C5B6A7988), normalised, in FP64 (pgd.cpp:131-134).
+  std::vector<double> v0(2 * static_cast<size_t>(M));
+  ufpgd_power_v0_f64(M, v0.data());
+  double2* dv0 = nullptr;
+  UFPGD_CUDA(cudaMallocAsync(&dv0, sizeof(double2) * M, s));
+  UFPGD_CUDA(cudaMemcpyAsync(dv0, v0.data(), sizeof(double2) * M, cudaMemcpyHostToDevice, s));
+  cudaError_t e = launch_lipschitz_exact(reinterpret_cast<const double2*>(H), B, K, M, dv0, Lout, status, s);
+  cudaFreeAsync(dv0, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // v0 host buffer lifetime
+  if (e != cudaSuccess) return cuda_fail(e, "lipschitz_exact kernel");
+  return UFPGD_OK;
+}
+
 int ufpgd_gpu_pgd_fixed(const ufpgd_c64* H, int64_t B, int K, int M, const float* eta_in,
                         int power_steps, double lambda, int64_t iters, const double* c, int w0_mode,
                         const ufpgd_c64* W0, ufpgd_c64* W, int32_t* diverged_at, float* l21,
@@ -643,10 +664,12 @@ int ufpgd_gpu_shutdown(void) {
 
 int ufpgd_gpu_unfolded_forward_sharded(const ufpgd_c64* H, int64_t B, int K, int M,
                                        const double* lambda, const double* eta, int L,
-                                       const double* c, ufpgd_c64* W, int32_t* diverged_at,
-                                       double* stats, double alpha) {
+                                       const double* c, int w0_mode, ufpgd_c64* W,
+                                       int32_t* diverged_at, double* stats, double alpha) {
   int rc;
   if ((rc = check_shape(B, K, M)) || (rc = check_layers(lambda, eta, L)) || (rc = check_c(c, K))) return rc;
+  if (w0_mode != UFPGD_W0_ZERO && w0_mode != UFPGD_W0_CONJ_H)
+    return fail(UFPGD_EINVAL_PARAM, "sharded forward supports W0 = 0 or H^*");
   std::lock_guard<std::mutex> lock(g_nccl_mu);
   const int G = static_cast<int>(g_comms.size());
   if (G == 0) return fail(UFPGD_ENCCL, "call ufpgd_gpu_init first");
@@ -664,7 +687,7 @@ int ufpgd_gpu_unfolded_forward_sharded(const ufpgd_c64* H, int64_t B, int K, int
       cudaMalloc(&dstats[gi], 3 * sizeof(double));
       double part[3] = {0, 0, 0};
       int r = ufpgd_gpu_unfolded_forward_host(H + b0 * K * M, nb, K, M, lambda, eta, L, c,
-                                              UFPGD_W0_ZERO, nullptr, W + b0 * K * M,
+                                              w0_mode, nullptr, W + b0 * K * M,
                                               diverged_at ? diverged_at + b0 : nullptr, part, alpha, gi);
       if (r != UFPGD_OK && r != UFPGD_EDIVERGED) errs[gi] = g_last_error;
       rcs[gi] = r;

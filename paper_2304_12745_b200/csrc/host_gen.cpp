@@ -76,6 +76,19 @@ extern "C" int ufpgd_generate_channels(uint64_t seed_h, uint64_t seed_g, double 
   return UFPGD_OK;
 }
 
+extern "C" int ufpgd_power_v0_f64(int M, double* v0) {
+  if (M < 1 || !v0) return UFPGD_EINVAL_SHAPE;
+  Rng rng(0x1F2E3D4C5B6A7988ULL);  // pgd.cpp:14, :131-134
+  double s = 0.0;
+  for (int i = 0; i < M; ++i) {
+    rng.complex_gaussian(v0[2 * i], v0[2 * i + 1]);
+    s += v0[2 * i] * v0[2 * i] + v0[2 * i + 1] * v0[2 * i + 1];
+  }
+  const double n = std::sqrt(s);
+  for (int i = 0; i < 2 * M; ++i) v0[i] /= n;
+  return UFPGD_OK;
+}
+
 extern "C" int ufpgd_power_v0(int M, ufpgd_c64* v0) {
   if (M < 1 || !v0) return UFPGD_EINVAL_SHAPE;
   Rng rng(0x1F2E3D4C5B6A7988ULL);  // pgd.cpp:14, :131-134

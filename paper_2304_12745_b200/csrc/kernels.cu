@@ -672,6 +672,78 @@ __global__ void __launch_bounds__(128) power_kernel(const __grid_constant__ Powe
   if (lane == 0) p.Lout[rid] = est;
 }
 
+// FP64 power iteration with the reference's converged rule (pgd.cpp:120-169):
+// relative change <= 1e-8 marks convergence, iteration continues to 1e-13 or
+// the 1e4 cap; status = UFPGD_ECONVERGENCE when 1e-8 was never reached. One
+// warp per realization; serves the per-channel lipschitz_bound of the C++ API.
+__global__ void __launch_bounds__(128) lipschitz_exact_kernel(const double2* __restrict__ H, long long B, int K,
+                                                              int M, const double2* __restrict__ v0,
+                                                              double* Lout, int32_t* status) {
+  extern __shared__ double2 lsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long rid = static_cast<long long>(blockIdx.x) * 4 + wid;
+  if (rid >= B) return;  // warp-uniform
+  double2* v = lsm + wid * (2 * M + K);
+  double2* w = v + M;
+  double2* u = w + M;
+  const double2* h = H + rid * static_cast<long long>(K) * M;
+  for (int m = lane; m < M; m += 32) v[m] = v0[m];
+  __syncwarp();
+  double estimate = 0.0, previous = -1.0;
+  bool reached = false, zero = false;
+  for (int iter = 0; iter < 10000; ++iter) {
+    for (int j = 0; j < K; ++j) {  // u = H^* v
+      double re = 0.0, im = 0.0;
+      for (int m = lane; m < M; m += 32) {
+        const double2 a = h[m * K + j], b = v[m];
+        re += a.x * b.x + a.y * b.y;
+        im += a.x * b.y - a.y * b.x;
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        re += __shfl_xor_sync(kFull, re, off);
+        im += __shfl_xor_sync(kFull, im, off);
+      }
+      if (lane == 0) u[j] = make_double2(re, im);
+    }
+    __syncwarp();
+    double dot = 0.0, wn2 = 0.0;
+    for (int m = lane; m < M; m += 32) {  // w = H^T u
+      double re = 0.0, im = 0.0;
+      for (int j = 0; j < K; ++j) {
+        const double2 a = h[m * K + j], b = u[j];
+        re += a.x * b.x - a.y * b.y;
+        im += a.x * b.y + a.y * b.x;
+      }
+      w[m] = make_double2(re, im);
+      dot += v[m].x * re + v[m].y * im;  // Re(conj(v) w)
+      wn2 += re * re + im * im;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      dot += __shfl_xor_sync(kFull, dot, off);
+      wn2 += __shfl_xor_sync(kFull, wn2, off);
+    }
+    estimate = dot;
+    const double wn = sqrt(wn2);
+    if (wn == 0.0) {
+      zero = true;
+      break;
+    }
+    __syncwarp();
+    for (int m = lane; m < M; m += 32) v[m] = make_double2(w[m].x / wn, w[m].y / wn);
+    __syncwarp();
+    if (previous >= 0.0) {
+      const double change = fabs(estimate - previous) / fmax(fabs(estimate), 1e-300);
+      if (change <= 1e-8) reached = true;
+      if (change <= 1e-13) break;
+    }
+    previous = estimate;
+  }
+  if (lane == 0) {
+    Lout[rid] = zero ? 0.0 : estimate;
+    if (status) status[rid] = (zero || reached) ? 0 : UFPGD_ECONVERGENCE;
+  }
+}
+
 // Deterministic sum of per-block partials [n][3] -> stats[3].
 __global__ void __launch_bounds__(256) stats_finalize_kernel(const double* __restrict__ part, long long n,
                                                              double* __restrict__ stats) {
@@ -843,6 +915,16 @@ cudaError_t measure_fp32_peak(double* tflops, double* sm_ghz) {
   if (a) cudaEventDestroy(a);
   if (b) cudaEventDestroy(b);
   return e;
+}
+
+cudaError_t launch_lipschitz_exact(const double2* H, long long B, int K, int M, const double2* v0, double* Lout,
+                                   int32_t* status, cudaStream_t s) {
+  const size_t smem = 4 * (2 * M + K) * sizeof(double2);
+  cudaError_t e = cudaFuncSetAttribute(lipschitz_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  lipschitz_exact_kernel<<<static_cast<unsigned>((B + 3) / 4), 128, smem, s>>>(H, B, K, M, v0, Lout, status);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_stats_finalize(const double* partials, long long n, double* stats, cudaStream_t s) {

@@ -82,6 +82,8 @@ cudaError_t launch_fused(const FusedArgs& a, bool pgd, int K, int M, cudaStream_
 size_t general_smem_bytes(int K, int M);
 cudaError_t launch_general(const GeneralArgs& a, cudaStream_t s);
 cudaError_t launch_power(const PowerArgs& a, cudaStream_t s);
+cudaError_t launch_lipschitz_exact(const double2* H, long long B, int K, int M, const double2* v0,
+                                   double* Lout, int32_t* status, cudaStream_t s);
 cudaError_t measure_fp32_peak(double* tflops, double* sm_ghz);
 cudaError_t launch_stats_finalize(const double* partials, long long n, double* stats,
                                   cudaStream_t s);

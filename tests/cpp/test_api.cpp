@@ -1,0 +1,337 @@
+// C++ API tests on the B200: the reference's own test cases for the hot path
+// (/root/reference/proj/tests/test_pgd.cpp, test_unfolded.cpp) run against the
+// drop-in headers include/ufpgd/*.hpp, which execute on the device. FP64
+// tolerances of the reference become FP32 ones where the math runs in FP32
+// (noted per check); lipschitz_bound runs in FP64 and keeps 1e-9 / 1e-10.
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "ufpgd/batch.hpp"
+#include "ufpgd/errors.hpp"
+#include "ufpgd/metrics.hpp"
+#include "ufpgd/pgd.hpp"
+#include "ufpgd/rng.hpp"
+#include "ufpgd/unfolded.hpp"
+
+using namespace ufpgd;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(cond)                                                      \
+  do {                                                                   \
+    ++g_checks;                                                          \
+    if (!(cond)) {                                                       \
+      ++g_fail;                                                          \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);        \
+    }                                                                    \
+  } while (0)
+#define CHECK_THROWS_AS(expr, T)                                         \
+  do {                                                                   \
+    ++g_checks;                                                          \
+    bool caught = false;                                                 \
+    try {                                                                \
+      (void)(expr);                                                      \
+    } catch (const T&) {                                                 \
+      caught = true;                                                     \
+    } catch (...) {                                                      \
+    }                                                                    \
+    if (!caught) {                                                       \
+      ++g_fail;                                                          \
+      std::printf("FAIL %s:%d: %s does not throw %s\n", __FILE__, __LINE__, #expr, #T); \
+    }                                                                    \
+  } while (0)
+
+static ChannelMatrix channel_for(const SystemConfig& cfg, std::uint64_t seed, std::uint64_t stream) {
+  Rng rng = Rng::stream(seed, stream);
+  return generate_channel(cfg, rng);
+}
+
+static ComplexMatrix random_matrix(int r, int c, Rng& rng) {
+  ComplexMatrix m(r, c);
+  for (int i = 0; i < r; ++i)
+    for (int j = 0; j < c; ++j) m(i, j) = rng.complex_gaussian();
+  return m;
+}
+
+// test_pgd.cpp:247-308 scripted evaluation
+static ComplexMatrix scripted_layer(const ComplexMatrix& w, const ChannelMatrix& h, const std::vector<double>& target,
+                                    double lambda, double eta, bool* hit_zero) {
+  const int rows = static_cast<int>(w.rows()), cols = static_cast<int>(w.cols());
+  ComplexMatrix v(rows, cols);
+  for (int k = 0; k < rows; ++k)
+    for (int m = 0; m < cols; ++m) {
+      Complex smooth(0.0, 0.0);
+      for (int j = 0; j < rows; ++j) {
+        Complex wh(0.0, 0.0);
+        for (int l = 0; l < cols; ++l) wh += w(k, l) * h(j, l);
+        smooth += wh * std::conj(h(j, m));
+      }
+      smooth -= target[static_cast<std::size_t>(k)] * std::conj(h(k, m));
+      v(k, m) = w(k, m) - eta * smooth;
+    }
+  const double t = lambda * eta;
+  ComplexMatrix out(rows, cols);
+  for (int m = 0; m < cols; ++m) {
+    double acc = 0.0;
+    for (int k = 0; k < rows; ++k) acc += std::norm(v(k, m));
+    const double n = std::sqrt(acc);
+    if (n > t) {
+      for (int k = 0; k < rows; ++k) out(k, m) = (1.0 - t / n) * v(k, m);
+    } else if (hit_zero) {
+      *hit_zero = true;
+    }
+  }
+  return out;
+}
+
+static void fixture(SystemConfig& cfg, ChannelMatrix& h) {
+  cfg.K = 2;
+  cfg.M = 4;
+  cfg.sigma_nu = 0.8;
+  cfg.gamma = RealVector{2.0, 0.5};
+  cfg.alpha = 1.0;
+  cfg.validate();
+  h = ChannelMatrix(2, 4);
+  h(0, 0) = {0.6, 0.3};
+  h(0, 1) = {-0.2, 0.9};
+  h(0, 2) = {0.05, -0.02};
+  h(0, 3) = {1.1, 0.0};
+  h(1, 0) = {-0.7, 0.1};
+  h(1, 1) = {0.4, -0.4};
+  h(1, 2) = {0.03, 0.01};
+  h(1, 3) = {-0.5, 0.6};
+}
+
+int main() {
+  // --- test_pgd.cpp ------------------------------------------------------------
+  {  // params validation
+    PgdParams p;
+    p.lambda = 0.1;
+    p.eta = 0.01;
+    p.max_iters = 10;
+    p.residual_tol = 1e-8;
+    p.validate();
+    PgdParams bad = p;
+    bad.lambda = -1e-9;
+    CHECK_THROWS_AS(bad.validate(), std::invalid_argument);
+    bad = p;
+    bad.eta = 0.0;
+    CHECK_THROWS_AS(bad.validate(), std::invalid_argument);
+  }
+  {  // grad_f at zero is the negated data term (1e-14 -> FP32 1e-6 relative)
+    SystemConfig cfg = SystemConfig::uniform(3, 6, 10.0, 0.7);
+    ChannelMatrix h = channel_for(cfg, 12, 0);
+    ComplexMatrix g = grad_f(PrecoderMatrix::Zero(3, 6), h, cfg);
+    const RealVector t = cfg.constraint_diag();
+    double err = 0.0;
+    for (int k = 0; k < 3; ++k)
+      for (int m = 0; m < 6; ++m) err = std::max(err, std::abs(g(k, m) + t[k] * std::conj(h(k, m))));
+    CHECK(err < 1e-5);
+  }
+  {  // prox closed forms, strict '>' tie
+    ComplexMatrix v(3, 4);
+    v(0, 0) = {1, 1};
+    v(1, 0) = {1, -1};
+    v(0, 1) = {0.3, 0};
+    v(0, 2) = {0.5, 0};
+    v(0, 3) = {0, 2};
+    v(1, 3) = {-0.4, 0.1};
+    v(2, 3) = {0.2, -0.9};
+    PrecoderMatrix out = prox_l21(v, 0.5);
+    double e0 = 0.0;
+    for (int k = 0; k < 3; ++k) e0 = std::max(e0, std::abs(out(k, 0) - 0.75 * v(k, 0)));
+    CHECK(e0 < 1e-6);
+    CHECK(out.colNorm(1) == 0.0);
+    CHECK(out.colNorm(2) == 0.0);  // exactly at the threshold -> zero
+    CHECK((prox_l21(v, 0.0) - v).norm() < 1e-6);
+    CHECK_THROWS_AS(prox_l21(v, -0.1), std::invalid_argument);
+  }
+  {  // scripted one-step fixture
+    SystemConfig cfg;
+    ChannelMatrix h;
+    fixture(cfg, h);
+    std::vector<double> target = {0.8 * std::sqrt(2.0), 0.8 * std::sqrt(0.5)};
+    ComplexMatrix scripted = scripted_layer(h.conjugate(), h, target, 1.5, 0.05, nullptr);
+    PrecoderMatrix stepped = pgd_step(h.conjugate(), h, cfg, 1.5, 0.05);
+    CHECK((stepped - scripted).norm() < 1e-6 * std::max(1.0, scripted.norm()));
+    CHECK(stepped.colNorm(2) == 0.0);
+  }
+  {  // mp bound
+    CHECK(std::abs(mp_bound(8, 64) - 117.25483399593904) < 1e-12 * 117.25);
+    CHECK_THROWS_AS(mp_bound(0, 64), std::invalid_argument);
+  }
+  {  // lipschitz bound: identity channel, FP64 on the device
+    LipschitzBound b = lipschitz_bound(ChannelMatrix::Identity(5, 5));
+    CHECK(std::abs(b.exact - 1.0) < 1e-10);
+    CHECK(std::abs(b.mp - 20.0) < 1e-12);
+  }
+  {  // MP dominance >= 950 / 1000 (test_pgd.cpp:341-354), FP64 power iteration on device
+    SystemConfig cfg = SystemConfig::uniform(8, 64, 10.0);
+    const double mp = mp_bound(8, 64);
+    int covered = 0;
+    for (int d = 0; d < 200; ++d) covered += lipschitz_bound(channel_for(cfg, 23, d)).exact <= mp;
+    CHECK(covered >= 190);
+  }
+  {  // divergence index >= 1 (test_pgd.cpp:454-470)
+    SystemConfig cfg = SystemConfig::uniform(4, 16, 10.0);
+    ChannelMatrix h = channel_for(cfg, 31, 0);
+    PgdParams p;
+    p.lambda = 0.0;
+    p.eta = 1e6;
+    p.max_iters = 200;
+    long reported = -1;
+    try {
+      solve_pgd(h, cfg, p);
+    } catch (const DivergenceError& e) {
+      reported = e.index;
+    }
+    CHECK(reported >= 1);
+  }
+  {  // iterate-change stop fires (test_pgd.cpp:384-397)
+    SystemConfig cfg = SystemConfig::uniform(4, 16, 10.0);
+    ChannelMatrix h = channel_for(cfg, 27, 0);
+    PgdParams p;
+    p.lambda = 0.0;
+    p.eta = 1.0 / lipschitz_bound(h).exact;
+    p.max_iters = 50000;
+    p.residual_tol = 1e-3;
+    PgdResult r = solve_pgd(h, cfg, p);
+    CHECK(r.iterations > 0 && r.iterations < 5000);
+  }
+  {  // zero iterations returns H^*
+    SystemConfig cfg = SystemConfig::uniform(3, 8, 10.0);
+    ChannelMatrix h = channel_for(cfg, 32, 0);
+    PgdParams p;
+    p.eta = 1.0 / mp_bound(3, 8);
+    p.max_iters = 0;
+    PgdResult r = solve_pgd(h, cfg, p);
+    CHECK(r.iterations == 0);
+    CHECK((r.precoder - h.conjugate()).norm() == 0.0);
+  }
+  // --- test_unfolded.cpp -----------------------------------------------------------
+  {  // forward with constant params reproduces solve_pgd (1e-12 -> FP32 1e-5)
+    SystemConfig cfg = SystemConfig::uniform(4, 16, 10.0);
+    UnfoldedNetwork net = UnfoldedNetwork::pgd_init(4, 16, 20, 1.0 / 15.0);
+    PgdParams p;
+    p.lambda = 1.0 / 15.0;
+    p.eta = 1.0 / net.mp_bound;
+    p.max_iters = 20;
+    for (int d = 0; d < 5; ++d) {
+      ChannelMatrix h = channel_for(cfg, 41, d);
+      PrecoderMatrix a = forward(net, h, cfg).output;
+      PrecoderMatrix b = solve_pgd(h, cfg, p).precoder;
+      CHECK((a - b).norm() < 1e-5 * std::max(1.0, b.norm()));
+      CHECK((forward_infer(net, h, cfg) - a).norm() == 0.0);
+    }
+  }
+  {  // scripted 3-layer fixture + iterates
+    SystemConfig cfg;
+    ChannelMatrix h;
+    fixture(cfg, h);
+    UnfoldedNetwork net;
+    net.num_users = 2;
+    net.num_antennas = 4;
+    net.mp_bound = mp_bound(2, 4);
+    net.layers = {{0.9, 0.05}, {1.5, 0.07}, {0.3, 0.08}};
+    net.validate();
+    std::vector<double> target = {0.8 * std::sqrt(2.0), 0.8 * std::sqrt(0.5)};
+    ComplexMatrix s = h.conjugate();
+    bool hit = false;
+    for (const LayerParams& l : net.layers) s = scripted_layer(s, h, target, l.lambda_i, l.eta_i, &hit);
+    CHECK(hit);
+    // The box check is off for this fixture in the reference too? No: forward
+    // checks the box; the fixture's steps are inside [1/(2L), 1/L] for L = mp(2, 4).
+    ForwardOptions opt;
+    opt.with_iterates = true;
+    ForwardResult r = forward(net, h, cfg, std::nullopt, opt);
+    CHECK((r.output - s).norm() < 1e-6 * std::max(1.0, s.norm()));
+    CHECK(r.iterates.size() == 4);
+    CHECK((r.iterates.back() - r.output).norm() == 0.0);
+  }
+  {  // projection clamps; unprojected rejected
+    const double mp = mp_bound(8, 64);
+    UnfoldedNetwork net;
+    net.num_users = 8;
+    net.num_antennas = 64;
+    net.mp_bound = mp;
+    net.layers = {{-0.1, 1.0}, {0.5, 0.006}, {0.02, 1e-9}};
+    UnfoldedNetwork p = project_params(net);
+    CHECK(p.layers[0].lambda_i == 0.0 && p.layers[0].eta_i == 1.0 / mp);
+    CHECK(p.layers[2].eta_i == 1.0 / (2.0 * mp));
+    SystemConfig cfg = SystemConfig::uniform(3, 8, 10.0);
+    UnfoldedNetwork bad = UnfoldedNetwork::pgd_init(3, 8, 2, 0.1);
+    bad.layers[1].eta_i = 1.0;
+    CHECK_THROWS_AS(forward(bad, channel_for(cfg, 43, 0), cfg), std::invalid_argument);
+  }
+  {  // pathological channel diverges at layer 0
+    SystemConfig cfg = SystemConfig::uniform(2, 4, 10.0);
+    ChannelMatrix h = ChannelMatrix::Constant(2, 4, Complex(1e200, 0.0));
+    UnfoldedNetwork net = UnfoldedNetwork::pgd_init(2, 4, 3, 0.1);
+    long reported = -1;
+    try {
+      forward(net, h, cfg);
+    } catch (const DivergenceError& e) {
+      reported = e.index;
+    }
+    CHECK(reported == 0);
+  }
+  {  // tapes consistent with iterates
+    SystemConfig cfg = SystemConfig::uniform(4, 12, 10.0);
+    ChannelMatrix h = channel_for(cfg, 44, 0);
+    UnfoldedNetwork net = UnfoldedNetwork::pgd_init(4, 12, 6, 0.4);
+    ForwardOptions opt;
+    opt.with_tape = true;
+    opt.with_iterates = true;
+    ForwardResult a = forward(net, h, cfg, std::nullopt, opt);
+    ForwardResult b = forward(net, h, cfg, std::nullopt, opt);
+    CHECK(a.tape.layers.size() == 6);
+    for (std::size_t i = 0; i < a.tape.layers.size(); ++i) {
+      CHECK((a.tape.layers[i].step_image - b.tape.layers[i].step_image).norm() == 0.0);
+      CHECK((a.tape.layers[i].input - a.iterates[i]).norm() == 0.0);
+      for (std::ptrdiff_t m = 0; m < 12; ++m)
+        CHECK(std::abs(a.tape.layers[i].column_norms[m] - a.tape.layers[i].step_image.colNorm(m)) <=
+              1e-5 * a.tape.layers[i].column_norms[m]);
+    }
+  }
+  // --- batched entry points --------------------------------------------------------
+  {
+    SystemConfig cfg = SystemConfig::uniform(8, 64, 10.0);
+    UnfoldedNetwork net = UnfoldedNetwork::pgd_init(8, 64, 20, 1.0 / 15.0);
+    const int B = 300;
+    std::vector<std::complex<float>> H(static_cast<std::size_t>(B) * 8 * 64);
+    std::vector<ChannelMatrix> hs;
+    for (int b = 0; b < B; ++b) {
+      hs.push_back(channel_for(cfg, 41, b));
+      for (int m = 0; m < 64; ++m)
+        for (int k = 0; k < 8; ++k)
+          H[static_cast<std::size_t>(b) * 512 + m * 8 + k] = std::complex<float>(hs.back()(k, m));
+    }
+    BatchResult r = forward_batch(net, H.data(), B, cfg);
+    CHECK(r.diverged == 0);
+    double maxrel = 0.0, cp = 0.0;
+    for (int b = 0; b < B; b += 37) {
+      ChannelMatrix hf(8, 64);
+      for (int m = 0; m < 64; ++m)
+        for (int k = 0; k < 8; ++k) hf(k, m) = Complex(H[static_cast<std::size_t>(b) * 512 + m * 8 + k]);
+      PrecoderMatrix one = forward_infer(net, hf, cfg);
+      PrecoderMatrix bw(8, 64);
+      for (int m = 0; m < 64; ++m)
+        for (int k = 0; k < 8; ++k) bw(k, m) = Complex(r.precoders[static_cast<std::size_t>(b) * 512 + m * 8 + k]);
+      maxrel = std::max(maxrel, (one - bw).norm() / one.norm());
+    }
+    for (int b = 0; b < B; ++b) {
+      PrecoderMatrix bw(8, 64);
+      for (int m = 0; m < 64; ++m)
+        for (int k = 0; k < 8; ++k) bw(k, m) = Complex(r.precoders[static_cast<std::size_t>(b) * 512 + m * 8 + k]);
+      cp += consumed_power(bw, cfg.alpha);
+    }
+    CHECK(maxrel < 1e-5);  // fused team kernel vs general kernel, both FP32
+    CHECK(std::abs(cp - r.consumed_power_sum) < 1e-5 * cp);
+    BatchResult p = solve_pgd_batch(H.data(), 64, cfg, 0.05, 500);
+    CHECK(p.diverged == 0 && p.steps.size() == 64 && p.steps[0] > 0.0f);
+  }
+  std::printf("%d checks, %d failures\n", g_checks, g_fail);
+  return g_fail == 0 ? 0 : 1;
+}
