@@ -197,8 +197,10 @@ def run_ours(args, world, rank, local):
     w = U.CONFIGS[args.config]
     if w.kind != "unfolded":
         raise SystemExit("bench.py times the unfolded configs; see tools/quick_time.py for PGD")
-    B = w.B
-    H_host = torch.from_numpy(U.make_inputs(w, rank * B, B)).pin_memory()
+    from paper_2304_12745_b200 import sharding
+
+    first, B = sharding.weak_shard(rank, w.B)
+    H_host = torch.from_numpy(U.make_inputs(w, first, B)).pin_memory()
     lam, eta = w.layer_params()
     Hd = H_host.to(dev, non_blocking=False)
     Wd = torch.empty_like(Hd)
@@ -206,8 +208,7 @@ def run_ours(args, world, rank, local):
 
     def step():
         out = U.unfolded_forward(Hd, lam, eta, w.c, w0_mode=w.w0_mode, out=Wd)
-        if world > 1:
-            dist.all_reduce(out["stats"])  # the one collective: 3 doubles
+        sharding.reduce_stats(out["stats"])  # the one collective: 3 doubles (N > 1)
         return out
 
     for _ in range(max(3, args.warmup)):
@@ -229,8 +230,7 @@ def run_ours(args, world, rank, local):
         ev[k][0].record(stream)
         out = U.unfolded_forward(Hd, lam, eta, w.c, w0_mode=w.w0_mode, out=Wd)
         ev[k][1].record(stream)
-        if world > 1:
-            dist.all_reduce(out["stats"])
+        sharding.reduce_stats(out["stats"])
     t_end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -260,8 +260,7 @@ def run_ours(args, world, rank, local):
     for _ in range(e2e_steps):
         r = U.unfolded_forward_host(Hn, lam, eta, w.c, w0_mode=w.w0_mode, out=Wn, device=local)
         if world > 1:
-            st = torch.from_numpy(r["stats"]).to(dev)
-            dist.all_reduce(st)
+            sharding.reduce_stats(torch.from_numpy(r["stats"]).to(dev))
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if world > 1:
@@ -310,8 +309,7 @@ def run_ours(args, world, rank, local):
                     "path": "ufpgd_gpu_unfolded_forward_host (pinned host H in, W + diverged + stats out)"},
             "gpu_launches": 2 * args.steps,
             "clocks": clocks.report(),
-            "stats": {"mean_consumed_power": float(stats[0]) / (world * B), "mean_active": float(stats[1]) / (world * B),
-                      "diverged": int(stats[2])},
+            "stats": sharding.summarize(stats, world * B),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

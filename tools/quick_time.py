@@ -4,8 +4,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2304_12745_b200 as U
 
-def t_uf(cfg, reps=10):
+def t_uf(cfg, reps=10, n=None):
     w = U.CONFIGS[cfg]
+    if n is not None:
+        import dataclasses
+        w = dataclasses.replace(w, B=n)
     t0 = time.time(); H = U.make_inputs(w); tg = time.time() - t0
     lam, eta = w.layer_params()
     Hd = torch.from_numpy(H).cuda(); W = torch.empty_like(Hd)
@@ -32,4 +35,5 @@ def t_pgd(n=4096):
 if __name__ == "__main__":
     for c in [int(x) for x in (sys.argv[1:] or ["1", "2", "4"])]:
         if c == 3: t_pgd()
+        elif c == 5: t_uf(5, reps=2, n=int(os.environ.get("CFG5_B", "65536")))
         else: t_uf(c, reps=10 if c != 4 else 2)
