@@ -102,13 +102,53 @@ def test_config3_pgd_with_power_iteration_subset():
 
 
 @pytest.mark.parametrize("cfg,n", [(4, 64), (5, 256)])
-def test_large_shapes_general_path_parity(cfg, n):
+def test_large_shapes_tile_kernel_parity(cfg, n):
     w = U.CONFIGS[cfg]
     H = U.make_inputs(w, 0, n)
     lam, eta = w.layer_params()
     g = run_uf(w, H, lam, eta)
     ora = O.forward_batch_f32(H, w.c, lam, eta, w0_mode=w.w0_mode)
-    assert_parity(report(H, g["W"], ora, w.c, LAM_OBJ_UF))
+    rep = report(H, g["W"], ora, w.c, LAM_OBJ_UF)
+    print(f"cfg{cfg}: rel max {rep['rel_max']:.2e} obj {rep['obj_max']:.2e}")
+    assert_parity(rep)
+    assert np.array_equal(g["active"], ora["active"])
+    assert np.allclose(g["l21"], ora["l21"], rtol=1e-5)
+
+
+@pytest.mark.parametrize("K,M", [(16, 128), (32, 256)])
+@pytest.mark.parametrize("w0_mode", [U.W0_CONJ_H, U.W0_GIVEN])
+def test_tile_kernel_start_modes_and_sparsity(K, M, w0_mode):
+    L, B = 12, 24
+    H = U.generate_channels(99, 7, 30.0, 0, B, K, M)
+    lam = np.full(L, 6.0)  # large enough to zero antennas (prox zero branch)
+    eta = np.full(L, 1.0 / U.mp_bound(K, M))
+    c = np.full(K, math.sqrt(10.0))
+    W0 = None
+    if w0_mode == U.W0_GIVEN:
+        rng = np.random.default_rng(5)
+        W0 = ((rng.standard_normal(H.shape) + 1j * rng.standard_normal(H.shape)) * 0.05).astype(np.complex64)
+    out = U.unfolded_forward(dev(H), lam, eta, c, w0_mode=w0_mode, W0=None if W0 is None else dev(W0),
+                             want_per_realization=True)
+    torch.cuda.synchronize()
+    ora = O.forward_batch_f32(H, c, lam, eta, w0_mode=w0_mode, W0=W0)
+    rep = report(H, out["W"].cpu().numpy(), ora, c, 6.0)
+    clean = ora["tie_margin"] >= 1e-4
+    assert clean.sum() >= B // 2
+    assert rep["rel"][clean].max() <= 1e-4
+    assert rep["support_mismatch"] == 0
+
+
+@pytest.mark.parametrize("K,M", [(16, 128), (32, 256)])
+def test_tile_kernel_pgd_with_power_iteration(K, M):
+    B, iters, lam = 16, 300, 0.05
+    H = U.generate_channels(123, 0, 0.0, 0, B, K, M)
+    c = np.full(K, math.sqrt(10.0))
+    out = U.pgd_fixed(dev(H), lam, iters, c, power_steps=30)
+    torch.cuda.synchronize()
+    Lo, _ = O.power_iteration_batch_f32(H, 30)
+    assert np.max(np.abs(out["eta"].cpu().numpy() * Lo - 1.0)) <= 1e-5
+    ora = O.pgd_batch_f32(H, c, lam, 1.0 / Lo, iters, w0_mode=U.W0_CONJ_H)
+    assert_parity(report(H, out["W"].cpu().numpy(), ora, c, lam))
 
 
 def test_scripted_fixture_through_general_kernel():
