@@ -202,13 +202,17 @@ bool load_nccl() {
 struct HostWorkspace {
   std::mutex mu;
   bool init = false;
-  static constexpr int NS = 3;
+  static constexpr int NS = 4;
   cudaStream_t st[NS] = {};
   void* buf[NS][5] = {};
   size_t cap[NS][5] = {};
   double* partials = nullptr;
   size_t partials_cap = 0;
   double* dstats = nullptr;
+  // pinned staging of the small per-realization outputs: a D2H copy into
+  // pageable memory would block the host thread and serialise the pipeline
+  void* pinned = nullptr;
+  size_t pinned_cap = 0;
 };
 HostWorkspace g_ws[64];
 
@@ -249,7 +253,19 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
     e = ensure(pp, ws.partials_cap, sizeof(double) * 3 * std::max<long long>(1, parts_per_chunk_max * nchunks));
     ws.partials = static_cast<double*>(pp);
   }
+  const size_t small_need = (diverged_at ? sizeof(int32_t) * B : 0) + (eta_out ? sizeof(float) * B : 0) + 64;
+  if (e == cudaSuccess && small_need > ws.pinned_cap) {
+    if (ws.pinned) cudaFreeHost(ws.pinned);
+    ws.pinned = nullptr;
+    ws.pinned_cap = 0;
+    e = cudaHostAlloc(&ws.pinned, small_need, cudaHostAllocDefault);
+    if (e == cudaSuccess) ws.pinned_cap = small_need;
+  }
   if (e != cudaSuccess) return cuda_fail(e, "host pipeline allocation");
+  int32_t* div_stage = diverged_at ? static_cast<int32_t*>(ws.pinned) : nullptr;
+  float* eta_stage = eta_out ? reinterpret_cast<float*>(static_cast<char*>(ws.pinned) +
+                                                        (diverged_at ? sizeof(int32_t) * B : 0))
+                             : nullptr;
   int rc = UFPGD_OK;
   std::vector<long long> part_off(nchunks + 1, 0);
   for (int64_t ci = 0; ci < nchunks && rc == UFPGD_OK; ++ci) {
@@ -273,9 +289,9 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
     part_off[ci + 1] = part_off[ci] + np;
     e = cudaMemcpyAsync(W + b0 * K * M, dw, per * nb, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && diverged_at)
-      e = cudaMemcpyAsync(diverged_at + b0, ddiv, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, s);
+      e = cudaMemcpyAsync(div_stage + b0, ddiv, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && eta_out)
-      e = cudaMemcpyAsync(eta_out + b0, deta, sizeof(float) * nb, cudaMemcpyDeviceToHost, s);
+      e = cudaMemcpyAsync(eta_stage + b0, deta, sizeof(float) * nb, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) rc = cuda_fail(e, "D2H");
   }
   double host_stats[3] = {0.0, 0.0, 0.0};
@@ -295,6 +311,8 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
   }
   for (int i = 0; i < NS; ++i) cudaStreamSynchronize(ws.st[i]);
   if (rc != UFPGD_OK) return rc;
+  if (diverged_at) std::memcpy(diverged_at, div_stage, sizeof(int32_t) * B);
+  if (eta_out) std::memcpy(eta_out, eta_stage, sizeof(float) * B);
   if (stats) std::memcpy(stats, host_stats, sizeof(host_stats));
   if (host_stats[2] > 0.0) return fail(UFPGD_EDIVERGED, "non-finite iterate in at least one realization");
   return UFPGD_OK;
@@ -542,8 +560,8 @@ int ufpgd_gpu_unfolded_forward_host(const ufpgd_c64* H, int64_t B, int K, int M,
   DeviceGuard g(device);
   if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
   const bool fused = fused_supported(K, M) && L >= 1;
-  // ~32 MiB of H per chunk keeps three chunks in flight well inside HBM.
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, (32ll << 20) / (8ll * K * M)));
+  // 16 MiB of H per chunk: short pipeline fill, chunks still fill the GPU.
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, (16ll << 20) / (8ll * K * M)));
   const long long ppc = partial_count(chunk, K, M, fused);
   return host_pipeline(
       device, H, B, K, M, w0_mode == UFPGD_W0_GIVEN ? W0 : nullptr, W, diverged_at, nullptr, ppc, chunk, stats,
