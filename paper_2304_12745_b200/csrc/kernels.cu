@@ -77,8 +77,17 @@ struct Team {
   static constexpr int KA = K / TK;     // users per thread
   static constexpr int P = KA / 2;      // user pairs per thread (FFMA2 lanes)
   static constexpr int MB = M / TM;     // antennas per thread
-  static constexpr int HS = 2 * K + 4;  // padded H row stride in floats
+  static constexpr int HS = 2 * K;      // H row stride in floats (XOR-swizzled units, no padding)
+  static constexpr int U = K / 2;       // 16-byte units per H row
   static constexpr int SMEM_PER_WARP = R * M * HS * 4;
+  // Unit swizzle of row m: with U >= 4 units per row, rows m and m + 2 of a
+  // quarter-warp LDS.128 phase would hit the same banks; XOR-ing the unit
+  // index with (m >> 1) mod U separates them. U <= 2 is conflict-free as is.
+  static __device__ __forceinline__ int swz(int m) { return U >= 4 ? (m >> 1) & (U - 1) : 0; }
+  // Address of complex H(c, m) (user c, antenna m) in the tile.
+  static __device__ __forceinline__ const float* hat(const float* hs, int m, int c) {
+    return hs + m * HS + 4 * ((c >> 1) ^ swz(m)) + 2 * (c & 1);
+  }
   static_assert(32 % T == 0, "a team must divide the warp");
   static_assert(K % TK == 0 && M % TM == 0, "team must tile (K, M)");
   static_assert(KA % 2 == 0 && K % 2 == 0, "users are processed in FFMA2 pairs");
@@ -100,9 +109,10 @@ __device__ __forceinline__ float2 zero2() { return make_float2(0.f, 0.f); }
 template <class S>
 __device__ __forceinline__ void load_col(const float* hs, int m, float2 (&h)[S::K]) {
   const float4* hp = reinterpret_cast<const float4*>(hs + m * S::HS);
+  const int f = S::swz(m);
 #pragma unroll
   for (int q = 0; q < S::K / 2; ++q) {
-    const float4 t = hp[q];
+    const float4 t = hp[q ^ f];
     h[2 * q] = make_float2(t.x, t.y);
     h[2 * q + 1] = make_float2(t.z, t.w);
   }
@@ -265,9 +275,11 @@ __device__ float team_power(const float* hs, const float2* v0, int steps, int a,
     for (int jj = 0; jj < S::KA; ++jj) u[jj] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int i = 0; i < S::MB; ++i) {
-      const float2* hrow = reinterpret_cast<const float2*>(hs + (i * S::TM + b) * S::HS) + a * S::KA;
 #pragma unroll
-      for (int jj = 0; jj < S::KA; ++jj) cmac(u[jj], v[i], make_float2(hrow[jj].x, -hrow[jj].y));
+      for (int jj = 0; jj < S::KA; ++jj) {
+        const float2 hv = *reinterpret_cast<const float2*>(S::hat(hs, i * S::TM + b, a * S::KA + jj));
+        cmac(u[jj], v[i], make_float2(hv.x, -hv.y));
+      }
     }
 #pragma unroll
     for (int jj = 0; jj < S::KA; ++jj)
@@ -280,10 +292,10 @@ __device__ float team_power(const float* hs, const float2* v0, int steps, int a,
     float2 wv[S::MB];
 #pragma unroll
     for (int i = 0; i < S::MB; ++i) {
-      const float2* hrow = reinterpret_cast<const float2*>(hs + (i * S::TM + b) * S::HS) + a * S::KA;
       float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int jj = 0; jj < S::KA; ++jj) cmac(acc, hrow[jj], u[jj]);
+      for (int jj = 0; jj < S::KA; ++jj)
+        cmac(acc, *reinterpret_cast<const float2*>(S::hat(hs, i * S::TM + b, a * S::KA + jj)), u[jj]);
 #pragma unroll
       for (int off = S::TM; off < S::T; off <<= 1) {
         acc.x += __shfl_xor_sync(kFull, acc.x, off);
@@ -334,7 +346,7 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
 #pragma unroll
     for (int q = 0; q < NV / S::T; ++q) {
       const int e = 2 * (tl + q * S::T);
-      *reinterpret_cast<float4*>(hs + (e / S::K) * S::HS + 2 * (e % S::K)) = buf[q];
+      *reinterpret_cast<float4*>(const_cast<float*>(S::hat(hs, e / S::K, e % S::K))) = buf[q];
     }
     __syncwarp();
   }
@@ -369,10 +381,9 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
     if (p.w0_mode == UFPGD_W0_CONJ_H) {
 #pragma unroll
       for (int i = 0; i < S::MB; ++i) {
-        const float4* hrow = reinterpret_cast<const float4*>(hs + (i * S::TM + b) * S::HS + 2 * a * S::KA);
 #pragma unroll
         for (int q = 0; q < S::P; ++q) {
-          const float4 t = hrow[q];
+          const float4 t = *reinterpret_cast<const float4*>(S::hat(hs, i * S::TM + b, a * S::KA + 2 * q));
           wr[i][q] = make_float2(t.x, t.z);
           wi[i][q] = make_float2(-t.y, -t.w);
         }
