@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <vector>
 
+#include "ufpgd/metrics.hpp"
 #include "ufpgd/pgd.hpp"
 #include "ufpgd/system_config.hpp"
 #include "ufpgd/unfolded.hpp"
@@ -41,5 +42,17 @@ BatchResult solve_pgd_batch(const std::complex<float>* channels, std::int64_t B,
 // all-reduce of the statistics).
 BatchResult forward_batch_multi_gpu(const UnfoldedNetwork& net, const std::complex<float>* channels,
                                     std::int64_t B, const SystemConfig& cfg, int ngpus);
+
+// evaluate (training.cpp:310-421) without per-layer curves: forward on every
+// channel, device metrics, means and standard errors at the final layer.
+struct EvaluationSummary {
+  MetricsReport mean;
+  MetricsReport std_error;
+  std::size_t num_channels = 0;
+  long singular = 0;  // channels whose ZF reference is singular (the reference throws)
+};
+
+EvaluationSummary evaluate_batch(const UnfoldedNetwork& net, const std::complex<float>* channels, std::int64_t B,
+                                 const SystemConfig& cfg);
 
 }  // namespace ufpgd

@@ -184,6 +184,19 @@ int ufpgd_gpu_unfolded_forward_sharded(const ufpgd_c64* H, int64_t B, int K, int
                                        int32_t* diverged_at, double* stats, double alpha);
 
 /*
+ * Batched metrics — compute_metrics (metrics.cpp:79-91)
+ * with the ZF reference of zf_precoder (zf.cpp:9-30) for B (H, W) pairs,
+ * the body of evaluate's parallel_for (training.cpp:324-357). FP64 on the
+ * device. out[b][6 + K] = {tx_power, cons_power, sum_rate, pcg, residual,
+ * zf_ok, sinr[0..K-1]}; zf_ok = 0 where zf_precoder would throw
+ * SingularChannelError (pcg = NaN there). Wzf (nullable) receives the ZF
+ * precoders. K <= 32. Synchronous on `stream`.
+ */
+int ufpgd_gpu_metrics(const ufpgd_c64* H, const ufpgd_c64* W, int64_t B, int K, int M, const double* c,
+                      double sigma_nu, double alpha, double* out, ufpgd_c64* Wzf, int device,
+                      ufpgd_stream_t stream);
+
+/*
  * Measurement helper (not a reference interface): FP32 FMA throughput of the
  * device with the kernel's own FFMA2 instruction form, and the SM clock read
  * in-kernel during the probe. The roofline denominator of bench.py.

@@ -70,6 +70,8 @@ def lib():
             "ora_power_iteration_batch_f32": (i, [P, i64, i, i, i, P, P, i]),
             "ora_lagrangian_batch_f32": (i, [P, P, i64, P, i, i, d, P, i]),
             "ora_lagrangian_batch_f64": (i, [P, P, i64, P, i, i, d, P, i]),
+            "ora_metrics": (i, [P, P, P, d, d, i, i, P]),
+            "ora_metrics_batch_f32": (i, [P, P, i64, P, d, d, i, i, P, i]),
         }
         for name, (res, args) in sigs.items():
             fn = getattr(L, name)
@@ -390,6 +392,48 @@ def zf_precoder(H, cfg) -> np.ndarray:
     if rc == ORA_ESINGULAR:
         raise SingularChannelError("zf_precoder: channel Gram matrix is singular")
     return from_storage(out, K, M)
+
+
+@dataclass
+class MetricsReport:  # metrics.hpp:44-51
+    tx_power: float
+    cons_power: float
+    sinr: np.ndarray
+    sum_rate: float
+    pcg: float
+    residual: float
+
+
+def compute_metrics(H, W, cfg) -> MetricsReport:
+    """metrics.cpp:79-91 with the ZF reference computed here (zf.cpp:9-30)."""
+    K, M = H.shape
+    out = np.empty(6 + K)
+    lib().ora_metrics(_p(to_storage(H)), _p(to_storage(W)), _p(cfg.constraint_diag()), cfg.sigma_nu, cfg.alpha,
+                      K, M, _p(out))
+    if out[5] == 0.0:
+        raise SingularChannelError("zf_precoder: channel Gram matrix is singular")
+    return MetricsReport(out[0], out[1], out[6:].copy(), out[2], out[3], out[4])
+
+
+def sinr_per_user(H, W, cfg) -> np.ndarray:
+    return compute_metrics(H, W, cfg).sinr
+
+
+def sum_rate(sinr) -> float:
+    return float(sum(math.log2(1.0 + s) for s in sinr))
+
+
+def metrics_batch_f32(H, W, c, sigma_nu=1.0, alpha=1.0, threads=0):
+    """[B, 6 + K]: tx, cons, sum_rate, pcg, residual, zf_ok, sinr[K]."""
+    H = np.ascontiguousarray(H, dtype=np.complex64)
+    W = np.ascontiguousarray(W, dtype=np.complex64)
+    B, M, K = H.shape
+    out = np.empty((B, 6 + K))
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    rc = lib().ora_metrics_batch_f32(_p(H), _p(W), B, _p(c), float(sigma_nu), float(alpha), K, M, _p(out), threads)
+    if rc != ORA_OK:
+        raise ValueError("metrics batch failed")
+    return out
 
 
 def pcg(H, W, cfg) -> float:

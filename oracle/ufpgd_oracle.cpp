@@ -538,6 +538,64 @@ double ora_lagrangian(const double* W, const double* H, const double* c, int K, 
   return lambda * l21(as_c(W), K, M) + r * r;
 }
 
+// metrics.cpp:29-91 + zf.cpp:9-30 for one realization. out = [tx_power,
+// cons_power, sum_rate, pcg, residual, zf_ok, sinr[K]]; zf_ok = 0 when
+// zf_precoder throws SingularChannelError (then pcg = NaN).
+int ora_metrics(const double* Hp, const double* Wp, const double* c, double sigma_nu, double alpha, int K,
+                int M, double* out) {
+  const cd* H = as_c(Hp);
+  const cd* W = as_c(Wp);
+  double tx = 0.0;
+  for (int i = 0; i < K * M; ++i) tx += std::norm(W[i]);
+  const double l21w = l21(W, K, M);
+  // effective channel H W^T (K x K): E(k, j) = sum_m H(k, m) W(j, m)
+  std::vector<cd> E(static_cast<std::size_t>(K) * K, 0.0);
+  for (int m = 0; m < M; ++m)
+    for (int j = 0; j < K; ++j)
+      for (int k = 0; k < K; ++k) E[j * K + k] += H[static_cast<std::size_t>(m) * K + k] * W[static_cast<std::size_t>(m) * K + j];
+  const double noise = sigma_nu * sigma_nu;
+  double rate = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const double signal = std::norm(E[k * K + k]);
+    double row = 0.0;
+    for (int j = 0; j < K; ++j) row += std::norm(E[j * K + k]);
+    const double sinr = signal / ((row - signal) + noise);
+    out[6 + k] = sinr;
+    rate += std::log2(1.0 + sinr);
+  }
+  double res = 0.0;
+  for (int j = 0; j < K; ++j)
+    for (int k = 0; k < K; ++k) {
+      cd e = E[j * K + k];
+      if (k == j) e -= c[k];
+      res += std::norm(e);
+    }
+  std::vector<cd> Z(static_cast<std::size_t>(K) * M);
+  const int zrc = zf(H, c, K, M, Z.data());
+  out[0] = tx;
+  out[1] = alpha * l21w;
+  out[2] = rate;
+  out[3] = zrc == ORA_OK && l21w > 0.0 ? l21(Z.data(), K, M) / l21w : std::nan("");
+  out[4] = std::sqrt(res);
+  out[5] = zrc == ORA_OK ? 1.0 : 0.0;
+  return ORA_OK;
+}
+
+int ora_metrics_batch_f32(const float* H, const float* W, std::int64_t B, const double* c, double sigma_nu,
+                          double alpha, int K, int M, double* out, int threads) {
+  const std::size_t n = static_cast<std::size_t>(K) * M;
+  return guarded([&] {
+    parallel_for(static_cast<std::size_t>(B), [&](std::size_t b) {
+      std::vector<cd> h, w;
+      promote(H + 2 * n * b, n, h);
+      promote(W + 2 * n * b, n, w);
+      ora_metrics(reinterpret_cast<const double*>(h.data()), reinterpret_cast<const double*>(w.data()), c,
+                  sigma_nu, alpha, K, M, out + b * (6 + K));
+    }, threads);
+    return ORA_OK;
+  });
+}
+
 int ora_zf_precoder(const double* H, const double* c, int K, int M, double* W) {
   if (K < 1 || M < K) return ORA_EINVAL;
   return zf(as_c(H), c, K, M, as_c(W));

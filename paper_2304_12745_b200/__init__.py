@@ -29,6 +29,8 @@ from .capi import (  # noqa: F401
     layer_params,
     layers_general,
     lipschitz_exact,
+    metrics,
+    summarize_metrics,
     lib,
     lib_path,
     pgd_fixed,

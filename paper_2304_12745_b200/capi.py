@@ -65,6 +65,7 @@ def lib():
             "ufpgd_gpu_unfolded_forward_host": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, P, d, i]),
             "ufpgd_gpu_pgd_fixed_host": (i, [P, i64, i, i, i, d, i64, P, i, P, P, P, P, P, d, i]),
             "ufpgd_gpu_fp32_peak": (i, [i, P, P]),
+            "ufpgd_gpu_metrics": (i, [P, P, i64, i, i, P, d, d, P, P, i, P]),
             "ufpgd_gpu_init": (i, [i]),
             "ufpgd_gpu_shutdown": (i, []),
             "ufpgd_gpu_unfolded_forward_sharded": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, d]),
@@ -282,6 +283,39 @@ def lipschitz_exact(H, stream=None):
     _check(lib().ufpgd_gpu_lipschitz_exact(_ptr(H), B, K, M, _ptr(Lout), _ptr(st), H.device.index or 0,
                                            _stream_ptr(stream)))
     return Lout, st
+
+
+def metrics(H, W, c, *, sigma_nu: float = 1.0, alpha: float = 1.0, want_zf: bool = False, stream=None):
+    """Batched compute_metrics + ZF reference (metrics.cpp:79-91, zf.cpp:9-30)
+    on device tensors [B, M, K]. Returns dict(out=float64 [B, 6 + K] with
+    columns tx_power, cons_power, sum_rate, pcg, residual, zf_ok, sinr..., zf)."""
+    import torch
+
+    B, K, M = _check_batch(H)
+    if W.shape != H.shape or W.dtype != H.dtype or not W.is_cuda:
+        raise ValueError("W must match H")
+    cc = _f64(c)
+    out = torch.empty((B, 6 + K), dtype=torch.float64, device=H.device)
+    zf = torch.empty_like(H) if want_zf else None
+    _check(lib().ufpgd_gpu_metrics(_ptr(H), _ptr(W), B, K, M, _ptr(cc), float(sigma_nu), float(alpha), _ptr(out),
+                                   _ptr(zf), H.device.index or 0, _stream_ptr(stream)))
+    return dict(out=out, zf=zf)
+
+
+def summarize_metrics(out):
+    """evaluate's reduction (training.cpp:361-399): means and standard errors
+    of tx_power, cons_power, sinr, sum_rate, pcg, residual over realizations."""
+    o = np.asarray(out, dtype=np.float64)
+    n = len(o)
+    cols = {"tx_power": o[:, 0], "cons_power": o[:, 1], "sum_rate": o[:, 2], "pcg": o[:, 3], "residual": o[:, 4]}
+    mean = {k: float(v.mean()) for k, v in cols.items()}
+    mean["sinr"] = o[:, 6:].mean(axis=0)
+    se = {}
+    if n > 1:
+        scale = 1.0 / ((n - 1) * n)
+        se = {k: float(np.sqrt(((v - mean[k]) ** 2).sum() * scale)) for k, v in cols.items()}
+        se["sinr"] = np.sqrt(((o[:, 6:] - mean["sinr"]) ** 2).sum(axis=0) * scale)
+    return {"num_channels": n, "mean": mean, "std_error": se}
 
 
 def fp32_peak(device: int = 0):

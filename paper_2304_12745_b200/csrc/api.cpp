@@ -479,6 +479,82 @@ int count_active_columns(const PrecoderMatrix& precoder) {
   return a;
 }
 
+namespace {
+// out = {tx, cons, sum_rate, pcg, residual, zf_ok, sinr[K]} for one pair.
+std::vector<double> device_metrics(const ChannelMatrix& channel, const PrecoderMatrix& precoder,
+                                   const SystemConfig& cfg, PrecoderMatrix* zf_out) {
+  cfg.validate();
+  if (channel.rows() != cfg.K || channel.cols() != cfg.M || precoder.rows() != cfg.K || precoder.cols() != cfg.M)
+    throw std::invalid_argument("sinr_per_user: shape mismatch");
+  const int K = cfg.K, M = cfg.M;
+  const std::size_t n = static_cast<std::size_t>(K) * M;
+  DeviceScope scope;
+  DeviceBuffer<ufpgd_c64> dH(n), dW(n), dZ(zf_out ? n : 0);
+  DeviceBuffer<double> dout(6 + K);
+  const auto h = to_c64(channel);
+  const auto w = to_c64(precoder);
+  dH.upload(h.data());
+  dW.upload(w.data());
+  const RealVector c = cfg.constraint_diag();
+  check(ufpgd_gpu_metrics(dH.p, dW.p, 1, K, M, c.data(), cfg.sigma_nu, cfg.alpha, dout.p, dZ.p, g_device, nullptr));
+  std::vector<double> out(6 + K);
+  dout.download(out.data());
+  if (zf_out) {
+    std::vector<ufpgd_c64> z(n);
+    dZ.download(z.data());
+    *zf_out = from_c64(z.data(), K, M);
+  }
+  return out;
+}
+}  // namespace
+
+PrecoderMatrix zf_precoder(const ChannelMatrix& channel, const SystemConfig& cfg) {
+  PrecoderMatrix z;
+  const auto out = device_metrics(channel, channel.conjugate(), cfg, &z);
+  if (out[5] == 0.0) throw SingularChannelError("zf_precoder: channel Gram matrix is singular");
+  return z;
+}
+
+RealVector sinr_per_user(const ChannelMatrix& channel, const PrecoderMatrix& precoder, const SystemConfig& cfg) {
+  const auto out = device_metrics(channel, precoder, cfg, nullptr);
+  RealVector s(cfg.K);
+  for (int k = 0; k < cfg.K; ++k) s[k] = out[6 + k];
+  return s;
+}
+
+double sum_rate(const RealVector& sinr) {  // metrics.cpp:48-54
+  double total = 0.0;
+  for (std::ptrdiff_t k = 0; k < sinr.size(); ++k) total += std::log2(1.0 + sinr[k]);
+  return total;
+}
+
+double pcg_from_reference(const PrecoderMatrix& zf_reference, const PrecoderMatrix& precoder) {
+  const double denom = l21_norm(precoder);
+  if (!(denom > 0.0)) throw std::invalid_argument("pcg: precoder consumes zero power");
+  return l21_norm(zf_reference) / denom;
+}
+
+double pcg(const ChannelMatrix& channel, const PrecoderMatrix& precoder, const SystemConfig& cfg) {
+  if (!(l21_norm(precoder) > 0.0)) throw std::invalid_argument("pcg: precoder consumes zero power");
+  const auto out = device_metrics(channel, precoder, cfg, nullptr);
+  if (out[5] == 0.0) throw SingularChannelError("zf_precoder: channel Gram matrix is singular");
+  return out[3];
+}
+
+MetricsReport compute_metrics(const ChannelMatrix& channel, const PrecoderMatrix& precoder, const SystemConfig& cfg) {
+  const auto out = device_metrics(channel, precoder, cfg, nullptr);
+  if (out[5] == 0.0) throw SingularChannelError("zf_precoder: channel Gram matrix is singular");
+  MetricsReport r;
+  r.tx_power = out[0];
+  r.cons_power = out[1];
+  r.sum_rate = out[2];
+  r.pcg = out[3];
+  r.residual = out[4];
+  r.sinr = RealVector(cfg.K);
+  for (int k = 0; k < cfg.K; ++k) r.sinr[k] = out[6 + k];
+  return r;
+}
+
 // ---- batch.hpp ------------------------------------------------------------------
 BatchResult forward_batch(const UnfoldedNetwork& net, const std::complex<float>* channels, std::int64_t B,
                           const SystemConfig& cfg, StartMode start, const std::complex<float>* W0) {
@@ -558,6 +634,74 @@ BatchResult forward_batch_multi_gpu(const UnfoldedNetwork& net, const std::compl
   r.active_sum = stats[1];
   r.diverged = static_cast<long>(stats[2]);
   return r;
+}
+
+EvaluationSummary evaluate_batch(const UnfoldedNetwork& net, const std::complex<float>* channels, std::int64_t B,
+                                 const SystemConfig& cfg) {
+  BatchResult r = forward_batch(net, channels, B, cfg, StartMode::ConjChannel);
+  if (r.diverged) throw DivergenceError("evaluate: non-finite iterate", r.diverged_at[0]);
+  const int K = cfg.K, M = cfg.M;
+  const std::size_t n = static_cast<std::size_t>(B) * K * M;
+  EvaluationSummary s;
+  s.num_channels = static_cast<std::size_t>(B);
+  if (B == 0) return s;
+  DeviceScope scope;
+  DeviceBuffer<ufpgd_c64> dH(n), dW(n);
+  DeviceBuffer<double> dout(static_cast<std::size_t>(B) * (6 + K));
+  dH.upload(reinterpret_cast<const ufpgd_c64*>(channels));
+  dW.upload(reinterpret_cast<const ufpgd_c64*>(r.precoders.data()));
+  const RealVector c = cfg.constraint_diag();
+  check(ufpgd_gpu_metrics(dH.p, dW.p, B, K, M, c.data(), cfg.sigma_nu, cfg.alpha, dout.p, nullptr, g_device, nullptr));
+  std::vector<double> out(static_cast<std::size_t>(B) * (6 + K));
+  dout.download(out.data());
+  // training.cpp:361-399 (singular channels are counted and skipped instead
+  // of aborting the whole evaluation)
+  s.mean.sinr = RealVector(K);
+  s.std_error.sinr = RealVector(K);
+  std::size_t used = 0;
+  for (std::int64_t b = 0; b < B; ++b) {
+    const double* o = &out[static_cast<std::size_t>(b) * (6 + K)];
+    if (o[5] == 0.0) {
+      ++s.singular;
+      continue;
+    }
+    ++used;
+    s.mean.tx_power += o[0];
+    s.mean.cons_power += o[1];
+    s.mean.sum_rate += o[2];
+    s.mean.pcg += o[3];
+    s.mean.residual += o[4];
+    for (int k = 0; k < K; ++k) s.mean.sinr[k] += o[6 + k];
+  }
+  if (used == 0) return s;
+  const double scale = 1.0 / static_cast<double>(used);
+  s.mean.tx_power *= scale;
+  s.mean.cons_power *= scale;
+  s.mean.sum_rate *= scale;
+  s.mean.pcg *= scale;
+  s.mean.residual *= scale;
+  for (int k = 0; k < K; ++k) s.mean.sinr[k] *= scale;
+  if (used > 1) {
+    auto sq = [](double d) { return d * d; };
+    for (std::int64_t b = 0; b < B; ++b) {
+      const double* o = &out[static_cast<std::size_t>(b) * (6 + K)];
+      if (o[5] == 0.0) continue;
+      s.std_error.tx_power += sq(o[0] - s.mean.tx_power);
+      s.std_error.cons_power += sq(o[1] - s.mean.cons_power);
+      s.std_error.sum_rate += sq(o[2] - s.mean.sum_rate);
+      s.std_error.pcg += sq(o[3] - s.mean.pcg);
+      s.std_error.residual += sq(o[4] - s.mean.residual);
+      for (int k = 0; k < K; ++k) s.std_error.sinr[k] += sq(o[6 + k] - s.mean.sinr[k]);
+    }
+    const double vs = 1.0 / (static_cast<double>(used - 1) * static_cast<double>(used));
+    s.std_error.tx_power = std::sqrt(s.std_error.tx_power * vs);
+    s.std_error.cons_power = std::sqrt(s.std_error.cons_power * vs);
+    s.std_error.sum_rate = std::sqrt(s.std_error.sum_rate * vs);
+    s.std_error.pcg = std::sqrt(s.std_error.pcg * vs);
+    s.std_error.residual = std::sqrt(s.std_error.residual * vs);
+    for (int k = 0; k < K; ++k) s.std_error.sinr[k] = std::sqrt(s.std_error.sinr[k] * vs);
+  }
+  return s;
 }
 
 }  // namespace ufpgd

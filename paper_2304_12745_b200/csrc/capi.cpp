@@ -645,6 +645,33 @@ int ufpgd_gpu_pgd_fixed_host(const ufpgd_c64* H, int64_t B, int K, int M, int po
       });
 }
 
+int ufpgd_gpu_metrics(const ufpgd_c64* H, const ufpgd_c64* W, int64_t B, int K, int M, const double* c,
+                      double sigma_nu, double alpha, double* out, ufpgd_c64* Wzf, int device,
+                      ufpgd_stream_t stream) {
+  int rc;
+  if ((rc = check_shape(B, K, M)) || (rc = check_c(c, K))) return rc;
+  if (K > 32) return fail(UFPGD_ENOTSUP, "metrics support K <= 32");
+  if (!(sigma_nu >= 0.0)) return fail(UFPGD_EINVAL_PARAM, "SystemConfig: sigma_nu must be >= 0");
+  if (!(alpha > 0.0)) return fail(UFPGD_EINVAL_PARAM, "alpha must be > 0");
+  if (B > 0 && (!H || !W || !out)) return fail(UFPGD_EINVAL_PARAM, "H, W and out are required");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
+  if (B == 0) return UFPGD_OK;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (metrics_smem_bytes(K, M) > static_cast<size_t>(optin)) return fail(UFPGD_ENOTSUP, "(K, M) too large for metrics");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* dc = nullptr;
+  UFPGD_CUDA(cudaMallocAsync(&dc, sizeof(double) * K, s));
+  UFPGD_CUDA(cudaMemcpyAsync(dc, c, sizeof(double) * K, cudaMemcpyHostToDevice, s));
+  cudaError_t e = launch_metrics(reinterpret_cast<const float2*>(H), reinterpret_cast<const float2*>(W), B, K, M,
+                                 dc, sigma_nu * sigma_nu, alpha, out, reinterpret_cast<float2*>(Wzf), s);
+  cudaFreeAsync(dc, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // c is a host buffer of the caller
+  if (e != cudaSuccess) return cuda_fail(e, "metrics kernel");
+  return UFPGD_OK;
+}
+
 int ufpgd_gpu_fp32_peak(int device, double* tflops, double* sm_ghz) {
   if (!tflops || !sm_ghz) return fail(UFPGD_EINVAL_PARAM, "null output");
   DeviceGuard g(device);

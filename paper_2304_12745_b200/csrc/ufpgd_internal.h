@@ -84,6 +84,9 @@ cudaError_t launch_general(const GeneralArgs& a, cudaStream_t s);
 cudaError_t launch_power(const PowerArgs& a, cudaStream_t s);
 cudaError_t launch_lipschitz_exact(const double2* H, long long B, int K, int M, const double2* v0,
                                    double* Lout, int32_t* status, cudaStream_t s);
+size_t metrics_smem_bytes(int K, int M);
+cudaError_t launch_metrics(const float2* H, const float2* W, long long B, int K, int M, const double* c,
+                           double sigma2, double alpha, double* out, float2* Wzf, cudaStream_t s);
 cudaError_t measure_fp32_peak(double* tflops, double* sm_ghz);
 cudaError_t launch_stats_finalize(const double* partials, long long n, double* stats,
                                   cudaStream_t s);

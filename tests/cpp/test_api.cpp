@@ -332,6 +332,38 @@ int main() {
     BatchResult p = solve_pgd_batch(H.data(), 64, cfg, 0.05, 500);
     CHECK(p.diverged == 0 && p.steps.size() == 64 && p.steps[0] > 0.0f);
   }
+  // --- test_metrics.cpp / evaluate on the device -------------------------------------
+  {
+    SystemConfig cfg = SystemConfig::uniform(4, 16, 10.0);
+    Rng rng(7);
+    ChannelMatrix h = generate_channel(cfg, rng);
+    PrecoderMatrix zf = zf_precoder(h, cfg);
+    RealVector s = sinr_per_user(h, zf, cfg);
+    for (int k = 0; k < 4; ++k) CHECK(std::abs(s[k] - 10.0) < 1e-4);
+    CHECK(std::abs(sum_rate(s) - 4.0 * std::log2(11.0)) < 1e-4);
+    CHECK(std::abs(pcg(h, zf, cfg) - 1.0) < 1e-6);
+    CHECK_THROWS_AS(pcg(h, PrecoderMatrix::Zero(4, 16), cfg), std::invalid_argument);
+    ChannelMatrix bad = h;
+    for (int m = 0; m < 16; ++m) bad(1, m) = bad(0, m);
+    CHECK_THROWS_AS(zf_precoder(bad, cfg), SingularChannelError);
+    MetricsReport rep = compute_metrics(h, 0.9 * zf, cfg);
+    CHECK(std::abs(rep.pcg - 1.0 / 0.9) < 1e-5);
+  }
+  {  // evaluate: untrained network == PGD-20, mean PCG in [0.97, 1.03] (test_pgd.cpp:519-538)
+    SystemConfig cfg = SystemConfig::uniform(8, 64, 10.0);
+    UnfoldedNetwork net = UnfoldedNetwork::pgd_init(8, 64, 20, 1.0 / 15.0);
+    const int B = 200;
+    std::vector<std::complex<float>> H(static_cast<std::size_t>(B) * 512);
+    for (int b = 0; b < B; ++b) {
+      ChannelMatrix h = channel_for(cfg, 33, b);
+      for (int m = 0; m < 64; ++m)
+        for (int k = 0; k < 8; ++k) H[static_cast<std::size_t>(b) * 512 + m * 8 + k] = std::complex<float>(h(k, m));
+    }
+    EvaluationSummary s = evaluate_batch(net, H.data(), B, cfg);
+    CHECK(s.num_channels == 200 && s.singular == 0);
+    CHECK(s.mean.pcg > 0.97 && s.mean.pcg < 1.03);
+    CHECK(s.std_error.pcg > 0.0);
+  }
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
