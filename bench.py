@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-other-configs", action="store_true")
     return ap.parse_args()
 
 
@@ -184,6 +185,51 @@ def load_traffic(w):
         return None
 
 
+def measure_other_configs(U, torch, local):
+    """Device-timed throughput of the other BASELINE configs (parity-test cases,
+    not bench lines): one warm-up launch, then CUDA-event timing. Config 5 times
+    the full 1,048,576-realization batch built from 65,536 distinct seeded
+    realizations tiled 16x (host generation of 2^20 channels takes minutes;
+    the kernel's cost does not depend on the values)."""
+    import dataclasses
+
+    res = {}
+    for cid in (1, 3, 4, 5):
+        w = U.CONFIGS[cid]
+        n_distinct = min(w.B, 65536)
+        H = torch.from_numpy(U.make_inputs(w, 0, n_distinct)).to(f"cuda:{local}")
+        if n_distinct < w.B:
+            H = H.repeat(w.B // n_distinct, 1, 1).contiguous()
+        reps = 3 if cid in (3, 4, 5) else 20
+
+        if w.kind == "pgd":
+            def run():
+                return U.pgd_fixed(H, w.lambda_pgd, w.L, w.c, power_steps=w.power_steps, w0_mode=w.w0_mode)
+        else:
+            lam, eta = w.layer_params()
+            Wd = torch.empty_like(H)
+
+            def run():
+                return U.unfolded_forward(H, lam, eta, w.c, w0_mode=w.w0_mode, out=Wd)
+        run()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            out = run()
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps
+        st = out["stats"].cpu().numpy()
+        res[f"cfg{cid}"] = {"workload": w.name(), "ms_per_batch": ms, "precoders_per_s": w.B / ms * 1e3,
+                            "tflops": w.flops_per_realization() * w.B / ms / 1e9, "diverged": int(st[2]),
+                            "mean_active": float(st[1]) / w.B,
+                            "note": "65,536 distinct realizations tiled 16x" if n_distinct < w.B else "full batch"}
+        del H
+        torch.cuda.empty_cache()
+    return res
+
+
 def run_ours(args, world, rank, local):
     import torch
     import torch.distributed as dist
@@ -273,6 +319,9 @@ def run_ours(args, world, rank, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(w, H_host.numpy(), lam, eta, args.cpu_seconds)
+    others = None
+    if rank == 0 and world == 1 and not args.no_other_configs:
+        others = measure_other_configs(U, torch, local)
 
     if rank == 0:
         flops = w.flops_per_realization() * B
@@ -310,6 +359,7 @@ def run_ours(args, world, rank, local):
             "gpu_launches": 2 * args.steps,
             "clocks": clocks.report(),
             "stats": sharding.summarize(stats, world * B),
+            "other_configs": others,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
