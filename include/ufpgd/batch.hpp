@@ -43,6 +43,21 @@ BatchResult solve_pgd_batch(const std::complex<float>* channels, std::int64_t B,
 BatchResult forward_batch_multi_gpu(const UnfoldedNetwork& net, const std::complex<float>* channels,
                                     std::int64_t B, const SystemConfig& cfg, int ngpus);
 
+// The per-sample body of train (training.cpp:205-246) for one mini-batch on
+// the device: taped forward from H^*, loss, loss gradient, backward, then the
+// deterministic batch mean. grads are packed (d_lambda_0, d_eta_0, ...) as
+// pack_params orders them (training.hpp:50-51), ready for adam_update.
+enum class LossKind { Unsupervised = 0, Supervised = 1 };
+
+struct TrainGradients {
+  double loss = 0.0;          // batch mean loss
+  std::vector<double> grads;  // batch mean gradient, size 2L
+};
+
+TrainGradients train_gradients(const UnfoldedNetwork& net, const std::complex<float>* channels, std::int64_t B,
+                               const SystemConfig& cfg, LossKind kind = LossKind::Unsupervised,
+                               double lambda_cost = 1.0 / 15.0, const std::complex<float>* labels = nullptr);
+
 // evaluate (training.cpp:310-421) without per-layer curves: forward on every
 // channel, device metrics, means and standard errors at the final layer.
 struct EvaluationSummary {

@@ -184,6 +184,22 @@ int ufpgd_gpu_unfolded_forward_sharded(const ufpgd_c64* H, int64_t B, int K, int
                                        int32_t* diverged_at, double* stats, double alpha);
 
 /*
+ * Training-step gradients — the per-sample body of
+ * ufpgd::train (training.cpp:205-234) over B channels: taped forward from
+ * W0 (H^* = the reference's default, or 0), the loss (loss_kind 0:
+ * unsupervised_loss = lagrangian with lambda_cost; 1: supervised
+ * ||W - labels||^2, training.cpp:59-95), its gradient, and backward
+ * (unfolded.cpp:158-239). Device outputs: loss[B], grads[B][2L] in pack order
+ * (d_lambda_0, d_eta_0, ...; training.hpp:50-51) and, if non-null,
+ * mean[1 + 2L] = batch means (deterministic order) — what adam_update
+ * consumes. FP32 compute, FP64 reductions. Async on `stream`.
+ */
+int ufpgd_gpu_unfolded_grad(const ufpgd_c64* H, int64_t B, int K, int M, const double* lambda,
+                            const double* eta, int L, const double* c, int w0_mode, int loss_kind,
+                            double lambda_cost, const ufpgd_c64* labels, double* loss, double* grads,
+                            double* mean, int device, ufpgd_stream_t stream);
+
+/*
  * Batched metrics — compute_metrics (metrics.cpp:79-91)
  * with the ZF reference of zf_precoder (zf.cpp:9-30) for B (H, W) pairs,
  * the body of evaluate's parallel_for (training.cpp:324-357). FP64 on the

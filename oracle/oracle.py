@@ -71,6 +71,9 @@ def lib():
             "ora_lagrangian_batch_f32": (i, [P, P, i64, P, i, i, d, P, i]),
             "ora_lagrangian_batch_f64": (i, [P, P, i64, P, i, i, d, P, i]),
             "ora_metrics": (i, [P, P, P, d, d, i, i, P]),
+            "ora_backward": (i, [P, i, i, P, P, i, P, P, P, P, P, P, P]),
+            "ora_train_sample": (i, [P, P, i, i, P, P, i, i, d, P, P, P]),
+            "ora_train_batch_f32": (i, [P, i64, P, i, i, P, P, i, i, d, P, P, P, P, i]),
             "ora_metrics_batch_f32": (i, [P, P, i64, P, d, d, i, i, P, i]),
         }
         for name, (res, args) in sigs.items():
@@ -109,6 +112,10 @@ class ConvergenceError(RuntimeError):
 
 
 class SingularChannelError(RuntimeError):
+    pass
+
+
+class TrainingError(RuntimeError):
     pass
 
 
@@ -592,6 +599,68 @@ def forward(net: UnfoldedNetwork, H, cfg: SystemConfig, start=None,
 
 def forward_infer(net, H, cfg) -> np.ndarray:
     return forward(net, H, cfg).output
+
+
+@dataclass
+class ParamGradients:
+    d_lambda: np.ndarray
+    d_eta: np.ndarray
+
+
+def backward(tape: List[LayerTape], net: UnfoldedNetwork, H, cfg, dcost_dw) -> ParamGradients:
+    """unfolded.cpp:158-239."""
+    net.validate()
+    cfg.validate()
+    L = len(net.layers)
+    K, M = H.shape
+    if len(tape) != L:
+        raise TrainingError("backward: tape depth does not match network")
+    if dcost_dw.shape != (K, M) or H.shape != (cfg.K, cfg.M):
+        raise TrainingError("backward: shape mismatch")
+    lam = np.array([l.lambda_i for l in net.layers])
+    eta = np.array([l.eta_i for l in net.layers])
+    tin = np.stack([to_storage(t.input) for t in tape])
+    tv = np.stack([to_storage(t.step_image) for t in tape])
+    tn = np.stack([t.column_norms for t in tape]).astype(np.float64)
+    ts = np.stack([t.shrink_factors for t in tape]).astype(np.float64)
+    dl, de = np.empty(L), np.empty(L)
+    rc = lib().ora_backward(_p(to_storage(H)), K, M, _p(lam), _p(eta), L, _p(tin), _p(tv), _p(tn), _p(ts),
+                            _p(to_storage(dcost_dw)), _p(dl), _p(de))
+    if rc != ORA_OK:
+        raise TrainingError("backward: layer step size must be > 0")
+    return ParamGradients(dl, de)
+
+
+def unsupervised_loss(W, H, cfg, lambda_cost) -> float:  # training.cpp:76-81
+    return lagrangian_value(W, H, cfg, lambda_cost)
+
+
+def unsupervised_loss_grad(W, H, cfg, lambda_cost) -> np.ndarray:  # training.cpp:83-95
+    g = 2.0 * grad_f(W, H, cfg)
+    for m in range(W.shape[1]):
+        n = np.linalg.norm(W[:, m])
+        if n > 0.0:
+            g[:, m] += (lambda_cost / n) * W[:, m]
+    return g
+
+
+def train_batch_f32(H, c, lam, eta, loss_kind=0, lambda_cost=1.0 / 15.0, labels=None, threads=0):
+    """Per-sample loss and (d_lambda_i, d_eta_i) of train's inner loop
+    (training.cpp:205-234) over complex64 channels [B][M][K]."""
+    H = np.ascontiguousarray(H, dtype=np.complex64)
+    B, M, K = H.shape
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    eta = np.ascontiguousarray(eta, dtype=np.float64)
+    L = lam.size
+    loss = np.empty(B)
+    grads = np.empty((B, 2 * L))
+    st = np.empty(B, dtype=np.int32)
+    lab = None if labels is None else np.ascontiguousarray(labels, dtype=np.complex64)
+    rc = lib().ora_train_batch_f32(_p(H), B, _p(np.ascontiguousarray(c, dtype=np.float64)), K, M, _p(lam), _p(eta), L,
+                                   loss_kind, float(lambda_cost), _p(lab), _p(loss), _p(grads), _p(st), threads)
+    if rc != ORA_OK:
+        raise ValueError("train batch failed")
+    return loss, grads, st
 
 
 # --------------------------------------------------------------------------

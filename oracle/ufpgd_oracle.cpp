@@ -596,6 +596,126 @@ int ora_metrics_batch_f32(const float* H, const float* W, std::int64_t B, const 
   });
 }
 
+// backward (unfolded.cpp:158-239) over the tape of forward_one. dcost is the
+// real-pair cost gradient dC/dRe(W) + i dC/dIm(W) of the output.
+int ora_backward(const double* Hp, int K, int M, const double* lambda, const double* eta, int L,
+                 const double* tape_in, const double* tape_v, const double* tape_norms,
+                 const double* tape_shrink, const double* dcost, double* d_lambda, double* d_eta) {
+  const std::size_t n = static_cast<std::size_t>(K) * M;
+  const cd* H = as_c(Hp);
+  std::vector<cd> g(as_c(dcost), as_c(dcost) + n), gimg(n), S(static_cast<std::size_t>(K) * K);
+  for (int idx = L - 1; idx >= 0; --idx) {
+    const cd* Win = as_c(tape_in) + n * idx;
+    const cd* V = as_c(tape_v) + n * idx;
+    const double* norms = tape_norms + static_cast<std::size_t>(M) * idx;
+    const double* shrink = tape_shrink + static_cast<std::size_t>(M) * idx;
+    const double lam = lambda[idx], et = eta[idx];
+    if (!(et > 0.0)) return ORA_EINVAL;  // TrainingError (unfolded.cpp:189-191)
+    const double t = lam * et;
+    double d_t = 0.0;
+    for (int m = 0; m < M; ++m) {
+      const double nrm = norms[m];
+      const cd* v = V + static_cast<std::size_t>(m) * K;
+      const cd* gm = g.data() + static_cast<std::size_t>(m) * K;
+      cd* gi = gimg.data() + static_cast<std::size_t>(m) * K;
+      if (nrm > t) {
+        cd dot = 0.0;
+        for (int k = 0; k < K; ++k) dot += std::conj(v[k]) * gm[k];
+        const double inner = dot.real();
+        d_t -= inner / nrm;
+        for (int k = 0; k < K; ++k) gi[k] = shrink[m] * gm[k] + (t / (nrm * nrm * nrm)) * inner * v[k];
+      } else {
+        for (int k = 0; k < K; ++k) gi[k] = 0.0;
+      }
+    }
+    double d_eta_direct = 0.0;
+    for (int m = 0; m < M; ++m) {
+      cd dot = 0.0;
+      for (int k = 0; k < K; ++k) {
+        const std::size_t e = static_cast<std::size_t>(m) * K + k;
+        dot += std::conj(gimg[e]) * (Win[e] - V[e]);
+      }
+      d_eta_direct -= dot.real() / et;
+    }
+    d_lambda[idx] = et * d_t;
+    d_eta[idx] = lam * d_t + d_eta_direct;
+    w_times_ht(gimg.data(), H, K, M, S.data());  // S(k, j) = sum_m gimg(k, m) H(j, m)
+    for (int m = 0; m < M; ++m)
+      for (int k = 0; k < K; ++k) {
+        cd acc = 0.0;
+        for (int j = 0; j < K; ++j) acc += S[j * K + k] * std::conj(H[static_cast<std::size_t>(m) * K + j]);
+        const std::size_t e = static_cast<std::size_t>(m) * K + k;
+        g[e] = gimg[e] - et * acc;
+      }
+  }
+  return ORA_OK;
+}
+
+// The per-sample body of train's parallel_for (training.cpp:205-234): taped
+// forward from H^*, loss, loss gradient (training.cpp:59-95), backward.
+// loss_kind 0 = unsupervised (lagrangian with lambda_cost), 1 = supervised
+// (||W - label||^2). grads = (d_lambda_0, d_eta_0, d_lambda_1, ...).
+int ora_train_sample(const double* Hp, const double* c, int K, int M, const double* lambda, const double* eta, int L,
+                     int loss_kind, double lambda_cost, const double* label, double* loss, double* grads) {
+  const std::size_t n = static_cast<std::size_t>(K) * M;
+  const cd* H = as_c(Hp);
+  std::vector<cd> W(n), tin(n * L), tv(n * L);
+  std::vector<double> tn(static_cast<std::size_t>(M) * L), ts(static_cast<std::size_t>(M) * L);
+  const long d = forward_one(H, c, K, M, lambda, eta, L, nullptr, W.data(), nullptr, tin.data(), tv.data(), tn.data(),
+                             ts.data(), nullptr);
+  if (d >= 0) return ORA_EDIVERGED;
+  std::vector<cd> dc(n);
+  if (loss_kind == 1) {
+    const cd* lab = as_c(label);
+    double l = 0.0;
+    for (std::size_t i = 0; i < n; ++i) {
+      l += std::norm(W[i] - lab[i]);
+      dc[i] = 2.0 * (W[i] - lab[i]);
+    }
+    *loss = l;
+  } else {
+    const double r = residual(H, W.data(), c, K, M);
+    *loss = lambda_cost * l21(W.data(), K, M) + r * r;
+    ora_grad_f(reinterpret_cast<const double*>(W.data()), Hp, c, K, M, reinterpret_cast<double*>(dc.data()));
+    for (int m = 0; m < M; ++m) {
+      const cd* w = W.data() + static_cast<std::size_t>(m) * K;
+      const double nrm = col_norm(w, K);
+      for (int k = 0; k < K; ++k) {
+        cd& e = dc[static_cast<std::size_t>(m) * K + k];
+        e = 2.0 * e;
+        if (nrm > 0.0) e += (lambda_cost / nrm) * w[k];
+      }
+    }
+  }
+  std::vector<double> dl(L), de(L);
+  const int rc = ora_backward(Hp, K, M, lambda, eta, L, reinterpret_cast<const double*>(tin.data()),
+                              reinterpret_cast<const double*>(tv.data()), tn.data(), ts.data(),
+                              reinterpret_cast<const double*>(dc.data()), dl.data(), de.data());
+  for (int i = 0; i < L; ++i) {
+    grads[2 * i] = dl[i];
+    grads[2 * i + 1] = de[i];
+  }
+  return rc;
+}
+
+int ora_train_batch_f32(const float* H, std::int64_t B, const double* c, int K, int M, const double* lambda,
+                        const double* eta, int L, int loss_kind, double lambda_cost, const float* labels,
+                        double* loss, double* grads, std::int32_t* status, int threads) {
+  const std::size_t n = static_cast<std::size_t>(K) * M;
+  return guarded([&] {
+    parallel_for(static_cast<std::size_t>(B), [&](std::size_t b) {
+      std::vector<cd> h, lab;
+      promote(H + 2 * n * b, n, h);
+      if (labels) promote(labels + 2 * n * b, n, lab);
+      const int rc = ora_train_sample(reinterpret_cast<const double*>(h.data()), c, K, M, lambda, eta, L, loss_kind,
+                                      lambda_cost, labels ? reinterpret_cast<const double*>(lab.data()) : nullptr,
+                                      loss + b, grads + 2 * L * b);
+      if (status) status[b] = rc;
+    }, threads);
+    return ORA_OK;
+  });
+}
+
 int ora_zf_precoder(const double* H, const double* c, int K, int M, double* W) {
   if (K < 1 || M < K) return ORA_EINVAL;
   return zf(as_c(H), c, K, M, as_c(W));

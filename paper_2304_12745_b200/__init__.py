@@ -39,5 +39,6 @@ from .capi import (  # noqa: F401
     power_v0,
     unfolded_forward,
     unfolded_forward_host,
+    unfolded_grad,
 )
 from .workloads import CONFIGS, Workload, make_inputs, mp_bound, project_params  # noqa: F401

@@ -66,6 +66,7 @@ def lib():
             "ufpgd_gpu_pgd_fixed_host": (i, [P, i64, i, i, i, d, i64, P, i, P, P, P, P, P, d, i]),
             "ufpgd_gpu_fp32_peak": (i, [i, P, P]),
             "ufpgd_gpu_metrics": (i, [P, P, i64, i, i, P, d, d, P, P, i, P]),
+            "ufpgd_gpu_unfolded_grad": (i, [P, i64, i, i, P, P, i, P, i, i, d, P, P, P, P, i, P]),
             "ufpgd_gpu_init": (i, [i]),
             "ufpgd_gpu_shutdown": (i, []),
             "ufpgd_gpu_unfolded_forward_sharded": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, d]),
@@ -300,6 +301,25 @@ def metrics(H, W, c, *, sigma_nu: float = 1.0, alpha: float = 1.0, want_zf: bool
     _check(lib().ufpgd_gpu_metrics(_ptr(H), _ptr(W), B, K, M, _ptr(cc), float(sigma_nu), float(alpha), _ptr(out),
                                    _ptr(zf), H.device.index or 0, _stream_ptr(stream)))
     return dict(out=out, zf=zf)
+
+
+def unfolded_grad(H, lambda_, eta, c, *, w0_mode: int = W0_CONJ_H, loss_kind: int = 0,
+                  lambda_cost: float = 1.0 / 15.0, labels=None, stream=None):
+    """Per-sample loss and parameter gradients of train's inner loop
+    (training.cpp:205-234) for device channels [B, M, K]; returns dict(loss
+    [B], grads [B, 2L] in pack order, mean [1 + 2L])."""
+    import torch
+
+    B, K, M = _check_batch(H)
+    lam, et, cc = _f64(lambda_), _f64(eta), _f64(c)
+    L = lam.size
+    loss = torch.empty(B, dtype=torch.float64, device=H.device)
+    grads = torch.empty((B, 2 * L), dtype=torch.float64, device=H.device)
+    mean = torch.empty(1 + 2 * L, dtype=torch.float64, device=H.device)
+    _check(lib().ufpgd_gpu_unfolded_grad(_ptr(H), B, K, M, _ptr(lam), _ptr(et), L, _ptr(cc), w0_mode, loss_kind,
+                                         float(lambda_cost), _ptr(labels), _ptr(loss), _ptr(grads), _ptr(mean),
+                                         H.device.index or 0, _stream_ptr(stream)))
+    return dict(loss=loss, grads=grads, mean=mean)
 
 
 def summarize_metrics(out):

@@ -636,6 +636,41 @@ BatchResult forward_batch_multi_gpu(const UnfoldedNetwork& net, const std::compl
   return r;
 }
 
+TrainGradients train_gradients(const UnfoldedNetwork& net, const std::complex<float>* channels, std::int64_t B,
+                               const SystemConfig& cfg, LossKind kind, double lambda_cost,
+                               const std::complex<float>* labels) {
+  net.validate();
+  check_projected(net);
+  cfg.validate();
+  if (cfg.K != net.num_users || cfg.M != net.num_antennas) throw std::invalid_argument("forward: dimension mismatch");
+  if (kind == LossKind::Supervised && !labels) throw TrainingError("train: supervised mode requires labeled datasets");
+  const int L = static_cast<int>(net.layers.size());
+  std::vector<double> lam, eta;
+  for (const LayerParams& l : net.layers) {
+    lam.push_back(l.lambda_i);
+    eta.push_back(l.eta_i);
+  }
+  const std::size_t n = static_cast<std::size_t>(B) * cfg.K * cfg.M;
+  TrainGradients r;
+  r.grads.assign(2 * static_cast<std::size_t>(L), 0.0);
+  if (B == 0) return r;
+  DeviceScope scope;
+  DeviceBuffer<ufpgd_c64> dH(n), dLab(labels ? n : 0);
+  DeviceBuffer<double> dloss(static_cast<std::size_t>(B)), dgr(static_cast<std::size_t>(B) * 2 * L), dmean(1 + 2 * L);
+  dH.upload(reinterpret_cast<const ufpgd_c64*>(channels));
+  if (labels) dLab.upload(reinterpret_cast<const ufpgd_c64*>(labels));
+  const RealVector c = cfg.constraint_diag();
+  check(ufpgd_gpu_unfolded_grad(dH.p, B, cfg.K, cfg.M, lam.data(), eta.data(), L, c.data(), UFPGD_W0_CONJ_H,
+                                static_cast<int>(kind), lambda_cost, dLab.p, dloss.p, dgr.p, dmean.p, g_device,
+                                nullptr));
+  std::vector<double> mean(1 + 2 * static_cast<std::size_t>(L));
+  dmean.download(mean.data());
+  if (!std::isfinite(mean[0])) throw TrainingError("train: non-finite loss");
+  r.loss = mean[0];
+  for (int i = 0; i < 2 * L; ++i) r.grads[static_cast<std::size_t>(i)] = mean[1 + i];
+  return r;
+}
+
 EvaluationSummary evaluate_batch(const UnfoldedNetwork& net, const std::complex<float>* channels, std::int64_t B,
                                  const SystemConfig& cfg) {
   BatchResult r = forward_batch(net, channels, B, cfg, StartMode::ConjChannel);

@@ -672,6 +672,49 @@ int ufpgd_gpu_metrics(const ufpgd_c64* H, const ufpgd_c64* W, int64_t B, int K, 
   return UFPGD_OK;
 }
 
+int ufpgd_gpu_unfolded_grad(const ufpgd_c64* H, int64_t B, int K, int M, const double* lambda, const double* eta,
+                            int L, const double* c, int w0_mode, int loss_kind, double lambda_cost,
+                            const ufpgd_c64* labels, double* loss, double* grads, double* mean, int device,
+                            ufpgd_stream_t stream) {
+  int rc;
+  if ((rc = check_shape(B, K, M)) || (rc = check_layers(lambda, eta, L)) || (rc = check_c(c, K))) return rc;
+  if (L < 1) return fail(UFPGD_EINVAL_PARAM, "need at least one layer");
+  if (w0_mode != UFPGD_W0_ZERO && w0_mode != UFPGD_W0_CONJ_H) return fail(UFPGD_EINVAL_PARAM, "W0 = 0 or H^* only");
+  if (loss_kind != 0 && loss_kind != 1) return fail(UFPGD_EINVAL_PARAM, "bad loss kind");
+  if (loss_kind == 1 && !labels) return fail(UFPGD_EINVAL_PARAM, "supervised mode requires labels");
+  if (!(lambda_cost >= 0.0)) return fail(UFPGD_EINVAL_PARAM, "TrainConfig: lambda_cost must be >= 0");
+  if (B > 0 && (!H || !loss || !grads)) return fail(UFPGD_EINVAL_PARAM, "H, loss and grads are required");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
+  if (B == 0) return UFPGD_OK;
+  if (!general_fits(K, M)) return fail(UFPGD_ENOTSUP, "(K, M) too large for the gradient kernel");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  GradArgs a{};
+  a.H = reinterpret_cast<const float2*>(H);
+  a.labels = reinterpret_cast<const float2*>(labels);
+  a.out_loss = loss;
+  a.out_grads = grads;
+  a.B = B;
+  a.K = K;
+  a.M = M;
+  a.L = L;
+  a.w0_mode = w0_mode;
+  a.loss_kind = loss_kind;
+  a.lambda_cost = static_cast<float>(lambda_cost);
+  for (int k = 0; k < K; ++k) a.c[k] = static_cast<float>(c[k]);
+  for (int l = 0; l < L; ++l) {
+    a.eta[l] = static_cast<float>(eta[l]);
+    a.thr[l] = static_cast<float>(lambda[l] * eta[l]);
+    a.lam[l] = lambda[l];
+    a.eta64[l] = eta[l];
+  }
+  UFPGD_CUDA(cudaMallocAsync(&a.tape, sizeof(float2) * 2ull * L * K * M * B, s));
+  cudaError_t e = launch_grad(a, mean, s);
+  cudaFreeAsync(a.tape, s);
+  if (e != cudaSuccess) return cuda_fail(e, "gradient kernel");
+  return UFPGD_OK;
+}
+
 int ufpgd_gpu_fp32_peak(int device, double* tflops, double* sm_ghz) {
   if (!tflops || !sm_ghz) return fail(UFPGD_EINVAL_PARAM, "null output");
   DeviceGuard g(device);

@@ -65,6 +65,25 @@ struct GeneralArgs {
   float thr[UFPGD_MAX_LAYERS];
 };
 
+// Arguments of the training-gradient kernel (one CTA per realization).
+struct GradArgs {
+  const float2* H;
+  const float2* labels;  // supervised loss targets (nullable)
+  float2* tape;          // [B][2][L][M*K] workspace
+  double* out_loss;      // [B]
+  double* out_grads;     // [B][2L]
+  long long B;
+  int K, M, L;
+  int w0_mode;
+  int loss_kind;  // 0 unsupervised (lagrangian, lambda_cost), 1 supervised
+  float lambda_cost;
+  float c[UFPGD_MAX_USERS];
+  float eta[UFPGD_MAX_LAYERS];
+  float thr[UFPGD_MAX_LAYERS];
+  double lam[UFPGD_MAX_LAYERS];
+  double eta64[UFPGD_MAX_LAYERS];
+};
+
 struct PowerArgs {
   const float2* H;
   float* Lout;
@@ -87,6 +106,8 @@ cudaError_t launch_lipschitz_exact(const double2* H, long long B, int K, int M, 
 size_t metrics_smem_bytes(int K, int M);
 cudaError_t launch_metrics(const float2* H, const float2* W, long long B, int K, int M, const double* c,
                            double sigma2, double alpha, double* out, float2* Wzf, cudaStream_t s);
+size_t grad_smem_bytes(int K, int M);
+cudaError_t launch_grad(const GradArgs& a, double* mean, cudaStream_t s);
 cudaError_t measure_fp32_peak(double* tflops, double* sm_ghz);
 cudaError_t launch_stats_finalize(const double* partials, long long n, double* stats,
                                   cudaStream_t s);

@@ -364,6 +364,31 @@ int main() {
     CHECK(s.mean.pcg > 0.97 && s.mean.pcg < 1.03);
     CHECK(s.std_error.pcg > 0.0);
   }
+  {  // training-step gradients: zero-cost limit and a descent direction
+    SystemConfig cfg = SystemConfig::uniform(4, 16, 10.0);
+    UnfoldedNetwork net = UnfoldedNetwork::pgd_init(4, 16, 5, 0.2);
+    const int B = 64;
+    std::vector<std::complex<float>> H(static_cast<std::size_t>(B) * 64);
+    for (int b = 0; b < B; ++b) {
+      ChannelMatrix h = channel_for(cfg, 80, b);
+      for (int m = 0; m < 16; ++m)
+        for (int k = 0; k < 4; ++k) H[static_cast<std::size_t>(b) * 64 + m * 4 + k] = std::complex<float>(h(k, m));
+    }
+    TrainGradients g = train_gradients(net, H.data(), B, cfg);
+    CHECK(g.grads.size() == 10 && std::isfinite(g.loss) && g.loss > 0.0);
+    // a small projected step against the gradient must not increase the loss
+    UnfoldedNetwork next = net;
+    double gn = 0.0;
+    for (double v : g.grads) gn += v * v;
+    gn = std::sqrt(gn);
+    for (std::size_t i = 0; i < next.layers.size(); ++i) {
+      next.layers[i].lambda_i -= 1e-4 * g.grads[2 * i] / gn;
+      next.layers[i].eta_i -= 1e-9 * g.grads[2 * i + 1] / gn;
+    }
+    next = project_params(next);
+    CHECK(train_gradients(next, H.data(), B, cfg).loss <= g.loss * (1.0 + 1e-9));
+    CHECK_THROWS_AS(train_gradients(net, H.data(), B, cfg, LossKind::Supervised), TrainingError);
+  }
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
