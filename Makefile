@@ -7,7 +7,7 @@ PKG      := paper_2304_12745_b200
 LIBDIR   := $(PKG)/lib
 OBJDIR   := build/obj
 SRCS_CU  := $(PKG)/csrc/kernels.cu
-SRCS_CPP := $(PKG)/csrc/capi.cpp $(PKG)/csrc/host_gen.cpp $(PKG)/csrc/api.cpp
+SRCS_CPP := $(PKG)/csrc/capi.cpp $(PKG)/csrc/host_gen.cpp $(PKG)/csrc/api.cpp $(PKG)/csrc/dataset_io.cpp
 CXX      ?= g++
 CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -Iinclude -I$(PKG)/csrc -I/usr/local/cuda/include
 OBJS     := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(SRCS_CU)) $(patsubst $(PKG)/csrc/%.cpp,$(OBJDIR)/%.o,$(SRCS_CPP))

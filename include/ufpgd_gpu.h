@@ -50,7 +50,8 @@ enum ufpgd_status {
   UFPGD_ECONVERGENCE = -4, /* ConvergenceError (errors.hpp:27-31) */
   UFPGD_ECUDA = -5,
   UFPGD_ENCCL = -6,
-  UFPGD_ENOTSUP = -7
+  UFPGD_ENOTSUP = -7,
+  UFPGD_EDATAFORMAT = -8 /* DataFormatError (errors.hpp:33-37) */
 };
 
 enum ufpgd_w0_mode {
@@ -211,6 +212,31 @@ int ufpgd_gpu_unfolded_grad(const ufpgd_c64* H, int64_t B, int K, int M, const d
 int ufpgd_gpu_metrics(const ufpgd_c64* H, const ufpgd_c64* W, int64_t B, int K, int M, const double* c,
                       double sigma_nu, double alpha, double* out, ufpgd_c64* Wzf, int device,
                       ufpgd_stream_t stream);
+
+/*
+ * UFPD dataset files — the reference's binary format
+ * (dataset.hpp:23-36, dataset.cpp:38-175): 36-byte little-endian header,
+ * then N row-major K x M matrices of interleaved f64 (re, im), then N labels
+ * when flagged. Errors are UFPGD_EDATAFORMAT (magic, version, dimensions,
+ * truncation, trailing bytes, missing file) with ufpgd_dataset_last_error().
+ *   read_header: host only.
+ *   gpu_ufpd_load: samples [first, first + count) of the channels (which = 0)
+ *     or labels (1) into a DEVICE complex64 batch [count][M][K]; the f64
+ *     payload is streamed through pinned memory and transposed / rounded on
+ *     the device. Synchronous.
+ *   gpu_ufpd_store: write_dataset from DEVICE batches (labels nullable),
+ *     atomically (temp file + rename).
+ *   gpu_convert_f64_rowmajor: the device layout conversion alone
+ *     (to_c64 = 1: f64 [B][K][M][2] -> c64 [B][M][K]; 0: the reverse, src is
+ *     then the f64 destination). Async on `stream`.
+ */
+const char* ufpgd_dataset_last_error(void);
+int ufpgd_ufpd_read_header(const char* path, int* K, int* M, int64_t* N, uint64_t* seed, int* has_labels);
+int ufpgd_gpu_ufpd_load(const char* path, int64_t first, int64_t count, int which, ufpgd_c64* dst, int device);
+int ufpgd_gpu_ufpd_store(const char* path, int K, int M, int64_t N, uint64_t seed, const ufpgd_c64* channels,
+                         const ufpgd_c64* labels, int device);
+int ufpgd_gpu_convert_f64_rowmajor(const double* src, int64_t B, int K, int M, ufpgd_c64* dst, int to_c64,
+                                   int device, ufpgd_stream_t stream);
 
 /*
  * Measurement helper (not a reference interface): FP32 FMA throughput of the

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 from .capi import (  # noqa: F401
     ConvergenceError,
+    DataFormatError,
     DivergenceError,
     UfpgdError,
     W0_CONJ_H,
@@ -40,5 +41,8 @@ from .capi import (  # noqa: F401
     unfolded_forward,
     unfolded_forward_host,
     unfolded_grad,
+    ufpd_header,
+    ufpd_load,
+    ufpd_store,
 )
 from .workloads import CONFIGS, Workload, make_inputs, mp_bound, project_params  # noqa: F401

@@ -16,7 +16,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = os.path.join(_HERE, "lib", "libufpgd_gpu.so")
 
-OK, EINVAL_SHAPE, EINVAL_PARAM, EDIVERGED, ECONVERGENCE, ECUDA, ENCCL, ENOTSUP = 0, -1, -2, -3, -4, -5, -6, -7
+OK, EINVAL_SHAPE, EINVAL_PARAM, EDIVERGED, ECONVERGENCE, ECUDA, ENCCL, ENOTSUP, EDATAFORMAT = (
+    0, -1, -2, -3, -4, -5, -6, -7, -8)
 W0_ZERO, W0_CONJ_H, W0_GIVEN = 0, 1, 2
 
 
@@ -36,6 +37,10 @@ class DivergenceError(RuntimeError):
 
 class ConvergenceError(RuntimeError):
     pass
+
+
+class DataFormatError(RuntimeError):
+    """errors.hpp:33-37 — malformed or truncated dataset file."""
 
 
 _lib = None
@@ -65,6 +70,11 @@ def lib():
             "ufpgd_gpu_unfolded_forward_host": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, P, d, i]),
             "ufpgd_gpu_pgd_fixed_host": (i, [P, i64, i, i, i, d, i64, P, i, P, P, P, P, P, d, i]),
             "ufpgd_gpu_fp32_peak": (i, [i, P, P]),
+            "ufpgd_dataset_last_error": (C.c_char_p, []),
+            "ufpgd_ufpd_read_header": (i, [C.c_char_p, P, P, P, P, P]),
+            "ufpgd_gpu_ufpd_load": (i, [C.c_char_p, i64, i64, i, P, i]),
+            "ufpgd_gpu_ufpd_store": (i, [C.c_char_p, i, i, i64, u64, P, P, i]),
+            "ufpgd_gpu_convert_f64_rowmajor": (i, [P, i64, i, i, P, i, i, P]),
             "ufpgd_gpu_metrics": (i, [P, P, i64, i, i, P, d, d, P, P, i, P]),
             "ufpgd_gpu_unfolded_grad": (i, [P, i64, i, i, P, P, i, P, i, i, d, P, P, P, P, i, P]),
             "ufpgd_gpu_init": (i, [i]),
@@ -336,6 +346,43 @@ def summarize_metrics(out):
         se = {k: float(np.sqrt(((v - mean[k]) ** 2).sum() * scale)) for k, v in cols.items()}
         se["sinr"] = np.sqrt(((o[:, 6:] - mean["sinr"]) ** 2).sum(axis=0) * scale)
     return {"num_channels": n, "mean": mean, "std_error": se}
+
+
+def _check_data(rc):
+    if rc == EDATAFORMAT:
+        raise DataFormatError(lib().ufpgd_dataset_last_error().decode())
+    if rc != OK:
+        msg = lib().ufpgd_dataset_last_error().decode() or lib().ufpgd_gpu_last_error().decode()
+        if rc in (EINVAL_SHAPE, EINVAL_PARAM):
+            raise ValueError(msg)
+        raise UfpgdError(f"ufpgd status {rc}: {msg}")
+
+
+def ufpd_header(path: str) -> dict:
+    """Header of a UFPD dataset file (dataset.hpp:23-33); host only."""
+    K, M, N, seed, lab = C.c_int(), C.c_int(), C.c_int64(), C.c_uint64(), C.c_int()
+    _check_data(lib().ufpgd_ufpd_read_header(path.encode(), C.byref(K), C.byref(M), C.byref(N), C.byref(seed),
+                                             C.byref(lab)))
+    return dict(K=K.value, M=M.value, N=N.value, seed=seed.value, has_labels=bool(lab.value))
+
+
+def ufpd_load(path: str, first: int = 0, count=None, labels: bool = False, device: int = 0):
+    """Samples of a UFPD file as a CUDA complex64 batch [count, M, K]."""
+    import torch
+
+    h = ufpd_header(path)
+    n = h["N"] - first if count is None else count
+    out = torch.empty((n, h["M"], h["K"]), dtype=torch.complex64, device=f"cuda:{device}")
+    _check_data(lib().ufpgd_gpu_ufpd_load(path.encode(), first, n, 1 if labels else 0, _ptr(out), device))
+    return out
+
+
+def ufpd_store(path: str, channels, labels=None, seed: int = 0, device: int = 0):
+    """write_dataset from CUDA complex64 batches [N, M, K] (labels optional)."""
+    N, M, K = channels.shape
+    if labels is not None and tuple(labels.shape) != tuple(channels.shape):
+        raise ValueError("write_dataset: label shape mismatch")
+    _check_data(lib().ufpgd_gpu_ufpd_store(path.encode(), K, M, N, seed, _ptr(channels), _ptr(labels), device))
 
 
 def fp32_peak(device: int = 0):

@@ -1479,6 +1479,50 @@ __global__ void __launch_bounds__(128) row_mean_kernel(const double* __restrict_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Dataset layout conversion: the reference's UFPD payload
+// stores each K x M matrix row-major with interleaved f64 (re, im)
+// (dataset.cpp:38-45, dataset.hpp:28-33); the device batches are complex64
+// [B][M][K]. One CTA per realization transposes through shared memory so both
+// the f64 reads (along m) and the c64 writes (along k) are coalesced. Pure
+// HBM traffic: 16KM bytes in, 8KM out (or the reverse for the writer).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) f64_rowmajor_to_c64_kernel(const double2* __restrict__ src, float2* __restrict__ dst,
+                                                                  int K, int M) {
+  extern __shared__ float2 tsm[];  // [K][M + 1]
+  const long long r = blockIdx.x;
+  const double2* s = src + r * K * M;
+  float2* d = dst + r * K * M;
+  for (int e = threadIdx.x; e < K * M; e += blockDim.x) {
+    const int k = e / M, m = e % M;
+    const double2 v = s[e];
+    tsm[k * (M + 1) + m] = make_float2(__double2float_rn(v.x), __double2float_rn(v.y));
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < K * M; e += blockDim.x) {
+    const int m = e / K, k = e % K;
+    d[e] = tsm[k * (M + 1) + m];
+  }
+}
+
+__global__ void __launch_bounds__(256) c64_to_f64_rowmajor_kernel(const float2* __restrict__ src, double2* __restrict__ dst,
+                                                                  int K, int M) {
+  extern __shared__ float2 tsm[];  // [M][K + 1]
+  const long long r = blockIdx.x;
+  const float2* s = src + r * K * M;
+  double2* d = dst + r * K * M;
+  for (int e = threadIdx.x; e < K * M; e += blockDim.x) {
+    const int m = e / K, k = e % K;
+    tsm[m * (K + 1) + k] = s[e];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < K * M; e += blockDim.x) {
+    const int k = e / M, m = e % M;
+    const float2 v = tsm[m * (K + 1) + k];
+    d[e] = make_double2(v.x, v.y);
+  }
+}
+
 // Standalone fixed-step power iteration, one warp per realization, any shape
 // (H read straight from global memory; it is tiny next to the PGD loop).
 __global__ void __launch_bounds__(128) power_kernel(const __grid_constant__ PowerArgs p) {
@@ -1836,6 +1880,25 @@ cudaError_t launch_grad(const GradArgs& a, double* mean, cudaStream_t s) {
     e = cudaGetLastError();
   }
   return e;
+}
+
+cudaError_t launch_convert(const void* src, void* dst, long long B, int K, int M, bool to_c64, cudaStream_t s) {
+  if (B == 0) return cudaSuccess;
+  const size_t smem = static_cast<size_t>(K + 1) * (M + 1) * sizeof(float2);
+  if (to_c64) {
+    cudaError_t e = cudaFuncSetAttribute(f64_rowmajor_to_c64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    f64_rowmajor_to_c64_kernel<<<static_cast<unsigned>(B), 256, smem, s>>>(static_cast<const double2*>(src),
+                                                                            static_cast<float2*>(dst), K, M);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(c64_to_f64_rowmajor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    c64_to_f64_rowmajor_kernel<<<static_cast<unsigned>(B), 256, smem, s>>>(static_cast<const float2*>(src),
+                                                                            static_cast<double2*>(dst), K, M);
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_stats_finalize(const double* partials, long long n, double* stats, cudaStream_t s) {

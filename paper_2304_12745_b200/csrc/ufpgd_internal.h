@@ -108,6 +108,7 @@ cudaError_t launch_metrics(const float2* H, const float2* W, long long B, int K,
                            double sigma2, double alpha, double* out, float2* Wzf, cudaStream_t s);
 size_t grad_smem_bytes(int K, int M);
 cudaError_t launch_grad(const GradArgs& a, double* mean, cudaStream_t s);
+cudaError_t launch_convert(const void* src, void* dst, long long B, int K, int M, bool to_c64, cudaStream_t s);
 cudaError_t measure_fp32_peak(double* tflops, double* sm_ghz);
 cudaError_t launch_stats_finalize(const double* partials, long long n, double* stats,
                                   cudaStream_t s);
