@@ -153,6 +153,44 @@ int ufpgd_gpu_layers_general(const ufpgd_c64* H, int64_t B, int K, int M, const 
                              float* tape_shrink, int device, ufpgd_stream_t stream);
 
 /*
+ * FP64 twin of ufpgd_gpu_layers_general (all arrays interleaved complex128 /
+ * double, device): the precision path behind the per-channel C++ API, so a
+ * single-channel forward / solve_pgd / pgd_step / grad_f / prox_l21 on the
+ * device reproduces the FP64 reference to rounding. K*M <= ~4500.
+ */
+int ufpgd_gpu_layers_general64(const double* H, int64_t B, int K, int M, const double* eta,
+                               const double* thr, int L, const double* c, int w0_mode,
+                               const double* W0, int mode, double residual_tol, int index_base,
+                               double* W, int32_t* diverged_at, int64_t* iterations,
+                               double* iterates, double* tape_v, double* tape_norms,
+                               double* tape_shrink, int device, ufpgd_stream_t stream);
+
+/*
+ * solve_pgd in FP64 (pgd.cpp:178-268, trace off) over B channels with a
+ * per-realization step eta[B] (device), shared lambda, max_iters and the
+ * iterate-change stop residual_tol (0 disables); W0 (device, nullable ->
+ * H^*). diverged_at[B]: 1-based iteration of the first non-finite step image
+ * (the run stops there), -1 if none. Async on `stream`.
+ */
+int ufpgd_gpu_solve_pgd64(const double* H, int64_t B, int K, int M, const double* c, double lambda,
+                          const double* eta, int64_t max_iters, double residual_tol, const double* W0,
+                          double* W, int64_t* iterations, int32_t* diverged_at, int device,
+                          ufpgd_stream_t stream);
+
+/*
+ * oracle_solve at scale (pgd.cpp:270-279) in FP64 over B
+ * channels (complex128 [B][M][K], device): eta_b = 1 / the converged power
+ * iteration (ufpgd_gpu_lipschitz_exact), PGD from H^* with lambda, at most
+ * max_iters iterations and the per-realization iterate-change stop
+ * residual_tol (the reference uses 1e5 and 1e-10). Outputs (device): W
+ * complex128, eta_out[B] (nullable), iterations[B] (nullable), status[B] =
+ * 0, UFPGD_ECONVERGENCE or UFPGD_EDIVERGED. Synchronous.
+ */
+int ufpgd_gpu_oracle_solve(const double* H, int64_t B, int K, int M, const double* c, double lambda,
+                           int64_t max_iters, double residual_tol, double* W, double* eta_out,
+                           int64_t* iterations, int32_t* status, int device, ufpgd_stream_t stream);
+
+/*
  * Host-buffer (end-to-end) unfolded forward: H, W0, W, diverged_at and stats
  * are HOST pointers. The batch is streamed through the device in chunks with
  * H2D copy, kernel and D2H copy overlapped on separate streams; pageable

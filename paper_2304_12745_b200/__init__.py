@@ -31,6 +31,7 @@ from .capi import (  # noqa: F401
     layers_general,
     lipschitz_exact,
     metrics,
+    oracle_solve,
     summarize_metrics,
     lib,
     lib_path,

@@ -76,6 +76,9 @@ def lib():
             "ufpgd_gpu_ufpd_store": (i, [C.c_char_p, i, i, i64, u64, P, P, i]),
             "ufpgd_gpu_convert_f64_rowmajor": (i, [P, i64, i, i, P, i, i, P]),
             "ufpgd_gpu_metrics": (i, [P, P, i64, i, i, P, d, d, P, P, i, P]),
+            "ufpgd_gpu_layers_general64": (i, [P, i64, i, i, P, P, i, P, i, P, i, d, i, P, P, P, P, P, P, P, i, P]),
+            "ufpgd_gpu_solve_pgd64": (i, [P, i64, i, i, P, d, P, i64, d, P, P, P, P, i, P]),
+            "ufpgd_gpu_oracle_solve": (i, [P, i64, i, i, P, d, i64, d, P, P, P, P, i, P]),
             "ufpgd_gpu_unfolded_grad": (i, [P, i64, i, i, P, P, i, P, i, i, d, P, P, P, P, i, P]),
             "ufpgd_gpu_init": (i, [i]),
             "ufpgd_gpu_shutdown": (i, []),
@@ -383,6 +386,25 @@ def ufpd_store(path: str, channels, labels=None, seed: int = 0, device: int = 0)
     if labels is not None and tuple(labels.shape) != tuple(channels.shape):
         raise ValueError("write_dataset: label shape mismatch")
     _check_data(lib().ufpgd_gpu_ufpd_store(path.encode(), K, M, N, seed, _ptr(channels), _ptr(labels), device))
+
+
+def oracle_solve(H, c, lambda_: float, *, max_iters: int = 100000, residual_tol: float = 1e-10, stream=None):
+    """oracle_solve at scale (pgd.cpp:270-279) in FP64 for a complex128 CUDA
+    batch [B, M, K]: returns dict(W complex128, eta, iterations, status)."""
+    import torch
+
+    if not (isinstance(H, torch.Tensor) and H.is_cuda and H.dtype == torch.complex128 and H.dim() == 3
+            and H.is_contiguous()):
+        raise ValueError("H must be a contiguous CUDA complex128 tensor [B, M, K]")
+    B, M, K = H.shape
+    W = torch.empty_like(H)
+    eta = torch.empty(B, dtype=torch.float64, device=H.device)
+    its = torch.empty(B, dtype=torch.int64, device=H.device)
+    st = torch.empty(B, dtype=torch.int32, device=H.device)
+    _check(lib().ufpgd_gpu_oracle_solve(_ptr(H), B, K, M, _ptr(_f64(c)), float(lambda_), int(max_iters),
+                                        float(residual_tol), _ptr(W), _ptr(eta), _ptr(its), _ptr(st),
+                                        H.device.index or 0, _stream_ptr(stream)))
+    return dict(W=W, eta=eta, iterations=its, status=st)
 
 
 def fp32_peak(device: int = 0):

@@ -110,13 +110,14 @@ void check_projected(const UnfoldedNetwork& net) {  // unfolded.cpp:19-35
   }
 }
 
-// Runs the general-shape layer sweep on one realization.
+// Runs the FP64 general-shape layer sweep on one realization: the reference's
+// own precision, on the device. A ComplexMatrix (col-major complex<double>)
+// is already the kernel's interleaved [M][K] FP64 layout.
 struct LayerRun {
   PrecoderMatrix W;
   int32_t diverged = -1;
   int64_t iterations = 0;
-  std::vector<ufpgd_c64> iterates, tape_v;
-  std::vector<float> tape_norms, tape_shrink;
+  std::vector<double> iterates, tape_v, tape_norms, tape_shrink;
 };
 
 LayerRun run_layers(const ChannelMatrix& H, const RealVector& c, const std::vector<double>& eta,
@@ -126,33 +127,28 @@ LayerRun run_layers(const ChannelMatrix& H, const RealVector& c, const std::vect
   const int L = mode == 1 ? 1 : static_cast<int>(eta.size());
   const std::size_t n = static_cast<std::size_t>(K) * M;
   DeviceScope scope;
-  DeviceBuffer<ufpgd_c64> dH(n), dW(n), dW0(W0 ? n : 0);
+  DeviceBuffer<double> dH(2 * n), dW(2 * n), dW0(W0 ? 2 * n : 0);
   DeviceBuffer<int32_t> ddiv(1);
   DeviceBuffer<int64_t> dits(1);
-  DeviceBuffer<ufpgd_c64> ditr(iterates ? (L + 1) * n : 0), dtv(tape ? L * n : 0);
-  DeviceBuffer<float> dtn(tape ? static_cast<std::size_t>(L) * M : 0), dts(tape ? static_cast<std::size_t>(L) * M : 0);
-  const auto h = to_c64(H);
-  dH.upload(h.data());
-  if (W0) {
-    const auto w0 = to_c64(*W0);
-    dW0.upload(w0.data());
-  }
-  check(ufpgd_gpu_layers_general(dH.p, 1, K, M, eta.data(), thr.data(), L, c.data(), w0_mode, dW0.p, mode,
-                                 residual_tol, index_base, dW.p, ddiv.p, dits.p, ditr.p, dtv.p, dtn.p, dts.p,
-                                 g_device, nullptr));
-  cuda_check(cudaDeviceSynchronize(), "layers_general");
+  DeviceBuffer<double> ditr(iterates ? 2 * (L + 1) * n : 0), dtv(tape ? 2 * L * n : 0);
+  DeviceBuffer<double> dtn(tape ? static_cast<std::size_t>(L) * M : 0), dts(tape ? static_cast<std::size_t>(L) * M : 0);
+  dH.upload(reinterpret_cast<const double*>(H.data()));
+  if (W0) dW0.upload(reinterpret_cast<const double*>(W0->data()));
+  check(ufpgd_gpu_layers_general64(dH.p, 1, K, M, eta.data(), thr.data(), L, c.data(), w0_mode, dW0.p, mode,
+                                   residual_tol, index_base, dW.p, ddiv.p, dits.p, ditr.p, dtv.p, dtn.p, dts.p,
+                                   g_device, nullptr));
+  cuda_check(cudaDeviceSynchronize(), "layers_general64");
   LayerRun r;
-  std::vector<ufpgd_c64> w(n);
-  dW.download(w.data());
-  r.W = from_c64(w.data(), K, M);
+  r.W = ComplexMatrix(K, M);
+  dW.download(reinterpret_cast<double*>(r.W.data()));
   ddiv.download(&r.diverged);
   dits.download(&r.iterations);
   if (iterates) {
-    r.iterates.resize((L + 1) * n);
+    r.iterates.resize(2 * (L + 1) * n);
     ditr.download(r.iterates.data());
   }
   if (tape) {
-    r.tape_v.resize(L * n);
+    r.tape_v.resize(2 * L * n);
     r.tape_norms.resize(static_cast<std::size_t>(L) * M);
     r.tape_shrink.resize(static_cast<std::size_t>(L) * M);
     dtv.download(r.tape_v.data());
@@ -160,6 +156,12 @@ LayerRun run_layers(const ChannelMatrix& H, const RealVector& c, const std::vect
     dts.download(r.tape_shrink.data());
   }
   return r;
+}
+
+ComplexMatrix from_f64(const double* d, std::ptrdiff_t K, std::ptrdiff_t M) {
+  ComplexMatrix A(K, M);
+  std::memcpy(A.data(), d, sizeof(double) * 2 * K * M);
+  return A;
 }
 
 std::uint64_t mix64(std::uint64_t x) {  // rng.cpp:10-15
@@ -325,33 +327,50 @@ PgdResult solve_pgd(const ChannelMatrix& channel, const SystemConfig& cfg, const
     result.precoder = start ? *start : channel.conjugate();
     return result;
   }
-  // The general kernel takes <= UFPGD_MAX_LAYERS (eta, thr) pairs per launch;
-  // longer runs are chained launch by launch from the previous iterate.
-  PrecoderMatrix w = start ? *start : channel.conjugate();
-  long done = 0;
-  while (done < params.max_iters) {
-    const long chunk = std::min<long>(UFPGD_MAX_LAYERS, params.max_iters - done);
-    std::vector<double> eta(static_cast<std::size_t>(chunk), params.eta);
-    std::vector<double> thr(static_cast<std::size_t>(chunk), params.lambda * params.eta);
-    LayerRun r = run_layers(channel, cfg.constraint_diag(), eta, thr, UFPGD_W0_GIVEN, &w, 0, params.residual_tol, 1,
-                            false, false);
-    if (r.diverged >= 0) throw DivergenceError("solve_pgd: non-finite iterate", done + r.diverged);
-    w = r.W;
-    done += r.iterations;
-    if (r.iterations < chunk) break;  // residual_tol stop inside the chunk
-  }
-  result.precoder = w;
-  result.iterations = done;
+  const int K = cfg.K, M = cfg.M;
+  const std::size_t n = static_cast<std::size_t>(K) * M;
+  DeviceScope scope;
+  DeviceBuffer<double> dH(2 * n), dW(2 * n), dW0(start ? 2 * n : 0), deta(1);
+  DeviceBuffer<int32_t> ddiv(1);
+  DeviceBuffer<int64_t> dits(1);
+  dH.upload(reinterpret_cast<const double*>(channel.data()));
+  if (start) dW0.upload(reinterpret_cast<const double*>(start->data()));
+  deta.upload(&params.eta);
+  const RealVector c = cfg.constraint_diag();
+  check(ufpgd_gpu_solve_pgd64(dH.p, 1, K, M, c.data(), params.lambda, deta.p, params.max_iters, params.residual_tol,
+                              start ? dW0.p : nullptr, dW.p, dits.p, ddiv.p, g_device, nullptr));
+  cuda_check(cudaDeviceSynchronize(), "solve_pgd");
+  int32_t div = -1;
+  ddiv.download(&div);
+  if (div >= 0) throw DivergenceError("solve_pgd: non-finite iterate", div);
+  result.precoder = ComplexMatrix(K, M);
+  dW.download(reinterpret_cast<double*>(result.precoder.data()));
+  int64_t its = 0;
+  dits.download(&its);
+  result.iterations = static_cast<long>(its);
   return result;
 }
 
 PrecoderMatrix oracle_solve(const ChannelMatrix& channel, const SystemConfig& cfg, double lambda) {
-  PgdParams params;
-  params.lambda = lambda;
-  params.eta = 1.0 / lipschitz_bound(channel).exact;
-  params.max_iters = 100000;
-  params.residual_tol = 1e-10;
-  return solve_pgd(channel, cfg, params).precoder;
+  check_shapes(channel, cfg);
+  if (!(lambda >= 0.0)) throw std::invalid_argument("PgdParams: lambda must be >= 0");
+  const int K = cfg.K, M = cfg.M;
+  const std::size_t n = static_cast<std::size_t>(K) * M;
+  DeviceScope scope;
+  DeviceBuffer<double> dH(2 * n), dW(2 * n);
+  DeviceBuffer<int32_t> dst(1);
+  dH.upload(reinterpret_cast<const double*>(channel.data()));
+  const RealVector c = cfg.constraint_diag();
+  check(ufpgd_gpu_oracle_solve(dH.p, 1, K, M, c.data(), lambda, 100000, 1e-10, dW.p, nullptr, nullptr, dst.p, g_device,
+                               nullptr));
+  int32_t st = 0;
+  dst.download(&st);
+  if (st == UFPGD_ECONVERGENCE)
+    throw ConvergenceError("lipschitz_bound: power iteration did not reach tolerance 1e-8 within 10000 iterations");
+  if (st == UFPGD_EDIVERGED) throw DivergenceError("solve_pgd: non-finite iterate", -1);
+  ComplexMatrix W(K, M);
+  dW.download(reinterpret_cast<double*>(W.data()));
+  return W;
 }
 
 // ---- unfolded.cpp -------------------------------------------------------------
@@ -423,13 +442,13 @@ ForwardResult forward(const UnfoldedNetwork& net, const ChannelMatrix& channel, 
   result.output = r.W;
   const std::ptrdiff_t K = cfg.K, M = cfg.M, n = K * M;
   if (options.with_iterates)
-    for (int i = 0; i <= L; ++i) result.iterates.push_back(from_c64(r.iterates.data() + i * n, K, M));
+    for (int i = 0; i <= L; ++i) result.iterates.push_back(from_f64(r.iterates.data() + 2 * i * n, K, M));
   if (options.with_tape) {
     result.tape.layers.resize(static_cast<std::size_t>(L));
     for (int i = 0; i < L; ++i) {
       LayerTape& t = result.tape.layers[static_cast<std::size_t>(i)];
-      t.input = from_c64(r.iterates.data() + i * n, K, M);
-      t.step_image = from_c64(r.tape_v.data() + i * n, K, M);
+      t.input = from_f64(r.iterates.data() + 2 * i * n, K, M);
+      t.step_image = from_f64(r.tape_v.data() + 2 * i * n, K, M);
       t.column_norms.resize(M);
       t.shrink_factors.resize(M);
       for (std::ptrdiff_t m = 0; m < M; ++m) {

@@ -547,6 +547,153 @@ int ufpgd_gpu_layers_general(const ufpgd_c64* H, int64_t B, int K, int M, const 
   return UFPGD_OK;
 }
 
+int ufpgd_gpu_layers_general64(const double* H, int64_t B, int K, int M, const double* eta, const double* thr, int L,
+                               const double* c, int w0_mode, const double* W0, int mode, double residual_tol,
+                               int index_base, double* W, int32_t* diverged_at, int64_t* iterations,
+                               double* iterates, double* tape_v, double* tape_norms, double* tape_shrink, int device,
+                               ufpgd_stream_t stream) {
+  int rc;
+  if ((rc = check_shape(B, K, M)) || (rc = check_c(c, K)) || (rc = check_w0(w0_mode, W0))) return rc;
+  if (mode != 0 && mode != 1) return fail(UFPGD_EINVAL_PARAM, "bad mode");
+  if (L < 0 || L > UFPGD_MAX_LAYERS) return fail(UFPGD_EINVAL_PARAM, "layer count out of range");
+  if (mode == 1) L = 1;
+  if (L > 0 && (!eta || !thr)) return fail(UFPGD_EINVAL_PARAM, "eta/thr required");
+  for (int l = 0; l < L; ++l)
+    if (!(eta[l] >= 0.0) || !(thr[l] >= 0.0)) return fail(UFPGD_EINVAL_PARAM, "need eta >= 0, thr >= 0");
+  if (!(residual_tol >= 0.0)) return fail(UFPGD_EINVAL_PARAM, "residual_tol must be >= 0");
+  if (B > 0 && (!H || !W)) return fail(UFPGD_EINVAL_PARAM, "H and W are required");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
+  if (B == 0) return UFPGD_OK;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (general64_smem_bytes(K, M) > static_cast<size_t>(optin)) return fail(UFPGD_ENOTSUP, "(K, M) too large for FP64");
+  GeneralArgs64 a{};
+  a.H = reinterpret_cast<const double2*>(H);
+  a.W = reinterpret_cast<double2*>(W);
+  a.W0 = reinterpret_cast<const double2*>(W0);
+  a.diverged_at = diverged_at;
+  a.iterations = iterations;
+  a.iterates = reinterpret_cast<double2*>(iterates);
+  a.tape_v = reinterpret_cast<double2*>(tape_v);
+  a.tape_norms = tape_norms;
+  a.tape_shrink = tape_shrink;
+  a.B = B;
+  a.K = K;
+  a.M = M;
+  a.L = L;
+  a.w0_mode = w0_mode;
+  a.mode = mode;
+  a.index_base = index_base;
+  a.residual_tol = residual_tol;
+  a.alpha = 1.0;
+  for (int k = 0; k < K; ++k) a.c[k] = c[k];
+  for (int l = 0; l < L; ++l) {
+    a.eta[l] = eta[l];
+    a.thr[l] = thr[l];
+  }
+  cudaError_t e = launch_general64(a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "general FP64 kernel");
+  return UFPGD_OK;
+}
+
+int ufpgd_gpu_solve_pgd64(const double* H, int64_t B, int K, int M, const double* c, double lambda,
+                          const double* eta, int64_t max_iters, double residual_tol, const double* W0, double* W,
+                          int64_t* iterations, int32_t* diverged_at, int device, ufpgd_stream_t stream) {
+  int rc;
+  if ((rc = check_shape(B, K, M)) || (rc = check_c(c, K))) return rc;
+  if (!(lambda >= 0.0)) return fail(UFPGD_EINVAL_PARAM, "PgdParams: lambda must be >= 0");
+  if (max_iters < 0 || !(residual_tol >= 0.0)) return fail(UFPGD_EINVAL_PARAM, "bad PGD parameters");
+  if (B > 0 && (!H || !W || !eta)) return fail(UFPGD_EINVAL_PARAM, "H, eta and W are required");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
+  if (B == 0) return UFPGD_OK;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (general64_smem_bytes(K, M) > static_cast<size_t>(optin)) return fail(UFPGD_ENOTSUP, "(K, M) too large for FP64");
+  GeneralArgs64 a{};
+  a.H = reinterpret_cast<const double2*>(H);
+  a.W = reinterpret_cast<double2*>(W);
+  a.W0 = reinterpret_cast<const double2*>(W0);
+  a.diverged_at = diverged_at;
+  a.iterations = iterations;
+  a.B = B;
+  a.K = K;
+  a.M = M;
+  a.w0_mode = W0 ? UFPGD_W0_GIVEN : UFPGD_W0_CONJ_H;
+  a.pgd = 1;
+  a.iters = max_iters;
+  a.eta_b = eta;
+  a.lambda = lambda;
+  a.index_base = 1;
+  a.residual_tol = residual_tol;
+  a.alpha = 1.0;
+  for (int k = 0; k < K; ++k) a.c[k] = c[k];
+  cudaError_t e = launch_general64(a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "solve_pgd FP64 kernel");
+  return UFPGD_OK;
+}
+
+int ufpgd_gpu_oracle_solve(const double* H, int64_t B, int K, int M, const double* c, double lambda,
+                           int64_t max_iters, double residual_tol, double* W, double* eta_out, int64_t* iterations,
+                           int32_t* status, int device, ufpgd_stream_t stream) {
+  int rc;
+  if ((rc = check_shape(B, K, M)) || (rc = check_c(c, K))) return rc;
+  if (!(lambda >= 0.0)) return fail(UFPGD_EINVAL_PARAM, "PgdParams: lambda must be >= 0");
+  if (max_iters < 0 || !(residual_tol >= 0.0)) return fail(UFPGD_EINVAL_PARAM, "bad PGD parameters");
+  if (B > 0 && (!H || !W || !status)) return fail(UFPGD_EINVAL_PARAM, "H, W and status are required");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
+  if (B == 0) return UFPGD_OK;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (general64_smem_bytes(K, M) > static_cast<size_t>(optin)) return fail(UFPGD_ENOTSUP, "(K, M) too large for FP64");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* lip = nullptr;
+  int32_t* div = nullptr;
+  UFPGD_CUDA(cudaMallocAsync(&lip, sizeof(double) * B, s));
+  UFPGD_CUDA(cudaMallocAsync(&div, sizeof(int32_t) * B, s));
+  // pgd.cpp:270-279: eta = 1 / lipschitz_bound(H).exact (converged, FP64)
+  rc = ufpgd_gpu_lipschitz_exact(H, B, K, M, lip, status, device, stream);
+  if (rc == UFPGD_OK) {
+    GeneralArgs64 a{};
+    a.H = reinterpret_cast<const double2*>(H);
+    a.W = reinterpret_cast<double2*>(W);
+    a.diverged_at = div;
+    a.iterations = iterations;
+    a.B = B;
+    a.K = K;
+    a.M = M;
+    a.w0_mode = UFPGD_W0_CONJ_H;
+    a.pgd = 1;
+    a.iters = max_iters;
+    a.lip_b = lip;
+    a.eta_out = eta_out;
+    a.lambda = lambda;
+    a.index_base = 1;
+    a.residual_tol = residual_tol;
+    a.alpha = 1.0;
+    for (int k = 0; k < K; ++k) a.c[k] = c[k];
+    cudaError_t e = launch_general64(a, s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "oracle_solve kernel");
+  }
+  if (rc == UFPGD_OK) {
+    // fold divergence into status (ECONVERGENCE from the power iteration wins)
+    std::vector<int32_t> hs(static_cast<size_t>(B)), hd(static_cast<size_t>(B));
+    cudaMemcpyAsync(hs.data(), status, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(hd.data(), div, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "oracle_solve");
+    for (int64_t b = 0; b < B && rc == UFPGD_OK; ++b)
+      if (hs[b] == 0 && hd[b] >= 0) hs[b] = UFPGD_EDIVERGED;
+    if (rc == UFPGD_OK) cudaMemcpy(status, hs.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice);
+  }
+  cudaFreeAsync(lip, s);
+  cudaFreeAsync(div, s);
+  cudaStreamSynchronize(s);
+  return rc;
+}
+
 int ufpgd_gpu_unfolded_forward_host(const ufpgd_c64* H, int64_t B, int K, int M,
                                     const double* lambda, const double* eta, int L, const double* c,
                                     int w0_mode, const ufpgd_c64* W0, ufpgd_c64* W,

@@ -934,33 +934,58 @@ __global__ void __launch_bounds__(T::NT) tile_kernel(const __grid_constant__ Fus
 // reference's per-realization helpers (grad_f, prox_l21, pgd_step) and the
 // taped forward (unfolded.cpp:127-143). Exact FP32 sqrt/div in the prox.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float block_sum(float v, float* scratch) {
+template <class T>
+__device__ __forceinline__ T block_sum(T v, T* scratch) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __syncthreads();
   if (lane == 0) scratch[warp] = v;
   __syncthreads();
-  float t = 0.f;
+  T t = 0;
   for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += scratch[q];
   return t;
 }
 
-__global__ void __launch_bounds__(kGenThreads) general_kernel(const __grid_constant__ GeneralArgs p) {
-  extern __shared__ __align__(16) float2 gsm[];
-  __shared__ float scratch[kGenThreads / 32];
+template <class V2, class T>
+__device__ __forceinline__ V2 mk2(T x, T y) {
+  V2 r;
+  r.x = x;
+  r.y = y;
+  return r;
+}
+
+template <class T>
+__device__ __forceinline__ T nan_of();
+template <>
+__device__ __forceinline__ float nan_of<float>() {
+  return __int_as_float(0x7fc00000);
+}
+template <>
+__device__ __forceinline__ double nan_of<double>() {
+  return __longlong_as_double(0x7ff8000000000000LL);
+}
+
+// Generic-precision body: T = float (the general FP32 kernel) or double (the
+// FP64 precision path). Plain loops; serves every shape.
+template <class T>
+__global__ void __launch_bounds__(kGenThreads) general_kernel_t(const __grid_constant__ GeneralArgsT<T> p) {
+  using V2 = typename Vec2<T>::type;
+  extern __shared__ __align__(16) unsigned char gsm_raw[];
+  __shared__ T scratch[kGenThreads / 32];
+  V2* gsm = reinterpret_cast<V2*>(gsm_raw);
   const int K = p.K, M = p.M, n = K * M, tid = threadIdx.x, nt = blockDim.x;
   const long long rid = blockIdx.x;
-  float2* hs = gsm;
-  float2* ws = hs + n;
-  float2* vs = ws + n;
-  float2* xs = vs + n;
-  const float2* hg = p.H + rid * n;
+  V2* hs = gsm;
+  V2* ws = hs + n;
+  V2* vs = ws + n;
+  V2* xs = vs + n;
+  const V2* hg = p.H + rid * n;
   for (int e = tid; e < n; e += nt) {
-    const float2 h = hg[e];
+    const V2 h = hg[e];
     hs[e] = h;
-    ws[e] = p.w0_mode == UFPGD_W0_ZERO ? make_float2(0.f, 0.f)
-            : p.w0_mode == UFPGD_W0_CONJ_H ? make_float2(h.x, -h.y)
+    ws[e] = p.w0_mode == UFPGD_W0_ZERO ? mk2<V2, T>(0, 0)
+            : p.w0_mode == UFPGD_W0_CONJ_H ? mk2<V2, T>(h.x, -h.y)
                                            : p.W0[rid * n + e];
   }
   __syncthreads();
@@ -969,9 +994,9 @@ __global__ void __launch_bounds__(kGenThreads) general_kernel(const __grid_const
 
   int first_bad = -1;
   long long taken = 0;
-  float eta_r = 0.f, thr_r = 0.f;
+  T eta_r = 0, thr_r = 0;
   if (p.pgd) {
-    eta_r = p.eta_b ? p.eta_b[rid] : 1.f / p.lip_b[rid];
+    eta_r = p.eta_b ? p.eta_b[rid] : T(1) / p.lip_b[rid];
     thr_r = p.lambda * eta_r;
     if (p.eta_out && tid == 0) p.eta_out[rid] = eta_r;
   }
@@ -980,43 +1005,55 @@ __global__ void __launch_bounds__(kGenThreads) general_kernel(const __grid_const
     // stage 1: X'(k, j) = sum_m W(k, m) H(j, m) - c_k [k == j]
     for (int o = tid; o < K * K; o += nt) {
       const int k = o % K, j = o / K;
-      float2 acc = make_float2(0.f, 0.f);
-      for (int m = 0; m < M; ++m) cmac(acc, ws[m * K + k], hs[m * K + j]);
-      if (k == j) acc.x -= p.c[k];
-      xs[o] = acc;
+      T ar = 0, ai = 0;
+      for (int m = 0; m < M; ++m) {
+        const V2 a = ws[m * K + k], b = hs[m * K + j];
+        ar = fma(a.x, b.x, ar);
+        ar = fma(-a.y, b.y, ar);
+        ai = fma(a.x, b.y, ai);
+        ai = fma(a.y, b.x, ai);
+      }
+      if (k == j) ar -= p.c[k];
+      xs[o] = mk2<V2, T>(ar, ai);
     }
     __syncthreads();
     // stage 2: G = X' H^*, V = W - eta G
-    const float eta = p.pgd ? eta_r : p.eta[l], thr = p.pgd ? thr_r : p.thr[l];
+    const T eta = p.pgd ? eta_r : p.eta[l], thr = p.pgd ? thr_r : p.thr[l];
     for (int e = tid; e < n; e += nt) {
       const int m = e / K, k = e % K;
-      float2 g = make_float2(0.f, 0.f);
-      for (int j = 0; j < K; ++j) cmac_conj(g, xs[j * K + k], hs[m * K + j]);
+      T gr = 0, gi = 0;
+      for (int j = 0; j < K; ++j) {
+        const V2 a = xs[j * K + k], b = hs[m * K + j];  // a * conj(b)
+        gr = fma(a.x, b.x, gr);
+        gr = fma(a.y, b.y, gr);
+        gi = fma(a.y, b.x, gi);
+        gi = fma(-a.x, b.y, gi);
+      }
       if (p.mode == 1) {
-        p.W[rid * n + e] = g;
+        p.W[rid * n + e] = mk2<V2, T>(gr, gi);
       } else {
-        vs[e] = make_float2(fmaf(-eta, g.x, ws[e].x), fmaf(-eta, g.y, ws[e].y));
+        vs[e] = mk2<V2, T>(fma(-eta, gr, ws[e].x), fma(-eta, gi, ws[e].y));
       }
     }
     if (p.mode == 1) return;
     __syncthreads();
     // prox per antenna (pgd.cpp:85-99, exact sqrt and division)
-    float bad = 0.f, d2 = 0.f, s2 = 0.f;
+    T bad = 0, d2 = 0, s2 = 0;
     for (int m = tid; m < M; m += nt) {
-      float s = 0.f;
+      T s = 0;
       for (int k = 0; k < K; ++k) {
-        const float2 v = vs[m * K + k];
-        if (!isfinite(v.x) || !isfinite(v.y)) bad = 1.f;
-        s = fmaf(v.x, v.x, fmaf(v.y, v.y, s));
+        const V2 v = vs[m * K + k];
+        if (!isfinite(v.x) || !isfinite(v.y)) bad = 1;
+        s = fma(v.x, v.x, fma(v.y, v.y, s));
       }
-      const float nrm = sqrtf(s);
+      const T nrm = sqrt(s);
       const bool on = nrm > thr;
-      const float sh = on ? 1.f - thr / nrm : 0.f;
+      const T sh = on ? T(1) - thr / nrm : T(0);
       for (int k = 0; k < K; ++k) {
-        const float2 v = vs[m * K + k];
-        const float2 wn = on ? make_float2(sh * v.x, sh * v.y) : make_float2(0.f, 0.f);
-        if (p.residual_tol > 0.f) {
-          const float2 wo = ws[m * K + k];
+        const V2 v = vs[m * K + k];
+        const V2 wn = on ? mk2<V2, T>(sh * v.x, sh * v.y) : mk2<V2, T>(0, 0);
+        if (p.residual_tol > T(0)) {
+          const V2 wo = ws[m * K + k];
           d2 += (wn.x - wo.x) * (wn.x - wo.x) + (wn.y - wo.y) * (wn.y - wo.y);
           s2 += wo.x * wo.x + wo.y * wo.y;
         }
@@ -1027,35 +1064,37 @@ __global__ void __launch_bounds__(kGenThreads) general_kernel(const __grid_const
     }
     if (p.tape_v)
       for (int e = tid; e < n; e += nt) p.tape_v[(l * p.B + rid) * n + e] = vs[e];
-    bad = block_sum(bad, scratch);
-    if (bad > 0.f && first_bad < 0) first_bad = static_cast<int>(l);
+    bad = block_sum<T>(bad, scratch);
+    if (bad > T(0) && first_bad < 0) first_bad = static_cast<int>(l);
     taken = l + 1;
     if (p.iterates)
       for (int e = tid; e < n; e += nt) p.iterates[((l + 1) * p.B + rid) * n + e] = ws[e];
-    if (p.residual_tol > 0.f) {
-      d2 = block_sum(d2, scratch);
-      s2 = block_sum(s2, scratch);
-      if (sqrtf(d2) / fmaxf(sqrtf(s2), 1e-12f) < p.residual_tol) break;
+    // solve_pgd stops at the first non-finite step image (pgd.cpp:231-235)
+    if (first_bad >= 0 && p.index_base == 1) break;
+    if (p.residual_tol > T(0)) {
+      d2 = block_sum<T>(d2, scratch);
+      s2 = block_sum<T>(s2, scratch);
+      if (sqrt(d2) / fmax(sqrt(s2), T(1e-12)) < p.residual_tol) break;
     }
     __syncthreads();
   }
   __syncthreads();
   for (int e = tid; e < n; e += nt) p.W[rid * n + e] = ws[e];
   // statistics
-  float l21 = 0.f, act = 0.f;
+  T l21 = 0, act = 0;
   for (int m = tid; m < M; m += nt) {
-    float s = 0.f;
-    for (int k = 0; k < K; ++k) s = fmaf(ws[m * K + k].x, ws[m * K + k].x, fmaf(ws[m * K + k].y, ws[m * K + k].y, s));
-    l21 += sqrtf(s);
-    act += s > 0.f ? 1.f : 0.f;
+    T s = 0;
+    for (int k = 0; k < K; ++k) s = fma(ws[m * K + k].x, ws[m * K + k].x, fma(ws[m * K + k].y, ws[m * K + k].y, s));
+    l21 += sqrt(s);
+    act += s > T(0) ? T(1) : T(0);
   }
-  l21 = block_sum(l21, scratch);
-  act = block_sum(act, scratch);
+  l21 = block_sum<T>(l21, scratch);
+  act = block_sum<T>(act, scratch);
   if (tid == 0) {
     const bool diverged = first_bad >= 0;
     if (p.diverged_at) p.diverged_at[rid] = diverged ? first_bad + p.index_base : -1;
     if (p.iterations) p.iterations[rid] = taken;
-    if (p.l21) p.l21[rid] = diverged ? __int_as_float(0x7fc00000) : l21;
+    if (p.l21) p.l21[rid] = diverged ? nan_of<T>() : l21;
     if (p.active) p.active[rid] = diverged ? -1 : static_cast<int32_t>(act);
     if (p.block_partials) {
       p.block_partials[rid * 3 + 0] = diverged ? 0.0 : static_cast<double>(p.alpha) * l21;
@@ -1779,10 +1818,23 @@ size_t general_smem_bytes(int K, int M) {
 
 cudaError_t launch_general(const GeneralArgs& a, cudaStream_t s) {
   const size_t smem = general_smem_bytes(a.K, a.M);
-  cudaError_t e = cudaFuncSetAttribute(general_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(general_kernel_t<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  general_kernel<<<static_cast<unsigned>(a.B), kGenThreads, smem, s>>>(a);
+  general_kernel_t<float><<<static_cast<unsigned>(a.B), kGenThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+size_t general64_smem_bytes(int K, int M) {
+  return (3ull * K * M + static_cast<size_t>(K) * K) * sizeof(double2);
+}
+
+cudaError_t launch_general64(const GeneralArgs64& a, cudaStream_t s) {
+  const size_t smem = general64_smem_bytes(a.K, a.M);
+  cudaError_t e = cudaFuncSetAttribute(general_kernel_t<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  general_kernel_t<double><<<static_cast<unsigned>(a.B), kGenThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -33,37 +33,55 @@ struct FusedArgs {
   float2 v0[256];         // power-iteration start vector (PGD)
 };
 
-// Arguments of the general-shape kernel (one CTA per realization).
-struct GeneralArgs {
-  const float2* H;
-  float2* W;
-  const float2* W0;
+// Vector type of a real type for the general kernel (FP32 and FP64 builds).
+template <class T>
+struct Vec2;
+template <>
+struct Vec2<float> {
+  using type = float2;
+};
+template <>
+struct Vec2<double> {
+  using type = double2;
+};
+
+// Arguments of the general-shape kernel (one CTA per realization), in FP32
+// (GeneralArgs) or FP64 (GeneralArgs64: the precision path of the
+// per-channel C++ API and of oracle_solve).
+template <class T>
+struct GeneralArgsT {
+  using V2 = typename Vec2<T>::type;
+  const V2* H;
+  V2* W;
+  const V2* W0;
   int32_t* diverged_at;
   int64_t* iterations;
-  float* l21;
+  T* l21;
   int32_t* active;
   double* block_partials;  // [B][3]
-  float2* iterates;
-  float2* tape_v;
-  float* tape_norms;
-  float* tape_shrink;
+  V2* iterates;
+  V2* tape_v;
+  T* tape_norms;
+  T* tape_shrink;
   long long B;
   int K, M, L;
   int w0_mode;
   int mode;         // 0 layers, 1 gradient only
   int pgd;          // 1: every layer uses the realization's own step (below)
   long long iters;  // layer / iteration count when pgd == 1
-  const float* eta_b;  // pgd: per-realization step (nullable -> 1 / lip_b)
-  const float* lip_b;  // pgd: per-realization Lipschitz estimate
-  float* eta_out;      // pgd: step used (nullable)
-  float lambda;        // pgd: thr = lambda * eta
+  const T* eta_b;   // pgd: per-realization step (nullable -> 1 / lip_b)
+  const T* lip_b;   // pgd: per-realization Lipschitz estimate
+  T* eta_out;       // pgd: step used (nullable)
+  T lambda;         // pgd: thr = lambda * eta
   int index_base;   // 0: layer index, 1: 1-based iteration
-  float residual_tol;
-  float alpha;
-  float c[UFPGD_MAX_USERS];
-  float eta[UFPGD_MAX_LAYERS];
-  float thr[UFPGD_MAX_LAYERS];
+  T residual_tol;
+  T alpha;
+  T c[UFPGD_MAX_USERS];
+  T eta[UFPGD_MAX_LAYERS];
+  T thr[UFPGD_MAX_LAYERS];
 };
+using GeneralArgs = GeneralArgsT<float>;
+using GeneralArgs64 = GeneralArgsT<double>;
 
 // Arguments of the training-gradient kernel (one CTA per realization).
 struct GradArgs {
@@ -100,6 +118,8 @@ cudaError_t launch_fused(const FusedArgs& a, bool pgd, int K, int M, cudaStream_
                          long long* nblocks);
 size_t general_smem_bytes(int K, int M);
 cudaError_t launch_general(const GeneralArgs& a, cudaStream_t s);
+cudaError_t launch_general64(const GeneralArgs64& a, cudaStream_t s);
+size_t general64_smem_bytes(int K, int M);
 cudaError_t launch_power(const PowerArgs& a, cudaStream_t s);
 cudaError_t launch_lipschitz_exact(const double2* H, long long B, int K, int M, const double2* v0,
                                    double* Lout, int32_t* status, cudaStream_t s);
