@@ -14,7 +14,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB = os.path.join(_HERE, "lib", "libufpgd_gpu.so")
+# UFPGD_LIB overrides the library path (A/B builds of the same ABI in tools/).
+_LIB = os.environ.get("UFPGD_LIB") or os.path.join(_HERE, "lib", "libufpgd_gpu.so")
 
 OK, EINVAL_SHAPE, EINVAL_PARAM, EDIVERGED, ECONVERGENCE, ECUDA, ENCCL, ENOTSUP, EDATAFORMAT = (
     0, -1, -2, -3, -4, -5, -6, -7, -8)

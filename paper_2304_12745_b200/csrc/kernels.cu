@@ -196,64 +196,84 @@ __device__ __forceinline__ void team_stage1(const float2 (&wr)[S::MB][S::P], con
 // One layer (or PGD iteration). STAGE1: also build X' for the next layer.
 // STATS: accumulate ||W||_{2,1} and the active count for this thread's
 // antennas (counted on the a == 0 threads only).
+// Antennas processed together per step of the layer loop (their stage-2
+// contractions, norm shuffles and prox tails are independent). Measured on
+// B200: 1 and 2 run at the same speed (ptxas already interleaves antennas of
+// the unrolled loop), and 2 spills a few registers, so 1.
+#ifndef UFPGD_TEAM_AB
+#define UFPGD_TEAM_AB 1
+#endif
+
 template <class S, bool STAGE1, bool STATS>
 __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&wi)[S::MB][S::P], XAcc<S>& x,
                                            const float* hs, int a, int b, float eta, float thr,
                                            const float2 (&cdiag)[S::P], bool& nonfinite, float& l21,
                                            int& act) {
+  constexpr int AB = (S::MB % UFPGD_TEAM_AB == 0) ? UFPGD_TEAM_AB : 1;
   XAcc<S> xn;
   if (STAGE1) xacc_init<S>(xn, cdiag, a);
   const float thr2 = thr * thr;
 #pragma unroll
-  for (int i = 0; i < S::MB; ++i) {
-    float2 h[S::K];
-    load_col<S>(hs, i * S::TM + b, h);
-    // stage 2: G(k, m) = sum_j X'(k, j) conj(H(j, m)); V = W - eta G
-    float2 vr[S::P], vi[S::P];
-    float2 s2 = zero2();
+  for (int i0 = 0; i0 < S::MB; i0 += AB) {
+    float2 h[AB][S::K];
+    float2 vr[AB][S::P], vi[AB][S::P];
+    float s[AB];
 #pragma unroll
-    for (int p = 0; p < S::P; ++p) {
-      float2 gr0 = zero2(), gr1 = zero2(), gi0 = zero2(), gi1 = zero2();
+    for (int u = 0; u < AB; ++u) {
+      const int i = i0 + u;
+      load_col<S>(hs, i * S::TM + b, h[u]);
+      // stage 2: G(k, m) = sum_j X'(k, j) conj(H(j, m)); V = W - eta G
+      float2 s2 = zero2();
 #pragma unroll
-      for (int j = 0; j < S::K; j += 2) {
-        gr0 = ffma2(h[j].x, x.re[p][j], gr0);
-        gr0 = ffma2(h[j].y, x.im[p][j], gr0);
-        gi0 = ffma2(h[j].x, x.im[p][j], gi0);
-        gi0 = ffma2(-h[j].y, x.re[p][j], gi0);
-        gr1 = ffma2(h[j + 1].x, x.re[p][j + 1], gr1);
-        gr1 = ffma2(h[j + 1].y, x.im[p][j + 1], gr1);
-        gi1 = ffma2(h[j + 1].x, x.im[p][j + 1], gi1);
-        gi1 = ffma2(-h[j + 1].y, x.re[p][j + 1], gi1);
+      for (int p = 0; p < S::P; ++p) {
+        float2 gr0 = zero2(), gr1 = zero2(), gi0 = zero2(), gi1 = zero2();
+#pragma unroll
+        for (int j = 0; j < S::K; j += 2) {
+          gr0 = ffma2(h[u][j].x, x.re[p][j], gr0);
+          gr0 = ffma2(h[u][j].y, x.im[p][j], gr0);
+          gi0 = ffma2(h[u][j].x, x.im[p][j], gi0);
+          gi0 = ffma2(-h[u][j].y, x.re[p][j], gi0);
+          gr1 = ffma2(h[u][j + 1].x, x.re[p][j + 1], gr1);
+          gr1 = ffma2(h[u][j + 1].y, x.im[p][j + 1], gr1);
+          gi1 = ffma2(h[u][j + 1].x, x.im[p][j + 1], gi1);
+          gi1 = ffma2(-h[u][j + 1].y, x.re[p][j + 1], gi1);
+        }
+        vr[u][p] = ffma2(-eta, fadd2(gr0, gr1), wr[i][p]);
+        vi[u][p] = ffma2(-eta, fadd2(gi0, gi1), wi[i][p]);
+        s2 = __ffma2_rn(vr[u][p], vr[u][p], s2);
+        s2 = __ffma2_rn(vi[u][p], vi[u][p], s2);
       }
-      vr[p] = ffma2(-eta, fadd2(gr0, gr1), wr[i][p]);
-      vi[p] = ffma2(-eta, fadd2(gi0, gi1), wi[i][p]);
-      s2 = __ffma2_rn(vr[p], vr[p], s2);
-      s2 = __ffma2_rn(vi[p], vi[p], s2);
+      s[u] = s2.x + s2.y;
     }
-    float s = s2.x + s2.y;
     // ||v_m||^2 across the TK threads holding antenna m
 #pragma unroll
-    for (int off = S::TM; off < S::T; off <<= 1) s += __shfl_xor_sync(kFull, s, off);
-    // Non-finite step image (unfolded.cpp:120-125): any NaN/Inf entry of
-    // v_m makes its squared column norm NaN/Inf. (A finite column whose
-    // squared norm overflows FP32, |v| > ~6e18, is flagged too.)
-    nonfinite |= !(s <= FLT_MAX);
-    // prox (pgd.cpp:85-99): strict ||v|| > t, i.e. s > t^2
-    const bool on = s > thr2;
-    const float r = rsqrtf(s);
-    const float scale = on ? fmaf(-thr, r, 1.f) : 0.f;
+    for (int off = S::TM; off < S::T; off <<= 1)
 #pragma unroll
-    for (int p = 0; p < S::P; ++p) {
-      wr[i][p] = fmul2(scale, vr[p]);
-      wi[i][p] = fmul2(scale, vi[p]);
-    }
-    if (STATS) {
-      if (a == 0 && on) {
-        l21 += fmaf(s, r, -thr);  // ||w_m|| = ||v_m|| - t
-        act += 1;
+      for (int u = 0; u < AB; ++u) s[u] += __shfl_xor_sync(kFull, s[u], off);
+#pragma unroll
+    for (int u = 0; u < AB; ++u) {
+      const int i = i0 + u;
+      // Non-finite step image (unfolded.cpp:120-125): any NaN/Inf entry of
+      // v_m makes its squared column norm NaN/Inf. (A finite column whose
+      // squared norm overflows FP32, |v| > ~6e18, is flagged too.)
+      nonfinite |= !(s[u] <= FLT_MAX);
+      // prox (pgd.cpp:85-99): strict ||v|| > t, i.e. s > t^2
+      const bool on = s[u] > thr2;
+      const float r = rsqrtf(s[u]);
+      const float scale = on ? fmaf(-thr, r, 1.f) : 0.f;
+#pragma unroll
+      for (int p = 0; p < S::P; ++p) {
+        wr[i][p] = fmul2(scale, vr[u][p]);
+        wi[i][p] = fmul2(scale, vi[u][p]);
       }
+      if (STATS) {
+        if (a == 0 && on) {
+          l21 += fmaf(s[u], r, -thr);  // ||w_m|| = ||v_m|| - t
+          act += 1;
+        }
+      }
+      if (STAGE1) stage1_accumulate<S>(xn, wr[i], wi[i], h[u]);
     }
-    if (STAGE1) stage1_accumulate<S>(xn, wr[i], wi[i], h);
   }
   if (STAGE1) allreduce<S>(xn, x);
 }
