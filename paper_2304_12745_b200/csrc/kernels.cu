@@ -526,6 +526,11 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
 // (split, [j][k]) live in shared memory with padded strides (odd numbers of
 // 16-byte units between consecutive rows: conflict-free LDS.128 phases).
 // ---------------------------------------------------------------------------
+#ifndef UFPGD_TILE_UNROLL
+#define UFPGD_TILE_UNROLL 1
+#endif
+constexpr int kTileUnroll = UFPGD_TILE_UNROLL;  // stage-2 j-loop unroll (A/B builds)
+
 template <int K_, int M_, int NW_, int TA_>
 struct Tile {
   static constexpr int K = K_, M = M_, NW = NW_, NT = 32 * NW_, TA = TA_;
@@ -535,8 +540,8 @@ struct Tile {
   static constexpr int XT = (K / 8) * (K / 8);  // 8 x 8 tiles of X'
   static constexpr int S = NT / XT;          // antenna slices of stage 1
   static constexpr int MS = M / S;           // antennas per slice
-  static constexpr int HSTR = 2 * K + 4;     // floats
-  static constexpr int WSTR = K + 4;
+  static constexpr int HSTR = 2 * K;         // floats, unpadded (XOR-swizzled units)
+  static constexpr int WSTR = K;
   static constexpr int XSTR = K + 4;
   static constexpr int OFF_H = 0;
   static constexpr int OFF_WR = OFF_H + M * HSTR;
@@ -550,7 +555,16 @@ struct Tile {
   static_assert(RG * AG == NT, "stage-2 tiles must cover V exactly");
   static_assert(NT % XT == 0 && XT <= 32 && 32 % XT == 0, "stage-1 tiles within a warp");
   static_assert(M % S == 0, "");
-  static_assert((HSTR / 4) % 2 == 1 && (WSTR / 4) % 2 == 1, "odd 16-byte strides");
+  static_assert(K >= 16 && 8 % RG == 0, "swizzles assume >= 8 H units per row");
+  // H(c, m): 16-byte unit (c >> 1) of row m, XOR-swizzled by m mod (8 / RG):
+  // the 8 / RG antenna rows a stage-2 LDS.128 phase touches land on
+  // distinct banks (rows are 8 units = one bank period apart otherwise).
+  static __device__ __forceinline__ int hsw(int m) { return m & (8 / RG - 1); }
+  static __device__ __forceinline__ int hoff(int m, int c) { return m * HSTR + 4 * ((c >> 1) ^ hsw(m)) + 2 * (c & 1); }
+  // W planes: unit (k >> 2) of row m, bit 0 XOR-ed with ((m * K / 4) >> 3) & 1
+  // so the two rows whose bases coincide mod 8 units flip unit parity.
+  static __device__ __forceinline__ int wsw(int m) { return ((m * (K / 4)) >> 3) & 1; }
+  static __device__ __forceinline__ int woff(int m, int k) { return m * WSTR + 4 * ((k >> 2) ^ wsw(m)) + (k & 3); }
 };
 
 template <int NW>
@@ -581,18 +595,18 @@ __device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid) 
 #pragma unroll 2
   for (int i = 0; i < T::MS; ++i) {
     const int m = i * T::S + s;
-    const float4* wrp = reinterpret_cast<const float4*>(Wre + m * T::WSTR + tr * 8);
-    const float4* wip = reinterpret_cast<const float4*>(Wim + m * T::WSTR + tr * 8);
-    const float4 a0 = wrp[0], a1 = wrp[1], b0 = wip[0], b1 = wip[1];
+    const float4 a0 = *reinterpret_cast<const float4*>(Wre + T::woff(m, tr * 8));
+    const float4 a1 = *reinterpret_cast<const float4*>(Wre + T::woff(m, tr * 8 + 4));
+    const float4 b0 = *reinterpret_cast<const float4*>(Wim + T::woff(m, tr * 8));
+    const float4 b1 = *reinterpret_cast<const float4*>(Wim + T::woff(m, tr * 8 + 4));
     const float2 wr[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w), make_float2(a1.x, a1.y),
                           make_float2(a1.z, a1.w)};
     const float2 wi[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
                           make_float2(b1.z, b1.w)};
-    const float4* hp = reinterpret_cast<const float4*>(Hs + m * T::HSTR + tc * 16);
     float2 h[8];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float4 v = hp[q];
+      const float4 v = *reinterpret_cast<const float4*>(Hs + T::hoff(m, tc * 8 + 2 * q));
       h[2 * q] = make_float2(v.x, v.y);
       h[2 * q + 1] = make_float2(v.z, v.w);
     }
@@ -690,7 +704,7 @@ __device__ __forceinline__ void tile_stage2(float* sm, int tid, float eta, float
       gr[q][i] = zero2();
       gi[q][i] = zero2();
     }
-#pragma unroll 1
+#pragma unroll kTileUnroll
   for (int j = 0; j < T::K; j += 2) {
     float2 xr[2][4], xi[2][4];
 #pragma unroll
@@ -710,7 +724,7 @@ __device__ __forceinline__ void tile_stage2(float* sm, int tid, float eta, float
 #pragma unroll
     for (int i = 0; i < T::TA; ++i) {
       const int m = i * T::AG + ag;
-      const float4 h = *reinterpret_cast<const float4*>(Hs + m * T::HSTR + 2 * j);
+      const float4 h = *reinterpret_cast<const float4*>(Hs + T::hoff(m, j));
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         // G(k, m) += X'(k, j) conj(H(j, m)) for j and j + 1
@@ -729,9 +743,11 @@ __device__ __forceinline__ void tile_stage2(float* sm, int tid, float eta, float
 #pragma unroll
   for (int i = 0; i < T::TA; ++i) {
     const int m = i * T::AG + ag;
-    float4* wrp = reinterpret_cast<float4*>(Wre + m * T::WSTR + k0);
-    float4* wip = reinterpret_cast<float4*>(Wim + m * T::WSTR + k0);
-    const float4 a0 = wrp[0], a1 = wrp[1], b0 = wip[0], b1 = wip[1];
+    float4* wr0 = reinterpret_cast<float4*>(Wre + T::woff(m, k0));
+    float4* wr1 = reinterpret_cast<float4*>(Wre + T::woff(m, k0 + 4));
+    float4* wi0 = reinterpret_cast<float4*>(Wim + T::woff(m, k0));
+    float4* wi1 = reinterpret_cast<float4*>(Wim + T::woff(m, k0 + 4));
+    const float4 a0 = *wr0, a1 = *wr1, b0 = *wi0, b1 = *wi1;
     const float2 wr[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w), make_float2(a1.x, a1.y),
                           make_float2(a1.z, a1.w)};
     const float2 wi[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
@@ -756,10 +772,10 @@ __device__ __forceinline__ void tile_stage2(float* sm, int tid, float eta, float
       vr[q] = fmul2(scale, vr[q]);
       vi[q] = fmul2(scale, vi[q]);
     }
-    wrp[0] = make_float4(vr[0].x, vr[0].y, vr[1].x, vr[1].y);
-    wrp[1] = make_float4(vr[2].x, vr[2].y, vr[3].x, vr[3].y);
-    wip[0] = make_float4(vi[0].x, vi[0].y, vi[1].x, vi[1].y);
-    wip[1] = make_float4(vi[2].x, vi[2].y, vi[3].x, vi[3].y);
+    *wr0 = make_float4(vr[0].x, vr[0].y, vr[1].x, vr[1].y);
+    *wr1 = make_float4(vr[2].x, vr[2].y, vr[3].x, vr[3].y);
+    *wi0 = make_float4(vi[0].x, vi[0].y, vi[1].x, vi[1].y);
+    *wi1 = make_float4(vi[2].x, vi[2].y, vi[3].x, vi[3].y);
     if (STATS && rg == 0 && on) {
       l21 += fmaf(s, r, -thr);
       act += 1;
@@ -784,7 +800,7 @@ __device__ float tile_power(float* sm, const float2* v0, int steps, int tid) {
     for (int j = tid; j < T::K; j += T::NT) {  // u = H^* v
       float2 acc = zero2();
       for (int m = 0; m < T::M; ++m) {
-        const float2 h = *reinterpret_cast<const float2*>(Hs + m * T::HSTR + 2 * j);
+        const float2 h = *reinterpret_cast<const float2*>(Hs + T::hoff(m, j));
         cmac(acc, make_float2(h.x, -h.y), v[m]);
       }
       u[j] = acc;
@@ -798,7 +814,7 @@ __device__ float tile_power(float* sm, const float2* v0, int steps, int tid) {
       float2 acc = zero2();
       if (m < T::M) {
         for (int j = 0; j < T::K; ++j)
-          cmac(acc, *reinterpret_cast<const float2*>(Hs + m * T::HSTR + 2 * j), u[j]);
+          cmac(acc, *reinterpret_cast<const float2*>(Hs + T::hoff(m, j)), u[j]);
         dot = fmaf(v[m].x, acc.x, fmaf(v[m].y, acc.y, dot));
         wn2 = fmaf(acc.x, acc.x, fmaf(acc.y, acc.y, wn2));
       }
@@ -854,7 +870,7 @@ __global__ void __launch_bounds__(T::NT) tile_kernel(const __grid_constant__ Fus
   for (int q = tid; q < NV; q += T::NT) {
     const float4 v = ldg_stream(hg + q);
     const int e = 2 * q;
-    *reinterpret_cast<float4*>(sm + T::OFF_H + (e / T::K) * T::HSTR + 2 * (e % T::K)) = v;
+    *reinterpret_cast<float4*>(sm + T::OFF_H + T::hoff(e / T::K, e % T::K)) = v;
   }
   cta_sync<T::NW>();
   // W0 into the split planes
@@ -862,13 +878,13 @@ __global__ void __launch_bounds__(T::NT) tile_kernel(const __grid_constant__ Fus
     const int m = e / T::K, k = e % T::K;
     float2 w = zero2();
     if (p.w0_mode == UFPGD_W0_CONJ_H) {
-      const float2 h = *reinterpret_cast<const float2*>(sm + T::OFF_H + m * T::HSTR + 2 * k);
+      const float2 h = *reinterpret_cast<const float2*>(sm + T::OFF_H + T::hoff(m, k));
       w = make_float2(h.x, -h.y);
     } else if (p.w0_mode == UFPGD_W0_GIVEN) {
       w = p.W0[rid * T::M * T::K + e];
     }
-    sm[T::OFF_WR + m * T::WSTR + k] = w.x;
-    sm[T::OFF_WI + m * T::WSTR + k] = w.y;
+    sm[T::OFF_WR + T::woff(m, k)] = w.x;
+    sm[T::OFF_WI + T::woff(m, k)] = w.y;
   }
   float eta_b = 0.f, thr_b = 0.f;
   if (PGD) {
@@ -931,8 +947,8 @@ __global__ void __launch_bounds__(T::NT) tile_kernel(const __grid_constant__ Fus
   float2* wg = p.W + rid * T::M * T::K;
   for (int e = tid; e < T::M * T::K / 2; e += T::NT) {
     const int m = (2 * e) / T::K, k = (2 * e) % T::K;
-    const float* wr = sm + T::OFF_WR + m * T::WSTR + k;
-    const float* wi = sm + T::OFF_WI + m * T::WSTR + k;
+    const float* wr = sm + T::OFF_WR + T::woff(m, k);  // k even: k, k + 1 share a unit
+    const float* wi = sm + T::OFF_WI + T::woff(m, k);
     stg_stream(reinterpret_cast<float4*>(wg) + e, make_float4(wr[0], wi[0], wr[1], wi[1]));
   }
   if (tid == 0) {
