@@ -295,6 +295,18 @@ int ufpgd_generate_channels(uint64_t seed_h, uint64_t seed_g, double gain_range_
                             int64_t first_index, int64_t B, int K, int M, ufpgd_c64* H,
                             int threads);
 
+/*
+ * The same draw on the DEVICE (for million-realization
+ * runs): DEVICE output [B][M][K], complex64 (out_f64 = 0; H is ufpgd_c64*) or
+ * interleaved FP64 (out_f64 = 1; H is double*, the reference's precision
+ * before rounding). The mt19937_64 integer streams are bit-identical to the
+ * host's; FP64 entries agree to a few ulp (CUDA log/sincos/pow vs glibc).
+ * K <= UFPGD_MAX_USERS. Async on `stream`.
+ */
+int ufpgd_gpu_generate_channels(uint64_t seed_h, uint64_t seed_g, double gain_range_db,
+                                int64_t first_index, int64_t B, int K, int M, void* H, int out_f64,
+                                int device, ufpgd_stream_t stream);
+
 /* The reference's power-iteration start vector (pgd.cpp:131-134), FP64 -> c64,
  * and in FP64 (interleaved re, im). */
 int ufpgd_power_v0(int M, ufpgd_c64* v0);

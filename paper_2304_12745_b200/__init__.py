@@ -27,6 +27,7 @@ from .capi import (  # noqa: F401
     shutdown_multi_gpu,
     unfolded_forward_sharded,
     generate_channels,
+    generate_channels_device,
     layer_params,
     layers_general,
     lipschitz_exact,

@@ -87,6 +87,7 @@ def lib():
             "ufpgd_gpu_lipschitz_exact": (i, [P, i64, i, i, P, P, i, P]),
             "ufpgd_power_v0_f64": (i, [i, P]),
             "ufpgd_generate_channels": (i, [u64, u64, d, i64, i64, i, i, P, i]),
+            "ufpgd_gpu_generate_channels": (i, [u64, u64, d, i64, i64, i, i, P, i, i, P]),
             "ufpgd_power_v0": (i, [i, P]),
             "ufpgd_layer_params": (i, [u64, i, i, i, P, P]),
         }
@@ -450,6 +451,26 @@ def generate_channels(seed_h: int, seed_g: int, gain_range_db: float, first_inde
     H = out if out is not None else np.empty((B, M, K), dtype=np.complex64)
     rc = lib().ufpgd_generate_channels(seed_h, seed_g, float(gain_range_db), first_index, B, K, M, _ptr(H),
                                        threads)
+    _check(rc)
+    return H
+
+
+def generate_channels_device(seed_h: int, seed_g: int, gain_range_db: float, first_index: int, B: int, K: int,
+                             M: int, *, dtype=None, device: int = 0, out=None, stream=None):
+    """The same seeded draw generated on the device:
+    a CUDA tensor [B, M, K], complex64 (default) or complex128. Async on
+    ``stream``; bit-identical integer streams, FP64 entries within a few ulp of
+    the host draw (CUDA log/sincos vs glibc)."""
+    import torch
+
+    dt = dtype if dtype is not None else torch.complex64
+    if dt not in (torch.complex64, torch.complex128):
+        raise ValueError("dtype must be complex64 or complex128")
+    H = out if out is not None else torch.empty((B, M, K), dtype=dt, device=f"cuda:{device}")
+    if out is not None and not (H.is_cuda and H.dtype == dt and tuple(H.shape) == (B, M, K) and H.is_contiguous()):
+        raise ValueError("out must be a contiguous CUDA tensor [B, M, K] of the requested dtype")
+    rc = lib().ufpgd_gpu_generate_channels(seed_h, seed_g, float(gain_range_db), first_index, B, K, M, _ptr(H),
+                                           int(dt == torch.complex128), H.device.index or 0, _stream_ptr(stream))
     _check(rc)
     return H
 

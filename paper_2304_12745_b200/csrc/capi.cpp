@@ -862,6 +862,22 @@ int ufpgd_gpu_unfolded_grad(const ufpgd_c64* H, int64_t B, int K, int M, const d
   return UFPGD_OK;
 }
 
+int ufpgd_gpu_generate_channels(uint64_t seed_h, uint64_t seed_g, double gain_range_db, int64_t first_index,
+                                int64_t B, int K, int M, void* H, int out_f64, int device, ufpgd_stream_t stream) {
+  int rc;
+  if ((rc = check_shape(B, K, M))) return rc;
+  if (!(gain_range_db >= 0.0) || !std::isfinite(gain_range_db))
+    return fail(UFPGD_EINVAL_PARAM, "gain_range_db must be finite and >= 0");
+  if (first_index < 0) return fail(UFPGD_EINVAL_PARAM, "first_index must be >= 0");
+  if (B > 0 && !H) return fail(UFPGD_EINVAL_PARAM, "H is required");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
+  const cudaError_t e = launch_channel_gen(seed_h, seed_g, gain_range_db, first_index, B, K, M, H, out_f64 != 0,
+                                           static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "channel generation kernel");
+  return UFPGD_OK;
+}
+
 int ufpgd_gpu_fp32_peak(int device, double* tflops, double* sm_ghz) {
   if (!tflops || !sm_ghz) return fail(UFPGD_EINVAL_PARAM, "null output");
   DeviceGuard g(device);

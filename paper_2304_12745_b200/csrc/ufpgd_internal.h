@@ -128,6 +128,8 @@ cudaError_t launch_metrics(const float2* H, const float2* W, long long B, int K,
                            double sigma2, double alpha, double* out, float2* Wzf, cudaStream_t s);
 size_t grad_smem_bytes(int K, int M);
 cudaError_t launch_grad(const GradArgs& a, double* mean, cudaStream_t s);
+cudaError_t launch_channel_gen(unsigned long long seed_h, unsigned long long seed_g, double gain_range_db,
+                               long long first_index, long long B, int K, int M, void* H, bool f64, cudaStream_t s);
 cudaError_t launch_convert(const void* src, void* dst, long long B, int K, int M, bool to_c64, cudaStream_t s);
 cudaError_t measure_fp32_peak(double* tflops, double* sm_ghz);
 cudaError_t launch_stats_finalize(const double* partials, long long n, double* stats,

@@ -32,7 +32,21 @@ def t_pgd(n=4096):
     fl = w.flops_per_realization() * n
     print(f"cfg3 B={n}: {ms:.3f} ms  {n/ms*1e3/1e3:.2f} k precoders/s  {fl/ms/1e9:.2f} TFLOP/s", flush=True)
 
+def t_gen(cfg):
+    w = U.CONFIGS[cfg]
+    n = w.B if cfg != 5 else 65536
+    Hd = torch.empty((n, w.M, w.K), dtype=torch.complex64, device="cuda")
+    U.generate_channels_device(w.seed_h, w.seed_g, w.gain_db, 0, n, w.K, w.M, out=Hd); torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(); U.generate_channels_device(w.seed_h, w.seed_g, w.gain_db, 0, n, w.K, w.M, out=Hd); e.record()
+    torch.cuda.synchronize(); ms = s.elapsed_time(e)
+    t0 = time.time(); U.make_inputs(w, 0, n); th = time.time() - t0
+    print(f"gen cfg{cfg} B={n}: device {ms:.3f} ms ({n/ms*1e3/1e6:.2f} M realizations/s), host {th*1e3:.0f} ms", flush=True)
+
 if __name__ == "__main__":
+    if sys.argv[1:2] == ["gen"]:
+        for c in (1, 2, 3, 4, 5): t_gen(c)
+        sys.exit(0)
     for c in [int(x) for x in (sys.argv[1:] or ["1", "2", "4"])]:
         if c == 3: t_pgd()
         elif c == 5: t_uf(5, reps=2, n=int(os.environ.get("CFG5_B", "65536")))
