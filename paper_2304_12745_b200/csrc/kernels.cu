@@ -69,6 +69,16 @@ __device__ __forceinline__ void cmac_conj(float2& acc, float2 a, float2 b) {
   acc.y = fmaf(-a.x, b.y, acc.y);
 }
 
+// Timing-only ablations for development (results are wrong when set):
+// bit 0 drops the X' all-reduce shuffles, bit 1 the column-norm shuffles.
+#ifndef UFPGD_ABL
+#define UFPGD_ABL 0
+#endif
+// Independent accumulation chains per stage-2 output pair (4 or 8).
+#ifndef UFPGD_S2CH
+#define UFPGD_S2CH 4
+#endif
+
 template <int K_, int M_, int TK_, int TM_>
 struct Team {
   static constexpr int K = K_, M = M_, TK = TK_, TM = TM_;
@@ -104,6 +114,13 @@ __device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) { return __
 __device__ __forceinline__ float2 fmul2(float a, float2 b) { return __fmul2_rn(bc(a), b); }
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 zero2() { return make_float2(0.f, 0.f); }
+// MUFU.RSQ without the subnormal-range fix-up rsqrtf() adds (same accuracy
+// for normal inputs; callers clamp the argument to >= FLT_MIN).
+__device__ __forceinline__ float rsqrt_ftz(float v) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
 
 // Loads row m of H (all K users, complex) from shared memory.
 template <class S>
@@ -113,6 +130,33 @@ __device__ __forceinline__ void load_col(const float* hs, int m, float2 (&h)[S::
 #pragma unroll
   for (int q = 0; q < S::K / 2; ++q) {
     const float4 t = hp[q ^ f];
+    h[2 * q] = make_float2(t.x, t.y);
+    h[2 * q + 1] = make_float2(t.z, t.w);
+  }
+}
+
+// Per-thread H row pointers: with TM even, the unit swizzle of antenna
+// m = i * TM + b splits into a compile-time part (from i) XOR a per-thread part
+// (from b), so u[q] = row b, unit q ^ swz_b, and column i, unit q is
+// u[q ^ swz_i] + i * TM * HS: an immediate offset from one of U registers, no
+// per-load address arithmetic in the unrolled layer loop.
+template <class S>
+struct ColPtr {
+  const float* u[S::U];
+  __device__ __forceinline__ ColPtr(const float* hs, int b) {
+    const int fb = S::U >= 4 ? (b >> 1) & (S::U - 1) : 0;
+#pragma unroll
+    for (int q = 0; q < S::U; ++q) u[q] = hs + b * S::HS + 4 * (q ^ fb);
+  }
+};
+
+template <class S>
+__device__ __forceinline__ void load_col(const ColPtr<S>& cp, int i, float2 (&h)[S::K]) {
+  static_assert(S::TM % 2 == 0, "swizzle split needs an even TM");
+  const int ci = S::U >= 4 ? (i * (S::TM / 2)) & (S::U - 1) : 0;  // folds: i is unrolled
+#pragma unroll
+  for (int q = 0; q < S::U; ++q) {
+    const float4 t = *reinterpret_cast<const float4*>(cp.u[q ^ ci] + i * S::TM * S::HS);
     h[2 * q] = make_float2(t.x, t.y);
     h[2 * q + 1] = make_float2(t.z, t.w);
   }
@@ -150,7 +194,7 @@ __device__ __forceinline__ void allreduce(XAcc<S>& xn, XAcc<S>& x) {
     for (int j = 0; j < S::K; ++j) {
       float2 r = xn.re[p][j], i = xn.im[p][j];
 #pragma unroll
-      for (int off = 1; off < S::TM; off <<= 1) {
+      for (int off = 1; off < ((UFPGD_ABL & 1) ? 1 : S::TM); off <<= 1) {
         const float2 ro = make_float2(__shfl_xor_sync(kFull, r.x, off), __shfl_xor_sync(kFull, r.y, off));
         const float2 io = make_float2(__shfl_xor_sync(kFull, i.x, off), __shfl_xor_sync(kFull, i.y, off));
         r = fadd2(r, ro);
@@ -184,10 +228,11 @@ __device__ __forceinline__ void team_stage1(const float2 (&wr)[S::MB][S::P], con
                                             const float2 (&cdiag)[S::P]) {
   XAcc<S> xn;
   xacc_init<S>(xn, cdiag, a);
+  const ColPtr<S> cp(hs, b);
 #pragma unroll
   for (int i = 0; i < S::MB; ++i) {
     float2 h[S::K];
-    load_col<S>(hs, i * S::TM + b, h);
+    load_col<S>(cp, i, h);
     stage1_accumulate<S>(xn, wr[i], wi[i], h);
   }
   allreduce<S>(xn, x);
@@ -213,6 +258,16 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
   XAcc<S> xn;
   if (STAGE1) xacc_init<S>(xn, cdiag, a);
   const float thr2 = thr * thr;
+  const ColPtr<S> cp(hs, b);
+  // Fold the step into X' once per layer (X' <- -eta X'), so each antenna's
+  // stage-2 chains start from W and V = W - eta G needs no extra FFMA2.
+#pragma unroll
+  for (int p = 0; p < S::P; ++p)
+#pragma unroll
+    for (int j = 0; j < S::K; ++j) {
+      x.re[p][j] = fmul2(-eta, x.re[p][j]);
+      x.im[p][j] = fmul2(-eta, x.im[p][j]);
+    }
 #pragma unroll
   for (int i0 = 0; i0 < S::MB; i0 += AB) {
     float2 h[AB][S::K];
@@ -221,12 +276,30 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
 #pragma unroll
     for (int u = 0; u < AB; ++u) {
       const int i = i0 + u;
-      load_col<S>(hs, i * S::TM + b, h[u]);
+      load_col<S>(cp, i, h[u]);
       // stage 2: G(k, m) = sum_j X'(k, j) conj(H(j, m)); V = W - eta G
       float2 s2 = zero2();
 #pragma unroll
       for (int p = 0; p < S::P; ++p) {
-        float2 gr0 = zero2(), gr1 = zero2(), gi0 = zero2(), gi1 = zero2();
+        float2 gr0 = wr[i][p], gr1 = zero2(), gi0 = wi[i][p], gi1 = zero2();
+#if UFPGD_S2CH == 8
+        float2 gr2 = zero2(), gr3 = zero2(), gi2 = zero2(), gi3 = zero2();
+#pragma unroll
+        for (int j = 0; j < S::K; j += 2) {
+          gr0 = ffma2(h[u][j].x, x.re[p][j], gr0);
+          gr2 = ffma2(h[u][j].y, x.im[p][j], gr2);
+          gi0 = ffma2(h[u][j].x, x.im[p][j], gi0);
+          gi2 = ffma2(-h[u][j].y, x.re[p][j], gi2);
+          gr1 = ffma2(h[u][j + 1].x, x.re[p][j + 1], gr1);
+          gr3 = ffma2(h[u][j + 1].y, x.im[p][j + 1], gr3);
+          gi1 = ffma2(h[u][j + 1].x, x.im[p][j + 1], gi1);
+          gi3 = ffma2(-h[u][j + 1].y, x.re[p][j + 1], gi3);
+        }
+        gr0 = fadd2(gr0, gr2);
+        gr1 = fadd2(gr1, gr3);
+        gi0 = fadd2(gi0, gi2);
+        gi1 = fadd2(gi1, gi3);
+#else
 #pragma unroll
         for (int j = 0; j < S::K; j += 2) {
           gr0 = ffma2(h[u][j].x, x.re[p][j], gr0);
@@ -238,8 +311,9 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
           gi1 = ffma2(h[u][j + 1].x, x.im[p][j + 1], gi1);
           gi1 = ffma2(-h[u][j + 1].y, x.re[p][j + 1], gi1);
         }
-        vr[u][p] = ffma2(-eta, fadd2(gr0, gr1), wr[i][p]);
-        vi[u][p] = ffma2(-eta, fadd2(gi0, gi1), wi[i][p]);
+#endif
+        vr[u][p] = fadd2(gr0, gr1);
+        vi[u][p] = fadd2(gi0, gi1);
         s2 = __ffma2_rn(vr[u][p], vr[u][p], s2);
         s2 = __ffma2_rn(vi[u][p], vi[u][p], s2);
       }
@@ -247,7 +321,7 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
     }
     // ||v_m||^2 across the TK threads holding antenna m
 #pragma unroll
-    for (int off = S::TM; off < S::T; off <<= 1)
+    for (int off = S::TM; off < ((UFPGD_ABL & 2) ? S::TM : S::T); off <<= 1)
 #pragma unroll
       for (int u = 0; u < AB; ++u) s[u] += __shfl_xor_sync(kFull, s[u], off);
 #pragma unroll
@@ -259,7 +333,7 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
       nonfinite |= !(s[u] <= FLT_MAX);
       // prox (pgd.cpp:85-99): strict ||v|| > t, i.e. s > t^2
       const bool on = s[u] > thr2;
-      const float r = rsqrtf(s[u]);
+      const float r = rsqrt_ftz(fmaxf(s[u], FLT_MIN));  // s = 0 or subnormal only matters at thr = 0
       const float scale = on ? fmaf(-thr, r, 1.f) : 0.f;
 #pragma unroll
       for (int p = 0; p < S::P; ++p) {
@@ -523,8 +597,9 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
 //     antenna slices, reduced with shuffles within the warp and through shared
 //     memory across warps.
 // H, W (split into re / im planes so FFMA2 operand pairs load directly) and X'
-// (split, [j][k]) live in shared memory with padded strides (odd numbers of
-// 16-byte units between consecutive rows: conflict-free LDS.128 phases).
+// (split, [j][k]) live in shared memory; H and W rows are unpadded with their
+// 16-byte units XOR-swizzled per row (Tile::hoff / woff) so the LDS.128 /
+// STS.128 phases of both stages are conflict-free.
 // ---------------------------------------------------------------------------
 #ifndef UFPGD_TILE_UNROLL
 #define UFPGD_TILE_UNROLL 1

@@ -15,10 +15,13 @@ def t_uf(cfg, reps=10, n=None):
     for _ in range(3): U.unfolded_forward(Hd, lam, eta, w.c, out=W)
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(reps): U.unfolded_forward(Hd, lam, eta, w.c, out=W)
-    e.record(); torch.cuda.synchronize()
-    ms = s.elapsed_time(e) / reps
+    best = float("inf")
+    for _ in range(int(os.environ.get("QT_ROUNDS", "5"))):  # best of rounds: robust to box noise
+        s.record()
+        for _ in range(reps): U.unfolded_forward(Hd, lam, eta, w.c, out=W)
+        e.record(); torch.cuda.synchronize()
+        best = min(best, s.elapsed_time(e) / reps)
+    ms = best
     fl = w.flops_per_realization() * w.B
     print(f"cfg{cfg} B={w.B}: {ms:.3f} ms/batch  {w.B/ms*1e3/1e6:.2f} M precoders/s  {fl/ms/1e9:.2f} TFLOP/s  (gen {tg:.1f}s)", flush=True)
 
