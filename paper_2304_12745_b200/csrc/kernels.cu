@@ -653,7 +653,7 @@ __device__ __forceinline__ void cta_sync() {
 // Stage 1: X'(k, j) = sum_m W(k, m) H(j, m) - c_k [k == j], written to the
 // split X' planes (Xre/Xim[j][k]).
 template <class T>
-__device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid) {
+__device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid, float neta) {
   const int t = tid % T::XT, s = tid / T::XT;
   const int tr = t % (T::K / 8), tc = t / (T::K / 8);
   float2 xr[4][8], xi[4][8];
@@ -707,12 +707,14 @@ __device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid) 
         xi[q][j] = fadd2(xi[q][j], make_float2(__shfl_xor_sync(kFull, xi[q][j].x, off),
                                                __shfl_xor_sync(kFull, xi[q][j].y, off)));
       }
+  // The consuming layer's step is folded in here: the stored X' is
+  // -eta (W H^T - diag c), so stage 2 accumulates V = W - eta G directly.
   float* Xre = sm + T::OFF_XR;
   float* Xim = sm + T::OFF_XI;
   const int lane = tid & 31, warp = tid >> 5;
   if (T::NW > 1) {
-    // cross-warp: lanes < XT of each warp publish their tile, then threads of
-    // warp 0 sum the NW partials in fixed order.
+    // cross-warp: lanes < XT of each warp publish their tile; then every
+    // thread of the CTA sums a strip of the NW partials in fixed warp order.
     float* part = sm + T::OFF_XP + warp * 2 * T::K * T::K;
     if (lane < T::XT) {
 #pragma unroll
@@ -725,24 +727,25 @@ __device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid) 
         }
     }
     __syncthreads();
-    if (warp == 0 && lane < T::XT) {
+    constexpr int NE = T::K * T::K / 2;  // float2 entries per plane
+    static_assert(NE % T::NT == 0, "reduction strips must tile the planes");
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+    for (int r = 0; r < NE / T::NT; ++r) {
+      const int e = tid + r * T::NT;
+      const int jj = e / (T::K / 2), k0 = 2 * (e % (T::K / 2));
+      float2 re = zero2(), im = zero2();
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int k0 = tr * 8 + 2 * q, jj = tc * 8 + j;
-          float2 r = zero2(), im = zero2();
-          for (int w = 0; w < T::NW; ++w) {
-            const float* pw = sm + T::OFF_XP + w * 2 * T::K * T::K;
-            r = fadd2(r, *reinterpret_cast<const float2*>(pw + jj * T::K + k0));
-            im = fadd2(im, *reinterpret_cast<const float2*>(pw + T::K * T::K + jj * T::K + k0));
-          }
-          xr[q][j] = r;
-          xi[q][j] = im;
-        }
+      for (int w = 0; w < T::NW; ++w) {
+        const float* pw = sm + T::OFF_XP + w * 2 * T::K * T::K;
+        re = fadd2(re, *reinterpret_cast<const float2*>(pw + jj * T::K + k0));
+        im = fadd2(im, *reinterpret_cast<const float2*>(pw + T::K * T::K + jj * T::K + k0));
+      }
+      if (k0 == jj) re.x -= c[jj];
+      if (k0 + 1 == jj) re.y -= c[jj];
+      *reinterpret_cast<float2*>(Xre + jj * T::XSTR + k0) = fmul2(neta, re);
+      *reinterpret_cast<float2*>(Xim + jj * T::XSTR + k0) = fmul2(neta, im);
     }
-  }
-  if (warp == 0 && lane < T::XT) {
+  } else if (warp == 0 && lane < T::XT) {
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -753,8 +756,8 @@ __device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid) 
           if (2 * q == j) r.x -= c[jj];
           if (2 * q + 1 == j) r.y -= c[jj];
         }
-        *reinterpret_cast<float2*>(Xre + jj * T::XSTR + k0) = r;
-        *reinterpret_cast<float2*>(Xim + jj * T::XSTR + k0) = xi[q][j];
+        *reinterpret_cast<float2*>(Xre + jj * T::XSTR + k0) = fmul2(neta, r);
+        *reinterpret_cast<float2*>(Xim + jj * T::XSTR + k0) = fmul2(neta, xi[q][j]);
       }
   }
   cta_sync<T::NW>();
@@ -764,6 +767,7 @@ __device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid) 
 template <class T, bool STATS>
 __device__ __forceinline__ void tile_stage2(float* sm, int tid, float eta, float thr, bool& nonfinite,
                                             float& l21, int& act) {
+  (void)eta;  // folded into X' by tile_stage1
   const int rg = tid % T::RG, ag = tid / T::RG;
   const int k0 = rg * 8;
   const float* Hs = sm + T::OFF_H;
@@ -771,14 +775,24 @@ __device__ __forceinline__ void tile_stage2(float* sm, int tid, float eta, float
   float* Wim = sm + T::OFF_WI;
   const float* Xre = sm + T::OFF_XR;
   const float* Xim = sm + T::OFF_XI;
+  // Accumulators start at W (X' arrives scaled by -eta): they end as V.
   float2 gr[4][T::TA], gi[4][T::TA];
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int i = 0; i < T::TA; ++i) {
-      gr[q][i] = zero2();
-      gi[q][i] = zero2();
-    }
+  for (int i = 0; i < T::TA; ++i) {
+    const int m = i * T::AG + ag;
+    const float4 a0 = *reinterpret_cast<const float4*>(Wre + T::woff(m, k0));
+    const float4 a1 = *reinterpret_cast<const float4*>(Wre + T::woff(m, k0 + 4));
+    const float4 b0 = *reinterpret_cast<const float4*>(Wim + T::woff(m, k0));
+    const float4 b1 = *reinterpret_cast<const float4*>(Wim + T::woff(m, k0 + 4));
+    gr[0][i] = make_float2(a0.x, a0.y);
+    gr[1][i] = make_float2(a0.z, a0.w);
+    gr[2][i] = make_float2(a1.x, a1.y);
+    gr[3][i] = make_float2(a1.z, a1.w);
+    gi[0][i] = make_float2(b0.x, b0.y);
+    gi[1][i] = make_float2(b0.z, b0.w);
+    gi[2][i] = make_float2(b1.x, b1.y);
+    gi[3][i] = make_float2(b1.z, b1.w);
+  }
 #pragma unroll kTileUnroll
   for (int j = 0; j < T::K; j += 2) {
     float2 xr[2][4], xi[2][4];
@@ -822,16 +836,11 @@ __device__ __forceinline__ void tile_stage2(float* sm, int tid, float eta, float
     float4* wr1 = reinterpret_cast<float4*>(Wre + T::woff(m, k0 + 4));
     float4* wi0 = reinterpret_cast<float4*>(Wim + T::woff(m, k0));
     float4* wi1 = reinterpret_cast<float4*>(Wim + T::woff(m, k0 + 4));
-    const float4 a0 = *wr0, a1 = *wr1, b0 = *wi0, b1 = *wi1;
-    const float2 wr[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w), make_float2(a1.x, a1.y),
-                          make_float2(a1.z, a1.w)};
-    const float2 wi[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
-                          make_float2(b1.z, b1.w)};
     float2 vr[4], vi[4], s2 = zero2();
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      vr[q] = ffma2(-eta, gr[q][i], wr[q]);
-      vi[q] = ffma2(-eta, gi[q][i], wi[q]);
+      vr[q] = gr[q][i];
+      vi[q] = gi[q][i];
       s2 = __ffma2_rn(vr[q], vr[q], s2);
       s2 = __ffma2_rn(vi[q], vi[q], s2);
     }
@@ -840,7 +849,7 @@ __device__ __forceinline__ void tile_stage2(float* sm, int tid, float eta, float
     for (int off = 1; off < T::RG; off <<= 1) s += __shfl_xor_sync(kFull, s, off);
     nonfinite |= !(s <= FLT_MAX);
     const bool on = s > thr2;
-    const float r = rsqrtf(s);
+    const float r = rsqrt_ftz(fmaxf(s, FLT_MIN));
     const float scale = on ? fmaf(-thr, r, 1.f) : 0.f;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -972,12 +981,12 @@ __global__ void __launch_bounds__(T::NT) tile_kernel(const __grid_constant__ Fus
   if (p.w0_mode == UFPGD_W0_ZERO) {
     for (int e = tid; e < T::K * T::K; e += T::NT) {
       const int j = e / T::K, k = e % T::K;
-      sm[T::OFF_XR + j * T::XSTR + k] = k == j ? -p.c[k] : 0.f;
+      sm[T::OFF_XR + j * T::XSTR + k] = k == j ? (PGD ? eta_b : p.eta[0]) * p.c[k] : 0.f;  // -eta0 (-diag c)
       sm[T::OFF_XI + j * T::XSTR + k] = 0.f;
     }
     cta_sync<T::NW>();
   } else {
-    tile_stage1<T>(sm, p.c, tid);
+    tile_stage1<T>(sm, p.c, tid, -(PGD ? eta_b : p.eta[0]));
   }
   bool nonfinite = false;
   long long first_bad = -1;
@@ -988,7 +997,7 @@ __global__ void __launch_bounds__(T::NT) tile_kernel(const __grid_constant__ Fus
     const float thr = PGD ? thr_b : p.thr[l];
     if (l + 1 < p.L) {
       tile_stage2<T, false>(sm, tid, eta, thr, nonfinite, l21, act);
-      tile_stage1<T>(sm, p.c, tid);
+      tile_stage1<T>(sm, p.c, tid, -(PGD ? eta_b : p.eta[l + 1]));
     } else {
       tile_stage2<T, true>(sm, tid, eta, thr, nonfinite, l21, act);
     }
