@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -228,6 +229,13 @@ cudaError_t ensure(void*& p, size_t& cap, size_t need) {
 
 // Chunked host pipeline shared by the unfolded and PGD host entry points.
 // `run` enqueues the kernel for one chunk on stream s given device buffers.
+// Pipeline chunk size in bytes of H (UFPGD_HOST_CHUNK_MB overrides, for tuning).
+long long host_chunk_bytes(long long default_mb) {
+  long long mb = default_mb;
+  if (const char* v = std::getenv("UFPGD_HOST_CHUNK_MB")) mb = std::max(1LL, std::atoll(v));
+  return mb << 20;
+}
+
 template <class Run>
 int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const ufpgd_c64* W0,
                   ufpgd_c64* W, int32_t* diverged_at, float* eta_out, long long parts_per_chunk_max,
@@ -708,7 +716,7 @@ int ufpgd_gpu_unfolded_forward_host(const ufpgd_c64* H, int64_t B, int K, int M,
   if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
   const bool fused = fused_supported(K, M) && L >= 1;
   // 16 MiB of H per chunk: short pipeline fill, chunks still fill the GPU.
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, (16ll << 20) / (8ll * K * M)));
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, host_chunk_bytes(16) / (8ll * K * M)));
   const long long ppc = partial_count(chunk, K, M, fused);
   return host_pipeline(
       device, H, B, K, M, w0_mode == UFPGD_W0_GIVEN ? W0 : nullptr, W, diverged_at, nullptr, ppc, chunk, stats,
