@@ -1,0 +1,73 @@
+"""Edge cases of the batched path on the GPU against the FP64 oracle: ragged
+and tiny batches on every kernel shape, the extreme layer counts, shapes the
+specialised kernels do not cover (general kernel), and a host batch that does
+not fill its last pipeline chunk."""
+import numpy as np
+import pytest
+
+import paper_2304_12745_b200 as U
+from oracle import oracle as O
+from _parity import assert_parity, report
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def params(K, M, L, seed=5):
+    lam, eta = U.layer_params(seed, L, K, M)
+    return U.project_params(lam, eta, K, M)
+
+
+@pytest.mark.parametrize("K,M", [(4, 32), (8, 64), (16, 128), (32, 256)])
+@pytest.mark.parametrize("B", [1, 2, 3, 17])
+def test_ragged_batches_every_kernel_shape(K, M, B):
+    H = U.generate_channels(77, 78, 10.0, 3, B, K, M)
+    lam, eta = params(K, M, 20)
+    c = np.full(K, np.sqrt(10.0))
+    for mode in (U.W0_ZERO, U.W0_CONJ_H):
+        g = U.unfolded_forward(dev(H), lam, eta, c, w0_mode=mode, want_per_realization=True)
+        ora = O.forward_batch_f32(H, c, lam, eta, w0_mode=mode)
+        rep = report(H, g["W"].cpu().numpy(), ora, c, 1.0 / 15.0)
+        assert_parity(rep)
+        assert np.array_equal(g["active"].cpu().numpy(), ora["active"])
+        assert np.all(g["diverged_at"].cpu().numpy() == -1)
+
+
+@pytest.mark.parametrize("K,M", [(8, 64), (16, 128)])
+def test_single_layer_and_zero_layers(K, M):
+    H = U.generate_channels(3, 4, 0.0, 0, 9, K, M)
+    c = np.full(K, np.sqrt(10.0))
+    lam, eta = params(K, M, 1)
+    g = U.unfolded_forward(dev(H), lam, eta, c, w0_mode=U.W0_CONJ_H)["W"].cpu().numpy()
+    ora = O.forward_batch_f32(H, c, lam, eta, w0_mode=U.W0_CONJ_H)
+    assert_parity(report(H, g, ora, c, 1.0 / 15.0))
+    # zero layers: forward returns the start point (unfolded.cpp:96, loop body never runs)
+    W0 = np.conj(H).astype(np.complex64)
+    z = U.unfolded_forward(dev(H), [], [], c, w0_mode=U.W0_GIVEN, W0=dev(W0))["W"].cpu().numpy()
+    assert np.array_equal(z, W0)
+
+
+@pytest.mark.parametrize("K,M", [(5, 40), (2, 3), (12, 12)])
+def test_shapes_outside_the_specialised_kernels(K, M):
+    H = U.generate_channels(11, 12, 0.0, 0, 6, K, M)
+    lam, eta = params(K, M, 20)
+    c = np.full(K, np.sqrt(10.0))
+    g = U.unfolded_forward(dev(H), lam, eta, c, w0_mode=U.W0_CONJ_H, want_per_realization=True)
+    ora = O.forward_batch_f32(H, c, lam, eta, w0_mode=U.W0_CONJ_H)
+    assert_parity(report(H, g["W"].cpu().numpy(), ora, c, 1.0 / 15.0))
+    assert np.array_equal(g["active"].cpu().numpy(), ora["active"])
+
+
+def test_host_batch_with_partial_last_chunk_matches_device_path():
+    w = U.CONFIGS[2]
+    B = (16 << 20) // (8 * w.K * w.M) + 37  # one full 16 MiB chunk plus a ragged tail
+    H = U.make_inputs(w, 123, B)
+    lam, eta = w.layer_params()
+    host = U.unfolded_forward_host(H, lam, eta, w.c, w0_mode=w.w0_mode)
+    devw = U.unfolded_forward(dev(H), lam, eta, w.c, w0_mode=w.w0_mode)
+    assert np.array_equal(host["W"], devw["W"].cpu().numpy())
+    assert np.allclose(host["stats"], devw["stats"].cpu().numpy(), rtol=1e-12)
