@@ -129,6 +129,15 @@ def reference_rate(w, H, lam, eta, steps, warmup, threads):
     return steps * len(H) / (time.perf_counter() - t0)
 
 
+def clamped_layers(w):
+    """Layers whose raw step mu_l was clamped by project_params (SURVEY §8d asks for the count)."""
+    import paper_2304_12745_b200 as U
+
+    raw_lam, raw_eta = U.layer_params(w.seed_p, w.L, w.K, w.M)
+    _, eta = U.project_params(raw_lam, raw_eta, w.K, w.M)
+    return int(np.count_nonzero(eta != raw_eta))
+
+
 def cpu_baseline(w, H, lam, eta, seconds):
     from oracle import oracle as O
 
@@ -141,7 +150,14 @@ def cpu_baseline(w, H, lam, eta, seconds):
         O.forward_batch_f32(sample, w.c, lam, eta, w0_mode=w.w0_mode, threads=threads, want_W=False)
         done += n
     rate = done / (time.perf_counter() - t0)
-    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+    # the same port on one core (SURVEY §8d asks for both), over a ~2 s sample
+    one = sample[:256]
+    done1, t1 = 0, time.perf_counter()
+    while time.perf_counter() - t1 < min(2.0, seconds):
+        O.forward_batch_f32(one, w.c, lam, eta, w0_mode=w.w0_mode, threads=1, want_W=False)
+        done1 += len(one)
+    rate1 = done1 / (time.perf_counter() - t1)
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "single_core_value": rate1,
             "sample": f"{done} realizations ({n} distinct of the rank-0 cfg{w.config} batch, repeated for "
                       f">= {seconds:g} s): FP64 C++ restatement of unfolded.cpp:83-146 forward, "
                       f"restated parallel_for (parallel.cpp:25-59) over {threads} threads"}
@@ -337,7 +353,8 @@ def run_ours(args, world, rank, local):
                        "M": w.M, "layers": w.L, "w0": "zero", "parallelism": f"dp{world} (independent shards, "
                        "NCCL all-reduce of 3 statistics per step)" if world > 1 else "single GPU",
                        "l2": f"inputs larger than L2: H = {w.B * elem / 2**20:.0f} MiB per GPU > 126 MB L2; no flush",
-                       "seeds": {"h": w.seed_h, "g": w.seed_g, "p": w.seed_p}},
+                       "seeds": {"h": w.seed_h, "g": w.seed_g, "p": w.seed_p},
+                       "layers_eta_clamped_by_projection": clamped_layers(w)},
             "roofline": {
                 "bound": "fp32", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
                 "frac": achieved / peak_tflops, "traffic": load_traffic(w),
