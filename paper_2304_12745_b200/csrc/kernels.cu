@@ -79,9 +79,11 @@ __device__ __forceinline__ void cmac_conj(float2& acc, float2 a, float2 b) {
 #define UFPGD_S2CH 4
 #endif
 
-template <int K_, int M_, int TK_, int TM_>
+template <int K_, int M_, int TK_, int TM_, int MAXT_ = 256, int MINB_ = 1>
 struct Team {
   static constexpr int K = K_, M = M_, TK = TK_, TM = TM_;
+  // launch bounds: register cap = 64K / (MAXT * MINB)
+  static constexpr int MAXT = MAXT_, MINB = MINB_;
   static constexpr int T = TK * TM;     // threads per realization
   static constexpr int R = 32 / T;      // realizations per warp
   static constexpr int KA = K / TK;     // users per thread
@@ -1980,8 +1982,13 @@ int pick_warps(int rpw, long long B) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  for (int nw = 8; nw > 1; nw >>= 1)
-    if ((B + static_cast<long long>(nw) * rpw - 1) / (static_cast<long long>(nw) * rpw) >= sms) return nw;
+  // Measured on B200 (tools/nw_sweep.py, quick_time): with many waves 4-warp
+  // blocks beat 8-warp ones by ~2% (a finished block's slot refills sooner);
+  // with under ~4 waves (config 3: 1.7) whole-SM 8-warp blocks are ~2% ahead.
+  const auto blocks = [&](int nw) { return (B + static_cast<long long>(nw) * rpw - 1) / (static_cast<long long>(nw) * rpw); };
+  if (blocks(8) >= sms && blocks(8) < 4LL * sms) return 8;
+  for (int nw = 4; nw > 1; nw >>= 1)
+    if (blocks(nw) >= sms) return nw;
   return 1;
 }
 
@@ -2019,12 +2026,13 @@ __global__ void __launch_bounds__(256) fp32_peak_kernel(const float* __restrict_
 
 template <class S>
 cudaError_t launch_team(const FusedArgs& a, bool pgd, cudaStream_t s, long long* nblocks) {
-  auto kern = pgd ? fused_kernel<S, true, 256, 1> : fused_kernel<S, false, 256, 1>;
+  auto kern = pgd ? fused_kernel<S, true, S::MAXT, S::MINB> : fused_kernel<S, false, S::MAXT, S::MINB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kFusedMaxWarps * S::SMEM_PER_WARP);
   if (e != cudaSuccess) return e;
   int nw = pick_warps(S::R, a.B);
   if (const char* f = std::getenv("UFPGD_FUSED_WARPS")) nw = std::max(1, std::min(8, std::atoi(f)));
+  nw = std::min(nw, S::MAXT / 32);
   const long long rpb = static_cast<long long>(nw) * S::R;
   const long long blocks = (a.B + rpb - 1) / rpb;
   if (nblocks) *nblocks = blocks;
@@ -2048,7 +2056,13 @@ using Tile_32_256 = Tile<32, 256, 4, 8>;
 // Team shapes (K, M) -> (TK, TM): KA = K/TK = 2 users and MB = M/TM antennas
 // per thread keep W, X' and the next X' in registers.
 using Team_4_32 = Team<4, 32, 2, 4>;
-using Team_8_64 = Team<8, 64, 4, 4>;
+#ifndef UFPGD_T864_MAXT
+#define UFPGD_T864_MAXT 256
+#endif
+#ifndef UFPGD_T864_MINB
+#define UFPGD_T864_MINB 1
+#endif
+using Team_8_64 = Team<8, 64, 4, 4, UFPGD_T864_MAXT, UFPGD_T864_MINB>;
 
 }  // namespace
 
