@@ -11,6 +11,7 @@
 #include "ufpgd/metrics.hpp"
 #include "ufpgd/pgd.hpp"
 #include "ufpgd/system_config.hpp"
+#include "ufpgd/training.hpp"
 #include "ufpgd/unfolded.hpp"
 
 namespace ufpgd {
@@ -47,7 +48,7 @@ BatchResult forward_batch_multi_gpu(const UnfoldedNetwork& net, const std::compl
 // the device: taped forward from H^*, loss, loss gradient, backward, then the
 // deterministic batch mean. grads are packed (d_lambda_0, d_eta_0, ...) as
 // pack_params orders them (training.hpp:50-51), ready for adam_update.
-enum class LossKind { Unsupervised = 0, Supervised = 1 };
+// (LossKind and EvaluationSummary are declared in ufpgd/training.hpp.)
 
 struct TrainGradients {
   double loss = 0.0;          // batch mean loss
@@ -58,15 +59,9 @@ TrainGradients train_gradients(const UnfoldedNetwork& net, const std::complex<fl
                                const SystemConfig& cfg, LossKind kind = LossKind::Unsupervised,
                                double lambda_cost = 1.0 / 15.0, const std::complex<float>* labels = nullptr);
 
-// evaluate (training.cpp:310-421) without per-layer curves: forward on every
-// channel, device metrics, means and standard errors at the final layer.
-struct EvaluationSummary {
-  MetricsReport mean;
-  MetricsReport std_error;
-  std::size_t num_channels = 0;
-  long singular = 0;  // channels whose ZF reference is singular (the reference throws)
-};
-
+// evaluate (training.cpp:310-421) over a stacked complex<float> batch without
+// per-layer curves: singular channels are counted in `singular` and skipped
+// instead of throwing.
 EvaluationSummary evaluate_batch(const UnfoldedNetwork& net, const std::complex<float>* channels, std::int64_t B,
                                  const SystemConfig& cfg);
 

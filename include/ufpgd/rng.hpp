@@ -4,6 +4,8 @@
 
 #include <cstdint>
 #include <random>
+#include <utility>
+#include <vector>
 
 #include "ufpgd/system_config.hpp"
 #include "ufpgd/types.hpp"
@@ -25,5 +27,15 @@ class Rng {
 };
 
 ChannelMatrix generate_channel(const SystemConfig& cfg, Rng& rng);
+
+// In-place Fisher-Yates shuffle driven by `rng` (rng.hpp:43-50): the order
+// train's mini-batches are drawn in.
+template <class T>
+void shuffle(std::vector<T>& items, Rng& rng) {
+  for (std::size_t i = items.size(); i > 1; --i) {
+    const std::size_t j = rng.index_below(i);
+    std::swap(items[i - 1], items[j]);
+  }
+}
 
 }  // namespace ufpgd

@@ -740,3 +740,91 @@ def lagrangian_batch(H: np.ndarray, W: np.ndarray, c: np.ndarray, lambda_: float
     if rc != ORA_OK:
         raise ValueError("lagrangian batch failed")
     return out
+
+
+# --------------------------------------------------------------------------
+# training.cpp:140-308 — the train loop over the FP64 per-sample restatement
+# (ora_train_batch_f32) with the reference's shuffle stream, ordered batch
+# means, Adam (training.cpp:116-138) and projection (training.cpp:33-38).
+# --------------------------------------------------------------------------
+SHUFFLE_STREAM = 0x7D5A1E0B33C4F216  # training.cpp:20
+
+
+def shuffle(items: list, rng: Rng) -> None:
+    """rng.hpp:43-50 Fisher-Yates."""
+    for i in range(len(items), 1, -1):
+        j = rng.index_below(i)
+        items[i - 1], items[j] = items[j], items[i - 1]
+
+
+def adam_update(state: dict, grads, params, lr: float) -> None:
+    for i, g in enumerate(grads):
+        if not math.isfinite(g):
+            raise ValueError(f"adam_update: non-finite gradient for parameter {i}")
+    state["step"] += 1
+    b1, b2, eps = 0.9, 0.999, 1e-8
+    bias1 = 1.0 - b1 ** state["step"]
+    bias2 = 1.0 - b2 ** state["step"]
+    m, v = state["m"], state["v"]
+    for i, g in enumerate(grads):
+        m[i] = b1 * m[i] + (1.0 - b1) * g
+        v[i] = b2 * v[i] + (1.0 - b2) * g * g
+        params[i] -= lr * (m[i] / bias1) / (math.sqrt(v[i] / bias2) + eps)
+
+
+def train_loop_f32(train_H, val_H, c, lam0, eta0, *, loss_kind=0, lambda_cost=1.0 / 15.0, batch_size=64,
+                   learning_rate=1e-3, max_epochs=200, patience=10, seed=0, train_labels=None, val_labels=None,
+                   sigma_nu=1.0, alpha=1.0, threads=0):
+    """Complex64 datasets [N][M][K]; returns dict(epochs=[(epoch, train_loss,
+    val_loss, val_pcg, val_sum_rate)], best_epoch, stopping_epoch, params)."""
+    N, M, K = train_H.shape
+    hi = 1.0 / mp_bound(K, M)
+    lo = 0.5 * hi
+    params = []
+    for lmb, et in zip(lam0, eta0):  # project_params, packed (training.hpp:50-51)
+        params += [max(0.0, lmb), min(max(et, lo), hi)]
+    state = dict(step=0, m=[0.0] * len(params), v=[0.0] * len(params))
+    rng = Rng.stream(seed, SHUFFLE_STREAM)
+    order = list(range(N))
+    epochs, best_val, best_epoch, best_params, since, stop = [], math.inf, -1, None, 0, -1
+    for epoch in range(max_epochs):
+        shuffle(order, rng)
+        loss_sum = 0.0
+        for start in range(0, N, batch_size):
+            idx = order[start:start + batch_size]
+            lam, eta = np.array(params[0::2]), np.array(params[1::2])
+            lab = None if train_labels is None else train_labels[idx]
+            loss, grads, _ = train_batch_f32(train_H[idx], c, lam, eta, loss_kind, lambda_cost, lab, threads)
+            n = len(idx)
+            batch_loss = 0.0
+            mean = [0.0] * len(params)
+            for b in range(n):  # ordered reduction (training.cpp:236-246)
+                batch_loss += loss[b]
+                for p in range(len(params)):
+                    mean[p] += grads[b, p]
+            batch_loss /= n
+            mean = [g / n for g in mean]
+            if not math.isfinite(batch_loss):
+                raise ValueError(f"train: non-finite loss at epoch {epoch}")
+            loss_sum += batch_loss * n
+            adam_update(state, mean, params, learning_rate)
+            for i in range(0, len(params), 2):
+                params[i] = max(0.0, params[i])
+                params[i + 1] = min(max(params[i + 1], lo), hi)
+        lam, eta = np.array(params[0::2]), np.array(params[1::2])
+        W = forward_batch_f32(val_H, c, lam, eta, w0_mode=1, threads=threads)["W"]
+        rows = metrics_batch_f32(val_H, W, c, sigma_nu, alpha, threads)
+        if loss_kind == 1:
+            vl = np.sum(np.abs(W - val_labels) ** 2, axis=(1, 2))
+        else:
+            vl = lambda_cost * rows[:, 1] / alpha + rows[:, 4] ** 2
+        rec = (epoch, loss_sum / N, float(np.mean(vl)), float(np.mean(rows[:, 3])), float(np.mean(rows[:, 2])))
+        epochs.append(rec)
+        stop = epoch
+        if rec[2] < best_val:
+            best_val, best_epoch, best_params, since = rec[2], epoch, list(params), 0
+        else:
+            since += 1
+        if since >= patience:
+            break
+    return dict(epochs=epochs, best_epoch=best_epoch, stopping_epoch=stop, params=best_params)

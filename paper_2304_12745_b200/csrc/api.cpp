@@ -5,19 +5,26 @@
 // metrics of one matrix) are host code, as in the reference.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <limits>
 #include <numbers>
+#include <numeric>
 #include <string>
 #include <vector>
 
 #include "ufpgd/batch.hpp"
+#include "ufpgd/dataset.hpp"
 #include "ufpgd/errors.hpp"
 #include "ufpgd/metrics.hpp"
 #include "ufpgd/pgd.hpp"
 #include "ufpgd/rng.hpp"
 #include "ufpgd/system_config.hpp"
+#include "ufpgd/training.hpp"
 #include "ufpgd/unfolded.hpp"
 #include "ufpgd_gpu.h"
 
@@ -160,7 +167,7 @@ LayerRun run_layers(const ChannelMatrix& H, const RealVector& c, const std::vect
 
 ComplexMatrix from_f64(const double* d, std::ptrdiff_t K, std::ptrdiff_t M) {
   ComplexMatrix A(K, M);
-  std::memcpy(A.data(), d, sizeof(double) * 2 * K * M);
+  std::memcpy(static_cast<void*>(A.data()), d, sizeof(double) * 2 * K * M);
   return A;
 }
 
@@ -756,6 +763,490 @@ EvaluationSummary evaluate_batch(const UnfoldedNetwork& net, const std::complex<
     for (int k = 0; k < K; ++k) s.std_error.sinr[k] = std::sqrt(s.std_error.sinr[k] * vs);
   }
   return s;
+}
+
+// ---- dataset.cpp: host files ------------------------------------------------
+namespace {
+
+void put_le(std::string& out, std::uint64_t v, int bytes) {
+  for (int i = 0; i < bytes; ++i) out.push_back(static_cast<char>((v >> (8 * i)) & 0xFF));
+}
+
+// Row-major K x M f64 (re, im) <-> the col-major ComplexMatrix (dataset.cpp:38-66).
+void append_rowmajor(std::vector<double>& out, const ComplexMatrix& A) {
+  for (std::ptrdiff_t k = 0; k < A.rows(); ++k)
+    for (std::ptrdiff_t m = 0; m < A.cols(); ++m) {
+      out.push_back(A(k, m).real());
+      out.push_back(A(k, m).imag());
+    }
+}
+
+ComplexMatrix from_rowmajor(const double* d, int K, int M) {
+  ComplexMatrix A(K, M);
+  for (int k = 0; k < K; ++k)
+    for (int m = 0; m < M; ++m) A(k, m) = Complex(d[2 * (k * M + m)], d[2 * (k * M + m) + 1]);
+  return A;
+}
+
+}  // namespace
+
+void write_dataset(const Dataset& data, const std::string& path) {  // dataset.cpp:70-127
+  if (data.num_users < 1 || data.num_antennas < 1) throw std::invalid_argument("write_dataset: bad dimensions");
+  if (data.has_labels() && data.labels.size() != data.channels.size())
+    throw std::invalid_argument("write_dataset: label count does not match channel count");
+  for (const ChannelMatrix& ch : data.channels)
+    if (ch.rows() != data.num_users || ch.cols() != data.num_antennas)
+      throw std::invalid_argument("write_dataset: channel shape mismatch");
+  for (const PrecoderMatrix& lb : data.labels)
+    if (lb.rows() != data.num_users || lb.cols() != data.num_antennas)
+      throw std::invalid_argument("write_dataset: label shape mismatch");
+  std::string header;
+  put_le(header, kDatasetMagic, 4);
+  put_le(header, kDatasetVersion, 4);
+  put_le(header, static_cast<std::uint32_t>(data.num_users), 4);
+  put_le(header, static_cast<std::uint32_t>(data.num_antennas), 4);
+  put_le(header, data.channels.size(), 8);
+  put_le(header, data.seed, 8);
+  put_le(header, data.has_labels() ? 1u : 0u, 4);
+  const std::filesystem::path target(path);
+  std::filesystem::path temp = target;
+  temp += ".tmp";
+  {
+    std::ofstream out(temp, std::ios::binary | std::ios::trunc);
+    if (!out) throw std::runtime_error("cannot open for writing: " + temp.string());
+    out.write(header.data(), static_cast<std::streamsize>(header.size()));
+    std::vector<double> buf;
+    for (const std::vector<ComplexMatrix>* set : {&data.channels, &data.labels})
+      for (const ComplexMatrix& A : *set) {
+        buf.clear();
+        append_rowmajor(buf, A);
+        out.write(reinterpret_cast<const char*>(buf.data()), static_cast<std::streamsize>(buf.size() * sizeof(double)));
+      }
+    out.flush();
+    if (!out) throw std::runtime_error("write failed: " + temp.string());
+  }
+  std::filesystem::rename(temp, target);
+}
+
+Dataset read_dataset(const std::string& path) {  // dataset.cpp:129-175
+  int K = 0, M = 0, labels = 0;
+  int64_t N = 0;
+  std::uint64_t seed = 0;
+  if (ufpgd_ufpd_read_header(path.c_str(), &K, &M, &N, &seed, &labels) != UFPGD_OK)
+    throw DataFormatError(ufpgd_dataset_last_error());
+  Dataset d;
+  d.num_users = K;
+  d.num_antennas = M;
+  d.seed = seed;
+  std::ifstream in(path, std::ios::binary);
+  in.seekg(static_cast<std::streamoff>(kDatasetHeaderBytes));
+  std::vector<double> buf(2 * static_cast<std::size_t>(K) * M);
+  for (int set = 0; set < (labels ? 2 : 1); ++set)
+    for (int64_t i = 0; i < N; ++i) {
+      in.read(reinterpret_cast<char*>(buf.data()), static_cast<std::streamsize>(buf.size() * sizeof(double)));
+      if (!in) throw DataFormatError("dataset truncated: " + path);
+      (set == 0 ? d.channels : d.labels).push_back(from_rowmajor(buf.data(), K, M));
+    }
+  return d;
+}
+
+// ---- training.cpp -------------------------------------------------------------
+namespace {
+
+constexpr std::uint64_t kShuffleStream = 0x7D5A1E0B33C4F216ULL;  // training.cpp:20
+
+void check_dataset(const Dataset& data, const SystemConfig& sys, const char* which) {  // training.cpp:22-31
+  if (data.size() == 0) throw TrainingError(std::string(which) + " dataset is empty");
+  if (data.num_users != sys.K || data.num_antennas != sys.M)
+    throw TrainingError(std::string(which) + " dataset dimensions do not match SystemConfig");
+}
+
+void project_flat(std::vector<double>& params, double eta_lo, double eta_hi) {  // training.cpp:33-38
+  for (std::size_t i = 0; i + 1 < params.size(); i += 2) {
+    params[i] = std::max(0.0, params[i]);
+    params[i + 1] = std::min(std::max(params[i + 1], eta_lo), eta_hi);
+  }
+}
+
+// A set of K x M matrices as one complex64 [N][M][K] device batch.
+std::vector<ufpgd_c64> stack_c64(const std::vector<ComplexMatrix>& mats) {
+  std::vector<ufpgd_c64> out;
+  for (const ComplexMatrix& A : mats) {
+    const std::vector<ufpgd_c64> a = to_c64(A);
+    out.insert(out.end(), a.begin(), a.end());
+  }
+  return out;
+}
+
+void layer_vectors(const UnfoldedNetwork& net, std::vector<double>& lam, std::vector<double>& eta) {
+  lam.clear();
+  eta.clear();
+  for (const LayerParams& l : net.layers) {
+    lam.push_back(l.lambda_i);
+    eta.push_back(l.eta_i);
+  }
+}
+
+// Device metrics rows [tx, cons, sum_rate, pcg, residual, ok, sinr_0..K-1]
+// for B (H, W) pairs; SingularChannelError where the ZF reference is singular
+// (zf.cpp:17-23 throws inside the reference's evaluate / train).
+std::vector<double> device_metric_rows(const ufpgd_c64* dH, const ufpgd_c64* dW, std::int64_t B,
+                                       const SystemConfig& sys) {
+  const int K = sys.K;
+  DeviceBuffer<double> dout(static_cast<std::size_t>(B) * (6 + K));
+  const RealVector c = sys.constraint_diag();
+  check(ufpgd_gpu_metrics(dH, dW, B, K, sys.M, c.data(), sys.sigma_nu, sys.alpha, dout.p, nullptr, g_device,
+                          nullptr));
+  std::vector<double> out(dout.n);
+  dout.download(out.data());
+  for (std::int64_t b = 0; b < B; ++b)
+    if (out[static_cast<std::size_t>(b) * (6 + K) + 5] == 0.0)
+      throw SingularChannelError("zf_precoder: channel Gram matrix is singular");
+  return out;
+}
+
+MetricsReport report_from_row(const double* o, int K) {
+  MetricsReport r;
+  r.tx_power = o[0];
+  r.cons_power = o[1];
+  r.sum_rate = o[2];
+  r.pcg = o[3];
+  r.residual = o[4];
+  r.sinr = RealVector(K);
+  for (int k = 0; k < K; ++k) r.sinr[k] = o[6 + k];
+  return r;
+}
+
+int active_of(const ufpgd_c64* w, int K, int M) {
+  int a = 0;
+  for (int m = 0; m < M; ++m) {
+    double s = 0.0;
+    for (int k = 0; k < K; ++k) s += static_cast<double>(w[m * K + k].re) * w[m * K + k].re +
+                                     static_cast<double>(w[m * K + k].im) * w[m * K + k].im;
+    if (s > 0.0) ++a;
+  }
+  return a;
+}
+
+}  // namespace
+
+void TrainConfig::validate() const {  // training.cpp:40-56
+  if (!(lambda_cost >= 0.0)) throw std::invalid_argument("TrainConfig: lambda_cost must be >= 0");
+  if (batch_size < 1) throw std::invalid_argument("TrainConfig: batch_size must be >= 1");
+  if (!(learning_rate >= 0.0)) throw std::invalid_argument("TrainConfig: learning_rate must be >= 0");
+  if (max_epochs < 1) throw std::invalid_argument("TrainConfig: max_epochs must be >= 1");
+  if (patience < 1) throw std::invalid_argument("TrainConfig: patience must be >= 1");
+}
+
+double supervised_loss(const PrecoderMatrix& precoder, const PrecoderMatrix& ground_truth) {
+  if (precoder.rows() != ground_truth.rows() || precoder.cols() != ground_truth.cols())
+    throw std::invalid_argument("supervised_loss: shape mismatch");
+  double s = 0.0;
+  for (std::ptrdiff_t i = 0; i < precoder.size(); ++i) s += std::norm(precoder.data()[i] - ground_truth.data()[i]);
+  return s;
+}
+
+ComplexMatrix supervised_loss_grad(const PrecoderMatrix& precoder, const PrecoderMatrix& ground_truth) {
+  if (precoder.rows() != ground_truth.rows() || precoder.cols() != ground_truth.cols())
+    throw std::invalid_argument("supervised_loss_grad: shape mismatch");
+  ComplexMatrix g(precoder.rows(), precoder.cols());
+  for (std::ptrdiff_t i = 0; i < precoder.size(); ++i) g.data()[i] = 2.0 * (precoder.data()[i] - ground_truth.data()[i]);
+  return g;
+}
+
+double unsupervised_loss(const PrecoderMatrix& precoder, const ChannelMatrix& channel, const SystemConfig& cfg,
+                         double lambda_cost) {
+  return lagrangian_value(precoder, channel, cfg, lambda_cost);
+}
+
+ComplexMatrix unsupervised_loss_grad(const PrecoderMatrix& precoder, const ChannelMatrix& channel,
+                                     const SystemConfig& cfg, double lambda_cost) {
+  ComplexMatrix g = grad_f(precoder, channel, cfg);  // FP64 on the device
+  for (std::ptrdiff_t i = 0; i < g.size(); ++i) g.data()[i] *= 2.0;
+  for (std::ptrdiff_t m = 0; m < precoder.cols(); ++m) {
+    const double n = precoder.colNorm(m);
+    if (n > 0.0)
+      for (std::ptrdiff_t k = 0; k < precoder.rows(); ++k) g(k, m) += (lambda_cost / n) * precoder(k, m);
+  }
+  return g;
+}
+
+std::vector<double> pack_params(const UnfoldedNetwork& net) {
+  std::vector<double> p(2 * net.layers.size());
+  for (std::size_t i = 0; i < net.layers.size(); ++i) {
+    p[2 * i] = net.layers[i].lambda_i;
+    p[2 * i + 1] = net.layers[i].eta_i;
+  }
+  return p;
+}
+
+void unpack_params(const std::vector<double>& params, UnfoldedNetwork& net) {
+  if (params.size() != 2 * net.layers.size()) throw std::invalid_argument("unpack_params: size mismatch");
+  for (std::size_t i = 0; i < net.layers.size(); ++i) {
+    net.layers[i].lambda_i = params[2 * i];
+    net.layers[i].eta_i = params[2 * i + 1];
+  }
+}
+
+void adam_update(AdamState& state, const std::vector<double>& grads, std::vector<double>& params, double lr) {
+  if (grads.size() != params.size() || grads.size() != state.m.size() || grads.size() != state.v.size())
+    throw TrainingError("adam_update: parameter/gradient size mismatch");
+  for (std::size_t i = 0; i < grads.size(); ++i)
+    if (!std::isfinite(grads[i])) throw TrainingError("adam_update: non-finite gradient for parameter " + std::to_string(i));
+  state.step += 1;
+  const double bias1 = 1.0 - std::pow(state.beta1, static_cast<double>(state.step));
+  const double bias2 = 1.0 - std::pow(state.beta2, static_cast<double>(state.step));
+  for (std::size_t i = 0; i < grads.size(); ++i) {
+    state.m[i] = state.beta1 * state.m[i] + (1.0 - state.beta1) * grads[i];
+    state.v[i] = state.beta2 * state.v[i] + (1.0 - state.beta2) * grads[i] * grads[i];
+    params[i] -= lr * (state.m[i] / bias1) / (std::sqrt(state.v[i] / bias2) + state.epsilon);
+  }
+}
+
+TrainResult train(const UnfoldedNetwork& net, const Dataset& train_set, const Dataset& val_set,
+                  const TrainConfig& cfg, const SystemConfig& sys) {
+  cfg.validate();
+  sys.validate();
+  check_dataset(train_set, sys, "train");
+  check_dataset(val_set, sys, "validation");
+  const bool supervised = cfg.loss_kind == LossKind::kSupervised;
+  if (supervised && (!train_set.has_labels() || !val_set.has_labels()))
+    throw TrainingError("train: supervised mode requires labeled datasets");
+  UnfoldedNetwork model = project_params(net);
+  if (model.num_users != sys.K || model.num_antennas != sys.M)
+    throw TrainingError("train: network dimensions do not match SystemConfig");
+  const int K = sys.K, M = sys.M, L = static_cast<int>(model.layers.size());
+  const std::size_t km = static_cast<std::size_t>(K) * M;
+  const double eta_hi = 1.0 / model.mp_bound, eta_lo = 0.5 * eta_hi;
+  std::vector<double> params = pack_params(model);
+  AdamState adam(params.size());
+  const RealVector c = sys.constraint_diag();
+
+  DeviceScope scope;
+  // The datasets as complex64 batches: training channels gathered per
+  // mini-batch on the host (the shuffle order), the validation set resident.
+  const std::vector<ufpgd_c64> tr = stack_c64(train_set.channels);
+  const std::vector<ufpgd_c64> tl = supervised ? stack_c64(train_set.labels) : std::vector<ufpgd_c64>{};
+  const std::int64_t nv = static_cast<std::int64_t>(val_set.size());
+  DeviceBuffer<ufpgd_c64> dV(static_cast<std::size_t>(nv) * km), dVW(static_cast<std::size_t>(nv) * km);
+  dV.upload(stack_c64(val_set.channels).data());
+  std::vector<ufpgd_c64> val_out(dVW.n);
+  const std::size_t bmax = std::min<std::size_t>(static_cast<std::size_t>(cfg.batch_size), train_set.size());
+  DeviceBuffer<ufpgd_c64> dB(bmax * km), dBL(supervised ? bmax * km : 0);
+  DeviceBuffer<double> dloss(bmax), dgr(bmax * 2 * L), dmean(1 + 2 * static_cast<std::size_t>(L));
+  DeviceBuffer<int32_t> ddiv(static_cast<std::size_t>(nv));
+  std::vector<ufpgd_c64> stage(bmax * km), stage_l(supervised ? bmax * km : 0);
+  std::vector<double> mean(1 + 2 * static_cast<std::size_t>(L));
+  device_metric_rows(dV.p, dV.p, nv, sys);  // ZF reference of every validation channel (training.cpp:165-171)
+
+  Rng shuffle_rng = Rng::stream(cfg.seed, kShuffleStream);
+  std::vector<std::size_t> order(train_set.size());
+  std::iota(order.begin(), order.end(), std::size_t{0});
+  TrainResult result;
+  TrainHistory& history = result.history;
+  double best_val = std::numeric_limits<double>::infinity();
+  int since_best = 0;
+  std::vector<double> lam, eta;
+  for (int epoch = 0; epoch < cfg.max_epochs; ++epoch) {
+    shuffle(order, shuffle_rng);
+    double epoch_loss_sum = 0.0;
+    for (std::size_t start = 0; start < train_set.size(); start += static_cast<std::size_t>(cfg.batch_size)) {
+      const std::size_t count = std::min<std::size_t>(static_cast<std::size_t>(cfg.batch_size), train_set.size() - start);
+      for (std::size_t b = 0; b < count; ++b) {
+        std::memcpy(&stage[b * km], &tr[order[start + b] * km], km * sizeof(ufpgd_c64));
+        if (supervised) std::memcpy(&stage_l[b * km], &tl[order[start + b] * km], km * sizeof(ufpgd_c64));
+      }
+      cuda_check(cudaMemcpy(dB.p, stage.data(), count * km * sizeof(ufpgd_c64), cudaMemcpyHostToDevice), "H2D");
+      if (supervised)
+        cuda_check(cudaMemcpy(dBL.p, stage_l.data(), count * km * sizeof(ufpgd_c64), cudaMemcpyHostToDevice), "H2D");
+      layer_vectors(model, lam, eta);
+      // per-sample taped forward from H^*, loss, backward; ordered batch mean
+      check(ufpgd_gpu_unfolded_grad(dB.p, static_cast<std::int64_t>(count), K, M, lam.data(), eta.data(), L,
+                                    c.data(), UFPGD_W0_CONJ_H, supervised ? 1 : 0, cfg.lambda_cost,
+                                    supervised ? dBL.p : nullptr, dloss.p, dgr.p, dmean.p, g_device, nullptr));
+      dmean.download(mean.data());
+      const double batch_loss = mean[0];
+      if (!std::isfinite(batch_loss))
+        throw TrainingError("train: non-finite loss at epoch " + std::to_string(epoch) + " batch " +
+                            std::to_string(start / static_cast<std::size_t>(cfg.batch_size)));
+      epoch_loss_sum += batch_loss * static_cast<double>(count);
+      const std::vector<double> grads(mean.begin() + 1, mean.end());
+      adam_update(adam, grads, params, cfg.learning_rate);
+      project_flat(params, eta_lo, eta_hi);
+      unpack_params(params, model);
+    }
+
+    // validation: forward_infer (start H^*) on the device, then device metrics
+    layer_vectors(model, lam, eta);
+    const int rc = ufpgd_gpu_unfolded_forward(dV.p, nv, K, M, lam.data(), eta.data(), L, c.data(), UFPGD_W0_CONJ_H,
+                                              nullptr, dVW.p, ddiv.p, nullptr, nullptr, nullptr, sys.alpha, g_device,
+                                              nullptr);
+    if (rc != UFPGD_OK) raise(rc);
+    cuda_check(cudaDeviceSynchronize(), "validation forward");
+    std::vector<int32_t> div(static_cast<std::size_t>(nv));
+    ddiv.download(div.data());
+    for (int32_t d : div)
+      if (d >= 0) throw DivergenceError("forward: non-finite iterate in validation", d);
+    const std::vector<double> rows = device_metric_rows(dV.p, dVW.p, nv, sys);
+    if (supervised) dVW.download(val_out.data());
+    EpochRecord rec;
+    rec.epoch = epoch;
+    rec.train_loss = epoch_loss_sum / static_cast<double>(train_set.size());
+    for (std::int64_t j = 0; j < nv; ++j) {
+      const double* o = &rows[static_cast<std::size_t>(j) * (6 + K)];
+      double loss;
+      if (supervised) {
+        loss = 0.0;
+        const ComplexMatrix& g = val_set.labels[static_cast<std::size_t>(j)];
+        const ufpgd_c64* w = &val_out[static_cast<std::size_t>(j) * km];
+        for (std::size_t i = 0; i < km; ++i) loss += std::norm(Complex(w[i].re, w[i].im) - g.data()[i]);
+      } else {
+        loss = cfg.lambda_cost * (o[1] / sys.alpha) + o[4] * o[4];  // lagrangian_value (pgd.cpp:171-176)
+      }
+      rec.val_loss += loss;
+      rec.val_mean_pcg += o[3];
+      rec.val_mean_sum_rate += o[2];
+    }
+    const double vn = static_cast<double>(nv);
+    rec.val_loss /= vn;
+    rec.val_mean_pcg /= vn;
+    rec.val_mean_sum_rate /= vn;
+    if (!std::isfinite(rec.val_loss))
+      throw TrainingError("train: non-finite validation loss at epoch " + std::to_string(epoch));
+    history.epochs.push_back(rec);
+    history.stopping_epoch = epoch;
+    if (rec.val_loss < best_val) {
+      best_val = rec.val_loss;
+      history.best_epoch = epoch;
+      history.best_params = model.layers;
+      since_best = 0;
+    } else {
+      ++since_best;
+    }
+    if (since_best >= cfg.patience) break;
+  }
+  model.layers = history.best_params;
+  result.network = std::move(model);
+  return result;
+}
+
+EvaluationSummary evaluate(const UnfoldedNetwork& net, const Dataset& test_set, const SystemConfig& sys,
+                           const EvalOptions& options) {
+  sys.validate();
+  check_dataset(test_set, sys, "test");
+  UnfoldedNetwork model = net;
+  model.validate();
+  check_projected(model);
+  if (model.num_users != sys.K || model.num_antennas != sys.M)
+    throw std::invalid_argument("forward: network dimensions do not match SystemConfig");
+  const int K = sys.K, M = sys.M, L = static_cast<int>(model.layers.size());
+  const std::size_t km = static_cast<std::size_t>(K) * M;
+  const std::int64_t n = static_cast<std::int64_t>(test_set.size());
+  std::vector<double> lam, eta, thr;
+  layer_vectors(model, lam, eta);
+  for (int l = 0; l < L; ++l) thr.push_back(lam[static_cast<std::size_t>(l)] * eta[static_cast<std::size_t>(l)]);
+  const RealVector c = sys.constraint_diag();
+  DeviceScope scope;
+  EvaluationSummary summary;
+  summary.num_channels = static_cast<std::size_t>(n);
+  std::vector<MetricsReport> reports;
+  reports.reserve(static_cast<std::size_t>(n));
+  if (options.per_layer) summary.per_layer.assign(static_cast<std::size_t>(L) + 1, TraceRecord{});
+  // chunks bound the (L + 1) iterates kept on the device for per-layer curves
+  const std::int64_t chunk = options.per_layer ? std::max<std::int64_t>(1, (std::int64_t{1} << 28) / ((L + 1) * km * 8))
+                                               : n;
+  const std::vector<ufpgd_c64> all = stack_c64(test_set.channels);
+  for (std::int64_t b0 = 0; b0 < n; b0 += chunk) {
+    const std::int64_t nb = std::min(chunk, n - b0);
+    DeviceBuffer<ufpgd_c64> dH(static_cast<std::size_t>(nb) * km), dW(static_cast<std::size_t>(nb) * km);
+    cuda_check(cudaMemcpy(dH.p, &all[static_cast<std::size_t>(b0) * km], dH.n * sizeof(ufpgd_c64),
+                          cudaMemcpyHostToDevice), "H2D");
+    DeviceBuffer<int32_t> ddiv(static_cast<std::size_t>(nb));
+    std::vector<int32_t> div(static_cast<std::size_t>(nb));
+    if (options.per_layer) {  // forward with_iterates (unfolded.cpp:112-146), FP32 general kernel
+      DeviceBuffer<ufpgd_c64> dI(static_cast<std::size_t>(L + 1) * dH.n);
+      DeviceBuffer<int64_t> dits(static_cast<std::size_t>(nb));
+      check(ufpgd_gpu_layers_general(dH.p, nb, K, M, eta.data(), thr.data(), L, c.data(), UFPGD_W0_CONJ_H, nullptr, 0,
+                                     0.0, 0, dW.p, ddiv.p, dits.p, dI.p, nullptr, nullptr, nullptr, g_device, nullptr));
+      cuda_check(cudaDeviceSynchronize(), "forward with iterates");
+      ddiv.download(div.data());
+      for (int32_t d : div)
+        if (d >= 0) throw DivergenceError("forward: non-finite iterate", d);
+      std::vector<ufpgd_c64> it(dH.n);
+      for (int l = 0; l <= L; ++l) {
+        const ufpgd_c64* dWl = dI.p + static_cast<std::size_t>(l) * dH.n;
+        const std::vector<double> rows = device_metric_rows(dH.p, dWl, nb, sys);
+        cuda_check(cudaMemcpy(it.data(), dWl, dH.n * sizeof(ufpgd_c64), cudaMemcpyDeviceToHost), "D2H");
+        TraceRecord& rec = summary.per_layer[static_cast<std::size_t>(l)];
+        for (std::int64_t j = 0; j < nb; ++j) {
+          const double* o = &rows[static_cast<std::size_t>(j) * (6 + K)];
+          rec.lagrangian += options.lagrangian_lambda * (o[1] / sys.alpha) + o[4] * o[4];
+          rec.residual += o[4];
+          rec.pcg += o[3];
+          rec.sum_rate += o[2];
+          rec.active_columns += active_of(&it[static_cast<std::size_t>(j) * km], K, M);
+          if (l == L) reports.push_back(report_from_row(o, K));
+        }
+      }
+    } else {  // forward_infer from H^* (fused kernels where the shape has one)
+      check(ufpgd_gpu_unfolded_forward(dH.p, nb, K, M, lam.data(), eta.data(), L, c.data(), UFPGD_W0_CONJ_H, nullptr,
+                                       dW.p, ddiv.p, nullptr, nullptr, nullptr, sys.alpha, g_device, nullptr));
+      cuda_check(cudaDeviceSynchronize(), "forward");
+      ddiv.download(div.data());
+      for (int32_t d : div)
+        if (d >= 0) throw DivergenceError("forward: non-finite iterate", d);
+      const std::vector<double> rows = device_metric_rows(dH.p, dW.p, nb, sys);
+      for (std::int64_t j = 0; j < nb; ++j) reports.push_back(report_from_row(&rows[static_cast<std::size_t>(j) * (6 + K)], K));
+    }
+  }
+  // training.cpp:361-399: means, then standard errors of the means
+  MetricsReport& mu = summary.mean;
+  MetricsReport& se = summary.std_error;
+  mu.sinr = RealVector(K);
+  se.sinr = RealVector(K);
+  for (const MetricsReport& r : reports) {
+    mu.tx_power += r.tx_power;
+    mu.cons_power += r.cons_power;
+    mu.sum_rate += r.sum_rate;
+    mu.pcg += r.pcg;
+    mu.residual += r.residual;
+    for (int k = 0; k < K; ++k) mu.sinr[k] += r.sinr[k];
+  }
+  const double scale = 1.0 / static_cast<double>(n);
+  mu.tx_power *= scale;
+  mu.cons_power *= scale;
+  mu.sum_rate *= scale;
+  mu.pcg *= scale;
+  mu.residual *= scale;
+  for (int k = 0; k < K; ++k) mu.sinr[k] *= scale;
+  if (n > 1) {
+    auto sq = [](double d) { return d * d; };
+    for (const MetricsReport& r : reports) {
+      se.tx_power += sq(r.tx_power - mu.tx_power);
+      se.cons_power += sq(r.cons_power - mu.cons_power);
+      se.sum_rate += sq(r.sum_rate - mu.sum_rate);
+      se.pcg += sq(r.pcg - mu.pcg);
+      se.residual += sq(r.residual - mu.residual);
+      for (int k = 0; k < K; ++k) se.sinr[k] += sq(r.sinr[k] - mu.sinr[k]);
+    }
+    const double vs = 1.0 / (static_cast<double>(n - 1) * static_cast<double>(n));
+    se.tx_power = std::sqrt(se.tx_power * vs);
+    se.cons_power = std::sqrt(se.cons_power * vs);
+    se.sum_rate = std::sqrt(se.sum_rate * vs);
+    se.pcg = std::sqrt(se.pcg * vs);
+    se.residual = std::sqrt(se.residual * vs);
+    for (int k = 0; k < K; ++k) se.sinr[k] = std::sqrt(se.sinr[k] * vs);
+  }
+  if (options.per_layer)
+    for (TraceRecord& rec : summary.per_layer) {
+      rec.lagrangian *= scale;
+      rec.residual *= scale;
+      rec.pcg *= scale;
+      rec.sum_rate *= scale;
+      rec.active_columns *= scale;
+    }
+  for (std::size_t l = 0; l < summary.per_layer.size(); ++l) summary.per_layer[l].index = static_cast<long>(l);
+  return summary;
 }
 
 }  // namespace ufpgd

@@ -11,10 +11,12 @@
 #include <vector>
 
 #include "ufpgd/batch.hpp"
+#include "ufpgd/dataset.hpp"
 #include "ufpgd/errors.hpp"
 #include "ufpgd/metrics.hpp"
 #include "ufpgd/pgd.hpp"
 #include "ufpgd/rng.hpp"
+#include "ufpgd/training.hpp"
 #include "ufpgd/unfolded.hpp"
 
 using namespace ufpgd;
@@ -103,6 +105,274 @@ static void fixture(SystemConfig& cfg, ChannelMatrix& h) {
   h(1, 1) = {0.4, -0.4};
   h(1, 2) = {0.03, 0.01};
   h(1, 3) = {-0.5, 0.6};
+}
+
+// test_training.cpp:33-70 helpers
+static Dataset make_dataset(const SystemConfig& cfg, std::uint64_t seed, std::size_t count, bool with_labels,
+                            double lambda) {
+  Dataset d;
+  d.num_users = cfg.K;
+  d.num_antennas = cfg.M;
+  d.seed = seed;
+  for (std::uint64_t i = 0; i < count; ++i) {
+    d.channels.push_back(channel_for(cfg, seed, i));
+    if (with_labels) d.labels.push_back(oracle_solve(d.channels.back(), cfg, lambda));
+  }
+  return d;
+}
+
+static double mean_unsupervised_loss(const UnfoldedNetwork& net, const Dataset& data, const SystemConfig& cfg,
+                                     double lambda) {
+  double acc = 0.0;
+  for (const ChannelMatrix& h : data.channels) acc += unsupervised_loss(forward_infer(net, h, cfg), h, cfg, lambda);
+  return acc / static_cast<double>(data.size());
+}
+
+static double mean_supervised_loss(const UnfoldedNetwork& net, const Dataset& data, const SystemConfig& cfg) {
+  double acc = 0.0;
+  for (std::size_t i = 0; i < data.size(); ++i)
+    acc += supervised_loss(forward_infer(net, data.channels[i], cfg), data.labels[i]);
+  return acc / static_cast<double>(data.size());
+}
+
+static double rel_err(double a, double b) { return std::abs(a - b) / std::max(std::abs(a), std::abs(b)); }
+
+static void training_tests() {
+  // --- test_training.cpp ----------------------------------------------------------
+  {  // train config validation (test_training.cpp:74-96)
+    TrainConfig tc;
+    tc.validate();
+    TrainConfig bad = tc;
+    bad.lambda_cost = -1.0;
+    CHECK_THROWS_AS(bad.validate(), std::invalid_argument);
+    bad = tc;
+    bad.batch_size = 0;
+    CHECK_THROWS_AS(bad.validate(), std::invalid_argument);
+    bad = tc;
+    bad.learning_rate = -1e-3;
+    CHECK_THROWS_AS(bad.validate(), std::invalid_argument);
+    bad = tc;
+    bad.max_epochs = 0;
+    CHECK_THROWS_AS(bad.validate(), std::invalid_argument);
+    bad = tc;
+    bad.patience = 0;
+    CHECK_THROWS_AS(bad.validate(), std::invalid_argument);
+  }
+  {  // supervised loss basics (test_training.cpp:98-116)
+    Rng rng = Rng::stream(60, 0);
+    ComplexMatrix w = random_matrix(3, 5, rng);
+    CHECK(supervised_loss(w, w) == 0.0);
+    ComplexMatrix shifted = w;
+    shifted(1, 2) += Complex(1.0, 0.0);
+    CHECK(std::abs(supervised_loss(shifted, w) - 1.0) < 1e-12);
+    CHECK(supervised_loss(w, shifted) == supervised_loss(shifted, w));
+    CHECK_THROWS_AS(supervised_loss(w, ComplexMatrix(3, 4)), std::invalid_argument);
+    ComplexMatrix g = supervised_loss_grad(shifted, w);
+    CHECK(std::abs(g(1, 2) - Complex(2.0, 0.0)) < 1e-12);
+  }
+  {  // unsupervised loss gradient vs central finite differences (test_training.cpp:153-177)
+    SystemConfig cfg = SystemConfig::uniform(3, 6, 10.0);
+    ChannelMatrix h = channel_for(cfg, 61, 0);
+    Rng rng = Rng::stream(62, 0);
+    ComplexMatrix w = random_matrix(3, 6, rng), d = random_matrix(3, 6, rng);
+    const double lam = 1.0 / 15.0, eps = 1e-6;
+    ComplexMatrix wp = w, wm = w;
+    for (std::ptrdiff_t i = 0; i < w.size(); ++i) {
+      wp.data()[i] += eps * d.data()[i];
+      wm.data()[i] -= eps * d.data()[i];
+    }
+    const double numeric = (unsupervised_loss(wp, h, cfg, lam) - unsupervised_loss(wm, h, cfg, lam)) / (2 * eps);
+    ComplexMatrix g = unsupervised_loss_grad(w, h, cfg, lam);
+    double analytic = 0.0;  // real-pair inner product <g, d>
+    for (std::ptrdiff_t i = 0; i < w.size(); ++i)
+      analytic += g.data()[i].real() * d.data()[i].real() + g.data()[i].imag() * d.data()[i].imag();
+    CHECK(rel_err(numeric, analytic) < 1e-6);
+  }
+  {  // adam (test_training.cpp:179-253)
+    std::vector<double> params{0.3, -0.2, 1.5};
+    const std::vector<double> before = params;
+    AdamState st(3);
+    adam_update(st, {0.0, 0.0, 0.0}, params, 1e-2);
+    CHECK(st.step == 1 && params == before);
+    AdamState s2(2);
+    std::vector<double> p2{1.0, 1.0};
+    adam_update(s2, {0.5, -2.0}, p2, 1e-3);  // bias-corrected first step = lr * sign(g)
+    CHECK(std::abs((p2[0] - 1.0) + 1e-3) < 1e-6 && std::abs((p2[1] - 1.0) - 1e-3) < 1e-6);
+    // scripted 1-D quadratic f = (theta - 3)^2
+    AdamState s3(1);
+    std::vector<double> th{0.0};
+    double m = 0.0, v = 0.0, ref = 0.0;
+    for (int t = 1; t <= 10; ++t) {
+      const double g = 2.0 * (th[0] - 3.0);
+      m = 0.9 * m + 0.1 * g;
+      v = 0.999 * v + 0.001 * g * g;
+      ref -= 0.1 * (m / (1 - std::pow(0.9, t))) / (std::sqrt(v / (1 - std::pow(0.999, t))) + 1e-8);
+      adam_update(s3, {g}, th, 0.1);
+    }
+    CHECK(rel_err(ref, th[0]) < 1e-12 && s3.step == 10);
+    AdamState s4(4);
+    std::vector<double> p4(4, 0.0);
+    bool named = false;
+    try {
+      adam_update(s4, {0.0, 0.0, 0.0, std::nan("")}, p4, 1e-3);
+    } catch (const TrainingError& e) {
+      named = std::string(e.what()).find('3') != std::string::npos;
+    }
+    CHECK(named);
+    CHECK_THROWS_AS(adam_update(s4, {0.0}, p4, 1e-3), TrainingError);
+  }
+  {  // pack / unpack (test_training.cpp:255-273)
+    UnfoldedNetwork net = UnfoldedNetwork::pgd_init(4, 16, 3, 0.1);
+    net.layers[1].lambda_i = 0.7;
+    net.layers[2].eta_i = 0.02;
+    std::vector<double> packed = pack_params(net);
+    CHECK(packed.size() == 6 && packed[0] == net.layers[0].lambda_i && packed[1] == net.layers[0].eta_i);
+    CHECK(packed[2] == 0.7 && packed[5] == 0.02);
+    packed[4] = 0.33;
+    unpack_params(packed, net);
+    CHECK(net.layers[2].lambda_i == 0.33);
+    CHECK_THROWS_AS(unpack_params(std::vector<double>(5), net), std::invalid_argument);
+  }
+  {  // zero learning rate: unchanged network, stops after patience + 1 epochs (test_training.cpp:275-305)
+    SystemConfig cfg = SystemConfig::uniform(4, 16, 10.0);
+    Dataset tr = make_dataset(cfg, 70, 16, false, 0.0), va = make_dataset(cfg, 71, 8, false, 0.0);
+    UnfoldedNetwork net = UnfoldedNetwork::pgd_init(cfg.K, cfg.M, 3, 1.0 / 15.0);
+    TrainConfig tc;
+    tc.batch_size = 8;
+    tc.learning_rate = 0.0;
+    tc.max_epochs = 20;
+    tc.patience = 3;
+    tc.seed = 99;
+    TrainResult r = train(net, tr, va, tc, cfg);
+    bool same = r.network.layers.size() == net.layers.size();
+    for (std::size_t i = 0; same && i < net.layers.size(); ++i)
+      same = r.network.layers[i].lambda_i == net.layers[i].lambda_i && r.network.layers[i].eta_i == net.layers[i].eta_i;
+    CHECK(same);
+    CHECK(r.history.epochs.size() == 4 && r.history.best_epoch == 0 && r.history.stopping_epoch == 3);
+  }
+  {  // reproducible for a fixed seed (test_training.cpp:307-343): bit-identical histories
+    SystemConfig cfg = SystemConfig::uniform(4, 16, 10.0);
+    Dataset tr = make_dataset(cfg, 72, 32, false, 0.0), va = make_dataset(cfg, 73, 16, false, 0.0);
+    UnfoldedNetwork net = UnfoldedNetwork::pgd_init(cfg.K, cfg.M, 4, 1.0 / 15.0);
+    TrainConfig tc;
+    tc.batch_size = 8;
+    tc.max_epochs = 3;
+    tc.seed = 1234;
+    tc.threads = 2;
+    TrainResult a = train(net, tr, va, tc, cfg), b = train(net, tr, va, tc, cfg);
+    bool same = a.history.epochs.size() == b.history.epochs.size() && a.history.best_epoch == b.history.best_epoch;
+    for (std::size_t i = 0; same && i < a.history.epochs.size(); ++i) {
+      const EpochRecord &x = a.history.epochs[i], &y = b.history.epochs[i];
+      same = x.epoch == y.epoch && x.train_loss == y.train_loss && x.val_loss == y.val_loss &&
+             x.val_mean_pcg == y.val_mean_pcg && x.val_mean_sum_rate == y.val_mean_sum_rate;
+    }
+    for (std::size_t i = 0; same && i < a.network.layers.size(); ++i)
+      same = a.network.layers[i].lambda_i == b.network.layers[i].lambda_i &&
+             a.network.layers[i].eta_i == b.network.layers[i].eta_i;
+    CHECK(same);
+  }
+  {  // supervised mode without labels (test_training.cpp:345-357)
+    SystemConfig cfg = SystemConfig::uniform(4, 16, 10.0);
+    Dataset tr = make_dataset(cfg, 74, 8, false, 0.0), va = make_dataset(cfg, 75, 4, false, 0.0);
+    UnfoldedNetwork net = UnfoldedNetwork::pgd_init(cfg.K, cfg.M, 2, 0.1);
+    TrainConfig tc;
+    tc.loss_kind = LossKind::kSupervised;
+    tc.batch_size = 4;
+    tc.max_epochs = 1;
+    CHECK_THROWS_AS(train(net, tr, va, tc, cfg), TrainingError);
+    Dataset empty;
+    empty.num_users = 4;
+    empty.num_antennas = 16;
+    tc.loss_kind = LossKind::kUnsupervised;
+    CHECK_THROWS_AS(train(net, empty, va, tc, cfg), TrainingError);
+  }
+  {  // unsupervised training improves the validation loss (test_training.cpp:359-390)
+    SystemConfig cfg = SystemConfig::uniform(8, 64, 10.0);
+    const double lambda = 1.0 / 15.0;
+    Dataset tr = make_dataset(cfg, 76, 512, false, 0.0), va = make_dataset(cfg, 77, 128, false, 0.0);
+    UnfoldedNetwork net = UnfoldedNetwork::pgd_init(cfg.K, cfg.M, 20, lambda);
+    const double baseline = mean_unsupervised_loss(net, va, cfg, lambda);
+    TrainConfig tc;
+    tc.lambda_cost = lambda;
+    tc.batch_size = 64;
+    tc.max_epochs = 5;
+    tc.patience = 5;
+    tc.seed = 2024;
+    TrainResult r = train(net, tr, va, tc, cfg);
+    CHECK(r.history.best_epoch >= 0);
+    const double best = r.history.epochs[static_cast<std::size_t>(r.history.best_epoch)].val_loss;
+    CHECK(best < baseline);
+    // the batched validation runs in FP32; the per-channel reload in FP64
+    CHECK(rel_err(best, mean_unsupervised_loss(r.network, va, cfg, lambda)) < 1e-5);
+  }
+  {  // supervised training improves the distance to the oracle (test_training.cpp:392-415)
+    SystemConfig cfg = SystemConfig::uniform(4, 16, 10.0);
+    const double lambda = 1.0 / 15.0;
+    Dataset tr = make_dataset(cfg, 78, 64, true, lambda), va = make_dataset(cfg, 79, 16, true, lambda);
+    UnfoldedNetwork net = UnfoldedNetwork::pgd_init(cfg.K, cfg.M, 5, lambda);
+    const double baseline = mean_supervised_loss(net, va, cfg);
+    TrainConfig tc;
+    tc.loss_kind = LossKind::kSupervised;
+    tc.lambda_cost = lambda;
+    tc.batch_size = 16;
+    tc.max_epochs = 8;
+    tc.patience = 8;
+    tc.seed = 31;
+    TrainResult r = train(net, tr, va, tc, cfg);
+    CHECK(mean_supervised_loss(r.network, va, cfg) < baseline);
+  }
+  {  // evaluating the untrained network equals plain PGD (test_training.cpp:454-493)
+    SystemConfig cfg = SystemConfig::uniform(4, 16, 10.0);
+    const double lambda = 1.0 / 15.0;
+    const int layers = 20;
+    Dataset te = make_dataset(cfg, 82, 32, false, 0.0);
+    UnfoldedNetwork net = UnfoldedNetwork::pgd_init(cfg.K, cfg.M, layers, lambda);
+    EvalOptions opt;
+    opt.per_layer = true;
+    opt.lagrangian_lambda = lambda;
+    EvaluationSummary s = evaluate(net, te, cfg, opt);
+    PgdParams p;
+    p.lambda = lambda;
+    p.eta = 1.0 / net.mp_bound;
+    p.max_iters = layers;
+    double acc = 0.0;
+    for (const ChannelMatrix& h : te.channels) acc += pcg(h, solve_pgd(h, cfg, p).precoder, cfg);
+    const double manual = acc / static_cast<double>(te.size());
+    CHECK(s.num_channels == 32);
+    CHECK(rel_err(manual, s.mean.pcg) < 1e-6);  // FP32 batched vs FP64 per channel (reference: 1e-12)
+    CHECK(s.std_error.pcg >= 0.0 && std::isfinite(s.std_error.sum_rate));
+    bool idx = s.per_layer.size() == static_cast<std::size_t>(layers) + 1;
+    for (std::size_t i = 0; idx && i < s.per_layer.size(); ++i) idx = s.per_layer[i].index == static_cast<long>(i);
+    CHECK(idx);
+    CHECK(rel_err(s.per_layer.back().pcg, s.mean.pcg) < 1e-12);
+    CHECK(s.per_layer.front().active_columns == 16.0);  // layer 0 = H^*: every antenna active
+    EvaluationSummary f = evaluate(net, te, cfg);  // final layer only (fused kernel path)
+    CHECK(f.per_layer.empty() && rel_err(f.mean.pcg, s.mean.pcg) < 1e-6);
+  }
+  {  // dataset files round trip and corruption (test_dataset.cpp)
+    SystemConfig cfg = SystemConfig::uniform(3, 5, 10.0);
+    Dataset d = make_dataset(cfg, 90, 4, true, 0.1);
+    d.seed = 0xABCDEF;
+    const std::string path = "/tmp/ufpgd_api_test.ufpd";
+    write_dataset(d, path);
+    Dataset r = read_dataset(path);
+    bool same = r.num_users == 3 && r.num_antennas == 5 && r.seed == 0xABCDEF && r.size() == 4 && r.has_labels();
+    for (std::size_t i = 0; same && i < 4; ++i)
+      for (std::ptrdiff_t j = 0; same && j < 15; ++j)
+        same = r.channels[i].data()[j] == d.channels[i].data()[j] && r.labels[i].data()[j] == d.labels[i].data()[j];
+    CHECK(same);
+    {
+      std::FILE* f = std::fopen(path.c_str(), "ab");
+      std::fputc(0, f);
+      std::fclose(f);
+    }
+    CHECK_THROWS_AS(read_dataset(path), DataFormatError);
+    CHECK_THROWS_AS(read_dataset("/tmp/does_not_exist.ufpd"), DataFormatError);
+    Dataset bad = d;
+    bad.labels.pop_back();
+    CHECK_THROWS_AS(write_dataset(bad, path), std::invalid_argument);
+    std::remove(path.c_str());
+  }
 }
 
 int main() {
@@ -441,6 +711,7 @@ int main() {
     CHECK(train_gradients(next, H.data(), B, cfg).loss <= g.loss * (1.0 + 1e-9));
     CHECK_THROWS_AS(train_gradients(net, H.data(), B, cfg, LossKind::Supervised), TrainingError);
   }
+  training_tests();
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
