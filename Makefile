@@ -13,7 +13,7 @@ CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -Iinclude -I$(PKG)/csrc -I/usr/lo
 OBJS     := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(SRCS_CU)) $(patsubst $(PKG)/csrc/%.cpp,$(OBJDIR)/%.o,$(SRCS_CPP))
 HDRS     := include/ufpgd_gpu.h $(PKG)/csrc/ufpgd_internal.h $(wildcard include/ufpgd/*.hpp)
 
-all: $(LIBDIR)/libufpgd_gpu.so oracle build/test_api build/train_dump
+all: $(LIBDIR)/libufpgd_gpu.so oracle build/test_api build/train_dump build/test_json
 
 $(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -28,6 +28,10 @@ $(LIBDIR)/libufpgd_gpu.so: $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl -lpthread
 
 build/test_api: tests/cpp/test_api.cpp $(LIBDIR)/libufpgd_gpu.so $(HDRS)
+	@mkdir -p build
+	$(CXX) -O2 -std=c++20 -Iinclude -I/usr/local/cuda/include $< -o $@ -L$(LIBDIR) -lufpgd_gpu -Wl,-rpath,'$$ORIGIN/../$(LIBDIR)'
+
+build/test_json: tests/cpp/test_json.cpp $(LIBDIR)/libufpgd_gpu.so $(HDRS)
 	@mkdir -p build
 	$(CXX) -O2 -std=c++20 -Iinclude -I/usr/local/cuda/include $< -o $@ -L$(LIBDIR) -lufpgd_gpu -Wl,-rpath,'$$ORIGIN/../$(LIBDIR)'
 

@@ -6,11 +6,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <charconv>
 #include <cmath>
 #include <complex>
 #include <cstring>
 #include <filesystem>
 #include <fstream>
+#include <iterator>
 #include <limits>
 #include <numbers>
 #include <numeric>
@@ -1247,6 +1249,233 @@ EvaluationSummary evaluate(const UnfoldedNetwork& net, const Dataset& test_set, 
     }
   for (std::size_t l = 0; l < summary.per_layer.size(); ++l) summary.per_layer[l].index = static_cast<long>(l);
   return summary;
+}
+
+}  // namespace ufpgd
+
+// ---- unfolded.cpp:241-298: model JSON -------------------------------------------
+namespace ufpgd {
+namespace {
+
+// nlohmann::json's number format: shortest round-trip, ".0" on integral doubles.
+std::string json_number(double v) {
+  if (!std::isfinite(v)) return "null";
+  char buf[64];
+  auto res = std::to_chars(buf, buf + sizeof(buf), v);
+  std::string s(buf, res.ptr);
+  if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
+  return s;
+}
+
+// Minimal JSON reader for the model schema: objects, arrays, numbers,
+// strings, true/false/null. Throws DataFormatError with a position.
+struct JsonValue {
+  enum Kind { Null, Bool, Number, String, Array, Object } kind = Null;
+  double number = 0.0;
+  bool integral = false;
+  std::string text;
+  std::vector<JsonValue> items;
+  std::vector<std::pair<std::string, JsonValue>> fields;
+  const JsonValue& at(const std::string& key) const {
+    if (kind != Object) throw DataFormatError("model JSON: expected an object");
+    for (const auto& f : fields)
+      if (f.first == key) return f.second;
+    throw DataFormatError("model JSON: missing key \"" + key + "\"");
+  }
+  double as_number(const char* what) const {
+    if (kind != Number) throw DataFormatError(std::string("model JSON: ") + what + " must be a number");
+    return number;
+  }
+  long as_integer(const char* what) const {
+    if (kind != Number || !integral) throw DataFormatError(std::string("model JSON: ") + what + " must be an integer");
+    return static_cast<long>(number);
+  }
+};
+
+class JsonParser {
+ public:
+  explicit JsonParser(const std::string& t) : t_(t) {}
+  JsonValue document() {
+    JsonValue v = value();
+    ws();
+    if (i_ != t_.size()) fail("trailing characters");
+    return v;
+  }
+
+ private:
+  const std::string& t_;
+  std::size_t i_ = 0;
+  [[noreturn]] void fail(const std::string& what) const {
+    throw DataFormatError("model JSON parse error at byte " + std::to_string(i_) + ": " + what);
+  }
+  void ws() {
+    while (i_ < t_.size() && (t_[i_] == ' ' || t_[i_] == '\n' || t_[i_] == '\t' || t_[i_] == '\r')) ++i_;
+  }
+  bool lit(const char* s) {
+    const std::size_t n = std::strlen(s);
+    if (t_.compare(i_, n, s) == 0) {
+      i_ += n;
+      return true;
+    }
+    return false;
+  }
+  std::string str() {
+    if (t_[i_] != '"') fail("expected a string");
+    ++i_;
+    std::string out;
+    while (i_ < t_.size() && t_[i_] != '"') {
+      if (t_[i_] == '\\') {
+        if (++i_ >= t_.size()) fail("bad escape");
+        const char e = t_[i_];
+        out.push_back(e == 'n' ? '\n' : e == 't' ? '\t' : e == 'r' ? '\r' : e == 'b' ? '\b' : e == 'f' ? '\f' : e);
+        ++i_;
+      } else {
+        out.push_back(t_[i_++]);
+      }
+    }
+    if (i_ >= t_.size()) fail("unterminated string");
+    ++i_;
+    return out;
+  }
+  JsonValue value() {
+    ws();
+    if (i_ >= t_.size()) fail("unexpected end of input");
+    JsonValue v;
+    const char ch = t_[i_];
+    if (ch == '{') {
+      v.kind = JsonValue::Object;
+      ++i_;
+      ws();
+      if (i_ < t_.size() && t_[i_] == '}') {
+        ++i_;
+        return v;
+      }
+      for (;;) {
+        ws();
+        std::string key = str();
+        ws();
+        if (i_ >= t_.size() || t_[i_] != ':') fail("expected ':'");
+        ++i_;
+        v.fields.emplace_back(std::move(key), value());
+        ws();
+        if (i_ < t_.size() && t_[i_] == ',') {
+          ++i_;
+          continue;
+        }
+        if (i_ < t_.size() && t_[i_] == '}') {
+          ++i_;
+          return v;
+        }
+        fail("expected ',' or '}'");
+      }
+    }
+    if (ch == '[') {
+      v.kind = JsonValue::Array;
+      ++i_;
+      ws();
+      if (i_ < t_.size() && t_[i_] == ']') {
+        ++i_;
+        return v;
+      }
+      for (;;) {
+        v.items.push_back(value());
+        ws();
+        if (i_ < t_.size() && t_[i_] == ',') {
+          ++i_;
+          continue;
+        }
+        if (i_ < t_.size() && t_[i_] == ']') {
+          ++i_;
+          return v;
+        }
+        fail("expected ',' or ']'");
+      }
+    }
+    if (ch == '"') {
+      v.kind = JsonValue::String;
+      v.text = str();
+      return v;
+    }
+    if (lit("true") || lit("false")) {
+      v.kind = JsonValue::Bool;
+      v.number = t_[i_ - 1] == 'e' && t_[i_ - 2] == 'u' ? 1.0 : 0.0;
+      return v;
+    }
+    if (lit("null")) return v;
+    const std::size_t start = i_;
+    while (i_ < t_.size() && std::strchr("+-0123456789.eE", t_[i_]) && t_[i_] != '\0') ++i_;
+    if (start == i_) fail("unexpected character");
+    const std::string num = t_.substr(start, i_ - start);
+    double d = 0.0;
+    auto res = std::from_chars(num.data(), num.data() + num.size(), d);
+    if (res.ec != std::errc() || res.ptr != num.data() + num.size()) fail("bad number");
+    v.kind = JsonValue::Number;
+    v.number = d;
+    v.integral = num.find_first_of(".eE") == std::string::npos;
+    return v;
+  }
+};
+
+}  // namespace
+
+std::string to_json_string(const UnfoldedNetwork& net) {
+  std::string s = "{\n";
+  s += "  \"I\": " + std::to_string(net.layers.size()) + ",\n";
+  s += "  \"K\": " + std::to_string(net.num_users) + ",\n";
+  s += "  \"M\": " + std::to_string(net.num_antennas) + ",\n";
+  s += "  \"layers\": [";
+  for (std::size_t i = 0; i < net.layers.size(); ++i) {
+    s += i ? ",\n    {\n" : "\n    {\n";
+    s += "      \"eta\": " + json_number(net.layers[i].eta_i) + ",\n";
+    s += "      \"lambda\": " + json_number(net.layers[i].lambda_i) + "\n    }";
+  }
+  s += net.layers.empty() ? "],\n" : "\n  ],\n";
+  s += "  \"mp_bound\": " + json_number(net.mp_bound) + ",\n";
+  s += "  \"version\": 1\n}\n";
+  return s;
+}
+
+UnfoldedNetwork network_from_json_string(const std::string& text) {
+  const JsonValue doc = JsonParser(text).document();
+  if (doc.at("version").as_integer("version") != 1) throw DataFormatError("model JSON: unsupported version");
+  UnfoldedNetwork net;
+  net.num_users = static_cast<int>(doc.at("K").as_integer("K"));
+  net.num_antennas = static_cast<int>(doc.at("M").as_integer("M"));
+  net.mp_bound = doc.at("mp_bound").as_number("mp_bound");
+  const JsonValue& layers = doc.at("layers");
+  if (layers.kind != JsonValue::Array || layers.items.empty())
+    throw DataFormatError("model JSON: layers must be a non-empty array");
+  if (doc.at("I").as_integer("I") != static_cast<long>(layers.items.size()))
+    throw DataFormatError("model JSON: I does not match layers length");
+  for (const JsonValue& e : layers.items)
+    net.layers.push_back(LayerParams{e.at("lambda").as_number("lambda"), e.at("eta").as_number("eta")});
+  try {
+    net.validate();
+  } catch (const std::invalid_argument& err) {
+    throw DataFormatError(std::string("model JSON: ") + err.what());
+  }
+  return net;
+}
+
+void save_network(const UnfoldedNetwork& net, const std::string& path) {
+  const std::filesystem::path target(path);
+  std::filesystem::path temp = target;
+  temp += ".tmp";
+  {
+    std::ofstream out(temp, std::ios::binary | std::ios::trunc);
+    if (!out) throw std::runtime_error("cannot open for writing: " + temp.string());
+    out << to_json_string(net);
+    out.flush();
+    if (!out) throw std::runtime_error("write failed: " + temp.string());
+  }
+  std::filesystem::rename(temp, target);
+}
+
+UnfoldedNetwork load_network(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw DataFormatError("cannot open model file: " + path);
+  std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  return network_from_json_string(text);
 }
 
 }  // namespace ufpgd
