@@ -2050,8 +2050,20 @@ cudaError_t launch_tile(const FusedArgs& a, bool pgd, cudaStream_t s, long long*
   return cudaGetLastError();
 }
 
-using Tile_16_128 = Tile<16, 128, 1, 8>;
-using Tile_32_256 = Tile<32, 256, 4, 8>;
+#ifndef UFPGD_T32_NW
+#define UFPGD_T32_NW 8
+#endif
+#ifndef UFPGD_T32_TA
+#define UFPGD_T32_TA 4
+#endif
+#ifndef UFPGD_T16_NW
+#define UFPGD_T16_NW 1
+#endif
+#ifndef UFPGD_T16_TA
+#define UFPGD_T16_TA 8
+#endif
+using Tile_16_128 = Tile<16, 128, UFPGD_T16_NW, UFPGD_T16_TA>;
+using Tile_32_256 = Tile<32, 256, UFPGD_T32_NW, UFPGD_T32_TA>;
 
 // Team shapes (K, M) -> (TK, TM): KA = K/TK = 2 users and MB = M/TM antennas
 // per thread keep W, X' and the next X' in registers.
