@@ -74,6 +74,11 @@ __device__ __forceinline__ void cmac_conj(float2& acc, float2 a, float2 b) {
 #ifndef UFPGD_ABL
 #define UFPGD_ABL 0
 #endif
+// 1: two sweeps per layer (stage 2 + prox, then stage 1 re-reading H), so X'
+// and the next X' are never live together (A/B knob).
+#ifndef UFPGD_TWO_SWEEP
+#define UFPGD_TWO_SWEEP 1
+#endif
 // Independent accumulation chains per stage-2 output pair (4 or 8).
 #ifndef UFPGD_S2CH
 #define UFPGD_S2CH 4
@@ -152,13 +157,22 @@ struct ColPtr {
   }
 };
 
-template <class S>
+// LDS.128 the compiler may not merge with an identical earlier load.
+__device__ __forceinline__ float4 lds128_fresh(const float* p) {
+  float4 v;
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+
+template <class S, bool FRESH = false>
 __device__ __forceinline__ void load_col(const ColPtr<S>& cp, int i, float2 (&h)[S::K]) {
   static_assert(S::TM % 2 == 0, "swizzle split needs an even TM");
   const int ci = S::U >= 4 ? (i * (S::TM / 2)) & (S::U - 1) : 0;  // folds: i is unrolled
 #pragma unroll
   for (int q = 0; q < S::U; ++q) {
-    const float4 t = *reinterpret_cast<const float4*>(cp.u[q ^ ci] + i * S::TM * S::HS);
+    const float* ptr = cp.u[q ^ ci] + i * S::TM * S::HS;
+    const float4 t = FRESH ? lds128_fresh(ptr) : *reinterpret_cast<const float4*>(ptr);
     h[2 * q] = make_float2(t.x, t.y);
     h[2 * q + 1] = make_float2(t.z, t.w);
   }
@@ -224,7 +238,7 @@ __device__ __forceinline__ void xacc_init(XAcc<S>& x, const float2 (&cdiag)[S::P
     }
 }
 
-template <class S>
+template <class S, bool FRESH = false>
 __device__ __forceinline__ void team_stage1(const float2 (&wr)[S::MB][S::P], const float2 (&wi)[S::MB][S::P],
                                             XAcc<S>& x, const float* hs, int a, int b,
                                             const float2 (&cdiag)[S::P]) {
@@ -234,7 +248,7 @@ __device__ __forceinline__ void team_stage1(const float2 (&wr)[S::MB][S::P], con
 #pragma unroll
   for (int i = 0; i < S::MB; ++i) {
     float2 h[S::K];
-    load_col<S>(cp, i, h);
+    load_col<S, FRESH>(cp, i, h);
     stage1_accumulate<S>(xn, wr[i], wi[i], h);
   }
   allreduce<S>(xn, x);
@@ -520,7 +534,13 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
   for (long long l = 0; l + 1 < L; ++l) {
     const float eta = PGD ? eta_b : p.eta[l];
     const float thr = PGD ? thr_b : p.thr[l];
+#if UFPGD_TWO_SWEEP
+    team_layer<S, false, false>(wr, wi, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
+    __syncwarp();  // scheduling fence: the next X' is built only after every prox
+    team_stage1<S, true>(wr, wi, x, hs, a, b, cdiag);
+#else
     team_layer<S, true, false>(wr, wi, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
+#endif
     if (nonfinite && first_bad < 0) first_bad = l;
   }
   if (L >= 1) {
@@ -2026,13 +2046,16 @@ __global__ void __launch_bounds__(256) fp32_peak_kernel(const float* __restrict_
 
 template <class S>
 cudaError_t launch_team(const FusedArgs& a, bool pgd, cudaStream_t s, long long* nblocks) {
-  auto kern = pgd ? fused_kernel<S, true, S::MAXT, S::MINB> : fused_kernel<S, false, S::MAXT, S::MINB>;
+  // The unfolded kernel takes the Team's launch bounds; the PGD kernel (power
+  // iteration prologue, more live state) keeps 256 x 1 (no register cap).
+  auto kern = pgd ? fused_kernel<S, true, 256, 1> : fused_kernel<S, false, S::MAXT, S::MINB>;
+  const int maxt = pgd ? 256 : S::MAXT;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kFusedMaxWarps * S::SMEM_PER_WARP);
   if (e != cudaSuccess) return e;
   int nw = pick_warps(S::R, a.B);
   if (const char* f = std::getenv("UFPGD_FUSED_WARPS")) nw = std::max(1, std::min(8, std::atoi(f)));
-  nw = std::min(nw, S::MAXT / 32);
+  nw = std::min(nw, maxt / 32);
   const long long rpb = static_cast<long long>(nw) * S::R;
   const long long blocks = (a.B + rpb - 1) / rpb;
   if (nblocks) *nblocks = blocks;
@@ -2068,11 +2091,13 @@ using Tile_32_256 = Tile<32, 256, UFPGD_T32_NW, UFPGD_T32_TA>;
 // Team shapes (K, M) -> (TK, TM): KA = K/TK = 2 users and MB = M/TM antennas
 // per thread keep W, X' and the next X' in registers.
 using Team_4_32 = Team<4, 32, 2, 4>;
+// Config 2's unfolded kernel: two sweeps per layer fit 168 registers without
+// spills, so 3 resident 4-warp blocks (12 warps/SM) — 3% over 8 warps at 255.
 #ifndef UFPGD_T864_MAXT
-#define UFPGD_T864_MAXT 256
+#define UFPGD_T864_MAXT 128
 #endif
 #ifndef UFPGD_T864_MINB
-#define UFPGD_T864_MINB 1
+#define UFPGD_T864_MINB 3
 #endif
 using Team_8_64 = Team<8, 64, 4, 4, UFPGD_T864_MAXT, UFPGD_T864_MINB>;
 
