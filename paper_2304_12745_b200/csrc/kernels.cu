@@ -662,6 +662,12 @@ struct Tile {
   // so the two rows whose bases coincide mod 8 units flip unit parity.
   static __device__ __forceinline__ int wsw(int m) { return ((m * (K / 4)) >> 3) & 1; }
   static __device__ __forceinline__ int woff(int m, int k) { return m * WSTR + 4 * ((k >> 2) ^ wsw(m)) + (k & 3); }
+  // Cross-warp X' partials [jj][k]: the publishing lanes of one STS write rows
+  // tc * 8 + j of the 8 x 8 tile columns; flipping unit bit 0 on odd tile rows
+  // spreads them over all 8 bank groups (2 wavefronts instead of 4).
+  static __device__ __forceinline__ int xpoff(int jj, int k) {
+    return jj * K + 4 * ((k >> 2) ^ ((jj >> 3) & 1)) + (k & 3);
+  }
 };
 
 template <int NW>
@@ -744,8 +750,8 @@ __device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid, 
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int k0 = tr * 8 + 2 * q, jj = tc * 8 + j;
-          *reinterpret_cast<float2*>(part + jj * T::K + k0) = xr[q][j];
-          *reinterpret_cast<float2*>(part + T::K * T::K + jj * T::K + k0) = xi[q][j];
+          *reinterpret_cast<float2*>(part + T::xpoff(jj, k0)) = xr[q][j];
+          *reinterpret_cast<float2*>(part + T::K * T::K + T::xpoff(jj, k0)) = xi[q][j];
         }
     }
     __syncthreads();
@@ -759,8 +765,8 @@ __device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid, 
 #pragma unroll
       for (int w = 0; w < T::NW; ++w) {
         const float* pw = sm + T::OFF_XP + w * 2 * T::K * T::K;
-        re = fadd2(re, *reinterpret_cast<const float2*>(pw + jj * T::K + k0));
-        im = fadd2(im, *reinterpret_cast<const float2*>(pw + T::K * T::K + jj * T::K + k0));
+        re = fadd2(re, *reinterpret_cast<const float2*>(pw + T::xpoff(jj, k0)));
+        im = fadd2(im, *reinterpret_cast<const float2*>(pw + T::K * T::K + T::xpoff(jj, k0)));
       }
       if (k0 == jj) re.x -= c[jj];
       if (k0 + 1 == jj) re.y -= c[jj];
