@@ -7,7 +7,11 @@ KEEP = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active', 'sm__inst_executed.avg.per_cycle_active',
         'l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed',
         'l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum',
-        'l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum', 'sm__cycles_elapsed.avg.per_second']
+        'l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum', 'sm__cycles_elapsed.avg.per_second',
+        'smsp__sass_thread_inst_executed_op_ffma_pred_on.sum.per_cycle_elapsed',
+        'smsp__sass_thread_inst_executed_op_fadd_pred_on.sum.per_cycle_elapsed',
+        'smsp__sass_thread_inst_executed_op_fmul_pred_on.sum.per_cycle_elapsed',
+        'derived__smsp__sass_thread_inst_executed_op_ffma_pred_on_x2']
 
 
 def main(rep, title, out):
