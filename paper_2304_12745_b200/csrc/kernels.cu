@@ -79,9 +79,10 @@ __device__ __forceinline__ void cmac_conj(float2& acc, float2 a, float2 b) {
 #ifndef UFPGD_TWO_SWEEP
 #define UFPGD_TWO_SWEEP 1
 #endif
-// Independent accumulation chains per stage-2 output pair (4 or 8).
+// Accumulation chains per stage-2 output pair: 2 (one per real / imaginary
+// part, K-deep; no merge adds — fastest at 3 warps per scheduler), 4 or 8.
 #ifndef UFPGD_S2CH
-#define UFPGD_S2CH 4
+#define UFPGD_S2CH 2
 #endif
 
 template <int K_, int M_, int TK_, int TM_, int MAXT_ = 256, int MINB_ = 1>
@@ -315,6 +316,15 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
         gr1 = fadd2(gr1, gr3);
         gi0 = fadd2(gi0, gi2);
         gi1 = fadd2(gi1, gi3);
+#elif UFPGD_S2CH == 2
+        // one chain per part, no merge adds (K-deep dependency chains)
+#pragma unroll
+        for (int j = 0; j < S::K; ++j) {
+          gr0 = ffma2(h[u][j].x, x.re[p][j], gr0);
+          gr0 = ffma2(h[u][j].y, x.im[p][j], gr0);
+          gi0 = ffma2(h[u][j].x, x.im[p][j], gi0);
+          gi0 = ffma2(-h[u][j].y, x.re[p][j], gi0);
+        }
 #else
 #pragma unroll
         for (int j = 0; j < S::K; j += 2) {
@@ -328,8 +338,13 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
           gi1 = ffma2(-h[u][j + 1].y, x.re[p][j + 1], gi1);
         }
 #endif
+#if UFPGD_S2CH == 2
+        vr[u][p] = gr0;
+        vi[u][p] = gi0;
+#else
         vr[u][p] = fadd2(gr0, gr1);
         vi[u][p] = fadd2(gi0, gi1);
+#endif
         s2 = __ffma2_rn(vr[u][p], vr[u][p], s2);
         s2 = __ffma2_rn(vi[u][p], vi[u][p], s2);
       }
