@@ -79,6 +79,10 @@ __device__ __forceinline__ void cmac_conj(float2& acc, float2 a, float2 b) {
 #ifndef UFPGD_TWO_SWEEP
 #define UFPGD_TWO_SWEEP 1
 #endif
+// 1: column norms of antenna pairs reduced as packed FP32x2 (needs TEAM_AB 2).
+#ifndef UFPGD_NORM_PAIRS
+#define UFPGD_NORM_PAIRS 1
+#endif
 // Accumulation chains per stage-2 output pair: 2 (one per real / imaginary
 // part, K-deep; no merge adds — fastest at 3 warps per scheduler), 4 or 8.
 #ifndef UFPGD_S2CH
@@ -259,11 +263,11 @@ __device__ __forceinline__ void team_stage1(const float2 (&wr)[S::MB][S::P], con
 // STATS: accumulate ||W||_{2,1} and the active count for this thread's
 // antennas (counted on the a == 0 threads only).
 // Antennas processed together per step of the layer loop (their stage-2
-// contractions, norm shuffles and prox tails are independent). Measured on
-// B200: 1 and 2 run at the same speed (ptxas already interleaves antennas of
-// the unrolled loop), and 2 spills a few registers, so 1.
+// contractions, norm shuffles and prox tails are independent). 2, so the two
+// antennas' squared norms reduce as one packed FP32x2 (UFPGD_NORM_PAIRS):
+// 0.7% over 1 on B200 (alone, batching 2 is no faster than 1).
 #ifndef UFPGD_TEAM_AB
-#define UFPGD_TEAM_AB 1
+#define UFPGD_TEAM_AB 2
 #endif
 
 template <class S, bool STAGE1, bool STATS>
@@ -290,6 +294,9 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
     float2 h[AB][S::K];
     float2 vr[AB][S::P], vi[AB][S::P];
     float s[AB];
+#if UFPGD_NORM_PAIRS
+    float2 s2p[AB];
+#endif
 #pragma unroll
     for (int u = 0; u < AB; ++u) {
       const int i = i0 + u;
@@ -348,13 +355,29 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
         s2 = __ffma2_rn(vr[u][p], vr[u][p], s2);
         s2 = __ffma2_rn(vi[u][p], vi[u][p], s2);
       }
+#if UFPGD_NORM_PAIRS
+      s2p[u] = s2;
+#else
       s[u] = s2.x + s2.y;
+#endif
     }
+#if UFPGD_NORM_PAIRS
+    // two antennas' squared norms as one packed pair: FADD2 for the partial
+    // sum and for each shuffle level
+    static_assert(AB == 2, "norm pairs need antenna batches of 2");
+    float2 sp = fadd2(make_float2(s2p[0].x, s2p[1].x), make_float2(s2p[0].y, s2p[1].y));
+#pragma unroll
+    for (int off = S::TM; off < S::T; off <<= 1)
+      sp = fadd2(sp, make_float2(__shfl_xor_sync(kFull, sp.x, off), __shfl_xor_sync(kFull, sp.y, off)));
+    s[0] = sp.x;
+    s[1] = sp.y;
+#else
     // ||v_m||^2 across the TK threads holding antenna m
 #pragma unroll
     for (int off = S::TM; off < ((UFPGD_ABL & 2) ? S::TM : S::T); off <<= 1)
 #pragma unroll
       for (int u = 0; u < AB; ++u) s[u] += __shfl_xor_sync(kFull, s[u], off);
+#endif
 #pragma unroll
     for (int u = 0; u < AB; ++u) {
       const int i = i0 + u;
