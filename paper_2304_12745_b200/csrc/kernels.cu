@@ -666,13 +666,14 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
 #endif
 constexpr int kTileUnroll = UFPGD_TILE_UNROLL;  // stage-2 j-loop unroll (A/B builds)
 
-template <int K_, int M_, int NW_, int TA_>
+template <int K_, int M_, int NW_, int TA_, int TS_ = 8>
 struct Tile {
   static constexpr int K = K_, M = M_, NW = NW_, NT = 32 * NW_, TA = TA_;
+  static constexpr int TS = TS_;             // stage-1 X' tile: TS x TS per thread
   static constexpr int TR = 8;               // stage-2 users per thread (4 FFMA2 pairs)
   static constexpr int RG = K / TR;          // user groups
   static constexpr int AG = M / TA;          // antenna groups
-  static constexpr int XT = (K / 8) * (K / 8);  // 8 x 8 tiles of X'
+  static constexpr int XT = (K / TS) * (K / TS);  // TS x TS tiles of X'
   static constexpr int S = NT / XT;          // antenna slices of stage 1
   static constexpr int MS = M / S;           // antennas per slice
   static constexpr int HSTR = 2 * K;         // floats, unpadded (XOR-swizzled units)
@@ -689,6 +690,7 @@ struct Tile {
   static constexpr int SMEM = SMEM_FLOATS * 4;
   static_assert(RG * AG == NT, "stage-2 tiles must cover V exactly");
   static_assert(NT % XT == 0 && XT <= 32 && 32 % XT == 0, "stage-1 tiles within a warp");
+  static_assert(TS == 8 || (TS == 4 && NW == 1), "4 x 4 stage-1 tiles only without cross-warp partials");
   static_assert(M % S == 0, "");
   static_assert(K >= 16 && 8 % RG == 0, "swizzles assume >= 8 H units per row");
   // H(c, m): 16-byte unit (c >> 1) of row m, XOR-swizzled by m mod (8 / RG):
@@ -720,13 +722,14 @@ __device__ __forceinline__ void cta_sync() {
 // split X' planes (Xre/Xim[j][k]).
 template <class T>
 __device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid, float neta) {
+  constexpr int TS = T::TS, TQ = TS / 2;  // users per tile side, user pairs per tile row
   const int t = tid % T::XT, s = tid / T::XT;
-  const int tr = t % (T::K / 8), tc = t / (T::K / 8);
-  float2 xr[4][8], xi[4][8];
+  const int tr = t % (T::K / TS), tc = t / (T::K / TS);
+  float2 xr[TQ][TS], xi[TQ][TS];
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < TQ; ++q)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < TS; ++j) {
       xr[q][j] = zero2();
       xi[q][j] = zero2();
     }
@@ -736,25 +739,27 @@ __device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid, 
 #pragma unroll 2
   for (int i = 0; i < T::MS; ++i) {
     const int m = i * T::S + s;
-    const float4 a0 = *reinterpret_cast<const float4*>(Wre + T::woff(m, tr * 8));
-    const float4 a1 = *reinterpret_cast<const float4*>(Wre + T::woff(m, tr * 8 + 4));
-    const float4 b0 = *reinterpret_cast<const float4*>(Wim + T::woff(m, tr * 8));
-    const float4 b1 = *reinterpret_cast<const float4*>(Wim + T::woff(m, tr * 8 + 4));
-    const float2 wr[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w), make_float2(a1.x, a1.y),
-                          make_float2(a1.z, a1.w)};
-    const float2 wi[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
-                          make_float2(b1.z, b1.w)};
-    float2 h[8];
+    float2 wr[TQ], wi[TQ];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float4 v = *reinterpret_cast<const float4*>(Hs + T::hoff(m, tc * 8 + 2 * q));
+    for (int u = 0; u < TS / 4; ++u) {
+      const float4 a = *reinterpret_cast<const float4*>(Wre + T::woff(m, tr * TS + 4 * u));
+      const float4 b = *reinterpret_cast<const float4*>(Wim + T::woff(m, tr * TS + 4 * u));
+      wr[2 * u] = make_float2(a.x, a.y);
+      wr[2 * u + 1] = make_float2(a.z, a.w);
+      wi[2 * u] = make_float2(b.x, b.y);
+      wi[2 * u + 1] = make_float2(b.z, b.w);
+    }
+    float2 h[TS];
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) {
+      const float4 v = *reinterpret_cast<const float4*>(Hs + T::hoff(m, tc * TS + 2 * q));
       h[2 * q] = make_float2(v.x, v.y);
       h[2 * q + 1] = make_float2(v.z, v.w);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < TQ; ++q)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < TS; ++j) {
         xr[q][j] = ffma2(h[j].x, wr[q], xr[q][j]);
         xr[q][j] = ffma2(-h[j].y, wi[q], xr[q][j]);
         xi[q][j] = ffma2(h[j].x, wi[q], xi[q][j]);
@@ -763,9 +768,9 @@ __device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid, 
   }
   // reduce the slices held by lanes of this warp (lane bits >= log2(XT))
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < TQ; ++q)
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < TS; ++j)
 #pragma unroll
       for (int off = T::XT; off < 32; off <<= 1) {
         xr[q][j] = fadd2(xr[q][j], make_float2(__shfl_xor_sync(kFull, xr[q][j].x, off),
@@ -784,10 +789,10 @@ __device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid, 
     float* part = sm + T::OFF_XP + warp * 2 * T::K * T::K;
     if (lane < T::XT) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < TQ; ++q)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int k0 = tr * 8 + 2 * q, jj = tc * 8 + j;
+        for (int j = 0; j < TS; ++j) {
+          const int k0 = tr * TS + 2 * q, jj = tc * TS + j;
           *reinterpret_cast<float2*>(part + T::xpoff(jj, k0)) = xr[q][j];
           *reinterpret_cast<float2*>(part + T::K * T::K + T::xpoff(jj, k0)) = xi[q][j];
         }
@@ -813,10 +818,10 @@ __device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid, 
     }
   } else if (warp == 0 && lane < T::XT) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < TQ; ++q)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int k0 = tr * 8 + 2 * q, jj = tc * 8 + j;
+      for (int j = 0; j < TS; ++j) {
+        const int k0 = tr * TS + 2 * q, jj = tc * TS + j;
         float2 r = xr[q][j];
         if (tr == tc) {  // diagonal tile: k == j at compile-time positions
           if (2 * q == j) r.x -= c[jj];
@@ -2129,7 +2134,10 @@ cudaError_t launch_tile(const FusedArgs& a, bool pgd, cudaStream_t s, long long*
 #ifndef UFPGD_T16_TA
 #define UFPGD_T16_TA 8
 #endif
-using Tile_16_128 = Tile<16, 128, UFPGD_T16_NW, UFPGD_T16_TA>;
+#ifndef UFPGD_T16_TS
+#define UFPGD_T16_TS 4
+#endif
+using Tile_16_128 = Tile<16, 128, UFPGD_T16_NW, UFPGD_T16_TA, UFPGD_T16_TS>;
 using Tile_32_256 = Tile<32, 256, UFPGD_T32_NW, UFPGD_T32_TA>;
 
 // Team shapes (K, M) -> (TK, TM): KA = K/TK = 2 users and MB = M/TM antennas
