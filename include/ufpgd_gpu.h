@@ -214,6 +214,8 @@ int ufpgd_gpu_pgd_fixed_host(const ufpgd_c64* H, int64_t B, int K, int M, int po
  * 0..ngpus-1 (one host thread and stream per device) and reduce the three
  * summary statistics with one ncclAllReduce over an NCCL communicator built by
  * ufpgd_gpu_init (ncclCommInitAll). Host buffers, synchronous.
+ * ufpgd_gpu_shutdown destroys the communicators and releases the per-device
+ * workspaces of the host-buffer entry points (they are re-created on demand).
  */
 int ufpgd_gpu_init(int ngpus);
 int ufpgd_gpu_shutdown(void);

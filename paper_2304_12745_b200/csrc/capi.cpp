@@ -197,7 +197,7 @@ bool load_nccl() {
          g_nccl.CommDestroy;
 }
 
-// Per-device workspace of the host-buffer path: three streams and grow-only
+// Per-device workspace of the host-buffer path: NS streams and grow-only
 // device buffers, kept across calls so an end-to-end call costs only its
 // copies and kernels. Host calls on one device are serialised by its mutex.
 struct HostWorkspace {
@@ -227,8 +227,6 @@ cudaError_t ensure(void*& p, size_t& cap, size_t need) {
   return e;
 }
 
-// Chunked host pipeline shared by the unfolded and PGD host entry points.
-// `run` enqueues the kernel for one chunk on stream s given device buffers.
 // Pipeline chunk size in bytes of H (UFPGD_HOST_CHUNK_MB overrides, for tuning).
 long long host_chunk_bytes(long long default_mb) {
   long long mb = default_mb;
@@ -236,6 +234,32 @@ long long host_chunk_bytes(long long default_mb) {
   return mb << 20;
 }
 
+// Releases a device's host-path workspace (ufpgd_gpu_shutdown).
+void release_workspace(HostWorkspace& ws) {
+  std::lock_guard<std::mutex> lock(ws.mu);
+  if (!ws.init) return;
+  for (int i = 0; i < HostWorkspace::NS; ++i) {
+    cudaStreamSynchronize(ws.st[i]);
+    for (int q = 0; q < 5; ++q) {
+      if (ws.buf[i][q]) cudaFree(ws.buf[i][q]);
+      ws.buf[i][q] = nullptr;
+      ws.cap[i][q] = 0;
+    }
+    cudaStreamDestroy(ws.st[i]);
+    ws.st[i] = nullptr;
+  }
+  if (ws.partials) cudaFree(ws.partials);
+  if (ws.dstats) cudaFree(ws.dstats);
+  if (ws.pinned) cudaFreeHost(ws.pinned);
+  ws.partials = nullptr;
+  ws.dstats = nullptr;
+  ws.pinned = nullptr;
+  ws.partials_cap = ws.pinned_cap = 0;
+  ws.init = false;
+}
+
+// Chunked host pipeline shared by the unfolded and PGD host entry points.
+// `run` enqueues the kernel for one chunk on stream s given device buffers.
 template <class Run>
 int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const ufpgd_c64* W0,
                   ufpgd_c64* W, int32_t* diverged_at, float* eta_out, long long parts_per_chunk_max,
@@ -914,10 +938,19 @@ int ufpgd_gpu_init(int ngpus) {
 }
 
 int ufpgd_gpu_shutdown(void) {
-  std::lock_guard<std::mutex> lock(g_nccl_mu);
-  for (ncclComm_t c : g_comms)
-    if (c) g_nccl.CommDestroy(c);
-  g_comms.clear();
+  {
+    std::lock_guard<std::mutex> lock(g_nccl_mu);
+    for (ncclComm_t c : g_comms)
+      if (c) g_nccl.CommDestroy(c);
+    g_comms.clear();
+  }
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) count = 0;
+  for (int d = 0; d < count && d < 64; ++d) {
+    if (!g_ws[d].init) continue;
+    DeviceGuard g(d);
+    release_workspace(g_ws[d]);
+  }
   return UFPGD_OK;
 }
 
