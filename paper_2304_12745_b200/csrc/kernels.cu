@@ -15,14 +15,15 @@
 // realization for ALL layers. Thread (a, b) of the team holds, in registers,
 //   w[i][kk] = W(k = a*KA + kk, m = i*TM + b)     (KA users x MB antennas)
 //   x[kk][j] = X'(a*KA + kk, j)                   (its KA rows of X')
-// and H lives in shared memory (row stride padded so the quarter-warp LDS.128
-// phases are bank-conflict free). One pass over the thread's antennas per
-// layer does stage 2 + prox for antenna m and, with the same H column still in
-// registers, accumulates antenna m's contribution to the NEXT layer's X'
-// (stage 1). Warp shuffles do the two reductions: the per-antenna norm across
-// the TK threads sharing an antenna, and the X' all-reduce across the TM
-// threads sharing rows (once per layer). H is read from HBM once
-// (ld.global.nc, streaming) and W written once (st.global.cs).
+// packed over user pairs for FFMA2, and H lives in shared memory (unpadded
+// rows, 16-byte units XOR-swizzled so the quarter-warp LDS.128 phases are
+// bank-conflict free). Per layer: stage 2 + prox over the thread's antennas,
+// then (two-sweep mode) stage 1 over them again, building the NEXT layer's X'
+// — so X' and the next X' are never live at once and the unfolded kernel fits
+// 168 registers (12 warps/SM). Warp shuffles do the two reductions: the
+// per-antenna norm across the TK threads sharing an antenna, and the X'
+// all-reduce across the TM threads sharing rows (once per layer). H is read
+// from HBM once (ld.global.nc, streaming) and W written once (st.global.cs).
 #include <cfloat>
 #include <climits>
 #include <cstdint>
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
   const bool valid = rid < p.B;
   float* hs = smem + (warp * S::R + team) * (S::M * S::HS);
 
-  // Stage H once: coalesced streaming float4 loads into the padded tile.
+  // Stage H once: coalesced streaming float4 loads into the swizzled tile.
   {
     constexpr int NV = S::M * S::K / 2;
     const float4* hg = reinterpret_cast<const float4*>(p.H) + (valid ? rid : 0LL) * NV;
