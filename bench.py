@@ -373,8 +373,9 @@ def run_ours(args, world, rank, local):
                 "nominal_peak": nominal_tflops, "frac_of_nominal": achieved / nominal_tflops,
                 "kernel": "fused_kernel<Team<8,64,4,4>> (+stats_finalize)", "kernel_ms": kern_ms,
                 "flops_per_launch": flops,
-                "flops_model": "(2L-1)*8*K^2*M + 10*K*M*L per realization (W0 = 0: layer-0 W H^T is zero "
-                               "and not computed); SURVEY §8d counts 2L contractions",
+                "flops_model": "(2L-2)*8*K^2*M + 10*K*M*L per realization (W0 = 0: neither layer-0 "
+                               "contraction is computed — W0 H^T is zero and X' = -diag(c)); SURVEY §8d "
+                               "counts 2L contractions",
                 "hbm": {"achieved_GBps": hbm_bytes / (kern_ms * 1e-3) / 1e9, "peak_GBps": 6547.8,
                         "frac": hbm_bytes / (kern_ms * 1e-3) / 1e9 / 6547.8,
                         "bytes_per_launch": hbm_bytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},

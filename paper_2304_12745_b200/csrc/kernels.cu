@@ -84,6 +84,10 @@ __device__ __forceinline__ void cmac_conj(float2& acc, float2 a, float2 b) {
 #ifndef UFPGD_NORM_PAIRS
 #define UFPGD_NORM_PAIRS 1
 #endif
+// 1: layer 0 from W0 = 0 as the exact diagonal shortcut (team kernel).
+#ifndef UFPGD_DIAG_LAYER0
+#define UFPGD_DIAG_LAYER0 1
+#endif
 // Accumulation chains per stage-2 output pair: 2 (one per real / imaginary
 // part, K-deep; no merge adds — fastest at 3 warps per scheduler), 4 or 8.
 #ifndef UFPGD_S2CH
@@ -407,6 +411,60 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
   if (STAGE1) allreduce<S>(xn, x);
 }
 
+// Layer 0 from W0 = 0 (BASELINE configs 1, 2): X' = -diag(c) exactly, so
+// V = W0 - eta X' H^* is eta c_k conj(H(k, m)) — the K x K x M contraction of
+// a diagonal matrix reduces to two FMUL2 per antenna on the thread's own rows
+// (bit-identical to running the contraction on the exact zeros). ceta holds
+// (eta c_k0, eta c_k0+1) per user pair.
+template <class S, bool STATS>
+__device__ __forceinline__ void team_layer0_diag(float2 (&wr)[S::MB][S::P], float2 (&wi)[S::MB][S::P],
+                                                 const float* hs, int a, int b, float thr,
+                                                 const float2 (&ceta)[S::P], bool& nonfinite, float& l21,
+                                                 int& act) {
+  const float thr2 = thr * thr;
+#pragma unroll
+  for (int i0 = 0; i0 < S::MB; i0 += 2) {
+    float2 vr[2][S::P], vi[2][S::P], s2p[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int m = (i0 + u) * S::TM + b;
+      float2 s2 = zero2();
+#pragma unroll
+      for (int p = 0; p < S::P; ++p) {
+        // H(k0, m), H(k0 + 1, m): one 16-byte unit of the swizzled row
+        const float4 h = *reinterpret_cast<const float4*>(S::hat(hs, m, a * S::KA + 2 * p));
+        vr[u][p] = __fmul2_rn(ceta[p], make_float2(h.x, h.z));
+        vi[u][p] = __fmul2_rn(ceta[p], make_float2(-h.y, -h.w));
+        s2 = __ffma2_rn(vr[u][p], vr[u][p], s2);
+        s2 = __ffma2_rn(vi[u][p], vi[u][p], s2);
+      }
+      s2p[u] = s2;
+    }
+    float2 sp = fadd2(make_float2(s2p[0].x, s2p[1].x), make_float2(s2p[0].y, s2p[1].y));
+#pragma unroll
+    for (int off = S::TM; off < S::T; off <<= 1)
+      sp = fadd2(sp, make_float2(__shfl_xor_sync(kFull, sp.x, off), __shfl_xor_sync(kFull, sp.y, off)));
+    const float sv[2] = {sp.x, sp.y};
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = i0 + u;
+      nonfinite |= !(sv[u] <= FLT_MAX);
+      const bool on = sv[u] > thr2;
+      const float r = rsqrt_ftz(fmaxf(sv[u], FLT_MIN));
+      const float scale = on ? fmaf(-thr, r, 1.f) : 0.f;
+#pragma unroll
+      for (int p = 0; p < S::P; ++p) {
+        wr[i][p] = fmul2(scale, vr[u][p]);
+        wi[i][p] = fmul2(scale, vi[u][p]);
+      }
+      if (STATS && a == 0 && on) {
+        l21 += fmaf(sv[u], r, -thr);
+        act += 1;
+      }
+    }
+  }
+}
+
 // Fixed-step power iteration on H^T H^* (pgd.cpp:146-162 with the BASELINE
 // 30-step rule) for the team's realization; every team thread returns the
 // Rayleigh quotient Re(v^H w) of the last step. Control flow is uniform
@@ -570,7 +628,25 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
   float l21 = 0.f;
   int act = 0;
   const long long L = p.L;
-  for (long long l = 0; l + 1 < L; ++l) {
+  long long l0 = 0;
+  if (!PGD && UFPGD_DIAG_LAYER0 && p.w0_mode == UFPGD_W0_ZERO && L >= 1) {
+    static_assert(S::MB % 2 == 0, "layer-0 path pairs antennas");
+    float2 ceta[S::P];
+#pragma unroll
+    for (int q = 0; q < S::P; ++q) {
+      const int k0 = a * S::KA + 2 * q;
+      ceta[q] = make_float2(p.eta[0] * p.c[k0], p.eta[0] * p.c[k0 + 1]);
+    }
+    if (L == 1) {
+      team_layer0_diag<S, true>(wr, wi, hs, a, b, p.thr[0], ceta, nonfinite, l21, act);
+    } else {
+      team_layer0_diag<S, false>(wr, wi, hs, a, b, p.thr[0], ceta, nonfinite, l21, act);
+      team_stage1<S, true>(wr, wi, x, hs, a, b, cdiag);  // X' for layer 1
+    }
+    if (nonfinite) first_bad = 0;
+    l0 = 1;
+  }
+  for (long long l = l0; l + 1 < L; ++l) {
     const float eta = PGD ? eta_b : p.eta[l];
     const float thr = PGD ? thr_b : p.thr[l];
 #if UFPGD_TWO_SWEEP
@@ -582,7 +658,7 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
 #endif
     if (nonfinite && first_bad < 0) first_bad = l;
   }
-  if (L >= 1) {
+  if (L >= 1 && L > l0) {
     const float eta = PGD ? eta_b : p.eta[L - 1];
     const float thr = PGD ? thr_b : p.thr[L - 1];
     team_layer<S, false, true>(wr, wi, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
@@ -836,10 +912,13 @@ __device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid, 
 }
 
 // Stage 2 + prox for the thread's 8 users x TA antennas, W updated in place.
-template <class T, bool STATS>
+// DIAG0: layer 0 from W0 = 0, where X' = -diag(c) exactly and V(k, m) is
+// eta c_k conj(H(k, m)) — the contraction of a diagonal X' is skipped
+// (bit-identical to running it on the exact zeros); c = the kernel's c[K].
+template <class T, bool STATS, bool DIAG0 = false>
 __device__ __forceinline__ void tile_stage2(float* sm, int tid, float eta, float thr, bool& nonfinite,
-                                            float& l21, int& act) {
-  (void)eta;  // folded into X' by tile_stage1
+                                            float& l21, int& act, const float* c = nullptr) {
+  (void)eta;  // folded into X' by tile_stage1 (used directly on the DIAG0 path)
   const int rg = tid % T::RG, ag = tid / T::RG;
   const int k0 = rg * 8;
   const float* Hs = sm + T::OFF_H;
@@ -849,6 +928,20 @@ __device__ __forceinline__ void tile_stage2(float* sm, int tid, float eta, float
   const float* Xim = sm + T::OFF_XI;
   // Accumulators start at W (X' arrives scaled by -eta): they end as V.
   float2 gr[4][T::TA], gi[4][T::TA];
+  if constexpr (DIAG0) {
+#pragma unroll
+    for (int i = 0; i < T::TA; ++i) {
+      const int m = i * T::AG + ag;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + 2 * q;
+        const float4 h = *reinterpret_cast<const float4*>(Hs + T::hoff(m, k));  // H(k, m), H(k + 1, m)
+        const float2 ce = make_float2(eta * c[k], eta * c[k + 1]);  // = the -eta-folded X'(k, k)
+        gr[q][i] = __fmul2_rn(ce, make_float2(h.x, h.z));
+        gi[q][i] = __fmul2_rn(ce, make_float2(-h.y, -h.w));
+      }
+    }
+  } else {
 #pragma unroll
   for (int i = 0; i < T::TA; ++i) {
     const int m = i * T::AG + ag;
@@ -899,6 +992,7 @@ __device__ __forceinline__ void tile_stage2(float* sm, int tid, float eta, float
         gi[q][i] = ffma2(-h.w, xr[1][q], gi[q][i]);
       }
     }
+  }
   }
   const float thr2 = thr * thr;
 #pragma unroll
@@ -1064,7 +1158,18 @@ __global__ void __launch_bounds__(T::NT) tile_kernel(const __grid_constant__ Fus
   long long first_bad = -1;
   float l21 = 0.f;
   int act = 0;
-  for (long long l = 0; l < p.L; ++l) {
+  long long l0 = 0;
+  if (!PGD && UFPGD_DIAG_LAYER0 && p.w0_mode == UFPGD_W0_ZERO && p.L >= 1) {
+    if (p.L == 1) {
+      tile_stage2<T, true, true>(sm, tid, p.eta[0], p.thr[0], nonfinite, l21, act, p.c);
+    } else {
+      tile_stage2<T, false, true>(sm, tid, p.eta[0], p.thr[0], nonfinite, l21, act, p.c);
+      tile_stage1<T>(sm, p.c, tid, -p.eta[1]);
+    }
+    if (nonfinite) first_bad = 0;
+    l0 = 1;
+  }
+  for (long long l = l0; l < p.L; ++l) {
     const float eta = PGD ? eta_b : p.eta[l];
     const float thr = PGD ? thr_b : p.thr[l];
     if (l + 1 < p.L) {

@@ -76,10 +76,11 @@ class Workload:
 
     def flops_per_realization(self, exact_w0: bool = True) -> float:
         """SURVEY §8d cost model: L (16 K^2 M + 10 K M) (+ power steps).
-        exact_w0: with W0 = 0 the layer-0 product W H^T is identically zero and
-        is not computed, so one of the 2L contractions is not counted."""
+        exact_w0: with W0 = 0 the kernels compute neither layer-0 contraction
+        (W0 H^T is identically zero and X' = -diag(c) makes the second a
+        per-entry scaling), so 2L - 2 contractions are counted, not 2L."""
         K, M, L = self.K, self.M, self.L
-        contractions = 2 * L - (1 if (exact_w0 and self.w0_mode == capi.W0_ZERO) else 0)
+        contractions = 2 * L - (2 if (exact_w0 and self.w0_mode == capi.W0_ZERO) else 0)
         f = contractions * 8 * K * K * M + L * 10 * K * M
         if self.kind == "pgd":
             f += self.power_steps * (16 * K * M + 14 * M)
