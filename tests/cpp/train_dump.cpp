@@ -3,6 +3,7 @@
 // UnfoldedNetwork::pgd_init start and prints the history and the trained
 // parameters as one JSON object.
 //   train_dump train.ufpd val.ufpd L lambda0 loss_kind lambda_cost batch lr epochs patience seed
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <exception>
@@ -30,15 +31,22 @@ int main(int argc, char** argv) {
     tc.max_epochs = std::atoi(argv[9]);
     tc.patience = std::atoi(argv[10]);
     tc.seed = std::strtoull(argv[11], nullptr, 10);
+    if (std::getenv("UFPGD_TRAIN_WARMUP")) {  // exclude CUDA context / module load from train_seconds
+      ufpgd::TrainConfig warm = tc;
+      warm.max_epochs = 1;
+      (void)ufpgd::train(net, tr, va, warm, sys);
+    }
+    const auto t0 = std::chrono::steady_clock::now();
     const ufpgd::TrainResult r = ufpgd::train(net, tr, va, tc, sys);
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     std::printf("{\"epochs\": [");
     for (std::size_t i = 0; i < r.history.epochs.size(); ++i) {
       const ufpgd::EpochRecord& e = r.history.epochs[i];
       std::printf("%s[%ld, %.17g, %.17g, %.17g, %.17g]", i ? ", " : "", e.epoch, e.train_loss, e.val_loss,
                   e.val_mean_pcg, e.val_mean_sum_rate);
     }
-    std::printf("], \"best_epoch\": %ld, \"stopping_epoch\": %ld, \"params\": [", r.history.best_epoch,
-                r.history.stopping_epoch);
+    std::printf("], \"train_seconds\": %.6f, \"best_epoch\": %ld, \"stopping_epoch\": %ld, \"params\": [", secs,
+                r.history.best_epoch, r.history.stopping_epoch);
     for (std::size_t i = 0; i < r.network.layers.size(); ++i)
       std::printf("%s%.17g, %.17g", i ? ", " : "", r.network.layers[i].lambda_i, r.network.layers[i].eta_i);
     std::printf("]}\n");
