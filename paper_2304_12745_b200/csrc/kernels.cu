@@ -70,28 +70,10 @@ __device__ __forceinline__ void cmac_conj(float2& acc, float2 a, float2 b) {
   acc.y = fmaf(-a.x, b.y, acc.y);
 }
 
-// Timing-only ablations for development (results are wrong when set):
-// bit 0 drops the X' all-reduce shuffles, bit 1 the column-norm shuffles.
-#ifndef UFPGD_ABL
-#define UFPGD_ABL 0
-#endif
 // 1: two sweeps per layer (stage 2 + prox, then stage 1 re-reading H), so X'
-// and the next X' are never live together (A/B knob).
+// and the next X' are never live together (A/B knob; 0 = one fused sweep).
 #ifndef UFPGD_TWO_SWEEP
 #define UFPGD_TWO_SWEEP 1
-#endif
-// 1: column norms of antenna pairs reduced as packed FP32x2 (needs TEAM_AB 2).
-#ifndef UFPGD_NORM_PAIRS
-#define UFPGD_NORM_PAIRS 1
-#endif
-// 1: layer 0 from W0 = 0 as the exact diagonal shortcut (team kernel).
-#ifndef UFPGD_DIAG_LAYER0
-#define UFPGD_DIAG_LAYER0 1
-#endif
-// Accumulation chains per stage-2 output pair: 2 (one per real / imaginary
-// part, K-deep; no merge adds — fastest at 3 warps per scheduler), 4 or 8.
-#ifndef UFPGD_S2CH
-#define UFPGD_S2CH 2
 #endif
 
 template <int K_, int M_, int TK_, int TM_, int MAXT_ = 256, int MINB_ = 1>
@@ -220,7 +202,7 @@ __device__ __forceinline__ void allreduce(XAcc<S>& xn, XAcc<S>& x) {
     for (int j = 0; j < S::K; ++j) {
       float2 r = xn.re[p][j], i = xn.im[p][j];
 #pragma unroll
-      for (int off = 1; off < ((UFPGD_ABL & 1) ? 1 : S::TM); off <<= 1) {
+      for (int off = 1; off < S::TM; off <<= 1) {
         const float2 ro = make_float2(__shfl_xor_sync(kFull, r.x, off), __shfl_xor_sync(kFull, r.y, off));
         const float2 io = make_float2(__shfl_xor_sync(kFull, i.x, off), __shfl_xor_sync(kFull, i.y, off));
         r = fadd2(r, ro);
@@ -267,20 +249,19 @@ __device__ __forceinline__ void team_stage1(const float2 (&wr)[S::MB][S::P], con
 // One layer (or PGD iteration). STAGE1: also build X' for the next layer.
 // STATS: accumulate ||W||_{2,1} and the active count for this thread's
 // antennas (counted on the a == 0 threads only).
-// Antennas processed together per step of the layer loop (their stage-2
-// contractions, norm shuffles and prox tails are independent). 2, so the two
-// antennas' squared norms reduce as one packed FP32x2 (UFPGD_NORM_PAIRS):
-// 0.7% over 1 on B200 (alone, batching 2 is no faster than 1).
-#ifndef UFPGD_TEAM_AB
-#define UFPGD_TEAM_AB 2
-#endif
+// Antennas go in pairs (their stage-2 contractions, norm shuffles and prox
+// tails are independent), so the two squared column norms reduce as one
+// packed FP32x2. Each stage-2 output part is ONE K-deep FFMA2 chain started
+// at W (no merge adds) — measured fastest at 3 warps per scheduler, against
+// 2- and 4-chain splits.
 
 template <class S, bool STAGE1, bool STATS>
 __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&wi)[S::MB][S::P], XAcc<S>& x,
                                            const float* hs, int a, int b, float eta, float thr,
                                            const float2 (&cdiag)[S::P], bool& nonfinite, float& l21,
                                            int& act) {
-  constexpr int AB = (S::MB % UFPGD_TEAM_AB == 0) ? UFPGD_TEAM_AB : 1;
+  constexpr int AB = 2;
+  static_assert(S::MB % AB == 0, "antennas are processed in pairs");
   XAcc<S> xn;
   if (STAGE1) xacc_init<S>(xn, cdiag, a);
   const float thr2 = thr * thr;
@@ -298,10 +279,7 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
   for (int i0 = 0; i0 < S::MB; i0 += AB) {
     float2 h[AB][S::K];
     float2 vr[AB][S::P], vi[AB][S::P];
-    float s[AB];
-#if UFPGD_NORM_PAIRS
     float2 s2p[AB];
-#endif
 #pragma unroll
     for (int u = 0; u < AB; ++u) {
       const int i = i0 + u;
@@ -310,79 +288,28 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
       float2 s2 = zero2();
 #pragma unroll
       for (int p = 0; p < S::P; ++p) {
-        float2 gr0 = wr[i][p], gr1 = zero2(), gi0 = wi[i][p], gi1 = zero2();
-#if UFPGD_S2CH == 8
-        float2 gr2 = zero2(), gr3 = zero2(), gi2 = zero2(), gi3 = zero2();
-#pragma unroll
-        for (int j = 0; j < S::K; j += 2) {
-          gr0 = ffma2(h[u][j].x, x.re[p][j], gr0);
-          gr2 = ffma2(h[u][j].y, x.im[p][j], gr2);
-          gi0 = ffma2(h[u][j].x, x.im[p][j], gi0);
-          gi2 = ffma2(-h[u][j].y, x.re[p][j], gi2);
-          gr1 = ffma2(h[u][j + 1].x, x.re[p][j + 1], gr1);
-          gr3 = ffma2(h[u][j + 1].y, x.im[p][j + 1], gr3);
-          gi1 = ffma2(h[u][j + 1].x, x.im[p][j + 1], gi1);
-          gi3 = ffma2(-h[u][j + 1].y, x.re[p][j + 1], gi3);
-        }
-        gr0 = fadd2(gr0, gr2);
-        gr1 = fadd2(gr1, gr3);
-        gi0 = fadd2(gi0, gi2);
-        gi1 = fadd2(gi1, gi3);
-#elif UFPGD_S2CH == 2
-        // one chain per part, no merge adds (K-deep dependency chains)
+        float2 gr = wr[i][p], gi = wi[i][p];
 #pragma unroll
         for (int j = 0; j < S::K; ++j) {
-          gr0 = ffma2(h[u][j].x, x.re[p][j], gr0);
-          gr0 = ffma2(h[u][j].y, x.im[p][j], gr0);
-          gi0 = ffma2(h[u][j].x, x.im[p][j], gi0);
-          gi0 = ffma2(-h[u][j].y, x.re[p][j], gi0);
+          gr = ffma2(h[u][j].x, x.re[p][j], gr);
+          gr = ffma2(h[u][j].y, x.im[p][j], gr);
+          gi = ffma2(h[u][j].x, x.im[p][j], gi);
+          gi = ffma2(-h[u][j].y, x.re[p][j], gi);
         }
-#else
-#pragma unroll
-        for (int j = 0; j < S::K; j += 2) {
-          gr0 = ffma2(h[u][j].x, x.re[p][j], gr0);
-          gr0 = ffma2(h[u][j].y, x.im[p][j], gr0);
-          gi0 = ffma2(h[u][j].x, x.im[p][j], gi0);
-          gi0 = ffma2(-h[u][j].y, x.re[p][j], gi0);
-          gr1 = ffma2(h[u][j + 1].x, x.re[p][j + 1], gr1);
-          gr1 = ffma2(h[u][j + 1].y, x.im[p][j + 1], gr1);
-          gi1 = ffma2(h[u][j + 1].x, x.im[p][j + 1], gi1);
-          gi1 = ffma2(-h[u][j + 1].y, x.re[p][j + 1], gi1);
-        }
-#endif
-#if UFPGD_S2CH == 2
-        vr[u][p] = gr0;
-        vi[u][p] = gi0;
-#else
-        vr[u][p] = fadd2(gr0, gr1);
-        vi[u][p] = fadd2(gi0, gi1);
-#endif
+        vr[u][p] = gr;
+        vi[u][p] = gi;
         s2 = __ffma2_rn(vr[u][p], vr[u][p], s2);
         s2 = __ffma2_rn(vi[u][p], vi[u][p], s2);
       }
-#if UFPGD_NORM_PAIRS
       s2p[u] = s2;
-#else
-      s[u] = s2.x + s2.y;
-#endif
     }
-#if UFPGD_NORM_PAIRS
-    // two antennas' squared norms as one packed pair: FADD2 for the partial
-    // sum and for each shuffle level
-    static_assert(AB == 2, "norm pairs need antenna batches of 2");
+    // the pair's squared norms as one packed FP32x2: partial sum, then the
+    // shuffle levels across the TK threads holding each antenna
     float2 sp = fadd2(make_float2(s2p[0].x, s2p[1].x), make_float2(s2p[0].y, s2p[1].y));
 #pragma unroll
     for (int off = S::TM; off < S::T; off <<= 1)
       sp = fadd2(sp, make_float2(__shfl_xor_sync(kFull, sp.x, off), __shfl_xor_sync(kFull, sp.y, off)));
-    s[0] = sp.x;
-    s[1] = sp.y;
-#else
-    // ||v_m||^2 across the TK threads holding antenna m
-#pragma unroll
-    for (int off = S::TM; off < ((UFPGD_ABL & 2) ? S::TM : S::T); off <<= 1)
-#pragma unroll
-      for (int u = 0; u < AB; ++u) s[u] += __shfl_xor_sync(kFull, s[u], off);
-#endif
+    const float s[AB] = {sp.x, sp.y};
 #pragma unroll
     for (int u = 0; u < AB; ++u) {
       const int i = i0 + u;
@@ -629,7 +556,7 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
   int act = 0;
   const long long L = p.L;
   long long l0 = 0;
-  if (!PGD && UFPGD_DIAG_LAYER0 && p.w0_mode == UFPGD_W0_ZERO && L >= 1) {
+  if (!PGD && p.w0_mode == UFPGD_W0_ZERO && L >= 1) {
     static_assert(S::MB % 2 == 0, "layer-0 path pairs antennas");
     float2 ceta[S::P];
 #pragma unroll
@@ -738,10 +665,6 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
 // 16-byte units XOR-swizzled per row (Tile::hoff / woff) so the LDS.128 /
 // STS.128 phases of both stages are conflict-free.
 // ---------------------------------------------------------------------------
-#ifndef UFPGD_TILE_UNROLL
-#define UFPGD_TILE_UNROLL 1
-#endif
-constexpr int kTileUnroll = UFPGD_TILE_UNROLL;  // stage-2 j-loop unroll (A/B builds)
 
 template <int K_, int M_, int NW_, int TA_, int TS_ = 8>
 struct Tile {
@@ -958,7 +881,7 @@ __device__ __forceinline__ void tile_stage2(float* sm, int tid, float eta, float
     gi[2][i] = make_float2(b1.x, b1.y);
     gi[3][i] = make_float2(b1.z, b1.w);
   }
-#pragma unroll kTileUnroll
+#pragma unroll 1  // unroll 2 measured slower at (16,128)
   for (int j = 0; j < T::K; j += 2) {
     float2 xr[2][4], xi[2][4];
 #pragma unroll
@@ -1159,7 +1082,7 @@ __global__ void __launch_bounds__(T::NT) tile_kernel(const __grid_constant__ Fus
   float l21 = 0.f;
   int act = 0;
   long long l0 = 0;
-  if (!PGD && UFPGD_DIAG_LAYER0 && p.w0_mode == UFPGD_W0_ZERO && p.L >= 1) {
+  if (!PGD && p.w0_mode == UFPGD_W0_ZERO && p.L >= 1) {
     if (p.L == 1) {
       tile_stage2<T, true, true>(sm, tid, p.eta[0], p.thr[0], nonfinite, l21, act, p.c);
     } else {
