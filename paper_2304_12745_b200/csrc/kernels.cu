@@ -2180,7 +2180,10 @@ using Team_4_32 = Team<4, 32, 2, 4>;
 #ifndef UFPGD_T864_MINB
 #define UFPGD_T864_MINB 3
 #endif
-using Team_8_64 = Team<8, 64, 4, 4, UFPGD_T864_MAXT, UFPGD_T864_MINB>;
+#ifndef UFPGD_T864_TK
+#define UFPGD_T864_TK 4
+#endif
+using Team_8_64 = Team<8, 64, UFPGD_T864_TK, 16 / UFPGD_T864_TK, UFPGD_T864_MAXT, UFPGD_T864_MINB>;
 
 }  // namespace
 
