@@ -6,12 +6,12 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC -Xcompiler -Wall -
 PKG      := paper_2304_12745_b200
 LIBDIR   := $(PKG)/lib
 OBJDIR   := build/obj
-SRCS_CU  := $(PKG)/csrc/kernels.cu
+SRCS_CU  := $(addprefix $(PKG)/csrc/,team.cu tile.cu general.cu metrics.cu grad.cu datagen.cu probe.cu)
 SRCS_CPP := $(PKG)/csrc/capi.cpp $(PKG)/csrc/host_gen.cpp $(PKG)/csrc/api.cpp $(PKG)/csrc/dataset_io.cpp
 CXX      ?= g++
 CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -Iinclude -I$(PKG)/csrc -I/usr/local/cuda/include
 OBJS     := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(SRCS_CU)) $(patsubst $(PKG)/csrc/%.cpp,$(OBJDIR)/%.o,$(SRCS_CPP))
-HDRS     := include/ufpgd_gpu.h $(PKG)/csrc/ufpgd_internal.h $(wildcard include/ufpgd/*.hpp)
+HDRS     := include/ufpgd_gpu.h $(PKG)/csrc/ufpgd_internal.h $(PKG)/csrc/device_common.cuh $(wildcard include/ufpgd/*.hpp)
 
 all: $(LIBDIR)/libufpgd_gpu.so oracle build/test_api build/train_dump build/test_json
 

@@ -3,7 +3,7 @@
 Python bindings over the C ABI in ``include/ufpgd_gpu.h`` (built into
 ``paper_2304_12745_b200/lib/libufpgd_gpu.so`` for sm_100a). Torch provides
 device memory and streams; every computation runs in the hand-written CUDA
-kernels of ``csrc/kernels.cu``. There is no CPU fallback: importing works
+kernels of ``csrc/*.cu``. There is no CPU fallback: importing works
 without a GPU, but every compute call raises if the library or the device is
 missing.
 

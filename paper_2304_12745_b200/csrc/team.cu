@@ -1,0 +1,683 @@
+// sm_100a kernels for the batched PA-aware precoder solver.
+//
+// Hot path: per realization
+// and per layer
+//     X' = W H^T - diag(c)            (K x K, contraction over the M antennas)
+//     V  = W - eta X' H^*             (K x M, contraction over the K users)
+//     w_m = max(0, 1 - t/||v_m||) v_m  (per-antenna group soft threshold)
+// which is unfolded.cpp:112-146 / pgd.cpp:226-244 with the constraint term
+// folded into X' (diag(c) H^* = (diag(c)) H^*, so X' H^* = grad_f(W),
+// pgd.hpp:41-47). The fold is exact algebra; it removes the K x M offset
+// matrix of SmoothGradient (pgd.cpp:51-59) and keeps FP32 error small over
+// thousands of iterations.
+//
+// Fused team kernel (fused_kernel): a team of T = TK*TM threads owns one
+// realization for ALL layers. Thread (a, b) of the team holds, in registers,
+//   w[i][kk] = W(k = a*KA + kk, m = i*TM + b)     (KA users x MB antennas)
+//   x[kk][j] = X'(a*KA + kk, j)                   (its KA rows of X')
+// packed over user pairs for FFMA2, and H lives in shared memory (unpadded
+// rows, 16-byte units XOR-swizzled so the quarter-warp LDS.128 phases are
+// bank-conflict free). Per layer: stage 2 + prox over the thread's antennas,
+// then (two-sweep mode) stage 1 over them again, building the NEXT layer's X'
+// — so X' and the next X' are never live at once and the unfolded kernel fits
+// 168 registers (12 warps/SM). Warp shuffles do the two reductions: the
+// per-antenna norm across the TK threads sharing an antenna, and the X'
+// all-reduce across the TM threads sharing rows (once per layer). H is read
+// from HBM once (ld.global.nc, streaming) and W written once (st.global.cs).
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+#include <cstdlib>
+#include <cmath>
+#include <algorithm>
+
+#include "ufpgd_internal.h"
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <algorithm>
+
+#include "device_common.cuh"
+
+namespace ufpgd_gpu_impl {
+namespace {
+
+// 1: two sweeps per layer (stage 2 + prox, then stage 1 re-reading H), so X'
+// and the next X' are never live together (A/B knob; 0 = one fused sweep).
+#ifndef UFPGD_TWO_SWEEP
+#define UFPGD_TWO_SWEEP 1
+#endif
+
+template <int K_, int M_, int TK_, int TM_, int MAXT_ = 256, int MINB_ = 1>
+struct Team {
+  static constexpr int K = K_, M = M_, TK = TK_, TM = TM_;
+  // launch bounds: register cap = 64K / (MAXT * MINB)
+  static constexpr int MAXT = MAXT_, MINB = MINB_;
+  static constexpr int T = TK * TM;     // threads per realization
+  static constexpr int R = 32 / T;      // realizations per warp
+  static constexpr int KA = K / TK;     // users per thread
+  static constexpr int P = KA / 2;      // user pairs per thread (FFMA2 lanes)
+  static constexpr int MB = M / TM;     // antennas per thread
+  static constexpr int HS = 2 * K;      // H row stride in floats (XOR-swizzled units, no padding)
+  static constexpr int U = K / 2;       // 16-byte units per H row
+  static constexpr int SMEM_PER_WARP = R * M * HS * 4;
+  // Unit swizzle of row m: with U >= 4 units per row, rows m and m + 2 of a
+  // quarter-warp LDS.128 phase would hit the same banks; XOR-ing the unit
+  // index with (m >> 1) mod U separates them. U <= 2 is conflict-free as is.
+  static __device__ __forceinline__ int swz(int m) { return U >= 4 ? (m >> 1) & (U - 1) : 0; }
+  // Address of complex H(c, m) (user c, antenna m) in the tile.
+  static __device__ __forceinline__ const float* hat(const float* hs, int m, int c) {
+    return hs + m * HS + 4 * ((c >> 1) ^ swz(m)) + 2 * (c & 1);
+  }
+  static_assert(32 % T == 0, "a team must divide the warp");
+  static_assert(K % TK == 0 && M % TM == 0, "team must tile (K, M)");
+  static_assert(KA % 2 == 0 && K % 2 == 0, "users are processed in FFMA2 pairs");
+};
+
+// Loads row m of H (all K users, complex) from shared memory.
+template <class S>
+__device__ __forceinline__ void load_col(const float* hs, int m, float2 (&h)[S::K]) {
+  const float4* hp = reinterpret_cast<const float4*>(hs + m * S::HS);
+  const int f = S::swz(m);
+#pragma unroll
+  for (int q = 0; q < S::K / 2; ++q) {
+    const float4 t = hp[q ^ f];
+    h[2 * q] = make_float2(t.x, t.y);
+    h[2 * q + 1] = make_float2(t.z, t.w);
+  }
+}
+
+// Per-thread H row pointers: with TM even, the unit swizzle of antenna
+// m = i * TM + b splits into a compile-time part (from i) XOR a per-thread part
+// (from b), so u[q] = row b, unit q ^ swz_b, and column i, unit q is
+// u[q ^ swz_i] + i * TM * HS: an immediate offset from one of U registers, no
+// per-load address arithmetic in the unrolled layer loop.
+template <class S>
+struct ColPtr {
+  const float* u[S::U];
+  __device__ __forceinline__ ColPtr(const float* hs, int b) {
+    const int fb = S::U >= 4 ? (b >> 1) & (S::U - 1) : 0;
+#pragma unroll
+    for (int q = 0; q < S::U; ++q) u[q] = hs + b * S::HS + 4 * (q ^ fb);
+  }
+};
+
+// LDS.128 the compiler may not merge with an identical earlier load.
+__device__ __forceinline__ float4 lds128_fresh(const float* p) {
+  float4 v;
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+
+template <class S, bool FRESH = false>
+__device__ __forceinline__ void load_col(const ColPtr<S>& cp, int i, float2 (&h)[S::K]) {
+  static_assert(S::TM % 2 == 0, "swizzle split needs an even TM");
+  const int ci = S::U >= 4 ? (i * (S::TM / 2)) & (S::U - 1) : 0;  // folds: i is unrolled
+#pragma unroll
+  for (int q = 0; q < S::U; ++q) {
+    const float* ptr = cp.u[q ^ ci] + i * S::TM * S::HS;
+    const float4 t = FRESH ? lds128_fresh(ptr) : *reinterpret_cast<const float4*>(ptr);
+    h[2 * q] = make_float2(t.x, t.y);
+    h[2 * q + 1] = make_float2(t.z, t.w);
+  }
+}
+
+// Split-complex accumulators of the thread's rows of X' (stage 1 output).
+template <class S>
+struct XAcc {
+  float2 re[S::P][S::K], im[S::P][S::K];
+};
+
+// Stage 1 contribution of antenna m: X'(k, j) += W(k, m) H(j, m).
+template <class S>
+__device__ __forceinline__ void stage1_accumulate(XAcc<S>& xn, const float2 (&wr)[S::P],
+                                                  const float2 (&wi)[S::P], const float2 (&h)[S::K]) {
+#pragma unroll
+  for (int p = 0; p < S::P; ++p)
+#pragma unroll
+    for (int j = 0; j < S::K; ++j) {
+      xn.re[p][j] = ffma2(h[j].x, wr[p], xn.re[p][j]);
+      xn.re[p][j] = ffma2(-h[j].y, wi[p], xn.re[p][j]);
+      xn.im[p][j] = ffma2(h[j].x, wi[p], xn.im[p][j]);
+      xn.im[p][j] = ffma2(h[j].y, wr[p], xn.im[p][j]);
+    }
+}
+
+// All-reduce of the stage-1 partials across the TM threads sharing rows. The
+// constraint fold X'(k, k) -= c_k is already in the partials: the b == 0
+// thread of each row group starts its accumulation from -diag(c) (xacc_init).
+template <class S>
+__device__ __forceinline__ void allreduce(XAcc<S>& xn, XAcc<S>& x) {
+#pragma unroll
+  for (int p = 0; p < S::P; ++p)
+#pragma unroll
+    for (int j = 0; j < S::K; ++j) {
+      float2 r = xn.re[p][j], i = xn.im[p][j];
+#pragma unroll
+      for (int off = 1; off < S::TM; off <<= 1) {
+        const float2 ro = make_float2(__shfl_xor_sync(kFull, r.x, off), __shfl_xor_sync(kFull, r.y, off));
+        const float2 io = make_float2(__shfl_xor_sync(kFull, i.x, off), __shfl_xor_sync(kFull, i.y, off));
+        r = fadd2(r, ro);
+        i = fadd2(i, io);
+      }
+      x.re[p][j] = r;
+      x.im[p][j] = i;
+    }
+}
+
+// Start value of the stage-1 accumulators: -diag(c) on the thread's rows for
+// the b == 0 thread (so the all-reduce applies the fold exactly once), zero
+// elsewhere. cdiag[p] = (-c_k0, -c_k0+1) or zero, precomputed per thread.
+template <class S>
+__device__ __forceinline__ void xacc_init(XAcc<S>& x, const float2 (&cdiag)[S::P], int a) {
+#pragma unroll
+  for (int p = 0; p < S::P; ++p)
+#pragma unroll
+    for (int j = 0; j < S::K; ++j) {
+      // j is compile-time; the row pair (k0, k0+1) = (a*KA + 2p, +1) is not:
+      // only j in that pair gets a non-zero start, selected with one compare.
+      const int k0 = a * S::KA + 2 * p;
+      x.re[p][j] = make_float2(j == k0 ? cdiag[p].x : 0.f, j == k0 + 1 ? cdiag[p].y : 0.f);
+      x.im[p][j] = zero2();
+    }
+}
+
+template <class S, bool FRESH = false>
+__device__ __forceinline__ void team_stage1(const float2 (&wr)[S::MB][S::P], const float2 (&wi)[S::MB][S::P],
+                                            XAcc<S>& x, const float* hs, int a, int b,
+                                            const float2 (&cdiag)[S::P]) {
+  XAcc<S> xn;
+  xacc_init<S>(xn, cdiag, a);
+  const ColPtr<S> cp(hs, b);
+#pragma unroll
+  for (int i = 0; i < S::MB; ++i) {
+    float2 h[S::K];
+    load_col<S, FRESH>(cp, i, h);
+    stage1_accumulate<S>(xn, wr[i], wi[i], h);
+  }
+  allreduce<S>(xn, x);
+}
+
+// One layer (or PGD iteration). STAGE1: also build X' for the next layer.
+// STATS: accumulate ||W||_{2,1} and the active count for this thread's
+// antennas (counted on the a == 0 threads only).
+// Antennas go in pairs (their stage-2 contractions, norm shuffles and prox
+// tails are independent), so the two squared column norms reduce as one
+// packed FP32x2. Each stage-2 output part is ONE K-deep FFMA2 chain started
+// at W (no merge adds) — measured fastest at 3 warps per scheduler, against
+// 2- and 4-chain splits.
+
+template <class S, bool STAGE1, bool STATS>
+__device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&wi)[S::MB][S::P], XAcc<S>& x,
+                                           const float* hs, int a, int b, float eta, float thr,
+                                           const float2 (&cdiag)[S::P], bool& nonfinite, float& l21,
+                                           int& act) {
+  constexpr int AB = 2;
+  static_assert(S::MB % AB == 0, "antennas are processed in pairs");
+  XAcc<S> xn;
+  if (STAGE1) xacc_init<S>(xn, cdiag, a);
+  const float thr2 = thr * thr;
+  const ColPtr<S> cp(hs, b);
+  // Fold the step into X' once per layer (X' <- -eta X'), so each antenna's
+  // stage-2 chains start from W and V = W - eta G needs no extra FFMA2.
+#pragma unroll
+  for (int p = 0; p < S::P; ++p)
+#pragma unroll
+    for (int j = 0; j < S::K; ++j) {
+      x.re[p][j] = fmul2(-eta, x.re[p][j]);
+      x.im[p][j] = fmul2(-eta, x.im[p][j]);
+    }
+#pragma unroll
+  for (int i0 = 0; i0 < S::MB; i0 += AB) {
+    float2 h[AB][S::K];
+    float2 vr[AB][S::P], vi[AB][S::P];
+    float2 s2p[AB];
+#pragma unroll
+    for (int u = 0; u < AB; ++u) {
+      const int i = i0 + u;
+      load_col<S>(cp, i, h[u]);
+      // stage 2: G(k, m) = sum_j X'(k, j) conj(H(j, m)); V = W - eta G
+      float2 s2 = zero2();
+#pragma unroll
+      for (int p = 0; p < S::P; ++p) {
+        float2 gr = wr[i][p], gi = wi[i][p];
+#pragma unroll
+        for (int j = 0; j < S::K; ++j) {
+          gr = ffma2(h[u][j].x, x.re[p][j], gr);
+          gr = ffma2(h[u][j].y, x.im[p][j], gr);
+          gi = ffma2(h[u][j].x, x.im[p][j], gi);
+          gi = ffma2(-h[u][j].y, x.re[p][j], gi);
+        }
+        vr[u][p] = gr;
+        vi[u][p] = gi;
+        s2 = __ffma2_rn(vr[u][p], vr[u][p], s2);
+        s2 = __ffma2_rn(vi[u][p], vi[u][p], s2);
+      }
+      s2p[u] = s2;
+    }
+    // the pair's squared norms as one packed FP32x2: partial sum, then the
+    // shuffle levels across the TK threads holding each antenna
+    float2 sp = fadd2(make_float2(s2p[0].x, s2p[1].x), make_float2(s2p[0].y, s2p[1].y));
+#pragma unroll
+    for (int off = S::TM; off < S::T; off <<= 1)
+      sp = fadd2(sp, make_float2(__shfl_xor_sync(kFull, sp.x, off), __shfl_xor_sync(kFull, sp.y, off)));
+    const float s[AB] = {sp.x, sp.y};
+#pragma unroll
+    for (int u = 0; u < AB; ++u) {
+      const int i = i0 + u;
+      // Non-finite step image (unfolded.cpp:120-125): any NaN/Inf entry of
+      // v_m makes its squared column norm NaN/Inf. (A finite column whose
+      // squared norm overflows FP32, |v| > ~6e18, is flagged too.)
+      nonfinite |= !(s[u] <= FLT_MAX);
+      // prox (pgd.cpp:85-99): strict ||v|| > t, i.e. s > t^2
+      const bool on = s[u] > thr2;
+      const float r = rsqrt_ftz(fmaxf(s[u], FLT_MIN));  // s = 0 or subnormal only matters at thr = 0
+      const float scale = on ? fmaf(-thr, r, 1.f) : 0.f;
+#pragma unroll
+      for (int p = 0; p < S::P; ++p) {
+        wr[i][p] = fmul2(scale, vr[u][p]);
+        wi[i][p] = fmul2(scale, vi[u][p]);
+      }
+      if (STATS) {
+        if (a == 0 && on) {
+          l21 += fmaf(s[u], r, -thr);  // ||w_m|| = ||v_m|| - t
+          act += 1;
+        }
+      }
+      if (STAGE1) stage1_accumulate<S>(xn, wr[i], wi[i], h[u]);
+    }
+  }
+  if (STAGE1) allreduce<S>(xn, x);
+}
+
+// Layer 0 from W0 = 0 (BASELINE configs 1, 2): X' = -diag(c) exactly, so
+// V = W0 - eta X' H^* is eta c_k conj(H(k, m)) — the K x K x M contraction of
+// a diagonal matrix reduces to two FMUL2 per antenna on the thread's own rows
+// (bit-identical to running the contraction on the exact zeros). ceta holds
+// (eta c_k0, eta c_k0+1) per user pair.
+template <class S, bool STATS>
+__device__ __forceinline__ void team_layer0_diag(float2 (&wr)[S::MB][S::P], float2 (&wi)[S::MB][S::P],
+                                                 const float* hs, int a, int b, float thr,
+                                                 const float2 (&ceta)[S::P], bool& nonfinite, float& l21,
+                                                 int& act) {
+  const float thr2 = thr * thr;
+#pragma unroll
+  for (int i0 = 0; i0 < S::MB; i0 += 2) {
+    float2 vr[2][S::P], vi[2][S::P], s2p[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int m = (i0 + u) * S::TM + b;
+      float2 s2 = zero2();
+#pragma unroll
+      for (int p = 0; p < S::P; ++p) {
+        // H(k0, m), H(k0 + 1, m): one 16-byte unit of the swizzled row
+        const float4 h = *reinterpret_cast<const float4*>(S::hat(hs, m, a * S::KA + 2 * p));
+        vr[u][p] = __fmul2_rn(ceta[p], make_float2(h.x, h.z));
+        vi[u][p] = __fmul2_rn(ceta[p], make_float2(-h.y, -h.w));
+        s2 = __ffma2_rn(vr[u][p], vr[u][p], s2);
+        s2 = __ffma2_rn(vi[u][p], vi[u][p], s2);
+      }
+      s2p[u] = s2;
+    }
+    float2 sp = fadd2(make_float2(s2p[0].x, s2p[1].x), make_float2(s2p[0].y, s2p[1].y));
+#pragma unroll
+    for (int off = S::TM; off < S::T; off <<= 1)
+      sp = fadd2(sp, make_float2(__shfl_xor_sync(kFull, sp.x, off), __shfl_xor_sync(kFull, sp.y, off)));
+    const float sv[2] = {sp.x, sp.y};
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = i0 + u;
+      nonfinite |= !(sv[u] <= FLT_MAX);
+      const bool on = sv[u] > thr2;
+      const float r = rsqrt_ftz(fmaxf(sv[u], FLT_MIN));
+      const float scale = on ? fmaf(-thr, r, 1.f) : 0.f;
+#pragma unroll
+      for (int p = 0; p < S::P; ++p) {
+        wr[i][p] = fmul2(scale, vr[u][p]);
+        wi[i][p] = fmul2(scale, vi[u][p]);
+      }
+      if (STATS && a == 0 && on) {
+        l21 += fmaf(sv[u], r, -thr);
+        act += 1;
+      }
+    }
+  }
+}
+
+// Fixed-step power iteration on H^T H^* (pgd.cpp:146-162 with the BASELINE
+// 30-step rule) for the team's realization; every team thread returns the
+// Rayleigh quotient Re(v^H w) of the last step. Control flow is uniform
+// across the warp (all teams run `steps` steps) so the shuffles stay legal.
+template <class S>
+__device__ float team_power(const float* hs, const float2* v0, int steps, int a, int b) {
+  float2 v[S::MB];
+#pragma unroll
+  for (int i = 0; i < S::MB; ++i) v[i] = v0[i * S::TM + b];
+  float est = 0.f;
+  bool zero = false;
+  for (int st = 0; st < steps; ++st) {
+    float2 u[S::KA];
+#pragma unroll
+    for (int jj = 0; jj < S::KA; ++jj) u[jj] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < S::MB; ++i) {
+#pragma unroll
+      for (int jj = 0; jj < S::KA; ++jj) {
+        const float2 hv = *reinterpret_cast<const float2*>(S::hat(hs, i * S::TM + b, a * S::KA + jj));
+        cmac(u[jj], v[i], make_float2(hv.x, -hv.y));
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < S::KA; ++jj)
+#pragma unroll
+      for (int off = 1; off < S::TM; off <<= 1) {
+        u[jj].x += __shfl_xor_sync(kFull, u[jj].x, off);
+        u[jj].y += __shfl_xor_sync(kFull, u[jj].y, off);
+      }
+    float dot = 0.f, wn2 = 0.f;
+    float2 wv[S::MB];
+#pragma unroll
+    for (int i = 0; i < S::MB; ++i) {
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int jj = 0; jj < S::KA; ++jj)
+        cmac(acc, *reinterpret_cast<const float2*>(S::hat(hs, i * S::TM + b, a * S::KA + jj)), u[jj]);
+#pragma unroll
+      for (int off = S::TM; off < S::T; off <<= 1) {
+        acc.x += __shfl_xor_sync(kFull, acc.x, off);
+        acc.y += __shfl_xor_sync(kFull, acc.y, off);
+      }
+      wv[i] = acc;
+      dot = fmaf(v[i].x, acc.x, fmaf(v[i].y, acc.y, dot));
+      wn2 = fmaf(acc.x, acc.x, fmaf(acc.y, acc.y, wn2));
+    }
+#pragma unroll
+    for (int off = 1; off < S::TM; off <<= 1) {
+      dot += __shfl_xor_sync(kFull, dot, off);
+      wn2 += __shfl_xor_sync(kFull, wn2, off);
+    }
+    if (!zero) {
+      if (wn2 == 0.f) {
+        zero = true;  // pgd.cpp:150-153: an all-zero channel has L = 0
+        est = 0.f;
+      } else {
+        est = dot;
+        const float inv = 1.f / sqrtf(wn2);
+#pragma unroll
+        for (int i = 0; i < S::MB; ++i) v[i] = make_float2(wv[i].x * inv, wv[i].y * inv);
+      }
+    }
+  }
+  return est;
+}
+
+template <class S, bool PGD, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant__ FusedArgs p) {
+  extern __shared__ __align__(16) float smem[];
+  __shared__ double red[kFusedMaxWarps][3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int team = lane / S::T, tl = lane % S::T, a = tl / S::TM, b = tl % S::TM;
+  const long long rid = (static_cast<long long>(blockIdx.x) * nwarps + warp) * S::R + team;
+  const bool valid = rid < p.B;
+  float* hs = smem + (warp * S::R + team) * (S::M * S::HS);
+
+  // Stage H once: coalesced streaming float4 loads into the swizzled tile.
+  {
+    constexpr int NV = S::M * S::K / 2;
+    const float4* hg = reinterpret_cast<const float4*>(p.H) + (valid ? rid : 0LL) * NV;
+    float4 buf[NV / S::T];
+#pragma unroll
+    for (int q = 0; q < NV / S::T; ++q)
+      buf[q] = valid ? ldg_stream(hg + tl + q * S::T) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < NV / S::T; ++q) {
+      const int e = 2 * (tl + q * S::T);
+      *reinterpret_cast<float4*>(const_cast<float*>(S::hat(hs, e / S::K, e % S::K))) = buf[q];
+    }
+    __syncwarp();
+  }
+
+  // W(a*KA + 2p + {0,1}, i*TM + b), split into real / imaginary user pairs.
+  float2 wr[S::MB][S::P], wi[S::MB][S::P];
+  XAcc<S> x;
+  float2 cdiag[S::P];
+#pragma unroll
+  for (int q = 0; q < S::P; ++q) {
+    const int k0 = a * S::KA + 2 * q;
+    cdiag[q] = b == 0 ? make_float2(-p.c[k0], -p.c[k0 + 1]) : zero2();
+  }
+  if (p.w0_mode == UFPGD_W0_ZERO) {
+#pragma unroll
+    for (int i = 0; i < S::MB; ++i)
+#pragma unroll
+      for (int q = 0; q < S::P; ++q) {
+        wr[i][q] = zero2();
+        wi[i][q] = zero2();
+      }
+    // X' = 0 H^T - diag(c): the layer-0 product is identically zero.
+#pragma unroll
+    for (int q = 0; q < S::P; ++q)
+#pragma unroll
+      for (int j = 0; j < S::K; ++j) {
+        const int k0 = a * S::KA + 2 * q;
+        x.re[q][j] = make_float2(j == k0 ? -p.c[j] : 0.f, j == k0 + 1 ? -p.c[j] : 0.f);
+        x.im[q][j] = zero2();
+      }
+  } else {
+    if (p.w0_mode == UFPGD_W0_CONJ_H) {
+#pragma unroll
+      for (int i = 0; i < S::MB; ++i) {
+#pragma unroll
+        for (int q = 0; q < S::P; ++q) {
+          const float4 t = *reinterpret_cast<const float4*>(S::hat(hs, i * S::TM + b, a * S::KA + 2 * q));
+          wr[i][q] = make_float2(t.x, t.z);
+          wi[i][q] = make_float2(-t.y, -t.w);
+        }
+      }
+    } else {
+      const float2* w0 = p.W0 + (valid ? rid : 0LL) * (S::M * S::K);
+#pragma unroll
+      for (int i = 0; i < S::MB; ++i)
+#pragma unroll
+        for (int q = 0; q < S::P; ++q) {
+          const float4 t = valid ? ldg_stream(reinterpret_cast<const float4*>(
+                                       w0 + (i * S::TM + b) * S::K + a * S::KA + 2 * q))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+          wr[i][q] = make_float2(t.x, t.z);
+          wi[i][q] = make_float2(t.y, t.w);
+        }
+    }
+    team_stage1<S>(wr, wi, x, hs, a, b, cdiag);
+  }
+
+  float eta_b = 0.f, thr_b = 0.f;
+  if (PGD) {
+    if (p.eta_in) {
+      eta_b = valid ? p.eta_in[rid] : 1.f;
+    } else {
+      const float Lb = team_power<S>(hs, p.v0, p.power_steps, a, b);
+      eta_b = 1.f / Lb;
+    }
+    thr_b = p.lambda * eta_b;
+    if (p.eta_out && valid && tl == 0) p.eta_out[rid] = eta_b;
+  }
+
+  bool nonfinite = false;
+  long long first_bad = -1;
+  float l21 = 0.f;
+  int act = 0;
+  const long long L = p.L;
+  long long l0 = 0;
+  if (!PGD && p.w0_mode == UFPGD_W0_ZERO && L >= 1) {
+    static_assert(S::MB % 2 == 0, "layer-0 path pairs antennas");
+    float2 ceta[S::P];
+#pragma unroll
+    for (int q = 0; q < S::P; ++q) {
+      const int k0 = a * S::KA + 2 * q;
+      ceta[q] = make_float2(p.eta[0] * p.c[k0], p.eta[0] * p.c[k0 + 1]);
+    }
+    if (L == 1) {
+      team_layer0_diag<S, true>(wr, wi, hs, a, b, p.thr[0], ceta, nonfinite, l21, act);
+    } else {
+      team_layer0_diag<S, false>(wr, wi, hs, a, b, p.thr[0], ceta, nonfinite, l21, act);
+      team_stage1<S, true>(wr, wi, x, hs, a, b, cdiag);  // X' for layer 1
+    }
+    if (nonfinite) first_bad = 0;
+    l0 = 1;
+  }
+  for (long long l = l0; l + 1 < L; ++l) {
+    const float eta = PGD ? eta_b : p.eta[l];
+    const float thr = PGD ? thr_b : p.thr[l];
+#if UFPGD_TWO_SWEEP
+    team_layer<S, false, false>(wr, wi, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
+    __syncwarp();  // scheduling fence: the next X' is built only after every prox
+    team_stage1<S, true>(wr, wi, x, hs, a, b, cdiag);
+#else
+    team_layer<S, true, false>(wr, wi, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
+#endif
+    if (nonfinite && first_bad < 0) first_bad = l;
+  }
+  if (L >= 1 && L > l0) {
+    const float eta = PGD ? eta_b : p.eta[L - 1];
+    const float thr = PGD ? thr_b : p.thr[L - 1];
+    team_layer<S, false, true>(wr, wi, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
+    if (nonfinite && first_bad < 0) first_bad = L - 1;
+  }
+
+  // Team-wide first divergence (min over the team, -1 = none).
+  long long fb = first_bad < 0 ? LLONG_MAX : first_bad;
+#pragma unroll
+  for (int off = 1; off < S::T; off <<= 1) fb = min(fb, __shfl_xor_sync(kFull, fb, off));
+#pragma unroll
+  for (int off = 1; off < S::TM; off <<= 1) {
+    l21 += __shfl_xor_sync(kFull, l21, off);
+    act += __shfl_xor_sync(kFull, act, off);
+  }
+  const bool diverged = fb != LLONG_MAX;
+
+  if (valid) {
+    float2* wg = p.W + rid * (S::M * S::K);
+#pragma unroll
+    for (int i = 0; i < S::MB; ++i)
+#pragma unroll
+      for (int q = 0; q < S::P; ++q)
+        stg_stream(reinterpret_cast<float4*>(wg + (i * S::TM + b) * S::K + a * S::KA + 2 * q),
+                   make_float4(wr[i][q].x, wi[i][q].x, wr[i][q].y, wi[i][q].y));
+    if (tl == 0) {
+      if (p.diverged_at) p.diverged_at[rid] = diverged ? static_cast<int32_t>(fb + (PGD ? 1 : 0)) : -1;
+      if (p.l21) p.l21[rid] = diverged ? __int_as_float(0x7fc00000) : l21;
+      if (p.active) p.active[rid] = diverged ? -1 : act;
+    }
+  }
+
+  if (p.block_partials) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    if (valid && tl == 0) {
+      if (diverged) {
+        s2 = 1.0;
+      } else {
+        s0 = static_cast<double>(p.alpha) * static_cast<double>(l21);
+        s1 = static_cast<double>(act);
+      }
+    }
+#pragma unroll
+    for (int off = S::T; off < 32; off <<= 1) {
+      s0 += __shfl_xor_sync(kFull, s0, off);
+      s1 += __shfl_xor_sync(kFull, s1, off);
+      s2 += __shfl_xor_sync(kFull, s2, off);
+    }
+    if (lane == 0) {
+      red[warp][0] = s0;
+      red[warp][1] = s1;
+      red[warp][2] = s2;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+      double t = 0.0;
+      for (int q = 0; q < nwarps; ++q) t += red[q][threadIdx.x];
+      p.block_partials[blockIdx.x * 3LL + threadIdx.x] = t;
+    }
+  }
+}
+
+
+// Block geometry. A realization stays resident for all its layers and each
+// warp runs close to its own dependency-latency limit, so the kernel wants the
+// register-limited maximum of 8 resident warps per SM and every SM busy. A
+// sweep of 1..8 warps per block on B200 (tools/sweep_warps.sh)
+// found 1, 2 and 8 equally fast when the grid covers the SMs, so: the largest
+// of {8, 4, 2, 1} whose grid still has at least one block per SM.
+int pick_warps(int rpw, long long B) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // Measured on B200 (tools/nw_sweep.py, quick_time): with many waves 4-warp
+  // blocks beat 8-warp ones by ~2% (a finished block's slot refills sooner);
+  // with under ~4 waves (config 3: 1.7) whole-SM 8-warp blocks are ~2% ahead.
+  const auto blocks = [&](int nw) { return (B + static_cast<long long>(nw) * rpw - 1) / (static_cast<long long>(nw) * rpw); };
+  if (blocks(8) >= sms && blocks(8) < 4LL * sms) return 8;
+  for (int nw = 4; nw > 1; nw >>= 1)
+    if (blocks(nw) >= sms) return nw;
+  return 1;
+}
+
+template <class S>
+cudaError_t launch_team(const FusedArgs& a, bool pgd, cudaStream_t s, long long* nblocks) {
+  // The unfolded kernel takes the Team's launch bounds; the PGD kernel (power
+  // iteration prologue, more live state) keeps 256 x 1 (no register cap).
+  auto kern = pgd ? fused_kernel<S, true, 256, 1> : fused_kernel<S, false, S::MAXT, S::MINB>;
+  const int maxt = pgd ? 256 : S::MAXT;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kFusedMaxWarps * S::SMEM_PER_WARP);
+  if (e != cudaSuccess) return e;
+  int nw = pick_warps(S::R, a.B);
+  if (const char* f = std::getenv("UFPGD_FUSED_WARPS")) nw = std::max(1, std::min(8, std::atoi(f)));
+  nw = std::min(nw, maxt / 32);
+  const long long rpb = static_cast<long long>(nw) * S::R;
+  const long long blocks = (a.B + rpb - 1) / rpb;
+  if (nblocks) *nblocks = blocks;
+  kern<<<static_cast<unsigned>(blocks), nw * 32, nw * S::SMEM_PER_WARP, s>>>(a);
+  return cudaGetLastError();
+}
+
+// Team shapes (K, M) -> (TK, TM): KA = K/TK = 2 users and MB = M/TM antennas
+// per thread keep W, X' and the next X' in registers.
+using Team_4_32 = Team<4, 32, 2, 4>;
+// Config 2's unfolded kernel: two sweeps per layer fit 168 registers without
+// spills, so 3 resident 4-warp blocks (12 warps/SM) — 3% over 8 warps at 255.
+#ifndef UFPGD_T864_MAXT
+#define UFPGD_T864_MAXT 128
+#endif
+#ifndef UFPGD_T864_MINB
+#define UFPGD_T864_MINB 3
+#endif
+#ifndef UFPGD_T864_TK
+#define UFPGD_T864_TK 4
+#endif
+using Team_8_64 = Team<8, 64, UFPGD_T864_TK, 16 / UFPGD_T864_TK, UFPGD_T864_MAXT, UFPGD_T864_MINB>;
+
+}  // namespace
+
+bool fused_supported(int K, int M) {
+  return (K == 4 && M == 32) || (K == 8 && M == 64) || (K == 16 && M == 128) || (K == 32 && M == 256);
+}
+
+// Upper bound on realizations per block (partials are sized with the smallest
+// block the geometry chooser can pick: one warp).
+
+int fused_realizations_per_block(int K, int M) {
+  if (K == 4 && M == 32) return Team_4_32::R;
+  if (K == 8 && M == 64) return Team_8_64::R;
+  return 1;  // tile kernels: one realization per block
+}
+
+cudaError_t launch_fused(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s, long long* nblocks) {
+  if (K == 4 && M == 32) return launch_team<Team_4_32>(a, pgd, s, nblocks);
+  if (K == 8 && M == 64) return launch_team<Team_8_64>(a, pgd, s, nblocks);
+  return launch_tiled(a, pgd, K, M, s, nblocks);  // tile.cu: (16,128), (32,256)
+}
+
+}  // namespace ufpgd_gpu_impl

@@ -1,0 +1,552 @@
+// Tiled CTA kernel (tile_kernel) for the larger BASELINE shapes, (K, M) =
+// (16, 128) and (32, 256): one CTA owns a realization for all layers.
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <algorithm>
+
+#include "device_common.cuh"
+
+namespace ufpgd_gpu_impl {
+namespace {
+
+// ---------------------------------------------------------------------------
+// Tiled CTA kernel for the larger shapes (K, M) = (16, 128), (32, 256):
+// SURVEY §8a rows a4/a5/a11 at configs 4 and 5. Here a K x K residual per
+// thread no longer fits in registers, so one CTA (NW warps) owns a realization
+// and both contractions run as register-tiled, shared-memory-fed GEMMs:
+//   stage 2 (V = W - eta X' H^*): thread tile 8 users x TA antennas, loop over
+//     the K users j of X' (operands: X' rows and H entries, 1 byte of shared
+//     memory per FFMA2 at TA = 8);
+//   prox: column norms reduced across the K/8 user-group lanes (shuffles);
+//   stage 1 (X' = W H^T - diag c): thread tile 8 x 8 of X', split over S
+//     antenna slices, reduced with shuffles within the warp and through shared
+//     memory across warps.
+// H, W (split into re / im planes so FFMA2 operand pairs load directly) and X'
+// (split, [j][k]) live in shared memory; H and W rows are unpadded with their
+// 16-byte units XOR-swizzled per row (Tile::hoff / woff) so the LDS.128 /
+// STS.128 phases of both stages are conflict-free.
+// ---------------------------------------------------------------------------
+
+template <int K_, int M_, int NW_, int TA_, int TS_ = 8>
+struct Tile {
+  static constexpr int K = K_, M = M_, NW = NW_, NT = 32 * NW_, TA = TA_;
+  static constexpr int TS = TS_;             // stage-1 X' tile: TS x TS per thread
+  static constexpr int TR = 8;               // stage-2 users per thread (4 FFMA2 pairs)
+  static constexpr int RG = K / TR;          // user groups
+  static constexpr int AG = M / TA;          // antenna groups
+  static constexpr int XT = (K / TS) * (K / TS);  // TS x TS tiles of X'
+  static constexpr int S = NT / XT;          // antenna slices of stage 1
+  static constexpr int MS = M / S;           // antennas per slice
+  static constexpr int HSTR = 2 * K;         // floats, unpadded (XOR-swizzled units)
+  static constexpr int WSTR = K;
+  static constexpr int XSTR = K + 4;
+  static constexpr int OFF_H = 0;
+  static constexpr int OFF_WR = OFF_H + M * HSTR;
+  static constexpr int OFF_WI = OFF_WR + M * WSTR;
+  static constexpr int OFF_XR = OFF_WI + M * WSTR;
+  static constexpr int OFF_XI = OFF_XR + K * XSTR;
+  static constexpr int OFF_XP = OFF_XI + K * XSTR;          // cross-warp partials
+  static constexpr int XPART = (NW > 1) ? NW * 2 * K * K : 0;
+  static constexpr int SMEM_FLOATS = OFF_XP + XPART;
+  static constexpr int SMEM = SMEM_FLOATS * 4;
+  static_assert(RG * AG == NT, "stage-2 tiles must cover V exactly");
+  static_assert(NT % XT == 0 && XT <= 32 && 32 % XT == 0, "stage-1 tiles within a warp");
+  static_assert(TS == 8 || (TS == 4 && NW == 1), "4 x 4 stage-1 tiles only without cross-warp partials");
+  static_assert(M % S == 0, "");
+  static_assert(K >= 16 && 8 % RG == 0, "swizzles assume >= 8 H units per row");
+  // H(c, m): 16-byte unit (c >> 1) of row m, XOR-swizzled by m mod (8 / RG):
+  // the 8 / RG antenna rows a stage-2 LDS.128 phase touches land on
+  // distinct banks (rows are 8 units = one bank period apart otherwise).
+  static __device__ __forceinline__ int hsw(int m) { return m & (8 / RG - 1); }
+  static __device__ __forceinline__ int hoff(int m, int c) { return m * HSTR + 4 * ((c >> 1) ^ hsw(m)) + 2 * (c & 1); }
+  // W planes: unit (k >> 2) of row m, bit 0 XOR-ed with ((m * K / 4) >> 3) & 1
+  // so the two rows whose bases coincide mod 8 units flip unit parity.
+  static __device__ __forceinline__ int wsw(int m) { return ((m * (K / 4)) >> 3) & 1; }
+  static __device__ __forceinline__ int woff(int m, int k) { return m * WSTR + 4 * ((k >> 2) ^ wsw(m)) + (k & 3); }
+  // Cross-warp X' partials [jj][k]: the publishing lanes of one STS write rows
+  // tc * 8 + j of the 8 x 8 tile columns; flipping unit bit 0 on odd tile rows
+  // spreads them over all 8 bank groups (2 wavefronts instead of 4).
+  static __device__ __forceinline__ int xpoff(int jj, int k) {
+    return jj * K + 4 * ((k >> 2) ^ ((jj >> 3) & 1)) + (k & 3);
+  }
+};
+
+template <int NW>
+__device__ __forceinline__ void cta_sync() {
+  if (NW == 1)
+    __syncwarp();
+  else
+    __syncthreads();
+}
+
+// Stage 1: X'(k, j) = sum_m W(k, m) H(j, m) - c_k [k == j], written to the
+// split X' planes (Xre/Xim[j][k]).
+template <class T>
+__device__ __forceinline__ void tile_stage1(float* sm, const float* c, int tid, float neta) {
+  constexpr int TS = T::TS, TQ = TS / 2;  // users per tile side, user pairs per tile row
+  const int t = tid % T::XT, s = tid / T::XT;
+  const int tr = t % (T::K / TS), tc = t / (T::K / TS);
+  float2 xr[TQ][TS], xi[TQ][TS];
+#pragma unroll
+  for (int q = 0; q < TQ; ++q)
+#pragma unroll
+    for (int j = 0; j < TS; ++j) {
+      xr[q][j] = zero2();
+      xi[q][j] = zero2();
+    }
+  const float* Hs = sm + T::OFF_H;
+  const float* Wre = sm + T::OFF_WR;
+  const float* Wim = sm + T::OFF_WI;
+#pragma unroll 2
+  for (int i = 0; i < T::MS; ++i) {
+    const int m = i * T::S + s;
+    float2 wr[TQ], wi[TQ];
+#pragma unroll
+    for (int u = 0; u < TS / 4; ++u) {
+      const float4 a = *reinterpret_cast<const float4*>(Wre + T::woff(m, tr * TS + 4 * u));
+      const float4 b = *reinterpret_cast<const float4*>(Wim + T::woff(m, tr * TS + 4 * u));
+      wr[2 * u] = make_float2(a.x, a.y);
+      wr[2 * u + 1] = make_float2(a.z, a.w);
+      wi[2 * u] = make_float2(b.x, b.y);
+      wi[2 * u + 1] = make_float2(b.z, b.w);
+    }
+    float2 h[TS];
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) {
+      const float4 v = *reinterpret_cast<const float4*>(Hs + T::hoff(m, tc * TS + 2 * q));
+      h[2 * q] = make_float2(v.x, v.y);
+      h[2 * q + 1] = make_float2(v.z, v.w);
+    }
+#pragma unroll
+    for (int q = 0; q < TQ; ++q)
+#pragma unroll
+      for (int j = 0; j < TS; ++j) {
+        xr[q][j] = ffma2(h[j].x, wr[q], xr[q][j]);
+        xr[q][j] = ffma2(-h[j].y, wi[q], xr[q][j]);
+        xi[q][j] = ffma2(h[j].x, wi[q], xi[q][j]);
+        xi[q][j] = ffma2(h[j].y, wr[q], xi[q][j]);
+      }
+  }
+  // reduce the slices held by lanes of this warp (lane bits >= log2(XT))
+#pragma unroll
+  for (int q = 0; q < TQ; ++q)
+#pragma unroll
+    for (int j = 0; j < TS; ++j)
+#pragma unroll
+      for (int off = T::XT; off < 32; off <<= 1) {
+        xr[q][j] = fadd2(xr[q][j], make_float2(__shfl_xor_sync(kFull, xr[q][j].x, off),
+                                               __shfl_xor_sync(kFull, xr[q][j].y, off)));
+        xi[q][j] = fadd2(xi[q][j], make_float2(__shfl_xor_sync(kFull, xi[q][j].x, off),
+                                               __shfl_xor_sync(kFull, xi[q][j].y, off)));
+      }
+  // The consuming layer's step is folded in here: the stored X' is
+  // -eta (W H^T - diag c), so stage 2 accumulates V = W - eta G directly.
+  float* Xre = sm + T::OFF_XR;
+  float* Xim = sm + T::OFF_XI;
+  const int lane = tid & 31, warp = tid >> 5;
+  if (T::NW > 1) {
+    // cross-warp: lanes < XT of each warp publish their tile; then every
+    // thread of the CTA sums a strip of the NW partials in fixed warp order.
+    float* part = sm + T::OFF_XP + warp * 2 * T::K * T::K;
+    if (lane < T::XT) {
+#pragma unroll
+      for (int q = 0; q < TQ; ++q)
+#pragma unroll
+        for (int j = 0; j < TS; ++j) {
+          const int k0 = tr * TS + 2 * q, jj = tc * TS + j;
+          *reinterpret_cast<float2*>(part + T::xpoff(jj, k0)) = xr[q][j];
+          *reinterpret_cast<float2*>(part + T::K * T::K + T::xpoff(jj, k0)) = xi[q][j];
+        }
+    }
+    __syncthreads();
+    constexpr int NE = T::K * T::K / 2;  // float2 entries per plane
+    static_assert(NE % T::NT == 0, "reduction strips must tile the planes");
+#pragma unroll
+    for (int r = 0; r < NE / T::NT; ++r) {
+      const int e = tid + r * T::NT;
+      const int jj = e / (T::K / 2), k0 = 2 * (e % (T::K / 2));
+      float2 re = zero2(), im = zero2();
+#pragma unroll
+      for (int w = 0; w < T::NW; ++w) {
+        const float* pw = sm + T::OFF_XP + w * 2 * T::K * T::K;
+        re = fadd2(re, *reinterpret_cast<const float2*>(pw + T::xpoff(jj, k0)));
+        im = fadd2(im, *reinterpret_cast<const float2*>(pw + T::K * T::K + T::xpoff(jj, k0)));
+      }
+      if (k0 == jj) re.x -= c[jj];
+      if (k0 + 1 == jj) re.y -= c[jj];
+      *reinterpret_cast<float2*>(Xre + jj * T::XSTR + k0) = fmul2(neta, re);
+      *reinterpret_cast<float2*>(Xim + jj * T::XSTR + k0) = fmul2(neta, im);
+    }
+  } else if (warp == 0 && lane < T::XT) {
+#pragma unroll
+    for (int q = 0; q < TQ; ++q)
+#pragma unroll
+      for (int j = 0; j < TS; ++j) {
+        const int k0 = tr * TS + 2 * q, jj = tc * TS + j;
+        float2 r = xr[q][j];
+        if (tr == tc) {  // diagonal tile: k == j at compile-time positions
+          if (2 * q == j) r.x -= c[jj];
+          if (2 * q + 1 == j) r.y -= c[jj];
+        }
+        *reinterpret_cast<float2*>(Xre + jj * T::XSTR + k0) = fmul2(neta, r);
+        *reinterpret_cast<float2*>(Xim + jj * T::XSTR + k0) = fmul2(neta, xi[q][j]);
+      }
+  }
+  cta_sync<T::NW>();
+}
+
+// Stage 2 + prox for the thread's 8 users x TA antennas, W updated in place.
+// DIAG0: layer 0 from W0 = 0, where X' = -diag(c) exactly and V(k, m) is
+// eta c_k conj(H(k, m)) — the contraction of a diagonal X' is skipped
+// (bit-identical to running it on the exact zeros); c = the kernel's c[K].
+template <class T, bool STATS, bool DIAG0 = false>
+__device__ __forceinline__ void tile_stage2(float* sm, int tid, float eta, float thr, bool& nonfinite,
+                                            float& l21, int& act, const float* c = nullptr) {
+  (void)eta;  // folded into X' by tile_stage1 (used directly on the DIAG0 path)
+  const int rg = tid % T::RG, ag = tid / T::RG;
+  const int k0 = rg * 8;
+  const float* Hs = sm + T::OFF_H;
+  float* Wre = sm + T::OFF_WR;
+  float* Wim = sm + T::OFF_WI;
+  const float* Xre = sm + T::OFF_XR;
+  const float* Xim = sm + T::OFF_XI;
+  // Accumulators start at W (X' arrives scaled by -eta): they end as V.
+  float2 gr[4][T::TA], gi[4][T::TA];
+  if constexpr (DIAG0) {
+#pragma unroll
+    for (int i = 0; i < T::TA; ++i) {
+      const int m = i * T::AG + ag;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + 2 * q;
+        const float4 h = *reinterpret_cast<const float4*>(Hs + T::hoff(m, k));  // H(k, m), H(k + 1, m)
+        const float2 ce = make_float2(eta * c[k], eta * c[k + 1]);  // = the -eta-folded X'(k, k)
+        gr[q][i] = __fmul2_rn(ce, make_float2(h.x, h.z));
+        gi[q][i] = __fmul2_rn(ce, make_float2(-h.y, -h.w));
+      }
+    }
+  } else {
+#pragma unroll
+  for (int i = 0; i < T::TA; ++i) {
+    const int m = i * T::AG + ag;
+    const float4 a0 = *reinterpret_cast<const float4*>(Wre + T::woff(m, k0));
+    const float4 a1 = *reinterpret_cast<const float4*>(Wre + T::woff(m, k0 + 4));
+    const float4 b0 = *reinterpret_cast<const float4*>(Wim + T::woff(m, k0));
+    const float4 b1 = *reinterpret_cast<const float4*>(Wim + T::woff(m, k0 + 4));
+    gr[0][i] = make_float2(a0.x, a0.y);
+    gr[1][i] = make_float2(a0.z, a0.w);
+    gr[2][i] = make_float2(a1.x, a1.y);
+    gr[3][i] = make_float2(a1.z, a1.w);
+    gi[0][i] = make_float2(b0.x, b0.y);
+    gi[1][i] = make_float2(b0.z, b0.w);
+    gi[2][i] = make_float2(b1.x, b1.y);
+    gi[3][i] = make_float2(b1.z, b1.w);
+  }
+#pragma unroll 1  // unroll 2 measured slower at (16,128)
+  for (int j = 0; j < T::K; j += 2) {
+    float2 xr[2][4], xi[2][4];
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      const float4* rp = reinterpret_cast<const float4*>(Xre + (j + d) * T::XSTR + k0);
+      const float4* ip = reinterpret_cast<const float4*>(Xim + (j + d) * T::XSTR + k0);
+      const float4 r0 = rp[0], r1 = rp[1], i0 = ip[0], i1 = ip[1];
+      xr[d][0] = make_float2(r0.x, r0.y);
+      xr[d][1] = make_float2(r0.z, r0.w);
+      xr[d][2] = make_float2(r1.x, r1.y);
+      xr[d][3] = make_float2(r1.z, r1.w);
+      xi[d][0] = make_float2(i0.x, i0.y);
+      xi[d][1] = make_float2(i0.z, i0.w);
+      xi[d][2] = make_float2(i1.x, i1.y);
+      xi[d][3] = make_float2(i1.z, i1.w);
+    }
+#pragma unroll
+    for (int i = 0; i < T::TA; ++i) {
+      const int m = i * T::AG + ag;
+      const float4 h = *reinterpret_cast<const float4*>(Hs + T::hoff(m, j));
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        // G(k, m) += X'(k, j) conj(H(j, m)) for j and j + 1
+        gr[q][i] = ffma2(h.x, xr[0][q], gr[q][i]);
+        gr[q][i] = ffma2(h.y, xi[0][q], gr[q][i]);
+        gi[q][i] = ffma2(h.x, xi[0][q], gi[q][i]);
+        gi[q][i] = ffma2(-h.y, xr[0][q], gi[q][i]);
+        gr[q][i] = ffma2(h.z, xr[1][q], gr[q][i]);
+        gr[q][i] = ffma2(h.w, xi[1][q], gr[q][i]);
+        gi[q][i] = ffma2(h.z, xi[1][q], gi[q][i]);
+        gi[q][i] = ffma2(-h.w, xr[1][q], gi[q][i]);
+      }
+    }
+  }
+  }
+  const float thr2 = thr * thr;
+#pragma unroll
+  for (int i = 0; i < T::TA; ++i) {
+    const int m = i * T::AG + ag;
+    float4* wr0 = reinterpret_cast<float4*>(Wre + T::woff(m, k0));
+    float4* wr1 = reinterpret_cast<float4*>(Wre + T::woff(m, k0 + 4));
+    float4* wi0 = reinterpret_cast<float4*>(Wim + T::woff(m, k0));
+    float4* wi1 = reinterpret_cast<float4*>(Wim + T::woff(m, k0 + 4));
+    float2 vr[4], vi[4], s2 = zero2();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      vr[q] = gr[q][i];
+      vi[q] = gi[q][i];
+      s2 = __ffma2_rn(vr[q], vr[q], s2);
+      s2 = __ffma2_rn(vi[q], vi[q], s2);
+    }
+    float s = s2.x + s2.y;
+#pragma unroll
+    for (int off = 1; off < T::RG; off <<= 1) s += __shfl_xor_sync(kFull, s, off);
+    nonfinite |= !(s <= FLT_MAX);
+    const bool on = s > thr2;
+    const float r = rsqrt_ftz(fmaxf(s, FLT_MIN));
+    const float scale = on ? fmaf(-thr, r, 1.f) : 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      vr[q] = fmul2(scale, vr[q]);
+      vi[q] = fmul2(scale, vi[q]);
+    }
+    *wr0 = make_float4(vr[0].x, vr[0].y, vr[1].x, vr[1].y);
+    *wr1 = make_float4(vr[2].x, vr[2].y, vr[3].x, vr[3].y);
+    *wi0 = make_float4(vi[0].x, vi[0].y, vi[1].x, vi[1].y);
+    *wi1 = make_float4(vi[2].x, vi[2].y, vi[3].x, vi[3].y);
+    if (STATS && rg == 0 && on) {
+      l21 += fmaf(s, r, -thr);
+      act += 1;
+    }
+  }
+  cta_sync<T::NW>();
+}
+
+// Fixed-step power iteration with the CTA (PGD prologue), FP32; scratch in
+// the X' planes (free before the first stage 1).
+template <class T>
+__device__ float tile_power(float* sm, const float2* v0, int steps, int tid) {
+  float2* v = reinterpret_cast<float2*>(sm + T::OFF_XR);   // [M]
+  float2* u = v + T::M;                                    // [K]
+  float* red = reinterpret_cast<float*>(u + T::K);         // [2 * NW]
+  const float* Hs = sm + T::OFF_H;
+  for (int m = tid; m < T::M; m += T::NT) v[m] = v0[m];
+  cta_sync<T::NW>();
+  float est = 0.f;
+  bool zero = false;
+  for (int st = 0; st < steps; ++st) {
+    for (int j = tid; j < T::K; j += T::NT) {  // u = H^* v
+      float2 acc = zero2();
+      for (int m = 0; m < T::M; ++m) {
+        const float2 h = *reinterpret_cast<const float2*>(Hs + T::hoff(m, j));
+        cmac(acc, make_float2(h.x, -h.y), v[m]);
+      }
+      u[j] = acc;
+    }
+    cta_sync<T::NW>();
+    float dot = 0.f, wn2 = 0.f;
+    float2 wv[(T::M + T::NT - 1) / T::NT];
+#pragma unroll
+    for (int q = 0; q < (T::M + T::NT - 1) / T::NT; ++q) {
+      const int m = tid + q * T::NT;
+      float2 acc = zero2();
+      if (m < T::M) {
+        for (int j = 0; j < T::K; ++j)
+          cmac(acc, *reinterpret_cast<const float2*>(Hs + T::hoff(m, j)), u[j]);
+        dot = fmaf(v[m].x, acc.x, fmaf(v[m].y, acc.y, dot));
+        wn2 = fmaf(acc.x, acc.x, fmaf(acc.y, acc.y, wn2));
+      }
+      wv[q] = acc;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      dot += __shfl_xor_sync(kFull, dot, off);
+      wn2 += __shfl_xor_sync(kFull, wn2, off);
+    }
+    if (T::NW > 1) {
+      if ((tid & 31) == 0) {
+        red[2 * (tid >> 5)] = dot;
+        red[2 * (tid >> 5) + 1] = wn2;
+      }
+      __syncthreads();
+      dot = 0.f;
+      wn2 = 0.f;
+      for (int w = 0; w < T::NW; ++w) {
+        dot += red[2 * w];
+        wn2 += red[2 * w + 1];
+      }
+    }
+    cta_sync<T::NW>();
+    if (!zero) {
+      if (wn2 == 0.f) {
+        zero = true;
+        est = 0.f;
+      } else {
+        est = dot;
+        const float inv = 1.f / sqrtf(wn2);
+#pragma unroll
+        for (int q = 0; q < (T::M + T::NT - 1) / T::NT; ++q) {
+          const int m = tid + q * T::NT;
+          if (m < T::M) v[m] = make_float2(wv[q].x * inv, wv[q].y * inv);
+        }
+      }
+    }
+    cta_sync<T::NW>();
+  }
+  return est;
+}
+
+template <class T, bool PGD>
+__global__ void __launch_bounds__(T::NT) tile_kernel(const __grid_constant__ FusedArgs p) {
+  extern __shared__ __align__(16) float sm[];
+  __shared__ float red[2 * T::NW + 2];
+  const int tid = threadIdx.x;
+  const long long rid = blockIdx.x;
+  constexpr int NV = T::M * T::K / 2;  // float4 per realization
+  // stage H (coalesced float4 streaming loads)
+  const float4* hg = reinterpret_cast<const float4*>(p.H) + rid * NV;
+  for (int q = tid; q < NV; q += T::NT) {
+    const float4 v = ldg_stream(hg + q);
+    const int e = 2 * q;
+    *reinterpret_cast<float4*>(sm + T::OFF_H + T::hoff(e / T::K, e % T::K)) = v;
+  }
+  cta_sync<T::NW>();
+  // W0 into the split planes
+  for (int e = tid; e < T::M * T::K; e += T::NT) {
+    const int m = e / T::K, k = e % T::K;
+    float2 w = zero2();
+    if (p.w0_mode == UFPGD_W0_CONJ_H) {
+      const float2 h = *reinterpret_cast<const float2*>(sm + T::OFF_H + T::hoff(m, k));
+      w = make_float2(h.x, -h.y);
+    } else if (p.w0_mode == UFPGD_W0_GIVEN) {
+      w = p.W0[rid * T::M * T::K + e];
+    }
+    sm[T::OFF_WR + T::woff(m, k)] = w.x;
+    sm[T::OFF_WI + T::woff(m, k)] = w.y;
+  }
+  float eta_b = 0.f, thr_b = 0.f;
+  if (PGD) {
+    cta_sync<T::NW>();
+    eta_b = p.eta_in ? p.eta_in[rid] : 1.f / tile_power<T>(sm, p.v0, p.power_steps, tid);
+    thr_b = p.lambda * eta_b;
+    if (p.eta_out && tid == 0) p.eta_out[rid] = eta_b;
+  }
+  cta_sync<T::NW>();
+  if (p.w0_mode == UFPGD_W0_ZERO) {
+    for (int e = tid; e < T::K * T::K; e += T::NT) {
+      const int j = e / T::K, k = e % T::K;
+      sm[T::OFF_XR + j * T::XSTR + k] = k == j ? (PGD ? eta_b : p.eta[0]) * p.c[k] : 0.f;  // -eta0 (-diag c)
+      sm[T::OFF_XI + j * T::XSTR + k] = 0.f;
+    }
+    cta_sync<T::NW>();
+  } else {
+    tile_stage1<T>(sm, p.c, tid, -(PGD ? eta_b : p.eta[0]));
+  }
+  bool nonfinite = false;
+  long long first_bad = -1;
+  float l21 = 0.f;
+  int act = 0;
+  long long l0 = 0;
+  if (!PGD && p.w0_mode == UFPGD_W0_ZERO && p.L >= 1) {
+    if (p.L == 1) {
+      tile_stage2<T, true, true>(sm, tid, p.eta[0], p.thr[0], nonfinite, l21, act, p.c);
+    } else {
+      tile_stage2<T, false, true>(sm, tid, p.eta[0], p.thr[0], nonfinite, l21, act, p.c);
+      tile_stage1<T>(sm, p.c, tid, -p.eta[1]);
+    }
+    if (nonfinite) first_bad = 0;
+    l0 = 1;
+  }
+  for (long long l = l0; l < p.L; ++l) {
+    const float eta = PGD ? eta_b : p.eta[l];
+    const float thr = PGD ? thr_b : p.thr[l];
+    if (l + 1 < p.L) {
+      tile_stage2<T, false>(sm, tid, eta, thr, nonfinite, l21, act);
+      tile_stage1<T>(sm, p.c, tid, -(PGD ? eta_b : p.eta[l + 1]));
+    } else {
+      tile_stage2<T, true>(sm, tid, eta, thr, nonfinite, l21, act);
+    }
+    if (nonfinite && first_bad < 0) first_bad = l;
+  }
+  // per-realization reductions over the CTA
+  long long fb = first_bad < 0 ? LLONG_MAX : first_bad;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    fb = min(fb, __shfl_xor_sync(kFull, fb, off));
+    l21 += __shfl_xor_sync(kFull, l21, off);
+    act += __shfl_xor_sync(kFull, act, off);
+  }
+  __shared__ long long fbs[T::NW];
+  if (T::NW > 1) {
+    if ((tid & 31) == 0) {
+      fbs[tid >> 5] = fb;
+      red[2 * (tid >> 5)] = l21;
+      red[2 * (tid >> 5) + 1] = static_cast<float>(act);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < T::NW; ++w) {
+        fb = min(fb, fbs[w]);
+        l21 += red[2 * w];
+        act += static_cast<int>(red[2 * w + 1]);
+      }
+    }
+  }
+  // W out (coalesced, interleaved complex)
+  float2* wg = p.W + rid * T::M * T::K;
+  for (int e = tid; e < T::M * T::K / 2; e += T::NT) {
+    const int m = (2 * e) / T::K, k = (2 * e) % T::K;
+    const float* wr = sm + T::OFF_WR + T::woff(m, k);  // k even: k, k + 1 share a unit
+    const float* wi = sm + T::OFF_WI + T::woff(m, k);
+    stg_stream(reinterpret_cast<float4*>(wg) + e, make_float4(wr[0], wi[0], wr[1], wi[1]));
+  }
+  if (tid == 0) {
+    const bool diverged = fb != LLONG_MAX;
+    if (p.diverged_at) p.diverged_at[rid] = diverged ? static_cast<int32_t>(fb + (PGD ? 1 : 0)) : -1;
+    if (p.l21) p.l21[rid] = diverged ? __int_as_float(0x7fc00000) : l21;
+    if (p.active) p.active[rid] = diverged ? -1 : act;
+    if (p.block_partials) {
+      p.block_partials[rid * 3 + 0] = diverged ? 0.0 : static_cast<double>(p.alpha) * l21;
+      p.block_partials[rid * 3 + 1] = diverged ? 0.0 : static_cast<double>(act);
+      p.block_partials[rid * 3 + 2] = diverged ? 1.0 : 0.0;
+    }
+  }
+}
+
+
+template <class T>
+cudaError_t launch_tile(const FusedArgs& a, bool pgd, cudaStream_t s, long long* nblocks) {
+  auto kern = pgd ? tile_kernel<T, true> : tile_kernel<T, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+  if (e != cudaSuccess) return e;
+  if (nblocks) *nblocks = a.B;
+  kern<<<static_cast<unsigned>(a.B), T::NT, T::SMEM, s>>>(a);
+  return cudaGetLastError();
+}
+
+#ifndef UFPGD_T32_NW
+#define UFPGD_T32_NW 8
+#endif
+#ifndef UFPGD_T32_TA
+#define UFPGD_T32_TA 4
+#endif
+#ifndef UFPGD_T16_NW
+#define UFPGD_T16_NW 1
+#endif
+#ifndef UFPGD_T16_TA
+#define UFPGD_T16_TA 8
+#endif
+#ifndef UFPGD_T16_TS
+#define UFPGD_T16_TS 4
+#endif
+using Tile_16_128 = Tile<16, 128, UFPGD_T16_NW, UFPGD_T16_TA, UFPGD_T16_TS>;
+using Tile_32_256 = Tile<32, 256, UFPGD_T32_NW, UFPGD_T32_TA>;
+
+}  // namespace
+
+cudaError_t launch_tiled(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s, long long* nblocks) {
+  if (K == 16 && M == 128) return launch_tile<Tile_16_128>(a, pgd, s, nblocks);
+  if (K == 32 && M == 256) return launch_tile<Tile_32_256>(a, pgd, s, nblocks);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace ufpgd_gpu_impl

@@ -1,4 +1,4 @@
-// Internal interface between the C ABI (capi.cu) and the kernels (kernels.cu).
+// Internal interface between the C ABI (capi.cpp) and the kernels (csrc/*.cu).
 #pragma once
 
 #include <cstdint>
@@ -10,7 +10,7 @@
 namespace ufpgd_gpu_impl {
 
 // Arguments of the fused team kernel (one team of TK*TM threads per
-// realization; see kernels.cu). Passed by value as a __grid_constant__.
+// realization; see team.cu). Passed by value as a __grid_constant__.
 struct FusedArgs {
   const float2* H;
   float2* W;
@@ -116,6 +116,8 @@ int fused_realizations_per_block(int K, int M);
 // *nblocks receives the grid size (= number of block partials written).
 cudaError_t launch_fused(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s,
                          long long* nblocks);
+// Tiled CTA kernels (tile.cu) for (16,128) and (32,256); launch_fused forwards there.
+cudaError_t launch_tiled(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s, long long* nblocks);
 size_t general_smem_bytes(int K, int M);
 cudaError_t launch_general(const GeneralArgs& a, cudaStream_t s);
 cudaError_t launch_general64(const GeneralArgs64& a, cudaStream_t s);

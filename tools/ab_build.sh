@@ -4,10 +4,15 @@
 set -e
 name=$1; shift
 cd "$(dirname "$0")/.."
-mkdir -p tools/ablib/$name build/obj/ab
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++20 -Xcompiler -fPIC -Iinclude \
-  -Ipaper_2304_12745_b200/csrc "$@" -Xptxas -v -c paper_2304_12745_b200/csrc/kernels.cu \
-  -o build/obj/ab/kernels_$name.o 2> build/obj/ab/$name.log
+mkdir -p tools/ablib/$name build/obj/ab/$name
+objs=""
+for f in team tile general metrics grad datagen probe; do
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++20 -Xcompiler -fPIC -Iinclude \
+    -Ipaper_2304_12745_b200/csrc "$@" -Xptxas -v -c paper_2304_12745_b200/csrc/$f.cu \
+    -o build/obj/ab/$name/$f.o 2> build/obj/ab/$name/$f.log &
+  objs="$objs build/obj/ab/$name/$f.o"
+done
+wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o tools/ablib/$name/libufpgd_gpu.so \
-  build/obj/ab/kernels_$name.o build/obj/capi.o build/obj/host_gen.o build/obj/api.o build/obj/dataset_io.o -ldl -lpthread
-grep -A2 "fused_kernelINS0_4TeamILi8ELi64" build/obj/ab/$name.log | grep -oE "Used [0-9]+ registers|[0-9]+ bytes spill stores" | tr '\n' ' '; echo " [$name]"
+  $objs build/obj/capi.o build/obj/host_gen.o build/obj/api.o build/obj/dataset_io.o -ldl -lpthread
+grep -A2 "fused_kernelINS0_4TeamILi8ELi64" build/obj/ab/$name/team.log | grep -oE "Used [0-9]+ registers|[0-9]+ bytes spill stores" | tr '\n' ' '; echo " [$name]"
