@@ -241,6 +241,19 @@ int ufpgd_gpu_unfolded_grad(const ufpgd_c64* H, int64_t B, int K, int M, const d
                             double* mean, int device, ufpgd_stream_t stream);
 
 /*
+ * backward (unfolded.hpp:80-89, unfolded.cpp:158-239) in FP64 over B channels:
+ * the forward from W0 (w0_mode; UFPGD_W0_GIVEN reproduces a tape whose layer-0
+ * input is W0) is re-run on the device with its tape, and the reverse sweep
+ * starts from the given output gradient dcost_dw = dC/dRe(W) + i dC/dIm(W).
+ * Device buffers, interleaved FP64 complex [B][M][K]; grads[B][2L] in pack
+ * order (d_lambda_0, d_eta_0, ...). Async on `stream`.
+ */
+int ufpgd_gpu_unfolded_backward64(const double* H, int64_t B, int K, int M, const double* lambda,
+                                  const double* eta, int L, const double* c, int w0_mode,
+                                  const double* W0, const double* dcost_dw, double* grads, int device,
+                                  ufpgd_stream_t stream);
+
+/*
  * Batched metrics — compute_metrics (metrics.cpp:79-91)
  * with the ZF reference of zf_precoder (zf.cpp:9-30) for B (H, W) pairs,
  * the body of evaluate's parallel_for (training.cpp:324-357). FP64 on the

@@ -43,6 +43,7 @@ from .capi import (  # noqa: F401
     unfolded_forward,
     unfolded_forward_host,
     unfolded_grad,
+    unfolded_backward64,
     ufpd_header,
     ufpd_load,
     ufpd_store,

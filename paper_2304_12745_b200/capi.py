@@ -81,6 +81,7 @@ def lib():
             "ufpgd_gpu_solve_pgd64": (i, [P, i64, i, i, P, d, P, i64, d, P, P, P, P, i, P]),
             "ufpgd_gpu_oracle_solve": (i, [P, i64, i, i, P, d, i64, d, P, P, P, P, i, P]),
             "ufpgd_gpu_unfolded_grad": (i, [P, i64, i, i, P, P, i, P, i, i, d, P, P, P, P, i, P]),
+            "ufpgd_gpu_unfolded_backward64": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, i, P]),
             "ufpgd_gpu_init": (i, [i]),
             "ufpgd_gpu_shutdown": (i, []),
             "ufpgd_gpu_unfolded_forward_sharded": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, d]),
@@ -473,6 +474,25 @@ def generate_channels_device(seed_h: int, seed_g: int, gain_range_db: float, fir
                                            int(dt == torch.complex128), H.device.index or 0, _stream_ptr(stream))
     _check(rc)
     return H
+
+
+def unfolded_backward64(H, lambda_, eta, c, dcost_dw, *, w0_mode: int = W0_CONJ_H, W0=None, stream=None):
+    """backward (unfolded.cpp:158-239) in FP64 for complex128 CUDA batches
+    [B, M, K]: the forward from W0 is re-run on the device with its tape and
+    swept back from dcost_dw. Returns grads [B, 2L] in pack order."""
+    import torch
+
+    for t in (H, dcost_dw) + ((W0,) if W0 is not None else ()):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.complex128 and t.dim() == 3
+                and t.is_contiguous()):
+            raise ValueError("H, dcost_dw (and W0) must be contiguous CUDA complex128 tensors [B, M, K]")
+    B, M, K = H.shape
+    lam, et, cc = _f64(lambda_), _f64(eta), _f64(c)
+    grads = torch.empty((B, 2 * lam.size), dtype=torch.float64, device=H.device)
+    _check(lib().ufpgd_gpu_unfolded_backward64(_ptr(H), B, K, M, _ptr(lam), _ptr(et), lam.size, _ptr(cc), w0_mode,
+                                               _ptr(W0), _ptr(dcost_dw), _ptr(grads), H.device.index or 0,
+                                               _stream_ptr(stream)))
+    return grads
 
 
 def power_v0(M: int) -> np.ndarray:

@@ -473,6 +473,45 @@ PrecoderMatrix forward_infer(const UnfoldedNetwork& net, const ChannelMatrix& ch
   return forward(net, channel, cfg).output;
 }
 
+ParamGradients backward(const ForwardTape& tape, const UnfoldedNetwork& net, const ChannelMatrix& channel,
+                        const SystemConfig& cfg, const ComplexMatrix& dcost_dw) {  // unfolded.cpp:158-239
+  net.validate();
+  cfg.validate();
+  const std::size_t depth = net.layers.size();
+  if (tape.layers.size() != depth) throw TrainingError("backward: tape depth does not match network");
+  if (dcost_dw.rows() != cfg.K || dcost_dw.cols() != cfg.M || channel.rows() != cfg.K || channel.cols() != cfg.M)
+    throw TrainingError("backward: shape mismatch");
+  for (const LayerTape& layer : tape.layers)
+    if (layer.input.rows() != cfg.K || layer.input.cols() != cfg.M || layer.step_image.rows() != cfg.K ||
+        layer.step_image.cols() != cfg.M || layer.column_norms.size() != cfg.M ||
+        layer.shrink_factors.size() != cfg.M)
+      throw TrainingError("backward: malformed tape layer");
+  const int K = cfg.K, M = cfg.M, L = static_cast<int>(depth);
+  const std::size_t n = static_cast<std::size_t>(K) * M;
+  std::vector<double> lam, eta;
+  for (const LayerParams& l : net.layers) {
+    lam.push_back(l.lambda_i);
+    eta.push_back(l.eta_i);
+  }
+  const RealVector c = cfg.constraint_diag();
+  DeviceScope scope;
+  DeviceBuffer<double> dH(2 * n), dW0(2 * n), dG(2 * n), dgr(2 * static_cast<std::size_t>(L));
+  dH.upload(reinterpret_cast<const double*>(channel.data()));
+  dW0.upload(reinterpret_cast<const double*>(tape.layers[0].input.data()));
+  dG.upload(reinterpret_cast<const double*>(dcost_dw.data()));
+  check(ufpgd_gpu_unfolded_backward64(dH.p, 1, K, M, lam.data(), eta.data(), L, c.data(), UFPGD_W0_GIVEN, dW0.p,
+                                      dG.p, dgr.p, g_device, nullptr));
+  cuda_check(cudaDeviceSynchronize(), "backward");
+  std::vector<double> g(2 * static_cast<std::size_t>(L));
+  dgr.download(g.data());
+  ParamGradients out;
+  for (int i = 0; i < L; ++i) {
+    out.d_lambda.push_back(g[2 * static_cast<std::size_t>(i)]);
+    out.d_eta.push_back(g[2 * static_cast<std::size_t>(i) + 1]);
+  }
+  return out;
+}
+
 // ---- metrics.cpp ----------------------------------------------------------------
 double l21_norm(const PrecoderMatrix& precoder) {
   double total = 0.0;

@@ -910,6 +910,50 @@ int ufpgd_gpu_generate_channels(uint64_t seed_h, uint64_t seed_g, double gain_ra
   return UFPGD_OK;
 }
 
+int ufpgd_gpu_unfolded_backward64(const double* H, int64_t B, int K, int M, const double* lambda,
+                                  const double* eta, int L, const double* c, int w0_mode, const double* W0,
+                                  const double* dcost_dw, double* grads, int device, ufpgd_stream_t stream) {
+  int rc;
+  if ((rc = check_shape(B, K, M)) || (rc = check_layers(lambda, eta, L)) || (rc = check_c(c, K)) ||
+      (rc = check_w0(w0_mode, W0)))
+    return rc;
+  if (L < 1) return fail(UFPGD_EINVAL_PARAM, "need at least one layer");
+  if (B > 0 && (!H || !dcost_dw || !grads)) return fail(UFPGD_EINVAL_PARAM, "H, dcost_dw and grads are required");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
+  if (B == 0) return UFPGD_OK;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (grad64_smem_bytes(K, M) + 1024 > static_cast<size_t>(optin))
+    return fail(UFPGD_ENOTSUP, "(K, M) too large for the FP64 gradient kernel");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  GradArgs64 a{};
+  a.H = reinterpret_cast<const double2*>(H);
+  a.W0 = reinterpret_cast<const double2*>(W0);
+  a.dcost = reinterpret_cast<const double2*>(dcost_dw);
+  a.out_grads = grads;
+  a.B = B;
+  a.K = K;
+  a.M = M;
+  a.L = L;
+  a.w0_mode = w0_mode;
+  a.loss_kind = 2;
+  for (int k = 0; k < K; ++k) a.c[k] = c[k];
+  for (int l = 0; l < L; ++l) {
+    a.eta[l] = eta[l];
+    a.thr[l] = lambda[l] * eta[l];
+    a.lam[l] = lambda[l];
+    a.eta64[l] = eta[l];
+  }
+  UFPGD_CUDA(cudaMallocAsync(&a.tape, sizeof(double2) * 2ull * L * K * M * B, s));
+  UFPGD_CUDA(cudaMallocAsync(&a.out_loss, sizeof(double) * B, s));
+  cudaError_t e = launch_grad64(a, nullptr, s);
+  cudaFreeAsync(a.tape, s);
+  cudaFreeAsync(a.out_loss, s);
+  if (e != cudaSuccess) return cuda_fail(e, "FP64 backward kernel");
+  return UFPGD_OK;
+}
+
 int ufpgd_gpu_fp32_peak(int device, double* tflops, double* sm_ghz) {
   if (!tflops || !sm_ghz) return fail(UFPGD_EINVAL_PARAM, "null output");
   DeviceGuard g(device);

@@ -84,23 +84,29 @@ using GeneralArgs = GeneralArgsT<float>;
 using GeneralArgs64 = GeneralArgsT<double>;
 
 // Arguments of the training-gradient kernel (one CTA per realization).
-struct GradArgs {
-  const float2* H;
-  const float2* labels;  // supervised loss targets (nullable)
-  float2* tape;          // [B][2][L][M*K] workspace
-  double* out_loss;      // [B]
-  double* out_grads;     // [B][2L]
+template <class T>
+struct GradArgsT {
+  using V2 = typename Vec2<T>::type;
+  const V2* H;
+  const V2* labels;  // loss_kind 1: supervised loss targets
+  const V2* W0;      // w0_mode UFPGD_W0_GIVEN: start point [B][M][K]
+  const V2* dcost;   // loss_kind 2: given dC/dRe(W) + i dC/dIm(W) of the output [B][M][K]
+  V2* tape;          // [B][2][L][M*K] workspace
+  double* out_loss;  // [B] (0 for loss_kind 2)
+  double* out_grads; // [B][2L]
   long long B;
   int K, M, L;
   int w0_mode;
-  int loss_kind;  // 0 unsupervised (lagrangian, lambda_cost), 1 supervised
-  float lambda_cost;
-  float c[UFPGD_MAX_USERS];
-  float eta[UFPGD_MAX_LAYERS];
-  float thr[UFPGD_MAX_LAYERS];
+  int loss_kind;  // 0 unsupervised (lagrangian, lambda_cost), 1 supervised, 2 given dC/dW (backward)
+  T lambda_cost;
+  T c[UFPGD_MAX_USERS];
+  T eta[UFPGD_MAX_LAYERS];
+  T thr[UFPGD_MAX_LAYERS];
   double lam[UFPGD_MAX_LAYERS];
   double eta64[UFPGD_MAX_LAYERS];
 };
+using GradArgs = GradArgsT<float>;
+using GradArgs64 = GradArgsT<double>;
 
 struct PowerArgs {
   const float2* H;
@@ -130,6 +136,8 @@ cudaError_t launch_metrics(const float2* H, const float2* W, long long B, int K,
                            double sigma2, double alpha, double* out, float2* Wzf, cudaStream_t s);
 size_t grad_smem_bytes(int K, int M);
 cudaError_t launch_grad(const GradArgs& a, double* mean, cudaStream_t s);
+size_t grad64_smem_bytes(int K, int M);
+cudaError_t launch_grad64(const GradArgs64& a, double* mean, cudaStream_t s);
 cudaError_t launch_channel_gen(unsigned long long seed_h, unsigned long long seed_g, double gain_range_db,
                                long long first_index, long long B, int K, int M, void* H, bool f64, cudaStream_t s);
 cudaError_t launch_convert(const void* src, void* dst, long long B, int K, int M, bool to_c64, cudaStream_t s);

@@ -4,9 +4,11 @@
 // device. The per-channel API runs the FP64 kernels, so the reference's own
 // tolerances (1e-12 / 1e-14) apply; the batched entry points run in FP32
 // (tolerances noted where used).
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -136,6 +138,95 @@ static double mean_supervised_loss(const UnfoldedNetwork& net, const Dataset& da
 }
 
 static double rel_err(double a, double b) { return std::abs(a - b) / std::max(std::abs(a), std::abs(b)); }
+
+static void backward_tests() {
+  // --- test_unfolded.cpp: backward ---------------------------------------------
+  {  // central finite differences of a supervised cost (test_unfolded.cpp:302-381)
+    SystemConfig cfg = SystemConfig::uniform(4, 16, 10.0);
+    const int layers = 5;
+    const double lo = 1.0 / (2.0 * mp_bound(cfg.K, cfg.M)), hi = 1.0 / mp_bound(cfg.K, cfg.M);
+    const double fd = 1e-6, kink = 1e-4;
+    auto cost = [&](const UnfoldedNetwork& net, const ChannelMatrix& h, const ComplexMatrix& ref) {
+      PrecoderMatrix out = forward_infer(net, h, cfg);
+      double s = 0.0;
+      for (std::ptrdiff_t i = 0; i < out.size(); ++i) s += std::norm(out.data()[i] - ref.data()[i]);
+      return s;
+    };
+    bool clean = false;
+    for (std::uint64_t attempt = 0; attempt < 50 && !clean; ++attempt) {
+      ChannelMatrix h = channel_for(cfg, 48, attempt);
+      Rng rng = Rng::stream(49, attempt);
+      UnfoldedNetwork net;
+      net.num_users = cfg.K;
+      net.num_antennas = cfg.M;
+      net.mp_bound = mp_bound(cfg.K, cfg.M);
+      for (int i = 0; i < layers; ++i) {
+        const double lambda = (0.5 + rng.uniform()) / 15.0;
+        const double eta = lo + 3.0 * fd + rng.uniform() * (hi - lo - 6.0 * fd);
+        net.layers.push_back({lambda, eta});
+      }
+      ComplexMatrix ref = random_matrix(cfg.K, cfg.M, rng);
+      ForwardOptions opt;
+      opt.with_tape = true;
+      ForwardResult fwd = forward(net, h, cfg, std::nullopt, opt);
+      bool near = false;
+      for (int i = 0; i < layers; ++i) {
+        const double t = net.layers[static_cast<std::size_t>(i)].lambda_i * net.layers[static_cast<std::size_t>(i)].eta_i;
+        for (int m = 0; m < cfg.M; ++m)
+          if (std::abs(fwd.tape.layers[static_cast<std::size_t>(i)].column_norms[m] - t) < kink) near = true;
+      }
+      if (near) continue;
+      clean = true;
+      ComplexMatrix dcost(cfg.K, cfg.M);
+      for (std::ptrdiff_t i = 0; i < dcost.size(); ++i) dcost.data()[i] = 2.0 * (fwd.output.data()[i] - ref.data()[i]);
+      ParamGradients g = backward(fwd.tape, net, h, cfg, dcost);
+      bool ok = g.d_lambda.size() == static_cast<std::size_t>(layers) && g.d_eta.size() == static_cast<std::size_t>(layers);
+      for (int i = 0; ok && i < layers; ++i) {
+        const std::size_t idx = static_cast<std::size_t>(i);
+        for (int which = 0; which < 2; ++which) {
+          UnfoldedNetwork plus = net, minus = net;
+          double& pp = which == 0 ? plus.layers[idx].lambda_i : plus.layers[idx].eta_i;
+          double& mm = which == 0 ? minus.layers[idx].lambda_i : minus.layers[idx].eta_i;
+          pp += fd;
+          mm -= fd;
+          const double numeric = (cost(plus, h, ref) - cost(minus, h, ref)) / (2.0 * fd);
+          const double analytic = which == 0 ? g.d_lambda[idx] : g.d_eta[idx];
+          if (std::abs(numeric - analytic) > 1e-5 * std::max({std::abs(numeric), std::abs(analytic), 1e-2})) {
+            std::printf("  backward FD layer %d %s: numeric %.9g analytic %.9g\n", i, which ? "eta" : "lambda",
+                        numeric, analytic);
+            ok = false;
+          }
+        }
+      }
+      CHECK(ok);
+    }
+    CHECK(clean);
+  }
+  {  // a tape from a different network, a mis-shaped cost gradient (test_unfolded.cpp:384-400)
+    SystemConfig cfg = SystemConfig::uniform(3, 8, 10.0);
+    ChannelMatrix h = channel_for(cfg, 50, 0);
+    UnfoldedNetwork deep = UnfoldedNetwork::pgd_init(cfg.K, cfg.M, 5, 0.2), shallow = UnfoldedNetwork::pgd_init(cfg.K, cfg.M, 3, 0.2);
+    ForwardOptions opt;
+    opt.with_tape = true;
+    ForwardResult fwd = forward(deep, h, cfg, std::nullopt, opt);
+    CHECK_THROWS_AS(backward(fwd.tape, shallow, h, cfg, ComplexMatrix::Zero(cfg.K, cfg.M)), TrainingError);
+    CHECK_THROWS_AS(backward(fwd.tape, deep, h, cfg, ComplexMatrix::Zero(cfg.K, cfg.M + 1)), TrainingError);
+  }
+  {  // an all-zero output (huge threshold): zero gradients (test_unfolded.cpp:280-299)
+    SystemConfig cfg = SystemConfig::uniform(4, 16, 10.0);
+    ChannelMatrix h = channel_for(cfg, 46, 0);
+    UnfoldedNetwork net = UnfoldedNetwork::pgd_init(cfg.K, cfg.M, 1, 1e6);
+    ForwardOptions opt;
+    opt.with_tape = true;
+    ForwardResult fwd = forward(net, h, cfg, std::nullopt, opt);
+    bool zero = true;
+    for (std::ptrdiff_t i = 0; i < fwd.output.size(); ++i) zero = zero && fwd.output.data()[i] == Complex(0.0, 0.0);
+    CHECK(zero);
+    Rng rng = Rng::stream(47, 0);
+    ParamGradients g = backward(fwd.tape, net, h, cfg, random_matrix(cfg.K, cfg.M, rng));
+    CHECK(g.d_lambda[0] == 0.0 && g.d_eta[0] == 0.0);
+  }
+}
 
 static void training_tests() {
   // --- test_training.cpp ----------------------------------------------------------
@@ -711,6 +802,7 @@ int main() {
     CHECK(train_gradients(next, H.data(), B, cfg).loss <= g.loss * (1.0 + 1e-9));
     CHECK_THROWS_AS(train_gradients(net, H.data(), B, cfg, LossKind::Supervised), TrainingError);
   }
+  backward_tests();
   training_tests();
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;

@@ -74,3 +74,33 @@ def test_grad_validation():
         U.unfolded_grad(H, [0.1], [0.01], np.ones(4), loss_kind=1)  # no labels
     with pytest.raises(ValueError):
         U.unfolded_grad(H, [0.1], [0.01], np.ones(4), lambda_cost=-1.0)
+
+
+@pytest.mark.parametrize("K,M,L", [(4, 16, 5), (8, 64, 20), (3, 8, 2)])
+def test_fp64_backward_matches_oracle_backward(K, M, L):
+    """ufpgd_gpu_unfolded_backward64 (the C++ API's backward) against the
+    oracle's restatement of unfolded.cpp:158-239 on the oracle's own tape,
+    for an arbitrary output gradient, to FP64 rounding."""
+    cfg = O.SystemConfig.uniform(K, M, 10.0)
+    rng = O.Rng.stream(91, K)
+    net = O.UnfoldedNetwork.pgd_init(K, M, L, 1.0 / 15.0)
+    for layer in net.layers:
+        layer.lambda_i *= 0.5 + rng.uniform()
+        layer.eta_i *= 0.6 + 0.4 * rng.uniform()
+    net = O.project_params(net)
+    lam = np.array([l.lambda_i for l in net.layers])
+    eta = np.array([l.eta_i for l in net.layers])
+    Hs, Gs, ref = [], [], []
+    for d in range(4):
+        h = O.channel_for(cfg, 92, d)
+        dcost = O.random_matrix(K, M, rng)
+        fwd = O.forward(net, h, cfg, options=O.ForwardOptions(with_tape=True))
+        g = O.backward(fwd.tape, net, h, cfg, dcost)
+        Hs.append(O.to_storage(h))
+        Gs.append(O.to_storage(dcost))
+        ref.append(np.stack([g.d_lambda, g.d_eta], axis=1).reshape(-1))
+    H = torch.from_numpy(np.stack(Hs)).cuda()
+    G = torch.from_numpy(np.stack(Gs)).cuda()
+    out = U.unfolded_backward64(H, lam, eta, cfg.constraint_diag(), G).cpu().numpy()
+    ref = np.stack(ref)
+    assert np.allclose(out, ref, rtol=1e-9, atol=1e-12 * np.abs(ref).max()), np.abs(out - ref).max()
