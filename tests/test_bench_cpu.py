@@ -1,0 +1,36 @@
+"""bench.py contract checks that run without a GPU: the reference arm
+(`--impl reference`, the FP64 oracle port on the host cores) prints one JSON
+line with the fields the driver reads, and the cost model / geometry helpers
+are consistent."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_prints_one_contract_line():
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "1"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+def test_cost_model_counts_performed_contractions():
+    sys.path.insert(0, ROOT)
+    import paper_2304_12745_b200 as U
+
+    w = U.CONFIGS[2]
+    K, M, L = w.K, w.M, w.L
+    assert w.flops_per_realization() == (2 * L - 2) * 8 * K * K * M + 10 * K * M * L
+    assert w.flops_per_realization(exact_w0=False) == 2 * L * 8 * K * K * M + 10 * K * M * L
+    assert w.bytes_per_realization() == 16 * K * M
