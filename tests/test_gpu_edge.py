@@ -71,3 +71,20 @@ def test_host_batch_with_partial_last_chunk_matches_device_path():
     devw = U.unfolded_forward(dev(H), lam, eta, w.c, w0_mode=w.w0_mode)
     assert np.array_equal(host["W"], devw["W"].cpu().numpy())
     assert np.allclose(host["stats"], devw["stats"].cpu().numpy(), rtol=1e-12)
+
+
+@pytest.mark.parametrize("K,M", [(4, 32), (8, 64), (16, 128), (32, 256)])
+def test_divergence_from_a_zero_start_on_every_kernel_shape(K, M):
+    """W0 = 0 takes the exact layer-0 shortcut (eta c_k conj(H)); a channel that
+    is +inf in complex64 must still be reported at layer 0 (unfolded.cpp:120-125)
+    and leave its neighbours untouched."""
+    with np.errstate(over="ignore"):
+        H = np.full((3, M, K), 1e200, dtype=np.complex128).astype(np.complex64)
+    H[1] = U.generate_channels(5, 0, 0.0, 0, 1, K, M)[0]
+    lam, eta = params(K, M, 4)
+    c = np.full(K, np.sqrt(10.0))
+    out = U.unfolded_forward(dev(H), lam, eta, c, w0_mode=U.W0_ZERO, want_per_realization=True)
+    d = out["diverged_at"].cpu().numpy()
+    assert d[0] == 0 and d[2] == 0 and d[1] == -1
+    ora = O.forward_batch_f32(H[1:2], c, lam, eta, w0_mode=U.W0_ZERO)
+    assert_parity(report(H[1:2], out["W"].cpu().numpy()[1:2], ora, c, 1.0 / 15.0))
