@@ -18,9 +18,9 @@ struct PgdParams {
   double eta = 0.0;
   long max_iters = 0;
   double residual_tol = 0.0;
-  long trace_every = 0;  // tracing is not part of the B200 path: must be 0
+  long trace_every = 0;  // > 0: record a TraceRecord every trace_every iterations (pgd.cpp:196-223)
 
-  void validate() const;  // pgd.cpp:33-49 (+ trace_every == 0)
+  void validate() const;  // pgd.cpp:33-49
 };
 
 struct TraceRecord {

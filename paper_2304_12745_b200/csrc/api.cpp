@@ -241,8 +241,6 @@ void PgdParams::validate() const {
   if (max_iters < 0) throw std::invalid_argument("PgdParams: max_iters must be >= 0");
   if (!(residual_tol >= 0.0)) throw std::invalid_argument("PgdParams: residual_tol must be >= 0");
   if (trace_every < 0) throw std::invalid_argument("PgdParams: trace_every must be >= 0");
-  if (trace_every > 0)
-    throw std::invalid_argument("PgdParams: trace recording is not part of the B200 path (trace_every must be 0)");
 }
 
 SmoothGradient SmoothGradient::make(const ChannelMatrix& channel, const SystemConfig& cfg) {
@@ -326,37 +324,87 @@ double lagrangian_value(const PrecoderMatrix& precoder, const ChannelMatrix& cha
 }
 
 PgdResult solve_pgd(const ChannelMatrix& channel, const SystemConfig& cfg, const PgdParams& params,
-                    const std::optional<PrecoderMatrix>& start) {
+                    const std::optional<PrecoderMatrix>& start) {  // pgd.cpp:178-268
   check_shapes(channel, cfg);
   params.validate();
   if (start && (start->rows() != cfg.K || start->cols() != cfg.M))
     throw std::invalid_argument("solve_pgd: W0 shape mismatch");
   PgdResult result;
+  const bool tracing = params.trace_every > 0;
+  PrecoderMatrix zf_reference;
+  if (tracing) zf_reference = zf_precoder(channel, cfg);  // SingularChannelError as in the reference
+  PrecoderMatrix w = start ? *start : channel.conjugate();
+  // Trace record (pgd.cpp:204-221): FP64 on the host from the device iterate,
+  // exactly the reference's formulae (diagnostics, off the solver path).
+  auto record = [&](long index) {
+    const int K = cfg.K, M = cfg.M;
+    const RealVector c = cfg.constraint_diag();
+    TraceRecord rec;
+    rec.index = index;
+    double res2 = 0.0;
+    RealVector sinr(K);
+    const double noise = cfg.sigma_nu * cfg.sigma_nu;
+    for (int k = 0; k < K; ++k) {
+      double row2 = 0.0, signal = 0.0;
+      for (int j = 0; j < K; ++j) {
+        Complex e = 0.0;  // effective channel (H W^T)(k, j)
+        for (int m = 0; m < M; ++m) e += channel(k, m) * w(j, m);
+        const double p2 = std::norm(e);
+        row2 += p2;
+        if (j == k) signal = p2;
+        res2 += std::norm(j == k ? e - c[k] : e);
+      }
+      sinr[k] = signal / (row2 - signal + noise);
+    }
+    rec.residual = std::sqrt(res2);
+    rec.lagrangian = params.lambda * l21_norm(w) + rec.residual * rec.residual;
+    rec.pcg = pcg_from_reference(zf_reference, w);
+    rec.sum_rate = sum_rate(sinr);
+    rec.active_columns = count_active_columns(w);
+    result.trace.records.push_back(rec);
+  };
+  if (tracing) record(0);
   if (params.max_iters == 0) {
-    result.precoder = start ? *start : channel.conjugate();
+    result.precoder = w;
     return result;
   }
   const int K = cfg.K, M = cfg.M;
   const std::size_t n = static_cast<std::size_t>(K) * M;
   DeviceScope scope;
-  DeviceBuffer<double> dH(2 * n), dW(2 * n), dW0(start ? 2 * n : 0), deta(1);
+  DeviceBuffer<double> dH(2 * n), dW(2 * n), dW0(2 * n), deta(1);
   DeviceBuffer<int32_t> ddiv(1);
   DeviceBuffer<int64_t> dits(1);
   dH.upload(reinterpret_cast<const double*>(channel.data()));
-  if (start) dW0.upload(reinterpret_cast<const double*>(start->data()));
   deta.upload(&params.eta);
   const RealVector c = cfg.constraint_diag();
-  check(ufpgd_gpu_solve_pgd64(dH.p, 1, K, M, c.data(), params.lambda, deta.p, params.max_iters, params.residual_tol,
-                              start ? dW0.p : nullptr, dW.p, dits.p, ddiv.p, g_device, nullptr));
-  cuda_check(cudaDeviceSynchronize(), "solve_pgd");
-  int32_t div = -1;
-  ddiv.download(&div);
-  if (div >= 0) throw DivergenceError("solve_pgd: non-finite iterate", div);
-  result.precoder = ComplexMatrix(K, M);
-  dW.download(reinterpret_cast<double*>(result.precoder.data()));
-  int64_t its = 0;
-  dits.download(&its);
-  result.iterations = static_cast<long>(its);
+  // Without tracing one launch runs every iteration; with tracing the solve
+  // runs in chunks of trace_every iterations, each restarting from the last
+  // iterate (the iteration is memoryless), with a record after every chunk.
+  const long chunk = tracing ? params.trace_every : params.max_iters;
+  long done = 0, last_recorded = 0;
+  while (done < params.max_iters) {
+    const long its_now = std::min(chunk, params.max_iters - done);
+    dW0.upload(reinterpret_cast<const double*>(w.data()));
+    check(ufpgd_gpu_solve_pgd64(dH.p, 1, K, M, c.data(), params.lambda, deta.p, its_now, params.residual_tol, dW0.p,
+                                dW.p, dits.p, ddiv.p, g_device, nullptr));
+    cuda_check(cudaDeviceSynchronize(), "solve_pgd");
+    int32_t div = -1;
+    ddiv.download(&div);
+    if (div >= 0) throw DivergenceError("solve_pgd: non-finite iterate", done + div);
+    w = ComplexMatrix(K, M);
+    dW.download(reinterpret_cast<double*>(w.data()));
+    int64_t its = 0;
+    dits.download(&its);
+    done += its;
+    result.iterations = done;
+    if (tracing && done % params.trace_every == 0) {
+      record(done);
+      last_recorded = done;
+    }
+    if (its < its_now) break;  // residual_tol stop inside the chunk
+  }
+  if (tracing && result.iterations > last_recorded) record(result.iterations);
+  result.precoder = std::move(w);
   return result;
 }
 

@@ -139,6 +139,77 @@ static double mean_supervised_loss(const UnfoldedNetwork& net, const Dataset& da
 
 static double rel_err(double a, double b) { return std::abs(a - b) / std::max(std::abs(a), std::abs(b)); }
 
+static void trace_tests() {
+  // --- test_pgd.cpp: solve_pgd traces ---------------------------------------------
+  {  // the descent objective is non-increasing at the exact step (test_pgd.cpp:399-425)
+    SystemConfig cfg = SystemConfig::uniform(8, 64, 10.0);
+    const double lambda = 1.0 / 15.0;
+    bool mono = true, sized = true;
+    for (std::uint64_t draw = 0; draw < 5; ++draw) {
+      ChannelMatrix h = channel_for(cfg, 28, draw);
+      PgdParams p;
+      p.lambda = lambda;
+      p.eta = 1.0 / lipschitz_bound(h).exact;
+      p.max_iters = 300;
+      p.trace_every = 1;
+      PgdResult r = solve_pgd(h, cfg, p);
+      sized = sized && r.trace.records.size() == 301;
+      auto descent = [](const TraceRecord& rec) { return rec.lagrangian - 0.5 * rec.residual * rec.residual; };
+      for (std::size_t i = 1; i < r.trace.records.size(); ++i) {
+        const double prev = descent(r.trace.records[i - 1]), next = descent(r.trace.records[i]);
+        if (!(next <= prev + 1e-12 * std::max(1.0, std::abs(prev)))) mono = false;
+      }
+    }
+    CHECK(sized);
+    CHECK(mono);
+  }
+  {  // trace sampling covers start, stride and final iterate (test_pgd.cpp:472-516)
+    SystemConfig cfg = SystemConfig::uniform(3, 8, 10.0);
+    ChannelMatrix h = channel_for(cfg, 32, 0);
+    PgdParams p;
+    p.lambda = 1.0 / 15.0;
+    p.eta = 1.0 / mp_bound(cfg.K, cfg.M);
+    p.max_iters = 0;
+    p.trace_every = 1;
+    PgdResult r0 = solve_pgd(h, cfg, p);
+    CHECK(r0.trace.records.size() == 1 && r0.trace.records[0].index == 0 && r0.iterations == 0);
+    const double expected = lagrangian_value(h.conjugate(), h, cfg, p.lambda);
+    CHECK(std::abs(r0.trace.records[0].lagrangian - expected) <= 1e-15 * std::abs(expected));
+    p.max_iters = 7;
+    p.trace_every = 3;
+    PgdResult r = solve_pgd(h, cfg, p);
+    CHECK(r.trace.records.size() == 4);
+    if (r.trace.records.size() == 4)
+      CHECK(r.trace.records[0].index == 0 && r.trace.records[1].index == 3 && r.trace.records[2].index == 6 &&
+            r.trace.records[3].index == 7);
+    // the chunked, traced solve ends where the untraced one does
+    PgdParams q = p;
+    q.trace_every = 0;
+    PgdResult u = solve_pgd(h, cfg, q);
+    double diff = 0.0;
+    for (std::ptrdiff_t i = 0; i < u.precoder.size(); ++i) diff = std::max(diff, std::abs(u.precoder.data()[i] - r.precoder.data()[i]));
+    CHECK(u.trace.records.empty() && diff <= 1e-14);
+    CHECK(r.trace.records[3].pcg > 0.0 && r.trace.records[3].sum_rate > 0.0 && r.trace.records[3].active_columns > 0.0);
+  }
+  {  // a residual_tol stop inside a traced chunk records the final iterate once
+    SystemConfig cfg = SystemConfig::uniform(4, 16, 10.0);
+    ChannelMatrix h = channel_for(cfg, 33, 1);
+    PgdParams p;
+    p.lambda = 0.05;
+    p.eta = 1.0 / lipschitz_bound(h).exact;
+    p.max_iters = 100000;
+    p.residual_tol = 1e-6;
+    p.trace_every = 50;
+    PgdResult r = solve_pgd(h, cfg, p);
+    PgdParams q = p;
+    q.trace_every = 0;
+    PgdResult u = solve_pgd(h, cfg, q);
+    CHECK(r.iterations == u.iterations && r.iterations < 100000);
+    CHECK(!r.trace.records.empty() && r.trace.records.back().index == r.iterations);
+    CHECK(r.trace.records.size() == static_cast<std::size_t>(r.iterations / 50 + 1 + (r.iterations % 50 ? 1 : 0)));
+  }
+}
+
 static void backward_tests() {
   // --- test_unfolded.cpp: backward ---------------------------------------------
   {  // central finite differences of a supervised cost (test_unfolded.cpp:302-381)
@@ -802,6 +873,7 @@ int main() {
     CHECK(train_gradients(next, H.data(), B, cfg).loss <= g.loss * (1.0 + 1e-9));
     CHECK_THROWS_AS(train_gradients(net, H.data(), B, cfg, LossKind::Supervised), TrainingError);
   }
+  trace_tests();
   backward_tests();
   training_tests();
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
