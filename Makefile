@@ -7,13 +7,13 @@ PKG      := paper_2304_12745_b200
 LIBDIR   := $(PKG)/lib
 OBJDIR   := build/obj
 SRCS_CU  := $(addprefix $(PKG)/csrc/,team.cu tile.cu general.cu metrics.cu grad.cu datagen.cu probe.cu)
-SRCS_CPP := $(PKG)/csrc/capi.cpp $(PKG)/csrc/host_gen.cpp $(PKG)/csrc/api.cpp $(PKG)/csrc/dataset_io.cpp
+SRCS_CPP := $(PKG)/csrc/capi.cpp $(PKG)/csrc/host_gen.cpp $(PKG)/csrc/api.cpp $(PKG)/csrc/dataset_io.cpp $(PKG)/csrc/host_util.cpp
 CXX      ?= g++
 CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -Iinclude -I$(PKG)/csrc -I/usr/local/cuda/include
 OBJS     := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(SRCS_CU)) $(patsubst $(PKG)/csrc/%.cpp,$(OBJDIR)/%.o,$(SRCS_CPP))
 HDRS     := include/ufpgd_gpu.h $(PKG)/csrc/ufpgd_internal.h $(PKG)/csrc/device_common.cuh $(wildcard include/ufpgd/*.hpp)
 
-all: $(LIBDIR)/libufpgd_gpu.so oracle build/test_api build/train_dump build/test_json
+all: $(LIBDIR)/libufpgd_gpu.so oracle build/test_api build/train_dump build/test_host
 
 $(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -31,7 +31,7 @@ build/test_api: tests/cpp/test_api.cpp $(LIBDIR)/libufpgd_gpu.so $(HDRS)
 	@mkdir -p build
 	$(CXX) -O2 -std=c++20 -Iinclude -I/usr/local/cuda/include $< -o $@ -L$(LIBDIR) -lufpgd_gpu -Wl,-rpath,'$$ORIGIN/../$(LIBDIR)'
 
-build/test_json: tests/cpp/test_json.cpp $(LIBDIR)/libufpgd_gpu.so $(HDRS)
+build/test_host: tests/cpp/test_host.cpp $(LIBDIR)/libufpgd_gpu.so $(HDRS)
 	@mkdir -p build
 	$(CXX) -O2 -std=c++20 -Iinclude -I/usr/local/cuda/include $< -o $@ -L$(LIBDIR) -lufpgd_gpu -Wl,-rpath,'$$ORIGIN/../$(LIBDIR)'
 

@@ -21,7 +21,8 @@ def test_cpp_api_on_device():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-def test_model_json_files_on_host():
-    """unfolded.cpp:241-298 model files through the drop-in C++ API (no GPU needed)."""
-    r = subprocess.run([os.path.join(ROOT, "build", "test_json")], capture_output=True, text=True, timeout=120)
+def test_host_side_api_without_a_gpu():
+    """Model JSON files (unfolded.cpp:241-298), trace CSV files (trace_io.cpp)
+    and parallel_for (parallel.cpp:25-59) through the drop-in C++ API."""
+    r = subprocess.run([os.path.join(ROOT, "build", "test_host")], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr

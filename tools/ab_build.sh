@@ -14,5 +14,5 @@ for f in team tile general metrics grad datagen probe; do
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o tools/ablib/$name/libufpgd_gpu.so \
-  $objs build/obj/capi.o build/obj/host_gen.o build/obj/api.o build/obj/dataset_io.o -ldl -lpthread
+  $objs build/obj/capi.o build/obj/host_gen.o build/obj/api.o build/obj/dataset_io.o build/obj/host_util.o -ldl -lpthread
 grep -A2 "fused_kernelINS0_4TeamILi8ELi64" build/obj/ab/$name/team.log | grep -oE "Used [0-9]+ registers|[0-9]+ bytes spill stores" | tr '\n' ' '; echo " [$name]"
