@@ -14,11 +14,29 @@
 #include <thread>
 #include <vector>
 
+#include "ufpgd/channel.hpp"
 #include "ufpgd/errors.hpp"
 #include "ufpgd/parallel.hpp"
 #include "ufpgd/trace_io.hpp"
 
 namespace ufpgd {
+
+ComplexVector simulate_received(const ChannelMatrix& channel, const PrecoderMatrix& precoder,
+                                const ComplexVector& symbols, const SystemConfig& cfg, Rng& rng) {
+  cfg.validate();
+  if (channel.rows() != cfg.K || channel.cols() != cfg.M || precoder.rows() != cfg.K || precoder.cols() != cfg.M ||
+      static_cast<int>(symbols.size()) != cfg.K)
+    throw std::invalid_argument("simulate_received: shape mismatch");
+  ComplexVector x(static_cast<std::size_t>(cfg.M), Complex(0.0, 0.0));  // transmit vector W^T s
+  for (int m = 0; m < cfg.M; ++m)
+    for (int k = 0; k < cfg.K; ++k) x[m] += precoder(k, m) * symbols[k];
+  ComplexVector r(static_cast<std::size_t>(cfg.K), Complex(0.0, 0.0));
+  for (int k = 0; k < cfg.K; ++k) {
+    for (int m = 0; m < cfg.M; ++m) r[k] += channel(k, m) * x[m];
+    r[k] += cfg.sigma_nu * rng.complex_gaussian();
+  }
+  return r;
+}
 
 int default_thread_count() {
   if (const char* v = std::getenv("UFPGD_THREADS")) {
