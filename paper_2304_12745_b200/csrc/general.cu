@@ -358,6 +358,7 @@ size_t general64_smem_bytes(int K, int M) {
 }
 
 cudaError_t launch_general64(const GeneralArgs64& a, cudaStream_t s) {
+  if (pgd64_team_supported(a)) return launch_pgd64_team(a, s);
   const size_t smem = general64_smem_bytes(a.K, a.M);
   cudaError_t e = cudaFuncSetAttribute(general_kernel_t<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));

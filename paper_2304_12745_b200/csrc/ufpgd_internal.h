@@ -127,6 +127,10 @@ cudaError_t launch_tiled(const FusedArgs& a, bool pgd, int K, int M, cudaStream_
 size_t general_smem_bytes(int K, int M);
 cudaError_t launch_general(const GeneralArgs& a, cudaStream_t s);
 cudaError_t launch_general64(const GeneralArgs64& a, cudaStream_t s);
+// FP64 warp-per-realization PGD for (8,64) and (4,32) (team64.cu); launch_general64
+// dispatches there for plain batched PGD without tapes or iterates.
+bool pgd64_team_supported(const GeneralArgs64& a);
+cudaError_t launch_pgd64_team(const GeneralArgs64& a, cudaStream_t s);
 size_t general64_smem_bytes(int K, int M);
 cudaError_t launch_power(const PowerArgs& a, cudaStream_t s);
 cudaError_t launch_lipschitz_exact(const double2* H, long long B, int K, int M, const double2* v0,

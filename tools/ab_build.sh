@@ -6,7 +6,7 @@ name=$1; shift
 cd "$(dirname "$0")/.."
 mkdir -p tools/ablib/$name build/obj/ab/$name
 objs=""
-for f in team tile general metrics grad datagen probe; do
+for f in team team64 tile general metrics grad datagen probe; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++20 -Xcompiler -fPIC -Iinclude \
     -Ipaper_2304_12745_b200/csrc "$@" -Xptxas -v -c paper_2304_12745_b200/csrc/$f.cu \
     -o build/obj/ab/$name/$f.o 2> build/obj/ab/$name/$f.log &
