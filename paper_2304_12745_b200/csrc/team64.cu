@@ -32,7 +32,10 @@ struct Team64 {
 };
 
 template <class S>
-__global__ void __launch_bounds__(32) pgd64_team_kernel(const __grid_constant__ GeneralArgs64 p) {
+#ifndef UFPGD_T64_MINB
+#define UFPGD_T64_MINB 1
+#endif
+__global__ void __launch_bounds__(32, UFPGD_T64_MINB) pgd64_team_kernel(const __grid_constant__ GeneralArgs64 p) {
   __shared__ double2 hs[S::M * S::K];
   const int lane = threadIdx.x, a = lane / S::TM, b = lane % S::TM;
   const long long rid = blockIdx.x;
