@@ -59,6 +59,14 @@ TrainGradients train_gradients(const UnfoldedNetwork& net, const std::complex<fl
                                const SystemConfig& cfg, LossKind kind = LossKind::Unsupervised,
                                double lambda_cost = 1.0 / 15.0, const std::complex<float>* labels = nullptr);
 
+// oracle_solve (pgd.cpp:270-279) over many channels in FP64 on the device —
+// the supervised labels of train (commands.cpp:163-168): converged power
+// iteration, then PGD with the 1e-10 relative-change stop, one warp per
+// channel retiring on convergence. Same results as the per-channel call;
+// ConvergenceError / DivergenceError name the first failing channel.
+std::vector<PrecoderMatrix> oracle_solve_batch(const std::vector<ChannelMatrix>& channels, const SystemConfig& cfg,
+                                               double lambda);
+
 // evaluate (training.cpp:310-421) over a stacked complex<float> batch without
 // per-layer curves: singular channels are counted in `singular` and skipped
 // instead of throwing.

@@ -430,6 +430,43 @@ PrecoderMatrix oracle_solve(const ChannelMatrix& channel, const SystemConfig& cf
   return W;
 }
 
+std::vector<PrecoderMatrix> oracle_solve_batch(const std::vector<ChannelMatrix>& channels, const SystemConfig& cfg,
+                                               double lambda) {
+  cfg.validate();
+  if (!(lambda >= 0.0)) throw std::invalid_argument("PgdParams: lambda must be >= 0");
+  for (const ChannelMatrix& h : channels) check_shapes(h, cfg);
+  const int K = cfg.K, M = cfg.M;
+  const std::size_t n = static_cast<std::size_t>(K) * M, B = channels.size();
+  std::vector<PrecoderMatrix> out;
+  if (B == 0) return out;
+  DeviceScope scope;
+  DeviceBuffer<double> dH(2 * n * B), dW(2 * n * B);
+  DeviceBuffer<int32_t> dst(B);
+  std::vector<double> stage(2 * n * B);
+  for (std::size_t b = 0; b < B; ++b)
+    std::memcpy(&stage[2 * n * b], static_cast<const void*>(channels[b].data()), 2 * n * sizeof(double));
+  dH.upload(stage.data());
+  const RealVector c = cfg.constraint_diag();
+  check(ufpgd_gpu_oracle_solve(dH.p, static_cast<int64_t>(B), K, M, c.data(), lambda, 100000, 1e-10, dW.p, nullptr,
+                               nullptr, dst.p, g_device, nullptr));
+  std::vector<int32_t> st(B);
+  dst.download(st.data());
+  for (std::size_t b = 0; b < B; ++b) {
+    if (st[b] == UFPGD_ECONVERGENCE)
+      throw ConvergenceError("lipschitz_bound: power iteration did not reach tolerance 1e-8 within 10000 iterations "
+                             "(channel " + std::to_string(b) + ")");
+    if (st[b] == UFPGD_EDIVERGED) throw DivergenceError("solve_pgd: non-finite iterate (channel " + std::to_string(b) + ")", -1);
+  }
+  dW.download(stage.data());
+  out.reserve(B);
+  for (std::size_t b = 0; b < B; ++b) {
+    ComplexMatrix W(K, M);
+    std::memcpy(static_cast<void*>(W.data()), &stage[2 * n * b], 2 * n * sizeof(double));
+    out.push_back(std::move(W));
+  }
+  return out;
+}
+
 // ---- unfolded.cpp -------------------------------------------------------------
 UnfoldedNetwork UnfoldedNetwork::pgd_init(int num_users, int num_antennas, int num_layers, double lambda) {
   if (num_layers < 1) throw std::invalid_argument("pgd_init: need at least one layer");

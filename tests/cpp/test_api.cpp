@@ -139,6 +139,23 @@ static double mean_supervised_loss(const UnfoldedNetwork& net, const Dataset& da
 
 static double rel_err(double a, double b) { return std::abs(a - b) / std::max(std::abs(a), std::abs(b)); }
 
+static void oracle_batch_tests() {
+  {  // oracle_solve_batch == per-channel oracle_solve, bit for bit (one warp per channel either way)
+    SystemConfig cfg = SystemConfig::uniform(8, 64, 10.0);
+    std::vector<ChannelMatrix> hs;
+    for (int d = 0; d < 6; ++d) hs.push_back(channel_for(cfg, 95, d));
+    const std::vector<PrecoderMatrix> ws = oracle_solve_batch(hs, cfg, 1.0 / 15.0);
+    bool same = ws.size() == hs.size();
+    for (std::size_t d = 0; same && d < hs.size(); ++d) {
+      const PrecoderMatrix one = oracle_solve(hs[d], cfg, 1.0 / 15.0);
+      for (std::ptrdiff_t i = 0; same && i < one.size(); ++i) same = one.data()[i] == ws[d].data()[i];
+    }
+    CHECK(same);
+    CHECK(oracle_solve_batch({}, cfg, 0.1).empty());
+    CHECK_THROWS_AS(oracle_solve_batch(hs, cfg, -1.0), std::invalid_argument);
+  }
+}
+
 static void trace_tests() {
   // --- test_pgd.cpp: solve_pgd traces ---------------------------------------------
   {  // the descent objective is non-increasing at the exact step (test_pgd.cpp:399-425)
@@ -873,6 +890,7 @@ int main() {
     CHECK(train_gradients(next, H.data(), B, cfg).loss <= g.loss * (1.0 + 1e-9));
     CHECK_THROWS_AS(train_gradients(net, H.data(), B, cfg, LossKind::Supervised), TrainingError);
   }
+  oracle_batch_tests();
   trace_tests();
   backward_tests();
   training_tests();
