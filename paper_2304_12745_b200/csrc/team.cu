@@ -645,7 +645,10 @@ cudaError_t launch_team(const FusedArgs& a, bool pgd, cudaStream_t s, long long*
 
 // Team shapes (K, M) -> (TK, TM): KA = K/TK = 2 users and MB = M/TM antennas
 // per thread keep W, X' and the next X' in registers.
-using Team_4_32 = Team<4, 32, 2, 4>;
+#ifndef UFPGD_T432_TM
+#define UFPGD_T432_TM 4
+#endif
+using Team_4_32 = Team<4, 32, 2, UFPGD_T432_TM>;
 // Config 2's unfolded kernel: two sweeps per layer fit 168 registers without
 // spills, so 3 resident 4-warp blocks (12 warps/SM) — 3% over 8 warps at 255.
 #ifndef UFPGD_T864_MAXT
@@ -658,25 +661,41 @@ using Team_4_32 = Team<4, 32, 2, 4>;
 #define UFPGD_T864_TK 4
 #endif
 using Team_8_64 = Team<8, 64, UFPGD_T864_TK, 16 / UFPGD_T864_TK, UFPGD_T864_MAXT, UFPGD_T864_MINB>;
+// Neighbouring shapes of the BASELINE ones (the paper sweeps users and
+// antennas around K = 8, M = 64) get the same fused kernel instead of the
+// general one: 2 users x M/TM antennas per thread.
+using Team_4_16 = Team<4, 16, 2, 4>;
+using Team_4_64 = Team<4, 64, 2, 4>;
+using Team_8_32 = Team<8, 32, 4, 4>;
+using Team_8_128 = Team<8, 128, 4, 8, 128, 3>;
 
 }  // namespace
 
 bool fused_supported(int K, int M) {
-  return (K == 4 && M == 32) || (K == 8 && M == 64) || (K == 16 && M == 128) || (K == 32 && M == 256);
+  return (K == 4 && (M == 16 || M == 32 || M == 64)) || (K == 8 && (M == 32 || M == 64 || M == 128)) ||
+         (K == 16 && M == 128) || (K == 32 && M == 256);
 }
 
 // Upper bound on realizations per block (partials are sized with the smallest
 // block the geometry chooser can pick: one warp).
 
 int fused_realizations_per_block(int K, int M) {
+  if (K == 4 && M == 16) return Team_4_16::R;
   if (K == 4 && M == 32) return Team_4_32::R;
+  if (K == 4 && M == 64) return Team_4_64::R;
+  if (K == 8 && M == 32) return Team_8_32::R;
   if (K == 8 && M == 64) return Team_8_64::R;
+  if (K == 8 && M == 128) return Team_8_128::R;
   return 1;  // tile kernels: one realization per block
 }
 
 cudaError_t launch_fused(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s, long long* nblocks) {
+  if (K == 4 && M == 16) return launch_team<Team_4_16>(a, pgd, s, nblocks);
   if (K == 4 && M == 32) return launch_team<Team_4_32>(a, pgd, s, nblocks);
+  if (K == 4 && M == 64) return launch_team<Team_4_64>(a, pgd, s, nblocks);
+  if (K == 8 && M == 32) return launch_team<Team_8_32>(a, pgd, s, nblocks);
   if (K == 8 && M == 64) return launch_team<Team_8_64>(a, pgd, s, nblocks);
+  if (K == 8 && M == 128) return launch_team<Team_8_128>(a, pgd, s, nblocks);
   return launch_tiled(a, pgd, K, M, s, nblocks);  // tile.cu: (16,128), (32,256)
 }
 

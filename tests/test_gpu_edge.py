@@ -22,7 +22,7 @@ def params(K, M, L, seed=5):
     return U.project_params(lam, eta, K, M)
 
 
-@pytest.mark.parametrize("K,M", [(4, 32), (8, 64), (16, 128), (32, 256)])
+@pytest.mark.parametrize("K,M", [(4, 16), (4, 32), (4, 64), (8, 32), (8, 64), (8, 128), (16, 128), (32, 256)])
 @pytest.mark.parametrize("B", [1, 2, 3, 17])
 def test_ragged_batches_every_kernel_shape(K, M, B):
     H = U.generate_channels(77, 78, 10.0, 3, B, K, M)
@@ -73,7 +73,7 @@ def test_host_batch_with_partial_last_chunk_matches_device_path():
     assert np.allclose(host["stats"], devw["stats"].cpu().numpy(), rtol=1e-12)
 
 
-@pytest.mark.parametrize("K,M", [(4, 32), (8, 64), (16, 128), (32, 256)])
+@pytest.mark.parametrize("K,M", [(4, 16), (4, 32), (4, 64), (8, 32), (8, 64), (8, 128), (16, 128), (32, 256)])
 def test_divergence_from_a_zero_start_on_every_kernel_shape(K, M):
     """W0 = 0 takes the exact layer-0 shortcut (eta c_k conj(H)); a channel that
     is +inf in complex64 must still be reported at layer 0 (unfolded.cpp:120-125)
