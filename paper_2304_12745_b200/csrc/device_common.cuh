@@ -36,14 +36,6 @@ __device__ __forceinline__ void cmac(float2& acc, float2 a, float2 b) {
   acc.y = fmaf(a.y, b.x, acc.y);
 }
 
-// acc += a * conj(b)
-__device__ __forceinline__ void cmac_conj(float2& acc, float2 a, float2 b) {
-  acc.x = fmaf(a.x, b.x, acc.x);
-  acc.x = fmaf(a.y, b.y, acc.x);
-  acc.y = fmaf(a.y, b.x, acc.y);
-  acc.y = fmaf(-a.x, b.y, acc.y);
-}
-
 // Packed FP32x2 arithmetic (sm_100a FFMA2 / FMUL2 / FADD2). A complex matrix
 // is held split into real and imaginary parts, each packed over the thread's
 // user PAIR (rows k, k+1): re = (Re W(k,m), Re W(k+1,m)), im likewise. A

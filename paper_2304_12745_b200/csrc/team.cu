@@ -76,18 +76,6 @@ struct Team {
   static_assert(KA % 2 == 0 && K % 2 == 0, "users are processed in FFMA2 pairs");
 };
 
-// Loads row m of H (all K users, complex) from shared memory.
-template <class S>
-__device__ __forceinline__ void load_col(const float* hs, int m, float2 (&h)[S::K]) {
-  const float4* hp = reinterpret_cast<const float4*>(hs + m * S::HS);
-  const int f = S::swz(m);
-#pragma unroll
-  for (int q = 0; q < S::K / 2; ++q) {
-    const float4 t = hp[q ^ f];
-    h[2 * q] = make_float2(t.x, t.y);
-    h[2 * q + 1] = make_float2(t.z, t.w);
-  }
-}
 
 // Per-thread H row pointers: with TM even, the unit swizzle of antenna
 // m = i * TM + b splits into a compile-time part (from i) XOR a per-thread part
