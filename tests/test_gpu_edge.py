@@ -88,3 +88,23 @@ def test_divergence_from_a_zero_start_on_every_kernel_shape(K, M):
     assert d[0] == 0 and d[2] == 0 and d[1] == -1
     ora = O.forward_batch_f32(H[1:2], c, lam, eta, w0_mode=U.W0_ZERO)
     assert_parity(report(H[1:2], out["W"].cpu().numpy()[1:2], ora, c, 1.0 / 15.0))
+
+
+def test_pgd_host_path_matches_device_path():
+    """ufpgd_gpu_pgd_fixed_host (config 3 end to end: pinned-chunk pipeline,
+    in-kernel 30-step power iteration) equals the device entry point bit for
+    bit, including the per-realization step it reports."""
+    w = U.CONFIGS[3]
+    H = U.make_inputs(w, 0, 1000)
+    host = U.pgd_fixed_host(H, w.lambda_pgd, 300, w.c, power_steps=w.power_steps)
+    d = U.pgd_fixed(dev(H), w.lambda_pgd, 300, w.c, power_steps=w.power_steps)
+    assert np.array_equal(host["W"], d["W"].cpu().numpy())
+    assert np.array_equal(host["diverged_at"], d["diverged_at"].cpu().numpy())
+    assert np.allclose(host["stats"], d["stats"].cpu().numpy(), rtol=1e-12)
+
+
+def test_fp32_peak_probe_is_plausible():
+    """The roofline denominator bench.py reports: the FFMA2 probe on this B200
+    (nominal 148 SMs x 128 lanes x 2 x 1.965 GHz = 74.4 TFLOP/s)."""
+    tf, ghz = U.fp32_peak(0)
+    assert 30.0 < tf < 80.0 and 1.0 < ghz < 2.2, (tf, ghz)
