@@ -30,6 +30,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <algorithm>
+#include <type_traits>
 
 #include "ufpgd_internal.h"
 #include <cfloat>
@@ -50,8 +51,12 @@ namespace {
 #define UFPGD_TWO_SWEEP 1
 #endif
 
-template <int K_, int M_, int TK_, int TM_, int MAXT_ = 256, int MINB_ = 1>
+template <int K_, int M_, int TK_, int TM_, int MAXT_ = 256, int MINB_ = 1, bool WSMEM_ = false,
+          bool TWO_SWEEP_ = UFPGD_TWO_SWEEP>
 struct Team {
+  // WSMEM: W lives in shared memory (one 16-byte unit per thread and antenna)
+  // instead of registers; TWO_SWEEP: see UFPGD_TWO_SWEEP.
+  static constexpr bool WSMEM = WSMEM_, TWO_SWEEP = TWO_SWEEP_;
   static constexpr int K = K_, M = M_, TK = TK_, TM = TM_;
   // launch bounds: register cap = 64K / (MAXT * MINB)
   static constexpr int MAXT = MAXT_, MINB = MINB_;
@@ -62,7 +67,8 @@ struct Team {
   static constexpr int MB = M / TM;     // antennas per thread
   static constexpr int HS = 2 * K;      // H row stride in floats (XOR-swizzled units, no padding)
   static constexpr int U = K / 2;       // 16-byte units per H row
-  static constexpr int SMEM_PER_WARP = R * M * HS * 4;
+  static constexpr int SMEM_PER_WARP = R * M * HS * 4;          // H tiles
+  static constexpr int WSMEM_PER_WARP = WSMEM ? R * M * TK * P * 16 : 0;  // W tiles (bytes)
   // Unit swizzle of row m: with U >= 4 units per row, rows m and m + 2 of a
   // quarter-warp LDS.128 phase would hit the same banks; XOR-ing the unit
   // index with (m >> 1) mod U separates them. U <= 2 is conflict-free as is.
@@ -119,6 +125,41 @@ struct XAcc {
   float2 re[S::P][S::K], im[S::P][S::K];
 };
 
+// W(a*KA + 2p + {0,1}, i*TM + b) split into real / imaginary user pairs, in
+// registers (WReg) or in a shared-memory tile (WSm).
+template <class S>
+struct WReg {
+  float2 r[S::MB][S::P], im[S::MB][S::P];
+  __device__ __forceinline__ void ld(int i, int p, float2& wr, float2& wi) const {
+    wr = r[i][p];
+    wi = im[i][p];
+  }
+  __device__ __forceinline__ void st(int i, int p, float2 wr, float2 wi) {
+    r[i][p] = wr;
+    im[i][p] = wi;
+  }
+};
+
+// Shared-memory W tile: row m holds the TK user-pair units (re pair, im pair)
+// of antenna m; unit a is XOR-ed with ((m >> 1) & 1) << 1 so the 8 lanes of a
+// quarter-warp LDS.128 / STS.128 phase (a in {0,1}, b in 0..3) hit 8 distinct
+// units. With TM = 4 the swizzle depends on b only: one base pointer per thread.
+template <class S>
+struct WSm {
+  static_assert(S::P == 1 && S::TK == 4 && S::TM == 4, "WSm covers the (TK, TM) = (4, 4), one-pair team");
+  float* base;
+  __device__ __forceinline__ WSm(float* tile, int a, int b)
+      : base(tile + b * S::TK * 4 + 4 * (a ^ (((b >> 1) & 1) << 1))) {}
+  __device__ __forceinline__ void ld(int i, int p, float2& wr, float2& wi) const {
+    const float4 t = *reinterpret_cast<const float4*>(base + i * S::TM * S::TK * 4);
+    wr = make_float2(t.x, t.y);
+    wi = make_float2(t.z, t.w);
+  }
+  __device__ __forceinline__ void st(int i, int p, float2 wr, float2 wi) {
+    *reinterpret_cast<float4*>(base + i * S::TM * S::TK * 4) = make_float4(wr.x, wr.y, wi.x, wi.y);
+  }
+};
+
 // Stage 1 contribution of antenna m: X'(k, j) += W(k, m) H(j, m).
 template <class S>
 __device__ __forceinline__ void stage1_accumulate(XAcc<S>& xn, const float2 (&wr)[S::P],
@@ -173,9 +214,8 @@ __device__ __forceinline__ void xacc_init(XAcc<S>& x, const float2 (&cdiag)[S::P
     }
 }
 
-template <class S, bool FRESH = false>
-__device__ __forceinline__ void team_stage1(const float2 (&wr)[S::MB][S::P], const float2 (&wi)[S::MB][S::P],
-                                            XAcc<S>& x, const float* hs, int a, int b,
+template <class S, bool FRESH = false, class WS>
+__device__ __forceinline__ void team_stage1(const WS& w, XAcc<S>& x, const float* hs, int a, int b,
                                             const float2 (&cdiag)[S::P]) {
   XAcc<S> xn;
   xacc_init<S>(xn, cdiag, a);
@@ -184,7 +224,10 @@ __device__ __forceinline__ void team_stage1(const float2 (&wr)[S::MB][S::P], con
   for (int i = 0; i < S::MB; ++i) {
     float2 h[S::K];
     load_col<S, FRESH>(cp, i, h);
-    stage1_accumulate<S>(xn, wr[i], wi[i], h);
+    float2 wr[S::P], wi[S::P];
+#pragma unroll
+    for (int p = 0; p < S::P; ++p) w.ld(i, p, wr[p], wi[p]);
+    stage1_accumulate<S>(xn, wr, wi, h);
   }
   allreduce<S>(xn, x);
 }
@@ -198,8 +241,8 @@ __device__ __forceinline__ void team_stage1(const float2 (&wr)[S::MB][S::P], con
 // at W (no merge adds) — measured fastest at 3 warps per scheduler, against
 // 2- and 4-chain splits.
 
-template <class S, bool STAGE1, bool STATS>
-__device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&wi)[S::MB][S::P], XAcc<S>& x,
+template <class S, bool STAGE1, bool STATS, class WS>
+__device__ __forceinline__ void team_layer(WS& w, XAcc<S>& x,
                                            const float* hs, int a, int b, float eta, float thr,
                                            const float2 (&cdiag)[S::P], bool& nonfinite, float& l21,
                                            int& act) {
@@ -231,7 +274,8 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
       float2 s2 = zero2();
 #pragma unroll
       for (int p = 0; p < S::P; ++p) {
-        float2 gr = wr[i][p], gi = wi[i][p];
+        float2 gr, gi;
+        w.ld(i, p, gr, gi);
 #pragma unroll
         for (int j = 0; j < S::K; ++j) {
           gr = ffma2(h[u][j].x, x.re[p][j], gr);
@@ -264,10 +308,12 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
       const bool on = s[u] > thr2;
       const float r = rsqrt_ftz(fmaxf(s[u], FLT_MIN));  // s = 0 or subnormal only matters at thr = 0
       const float scale = on ? fmaf(-thr, r, 1.f) : 0.f;
+      float2 nwr[S::P], nwi[S::P];
 #pragma unroll
       for (int p = 0; p < S::P; ++p) {
-        wr[i][p] = fmul2(scale, vr[u][p]);
-        wi[i][p] = fmul2(scale, vi[u][p]);
+        nwr[p] = fmul2(scale, vr[u][p]);
+        nwi[p] = fmul2(scale, vi[u][p]);
+        w.st(i, p, nwr[p], nwi[p]);
       }
       if (STATS) {
         if (a == 0 && on) {
@@ -275,7 +321,7 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
           act += 1;
         }
       }
-      if (STAGE1) stage1_accumulate<S>(xn, wr[i], wi[i], h[u]);
+      if (STAGE1) stage1_accumulate<S>(xn, nwr, nwi, h[u]);
     }
   }
   if (STAGE1) allreduce<S>(xn, x);
@@ -286,9 +332,8 @@ __device__ __forceinline__ void team_layer(float2 (&wr)[S::MB][S::P], float2 (&w
 // a diagonal matrix reduces to two FMUL2 per antenna on the thread's own rows
 // (bit-identical to running the contraction on the exact zeros). ceta holds
 // (eta c_k0, eta c_k0+1) per user pair.
-template <class S, bool STATS>
-__device__ __forceinline__ void team_layer0_diag(float2 (&wr)[S::MB][S::P], float2 (&wi)[S::MB][S::P],
-                                                 const float* hs, int a, int b, float thr,
+template <class S, bool STATS, class WS>
+__device__ __forceinline__ void team_layer0_diag(WS& w, const float* hs, int a, int b, float thr,
                                                  const float2 (&ceta)[S::P], bool& nonfinite, float& l21,
                                                  int& act) {
   const float thr2 = thr * thr;
@@ -323,10 +368,7 @@ __device__ __forceinline__ void team_layer0_diag(float2 (&wr)[S::MB][S::P], floa
       const float r = rsqrt_ftz(fmaxf(sv[u], FLT_MIN));
       const float scale = on ? fmaf(-thr, r, 1.f) : 0.f;
 #pragma unroll
-      for (int p = 0; p < S::P; ++p) {
-        wr[i][p] = fmul2(scale, vr[u][p]);
-        wi[i][p] = fmul2(scale, vi[u][p]);
-      }
+      for (int p = 0; p < S::P; ++p) w.st(i, p, fmul2(scale, vr[u][p]), fmul2(scale, vi[u][p]));
       if (STATS && a == 0 && on) {
         l21 += fmaf(sv[u], r, -thr);
         act += 1;
@@ -402,6 +444,19 @@ __device__ float team_power(const float* hs, const float2* v0, int steps, int a,
   return est;
 }
 
+// W storage of the thread: registers, or its units of the team's W tile (W
+// tiles follow all the warps' H tiles in dynamic shared memory).
+template <class S>
+__device__ __forceinline__ typename std::conditional<S::WSMEM, WSm<S>, WReg<S>>::type make_wstore(
+    float* smem, int warp, int team, int nwarps, int a, int b) {
+  if constexpr (S::WSMEM) {
+    float* tiles = smem + nwarps * (S::SMEM_PER_WARP / 4);
+    return WSm<S>(tiles + (warp * S::R + team) * (S::M * S::TK * S::P * 4), a, b);
+  } else {
+    return WReg<S>{};
+  }
+}
+
 template <class S, bool PGD, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant__ FusedArgs p) {
   extern __shared__ __align__(16) float smem[];
@@ -429,7 +484,8 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
   }
 
   // W(a*KA + 2p + {0,1}, i*TM + b), split into real / imaginary user pairs.
-  float2 wr[S::MB][S::P], wi[S::MB][S::P];
+  using WS = typename std::conditional<S::WSMEM, WSm<S>, WReg<S>>::type;
+  WS w = make_wstore<S>(smem, warp, team, nwarps, a, b);
   XAcc<S> x;
   float2 cdiag[S::P];
 #pragma unroll
@@ -441,10 +497,7 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
 #pragma unroll
     for (int i = 0; i < S::MB; ++i)
 #pragma unroll
-      for (int q = 0; q < S::P; ++q) {
-        wr[i][q] = zero2();
-        wi[i][q] = zero2();
-      }
+      for (int q = 0; q < S::P; ++q) w.st(i, q, zero2(), zero2());
     // X' = 0 H^T - diag(c): the layer-0 product is identically zero.
 #pragma unroll
     for (int q = 0; q < S::P; ++q)
@@ -461,8 +514,7 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
 #pragma unroll
         for (int q = 0; q < S::P; ++q) {
           const float4 t = *reinterpret_cast<const float4*>(S::hat(hs, i * S::TM + b, a * S::KA + 2 * q));
-          wr[i][q] = make_float2(t.x, t.z);
-          wi[i][q] = make_float2(-t.y, -t.w);
+          w.st(i, q, make_float2(t.x, t.z), make_float2(-t.y, -t.w));
         }
       }
     } else {
@@ -474,11 +526,10 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
           const float4 t = valid ? ldg_stream(reinterpret_cast<const float4*>(
                                        w0 + (i * S::TM + b) * S::K + a * S::KA + 2 * q))
                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-          wr[i][q] = make_float2(t.x, t.z);
-          wi[i][q] = make_float2(t.y, t.w);
+          w.st(i, q, make_float2(t.x, t.z), make_float2(t.y, t.w));
         }
     }
-    team_stage1<S>(wr, wi, x, hs, a, b, cdiag);
+    team_stage1<S>(w, x, hs, a, b, cdiag);
   }
 
   float eta_b = 0.f, thr_b = 0.f;
@@ -508,10 +559,10 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
       ceta[q] = make_float2(p.eta[0] * p.c[k0], p.eta[0] * p.c[k0 + 1]);
     }
     if (L == 1) {
-      team_layer0_diag<S, true>(wr, wi, hs, a, b, p.thr[0], ceta, nonfinite, l21, act);
+      team_layer0_diag<S, true>(w, hs, a, b, p.thr[0], ceta, nonfinite, l21, act);
     } else {
-      team_layer0_diag<S, false>(wr, wi, hs, a, b, p.thr[0], ceta, nonfinite, l21, act);
-      team_stage1<S, true>(wr, wi, x, hs, a, b, cdiag);  // X' for layer 1
+      team_layer0_diag<S, false>(w, hs, a, b, p.thr[0], ceta, nonfinite, l21, act);
+      team_stage1<S, true>(w, x, hs, a, b, cdiag);  // X' for layer 1
     }
     if (nonfinite) first_bad = 0;
     l0 = 1;
@@ -519,19 +570,19 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
   for (long long l = l0; l + 1 < L; ++l) {
     const float eta = PGD ? eta_b : p.eta[l];
     const float thr = PGD ? thr_b : p.thr[l];
-#if UFPGD_TWO_SWEEP
-    team_layer<S, false, false>(wr, wi, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
-    __syncwarp();  // scheduling fence: the next X' is built only after every prox
-    team_stage1<S, true>(wr, wi, x, hs, a, b, cdiag);
-#else
-    team_layer<S, true, false>(wr, wi, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
-#endif
+    if constexpr (S::TWO_SWEEP) {
+      team_layer<S, false, false>(w, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
+      __syncwarp();  // scheduling fence: the next X' is built only after every prox
+      team_stage1<S, true>(w, x, hs, a, b, cdiag);
+    } else {
+      team_layer<S, true, false>(w, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
+    }
     if (nonfinite && first_bad < 0) first_bad = l;
   }
   if (L >= 1 && L > l0) {
     const float eta = PGD ? eta_b : p.eta[L - 1];
     const float thr = PGD ? thr_b : p.thr[L - 1];
-    team_layer<S, false, true>(wr, wi, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
+    team_layer<S, false, true>(w, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
     if (nonfinite && first_bad < 0) first_bad = L - 1;
   }
 
@@ -552,8 +603,12 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
     for (int i = 0; i < S::MB; ++i)
 #pragma unroll
       for (int q = 0; q < S::P; ++q)
+      {
+        float2 wr, wi;
+        w.ld(i, q, wr, wi);
         stg_stream(reinterpret_cast<float4*>(wg + (i * S::TM + b) * S::K + a * S::KA + 2 * q),
-                   make_float4(wr[i][q].x, wi[i][q].x, wr[i][q].y, wi[i][q].y));
+                   make_float4(wr.x, wi.x, wr.y, wi.y));
+      }
     if (tl == 0) {
       if (p.diverged_at) p.diverged_at[rid] = diverged ? static_cast<int32_t>(fb + (PGD ? 1 : 0)) : -1;
       if (p.l21) p.l21[rid] = diverged ? __int_as_float(0x7fc00000) : l21;
@@ -619,7 +674,7 @@ cudaError_t launch_team(const FusedArgs& a, bool pgd, cudaStream_t s, long long*
   auto kern = pgd ? fused_kernel<S, true, 256, 1> : fused_kernel<S, false, S::MAXT, S::MINB>;
   const int maxt = pgd ? 256 : S::MAXT;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kFusedMaxWarps * S::SMEM_PER_WARP);
+                                       kFusedMaxWarps * (S::SMEM_PER_WARP + S::WSMEM_PER_WARP));
   if (e != cudaSuccess) return e;
   int nw = pick_warps(S::R, a.B);
   if (const char* f = std::getenv("UFPGD_FUSED_WARPS")) nw = std::max(1, std::min(8, std::atoi(f)));
@@ -627,7 +682,7 @@ cudaError_t launch_team(const FusedArgs& a, bool pgd, cudaStream_t s, long long*
   const long long rpb = static_cast<long long>(nw) * S::R;
   const long long blocks = (a.B + rpb - 1) / rpb;
   if (nblocks) *nblocks = blocks;
-  kern<<<static_cast<unsigned>(blocks), nw * 32, nw * S::SMEM_PER_WARP, s>>>(a);
+  kern<<<static_cast<unsigned>(blocks), nw * 32, nw * (S::SMEM_PER_WARP + S::WSMEM_PER_WARP), s>>>(a);
   return cudaGetLastError();
 }
 
@@ -648,7 +703,11 @@ using Team_4_32 = Team<4, 32, 2, UFPGD_T432_TM>;
 #ifndef UFPGD_T864_TK
 #define UFPGD_T864_TK 4
 #endif
-using Team_8_64 = Team<8, 64, UFPGD_T864_TK, 16 / UFPGD_T864_TK, UFPGD_T864_MAXT, UFPGD_T864_MINB>;
+#ifndef UFPGD_T864_WSMEM
+#define UFPGD_T864_WSMEM 0
+#endif
+using Team_8_64 = Team<8, 64, UFPGD_T864_TK, 16 / UFPGD_T864_TK, UFPGD_T864_MAXT, UFPGD_T864_MINB, UFPGD_T864_WSMEM,
+                       UFPGD_T864_WSMEM ? false : UFPGD_TWO_SWEEP>;
 // Neighbouring shapes of the BASELINE ones (the paper sweeps users and
 // antennas around K = 8, M = 64) get the same fused kernel instead of the
 // general one: 2 users x M/TM antennas per thread.
