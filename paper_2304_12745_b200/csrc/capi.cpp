@@ -300,6 +300,10 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
                              : nullptr;
   int rc = UFPGD_OK;
   std::vector<long long> part_off(nchunks + 1, 0);
+  // UFPGD_HOST_TIMELINE=1: per-chunk event timeline on stderr (tuning aid)
+  const bool timeline = std::getenv("UFPGD_HOST_TIMELINE") != nullptr;
+  std::vector<cudaEvent_t> tev(timeline ? 4 * nchunks : 0);
+  for (cudaEvent_t& ev : tev) cudaEventCreate(&ev);
   for (int64_t ci = 0; ci < nchunks && rc == UFPGD_OK; ++ci) {
     const int i = static_cast<int>(ci % NS);
     const int64_t b0 = ci * chunk, nb = std::min<int64_t>(chunk, B - b0);
@@ -309,8 +313,10 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
     float2* dw0 = static_cast<float2*>(ws.buf[i][2]);
     int32_t* ddiv = static_cast<int32_t*>(ws.buf[i][3]);
     float* deta = static_cast<float*>(ws.buf[i][4]);
+    if (timeline) cudaEventRecord(tev[4 * ci], s);
     e = cudaMemcpyAsync(dh, H + b0 * K * M, per * nb, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && W0) e = cudaMemcpyAsync(dw0, W0 + b0 * K * M, per * nb, cudaMemcpyHostToDevice, s);
+    if (timeline) cudaEventRecord(tev[4 * ci + 1], s);
     if (e != cudaSuccess) {
       rc = cuda_fail(e, "H2D");
       break;
@@ -319,12 +325,24 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
     rc = run(dh, nb, W0 ? dw0 : nullptr, dw, ddiv, eta_out ? deta : nullptr, ws.partials + 3 * part_off[ci], &np, s);
     if (rc != UFPGD_OK) break;
     part_off[ci + 1] = part_off[ci] + np;
+    if (timeline) cudaEventRecord(tev[4 * ci + 2], s);
     e = cudaMemcpyAsync(W + b0 * K * M, dw, per * nb, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && diverged_at)
       e = cudaMemcpyAsync(div_stage + b0, ddiv, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && eta_out)
       e = cudaMemcpyAsync(eta_stage + b0, deta, sizeof(float) * nb, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) rc = cuda_fail(e, "D2H");
+    if (timeline) cudaEventRecord(tev[4 * ci + 3], s);
+  }
+  if (timeline) {
+    for (int i = 0; i < NS; ++i) cudaStreamSynchronize(ws.st[i]);
+    for (int64_t ci = 0; ci < nchunks; ++ci) {
+      float t[4];
+      for (int q = 0; q < 4; ++q) cudaEventElapsedTime(&t[q], tev[0], tev[4 * ci + q]);
+      std::fprintf(stderr, "chunk %3lld  h2d %7.3f-%7.3f  kernel -%7.3f  d2h -%7.3f ms\n", static_cast<long long>(ci),
+                   t[0], t[1], t[2], t[3]);
+    }
+    for (cudaEvent_t ev : tev) cudaEventDestroy(ev);
   }
   double host_stats[3] = {0.0, 0.0, 0.0};
   if (rc == UFPGD_OK) {
