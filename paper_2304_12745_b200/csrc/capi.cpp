@@ -205,6 +205,10 @@ struct HostWorkspace {
   bool init = false;
   static constexpr int NS = 4;
   cudaStream_t st[NS] = {};
+  // phased pipeline: copy-in, two kernel and copy-out streams, chained per
+  // buffer set by events
+  cudaStream_t sx[4] = {};
+  cudaEvent_t ev[NS][3] = {};
   void* buf[NS][5] = {};
   size_t cap[NS][5] = {};
   double* partials = nullptr;
@@ -247,6 +251,17 @@ void release_workspace(HostWorkspace& ws) {
     }
     cudaStreamDestroy(ws.st[i]);
     ws.st[i] = nullptr;
+    for (int q = 0; q < 3; ++q) {
+      if (ws.ev[i][q]) cudaEventDestroy(ws.ev[i][q]);
+      ws.ev[i][q] = nullptr;
+    }
+  }
+  for (cudaStream_t& x : ws.sx) {
+    if (x) {
+      cudaStreamSynchronize(x);
+      cudaStreamDestroy(x);
+    }
+    x = nullptr;
   }
   if (ws.partials) cudaFree(ws.partials);
   if (ws.dstats) cudaFree(ws.dstats);
@@ -270,11 +285,19 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
   constexpr int NS = HostWorkspace::NS;
   if (!ws.init) {
     for (int i = 0; i < NS; ++i) UFPGD_CUDA(cudaStreamCreateWithFlags(&ws.st[i], cudaStreamNonBlocking));
+    for (cudaStream_t& x : ws.sx) UFPGD_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    for (int i = 0; i < NS; ++i)
+      for (int q = 0; q < 3; ++q) UFPGD_CUDA(cudaEventCreateWithFlags(&ws.ev[i][q], cudaEventDisableTiming));
     UFPGD_CUDA(cudaMalloc(&ws.dstats, sizeof(double) * 3));
     ws.init = true;
   }
   const size_t per = static_cast<size_t>(K) * M * sizeof(float2);
-  const int64_t nchunks = B == 0 ? 0 : (B + chunk - 1) / chunk;
+  // Chunk boundaries (a geometric ramp of the first / last chunks was measured
+  // and is no faster with the phased pipeline: the copy-out stream paces it).
+  std::vector<int64_t> cs{0};
+  for (int64_t b = chunk; b < B; b += chunk) cs.push_back(b);
+  if (B > 0) cs.push_back(B);
+  const int64_t nchunks = static_cast<int64_t>(cs.size()) - 1;
   const size_t need[5] = {per * chunk, per * chunk, W0 ? per * chunk : 0, sizeof(int32_t) * chunk,
                           eta_out ? sizeof(float) * chunk : 0};
   cudaError_t e = cudaSuccess;
@@ -300,13 +323,83 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
                              : nullptr;
   int rc = UFPGD_OK;
   std::vector<long long> part_off(nchunks + 1, 0);
+  // Default pipeline ("phased"): one copy-in stream, two kernel streams, one
+  // copy-out stream, chained per buffer set by events. The copy-out of chunk
+  // k also waits for the copy-in of chunk k + 1, so every D2H starts together
+  // with an H2D: PCIe then splits evenly between the directions (~48 GB/s
+  // each), whereas a D2H started mid-way through an H2D takes the larger share
+  // and slows the H2D stream that paces the pipeline (tools/pipe_probe2.py:
+  // 88.8 vs 81.9 GB/s total). UFPGD_HOST_PIPE=streams selects the earlier
+  // depth-first pipeline over four streams, for A/B runs.
+  const char* pipe_env = std::getenv("UFPGD_HOST_PIPE");
+  const bool phased = !(pipe_env && std::strcmp(pipe_env, "streams") == 0);
   // UFPGD_HOST_TIMELINE=1: per-chunk event timeline on stderr (tuning aid)
   const bool timeline = std::getenv("UFPGD_HOST_TIMELINE") != nullptr;
   std::vector<cudaEvent_t> tev(timeline ? 4 * nchunks : 0);
   for (cudaEvent_t& ev : tev) cudaEventCreate(&ev);
-  for (int64_t ci = 0; ci < nchunks && rc == UFPGD_OK; ++ci) {
+  // Buffer set i = chunk % NS; events: 0 = copy-in done, 1 = kernel done,
+  // 2 = copy-out done. Copy-in of chunk k reuses the H buffer of chunk k - NS
+  // (waits for its kernel); the kernel reuses its W buffer (waits for its
+  // copy-out).
+  cudaStream_t sin = ws.sx[0], sout = ws.sx[3];
+  auto copy_out = [&](int64_t cj) -> int {
+    const int j = static_cast<int>(cj % NS);
+    const int64_t b0 = cs[cj], nb = cs[cj + 1] - b0;
+    cudaStreamWaitEvent(sout, ws.ev[j][1], 0);
+    if (cj + 1 < nchunks) cudaStreamWaitEvent(sout, ws.ev[(cj + 1) % NS][0], 0);
+    cudaError_t x = cudaMemcpyAsync(W + b0 * K * M, ws.buf[j][1], per * nb, cudaMemcpyDeviceToHost, sout);
+    if (x == cudaSuccess && diverged_at)
+      x = cudaMemcpyAsync(div_stage + b0, ws.buf[j][3], sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, sout);
+    if (x == cudaSuccess && eta_out)
+      x = cudaMemcpyAsync(eta_stage + b0, ws.buf[j][4], sizeof(float) * nb, cudaMemcpyDeviceToHost, sout);
+    if (x != cudaSuccess) return cuda_fail(x, "D2H");
+    if (timeline) cudaEventRecord(tev[4 * cj + 3], sout);
+    cudaEventRecord(ws.ev[j][2], sout);
+    return UFPGD_OK;
+  };
+  for (int64_t ci = 0; ci < nchunks && rc == UFPGD_OK && phased; ++ci) {
     const int i = static_cast<int>(ci % NS);
-    const int64_t b0 = ci * chunk, nb = std::min<int64_t>(chunk, B - b0);
+    const int64_t b0 = cs[ci], nb = cs[ci + 1] - b0;
+    cudaStream_t sk = ws.sx[1 + (ci & 1)];
+    float2* dh = static_cast<float2*>(ws.buf[i][0]);
+    float2* dw = static_cast<float2*>(ws.buf[i][1]);
+    float2* dw0 = static_cast<float2*>(ws.buf[i][2]);
+    int32_t* ddiv = static_cast<int32_t*>(ws.buf[i][3]);
+    float* deta = static_cast<float*>(ws.buf[i][4]);
+    if (ci >= NS) cudaStreamWaitEvent(sin, ws.ev[i][1], 0);
+    if (timeline) cudaEventRecord(tev[4 * ci], sin);
+    e = cudaMemcpyAsync(dh, H + b0 * K * M, per * nb, cudaMemcpyHostToDevice, sin);
+    if (e == cudaSuccess && W0) e = cudaMemcpyAsync(dw0, W0 + b0 * K * M, per * nb, cudaMemcpyHostToDevice, sin);
+    if (e != cudaSuccess) {
+      rc = cuda_fail(e, "H2D");
+      break;
+    }
+    cudaEventRecord(ws.ev[i][0], sin);
+    if (timeline) cudaEventRecord(tev[4 * ci + 1], sin);
+    cudaStreamWaitEvent(sk, ws.ev[i][0], 0);
+    if (ci >= NS) cudaStreamWaitEvent(sk, ws.ev[i][2], 0);
+    long long np = 0;
+    rc = run(dh, nb, W0 ? dw0 : nullptr, dw, ddiv, eta_out ? deta : nullptr, ws.partials + 3 * part_off[ci], &np, sk);
+    if (rc != UFPGD_OK) break;
+    part_off[ci + 1] = part_off[ci] + np;
+    cudaEventRecord(ws.ev[i][1], sk);
+    if (timeline) cudaEventRecord(tev[4 * ci + 2], sk);
+    if (ci >= 1) rc = copy_out(ci - 1);
+  }
+  if (phased && rc == UFPGD_OK && nchunks > 0) rc = copy_out(nchunks - 1);
+  if (phased) {
+    // join the pipeline streams into st[1..NS-1] so the common tail below sees them
+    for (int x = 0; x < 4; ++x) {
+      cudaEvent_t j;
+      cudaEventCreateWithFlags(&j, cudaEventDisableTiming);
+      cudaEventRecord(j, ws.sx[x]);
+      cudaStreamWaitEvent(ws.st[1 + x % (NS - 1)], j, 0);
+      cudaEventDestroy(j);
+    }
+  }
+  for (int64_t ci = 0; ci < nchunks && rc == UFPGD_OK && !phased; ++ci) {
+    const int i = static_cast<int>(ci % NS);
+    const int64_t b0 = cs[ci], nb = cs[ci + 1] - b0;
     cudaStream_t s = ws.st[i];
     float2* dh = static_cast<float2*>(ws.buf[i][0]);
     float2* dw = static_cast<float2*>(ws.buf[i][1]);
@@ -360,6 +453,7 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
     if (e != cudaSuccess) rc = cuda_fail(e, "host pipeline finalize");
   }
   for (int i = 0; i < NS; ++i) cudaStreamSynchronize(ws.st[i]);
+  for (cudaStream_t x : ws.sx) cudaStreamSynchronize(x);
   if (rc != UFPGD_OK) return rc;
   if (diverged_at) std::memcpy(diverged_at, div_stage, sizeof(int32_t) * B);
   if (eta_out) std::memcpy(eta_out, eta_stage, sizeof(float) * B);
