@@ -85,6 +85,11 @@ int ufpgd_gpu_device_count(int* count);
  *   active[B]         #{m : ||w_m||^2 > 0} (pgd.cpp:23-29), -1 when diverged
  *   stats[3] (double) {sum_b alpha*||W_b||_{2,1}, sum_b active_b, #diverged},
  *                     sums over non-diverged realizations, deterministic order.
+ *
+ * Kernels: the fused kernels for (4,16), (4,32), (4,64), (8,32), (8,64),
+ * (8,128), (16,128), (32,256); any other (K, M) within 6x the flops of one of
+ * them runs zero-padded on it (padded users / antennas stay exactly zero);
+ * the rest run the general CTA-per-realization kernel.
  */
 int ufpgd_gpu_unfolded_forward(const ufpgd_c64* H, int64_t B, int K, int M,
                                const double* lambda, const double* eta, int L,
@@ -215,7 +220,8 @@ int ufpgd_gpu_pgd_fixed_host(const ufpgd_c64* H, int64_t B, int K, int M, int po
  * summary statistics with one ncclAllReduce over an NCCL communicator built by
  * ufpgd_gpu_init (ncclCommInitAll). Host buffers, synchronous.
  * ufpgd_gpu_shutdown destroys the communicators and releases the per-device
- * workspaces of the host-buffer entry points (they are re-created on demand).
+ * workspaces of the host-buffer entry points and the scratch pool of the
+ * zero-padded forward (they are re-created on demand).
  */
 int ufpgd_gpu_init(int ngpus);
 int ufpgd_gpu_shutdown(void);

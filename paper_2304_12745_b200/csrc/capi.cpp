@@ -83,6 +83,69 @@ int finish_stats(double* partials, long long n, double* stats, cudaStream_t s) {
   return UFPGD_OK;
 }
 
+// Fused-kernel shape a (K, M) batch can be zero-padded to: the cheapest
+// supported (Kp >= K, Mp >= M) within 6x the flops (the fused kernels run
+// 7-8x the general kernel's rate). Padded users (H row 0, c = 0) and antennas
+// (H column 0) keep W exactly 0 through every layer and add exact zeros to
+// every contraction and norm, so the cropped result is the (K, M) solve.
+// Library-private stream-ordered pool for the padded path's scratch: keeps
+// its memory across calls (release threshold unbounded) without changing the
+// device's default pool that other code in the process may rely on.
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[64] = {};
+
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  {
+    std::lock_guard<std::mutex> lock(g_pool_mu);
+    if (!g_pool[dev]) {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      e = cudaMemPoolCreate(&g_pool[dev], &props);
+      if (e != cudaSuccess) return e;
+      unsigned long long keep = ~0ULL;
+      cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
+  return cudaMallocFromPoolAsync(p, bytes, g_pool[dev], s);
+}
+
+void release_pool(int dev) {
+  std::lock_guard<std::mutex> lock(g_pool_mu);
+  if (g_pool[dev]) {
+    cudaDeviceSynchronize();
+    cudaMemPoolDestroy(g_pool[dev]);
+    g_pool[dev] = nullptr;
+  }
+}
+
+long long pad_sub_bytes() {
+  const char* v = std::getenv("UFPGD_PAD_SUB_MB");  // tests: force several sub-batches
+  return (v ? std::max(1LL, std::atoll(v)) : 1024LL) << 20;
+}
+
+bool padded_shape(int K, int M, int* Kp, int* Mp) {
+  if (std::getenv("UFPGD_NO_PAD")) return false;
+  static const int shapes[][2] = {{4, 16}, {4, 32}, {4, 64}, {8, 32}, {8, 64}, {8, 128}, {16, 128}, {32, 256}};
+  double best = 6.0 * K * K * M;
+  bool found = false;
+  for (const auto& sh : shapes) {
+    const double cost = static_cast<double>(sh[0]) * sh[0] * sh[1];
+    if (sh[0] >= K && sh[1] >= M && cost <= best && fused_supported(sh[0], sh[1])) {
+      best = cost;
+      *Kp = sh[0];
+      *Mp = sh[1];
+      found = true;
+    }
+  }
+  return found;
+}
+
 // Enqueues an unfolded forward on `s` (device buffers). Used by the public
 // device API and by the chunked host path.
 int enqueue_unfolded(const float2* H, int64_t B, int K, int M, const double* lambda,
@@ -110,6 +173,39 @@ int enqueue_unfolded(const float2* H, int64_t B, int K, int M, const double* lam
     }
     cudaError_t e = launch_fused(a, false, K, M, s, nparts);
     if (e != cudaSuccess) return cuda_fail(e, "fused unfolded kernel");
+    return UFPGD_OK;
+  }
+  int Kp = 0, Mp = 0;
+  if (L >= 1 && padded_shape(K, M, &Kp, &Mp)) {
+    // sub-batches of <= 1 GiB of padded H bound the scratch
+    const int64_t sub = std::max<int64_t>(1, std::min<int64_t>(B, pad_sub_bytes() / (8ll * Kp * Mp)));
+    const size_t bytes = static_cast<size_t>(sub) * Kp * Mp * sizeof(float2);
+    float2 *hp = nullptr, *wp = nullptr, *w0p = nullptr;
+    cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&hp), bytes, s);
+    if (e == cudaSuccess) e = scratch_alloc(reinterpret_cast<void**>(&wp), bytes, s);
+    if (e == cudaSuccess && w0_mode == UFPGD_W0_GIVEN) e = scratch_alloc(reinterpret_cast<void**>(&w0p), bytes, s);
+    double cp[UFPGD_MAX_USERS] = {};
+    for (int k = 0; k < K; ++k) cp[k] = c[k];
+    int rc = UFPGD_OK;
+    long long parts = 0;
+    for (int64_t b0 = 0; b0 < B && e == cudaSuccess && rc == UFPGD_OK; b0 += sub) {
+      const int64_t nb = std::min<int64_t>(sub, B - b0);
+      e = launch_repack_c64(H + b0 * K * M, M, K, hp, Mp, Kp, nb, s);
+      if (e == cudaSuccess && w0p) e = launch_repack_c64(W0 + b0 * K * M, M, K, w0p, Mp, Kp, nb, s);
+      if (e != cudaSuccess) break;
+      long long np = 0;
+      rc = enqueue_unfolded(hp, nb, Kp, Mp, lambda, eta, L, cp, w0_mode, w0p, wp, diverged_at ? diverged_at + b0 : nullptr,
+                            l21 ? l21 + b0 : nullptr, active ? active + b0 : nullptr,
+                            partials ? partials + 3 * parts : nullptr, alpha, s, &np);
+      parts += np;
+      if (rc == UFPGD_OK) e = launch_repack_c64(wp, Mp, Kp, W + b0 * K * M, M, K, nb, s);
+    }
+    *nparts = parts;
+    if (hp) cudaFreeAsync(hp, s);
+    if (wp) cudaFreeAsync(wp, s);
+    if (w0p) cudaFreeAsync(w0p, s);
+    if (rc != UFPGD_OK) return rc;
+    if (e != cudaSuccess) return cuda_fail(e, "zero-padded fused forward");
     return UFPGD_OK;
   }
   if (!general_fits(K, M)) return fail(UFPGD_ENOTSUP, "(K, M) too large for the general kernel");
@@ -1103,9 +1199,10 @@ int ufpgd_gpu_shutdown(void) {
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess) count = 0;
   for (int d = 0; d < count && d < 64; ++d) {
-    if (!g_ws[d].init) continue;
+    if (!g_ws[d].init && !g_pool[d]) continue;
     DeviceGuard g(d);
     release_workspace(g_ws[d]);
+    release_pool(d);
   }
   return UFPGD_OK;
 }

@@ -195,7 +195,36 @@ __global__ void __launch_bounds__(256) c64_to_f64_rowmajor_kernel(const float2* 
   }
 }
 
+// Zero-padding repack between [B][Ms][Ks] and [B][Md][Kd] complex64 batches:
+// dst(b, m, k) = src(b, m, k) inside the source shape, 0 outside. Pads a
+// batch up to a fused-kernel shape and crops the result back. Blocks stride
+// over realizations, threads over a realization's destination elements
+// (coalesced stores, 32-bit index arithmetic).
+__global__ void __launch_bounds__(256) repack_c64_kernel(const float2* __restrict__ src, float2* __restrict__ dst,
+                                                         long long B, int Ms, int Ks, int Md, int Kd) {
+  const int per = Md * Kd;
+  for (long long b = blockIdx.x; b < B; b += gridDim.x) {
+    const float2* sb = src + b * Ms * Ks;
+    float2* db = dst + b * per;
+    for (int r = threadIdx.x; r < per; r += 256) {
+      const int m = r / Kd, k = r - m * Kd;
+      db[r] = (m < Ms && k < Ks) ? sb[m * Ks + k] : make_float2(0.f, 0.f);
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_repack_c64(const float2* src, int Ms, int Ks, float2* dst, int Md, int Kd, long long B,
+                              cudaStream_t s) {
+  if (B == 0) return cudaSuccess;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = static_cast<unsigned>(B < 16LL * sms ? B : 16LL * sms);
+  repack_c64_kernel<<<grid, 256, 0, s>>>(src, dst, B, Ms, Ks, Md, Kd);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_channel_gen(unsigned long long seed_h, unsigned long long seed_g, double gain_range_db,
                                long long first_index, long long B, int K, int M, void* H, bool f64, cudaStream_t s) {

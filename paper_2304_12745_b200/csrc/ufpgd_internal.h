@@ -145,6 +145,8 @@ cudaError_t launch_grad64(const GradArgs64& a, double* mean, cudaStream_t s);
 cudaError_t launch_channel_gen(unsigned long long seed_h, unsigned long long seed_g, double gain_range_db,
                                long long first_index, long long B, int K, int M, void* H, bool f64, cudaStream_t s);
 cudaError_t launch_convert(const void* src, void* dst, long long B, int K, int M, bool to_c64, cudaStream_t s);
+cudaError_t launch_repack_c64(const float2* src, int Ms, int Ks, float2* dst, int Md, int Kd, long long B,
+                              cudaStream_t s);
 cudaError_t measure_fp32_peak(double* tflops, double* sm_ghz);
 cudaError_t launch_stats_finalize(const double* partials, long long n, double* stats,
                                   cudaStream_t s);

@@ -62,6 +62,69 @@ def test_shapes_outside_the_specialised_kernels(K, M):
     assert np.array_equal(g["active"].cpu().numpy(), ora["active"])
 
 
+@pytest.mark.parametrize("K,M", [(3, 10), (5, 40), (6, 48), (7, 64), (8, 50), (12, 100), (24, 200), (30, 256)])
+def test_zero_padded_shapes_match_the_oracle(K, M):
+    """Shapes without a specialised kernel but within 6x the flops of one run
+    zero-padded on it (capi.cpp padded_shape): the cropped W, support and
+    per-realization outputs equal the oracle's, for every start mode; the
+    general kernel (UFPGD_NO_PAD) agrees too."""
+    import os
+
+    B = 23
+    H = U.generate_channels(41, 42, 10.0, 0, B, K, M)
+    lam, eta = params(K, M, 20)
+    c = np.full(K, np.sqrt(10.0))
+    W0 = (0.01 * np.conj(H)).astype(np.complex64)
+    for mode in (U.W0_ZERO, U.W0_CONJ_H, U.W0_GIVEN):
+        kw = dict(w0_mode=mode, want_per_realization=True)
+        if mode == U.W0_GIVEN:
+            kw["W0"] = dev(W0)
+        g = U.unfolded_forward(dev(H), lam, eta, c, **kw)
+        ora = O.forward_batch_f32(H, c, lam, eta, w0_mode=mode, W0=W0 if mode == U.W0_GIVEN else None)
+        assert_parity(report(H, g["W"].cpu().numpy(), ora, c, 1.0 / 15.0))
+        assert np.array_equal(g["active"].cpu().numpy(), ora["active"])
+        assert np.all(g["diverged_at"].cpu().numpy() == -1)
+        np.testing.assert_allclose(g["l21"].cpu().numpy(), ora["l21"], rtol=1e-5)
+        os.environ["UFPGD_NO_PAD"] = "1"
+        try:
+            gen = U.unfolded_forward(dev(H), lam, eta, c, **kw)
+        finally:
+            del os.environ["UFPGD_NO_PAD"]
+        assert_parity(report(H, gen["W"].cpu().numpy(), ora, c, 1.0 / 15.0))
+        np.testing.assert_allclose(g["stats"].cpu().numpy(), gen["stats"].cpu().numpy(), rtol=1e-5)
+
+
+def test_zero_padded_path_splits_large_batches():
+    """(6, 48) pads to (8, 64): with a 256 MiB scratch (UFPGD_PAD_SUB_MB) that
+    is 65,536 padded realizations per sub-batch, so 65,536 + 37 runs two
+    sub-batches; the seam and the stats partials of both must line up (checked
+    against the general kernel on all realizations and the oracle on the seam)."""
+    import os
+
+    os.environ["UFPGD_PAD_SUB_MB"] = "256"
+    K, M, B = 6, 48, 65536 + 37
+    H = U.generate_channels(43, 44, 10.0, 0, B, K, M)
+    lam, eta = params(K, M, 20)
+    c = np.full(K, np.sqrt(10.0))
+    try:
+        g = U.unfolded_forward(dev(H), lam, eta, c, want_per_realization=True)
+    finally:
+        del os.environ["UFPGD_PAD_SUB_MB"]
+    os.environ["UFPGD_NO_PAD"] = "1"
+    try:
+        gen = U.unfolded_forward(dev(H), lam, eta, c, want_per_realization=True)
+    finally:
+        del os.environ["UFPGD_NO_PAD"]
+    Wg, We = g["W"].cpu().numpy(), gen["W"].cpu().numpy()
+    rel = np.linalg.norm((Wg - We).reshape(B, -1), axis=1) / np.linalg.norm(We.reshape(B, -1), axis=1)
+    assert rel.max() < 1e-5, rel.max()
+    assert np.array_equal(g["active"].cpu().numpy(), gen["active"].cpu().numpy())
+    np.testing.assert_allclose(g["stats"].cpu().numpy(), gen["stats"].cpu().numpy(), rtol=1e-6)
+    seam = slice(65536 - 3, 65536 + 3)
+    ora = O.forward_batch_f32(H[seam], c, lam, eta)
+    assert_parity(report(H[seam], Wg[seam], ora, c, 1.0 / 15.0))
+
+
 def test_host_batch_with_partial_last_chunk_matches_device_path():
     w = U.CONFIGS[2]
     B = (16 << 20) // (8 * w.K * w.M) + 37  # one full 16 MiB chunk plus a ragged tail
