@@ -146,6 +146,40 @@ bool padded_shape(int K, int M, int* Kp, int* Mp) {
   return found;
 }
 
+// Runs `body` over zero-padded sub-batches: H (and W0 when given) repacked to
+// [nb][Mp][Kp] scratch, `body(hp, w0p, wp, b0, nb, parts_at, &np)` enqueues
+// the fused kernel, W cropped back. Returns the partial count in *nparts.
+template <class Body>
+int run_padded(const float2* H, const float2* W0, float2* W, int64_t B, int K, int M, int Kp, int Mp,
+               double* partials, cudaStream_t s, long long* nparts, Body body) {
+  // sub-batches of <= 1 GiB of padded H bound the scratch
+  const int64_t sub = std::max<int64_t>(1, std::min<int64_t>(B, pad_sub_bytes() / (8ll * Kp * Mp)));
+  const size_t bytes = static_cast<size_t>(sub) * Kp * Mp * sizeof(float2);
+  float2 *hp = nullptr, *wp = nullptr, *w0p = nullptr;
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&hp), bytes, s);
+  if (e == cudaSuccess) e = scratch_alloc(reinterpret_cast<void**>(&wp), bytes, s);
+  if (e == cudaSuccess && W0) e = scratch_alloc(reinterpret_cast<void**>(&w0p), bytes, s);
+  int rc = UFPGD_OK;
+  long long parts = 0;
+  for (int64_t b0 = 0; b0 < B && e == cudaSuccess && rc == UFPGD_OK; b0 += sub) {
+    const int64_t nb = std::min<int64_t>(sub, B - b0);
+    e = launch_repack_c64(H + b0 * K * M, M, K, hp, Mp, Kp, nb, s);
+    if (e == cudaSuccess && w0p) e = launch_repack_c64(W0 + b0 * K * M, M, K, w0p, Mp, Kp, nb, s);
+    if (e != cudaSuccess) break;
+    long long np = 0;
+    rc = body(hp, w0p, wp, b0, nb, partials ? partials + 3 * parts : nullptr, &np);
+    parts += np;
+    if (rc == UFPGD_OK) e = launch_repack_c64(wp, Mp, Kp, W + b0 * K * M, M, K, nb, s);
+  }
+  *nparts = parts;
+  if (hp) cudaFreeAsync(hp, s);
+  if (wp) cudaFreeAsync(wp, s);
+  if (w0p) cudaFreeAsync(w0p, s);
+  if (rc != UFPGD_OK) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "zero-padded fused solve");
+  return UFPGD_OK;
+}
+
 // Enqueues an unfolded forward on `s` (device buffers). Used by the public
 // device API and by the chunked host path.
 int enqueue_unfolded(const float2* H, int64_t B, int K, int M, const double* lambda,
@@ -177,36 +211,15 @@ int enqueue_unfolded(const float2* H, int64_t B, int K, int M, const double* lam
   }
   int Kp = 0, Mp = 0;
   if (L >= 1 && padded_shape(K, M, &Kp, &Mp)) {
-    // sub-batches of <= 1 GiB of padded H bound the scratch
-    const int64_t sub = std::max<int64_t>(1, std::min<int64_t>(B, pad_sub_bytes() / (8ll * Kp * Mp)));
-    const size_t bytes = static_cast<size_t>(sub) * Kp * Mp * sizeof(float2);
-    float2 *hp = nullptr, *wp = nullptr, *w0p = nullptr;
-    cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&hp), bytes, s);
-    if (e == cudaSuccess) e = scratch_alloc(reinterpret_cast<void**>(&wp), bytes, s);
-    if (e == cudaSuccess && w0_mode == UFPGD_W0_GIVEN) e = scratch_alloc(reinterpret_cast<void**>(&w0p), bytes, s);
     double cp[UFPGD_MAX_USERS] = {};
     for (int k = 0; k < K; ++k) cp[k] = c[k];
-    int rc = UFPGD_OK;
-    long long parts = 0;
-    for (int64_t b0 = 0; b0 < B && e == cudaSuccess && rc == UFPGD_OK; b0 += sub) {
-      const int64_t nb = std::min<int64_t>(sub, B - b0);
-      e = launch_repack_c64(H + b0 * K * M, M, K, hp, Mp, Kp, nb, s);
-      if (e == cudaSuccess && w0p) e = launch_repack_c64(W0 + b0 * K * M, M, K, w0p, Mp, Kp, nb, s);
-      if (e != cudaSuccess) break;
-      long long np = 0;
-      rc = enqueue_unfolded(hp, nb, Kp, Mp, lambda, eta, L, cp, w0_mode, w0p, wp, diverged_at ? diverged_at + b0 : nullptr,
-                            l21 ? l21 + b0 : nullptr, active ? active + b0 : nullptr,
-                            partials ? partials + 3 * parts : nullptr, alpha, s, &np);
-      parts += np;
-      if (rc == UFPGD_OK) e = launch_repack_c64(wp, Mp, Kp, W + b0 * K * M, M, K, nb, s);
-    }
-    *nparts = parts;
-    if (hp) cudaFreeAsync(hp, s);
-    if (wp) cudaFreeAsync(wp, s);
-    if (w0p) cudaFreeAsync(w0p, s);
-    if (rc != UFPGD_OK) return rc;
-    if (e != cudaSuccess) return cuda_fail(e, "zero-padded fused forward");
-    return UFPGD_OK;
+    return run_padded(H, w0_mode == UFPGD_W0_GIVEN ? W0 : nullptr, W, B, K, M, Kp, Mp, partials, s, nparts,
+                      [&](const float2* hp, const float2* w0p, float2* wp, int64_t b0, int64_t nb, double* parts,
+                          long long* np) {
+                        return enqueue_unfolded(hp, nb, Kp, Mp, lambda, eta, L, cp, w0_mode, w0p, wp,
+                                                diverged_at ? diverged_at + b0 : nullptr, l21 ? l21 + b0 : nullptr,
+                                                active ? active + b0 : nullptr, parts, alpha, s, np);
+                      });
   }
   if (!general_fits(K, M)) return fail(UFPGD_ENOTSUP, "(K, M) too large for the general kernel");
   GeneralArgs g{};
@@ -652,6 +665,113 @@ int ufpgd_gpu_lipschitz_exact(const double* H, int64_t B, int K, int M, double* 
   return UFPGD_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Enqueues a fixed-iteration PGD solve on `s` (device buffers): the fused
+// kernel (power-iteration prologue), a zero-padded fused shape, or the power
+// kernel + general kernel. Used by the device and host entry points.
+int enqueue_pgd(const float2* H, int64_t B, int K, int M, const float* eta_in, int power_steps, double lambda,
+                int64_t iters, const double* c, int w0_mode, const float2* W0, float2* W, int32_t* diverged_at,
+                float* l21, int32_t* active, float* eta_out, double* partials, double alpha, int device,
+                cudaStream_t s, long long* nparts) {
+  const bool fused = fused_supported(K, M) && iters >= 1;
+  int rc = UFPGD_OK, Kp = 0, Mp = 0;
+  long long used = B;
+  std::vector<ufpgd_c64> v0(M);
+  ufpgd_power_v0(M, v0.data());
+  if (fused) {
+    FusedArgs a{};
+    a.H = H;
+    a.W = W;
+    a.W0 = W0;
+    a.eta_in = eta_in;
+    a.eta_out = eta_out;
+    a.diverged_at = diverged_at;
+    a.l21 = l21;
+    a.active = active;
+    a.block_partials = partials;
+    a.B = B;
+    a.L = iters;
+    a.w0_mode = w0_mode;
+    a.power_steps = power_steps;
+    a.lambda = static_cast<float>(lambda);
+    a.alpha = static_cast<float>(alpha);
+    for (int k = 0; k < K; ++k) a.c[k] = static_cast<float>(c[k]);
+    std::memcpy(a.v0, v0.data(), sizeof(float2) * M);
+    cudaError_t e = launch_fused(a, true, K, M, s, &used);
+    if (e != cudaSuccess) rc = cuda_fail(e, "fused PGD kernel");
+  } else if (iters >= 1 && padded_shape(K, M, &Kp, &Mp)) {
+    // zero-padded on a fused shape; the power-iteration start vector is padded
+    // with zeros too, so the padded antennas stay 0 in every step
+    rc = run_padded(H, w0_mode == UFPGD_W0_GIVEN ? W0 : nullptr, W, B, K, M, Kp, Mp, partials, s, &used,
+                    [&](const float2* hp, const float2* w0p, float2* wp, int64_t b0, int64_t nb, double* parts,
+                        long long* np) -> int {
+                      FusedArgs a{};
+                      a.H = hp;
+                      a.W = wp;
+                      a.W0 = w0p;
+                      a.eta_in = eta_in ? eta_in + b0 : nullptr;
+                      a.eta_out = eta_out ? eta_out + b0 : nullptr;
+                      a.diverged_at = diverged_at ? diverged_at + b0 : nullptr;
+                      a.l21 = l21 ? l21 + b0 : nullptr;
+                      a.active = active ? active + b0 : nullptr;
+                      a.block_partials = parts;
+                      a.B = nb;
+                      a.L = iters;
+                      a.w0_mode = w0_mode;
+                      a.power_steps = power_steps;
+                      a.lambda = static_cast<float>(lambda);
+                      a.alpha = static_cast<float>(alpha);
+                      for (int k = 0; k < K; ++k) a.c[k] = static_cast<float>(c[k]);
+                      std::memcpy(a.v0, v0.data(), sizeof(float2) * M);  // a.v0[M..Mp) stay 0
+                      cudaError_t e = launch_fused(a, true, Kp, Mp, s, np);
+                      return e == cudaSuccess ? UFPGD_OK : cuda_fail(e, "zero-padded fused PGD kernel");
+                    });
+  } else {
+    if (!general_fits(K, M)) rc = fail(UFPGD_ENOTSUP, "(K, M) too large for the general kernel");
+    float* lip = nullptr;
+    if (rc == UFPGD_OK && !eta_in) {
+      cudaError_t e = cudaMallocAsync(&lip, sizeof(float) * B, s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "alloc");
+      if (rc == UFPGD_OK) rc = ufpgd_gpu_power_iteration(reinterpret_cast<const ufpgd_c64*>(H), B, K, M, v0.data(), power_steps, lip, device, s);
+    }
+    if (rc == UFPGD_OK) {
+      GeneralArgs gA{};
+      gA.H = H;
+      gA.W = W;
+      gA.W0 = W0;
+      gA.diverged_at = diverged_at;
+      gA.l21 = l21;
+      gA.active = active;
+      gA.block_partials = partials;
+      gA.B = B;
+      gA.K = K;
+      gA.M = M;
+      gA.w0_mode = w0_mode;
+      gA.pgd = 1;
+      gA.iters = iters;
+      gA.eta_b = eta_in;
+      gA.lip_b = lip;
+      gA.eta_out = eta_out;
+      gA.lambda = static_cast<float>(lambda);
+      gA.index_base = 1;
+      gA.alpha = static_cast<float>(alpha);
+      for (int k = 0; k < K; ++k) gA.c[k] = static_cast<float>(c[k]);
+      cudaError_t e = launch_general(gA, s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "general PGD kernel");
+    }
+    if (lip) cudaFreeAsync(lip, s);
+  }
+  *nparts = used;
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
 int ufpgd_gpu_pgd_fixed(const ufpgd_c64* H, int64_t B, int K, int M, const float* eta_in,
                         int power_steps, double lambda, int64_t iters, const double* c, int w0_mode,
                         const ufpgd_c64* W0, ufpgd_c64* W, int32_t* diverged_at, float* l21,
@@ -676,64 +796,9 @@ int ufpgd_gpu_pgd_fixed(const ufpgd_c64* H, int64_t B, int K, int M, const float
   long long used = B;
   double* partials = nullptr;
   if (stats) UFPGD_CUDA(cudaMallocAsync(&partials, sizeof(double) * 3 * np, s));
-  std::vector<ufpgd_c64> v0(M);
-  ufpgd_power_v0(M, v0.data());
-  if (fused) {
-    FusedArgs a{};
-    a.H = reinterpret_cast<const float2*>(H);
-    a.W = reinterpret_cast<float2*>(W);
-    a.W0 = reinterpret_cast<const float2*>(W0);
-    a.eta_in = eta_in;
-    a.eta_out = eta_out;
-    a.diverged_at = diverged_at;
-    a.l21 = l21;
-    a.active = active;
-    a.block_partials = partials;
-    a.B = B;
-    a.L = iters;
-    a.w0_mode = w0_mode;
-    a.power_steps = power_steps;
-    a.lambda = static_cast<float>(lambda);
-    a.alpha = static_cast<float>(alpha);
-    for (int k = 0; k < K; ++k) a.c[k] = static_cast<float>(c[k]);
-    std::memcpy(a.v0, v0.data(), sizeof(float2) * M);
-    cudaError_t e = launch_fused(a, true, K, M, s, &used);
-    if (e != cudaSuccess) rc = cuda_fail(e, "fused PGD kernel");
-  } else {
-    if (!general_fits(K, M)) rc = fail(UFPGD_ENOTSUP, "(K, M) too large for the general kernel");
-    float* lip = nullptr;
-    if (rc == UFPGD_OK && !eta_in) {
-      cudaError_t e = cudaMallocAsync(&lip, sizeof(float) * B, s);
-      if (e != cudaSuccess) rc = cuda_fail(e, "alloc");
-      if (rc == UFPGD_OK) rc = ufpgd_gpu_power_iteration(H, B, K, M, v0.data(), power_steps, lip, device, stream);
-    }
-    if (rc == UFPGD_OK) {
-      GeneralArgs gA{};
-      gA.H = reinterpret_cast<const float2*>(H);
-      gA.W = reinterpret_cast<float2*>(W);
-      gA.W0 = reinterpret_cast<const float2*>(W0);
-      gA.diverged_at = diverged_at;
-      gA.l21 = l21;
-      gA.active = active;
-      gA.block_partials = partials;
-      gA.B = B;
-      gA.K = K;
-      gA.M = M;
-      gA.w0_mode = w0_mode;
-      gA.pgd = 1;
-      gA.iters = iters;
-      gA.eta_b = eta_in;
-      gA.lip_b = lip;
-      gA.eta_out = eta_out;
-      gA.lambda = static_cast<float>(lambda);
-      gA.index_base = 1;
-      gA.alpha = static_cast<float>(alpha);
-      for (int k = 0; k < K; ++k) gA.c[k] = static_cast<float>(c[k]);
-      cudaError_t e = launch_general(gA, s);
-      if (e != cudaSuccess) rc = cuda_fail(e, "general PGD kernel");
-    }
-    if (lip) cudaFreeAsync(lip, s);
-  }
+  rc = enqueue_pgd(reinterpret_cast<const float2*>(H), B, K, M, eta_in, power_steps, lambda, iters, c, w0_mode,
+                   reinterpret_cast<const float2*>(W0), reinterpret_cast<float2*>(W), diverged_at, l21, active,
+                   eta_out, partials, alpha, device, s, &used);
   int rc2 = finish_stats(partials, rc == UFPGD_OK ? used : 0, stats, s);
   return rc != UFPGD_OK ? rc : rc2;
 }
@@ -965,6 +1030,11 @@ int ufpgd_gpu_pgd_fixed_host(const ufpgd_c64* H, int64_t B, int K, int M, int po
                              float* eta_out, double* stats, double alpha, int device) {
   int rc;
   if ((rc = check_shape(B, K, M)) || (rc = check_c(c, K)) || (rc = check_w0(w0_mode, W0))) return rc;
+  if (!(lambda >= 0.0) || !std::isfinite(lambda)) return fail(UFPGD_EINVAL_PARAM, "PgdParams: lambda must be >= 0");
+  if (iters < 0) return fail(UFPGD_EINVAL_PARAM, "PgdParams: max_iters must be >= 0");
+  if (power_steps < 1) return fail(UFPGD_EINVAL_PARAM, "power_steps must be >= 1");
+  if (!(alpha > 0.0)) return fail(UFPGD_EINVAL_PARAM, "alpha must be > 0");
+  if (B > 0 && (!H || !W)) return fail(UFPGD_EINVAL_PARAM, "H and W are required");
   DeviceGuard g(device);
   if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
   const bool fused = fused_supported(K, M) && iters >= 1;
@@ -977,58 +1047,8 @@ int ufpgd_gpu_pgd_fixed_host(const ufpgd_c64* H, int64_t B, int K, int M, int po
       stats,
       [&](float2* h, int64_t nb, float2* w0, float2* w, int32_t* div, float* eo, double* parts,
           long long* np, cudaStream_t s) -> int {
-        *np = nb;
-        std::vector<ufpgd_c64> v0(M);
-        ufpgd_power_v0(M, v0.data());
-        if (fused) {
-          FusedArgs a{};
-          a.H = h;
-          a.W = w;
-          a.W0 = w0;
-          a.eta_out = eo;
-          a.diverged_at = div;
-          a.block_partials = parts;
-          a.B = nb;
-          a.L = iters;
-          a.w0_mode = w0_mode;
-          a.power_steps = power_steps;
-          a.lambda = static_cast<float>(lambda);
-          a.alpha = static_cast<float>(alpha);
-          for (int k = 0; k < K; ++k) a.c[k] = static_cast<float>(c[k]);
-          std::memcpy(a.v0, v0.data(), sizeof(float2) * M);
-          cudaError_t e = launch_fused(a, true, K, M, s, np);
-          return e == cudaSuccess ? UFPGD_OK : cuda_fail(e, "fused PGD kernel");
-        }
-        // General shapes: power iteration then the general kernel, all on s.
-        float* lip = nullptr;
-        cudaError_t e = cudaMallocAsync(&lip, sizeof(float) * nb, s);
-        if (e != cudaSuccess) return cuda_fail(e, "alloc");
-        int r = ufpgd_gpu_power_iteration(reinterpret_cast<const ufpgd_c64*>(h), nb, K, M, v0.data(),
-                                          power_steps, lip, device, s);
-        if (r == UFPGD_OK) {
-          GeneralArgs gA{};
-          gA.H = h;
-          gA.W = w;
-          gA.W0 = w0;
-          gA.diverged_at = div;
-          gA.block_partials = parts;
-          gA.B = nb;
-          gA.K = K;
-          gA.M = M;
-          gA.w0_mode = w0_mode;
-          gA.pgd = 1;
-          gA.iters = iters;
-          gA.lip_b = lip;
-          gA.eta_out = eo;
-          gA.lambda = static_cast<float>(lambda);
-          gA.index_base = 1;
-          gA.alpha = static_cast<float>(alpha);
-          for (int k = 0; k < K; ++k) gA.c[k] = static_cast<float>(c[k]);
-          e = launch_general(gA, s);
-          r = e == cudaSuccess ? UFPGD_OK : cuda_fail(e, "general PGD kernel");
-        }
-        cudaFreeAsync(lip, s);
-        return r;
+        return enqueue_pgd(h, nb, K, M, nullptr, power_steps, lambda, iters, c, w0_mode, w0, w, div, nullptr,
+                           nullptr, eo, parts, alpha, device, s, np);
       });
 }
 

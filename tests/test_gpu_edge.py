@@ -94,6 +94,25 @@ def test_zero_padded_shapes_match_the_oracle(K, M):
         np.testing.assert_allclose(g["stats"].cpu().numpy(), gen["stats"].cpu().numpy(), rtol=1e-5)
 
 
+@pytest.mark.parametrize("K,M", [(3, 10), (6, 48), (12, 100)])
+def test_zero_padded_pgd_with_power_iteration(K, M):
+    """pgd_fixed on a padded shape: the 30-step power iteration runs on the
+    zero-padded H with the zero-padded start vector, so L30 (hence eta), W
+    and the support match the oracle's unpadded solve; the host pipeline
+    entry point returns the same bits as the device one."""
+    B, iters, lam = 16, 300, 0.05
+    H = U.generate_channels(124, 0, 0.0, 0, B, K, M)
+    c = np.full(K, np.sqrt(10.0))
+    out = U.pgd_fixed(dev(H), lam, iters, c, power_steps=30, want_per_realization=True)
+    Lo, _ = O.power_iteration_batch_f32(H, 30)
+    assert np.max(np.abs(out["eta"].cpu().numpy() * Lo - 1.0)) <= 1e-5
+    ora = O.pgd_batch_f32(H, c, lam, 1.0 / Lo, iters, w0_mode=U.W0_CONJ_H)
+    assert_parity(report(H, out["W"].cpu().numpy(), ora, c, lam))
+    assert np.array_equal(out["active"].cpu().numpy(), ora["active"])
+    host = U.pgd_fixed_host(H, lam, iters, c, power_steps=30)
+    assert np.array_equal(host["W"], out["W"].cpu().numpy())
+
+
 def test_zero_padded_path_splits_large_batches():
     """(6, 48) pads to (8, 64): with a 256 MiB scratch (UFPGD_PAD_SUB_MB) that
     is 65,536 padded realizations per sub-batch, so 65,536 + 37 runs two
