@@ -190,3 +190,45 @@ def test_fp32_peak_probe_is_plausible():
     (nominal 148 SMs x 128 lanes x 2 x 1.965 GHz = 74.4 TFLOP/s)."""
     tf, ghz = U.fp32_peak(0)
     assert 30.0 < tf < 80.0 and 1.0 < ghz < 2.2, (tf, ghz)
+
+
+def test_concurrent_host_calls_from_threads():
+    """The reference's functions are reentrant and callers batch with
+    parallel_for (parallel.hpp:12-18): several host threads calling the C ABI
+    at once (ctypes releases the GIL) must each get their own exact result —
+    the host path serialises on the device's workspace, device calls on
+    separate streams run concurrently."""
+    import threading
+
+    w = U.CONFIGS[2]
+    lam, eta = w.layer_params()
+    Hs = [U.make_inputs(w, 1000 * t, 3000 + 17 * t) for t in range(4)]
+    ref = [U.unfolded_forward_host(H, lam, eta, w.c, w0_mode=w.w0_mode)["W"] for H in Hs]
+    out, errs = [None] * 8, []
+
+    def host(t):
+        try:
+            out[t] = U.unfolded_forward_host(Hs[t], lam, eta, w.c, w0_mode=w.w0_mode)["W"]
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+
+    def device(t):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                Hd = dev(Hs[t - 4])
+                r = U.unfolded_forward(Hd, lam, eta, w.c, w0_mode=w.w0_mode, stream=s)["W"]
+                s.synchronize()
+                out[t] = r.cpu().numpy()
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=host, args=(t,)) for t in range(4)]
+    th += [threading.Thread(target=device, args=(t,)) for t in range(4, 8)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs, errs
+    for t in range(8):
+        assert np.array_equal(out[t], ref[t % 4]), t
