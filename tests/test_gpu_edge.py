@@ -172,6 +172,28 @@ def test_divergence_from_a_zero_start_on_every_kernel_shape(K, M):
     assert_parity(report(H[1:2], out["W"].cpu().numpy()[1:2], ora, c, 1.0 / 15.0))
 
 
+@pytest.mark.parametrize("K,M", [(4, 32), (8, 64), (16, 128), (32, 256), (6, 48), (5, 5)])
+def test_nan_channel_diverges_at_layer_zero_and_is_isolated(K, M):
+    """A NaN anywhere in H makes the first step image non-finite
+    (unfolded.cpp:120-125: allFinite is false for NaN as for inf): the
+    realization reports layer 0, counts as diverged in the stats, and its
+    neighbours are untouched — on the fused, tiled, padded and general paths."""
+    H = U.generate_channels(6, 0, 0.0, 0, 3, K, M)
+    H[1, M // 2, K - 1] = np.complex64(complex(np.nan, 0.0))
+    lam, eta = params(K, M, 4)
+    c = np.full(K, np.sqrt(10.0))
+    for mode in (U.W0_ZERO, U.W0_CONJ_H):
+        out = U.unfolded_forward(dev(H), lam, eta, c, w0_mode=mode, want_per_realization=True)
+        assert out["diverged_at"].cpu().numpy().tolist() == [-1, 0, -1]
+        assert out["stats"].cpu().numpy()[2] == 1.0
+        keep = [0, 2]
+        ora = O.forward_batch_f32(H[keep], c, lam, eta, w0_mode=mode)
+        assert_parity(report(H[keep], out["W"].cpu().numpy()[keep], ora, c, 1.0 / 15.0))
+    pg = U.pgd_fixed(dev(H), 0.05, 50, c, power_steps=30, want_per_realization=True)
+    d = pg["diverged_at"].cpu().numpy()
+    assert d[1] >= 1 and d[0] == -1 and d[2] == -1  # 1-based iteration index (pgd.cpp:231-235)
+
+
 def test_pgd_host_path_matches_device_path():
     """ufpgd_gpu_pgd_fixed_host (config 3 end to end: pinned-chunk pipeline,
     in-kernel 30-step power iteration) equals the device entry point bit for
