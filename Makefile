@@ -6,7 +6,7 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC -Xcompiler -Wall -
 PKG      := paper_2304_12745_b200
 LIBDIR   := $(PKG)/lib
 OBJDIR   := build/obj
-SRCS_CU  := $(addprefix $(PKG)/csrc/,team.cu team64.cu tile.cu general.cu metrics.cu grad.cu datagen.cu probe.cu)
+SRCS_CU  := $(addprefix $(PKG)/csrc/,team.cu team64.cu tile.cu mma.cu general.cu metrics.cu grad.cu datagen.cu probe.cu)
 SRCS_CPP := $(PKG)/csrc/capi.cpp $(PKG)/csrc/host_gen.cpp $(PKG)/csrc/api.cpp $(PKG)/csrc/dataset_io.cpp $(PKG)/csrc/host_util.cpp
 CXX      ?= g++
 CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -Iinclude -I$(PKG)/csrc -I/usr/local/cuda/include

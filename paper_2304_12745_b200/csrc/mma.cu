@@ -1,0 +1,494 @@
+// Tensor-core (tcgen05 / TMEM) kernel for the unfolded forward at
+// (K, M) = (32, 256) — BASELINE config 4, the "larger M x K x K complex
+// contractions" north_star reserves the tensor cores for. One CTA (8 warps,
+// thread = antenna) owns a realization for all layers (unfolded.cpp:112-146):
+//
+//   stage 1  X  = W H^T           tcgen05.mma  M=128 N=64 K=256 (x2)
+//   stage 2  G  = (-eta X') H^*   tcgen05.mma  M=128 N=64 K=64  (x6)
+//   prox     per-antenna group soft threshold on V = W + G, in registers
+//
+// Precision: FP32 products are split into f16 pairs, x = hi + 2^-11 lo
+// (lo = f16((x - hi) * 2^11)), and every real product is formed as
+// hi*hi + 2^-11 (hi*lo + lo*hi) with FP32 accumulation in TMEM — the
+// "3-term split" whose error (~2^-22 relative) matches FP32 arithmetic (a
+// numpy emulation of the whole 20-layer forward at config 4 gives 1.5e-7
+// W relative error against the FP64 oracle vs 1.4e-7 for plain FP32). Each
+// realization is scaled by an exact power of two g (max |g H| in [1, 2)) so
+// the f16 range is never approached: X is invariant (W_s = W / g), the step
+// becomes eta / g^2 and the threshold thr / g.
+//
+// Real forms (rows r = (part, k), part 0 = Re, 1 = Im, r in [0, 2K)):
+//   stage 1: D1[q][(p', k')] = sum_m Wop[q][m] Hop[(p', k')][m], q = (hilo, p, k)
+//            (A = [W_hi; W_lo] 128 x M, MN-major; B = H_hi or H_lo, K-major)
+//            X_r = P[(0,k),(0,k')] - P[(1,k),(1,k')], X_i = P[(0,k),(1,k')] + P[(1,k),(0,k')]
+//   stage 2: D2[m][(p, k)] = sum_(p', k') Hop[(p', k')][m] Bs[(p', k')][(p, k)]
+//            (A = H as M x 2K MN-major — the same shared-memory bytes as
+//            stage 1's K-major B — and Bs = the real form of -eta X'^T)
+// so H (hi and lo, f16) is staged once and read by both stages.
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+
+#include <cuda_fp16.h>
+
+#include "device_common.cuh"
+
+namespace ufpgd_gpu_impl {
+namespace {
+
+struct Mma32x256 {
+  static constexpr int K = 32, M = 256, NT = 256;
+  static constexpr int R = 2 * K;  // real-form rows (part, k)
+  // shared-memory byte offsets (all 1024-aligned)
+  static constexpr int OFF_HH = 0;                       // H hi  [R x M] f16, core layout hoff()
+  static constexpr int OFF_HL = OFF_HH + R * M * 2;      // H lo
+  static constexpr int OFF_W = OFF_HL + R * M * 2;       // [W_hi; W_lo] [2R x M] f16, woff()
+  static constexpr int OFF_BH = OFF_W + 2 * R * M * 2;   // Bs hi [R x R] f16, boff()
+  static constexpr int OFF_BL = OFF_BH + R * R * 2;      // Bs lo
+  static constexpr int FSTR = R + 4;                     // fp32 exchange rows (floats), conflict-free LDS/STS.128
+  static constexpr int OFF_F = OFF_BL + R * R * 2;       // F [R][FSTR]: hi rows of P
+  static constexpr int OFF_G = OFF_F + R * FSTR * 4;     // G [R][FSTR]: lo rows of P
+  static constexpr int OFF_BAR = OFF_G + R * FSTR * 4;   // 2 mbarriers, TMEM slot, reductions
+  static constexpr int SMEM = OFF_BAR + 256;
+  // TMEM columns (fp32 accumulators, 128 lanes)
+  static constexpr uint32_t T_D1A = 0, T_D1B = 64, T_D2M = 128, T_D2C = 256, T_COLS = 512;
+
+  // Canonical no-swizzle layouts: 8 x 16-byte core matrices (128 contiguous bytes).
+  // H: element (r, m); core (r / 8, m / 8); inside: row r % 8 (16 B), m % 8 (2 B).
+  //   stage 1 B (K-major, N = r, K = m): LBO (K-group) 128, SBO (N-group) 16 M
+  //   stage 2 A (MN-major, MN = m, K = r): LBO (K-group) 16 M, SBO (MN-group) 128
+  static __device__ __forceinline__ int hoff(int r, int m) {
+    return (r >> 3) * (16 * M) + (m >> 3) * 128 + (r & 7) * 16 + (m & 7) * 2;
+  }
+  // W operand: element (q, m), MN-major (MN = q, K = m): core (q / 8, m / 8);
+  // inside: row m % 8 (16 B), q % 8 (2 B). LBO (K-group) 16 * 2R, SBO 128.
+  static __device__ __forceinline__ int woff(int q, int m) {
+    return (m >> 3) * (16 * 2 * R) + (q >> 3) * 128 + (m & 7) * 16 + (q & 7) * 2;
+  }
+  // Bs: element (kk, n), K-major (K = kk, N = n): LBO (K-group) 128, SBO (N-group) 16 R.
+  static __device__ __forceinline__ int boff(int kk, int n) {
+    return (kk >> 3) * 128 + (n >> 3) * (16 * R) + (n & 7) * 16 + (kk & 7) * 2;
+  }
+};
+
+// ---- PTX wrappers -------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// tcgen05 shared-memory matrix descriptor, SWIZZLE_NONE, version 1 (sm_100).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+// Instruction descriptor, kind::f16: f16 A/B, f32 D, A MN-major, B K-major.
+template <int MM, int NN>
+__device__ __forceinline__ constexpr uint32_t idesc_f16_amn() {
+  return (1u << 4) | (1u << 15) | (static_cast<uint32_t>(NN >> 3) << 17) | (static_cast<uint32_t>(MM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  for (long long spin = 0;; ++spin) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (spin > (1ll << 28)) __trap();  // never hang the GPU on a lost arrive
+  }
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// 16 consecutive TMEM columns of this warp's 32 lanes -> 16 registers per thread.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
+        "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+      : "r"(taddr));
+}
+// Waits for this thread's tcgen05.ld results; the laundering asm keeps every
+// use of v after the wait.
+template <int N>
+__device__ __forceinline__ void tmem_wait(float* v) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" : "+f"(v[i]));
+}
+// f16 pair split of (a, b): hi = f16(x), lo = f16((x - hi) * 2^11).
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(a, b);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn((a - hf.x) * 2048.f, (b - hf.y) * 2048.f);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+__device__ __forceinline__ uint16_t f16_bits(__half h) { return *reinterpret_cast<const uint16_t*>(&h); }
+
+constexpr float kLoScale = 1.f / 2048.f;
+
+template <class T>
+__global__ void __launch_bounds__(T::NT, 1) mma_kernel(const __grid_constant__ FusedArgs p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int K = T::K, M = T::M, R = T::R;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long rid = blockIdx.x;
+  const uint32_t sb = smem_u32(smem);
+  const uint32_t bar1 = sb + T::OFF_BAR, bar2 = sb + T::OFF_BAR + 8;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + T::OFF_BAR + 16);
+  float* red = reinterpret_cast<float*>(smem + T::OFF_BAR + 32);           // [3][8]
+  long long* fbs = reinterpret_cast<long long*>(smem + T::OFF_BAR + 128);  // [8]
+
+  if (tid == 0) {
+    mbar_init(bar1, 1);
+    mbar_init(bar2, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "n"(T::T_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+
+  // ---- H row of antenna m = tid: registers, max |.| over the realization ----
+  const int m = tid;
+  float4 hv[K / 2];  // hv[j] = (Re H(2j, m), Im H(2j, m), Re H(2j+1, m), Im H(2j+1, m))
+  {
+    const float4* hg = reinterpret_cast<const float4*>(p.H + (rid * M + m) * K);
+#pragma unroll
+    for (int j = 0; j < K / 2; ++j) hv[j] = ldg_stream(hg + j);
+  }
+  float amax = 0.f;
+#pragma unroll
+  for (int j = 0; j < K / 2; ++j)
+    amax = fmaxf(amax, fmaxf(fmaxf(fabsf(hv[j].x), fabsf(hv[j].y)), fmaxf(fabsf(hv[j].z), fabsf(hv[j].w))));
+  // fmaxf drops NaN: flag it separately so a NaN channel keeps g = 1
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < K / 2; ++j) bad |= !(fabsf(hv[j].x) + fabsf(hv[j].y) + fabsf(hv[j].z) + fabsf(hv[j].w) <= FLT_MAX);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(kFull, amax, off));
+  const unsigned anybad = __ballot_sync(kFull, bad);
+  if (lane == 0) {
+    red[warp] = amax;
+    red[8 + warp] = anybad ? 1.f : 0.f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  float gmax = 0.f, gbad = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    gmax = fmaxf(gmax, red[w]);
+    gbad = fmaxf(gbad, red[8 + w]);
+  }
+  // g = 2^-e with gmax in [2^e, 2^(e+1)): g * gmax in [1, 2). Exact scaling.
+  float g = 1.f;
+  if (gbad == 0.f && gmax > 0.f && gmax <= FLT_MAX) g = ldexpf(1.f, -ilogbf(gmax));
+  const float ginv = 1.f / g;  // exact (power of two)
+
+  // ---- stage H (hi / lo f16) in the shared core layout -------------------------
+#pragma unroll
+  for (int j = 0; j < K / 2; ++j) {
+    const float vals[4] = {hv[j].x * g, hv[j].y * g, hv[j].z * g, hv[j].w * g};
+    const int rows[4] = {2 * j, K + 2 * j, 2 * j + 1, K + 2 * j + 1};  // Re k, Im k, Re k+1, Im k+1
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const __half h = __float2half_rn(vals[u]);
+      const __half l = __float2half_rn((vals[u] - __half2float(h)) * 2048.f);
+      *reinterpret_cast<uint16_t*>(smem + T::OFF_HH + T::hoff(rows[u], m)) = f16_bits(h);
+      *reinterpret_cast<uint16_t*>(smem + T::OFF_HL + T::hoff(rows[u], m)) = f16_bits(l);
+    }
+  }
+  fence_async_smem();  // H is read by the tensor cores (async proxy)
+
+  // ---- W0 (scaled: W_s = W / g) in registers: wr[k], wi[k] for antenna m ------
+  float wr[K], wi[K];
+  if (p.w0_mode == UFPGD_W0_CONJ_H) {
+#pragma unroll
+    for (int j = 0; j < K / 2; ++j) {
+      wr[2 * j] = hv[j].x * ginv;
+      wi[2 * j] = -hv[j].y * ginv;
+      wr[2 * j + 1] = hv[j].z * ginv;
+      wi[2 * j + 1] = -hv[j].w * ginv;
+    }
+  } else if (p.w0_mode == UFPGD_W0_GIVEN) {
+    const float4* wg0 = reinterpret_cast<const float4*>(p.W0 + (rid * M + m) * K);
+#pragma unroll
+    for (int j = 0; j < K / 2; ++j) {
+      const float4 v = wg0[j];
+      wr[2 * j] = v.x * ginv;
+      wi[2 * j] = v.y * ginv;
+      wr[2 * j + 1] = v.z * ginv;
+      wi[2 * j + 1] = v.w * ginv;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k) wr[k] = wi[k] = 0.f;
+  }
+
+  constexpr uint32_t IDESC = idesc_f16_amn<128, 64>();
+  float* F = reinterpret_cast<float*>(smem + T::OFF_F);
+  float* G = reinterpret_cast<float*>(smem + T::OFF_G);
+  uint32_t ph1 = 0, ph2 = 0;
+  bool nonfinite = false;
+  long long first_bad = -1;
+  float l21 = 0.f;
+  int act = 0;
+  const float g2inv = ginv * ginv;
+
+  for (long long l = 0; l < p.L; ++l) {
+    const bool xzero = (l == 0 && p.w0_mode == UFPGD_W0_ZERO);
+    const float ts = p.thr[l] * ginv;       // threshold in the scaled domain
+    const float fstep = -p.eta[l] * g2inv;  // -eta / g^2 folded into Bs
+    if (!xzero) {
+      // W operand (rows q = (hilo, part, k)) from the thread's antenna column
+#pragma unroll
+      for (int grp = 0; grp < R / 8; ++grp) {  // 8 rows (part, k .. k+7)
+        const float* src = grp < K / 8 ? wr + 8 * grp : wi + 8 * (grp - K / 8);
+        uint32_t h[4], lo[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) split2(src[2 * u], src[2 * u + 1], h[u], lo[u]);
+        *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(8 * grp, m)) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(R + 8 * grp, m)) =
+            make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
+      fence_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+#pragma unroll 1
+        for (int ks = 0; ks < M / 16; ++ks) {
+          const uint64_t a = sdesc(sb + T::OFF_W + ks * (2 * 16 * 2 * R), 16 * 2 * R, 128);
+          umma_f16(tmem + T::T_D1A, a, sdesc(sb + T::OFF_HH + ks * 256, 128, 16 * M), IDESC, ks > 0);
+          umma_f16(tmem + T::T_D1B, a, sdesc(sb + T::OFF_HL + ks * 256, 128, 16 * M), IDESC, ks > 0);
+        }
+        umma_commit(bar1);
+      }
+      if (warp < 4) {
+        mbar_wait(bar1, ph1);
+        tc_fence_after();
+        const uint32_t lrow = static_cast<uint32_t>(warp * 32) << 16;
+        // warps 0, 1: q = (hi, part = warp, k = lane): F row = D1a + 2^-11 D1b
+        // warps 2, 3: q = (lo, part = warp - 2, k): G row = 2^-11 D1a
+        float* dst = (warp < 2 ? F + (warp * 32 + lane) * T::FSTR : G + ((warp - 2) * 32 + lane) * T::FSTR);
+#pragma unroll
+        for (int cq = 0; cq < R; cq += 16) {
+          float a[16], b[16];
+          tmem_ld16(tmem + lrow + T::T_D1A + cq, a);
+          if (warp < 2) tmem_ld16(tmem + lrow + T::T_D1B + cq, b);
+          tmem_wait<16>(a);
+          if (warp < 2) {
+            tmem_wait<16>(b);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) a[i] = fmaf(kLoScale, b[i], a[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) a[i] *= kLoScale;
+          }
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(dst + cq + i) = make_float4(a[i], a[i + 1], a[i + 2], a[i + 3]);
+        }
+      }
+      ph1 ^= 1;
+    }
+    if (warp < 4) {
+      // Bs[(p_in, k')][(p_out, k)] = -eta/g^2 * { X'r, X'i ; X'i, -X'r }(k, k')
+      if (!xzero) named_bar(1, 128);
+      const int n = tid & (R - 1), pout = n / K, k = n % K, pin = tid / R;
+      const float* F0 = F + k * T::FSTR;        // P row (0, k): hi part
+      const float* F1 = F + (K + k) * T::FSTR;  // P row (1, k)
+      const float* G0 = G + k * T::FSTR;
+      const float* G1 = G + (K + k) * T::FSTR;
+#pragma unroll
+      for (int c8 = 0; c8 < K; c8 += 8) {
+        float v[8];
+#pragma unroll
+        for (int h4 = 0; h4 < 8; h4 += 4) {
+          float4 xr = make_float4(0.f, 0.f, 0.f, 0.f), xi = xr;
+          if (!xzero) {
+            const int c = c8 + h4;
+            // (k, k'..k'+3): P00 = F0[c] + G0[c], P11 = F1[K + c] + G1[K + c], ...
+            const float4 a00 = *reinterpret_cast<const float4*>(F0 + c);
+            const float4 b00 = *reinterpret_cast<const float4*>(G0 + c);
+            const float4 a11 = *reinterpret_cast<const float4*>(F1 + K + c);
+            const float4 b11 = *reinterpret_cast<const float4*>(G1 + K + c);
+            const float4 a01 = *reinterpret_cast<const float4*>(F0 + K + c);
+            const float4 b01 = *reinterpret_cast<const float4*>(G0 + K + c);
+            const float4 a10 = *reinterpret_cast<const float4*>(F1 + c);
+            const float4 b10 = *reinterpret_cast<const float4*>(G1 + c);
+            xr = make_float4((a00.x + b00.x) - (a11.x + b11.x), (a00.y + b00.y) - (a11.y + b11.y),
+                             (a00.z + b00.z) - (a11.z + b11.z), (a00.w + b00.w) - (a11.w + b11.w));
+            xi = make_float4((a01.x + b01.x) + (a10.x + b10.x), (a01.y + b01.y) + (a10.y + b10.y),
+                             (a01.z + b01.z) + (a10.z + b10.z), (a01.w + b01.w) + (a10.w + b10.w));
+          }
+          float re[4] = {xr.x, xr.y, xr.z, xr.w}, im[4] = {xi.x, xi.y, xi.z, xi.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (c8 + h4 + u == k) re[u] -= p.c[k];  // X' = X - diag(c)
+            const float val = (pout == pin) ? (pout == 0 ? re[u] : -re[u]) : im[u];
+            v[h4 + u] = fstep * val;
+          }
+        }
+        uint32_t h[4], lo[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) split2(v[2 * u], v[2 * u + 1], h[u], lo[u]);
+        const int kk = pin * K + c8;
+        *reinterpret_cast<uint4*>(smem + T::OFF_BH + T::boff(kk, n)) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4*>(smem + T::OFF_BL + T::boff(kk, n)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
+      fence_async_smem();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll 1
+      for (int tile = 0; tile < 2; ++tile) {
+        const uint32_t dm = tmem + T::T_D2M + tile * 64, dc = tmem + T::T_D2C + tile * 64;
+#pragma unroll
+        for (int ks = 0; ks < R / 16; ++ks) {
+          const uint64_t ah = sdesc(sb + T::OFF_HH + tile * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
+          const uint64_t al = sdesc(sb + T::OFF_HL + tile * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
+          const uint64_t bh = sdesc(sb + T::OFF_BH + ks * 256, 128, 16 * R);
+          const uint64_t bl = sdesc(sb + T::OFF_BL + ks * 256, 128, 16 * R);
+          umma_f16(dm, ah, bh, IDESC, ks > 0);
+          umma_f16(dc, ah, bl, IDESC, ks > 0);
+          umma_f16(dc, al, bh, IDESC, 1);
+        }
+      }
+      umma_commit(bar2);
+    }
+    mbar_wait(bar2, ph2);
+    ph2 ^= 1;
+    tc_fence_after();
+    {
+      // antenna m: TMEM lane m % 128 (warp quadrant warp % 4), tile m / 128
+      const uint32_t lrow = static_cast<uint32_t>((warp & 3) * 32) << 16;
+      const uint32_t cm = tmem + lrow + T::T_D2M + (m >> 7) * 64;
+      const uint32_t cc = tmem + lrow + T::T_D2C + (m >> 7) * 64;
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        float* w = part == 0 ? wr : wi;
+#pragma unroll
+        for (int k0 = 0; k0 < K; k0 += 16) {
+          float a[16], b[16];
+          tmem_ld16(cm + part * K + k0, a);
+          tmem_ld16(cc + part * K + k0, b);
+          tmem_wait<16>(a);
+          tmem_wait<16>(b);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) w[k0 + i] += fmaf(kLoScale, b[i], a[i]);  // V = W - eta X' H^*
+        }
+      }
+    }
+    tc_fence_before();
+    // prox_l21 on the antenna column (strict '>', pgd.cpp:237-244 / unfolded.cpp:135-143)
+    float s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) s2 = fmaf(wr[k], wr[k], fmaf(wi[k], wi[k], s2));
+    nonfinite |= !(s2 * (g * g) <= FLT_MAX);
+    const bool on = s2 > ts * ts;
+    const float r = rsqrt_ftz(fmaxf(s2, FLT_MIN));
+    const float scale = on ? fmaf(-ts, r, 1.f) : 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      wr[k] *= scale;
+      wi[k] *= scale;
+    }
+    if (l + 1 == p.L && on) {
+      l21 += g * fmaf(s2, r, -ts);
+      act += 1;
+    }
+    if (nonfinite && first_bad < 0) first_bad = l;
+  }
+
+  // ---- W out (unscaled), per-realization reductions ---------------------------
+  {
+    float4* wg = reinterpret_cast<float4*>(p.W + (rid * M + m) * K);
+#pragma unroll
+    for (int j = 0; j < K / 2; ++j)
+      stg_stream(wg + j, make_float4(wr[2 * j] * g, wi[2 * j] * g, wr[2 * j + 1] * g, wi[2 * j + 1] * g));
+  }
+  long long fb = first_bad < 0 ? LLONG_MAX : first_bad;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    fb = min(fb, __shfl_xor_sync(kFull, fb, off));
+    l21 += __shfl_xor_sync(kFull, l21, off);
+    act += __shfl_xor_sync(kFull, act, off);
+  }
+  if (lane == 0) {
+    fbs[warp] = fb;
+    red[warp] = l21;
+    red[8 + warp] = static_cast<float>(act);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(T::T_COLS) : "memory");
+  }
+  if (tid == 0) {
+    for (int w = 1; w < 8; ++w) {
+      fb = min(fb, fbs[w]);
+      l21 += red[w];
+      act += static_cast<int>(red[8 + w]);
+    }
+    const bool diverged = fb != LLONG_MAX;
+    if (p.diverged_at) p.diverged_at[rid] = diverged ? static_cast<int32_t>(fb) : -1;
+    if (p.l21) p.l21[rid] = diverged ? __int_as_float(0x7fc00000) : l21;
+    if (p.active) p.active[rid] = diverged ? -1 : act;
+    if (p.block_partials) {
+      p.block_partials[rid * 3 + 0] = diverged ? 0.0 : static_cast<double>(p.alpha) * l21;
+      p.block_partials[rid * 3 + 1] = diverged ? 0.0 : static_cast<double>(act);
+      p.block_partials[rid * 3 + 2] = diverged ? 1.0 : 0.0;
+    }
+  }
+}
+
+}  // namespace
+
+// Unfolded forward only (PGD keeps the FP32 tile kernel); UFPGD_NO_MMA=1
+// selects the CUDA-core tile kernel for A/B runs.
+bool mma_supported(int K, int M, bool pgd) {
+  if (pgd || K != 32 || M != 256) return false;
+  const char* off = std::getenv("UFPGD_NO_MMA");
+  return !(off && off[0] == '1');
+}
+
+cudaError_t launch_mma(const FusedArgs& a, int K, int M, cudaStream_t s, long long* nblocks) {
+  if (K != 32 || M != 256) return cudaErrorInvalidValue;
+  using T = Mma32x256;
+  auto kern = mma_kernel<T>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+  if (e != cudaSuccess) return e;
+  if (nblocks) *nblocks = a.B;
+  if (a.B == 0) return cudaSuccess;
+  kern<<<static_cast<unsigned>(a.B), T::NT, T::SMEM, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace ufpgd_gpu_impl

@@ -1,0 +1,94 @@
+"""Development check of the tcgen05 kernel (mma.cu) at (K, M) = (32, 256):
+single-layer closed forms, the 20-layer config-4 forward against the FP64
+oracle and the CUDA-core tile kernel, and CUDA-event timing of both."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2304_12745_b200 as U
+
+
+def run(H, lam, eta, c, w0_mode=0, W0=None, mma=True):
+    os.environ["UFPGD_NO_MMA"] = "0" if mma else "1"
+    Hd = torch.from_numpy(H).cuda()
+    W0d = torch.from_numpy(W0).cuda() if W0 is not None else None
+    out = U.unfolded_forward(Hd, lam, eta, c, w0_mode=w0_mode, W0=W0d, want_per_realization=True)
+    torch.cuda.synchronize()
+    return {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
+
+
+def rel(a, b):
+    B = a.shape[0]
+    return np.linalg.norm((a - b).reshape(B, -1), axis=1) / np.maximum(np.linalg.norm(b.reshape(B, -1), axis=1), 1e-30)
+
+
+def one_layer(B=4, seed=0):
+    rng = np.random.default_rng(seed)
+    K, M = 32, 256
+    H = ((rng.standard_normal((B, M, K)) + 1j * rng.standard_normal((B, M, K))) / np.sqrt(2)).astype(np.complex64)
+    c = np.full(K, np.sqrt(10.0))
+    eta = np.array([1 / 469.0]); lam = np.array([0.0])
+    Hk = np.transpose(H, (0, 2, 1)).astype(np.complex128)  # [B][K][M]
+    # a) W0 = 0: W1 = eta diag(c) H^*
+    o = run(H, lam, eta, c)
+    ref = eta[0] * c[None, :, None] * np.conj(Hk)
+    r = rel(np.transpose(o["W"], (0, 2, 1)), ref)
+    print(f"L=1 W0=0: rel max {r.max():.3e}", flush=True)
+    if r.max() > 1e-5:
+        Wg = np.transpose(o["W"], (0, 2, 1))
+        print("  sample got", Wg[0, :3, :3], "\n  want", ref[0, :3, :3])
+    # b) W0 given: W1 = W0 - eta (W0 H^T - diag c) H^*
+    W0 = ((rng.standard_normal((B, M, K)) + 1j * rng.standard_normal((B, M, K))) * 0.05).astype(np.complex64)
+    o = run(H, lam, eta, c, w0_mode=2, W0=W0)
+    W0k = np.transpose(W0, (0, 2, 1)).astype(np.complex128)
+    X = W0k @ np.transpose(Hk, (0, 2, 1)) - np.diag(c)[None]
+    ref = W0k - eta[0] * X @ np.conj(Hk)
+    r = rel(np.transpose(o["W"], (0, 2, 1)), ref)
+    print(f"L=1 W0 given: rel max {r.max():.3e}", flush=True)
+    if r.max() > 1e-5:
+        Wg = np.transpose(o["W"], (0, 2, 1))
+        d = np.abs(Wg - ref)[0]
+        print("  err by user", np.round(d.max(1), 4))
+        print("  err by antenna (first 16)", np.round(d.max(0)[:16], 4))
+        print("  G got", (Wg - W0k)[0, :2, :4], "\n  G want", (ref - W0k)[0, :2, :4])
+
+
+def cfg4(n=256):
+    from oracle import oracle as O
+    w = U.CONFIGS[4]
+    H = U.make_inputs(w, 0, n)
+    lam, eta = w.layer_params()
+    om = run(H, lam, eta, w.c)
+    ot = run(H, lam, eta, w.c, mma=False)
+    ora = O.forward_batch_f32(H, w.c, lam, eta, w0_mode=w.w0_mode)
+    rm, rt = rel(om["W"], ora["W"]), rel(ot["W"], ora["W"])
+    fo = O.lagrangian_batch(H, ora["W"], w.c, 1 / 15)
+    fm = O.lagrangian_batch(H, om["W"], w.c, 1 / 15)
+    print(f"cfg4 n={n}: mma W rel max {rm.max():.3e} median {np.median(rm):.3e}; tile {rt.max():.3e}; "
+          f"obj rel max {np.max(np.abs(fm - fo) / np.abs(fo)):.3e}; diverged {int((om['diverged_at'] >= 0).sum())}; "
+          f"active {om['active'].mean():.1f}; l21 rel {np.max(np.abs(om['l21'] - ot['l21']) / ot['l21']):.2e}", flush=True)
+
+
+def timing(n=16384, reps=3):
+    w = U.CONFIGS[4]
+    Hd = torch.empty((n, w.M, w.K), dtype=torch.complex64, device="cuda")
+    U.generate_channels_device(w.seed_h, w.seed_g, w.gain_db, 0, n, w.K, w.M, out=Hd)
+    lam, eta = w.layer_params()
+    W = torch.empty_like(Hd)
+    for mma in (True, False):
+        os.environ["UFPGD_NO_MMA"] = "0" if mma else "1"
+        U.unfolded_forward(Hd, lam, eta, w.c, out=W); torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps): U.unfolded_forward(Hd, lam, eta, w.c, out=W)
+        e.record(); torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / reps
+        fl = w.flops_per_realization() * n
+        print(f"{'mma ' if mma else 'tile'} cfg4 B={n}: {ms:.3f} ms  {n / ms * 1e3 / 1e3:.1f} k/s  "
+              f"{fl / ms / 1e9:.1f} TFLOP/s (FP32-equivalent)", flush=True)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1:] or ["one", "cfg4", "time"]
+    if "one" in what: one_layer()
+    if "cfg4" in what: cfg4()
+    if "time" in what: timing()
