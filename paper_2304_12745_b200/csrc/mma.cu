@@ -38,22 +38,34 @@
 namespace ufpgd_gpu_impl {
 namespace {
 
-struct Mma32x256 {
-  static constexpr int K = 32, M = 256, NT = 256;
-  static constexpr int R = 2 * K;  // real-form rows (part, k)
+// Shape of the tensor-core kernel: one thread per antenna (NT = M), 2K
+// real-form rows r = (part, k), Q = 4K operand rows q = (hilo, part, k) for
+// stage 1 (MMA M = Q: 128 at K = 32, 64 at K = 16), M / 128 stage-2 tiles.
+template <int K_, int M_, int MINB_>
+struct MmaShape {
+  static constexpr int K = K_, M = M_, NT = M_, MINB = MINB_;
+  static constexpr int R = 2 * K;     // real-form rows (part, k)
+  static constexpr int Q = 2 * R;     // stage-1 A rows (hilo, part, k) = stage-1 MMA M
+  static constexpr int NTILE = M / 128;
+  static constexpr int NW = NT / 32;
+  static_assert(Q == 64 || Q == 128, "stage-1 MMA M must be 64 or 128");
+  static_assert(M % 128 == 0 && NW <= 8 && K % 16 == 0, "");
   // shared-memory byte offsets (all 1024-aligned)
   static constexpr int OFF_HH = 0;                       // H hi  [R x M] f16, core layout hoff()
   static constexpr int OFF_HL = OFF_HH + R * M * 2;      // H lo
-  static constexpr int OFF_W = OFF_HL + R * M * 2;       // [W_hi; W_lo] [2R x M] f16, woff()
-  static constexpr int OFF_BH = OFF_W + 2 * R * M * 2;   // Bs hi [R x R] f16, boff()
+  static constexpr int OFF_W = OFF_HL + R * M * 2;       // [W_hi; W_lo] [Q x M] f16, woff()
+  static constexpr int OFF_BH = OFF_W + Q * M * 2;       // Bs hi [R x R] f16, boff()
   static constexpr int OFF_BL = OFF_BH + R * R * 2;      // Bs lo
   static constexpr int FSTR = R + 4;                     // fp32 exchange rows (floats), conflict-free LDS/STS.128
   static constexpr int OFF_F = OFF_BL + R * R * 2;       // F [R][FSTR]: hi rows of P
   static constexpr int OFF_G = OFF_F + R * FSTR * 4;     // G [R][FSTR]: lo rows of P
-  static constexpr int OFF_BAR = OFF_G + R * FSTR * 4;   // 2 mbarriers, TMEM slot, reductions
+  static constexpr int OFF_BAR = OFF_G + R * FSTR * 4;   // mbarriers, TMEM slot, reductions
   static constexpr int SMEM = OFF_BAR + 256;
-  // TMEM columns (fp32 accumulators, 128 lanes)
-  static constexpr uint32_t T_D1A = 0, T_D1B = 64, T_D2M = 128, T_D2C = 256, T_COLS = 512;
+  // TMEM columns (fp32 accumulators)
+  static constexpr uint32_t T_D1A = 0, T_D1B = R, T_D2M = 2 * R, T_D2C = 2 * R + NTILE * R;
+  static constexpr uint32_t T_USED = 2 * R + 2 * NTILE * R;
+  static constexpr uint32_t T_COLS = T_USED <= 32 ? 32 : T_USED <= 64 ? 64 : T_USED <= 128 ? 128 : T_USED <= 256 ? 256 : 512;
+  static_assert(T_USED <= 512, "");
 
   // Canonical no-swizzle layouts: 8 x 16-byte core matrices (128 contiguous bytes).
   // H: element (r, m); core (r / 8, m / 8); inside: row r % 8 (16 B), m % 8 (2 B).
@@ -63,9 +75,9 @@ struct Mma32x256 {
     return (r >> 3) * (16 * M) + (m >> 3) * 128 + (r & 7) * 16 + (m & 7) * 2;
   }
   // W operand: element (q, m), MN-major (MN = q, K = m): core (q / 8, m / 8);
-  // inside: row m % 8 (16 B), q % 8 (2 B). LBO (K-group) 16 * 2R, SBO 128.
+  // inside: row m % 8 (16 B), q % 8 (2 B). LBO (K-group) 16 Q, SBO 128.
   static __device__ __forceinline__ int woff(int q, int m) {
-    return (m >> 3) * (16 * 2 * R) + (q >> 3) * 128 + (m & 7) * 16 + (q & 7) * 2;
+    return (m >> 3) * (16 * Q) + (q >> 3) * 128 + (m & 7) * 16 + (q & 7) * 2;
   }
   // Bs: element (kk, n), K-major (K = kk, N = n): LBO (K-group) 128, SBO (N-group) 16 R.
   static __device__ __forceinline__ int boff(int kk, int n) {
@@ -147,20 +159,20 @@ __device__ __forceinline__ uint16_t f16_bits(__half h) { return *reinterpret_cas
 constexpr float kLoScale = 1.f / 2048.f;
 
 template <class T>
-__global__ void __launch_bounds__(T::NT, 1) mma_kernel(const __grid_constant__ FusedArgs p) {
+__global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_constant__ FusedArgs p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int K = T::K, M = T::M, R = T::R;
+  constexpr int K = T::K, M = T::M, R = T::R, Q = T::Q, NW = T::NW;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long rid = blockIdx.x;
   const uint32_t sb = smem_u32(smem);
-  const uint32_t bar1 = sb + T::OFF_BAR, bar2 = sb + T::OFF_BAR + 8;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + T::OFF_BAR + 16);
-  float* red = reinterpret_cast<float*>(smem + T::OFF_BAR + 32);           // [3][8]
+  const uint32_t bar1 = sb + T::OFF_BAR;  // stage 1 done; bar1 + 8 (1 + tile): stage-2 tile done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + T::OFF_BAR + 48);
+  float* red = reinterpret_cast<float*>(smem + T::OFF_BAR + 64);           // [2][8]
   long long* fbs = reinterpret_cast<long long*>(smem + T::OFF_BAR + 128);  // [8]
 
   if (tid == 0) {
-    mbar_init(bar1, 1);
-    mbar_init(bar2, 1);
+#pragma unroll
+    for (int b = 0; b <= T::NTILE; ++b) mbar_init(bar1 + 8 * b, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -179,13 +191,13 @@ __global__ void __launch_bounds__(T::NT, 1) mma_kernel(const __grid_constant__ F
     for (int j = 0; j < K / 2; ++j) hv[j] = ldg_stream(hg + j);
   }
   float amax = 0.f;
+  bool bad = false;  // fmaxf drops NaN: a non-finite channel keeps g = 1 (and diverges at layer 0)
 #pragma unroll
-  for (int j = 0; j < K / 2; ++j)
-    amax = fmaxf(amax, fmaxf(fmaxf(fabsf(hv[j].x), fabsf(hv[j].y)), fmaxf(fabsf(hv[j].z), fabsf(hv[j].w))));
-  // fmaxf drops NaN: flag it separately so a NaN channel keeps g = 1
-  bool bad = false;
-#pragma unroll
-  for (int j = 0; j < K / 2; ++j) bad |= !(fabsf(hv[j].x) + fabsf(hv[j].y) + fabsf(hv[j].z) + fabsf(hv[j].w) <= FLT_MAX);
+  for (int j = 0; j < K / 2; ++j) {
+    const float a = fmaxf(fmaxf(fabsf(hv[j].x), fabsf(hv[j].y)), fmaxf(fabsf(hv[j].z), fabsf(hv[j].w)));
+    amax = fmaxf(amax, a);
+    bad |= !(fabsf(hv[j].x) + fabsf(hv[j].y) + fabsf(hv[j].z) + fabsf(hv[j].w) <= FLT_MAX);
+  }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(kFull, amax, off));
   const unsigned anybad = __ballot_sync(kFull, bad);
@@ -199,13 +211,13 @@ __global__ void __launch_bounds__(T::NT, 1) mma_kernel(const __grid_constant__ F
   const uint32_t tmem = *tslot;
   float gmax = 0.f, gbad = 0.f;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) {
+  for (int w = 0; w < NW; ++w) {
     gmax = fmaxf(gmax, red[w]);
     gbad = fmaxf(gbad, red[8 + w]);
   }
   // g = 2^-e with gmax in [2^e, 2^(e+1)): g * gmax in [1, 2). Exact scaling.
   float g = 1.f;
-  if (gbad == 0.f && gmax > 0.f && gmax <= FLT_MAX) g = ldexpf(1.f, -ilogbf(gmax));
+  if (gbad == 0.f && gmax > 0.f) g = ldexpf(1.f, -ilogbf(gmax));
   const float ginv = 1.f / g;  // exact (power of two)
 
   // ---- stage H (hi / lo f16) in the shared core layout -------------------------
@@ -248,22 +260,25 @@ __global__ void __launch_bounds__(T::NT, 1) mma_kernel(const __grid_constant__ F
     for (int k = 0; k < K; ++k) wr[k] = wi[k] = 0.f;
   }
 
-  constexpr uint32_t IDESC = idesc_f16_amn<128, 64>();
+  constexpr uint32_t IDESC1 = idesc_f16_amn<Q, R>();
+  constexpr uint32_t IDESC2 = idesc_f16_amn<128, R>();
   float* F = reinterpret_cast<float*>(smem + T::OFF_F);
   float* G = reinterpret_cast<float*>(smem + T::OFF_G);
-  uint32_t ph1 = 0, ph2 = 0;
+  uint32_t ph1 = 0, ph2 = 0;  // stage-1 barrier (skipped at a W0 = 0 layer 0), stage-2 tile barriers
   bool nonfinite = false;
   long long first_bad = -1;
   float l21 = 0.f;
   int act = 0;
   const float g2inv = ginv * ginv;
+  const int tile = m >> 7;
+  const uint32_t lrow = static_cast<uint32_t>((warp & 3) * 32) << 16;  // this warp's TMEM lane quadrant
 
   for (long long l = 0; l < p.L; ++l) {
     const bool xzero = (l == 0 && p.w0_mode == UFPGD_W0_ZERO);
     const float ts = p.thr[l] * ginv;       // threshold in the scaled domain
     const float fstep = -p.eta[l] * g2inv;  // -eta / g^2 folded into Bs
     if (!xzero) {
-      // W operand (rows q = (hilo, part, k)) from the thread's antenna column
+      // W operand rows q = (hilo, part, k) from the thread's antenna column
 #pragma unroll
       for (int grp = 0; grp < R / 8; ++grp) {  // 8 rows (part, k .. k+7)
         const float* src = grp < K / 8 ? wr + 8 * grp : wi + 8 * (grp - K / 8);
@@ -281,115 +296,119 @@ __global__ void __launch_bounds__(T::NT, 1) mma_kernel(const __grid_constant__ F
         tc_fence_after();
 #pragma unroll 1
         for (int ks = 0; ks < M / 16; ++ks) {
-          const uint64_t a = sdesc(sb + T::OFF_W + ks * (2 * 16 * 2 * R), 16 * 2 * R, 128);
-          umma_f16(tmem + T::T_D1A, a, sdesc(sb + T::OFF_HH + ks * 256, 128, 16 * M), IDESC, ks > 0);
-          umma_f16(tmem + T::T_D1B, a, sdesc(sb + T::OFF_HL + ks * 256, 128, 16 * M), IDESC, ks > 0);
+          const uint64_t a = sdesc(sb + T::OFF_W + ks * 2 * 16 * Q, 16 * Q, 128);
+          umma_f16(tmem + T::T_D1A, a, sdesc(sb + T::OFF_HH + ks * 256, 128, 16 * M), IDESC1, ks > 0);
+          umma_f16(tmem + T::T_D1B, a, sdesc(sb + T::OFF_HL + ks * 256, 128, 16 * M), IDESC1, ks > 0);
         }
         umma_commit(bar1);
       }
-      if (warp < 4) {
-        mbar_wait(bar1, ph1);
-        tc_fence_after();
-        const uint32_t lrow = static_cast<uint32_t>(warp * 32) << 16;
-        // warps 0, 1: q = (hi, part = warp, k = lane): F row = D1a + 2^-11 D1b
-        // warps 2, 3: q = (lo, part = warp - 2, k): G row = 2^-11 D1a
-        float* dst = (warp < 2 ? F + (warp * 32 + lane) * T::FSTR : G + ((warp - 2) * 32 + lane) * T::FSTR);
+      // D1 rows q = (hilo, part, k): TMEM lane quadrant hilo * 2 + part, lane k
+      // (M = 128: lanes 32 q4 + k; M = 64: lanes 32 q4 + k for k < 16).
+      // Warp w reads quadrant w % 4, columns [w / 4 * CW, + CW).
+      constexpr int CW = R * 4 / NW;
+      const int quad = warp & 3, c0 = (warp >> 2) * CW, part = quad & 1;
+      mbar_wait(bar1, ph1);
+      ph1 ^= 1;
+      tc_fence_after();
+      float* dst = (quad < 2 ? F : G) + (part * K + lane) * T::FSTR + c0;
 #pragma unroll
-        for (int cq = 0; cq < R; cq += 16) {
-          float a[16], b[16];
-          tmem_ld16(tmem + lrow + T::T_D1A + cq, a);
-          if (warp < 2) tmem_ld16(tmem + lrow + T::T_D1B + cq, b);
-          tmem_wait<16>(a);
-          if (warp < 2) {
-            tmem_wait<16>(b);
+      for (int cq = 0; cq < CW; cq += 16) {
+        float a[16], b[16];
+        tmem_ld16(tmem + lrow + T::T_D1A + c0 + cq, a);
+        if (quad < 2) tmem_ld16(tmem + lrow + T::T_D1B + c0 + cq, b);
+        tmem_wait<16>(a);
+        if (quad < 2) {
+          tmem_wait<16>(b);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) a[i] = fmaf(kLoScale, b[i], a[i]);
-          } else {
+          for (int i = 0; i < 16; ++i) a[i] = fmaf(kLoScale, b[i], a[i]);  // hi rows: W_hi H_hi + W_hi H_lo
+        } else {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) a[i] *= kLoScale;
-          }
+          for (int i = 0; i < 16; ++i) a[i] *= kLoScale;  // lo rows: W_lo H_hi
+        }
+        if (lane < K) {
 #pragma unroll
           for (int i = 0; i < 16; i += 4)
             *reinterpret_cast<float4*>(dst + cq + i) = make_float4(a[i], a[i + 1], a[i + 2], a[i + 3]);
         }
       }
-      ph1 ^= 1;
+      __syncthreads();
     }
-    if (warp < 4) {
-      // Bs[(p_in, k')][(p_out, k)] = -eta/g^2 * { X'r, X'i ; X'i, -X'r }(k, k')
-      if (!xzero) named_bar(1, 128);
-      const int n = tid & (R - 1), pout = n / K, k = n % K, pin = tid / R;
-      const float* F0 = F + k * T::FSTR;        // P row (0, k): hi part
-      const float* F1 = F + (K + k) * T::FSTR;  // P row (1, k)
-      const float* G0 = G + k * T::FSTR;
-      const float* G1 = G + (K + k) * T::FSTR;
+    // Bs[(p_in, k')][(p_out, k)] = -eta/g^2 * { X'r, X'i ; X'i, -X'r }(k, k'), one
+    // 4-wide chunk of X' row k per thread
+    constexpr int NCH = K * K / 4;
 #pragma unroll
-      for (int c8 = 0; c8 < K; c8 += 8) {
-        float v[8];
-#pragma unroll
-        for (int h4 = 0; h4 < 8; h4 += 4) {
-          float4 xr = make_float4(0.f, 0.f, 0.f, 0.f), xi = xr;
-          if (!xzero) {
-            const int c = c8 + h4;
-            // (k, k'..k'+3): P00 = F0[c] + G0[c], P11 = F1[K + c] + G1[K + c], ...
-            const float4 a00 = *reinterpret_cast<const float4*>(F0 + c);
-            const float4 b00 = *reinterpret_cast<const float4*>(G0 + c);
-            const float4 a11 = *reinterpret_cast<const float4*>(F1 + K + c);
-            const float4 b11 = *reinterpret_cast<const float4*>(G1 + K + c);
-            const float4 a01 = *reinterpret_cast<const float4*>(F0 + K + c);
-            const float4 b01 = *reinterpret_cast<const float4*>(G0 + K + c);
-            const float4 a10 = *reinterpret_cast<const float4*>(F1 + c);
-            const float4 b10 = *reinterpret_cast<const float4*>(G1 + c);
-            xr = make_float4((a00.x + b00.x) - (a11.x + b11.x), (a00.y + b00.y) - (a11.y + b11.y),
-                             (a00.z + b00.z) - (a11.z + b11.z), (a00.w + b00.w) - (a11.w + b11.w));
-            xi = make_float4((a01.x + b01.x) + (a10.x + b10.x), (a01.y + b01.y) + (a10.y + b10.y),
-                             (a01.z + b01.z) + (a10.z + b10.z), (a01.w + b01.w) + (a10.w + b10.w));
-          }
-          float re[4] = {xr.x, xr.y, xr.z, xr.w}, im[4] = {xi.x, xi.y, xi.z, xi.w};
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (c8 + h4 + u == k) re[u] -= p.c[k];  // X' = X - diag(c)
-            const float val = (pout == pin) ? (pout == 0 ? re[u] : -re[u]) : im[u];
-            v[h4 + u] = fstep * val;
-          }
-        }
-        uint32_t h[4], lo[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) split2(v[2 * u], v[2 * u + 1], h[u], lo[u]);
-        const int kk = pin * K + c8;
-        *reinterpret_cast<uint4*>(smem + T::OFF_BH + T::boff(kk, n)) = make_uint4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<uint4*>(smem + T::OFF_BL + T::boff(kk, n)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    for (int ch = tid; ch < NCH; ch += T::NT) {
+      const int k = ch / (K / 4), c = (ch % (K / 4)) * 4;
+      float xr[4] = {0.f, 0.f, 0.f, 0.f}, xi[4] = {0.f, 0.f, 0.f, 0.f};
+      if (!xzero) {
+        const float* F0 = F + k * T::FSTR;        // P rows (0, k), (1, k): hi parts in F, lo in G
+        const float* F1 = F + (K + k) * T::FSTR;
+        const float* G0 = G + k * T::FSTR;
+        const float* G1 = G + (K + k) * T::FSTR;
+        const float4 a00 = *reinterpret_cast<const float4*>(F0 + c), b00 = *reinterpret_cast<const float4*>(G0 + c);
+        const float4 a11 = *reinterpret_cast<const float4*>(F1 + K + c), b11 = *reinterpret_cast<const float4*>(G1 + K + c);
+        const float4 a01 = *reinterpret_cast<const float4*>(F0 + K + c), b01 = *reinterpret_cast<const float4*>(G0 + K + c);
+        const float4 a10 = *reinterpret_cast<const float4*>(F1 + c), b10 = *reinterpret_cast<const float4*>(G1 + c);
+        xr[0] = (a00.x + b00.x) - (a11.x + b11.x);
+        xr[1] = (a00.y + b00.y) - (a11.y + b11.y);
+        xr[2] = (a00.z + b00.z) - (a11.z + b11.z);
+        xr[3] = (a00.w + b00.w) - (a11.w + b11.w);
+        xi[0] = (a01.x + b01.x) + (a10.x + b10.x);
+        xi[1] = (a01.y + b01.y) + (a10.y + b10.y);
+        xi[2] = (a01.z + b01.z) + (a10.z + b10.z);
+        xi[3] = (a01.w + b01.w) + (a10.w + b10.w);
       }
-      fence_async_smem();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (c + u == k) xr[u] -= p.c[k];  // X' = X - diag(c)
+        xr[u] *= fstep;
+        xi[u] *= fstep;
+      }
+      uint32_t rh[2], rl[2], nh[2], nl[2], ih[2], il[2];
+      split2(xr[0], xr[1], rh[0], rl[0]);
+      split2(xr[2], xr[3], rh[1], rl[1]);
+      split2(-xr[0], -xr[1], nh[0], nl[0]);
+      split2(-xr[2], -xr[3], nh[1], nl[1]);
+      split2(xi[0], xi[1], ih[0], il[0]);
+      split2(xi[2], xi[3], ih[1], il[1]);
+      // (p_in, p_out) = (0,0): X'r, (1,0): X'i, (0,1): X'i, (1,1): -X'r
+      *reinterpret_cast<uint2*>(smem + T::OFF_BH + T::boff(c, k)) = make_uint2(rh[0], rh[1]);
+      *reinterpret_cast<uint2*>(smem + T::OFF_BL + T::boff(c, k)) = make_uint2(rl[0], rl[1]);
+      *reinterpret_cast<uint2*>(smem + T::OFF_BH + T::boff(K + c, k)) = make_uint2(ih[0], ih[1]);
+      *reinterpret_cast<uint2*>(smem + T::OFF_BL + T::boff(K + c, k)) = make_uint2(il[0], il[1]);
+      *reinterpret_cast<uint2*>(smem + T::OFF_BH + T::boff(c, K + k)) = make_uint2(ih[0], ih[1]);
+      *reinterpret_cast<uint2*>(smem + T::OFF_BL + T::boff(c, K + k)) = make_uint2(il[0], il[1]);
+      *reinterpret_cast<uint2*>(smem + T::OFF_BH + T::boff(K + c, K + k)) = make_uint2(nh[0], nh[1]);
+      *reinterpret_cast<uint2*>(smem + T::OFF_BL + T::boff(K + c, K + k)) = make_uint2(nl[0], nl[1]);
     }
+    fence_async_smem();
     tc_fence_before();
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
 #pragma unroll 1
-      for (int tile = 0; tile < 2; ++tile) {
-        const uint32_t dm = tmem + T::T_D2M + tile * 64, dc = tmem + T::T_D2C + tile * 64;
+      for (int t = 0; t < T::NTILE; ++t) {
+        const uint32_t dm = tmem + T::T_D2M + t * R, dc = tmem + T::T_D2C + t * R;
 #pragma unroll
         for (int ks = 0; ks < R / 16; ++ks) {
-          const uint64_t ah = sdesc(sb + T::OFF_HH + tile * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
-          const uint64_t al = sdesc(sb + T::OFF_HL + tile * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
+          const uint64_t ah = sdesc(sb + T::OFF_HH + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
+          const uint64_t al = sdesc(sb + T::OFF_HL + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
           const uint64_t bh = sdesc(sb + T::OFF_BH + ks * 256, 128, 16 * R);
           const uint64_t bl = sdesc(sb + T::OFF_BL + ks * 256, 128, 16 * R);
-          umma_f16(dm, ah, bh, IDESC, ks > 0);
-          umma_f16(dc, ah, bl, IDESC, ks > 0);
-          umma_f16(dc, al, bh, IDESC, 1);
+          umma_f16(dm, ah, bh, IDESC2, ks > 0);
+          umma_f16(dc, ah, bl, IDESC2, ks > 0);
+          umma_f16(dc, al, bh, IDESC2, 1);
         }
+        umma_commit(bar1 + 8 * (1 + t));  // each tile's epilogue starts as soon as its MMAs retire
       }
-      umma_commit(bar2);
     }
-    mbar_wait(bar2, ph2);
+    mbar_wait(bar1 + 8 * (1 + tile), ph2);
     ph2 ^= 1;
     tc_fence_after();
     {
       // antenna m: TMEM lane m % 128 (warp quadrant warp % 4), tile m / 128
-      const uint32_t lrow = static_cast<uint32_t>((warp & 3) * 32) << 16;
-      const uint32_t cm = tmem + lrow + T::T_D2M + (m >> 7) * 64;
-      const uint32_t cc = tmem + lrow + T::T_D2C + (m >> 7) * 64;
+      const uint32_t cm = tmem + lrow + T::T_D2M + tile * R;
+      const uint32_t cc = tmem + lrow + T::T_D2C + tile * R;
 #pragma unroll
       for (int part = 0; part < 2; ++part) {
         float* w = part == 0 ? wr : wi;
@@ -452,7 +471,7 @@ __global__ void __launch_bounds__(T::NT, 1) mma_kernel(const __grid_constant__ F
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(T::T_COLS) : "memory");
   }
   if (tid == 0) {
-    for (int w = 1; w < 8; ++w) {
+    for (int w = 1; w < NW; ++w) {
       fb = min(fb, fbs[w]);
       l21 += red[w];
       act += static_cast<int>(red[8 + w]);
@@ -469,19 +488,11 @@ __global__ void __launch_bounds__(T::NT, 1) mma_kernel(const __grid_constant__ F
   }
 }
 
-}  // namespace
+using Mma_32_256 = MmaShape<32, 256, 1>;
+using Mma_16_128 = MmaShape<16, 128, 4>;
 
-// Unfolded forward only (PGD keeps the FP32 tile kernel); UFPGD_NO_MMA=1
-// selects the CUDA-core tile kernel for A/B runs.
-bool mma_supported(int K, int M, bool pgd) {
-  if (pgd || K != 32 || M != 256) return false;
-  const char* off = std::getenv("UFPGD_NO_MMA");
-  return !(off && off[0] == '1');
-}
-
-cudaError_t launch_mma(const FusedArgs& a, int K, int M, cudaStream_t s, long long* nblocks) {
-  if (K != 32 || M != 256) return cudaErrorInvalidValue;
-  using T = Mma32x256;
+template <class T>
+cudaError_t launch_mma_t(const FusedArgs& a, cudaStream_t s, long long* nblocks) {
   auto kern = mma_kernel<T>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
   if (e != cudaSuccess) return e;
@@ -489,6 +500,22 @@ cudaError_t launch_mma(const FusedArgs& a, int K, int M, cudaStream_t s, long lo
   if (a.B == 0) return cudaSuccess;
   kern<<<static_cast<unsigned>(a.B), T::NT, T::SMEM, s>>>(a);
   return cudaGetLastError();
+}
+
+}  // namespace
+
+// Unfolded forward only (PGD keeps the FP32 tile kernel); UFPGD_NO_MMA=1
+// selects the CUDA-core tile kernel for A/B runs.
+bool mma_supported(int K, int M, bool pgd) {
+  if (pgd || !((K == 32 && M == 256) || (K == 16 && M == 128))) return false;
+  const char* off = std::getenv("UFPGD_NO_MMA");
+  return !(off && off[0] == '1');
+}
+
+cudaError_t launch_mma(const FusedArgs& a, int K, int M, cudaStream_t s, long long* nblocks) {
+  if (K == 32 && M == 256) return launch_mma_t<Mma_32_256>(a, s, nblocks);
+  if (K == 16 && M == 128) return launch_mma_t<Mma_16_128>(a, s, nblocks);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace ufpgd_gpu_impl

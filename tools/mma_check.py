@@ -21,9 +21,8 @@ def rel(a, b):
     return np.linalg.norm((a - b).reshape(B, -1), axis=1) / np.maximum(np.linalg.norm(b.reshape(B, -1), axis=1), 1e-30)
 
 
-def one_layer(B=4, seed=0):
+def one_layer(K=32, M=256, B=4, seed=0):
     rng = np.random.default_rng(seed)
-    K, M = 32, 256
     H = ((rng.standard_normal((B, M, K)) + 1j * rng.standard_normal((B, M, K))) / np.sqrt(2)).astype(np.complex64)
     c = np.full(K, np.sqrt(10.0))
     eta = np.array([1 / 469.0]); lam = np.array([0.0])
@@ -32,7 +31,7 @@ def one_layer(B=4, seed=0):
     o = run(H, lam, eta, c)
     ref = eta[0] * c[None, :, None] * np.conj(Hk)
     r = rel(np.transpose(o["W"], (0, 2, 1)), ref)
-    print(f"L=1 W0=0: rel max {r.max():.3e}", flush=True)
+    print(f"({K},{M}) L=1 W0=0: rel max {r.max():.3e}", flush=True)
     if r.max() > 1e-5:
         Wg = np.transpose(o["W"], (0, 2, 1))
         print("  sample got", Wg[0, :3, :3], "\n  want", ref[0, :3, :3])
@@ -43,7 +42,7 @@ def one_layer(B=4, seed=0):
     X = W0k @ np.transpose(Hk, (0, 2, 1)) - np.diag(c)[None]
     ref = W0k - eta[0] * X @ np.conj(Hk)
     r = rel(np.transpose(o["W"], (0, 2, 1)), ref)
-    print(f"L=1 W0 given: rel max {r.max():.3e}", flush=True)
+    print(f"({K},{M}) L=1 W0 given: rel max {r.max():.3e}", flush=True)
     if r.max() > 1e-5:
         Wg = np.transpose(o["W"], (0, 2, 1))
         d = np.abs(Wg - ref)[0]
@@ -52,9 +51,9 @@ def one_layer(B=4, seed=0):
         print("  G got", (Wg - W0k)[0, :2, :4], "\n  G want", (ref - W0k)[0, :2, :4])
 
 
-def cfg4(n=256):
+def check(cfg=4, n=256):
     from oracle import oracle as O
-    w = U.CONFIGS[4]
+    w = U.CONFIGS[cfg]
     H = U.make_inputs(w, 0, n)
     lam, eta = w.layer_params()
     om = run(H, lam, eta, w.c)
@@ -63,13 +62,13 @@ def cfg4(n=256):
     rm, rt = rel(om["W"], ora["W"]), rel(ot["W"], ora["W"])
     fo = O.lagrangian_batch(H, ora["W"], w.c, 1 / 15)
     fm = O.lagrangian_batch(H, om["W"], w.c, 1 / 15)
-    print(f"cfg4 n={n}: mma W rel max {rm.max():.3e} median {np.median(rm):.3e}; tile {rt.max():.3e}; "
+    print(f"cfg{cfg} n={n}: mma W rel max {rm.max():.3e} median {np.median(rm):.3e}; tile {rt.max():.3e}; "
           f"obj rel max {np.max(np.abs(fm - fo) / np.abs(fo)):.3e}; diverged {int((om['diverged_at'] >= 0).sum())}; "
           f"active {om['active'].mean():.1f}; l21 rel {np.max(np.abs(om['l21'] - ot['l21']) / ot['l21']):.2e}", flush=True)
 
 
-def timing(n=16384, reps=3):
-    w = U.CONFIGS[4]
+def timing(cfg=4, n=16384, reps=3):
+    w = U.CONFIGS[cfg]
     Hd = torch.empty((n, w.M, w.K), dtype=torch.complex64, device="cuda")
     U.generate_channels_device(w.seed_h, w.seed_g, w.gain_db, 0, n, w.K, w.M, out=Hd)
     lam, eta = w.layer_params()
@@ -83,12 +82,17 @@ def timing(n=16384, reps=3):
         e.record(); torch.cuda.synchronize()
         ms = s.elapsed_time(e) / reps
         fl = w.flops_per_realization() * n
-        print(f"{'mma ' if mma else 'tile'} cfg4 B={n}: {ms:.3f} ms  {n / ms * 1e3 / 1e3:.1f} k/s  "
+        print(f"{'mma ' if mma else 'tile'} cfg{cfg} B={n}: {ms:.3f} ms  {n / ms * 1e3 / 1e3:.1f} k/s  "
               f"{fl / ms / 1e9:.1f} TFLOP/s (FP32-equivalent)", flush=True)
 
 
 if __name__ == "__main__":
     what = sys.argv[1:] or ["one", "cfg4", "time"]
-    if "one" in what: one_layer()
-    if "cfg4" in what: cfg4()
-    if "time" in what: timing()
+    if "one" in what:
+        one_layer(32, 256)
+        one_layer(16, 128)
+    if "cfg4" in what: check(4)
+    if "cfg5" in what: check(5, 1024)
+    if "time" in what:
+        timing(4, 16384)
+        timing(5, 65536)
