@@ -3,8 +3,8 @@
 // contractions" north_star reserves the tensor cores for. One CTA (8 warps,
 // thread = antenna) owns a realization for all layers (unfolded.cpp:112-146):
 //
-//   stage 1  X  = W H^T           tcgen05.mma  M=128 N=64 K=256 (x2)
-//   stage 2  G  = (-eta X') H^*   tcgen05.mma  M=128 N=64 K=64  (x6)
+//   stage 1  X  = W H^T           tcgen05.mma  M=128 N=128 K=256
+//   stage 2  G  = (-eta X') H^*   tcgen05.mma  M=128 N=128 + N=64, K=64, per 128-antenna tile
 //   prox     per-antenna group soft threshold on V = W + G, in registers
 //
 // Precision: FP32 products are split into f16 pairs, x = hi + 2^-11 lo
@@ -62,7 +62,8 @@ struct MmaShape {
   static constexpr int OFF_BAR = OFF_G + R * FSTR * 4;   // mbarriers, TMEM slot, reductions
   static constexpr int SMEM = OFF_BAR + 256;
   // TMEM columns (fp32 accumulators)
-  static constexpr uint32_t T_D1A = 0, T_D1B = R, T_D2M = 2 * R, T_D2C = 2 * R + NTILE * R;
+  // D1: [X-part with H_hi | with H_lo] (2R); D2 per tile t: [main | corr] at T_D2 + 2R t
+  static constexpr uint32_t T_D1A = 0, T_D1B = R, T_D2 = 2 * R;
   static constexpr uint32_t T_USED = 2 * R + 2 * NTILE * R;
   static constexpr uint32_t T_COLS = T_USED <= 32 ? 32 : T_USED <= 64 ? 64 : T_USED <= 128 ? 128 : T_USED <= 256 ? 256 : 512;
   static_assert(T_USED <= 512, "");
@@ -260,8 +261,11 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     for (int k = 0; k < K; ++k) wr[k] = wi[k] = 0.f;
   }
 
-  constexpr uint32_t IDESC1 = idesc_f16_amn<Q, R>();
+  constexpr uint32_t IDESC1 = idesc_f16_amn<Q, 2 * R>();
+  constexpr uint32_t IDESC2W = idesc_f16_amn<128, 2 * R>();
   constexpr uint32_t IDESC2 = idesc_f16_amn<128, R>();
+  static_assert(T::OFF_HL == T::OFF_HH + (R / 8) * 16 * M && T::OFF_BL == T::OFF_BH + (R / 8) * 16 * R,
+                "lo operands continue the hi ones along N");
   float* F = reinterpret_cast<float*>(smem + T::OFF_F);
   float* G = reinterpret_cast<float*>(smem + T::OFF_G);
   uint32_t ph1 = 0, ph2 = 0;  // stage-1 barrier (skipped at a W0 = 0 layer 0), stage-2 tile barriers
@@ -296,9 +300,9 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
         tc_fence_after();
 #pragma unroll 1
         for (int ks = 0; ks < M / 16; ++ks) {
+          // B = [H_hi | H_lo] (N = 2R: OFF_HL continues OFF_HH's N-group stride)
           const uint64_t a = sdesc(sb + T::OFF_W + ks * 2 * 16 * Q, 16 * Q, 128);
           umma_f16(tmem + T::T_D1A, a, sdesc(sb + T::OFF_HH + ks * 256, 128, 16 * M), IDESC1, ks > 0);
-          umma_f16(tmem + T::T_D1B, a, sdesc(sb + T::OFF_HL + ks * 256, 128, 16 * M), IDESC1, ks > 0);
         }
         umma_commit(bar1);
       }
@@ -388,16 +392,14 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
       tc_fence_after();
 #pragma unroll 1
       for (int t = 0; t < T::NTILE; ++t) {
-        const uint32_t dm = tmem + T::T_D2M + t * R, dc = tmem + T::T_D2C + t * R;
+        const uint32_t dm = tmem + T::T_D2 + t * 2 * R, dc = dm + R;
 #pragma unroll
         for (int ks = 0; ks < R / 16; ++ks) {
           const uint64_t ah = sdesc(sb + T::OFF_HH + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
           const uint64_t al = sdesc(sb + T::OFF_HL + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
-          const uint64_t bh = sdesc(sb + T::OFF_BH + ks * 256, 128, 16 * R);
-          const uint64_t bl = sdesc(sb + T::OFF_BL + ks * 256, 128, 16 * R);
-          umma_f16(dm, ah, bh, IDESC2, ks > 0);
-          umma_f16(dc, ah, bl, IDESC2, ks > 0);
-          umma_f16(dc, al, bh, IDESC2, 1);
+          const uint64_t bh = sdesc(sb + T::OFF_BH + ks * 256, 128, 16 * R);  // N = 2R spans [Bs_hi | Bs_lo]
+          umma_f16(dm, ah, bh, IDESC2W, ks > 0);  // [main | corr] = H_hi [Bs_hi | Bs_lo]
+          umma_f16(dc, al, bh, IDESC2, 1);        // corr += H_lo Bs_hi
         }
         umma_commit(bar1 + 8 * (1 + t));  // each tile's epilogue starts as soon as its MMAs retire
       }
@@ -407,8 +409,8 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     tc_fence_after();
     {
       // antenna m: TMEM lane m % 128 (warp quadrant warp % 4), tile m / 128
-      const uint32_t cm = tmem + lrow + T::T_D2M + tile * R;
-      const uint32_t cc = tmem + lrow + T::T_D2C + tile * R;
+      const uint32_t cm = tmem + lrow + T::T_D2 + tile * 2 * R;
+      const uint32_t cc = cm + R;
 #pragma unroll
       for (int part = 0; part < 2; ++part) {
         float* w = part == 0 ? wr : wi;

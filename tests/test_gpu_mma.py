@@ -1,0 +1,101 @@
+"""The tcgen05 tensor-core path (csrc/mma.cu) of the unfolded forward at the
+BASELINE shapes (16, 128) and (32, 256): parity with the FP64 oracle at the
+north_star bars, agreement with the CUDA-core tile kernel (UFPGD_NO_MMA=1),
+every W0 mode, and exact equivariance under power-of-two channel scaling —
+the property the kernel's per-realization f16 range scaling must preserve
+(unfolded.cpp:112-146 is homogeneous: H -> aH, eta -> eta/a^2,
+lambda -> a lambda maps W -> W/a)."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2304_12745_b200 as U
+from oracle import oracle as O
+from _parity import assert_parity, rel_fro, report
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+LAM_OBJ_UF = 1.0 / 15.0
+
+
+def run(H, lam, eta, c, w0_mode=0, W0=None, mma=True):
+    old = os.environ.get("UFPGD_NO_MMA")
+    os.environ["UFPGD_NO_MMA"] = "0" if mma else "1"
+    try:
+        out = U.unfolded_forward(torch.from_numpy(np.ascontiguousarray(H)).cuda(), lam, eta, c, w0_mode=w0_mode,
+                                 W0=None if W0 is None else torch.from_numpy(np.ascontiguousarray(W0)).cuda(),
+                                 want_per_realization=True)
+        torch.cuda.synchronize()
+    finally:
+        if old is None:
+            os.environ.pop("UFPGD_NO_MMA", None)
+        else:
+            os.environ["UFPGD_NO_MMA"] = old
+    return {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
+
+
+@pytest.mark.parametrize("cfg,n", [(4, 512), (5, 2048)])
+def test_mma_parity_and_tile_agreement(cfg, n):
+    w = U.CONFIGS[cfg]
+    H = U.make_inputs(w, 0, n)
+    lam, eta = w.layer_params()
+    g = run(H, lam, eta, w.c)
+    t = run(H, lam, eta, w.c, mma=False)
+    ora = O.forward_batch_f32(H, w.c, lam, eta, w0_mode=w.w0_mode)
+    rep = report(H, g["W"], ora, w.c, LAM_OBJ_UF)
+    print(f"cfg{cfg} mma: rel max {rep['rel_max']:.2e} obj {rep['obj_max']:.2e}")
+    assert_parity(rep)
+    # FP32-class accuracy, not just inside the bar: the 3-term f16 split is ~2^-22
+    assert rep["rel_max"] < 5e-6
+    assert rel_fro(g["W"], t["W"].astype(np.complex128)).max() < 5e-6
+    assert np.all(g["diverged_at"] == -1)
+    np.testing.assert_array_equal(g["active"], t["active"])
+    np.testing.assert_allclose(g["l21"], t["l21"], rtol=5e-6)
+
+
+@pytest.mark.parametrize("K,M", [(16, 128), (32, 256)])
+@pytest.mark.parametrize("w0_mode", [U.W0_CONJ_H, U.W0_GIVEN])
+def test_mma_w0_modes(K, M, w0_mode):
+    w = U.CONFIGS[4 if K == 32 else 5]
+    H = U.make_inputs(w, 7, 64)
+    lam, eta = w.layer_params()
+    rng = np.random.default_rng(3)
+    W0 = None
+    if w0_mode == U.W0_GIVEN:
+        W0 = (0.05 * (rng.standard_normal(H.shape) + 1j * rng.standard_normal(H.shape))).astype(np.complex64)
+    g = run(H, lam, eta, w.c, w0_mode=w0_mode, W0=W0)
+    ora = O.forward_batch_f32(H, w.c, lam, eta, w0_mode=w0_mode, W0=W0)
+    assert_parity(report(H, g["W"], ora, w.c, LAM_OBJ_UF))
+
+
+@pytest.mark.parametrize("K,M", [(16, 128), (32, 256)])
+@pytest.mark.parametrize("s", [-40, 40])
+def test_mma_power_of_two_scale_equivariance(K, M, s):
+    """H * 2^s with eta * 2^-2s and lambda * 2^s gives W * 2^-s bit-exactly:
+    channels far outside the f16 range (|H| ~ 1e12 or 1e-12) run like unit
+    ones, so the f16 split never overflows or flushes."""
+    w = U.CONFIGS[4 if K == 32 else 5]
+    H = U.make_inputs(w, 11, 16)
+    lam, eta = w.layer_params()
+    a = 2.0 ** s
+    g0 = run(H, lam, eta, w.c)
+    gs = run((H * np.float32(a)).astype(np.complex64), lam * a, eta / (a * a), w.c)
+    assert np.all(gs["diverged_at"] == -1)
+    np.testing.assert_array_equal(gs["W"], (g0["W"] * np.float32(1 / a)).astype(np.complex64))
+
+
+def test_mma_nonfinite_channel_isolated():
+    w = U.CONFIGS[4]
+    H = U.make_inputs(w, 0, 8)
+    lam, eta = w.layer_params()
+    clean = run(H, lam, eta, w.c)
+    Hb = H.copy()
+    Hb[3, 17, 5] = np.complex64(complex(np.nan, 0.0))
+    Hb[5, 200, 31] = np.complex64(complex(np.inf, 1.0))
+    g = run(Hb, lam, eta, w.c)
+    assert g["diverged_at"][3] == 0 and g["diverged_at"][5] == 0
+    ok = [i for i in range(8) if i not in (3, 5)]
+    assert np.all(g["diverged_at"][ok] == -1)
+    np.testing.assert_array_equal(g["W"][ok], clean["W"][ok])

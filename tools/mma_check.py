@@ -88,6 +88,10 @@ def timing(cfg=4, n=16384, reps=3):
 
 if __name__ == "__main__":
     what = sys.argv[1:] or ["one", "cfg4", "time"]
+    if what[0] == "prof":  # one launch per config for ncu (-k regex:mma_kernel)
+        for c in what[1:]:
+            timing(int(c), 16384 if c == "4" else 65536, reps=1)
+        sys.exit(0)
     if "one" in what:
         one_layer(32, 256)
         one_layer(16, 128)
