@@ -57,14 +57,19 @@ struct MmaShape {
   static constexpr int OFF_BH = OFF_W + Q * M * 2;       // Bs hi [R x R] f16, boff()
   static constexpr int OFF_BL = OFF_BH + R * R * 2;      // Bs lo
   static constexpr int FSTR = R + 4;                     // fp32 exchange rows (floats), conflict-free LDS/STS.128
-  static constexpr int OFF_F = OFF_BL + R * R * 2;       // F [R][FSTR]: hi rows of P
-  static constexpr int OFF_G = OFF_F + R * FSTR * 4;     // G [R][FSTR]: lo rows of P
-  static constexpr int OFF_BAR = OFF_G + R * FSTR * 4;   // mbarriers, TMEM slot, reductions
+  // F [R][FSTR] (hi rows of P) and G (lo rows) alias the W operand: they are
+  // written after the stage-1 MMAs retire and read before W is rewritten.
+  static constexpr int OFF_F = OFF_W;
+  static constexpr int OFF_G = OFF_F + R * FSTR * 4;
+  static_assert(2 * R * FSTR * 4 <= Q * M * 2, "");
+  static constexpr int OFF_BAR = OFF_BL + R * R * 2;     // mbarriers, TMEM slot, reductions
   static constexpr int SMEM = OFF_BAR + 256;
   // TMEM columns (fp32 accumulators)
-  // D1: [X-part with H_hi | with H_lo] (2R); D2 per tile t: [main | corr] at T_D2 + 2R t
-  static constexpr uint32_t T_D1A = 0, T_D1B = R, T_D2 = 2 * R;
-  static constexpr uint32_t T_USED = 2 * R + 2 * NTILE * R;
+  // D1: [X-part with H_hi | with H_lo] (2R); D2 per tile t: [main | corr] at T_D2 + 2R t.
+  // D1 and D2 share columns: D1 is drained (E1) before the stage-2 MMAs and
+  // D2 (E2) before the next stage-1 MMAs, each behind a CTA barrier.
+  static constexpr uint32_t T_D1A = 0, T_D1B = R, T_D2 = 0;
+  static constexpr uint32_t T_USED = 2 * NTILE * R;
   static constexpr uint32_t T_COLS = T_USED <= 32 ? 32 : T_USED <= 64 ? 64 : T_USED <= 128 ? 128 : T_USED <= 256 ? 256 : 512;
   static_assert(T_USED <= 512, "");
 
@@ -491,7 +496,10 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
 }
 
 using Mma_32_256 = MmaShape<32, 256, 1>;
-using Mma_16_128 = MmaShape<16, 128, 4>;
+#ifndef UFPGD_MMA16_MINB
+#define UFPGD_MMA16_MINB 4
+#endif
+using Mma_16_128 = MmaShape<16, 128, UFPGD_MMA16_MINB>;
 
 template <class T>
 cudaError_t launch_mma_t(const FusedArgs& a, cudaStream_t s, long long* nblocks) {

@@ -6,7 +6,7 @@ name=$1; shift
 cd "$(dirname "$0")/.."
 mkdir -p tools/ablib/$name build/obj/ab/$name
 objs=""
-for f in team team64 tile general metrics grad datagen probe; do
+for f in team team64 tile mma general metrics grad datagen probe; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++20 -Xcompiler -fPIC -Iinclude \
     -Ipaper_2304_12745_b200/csrc "$@" -Xptxas -v -c paper_2304_12745_b200/csrc/$f.cu \
     -o build/obj/ab/$name/$f.o 2> build/obj/ab/$name/$f.log &
@@ -15,4 +15,4 @@ done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o tools/ablib/$name/libufpgd_gpu.so \
   $objs build/obj/capi.o build/obj/host_gen.o build/obj/api.o build/obj/dataset_io.o build/obj/host_util.o -ldl -lpthread
-grep -A2 "fused_kernelINS0_4TeamILi8ELi64" build/obj/ab/$name/team.log | grep -oE "Used [0-9]+ registers|[0-9]+ bytes spill stores" | tr '\n' ' '; echo " [$name]"
+grep -A2 "${AB_GREP:-fused_kernelINS0_4TeamILi8ELi64}" build/obj/ab/$name/${AB_LOG:-team}.log | grep -oE "Used [0-9]+ registers|[0-9]+ bytes spill stores" | tr '\n' ' '; echo " [$name]"
