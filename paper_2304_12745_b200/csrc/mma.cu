@@ -501,433 +501,6 @@ using Mma_32_256 = MmaShape<32, 256, 1>;
 #endif
 using Mma_16_128 = MmaShape<16, 128, UFPGD_MMA16_MINB>;
 
-// ---------------------------------------------------------------------------
-// CTA-pair variant for (32, 256): a cluster of 2 CTAs shares one realization,
-// CTA r owning antennas [128 r, 128 r + 128) (its H, its W operand, its
-// stage-2 tile). Stage 1 is split-K over the pair: each CTA's MMAs reduce over
-// its own 128 antennas, and the Bs builder adds the peer's partial residual
-// rows through distributed shared memory (ld.shared::cluster). A CTA needs 80 KB
-// of shared memory and 128 TMEM columns, so two pairs' CTAs share an SM and
-// one realization's epilogue runs while the other's MMAs do — the single-CTA
-// kernel above leaves the tensor pipe idle during its own epilogues.
-// Cluster barrier protocol (every thread, in this order):
-//   start: amax exchange | per layer with stage 1: [wait B] W operand write
-//   (it aliases F) ... E1 -> arrive+wait A (peer F ready) -> Bs build reads
-//   peer F -> arrive B (done reading) | end: [wait B], stats to CTA 0, arrive+wait.
-// ---------------------------------------------------------------------------
-template <int K_, int M_>
-struct MmaPairShape {
-  static constexpr int K = K_, MG = M_, M = M_ / 2, NT = M_ / 2;  // M: antennas per CTA
-  static constexpr int R = 2 * K, Q = 2 * R, NW = NT / 32;
-  static_assert(M == 128 && Q == 128, "pair kernel: one 128-antenna tile per CTA, stage-1 M = 128");
-  static constexpr int OFF_HH = 0;
-  static constexpr int OFF_HL = OFF_HH + R * M * 2;
-  static constexpr int OFF_W = OFF_HL + R * M * 2;      // [W_hi; W_lo] [Q x M]
-  static constexpr int OFF_BH = OFF_W + Q * M * 2;
-  static constexpr int OFF_BL = OFF_BH + R * R * 2;
-  static constexpr int FSTR = R + 4;
-  static constexpr int OFF_F = OFF_W;                    // partial P [R][FSTR] fp32, aliases W
-  static_assert(R * FSTR * 4 <= Q * M * 2, "");
-  static constexpr int OFF_BAR = OFF_BL + R * R * 2;
-  static constexpr int SMEM = OFF_BAR + 256;
-  static constexpr uint32_t T_D1A = 0, T_D1B = R, T_D2 = 0, T_COLS = 2 * R;  // D1 / D2 aliased
-  static __device__ __forceinline__ int hoff(int r, int m) {
-    return (r >> 3) * (16 * M) + (m >> 3) * 128 + (r & 7) * 16 + (m & 7) * 2;
-  }
-  static __device__ __forceinline__ int woff(int q, int m) {
-    return (m >> 3) * (16 * Q) + (q >> 3) * 128 + (m & 7) * 16 + (q & 7) * 2;
-  }
-  static __device__ __forceinline__ int boff(int kk, int n) {
-    return (kk >> 3) * 128 + (n >> 3) * (16 * R) + (n & 7) * 16 + (kk & 7) * 2;
-  }
-};
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
-  uint32_t d;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(saddr), "r"(rank));
-  return d;
-}
-__device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
-__device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
-__device__ __forceinline__ float4 ld_cluster4(uint32_t a) {
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(a)
-               : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_cluster_f32(uint32_t a, float v) {
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
-}
-__device__ __forceinline__ void st_cluster_s64(uint32_t a, long long v) {
-  asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
-}
-
-template <class T>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T::NT, 2)
-    mma_pair_kernel(const __grid_constant__ FusedArgs p) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int K = T::K, M = T::M, R = T::R, Q = T::Q;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
-  const long long rid = blockIdx.x >> 1;
-  const uint32_t sb = smem_u32(smem);
-  const uint32_t bar1 = sb + T::OFF_BAR, bar2 = sb + T::OFF_BAR + 8;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + T::OFF_BAR + 16);
-  float* red = reinterpret_cast<float*>(smem + T::OFF_BAR + 32);           // [0..7] local, [8..15] flags
-  float* xch = reinterpret_cast<float*>(smem + T::OFF_BAR + 96);           // peer-written: amax, bad, l21, act
-  long long* xfb = reinterpret_cast<long long*>(smem + T::OFF_BAR + 128);  // peer-written first_bad
-  long long* fbs = reinterpret_cast<long long*>(smem + T::OFF_BAR + 160);  // [4]
-
-  if (tid == 0) {
-    mbar_init(bar1, 1);
-    mbar_init(bar2, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                 "n"(T::T_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  cl_arrive();  // both CTAs running before any distributed shared memory access
-  cl_wait();
-
-  const int m = tid, mg = static_cast<int>(rank) * M + tid;  // local / global antenna
-  float4 hv[K / 2];
-  {
-    const float4* hg = reinterpret_cast<const float4*>(p.H + (rid * T::MG + mg) * K);
-#pragma unroll
-    for (int j = 0; j < K / 2; ++j) hv[j] = ldg_stream(hg + j);
-  }
-  float amax = 0.f;
-  bool bad = false;
-#pragma unroll
-  for (int j = 0; j < K / 2; ++j) {
-    amax = fmaxf(amax, fmaxf(fmaxf(fabsf(hv[j].x), fabsf(hv[j].y)), fmaxf(fabsf(hv[j].z), fabsf(hv[j].w))));
-    bad |= !(fabsf(hv[j].x) + fabsf(hv[j].y) + fabsf(hv[j].z) + fabsf(hv[j].w) <= FLT_MAX);
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(kFull, amax, off));
-  const unsigned anybad = __ballot_sync(kFull, bad);
-  if (lane == 0) {
-    red[warp] = amax;
-    red[8 + warp] = anybad ? 1.f : 0.f;
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tslot;
-  float gmax = 0.f, gbad = 0.f;
-#pragma unroll
-  for (int w = 0; w < T::NW; ++w) {
-    gmax = fmaxf(gmax, red[w]);
-    gbad = fmaxf(gbad, red[8 + w]);
-  }
-  if (tid == 0) {  // to the peer; both then take the max of the two
-    st_cluster_f32(mapa(smem_u32(xch), peer), gmax);
-    st_cluster_f32(mapa(smem_u32(xch + 1), peer), gbad);
-  }
-  cl_arrive();
-  cl_wait();
-  gmax = fmaxf(gmax, xch[0]);
-  gbad = fmaxf(gbad, xch[1]);
-  float g = 1.f;
-  if (gbad == 0.f && gmax > 0.f) g = ldexpf(1.f, -ilogbf(gmax));
-  const float ginv = 1.f / g;
-
-#pragma unroll
-  for (int j = 0; j < K / 2; ++j) {
-    const float vals[4] = {hv[j].x * g, hv[j].y * g, hv[j].z * g, hv[j].w * g};
-    const int rows[4] = {2 * j, K + 2 * j, 2 * j + 1, K + 2 * j + 1};
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const __half h = __float2half_rn(vals[u]);
-      const __half l = __float2half_rn((vals[u] - __half2float(h)) * 2048.f);
-      *reinterpret_cast<uint16_t*>(smem + T::OFF_HH + T::hoff(rows[u], m)) = f16_bits(h);
-      *reinterpret_cast<uint16_t*>(smem + T::OFF_HL + T::hoff(rows[u], m)) = f16_bits(l);
-    }
-  }
-  fence_async_smem();
-
-  float wr[K], wi[K];
-  if (p.w0_mode == UFPGD_W0_CONJ_H) {
-#pragma unroll
-    for (int j = 0; j < K / 2; ++j) {
-      wr[2 * j] = hv[j].x * ginv;
-      wi[2 * j] = -hv[j].y * ginv;
-      wr[2 * j + 1] = hv[j].z * ginv;
-      wi[2 * j + 1] = -hv[j].w * ginv;
-    }
-  } else if (p.w0_mode == UFPGD_W0_GIVEN) {
-    const float4* wg0 = reinterpret_cast<const float4*>(p.W0 + (rid * T::MG + mg) * K);
-#pragma unroll
-    for (int j = 0; j < K / 2; ++j) {
-      const float4 v = wg0[j];
-      wr[2 * j] = v.x * ginv;
-      wi[2 * j] = v.y * ginv;
-      wr[2 * j + 1] = v.z * ginv;
-      wi[2 * j + 1] = v.w * ginv;
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < K; ++k) wr[k] = wi[k] = 0.f;
-  }
-
-  constexpr uint32_t IDESC1 = idesc_f16_amn<Q, 2 * R>();
-  constexpr uint32_t IDESC2W = idesc_f16_amn<128, 2 * R>();
-  constexpr uint32_t IDESC2 = idesc_f16_amn<128, R>();
-  float* F = reinterpret_cast<float*>(smem + T::OFF_F);
-  const uint32_t Fpeer = mapa(sb + T::OFF_F, peer);
-  uint32_t ph1 = 0, ph2 = 0;
-  bool pending = false;  // an arrive on barrier B (done reading the peer's F) awaits its wait
-  bool nonfinite = false;
-  long long first_bad = -1;
-  float l21 = 0.f;
-  int act = 0;
-  const float g2inv = ginv * ginv;
-  const uint32_t lrow = static_cast<uint32_t>(warp * 32) << 16;
-
-  for (long long l = 0; l < p.L; ++l) {
-    const bool xzero = (l == 0 && p.w0_mode == UFPGD_W0_ZERO);
-    const float ts = p.thr[l] * ginv;
-    const float fstep = -p.eta[l] * g2inv;
-    if (!xzero) {
-      if (pending) {  // the peer has finished reading F (aliased by the W operand)
-        cl_wait();
-        pending = false;
-      }
-#pragma unroll
-      for (int grp = 0; grp < R / 8; ++grp) {
-        const float* src = grp < K / 8 ? wr + 8 * grp : wi + 8 * (grp - K / 8);
-        uint32_t h[4], lo[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) split2(src[2 * u], src[2 * u + 1], h[u], lo[u]);
-        *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(8 * grp, m)) = make_uint4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(R + 8 * grp, m)) =
-            make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      }
-      fence_async_smem();
-      tc_fence_before();
-      __syncthreads();
-      if (tid == 0) {
-        tc_fence_after();
-#pragma unroll 1
-        for (int ks = 0; ks < M / 16; ++ks) {
-          const uint64_t a = sdesc(sb + T::OFF_W + ks * 2 * 16 * Q, 16 * Q, 128);
-          umma_f16(tmem + T::T_D1A, a, sdesc(sb + T::OFF_HH + ks * 256, 128, 16 * M), IDESC1, ks > 0);
-        }
-        umma_commit(bar1);
-      }
-      mbar_wait(bar1, ph1);
-      ph1 ^= 1;
-      tc_fence_after();
-      // warp w = quadrant (hilo, part): hi warps write P rows = D1a + 2^-11 D1b,
-      // lo warps add 2^-11 D1a after a barrier (one fp32 buffer, no G)
-      const int part = warp & 1;
-      float* dst = F + (part * K + lane) * T::FSTR;
-      float keep[R];
-#pragma unroll
-      for (int cq = 0; cq < R; cq += 16) {
-        float a[16], b[16];
-        tmem_ld16(tmem + lrow + T::T_D1A + cq, a);
-        if (warp < 2) tmem_ld16(tmem + lrow + T::T_D1B + cq, b);
-        tmem_wait<16>(a);
-        if (warp < 2) {
-          tmem_wait<16>(b);
-#pragma unroll
-          for (int i = 0; i < 16; i += 4)
-            *reinterpret_cast<float4*>(dst + cq + i) =
-                make_float4(fmaf(kLoScale, b[i], a[i]), fmaf(kLoScale, b[i + 1], a[i + 1]),
-                            fmaf(kLoScale, b[i + 2], a[i + 2]), fmaf(kLoScale, b[i + 3], a[i + 3]));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) keep[cq + i] = a[i] * kLoScale;
-        }
-      }
-      tc_fence_before();
-      __syncthreads();
-      if (warp >= 2) {
-#pragma unroll
-        for (int i = 0; i < R; i += 4) {
-          float4 v = *reinterpret_cast<const float4*>(dst + i);
-          v.x += keep[i];
-          v.y += keep[i + 1];
-          v.z += keep[i + 2];
-          v.w += keep[i + 3];
-          *reinterpret_cast<float4*>(dst + i) = v;
-        }
-      }
-      cl_arrive();  // my partial P complete; the peer's too after the wait
-      cl_wait();
-    }
-    constexpr int NCH = K * K / 4;
-#pragma unroll
-    for (int ch = tid; ch < NCH; ch += T::NT) {
-      const int k = ch / (K / 4), c = (ch % (K / 4)) * 4;
-      float xr[4] = {0.f, 0.f, 0.f, 0.f}, xi[4] = {0.f, 0.f, 0.f, 0.f};
-      if (!xzero) {
-        const int o0 = k * T::FSTR, o1 = (K + k) * T::FSTR;
-        // P = own + peer partial (the same sum, in the same order of operands,
-        // in both CTAs: fp32 addition commutes, so both build identical Bs)
-        float4 a00 = *reinterpret_cast<const float4*>(F + o0 + c);
-        float4 a11 = *reinterpret_cast<const float4*>(F + o1 + K + c);
-        float4 a01 = *reinterpret_cast<const float4*>(F + o0 + K + c);
-        float4 a10 = *reinterpret_cast<const float4*>(F + o1 + c);
-        const float4 b00 = ld_cluster4(Fpeer + 4 * (o0 + c));
-        const float4 b11 = ld_cluster4(Fpeer + 4 * (o1 + K + c));
-        const float4 b01 = ld_cluster4(Fpeer + 4 * (o0 + K + c));
-        const float4 b10 = ld_cluster4(Fpeer + 4 * (o1 + c));
-        xr[0] = (a00.x + b00.x) - (a11.x + b11.x);
-        xr[1] = (a00.y + b00.y) - (a11.y + b11.y);
-        xr[2] = (a00.z + b00.z) - (a11.z + b11.z);
-        xr[3] = (a00.w + b00.w) - (a11.w + b11.w);
-        xi[0] = (a01.x + b01.x) + (a10.x + b10.x);
-        xi[1] = (a01.y + b01.y) + (a10.y + b10.y);
-        xi[2] = (a01.z + b01.z) + (a10.z + b10.z);
-        xi[3] = (a01.w + b01.w) + (a10.w + b10.w);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (c + u == k) xr[u] -= p.c[k];
-        xr[u] *= fstep;
-        xi[u] *= fstep;
-      }
-      uint32_t rh[2], rl[2], nh[2], nl[2], ih[2], il[2];
-      split2(xr[0], xr[1], rh[0], rl[0]);
-      split2(xr[2], xr[3], rh[1], rl[1]);
-      split2(-xr[0], -xr[1], nh[0], nl[0]);
-      split2(-xr[2], -xr[3], nh[1], nl[1]);
-      split2(xi[0], xi[1], ih[0], il[0]);
-      split2(xi[2], xi[3], ih[1], il[1]);
-      *reinterpret_cast<uint2*>(smem + T::OFF_BH + T::boff(c, k)) = make_uint2(rh[0], rh[1]);
-      *reinterpret_cast<uint2*>(smem + T::OFF_BL + T::boff(c, k)) = make_uint2(rl[0], rl[1]);
-      *reinterpret_cast<uint2*>(smem + T::OFF_BH + T::boff(K + c, k)) = make_uint2(ih[0], ih[1]);
-      *reinterpret_cast<uint2*>(smem + T::OFF_BL + T::boff(K + c, k)) = make_uint2(il[0], il[1]);
-      *reinterpret_cast<uint2*>(smem + T::OFF_BH + T::boff(c, K + k)) = make_uint2(ih[0], ih[1]);
-      *reinterpret_cast<uint2*>(smem + T::OFF_BL + T::boff(c, K + k)) = make_uint2(il[0], il[1]);
-      *reinterpret_cast<uint2*>(smem + T::OFF_BH + T::boff(K + c, K + k)) = make_uint2(nh[0], nh[1]);
-      *reinterpret_cast<uint2*>(smem + T::OFF_BL + T::boff(K + c, K + k)) = make_uint2(nl[0], nl[1]);
-    }
-    if (!xzero) {
-      cl_arrive();  // done reading the peer's F
-      pending = true;
-    }
-    fence_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-#pragma unroll
-      for (int ks = 0; ks < R / 16; ++ks) {
-        const uint64_t ah = sdesc(sb + T::OFF_HH + ks * 2 * 16 * M, 16 * M, 128);
-        const uint64_t al = sdesc(sb + T::OFF_HL + ks * 2 * 16 * M, 16 * M, 128);
-        const uint64_t bh = sdesc(sb + T::OFF_BH + ks * 256, 128, 16 * R);
-        umma_f16(tmem + T::T_D2, ah, bh, IDESC2W, ks > 0);
-        umma_f16(tmem + T::T_D2 + R, al, bh, IDESC2, 1);
-      }
-      umma_commit(bar2);
-    }
-    mbar_wait(bar2, ph2);
-    ph2 ^= 1;
-    tc_fence_after();
-#pragma unroll
-    for (int part = 0; part < 2; ++part) {
-      float* w = part == 0 ? wr : wi;
-#pragma unroll
-      for (int k0 = 0; k0 < K; k0 += 16) {
-        float a[16], b[16];
-        tmem_ld16(tmem + lrow + T::T_D2 + part * K + k0, a);
-        tmem_ld16(tmem + lrow + T::T_D2 + R + part * K + k0, b);
-        tmem_wait<16>(a);
-        tmem_wait<16>(b);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) w[k0 + i] += fmaf(kLoScale, b[i], a[i]);
-      }
-    }
-    tc_fence_before();
-    float s2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < K; ++k) s2 = fmaf(wr[k], wr[k], fmaf(wi[k], wi[k], s2));
-    nonfinite |= !(s2 * (g * g) <= FLT_MAX);
-    const bool on = s2 > ts * ts;
-    const float r = rsqrt_ftz(fmaxf(s2, FLT_MIN));
-    const float scale = on ? fmaf(-ts, r, 1.f) : 0.f;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      wr[k] *= scale;
-      wi[k] *= scale;
-    }
-    if (l + 1 == p.L && on) {
-      l21 += g * fmaf(s2, r, -ts);
-      act += 1;
-    }
-    if (nonfinite && first_bad < 0) first_bad = l;
-  }
-
-  {
-    float4* wg = reinterpret_cast<float4*>(p.W + (rid * T::MG + mg) * K);
-#pragma unroll
-    for (int j = 0; j < K / 2; ++j)
-      stg_stream(wg + j, make_float4(wr[2 * j] * g, wi[2 * j] * g, wr[2 * j + 1] * g, wi[2 * j + 1] * g));
-  }
-  long long fb = first_bad < 0 ? LLONG_MAX : first_bad;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    fb = min(fb, __shfl_xor_sync(kFull, fb, off));
-    l21 += __shfl_xor_sync(kFull, l21, off);
-    act += __shfl_xor_sync(kFull, act, off);
-  }
-  if (lane == 0) {
-    fbs[warp] = fb;
-    red[warp] = l21;
-    red[8 + warp] = static_cast<float>(act);
-  }
-  if (pending) cl_wait();
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(T::T_COLS) : "memory");
-  }
-  if (tid == 0) {
-    for (int w = 1; w < T::NW; ++w) {
-      fb = min(fb, fbs[w]);
-      l21 += red[w];
-      act += static_cast<int>(red[8 + w]);
-    }
-    if (rank == 1) {  // CTA 1's sums to CTA 0
-      st_cluster_f32(mapa(smem_u32(xch + 2), 0), l21);
-      st_cluster_f32(mapa(smem_u32(xch + 3), 0), static_cast<float>(act));
-      st_cluster_s64(mapa(smem_u32(xfb), 0), fb);
-    }
-  }
-  cl_arrive();
-  cl_wait();
-  if (tid == 0 && rank == 0) {
-    fb = min(fb, *xfb);
-    l21 += xch[2];
-    act += static_cast<int>(xch[3]);
-    const bool diverged = fb != LLONG_MAX;
-    if (p.diverged_at) p.diverged_at[rid] = diverged ? static_cast<int32_t>(fb) : -1;
-    if (p.l21) p.l21[rid] = diverged ? __int_as_float(0x7fc00000) : l21;
-    if (p.active) p.active[rid] = diverged ? -1 : act;
-    if (p.block_partials) {
-      p.block_partials[rid * 3 + 0] = diverged ? 0.0 : static_cast<double>(p.alpha) * l21;
-      p.block_partials[rid * 3 + 1] = diverged ? 0.0 : static_cast<double>(act);
-      p.block_partials[rid * 3 + 2] = diverged ? 1.0 : 0.0;
-    }
-  }
-}
-
-using MmaPair_32_256 = MmaPairShape<32, 256>;
-
 template <class T>
 cudaError_t launch_mma_t(const FusedArgs& a, cudaStream_t s, long long* nblocks) {
   auto kern = mma_kernel<T>;
@@ -950,20 +523,7 @@ bool mma_supported(int K, int M, bool pgd) {
 }
 
 cudaError_t launch_mma(const FusedArgs& a, int K, int M, cudaStream_t s, long long* nblocks) {
-  if (K == 32 && M == 256) {
-    const char* v = std::getenv("UFPGD_MMA_PAIR");
-    if (v && v[0] == '1') {  // CTA-pair (cluster) kernel: measured slower (10.6 vs 8.3 ms), opt-in only
-      using T = MmaPair_32_256;
-      auto kern = mma_pair_kernel<T>;
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
-      if (e != cudaSuccess) return e;
-      if (nblocks) *nblocks = a.B;
-      if (a.B == 0) return cudaSuccess;
-      kern<<<static_cast<unsigned>(2 * a.B), T::NT, T::SMEM, s>>>(a);
-      return cudaGetLastError();
-    }
-    return launch_mma_t<Mma_32_256>(a, s, nblocks);
-  }
+  if (K == 32 && M == 256) return launch_mma_t<Mma_32_256>(a, s, nblocks);
   if (K == 16 && M == 128) return launch_mma_t<Mma_16_128>(a, s, nblocks);
   return cudaErrorInvalidValue;
 }
