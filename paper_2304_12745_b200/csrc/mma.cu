@@ -38,18 +38,20 @@
 namespace ufpgd_gpu_impl {
 namespace {
 
-// Shape of the tensor-core kernel: one thread per antenna (NT = M), 2K
+// Shape of the tensor-core kernel: US threads per antenna (NT = US M; thread
+// tid owns antenna tid % M and users [h K/US, (h+1) K/US), h = tid / M), 2K
 // real-form rows r = (part, k), Q = 4K operand rows q = (hilo, part, k) for
 // stage 1 (MMA M = Q: 128 at K = 32, 64 at K = 16), M / 128 stage-2 tiles.
-template <int K_, int M_, int MINB_>
+template <int K_, int M_, int MINB_, int US_ = 1>
 struct MmaShape {
-  static constexpr int K = K_, M = M_, NT = M_, MINB = MINB_;
+  static constexpr int K = K_, M = M_, US = US_, NT = US_ * M_, MINB = MINB_;
+  static constexpr int KH = K / US;   // users per thread
   static constexpr int R = 2 * K;     // real-form rows (part, k)
   static constexpr int Q = 2 * R;     // stage-1 A rows (hilo, part, k) = stage-1 MMA M
   static constexpr int NTILE = M / 128;
   static constexpr int NW = NT / 32;
   static_assert(Q == 64 || Q == 128, "stage-1 MMA M must be 64 or 128");
-  static_assert(M % 128 == 0 && NW <= 8 && K % 16 == 0, "");
+  static_assert(M % 128 == 0 && NW <= 16 && K % 16 == 0 && (US == 1 || US == 2) && KH % 16 == 0, "");
   // shared-memory byte offsets (all 1024-aligned)
   static constexpr int OFF_HH = 0;                       // H hi  [R x M] f16, core layout hoff()
   static constexpr int OFF_HL = OFF_HH + R * M * 2;      // H lo
@@ -63,11 +65,14 @@ struct MmaShape {
   static constexpr int OFF_G = OFF_F + R * FSTR * 4;
   static_assert(2 * R * FSTR * 4 <= Q * M * 2, "");
   static constexpr int OFF_BAR = OFF_BL + R * R * 2;     // mbarriers, TMEM slot, reductions
-  static constexpr int SMEM = OFF_BAR + 256;
+  static constexpr int OFF_NRM = OFF_BAR + 512;          // US > 1: partial column norms [US][M]
+  static constexpr int SMEM = OFF_NRM + (US > 1 ? US * M * 4 : 0);
   // TMEM columns (fp32 accumulators)
-  // D1: [X-part with H_hi | with H_lo] (2R); D2 per tile t: [main | corr] at T_D2 + 2R t.
-  // D1 and D2 share columns: D1 is drained (E1) before the stage-2 MMAs and
-  // D2 (E2) before the next stage-1 MMAs, each behind a CTA barrier.
+  // D1 part t: [X-part with H_hi | with H_lo] (2R) over antenna tile t (stage 1 is
+  // split-K by tile so each tile's antennas start their MMAs as soon as their own
+  // W operand is written); D2 per tile t: [main | corr]. Both at column 2R t:
+  // tile t's threads drain D2 part t (E2) before issuing D1 part t, and D1 is
+  // drained (E1) behind a CTA barrier before the stage-2 MMAs.
   static constexpr uint32_t T_D1A = 0, T_D1B = R, T_D2 = 0;
   static constexpr uint32_t T_USED = 2 * NTILE * R;
   static constexpr uint32_t T_COLS = T_USED <= 32 ? 32 : T_USED <= 64 ? 64 : T_USED <= 128 ? 128 : T_USED <= 256 ? 256 : 512;
@@ -167,18 +172,20 @@ constexpr float kLoScale = 1.f / 2048.f;
 template <class T>
 __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_constant__ FusedArgs p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int K = T::K, M = T::M, R = T::R, Q = T::Q, NW = T::NW;
+  constexpr int K = T::K, M = T::M, R = T::R, Q = T::Q, NW = T::NW, KH = T::KH, US = T::US;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long rid = blockIdx.x;
   const uint32_t sb = smem_u32(smem);
-  const uint32_t bar1 = sb + T::OFF_BAR;  // stage 1 done; bar1 + 8 (1 + tile): stage-2 tile done
+  const uint32_t bar1 = sb + T::OFF_BAR;                // + 8 t: stage-1 part t done
+  const uint32_t bar2 = sb + T::OFF_BAR + 8 * T::NTILE;  // + 8 t: stage-2 tile t done
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + T::OFF_BAR + 48);
-  float* red = reinterpret_cast<float*>(smem + T::OFF_BAR + 64);           // [2][8]
-  long long* fbs = reinterpret_cast<long long*>(smem + T::OFF_BAR + 128);  // [8]
+  float* red = reinterpret_cast<float*>(smem + T::OFF_BAR + 64);           // [2][16]
+  long long* fbs = reinterpret_cast<long long*>(smem + T::OFF_BAR + 192);  // [16]
+  float* nrm = reinterpret_cast<float*>(smem + T::OFF_NRM);
 
   if (tid == 0) {
 #pragma unroll
-    for (int b = 0; b <= T::NTILE; ++b) mbar_init(bar1 + 8 * b, 1);
+    for (int b = 0; b < 2 * T::NTILE; ++b) mbar_init(bar1 + 8 * b, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -188,18 +195,18 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
 
-  // ---- H row of antenna m = tid: registers, max |.| over the realization ----
-  const int m = tid;
-  float4 hv[K / 2];  // hv[j] = (Re H(2j, m), Im H(2j, m), Re H(2j+1, m), Im H(2j+1, m))
+  // ---- H of antenna m, users [k0, k0 + KH): registers, max |.| over the realization ----
+  const int m = tid % M, hh = tid / M, k0 = hh * KH;
+  float4 hv[KH / 2];  // hv[j] = (Re H(k0+2j, m), Im H(k0+2j, m), Re H(k0+2j+1, m), Im H(k0+2j+1, m))
   {
-    const float4* hg = reinterpret_cast<const float4*>(p.H + (rid * M + m) * K);
+    const float4* hg = reinterpret_cast<const float4*>(p.H + (rid * M + m) * K + k0);
 #pragma unroll
-    for (int j = 0; j < K / 2; ++j) hv[j] = ldg_stream(hg + j);
+    for (int j = 0; j < KH / 2; ++j) hv[j] = ldg_stream(hg + j);
   }
   float amax = 0.f;
   bool bad = false;  // fmaxf drops NaN: a non-finite channel keeps g = 1 (and diverges at layer 0)
 #pragma unroll
-  for (int j = 0; j < K / 2; ++j) {
+  for (int j = 0; j < KH / 2; ++j) {
     const float a = fmaxf(fmaxf(fabsf(hv[j].x), fabsf(hv[j].y)), fmaxf(fabsf(hv[j].z), fabsf(hv[j].w)));
     amax = fmaxf(amax, a);
     bad |= !(fabsf(hv[j].x) + fabsf(hv[j].y) + fabsf(hv[j].z) + fabsf(hv[j].w) <= FLT_MAX);
@@ -209,7 +216,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
   const unsigned anybad = __ballot_sync(kFull, bad);
   if (lane == 0) {
     red[warp] = amax;
-    red[8 + warp] = anybad ? 1.f : 0.f;
+    red[16 + warp] = anybad ? 1.f : 0.f;
   }
   tc_fence_before();
   __syncthreads();
@@ -219,7 +226,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
     gmax = fmaxf(gmax, red[w]);
-    gbad = fmaxf(gbad, red[8 + w]);
+    gbad = fmaxf(gbad, red[16 + w]);
   }
   // g = 2^-e with gmax in [2^e, 2^(e+1)): g * gmax in [1, 2). Exact scaling.
   float g = 1.f;
@@ -228,9 +235,10 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
 
   // ---- stage H (hi / lo f16) in the shared core layout -------------------------
 #pragma unroll
-  for (int j = 0; j < K / 2; ++j) {
+  for (int j = 0; j < KH / 2; ++j) {
     const float vals[4] = {hv[j].x * g, hv[j].y * g, hv[j].z * g, hv[j].w * g};
-    const int rows[4] = {2 * j, K + 2 * j, 2 * j + 1, K + 2 * j + 1};  // Re k, Im k, Re k+1, Im k+1
+    const int kk = k0 + 2 * j;
+    const int rows[4] = {kk, K + kk, kk + 1, K + kk + 1};  // Re k, Im k, Re k+1, Im k+1
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const __half h = __float2half_rn(vals[u]);
@@ -241,20 +249,20 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
   }
   fence_async_smem();  // H is read by the tensor cores (async proxy)
 
-  // ---- W0 (scaled: W_s = W / g) in registers: wr[k], wi[k] for antenna m ------
-  float wr[K], wi[K];
+  // ---- W0 (scaled: W_s = W / g) in registers: wr[k], wi[k], users k0 + k ----
+  float wr[KH], wi[KH];
   if (p.w0_mode == UFPGD_W0_CONJ_H) {
 #pragma unroll
-    for (int j = 0; j < K / 2; ++j) {
+    for (int j = 0; j < KH / 2; ++j) {
       wr[2 * j] = hv[j].x * ginv;
       wi[2 * j] = -hv[j].y * ginv;
       wr[2 * j + 1] = hv[j].z * ginv;
       wi[2 * j + 1] = -hv[j].w * ginv;
     }
   } else if (p.w0_mode == UFPGD_W0_GIVEN) {
-    const float4* wg0 = reinterpret_cast<const float4*>(p.W0 + (rid * M + m) * K);
+    const float4* wg0 = reinterpret_cast<const float4*>(p.W0 + (rid * M + m) * K + k0);
 #pragma unroll
-    for (int j = 0; j < K / 2; ++j) {
+    for (int j = 0; j < KH / 2; ++j) {
       const float4 v = wg0[j];
       wr[2 * j] = v.x * ginv;
       wi[2 * j] = v.y * ginv;
@@ -263,7 +271,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     }
   } else {
 #pragma unroll
-    for (int k = 0; k < K; ++k) wr[k] = wi[k] = 0.f;
+    for (int k = 0; k < KH; ++k) wr[k] = wi[k] = 0.f;
   }
 
   constexpr uint32_t IDESC1 = idesc_f16_amn<Q, 2 * R>();
@@ -282,42 +290,62 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
   const int tile = m >> 7;
   const uint32_t lrow = static_cast<uint32_t>((warp & 3) * 32) << 16;  // this warp's TMEM lane quadrant
 
+#ifdef UFPGD_MMA_TIMING
+  // development probe: thread 0 of realization 5000 stamps the phases of layer 10
+  // into its own W output (a timing-only build; W is garbage there)
+  long long tst[10];
+  const bool probe = (rid == 5000 && tid == 0);
+#define TSTAMP(i) \
+  if (probe && l == 10) tst[i] = clock64();
+#else
+#define TSTAMP(i)
+#endif
   for (long long l = 0; l < p.L; ++l) {
+    TSTAMP(0)
     const bool xzero = (l == 0 && p.w0_mode == UFPGD_W0_ZERO);
     const float ts = p.thr[l] * ginv;       // threshold in the scaled domain
     const float fstep = -p.eta[l] * g2inv;  // -eta / g^2 folded into Bs
     if (!xzero) {
-      // W operand rows q = (hilo, part, k) from the thread's antenna column
+      // W operand rows q = (hilo, part, k), k in the thread's user range
 #pragma unroll
-      for (int grp = 0; grp < R / 8; ++grp) {  // 8 rows (part, k .. k+7)
-        const float* src = grp < K / 8 ? wr + 8 * grp : wi + 8 * (grp - K / 8);
+      for (int pg = 0; pg < 2 * (KH / 8); ++pg) {  // 8 rows (part, k .. k+7)
+        const int part = pg / (KH / 8), kg = pg % (KH / 8);
+        const float* src = (part == 0 ? wr : wi) + 8 * kg;
+        const int q0 = part * K + k0 + 8 * kg;
         uint32_t h[4], lo[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) split2(src[2 * u], src[2 * u + 1], h[u], lo[u]);
-        *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(8 * grp, m)) = make_uint4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(R + 8 * grp, m)) =
-            make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(q0, m)) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(R + q0, m)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
       fence_async_smem();
       tc_fence_before();
-      __syncthreads();
-      if (tid == 0) {
+      // tile group: its antennas' W rows are written and its D2 part drained
+      if (T::NTILE > 1) named_bar(1 + tile, T::NT / T::NTILE);
+      else __syncthreads();
+      TSTAMP(1)
+      if (tid == tile * 128) {  // US = 1: thread 128 t; US = 2: the hh = 0 thread of antenna 128 t
         tc_fence_after();
+        constexpr int KST = 128 / 16;  // K-steps per antenna tile
 #pragma unroll 1
-        for (int ks = 0; ks < M / 16; ++ks) {
+        for (int ks = tile * KST; ks < (tile + 1) * KST; ++ks) {
           // B = [H_hi | H_lo] (N = 2R: OFF_HL continues OFF_HH's N-group stride)
           const uint64_t a = sdesc(sb + T::OFF_W + ks * 2 * 16 * Q, 16 * Q, 128);
-          umma_f16(tmem + T::T_D1A, a, sdesc(sb + T::OFF_HH + ks * 256, 128, 16 * M), IDESC1, ks > 0);
+          umma_f16(tmem + tile * 2 * R + T::T_D1A, a, sdesc(sb + T::OFF_HH + ks * 256, 128, 16 * M), IDESC1,
+                   ks > tile * KST);
         }
-        umma_commit(bar1);
+        umma_commit(bar1 + 8 * tile);
       }
+      TSTAMP(2)
       // D1 rows q = (hilo, part, k): TMEM lane quadrant hilo * 2 + part, lane k
-      // (M = 128: lanes 32 q4 + k; M = 64: lanes 32 q4 + k for k < 16).
-      // Warp w reads quadrant w % 4, columns [w / 4 * CW, + CW).
+      // (M = 128: lanes 32 q4 + k; M = 64: lanes 32 q4 + k for k < 16), summed
+      // over the tile parts. Warp w reads quadrant w % 4, columns [w / 4 * CW, + CW).
       constexpr int CW = R * 4 / NW;
       const int quad = warp & 3, c0 = (warp >> 2) * CW, part = quad & 1;
-      mbar_wait(bar1, ph1);
+#pragma unroll
+      for (int t = 0; t < T::NTILE; ++t) mbar_wait(bar1 + 8 * t, ph1);
       ph1 ^= 1;
+      TSTAMP(3)
       tc_fence_after();
       float* dst = (quad < 2 ? F : G) + (part * K + lane) * T::FSTR + c0;
 #pragma unroll
@@ -326,8 +354,22 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
         tmem_ld16(tmem + lrow + T::T_D1A + c0 + cq, a);
         if (quad < 2) tmem_ld16(tmem + lrow + T::T_D1B + c0 + cq, b);
         tmem_wait<16>(a);
+        if (quad < 2) tmem_wait<16>(b);
+#pragma unroll
+        for (int t = 1; t < T::NTILE; ++t) {  // the other antenna tiles' partial sums, in tile order
+          float a2[16], b2[16];
+          tmem_ld16(tmem + lrow + t * 2 * R + T::T_D1A + c0 + cq, a2);
+          if (quad < 2) tmem_ld16(tmem + lrow + t * 2 * R + T::T_D1B + c0 + cq, b2);
+          tmem_wait<16>(a2);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) a[i] += a2[i];
+          if (quad < 2) {
+            tmem_wait<16>(b2);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) b[i] += b2[i];
+          }
+        }
         if (quad < 2) {
-          tmem_wait<16>(b);
 #pragma unroll
           for (int i = 0; i < 16; ++i) a[i] = fmaf(kLoScale, b[i], a[i]);  // hi rows: W_hi H_hi + W_hi H_lo
         } else {
@@ -342,6 +384,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
       }
       __syncthreads();
     }
+    TSTAMP(4)
     // Bs[(p_in, k')][(p_out, k)] = -eta/g^2 * { X'r, X'i ; X'i, -X'r }(k, k'), one
     // 4-wide chunk of X' row k per thread
     constexpr int NCH = K * K / 4;
@@ -393,6 +436,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     fence_async_smem();
     tc_fence_before();
     __syncthreads();
+    TSTAMP(5)
     if (tid == 0) {
       tc_fence_after();
 #pragma unroll 1
@@ -406,11 +450,13 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
           umma_f16(dm, ah, bh, IDESC2W, ks > 0);  // [main | corr] = H_hi [Bs_hi | Bs_lo]
           umma_f16(dc, al, bh, IDESC2, 1);        // corr += H_lo Bs_hi
         }
-        umma_commit(bar1 + 8 * (1 + t));  // each tile's epilogue starts as soon as its MMAs retire
+        umma_commit(bar2 + 8 * t);  // each tile's epilogue starts as soon as its MMAs retire
       }
     }
-    mbar_wait(bar1 + 8 * (1 + tile), ph2);
+    TSTAMP(6)
+    mbar_wait(bar2 + 8 * tile, ph2);
     ph2 ^= 1;
+    TSTAMP(7)
     tc_fence_after();
     {
       // antenna m: TMEM lane m % 128 (warp quadrant warp % 4), tile m / 128
@@ -420,14 +466,14 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
       for (int part = 0; part < 2; ++part) {
         float* w = part == 0 ? wr : wi;
 #pragma unroll
-        for (int k0 = 0; k0 < K; k0 += 16) {
+        for (int j0 = 0; j0 < KH; j0 += 16) {
           float a[16], b[16];
-          tmem_ld16(cm + part * K + k0, a);
-          tmem_ld16(cc + part * K + k0, b);
+          tmem_ld16(cm + part * K + k0 + j0, a);
+          tmem_ld16(cc + part * K + k0 + j0, b);
           tmem_wait<16>(a);
           tmem_wait<16>(b);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) w[k0 + i] += fmaf(kLoScale, b[i], a[i]);  // V = W - eta X' H^*
+          for (int i = 0; i < 16; ++i) w[j0 + i] += fmaf(kLoScale, b[i], a[i]);  // V = W - eta X' H^*
         }
       }
     }
@@ -435,29 +481,43 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     // prox_l21 on the antenna column (strict '>', pgd.cpp:237-244 / unfolded.cpp:135-143)
     float s2 = 0.f;
 #pragma unroll
-    for (int k = 0; k < K; ++k) s2 = fmaf(wr[k], wr[k], fmaf(wi[k], wi[k], s2));
+    for (int k = 0; k < KH; ++k) s2 = fmaf(wr[k], wr[k], fmaf(wi[k], wi[k], s2));
+    if constexpr (US > 1) {  // the antenna's users are split over US threads: combine in a fixed order
+      nrm[hh * M + m] = s2;
+      __syncthreads();
+      s2 = 0.f;
+#pragma unroll
+      for (int u = 0; u < US; ++u) s2 += nrm[u * M + m];
+    }
     nonfinite |= !(s2 * (g * g) <= FLT_MAX);
     const bool on = s2 > ts * ts;
     const float r = rsqrt_ftz(fmaxf(s2, FLT_MIN));
     const float scale = on ? fmaf(-ts, r, 1.f) : 0.f;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
+    for (int k = 0; k < KH; ++k) {
       wr[k] *= scale;
       wi[k] *= scale;
     }
-    if (l + 1 == p.L && on) {
+    if (l + 1 == p.L && on && hh == 0) {
       l21 += g * fmaf(s2, r, -ts);
       act += 1;
     }
     if (nonfinite && first_bad < 0) first_bad = l;
+    TSTAMP(8)
   }
 
   // ---- W out (unscaled), per-realization reductions ---------------------------
   {
-    float4* wg = reinterpret_cast<float4*>(p.W + (rid * M + m) * K);
+    float4* wg = reinterpret_cast<float4*>(p.W + (rid * M + m) * K + k0);
 #pragma unroll
-    for (int j = 0; j < K / 2; ++j)
+    for (int j = 0; j < KH / 2; ++j)
       stg_stream(wg + j, make_float4(wr[2 * j] * g, wi[2 * j] * g, wr[2 * j + 1] * g, wi[2 * j + 1] * g));
+#ifdef UFPGD_MMA_TIMING
+    if (probe) {
+      long long* o = reinterpret_cast<long long*>(p.W + rid * M * K);
+      for (int i = 0; i < 9; ++i) o[i] = tst[i];
+    }
+#endif
   }
   long long fb = first_bad < 0 ? LLONG_MAX : first_bad;
 #pragma unroll
@@ -469,7 +529,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
   if (lane == 0) {
     fbs[warp] = fb;
     red[warp] = l21;
-    red[8 + warp] = static_cast<float>(act);
+    red[16 + warp] = static_cast<float>(act);
   }
   tc_fence_before();
   __syncthreads();
@@ -481,7 +541,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     for (int w = 1; w < NW; ++w) {
       fb = min(fb, fbs[w]);
       l21 += red[w];
-      act += static_cast<int>(red[8 + w]);
+      act += static_cast<int>(red[16 + w]);
     }
     const bool diverged = fb != LLONG_MAX;
     if (p.diverged_at) p.diverged_at[rid] = diverged ? static_cast<int32_t>(fb) : -1;
@@ -495,11 +555,17 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
   }
 }
 
-using Mma_32_256 = MmaShape<32, 256, 1>;
+#ifndef UFPGD_MMA32_US
+#define UFPGD_MMA32_US 1
+#endif
+#ifndef UFPGD_MMA16_US
+#define UFPGD_MMA16_US 1
+#endif
+using Mma_32_256 = MmaShape<32, 256, 1, UFPGD_MMA32_US>;
 #ifndef UFPGD_MMA16_MINB
 #define UFPGD_MMA16_MINB 4
 #endif
-using Mma_16_128 = MmaShape<16, 128, UFPGD_MMA16_MINB>;
+using Mma_16_128 = MmaShape<16, 128, UFPGD_MMA16_MINB, UFPGD_MMA16_US>;
 
 template <class T>
 cudaError_t launch_mma_t(const FusedArgs& a, cudaStream_t s, long long* nblocks) {

@@ -88,6 +88,8 @@ def timing(cfg=4, n=16384, reps=3):
 
 if __name__ == "__main__":
     what = sys.argv[1:] or ["one", "cfg4", "time"]
+    if what[0] == "phases":
+        what = ["phases-only"]
     if what[0] == "prof":  # one launch per config for ncu (-k regex:mma_kernel)
         for c in what[1:]:
             timing(int(c), 16384 if c == "4" else 65536, reps=1)
@@ -100,3 +102,26 @@ if __name__ == "__main__":
     if "time" in what:
         timing(4, 16384)
         timing(5, 65536)
+
+
+def phase_probe(cfg):
+    """With a -DUFPGD_MMA_TIMING library (tools/ab_build.sh): clock64 stamps of
+    layer 10 of realization 5000, written into its W."""
+    w = U.CONFIGS[cfg]
+    n = 16384
+    Hd = torch.empty((n, w.M, w.K), dtype=torch.complex64, device="cuda")
+    U.generate_channels_device(w.seed_h, w.seed_g, w.gain_db, 0, n, w.K, w.M, out=Hd)
+    lam, eta = w.layer_params()
+    W = torch.empty_like(Hd)
+    for _ in range(2):
+        U.unfolded_forward(Hd, lam, eta, w.c, out=W)
+    torch.cuda.synchronize()
+    t = W[5000].view(torch.int64).flatten()[:9].cpu().numpy()
+    d = np.diff(t)
+    names = ["Wop+sync", "s1 issue", "s1 wait", "E1+sync", "Bs+sync", "s2 issue", "s2 wait", "E2+prox"]
+    print(f"cfg{cfg} layer clocks total {t[8] - t[0]}: " + ", ".join(f"{a} {b}" for a, b in zip(names, d)))
+
+
+if __name__ == "__main__" and sys.argv[1:2] == ["phases"]:
+    for c in sys.argv[2:]:
+        phase_probe(int(c))
