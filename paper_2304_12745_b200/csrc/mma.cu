@@ -31,6 +31,8 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include <type_traits>
+
 #include <cuda_fp16.h>
 
 #include "device_common.cuh"
@@ -387,51 +389,67 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     TSTAMP(4)
     // Bs[(p_in, k')][(p_out, k)] = -eta/g^2 * { X'r, X'i ; X'i, -X'r }(k, k'), one
     // 4-wide chunk of X' row k per thread
-    constexpr int NCH = K * K / 4;
+    // CWD-wide chunks of X' row k per thread (CWD = 4, or 2 when K / 4 chunks per
+    // row would leave threads idle; 2-wide keeps a quarter-warp on one F row)
+    constexpr int CWD = (K * K / 4 >= T::NT) ? 4 : 2, NCH = K * K / CWD, CPR = K / CWD;
+    using FV = typename std::conditional<CWD == 4, float4, float2>::type;
 #pragma unroll
     for (int ch = tid; ch < NCH; ch += T::NT) {
-      const int k = ch / (K / 4), c = (ch % (K / 4)) * 4;
-      float xr[4] = {0.f, 0.f, 0.f, 0.f}, xi[4] = {0.f, 0.f, 0.f, 0.f};
+      const int k = ch / CPR, c = (ch % CPR) * CWD;
+      float xr[CWD], xi[CWD];
+#pragma unroll
+      for (int u = 0; u < CWD; ++u) xr[u] = xi[u] = 0.f;
       if (!xzero) {
         const float* F0 = F + k * T::FSTR;        // P rows (0, k), (1, k): hi parts in F, lo in G
         const float* F1 = F + (K + k) * T::FSTR;
         const float* G0 = G + k * T::FSTR;
         const float* G1 = G + (K + k) * T::FSTR;
-        const float4 a00 = *reinterpret_cast<const float4*>(F0 + c), b00 = *reinterpret_cast<const float4*>(G0 + c);
-        const float4 a11 = *reinterpret_cast<const float4*>(F1 + K + c), b11 = *reinterpret_cast<const float4*>(G1 + K + c);
-        const float4 a01 = *reinterpret_cast<const float4*>(F0 + K + c), b01 = *reinterpret_cast<const float4*>(G0 + K + c);
-        const float4 a10 = *reinterpret_cast<const float4*>(F1 + c), b10 = *reinterpret_cast<const float4*>(G1 + c);
-        xr[0] = (a00.x + b00.x) - (a11.x + b11.x);
-        xr[1] = (a00.y + b00.y) - (a11.y + b11.y);
-        xr[2] = (a00.z + b00.z) - (a11.z + b11.z);
-        xr[3] = (a00.w + b00.w) - (a11.w + b11.w);
-        xi[0] = (a01.x + b01.x) + (a10.x + b10.x);
-        xi[1] = (a01.y + b01.y) + (a10.y + b10.y);
-        xi[2] = (a01.z + b01.z) + (a10.z + b10.z);
-        xi[3] = (a01.w + b01.w) + (a10.w + b10.w);
+        const FV a00 = *reinterpret_cast<const FV*>(F0 + c), b00 = *reinterpret_cast<const FV*>(G0 + c);
+        const FV a11 = *reinterpret_cast<const FV*>(F1 + K + c), b11 = *reinterpret_cast<const FV*>(G1 + K + c);
+        const FV a01 = *reinterpret_cast<const FV*>(F0 + K + c), b01 = *reinterpret_cast<const FV*>(G0 + K + c);
+        const FV a10 = *reinterpret_cast<const FV*>(F1 + c), b10 = *reinterpret_cast<const FV*>(G1 + c);
+        const float* A00 = reinterpret_cast<const float*>(&a00);
+        const float* B00 = reinterpret_cast<const float*>(&b00);
+        const float* A11 = reinterpret_cast<const float*>(&a11);
+        const float* B11 = reinterpret_cast<const float*>(&b11);
+        const float* A01 = reinterpret_cast<const float*>(&a01);
+        const float* B01 = reinterpret_cast<const float*>(&b01);
+        const float* A10 = reinterpret_cast<const float*>(&a10);
+        const float* B10 = reinterpret_cast<const float*>(&b10);
+#pragma unroll
+        for (int u = 0; u < CWD; ++u) {
+          xr[u] = (A00[u] + B00[u]) - (A11[u] + B11[u]);
+          xi[u] = (A01[u] + B01[u]) + (A10[u] + B10[u]);
+        }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < CWD; ++u) {
         if (c + u == k) xr[u] -= p.c[k];  // X' = X - diag(c)
         xr[u] *= fstep;
         xi[u] *= fstep;
       }
-      uint32_t rh[2], rl[2], nh[2], nl[2], ih[2], il[2];
-      split2(xr[0], xr[1], rh[0], rl[0]);
-      split2(xr[2], xr[3], rh[1], rl[1]);
-      split2(-xr[0], -xr[1], nh[0], nl[0]);
-      split2(-xr[2], -xr[3], nh[1], nl[1]);
-      split2(xi[0], xi[1], ih[0], il[0]);
-      split2(xi[2], xi[3], ih[1], il[1]);
+      uint32_t rh[CWD / 2], rl[CWD / 2], nh[CWD / 2], nl[CWD / 2], ih[CWD / 2], il[CWD / 2];
+#pragma unroll
+      for (int v = 0; v < CWD / 2; ++v) {
+        split2(xr[2 * v], xr[2 * v + 1], rh[v], rl[v]);
+        split2(-xr[2 * v], -xr[2 * v + 1], nh[v], nl[v]);
+        split2(xi[2 * v], xi[2 * v + 1], ih[v], il[v]);
+      }
       // (p_in, p_out) = (0,0): X'r, (1,0): X'i, (0,1): X'i, (1,1): -X'r
-      *reinterpret_cast<uint2*>(smem + T::OFF_BH + T::boff(c, k)) = make_uint2(rh[0], rh[1]);
-      *reinterpret_cast<uint2*>(smem + T::OFF_BL + T::boff(c, k)) = make_uint2(rl[0], rl[1]);
-      *reinterpret_cast<uint2*>(smem + T::OFF_BH + T::boff(K + c, k)) = make_uint2(ih[0], ih[1]);
-      *reinterpret_cast<uint2*>(smem + T::OFF_BL + T::boff(K + c, k)) = make_uint2(il[0], il[1]);
-      *reinterpret_cast<uint2*>(smem + T::OFF_BH + T::boff(c, K + k)) = make_uint2(ih[0], ih[1]);
-      *reinterpret_cast<uint2*>(smem + T::OFF_BL + T::boff(c, K + k)) = make_uint2(il[0], il[1]);
-      *reinterpret_cast<uint2*>(smem + T::OFF_BH + T::boff(K + c, K + k)) = make_uint2(nh[0], nh[1]);
-      *reinterpret_cast<uint2*>(smem + T::OFF_BL + T::boff(K + c, K + k)) = make_uint2(nl[0], nl[1]);
+      auto put = [&](int off, const uint32_t* v) {
+        if constexpr (CWD == 4)
+          *reinterpret_cast<uint2*>(smem + off) = make_uint2(v[0], v[1]);
+        else
+          *reinterpret_cast<uint32_t*>(smem + off) = v[0];
+      };
+      put(T::OFF_BH + T::boff(c, k), rh);
+      put(T::OFF_BL + T::boff(c, k), rl);
+      put(T::OFF_BH + T::boff(K + c, k), ih);
+      put(T::OFF_BL + T::boff(K + c, k), il);
+      put(T::OFF_BH + T::boff(c, K + k), ih);
+      put(T::OFF_BL + T::boff(c, K + k), il);
+      put(T::OFF_BH + T::boff(K + c, K + k), nh);
+      put(T::OFF_BL + T::boff(K + c, K + k), nl);
     }
     fence_async_smem();
     tc_fence_before();
