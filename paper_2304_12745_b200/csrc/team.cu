@@ -24,21 +24,13 @@
 // per-antenna norm across the TK threads sharing an antenna, and the X'
 // all-reduce across the TM threads sharing rows (once per layer). H is read
 // from HBM once (ld.global.nc, streaming) and W written once (st.global.cs).
+#include <algorithm>
 #include <cfloat>
 #include <climits>
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
-#include <cmath>
-#include <algorithm>
 #include <type_traits>
-
-#include "ufpgd_internal.h"
-#include <cfloat>
-#include <climits>
-#include <cmath>
-#include <cstdint>
-#include <cstdlib>
-#include <algorithm>
 
 #include "device_common.cuh"
 
