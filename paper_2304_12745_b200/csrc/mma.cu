@@ -171,7 +171,83 @@ __device__ __forceinline__ uint16_t f16_bits(__half h) { return *reinterpret_cas
 
 constexpr float kLoScale = 1.f / 2048.f;
 
+// Fixed-step power iteration on H^T H^* (pgd.cpp:146-162 with the BASELINE
+// 30-step rule), FP32 on the unscaled H, one thread per antenna (US = 1):
+// u = H^* v reduced over the CTA (shuffles, then per-warp partials in `scr`),
+// w_m = sum_k H(k, m) u_k in-thread, Rayleigh quotient Re(v^H w) of the last step.
 template <class T>
+__device__ float cta_power(const float4 (&hv)[T::K / 2], const float2* v0, int steps, float* scr, float* red,
+                           int warp, int lane) {
+  constexpr int K = T::K, NW = T::NW;
+  const int m = threadIdx.x;
+  float2 v = v0[m];
+  float est = 0.f;
+  bool zero = false;
+  for (int st = 0; st < steps; ++st) {
+    float u[2 * K];  // (Re, Im) of conj(H(k, m)) v_m, then of u_k
+#pragma unroll
+    for (int j = 0; j < K / 2; ++j) {
+      u[4 * j + 0] = hv[j].x * v.x + hv[j].y * v.y;  // conj(h) v = (hr vr + hi vi, hr vi - hi vr)
+      u[4 * j + 1] = hv[j].x * v.y - hv[j].y * v.x;
+      u[4 * j + 2] = hv[j].z * v.x + hv[j].w * v.y;
+      u[4 * j + 3] = hv[j].z * v.y - hv[j].w * v.x;
+    }
+#pragma unroll
+    for (int i = 0; i < 2 * K; ++i)
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) u[i] += __shfl_xor_sync(kFull, u[i], off);
+    if (lane == 0)
+#pragma unroll
+      for (int i = 0; i < 2 * K; ++i) scr[warp * 2 * K + i] = u[i];
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2 * K; ++i) {
+      float a = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) a += scr[w * 2 * K + i];
+      u[i] = a;
+    }
+    float2 wm = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < K / 2; ++j) {
+      cmac(wm, make_float2(hv[j].x, hv[j].y), make_float2(u[4 * j], u[4 * j + 1]));
+      cmac(wm, make_float2(hv[j].z, hv[j].w), make_float2(u[4 * j + 2], u[4 * j + 3]));
+    }
+    float dot = fmaf(v.x, wm.x, v.y * wm.y), wn2 = fmaf(wm.x, wm.x, wm.y * wm.y);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      dot += __shfl_xor_sync(kFull, dot, off);
+      wn2 += __shfl_xor_sync(kFull, wn2, off);
+    }
+    __syncthreads();  // scr reads done before the next step's writes
+    if (lane == 0) {
+      red[warp] = dot;
+      red[16 + warp] = wn2;
+    }
+    __syncthreads();
+    dot = 0.f;
+    wn2 = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      dot += red[w];
+      wn2 += red[16 + w];
+    }
+    __syncthreads();
+    if (!zero) {
+      if (wn2 == 0.f) {
+        zero = true;
+        est = 0.f;
+      } else {
+        est = dot;
+        const float inv = 1.f / sqrtf(wn2);
+        v = make_float2(wm.x * inv, wm.y * inv);
+      }
+    }
+  }
+  return est;
+}
+
+template <class T, bool PGD>
 __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_constant__ FusedArgs p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int K = T::K, M = T::M, R = T::R, Q = T::Q, NW = T::NW, KH = T::KH, US = T::US;
@@ -302,11 +378,22 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
 #else
 #define TSTAMP(i)
 #endif
+  float eta_b = 0.f, thr_b = 0.f;  // PGD: the realization's fixed step 1/L and threshold lambda/L
+  if constexpr (PGD) {
+    static_assert(US == 1, "PGD power iteration assumes one thread per antenna");
+    if (p.eta_in) {
+      eta_b = p.eta_in[rid];
+    } else {
+      eta_b = 1.f / cta_power<T>(hv, p.v0, p.power_steps, F, red, warp, lane);  // F: free before stage 1
+    }
+    thr_b = p.lambda * eta_b;
+    if (p.eta_out && tid == 0) p.eta_out[rid] = eta_b;
+  }
   for (long long l = 0; l < p.L; ++l) {
     TSTAMP(0)
     const bool xzero = (l == 0 && p.w0_mode == UFPGD_W0_ZERO);
-    const float ts = p.thr[l] * ginv;       // threshold in the scaled domain
-    const float fstep = -p.eta[l] * g2inv;  // -eta / g^2 folded into Bs
+    const float ts = (PGD ? thr_b : p.thr[l]) * ginv;       // threshold in the scaled domain
+    const float fstep = -(PGD ? eta_b : p.eta[l]) * g2inv;  // -eta / g^2 folded into Bs
     if (!xzero) {
       // W operand rows q = (hilo, part, k), k in the thread's user range
 #pragma unroll
@@ -562,7 +649,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
       act += static_cast<int>(red[16 + w]);
     }
     const bool diverged = fb != LLONG_MAX;
-    if (p.diverged_at) p.diverged_at[rid] = diverged ? static_cast<int32_t>(fb) : -1;
+    if (p.diverged_at) p.diverged_at[rid] = diverged ? static_cast<int32_t>(fb + (PGD ? 1 : 0)) : -1;
     if (p.l21) p.l21[rid] = diverged ? __int_as_float(0x7fc00000) : l21;
     if (p.active) p.active[rid] = diverged ? -1 : act;
     if (p.block_partials) {
@@ -586,8 +673,8 @@ using Mma_32_256 = MmaShape<32, 256, 1, UFPGD_MMA32_US>;
 using Mma_16_128 = MmaShape<16, 128, UFPGD_MMA16_MINB, UFPGD_MMA16_US>;
 
 template <class T>
-cudaError_t launch_mma_t(const FusedArgs& a, cudaStream_t s, long long* nblocks) {
-  auto kern = mma_kernel<T>;
+cudaError_t launch_mma_t(const FusedArgs& a, bool pgd, cudaStream_t s, long long* nblocks) {
+  auto kern = pgd ? mma_kernel<T, true> : mma_kernel<T, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
   if (e != cudaSuccess) return e;
   if (nblocks) *nblocks = a.B;
@@ -598,17 +685,18 @@ cudaError_t launch_mma_t(const FusedArgs& a, cudaStream_t s, long long* nblocks)
 
 }  // namespace
 
-// Unfolded forward only (PGD keeps the FP32 tile kernel); UFPGD_NO_MMA=1
+// Unfolded forward and fixed-step PGD at (16,128), (32,256); UFPGD_NO_MMA=1
 // selects the CUDA-core tile kernel for A/B runs.
 bool mma_supported(int K, int M, bool pgd) {
-  if (pgd || !((K == 32 && M == 256) || (K == 16 && M == 128))) return false;
+  if (!((K == 32 && M == 256) || (K == 16 && M == 128))) return false;
+  if (pgd && (K == 32 ? Mma_32_256::US : Mma_16_128::US) != 1) return false;
   const char* off = std::getenv("UFPGD_NO_MMA");
   return !(off && off[0] == '1');
 }
 
-cudaError_t launch_mma(const FusedArgs& a, int K, int M, cudaStream_t s, long long* nblocks) {
-  if (K == 32 && M == 256) return launch_mma_t<Mma_32_256>(a, s, nblocks);
-  if (K == 16 && M == 128) return launch_mma_t<Mma_16_128>(a, s, nblocks);
+cudaError_t launch_mma(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s, long long* nblocks) {
+  if (K == 32 && M == 256) return launch_mma_t<Mma_32_256>(a, pgd, s, nblocks);
+  if (K == 16 && M == 128) return launch_mma_t<Mma_16_128>(a, pgd, s, nblocks);
   return cudaErrorInvalidValue;
 }
 

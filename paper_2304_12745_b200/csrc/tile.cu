@@ -544,7 +544,7 @@ using Tile_32_256 = Tile<32, 256, UFPGD_T32_NW, UFPGD_T32_TA>;
 }  // namespace
 
 cudaError_t launch_tiled(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s, long long* nblocks) {
-  if (mma_supported(K, M, pgd)) return launch_mma(a, K, M, s, nblocks);  // mma.cu: tcgen05 path
+  if (mma_supported(K, M, pgd)) return launch_mma(a, pgd, K, M, s, nblocks);  // mma.cu: tcgen05 path
   if (K == 16 && M == 128) return launch_tile<Tile_16_128>(a, pgd, s, nblocks);
   if (K == 32 && M == 256) return launch_tile<Tile_32_256>(a, pgd, s, nblocks);
   return cudaErrorInvalidValue;

@@ -124,9 +124,10 @@ cudaError_t launch_fused(const FusedArgs& a, bool pgd, int K, int M, cudaStream_
                          long long* nblocks);
 // Tiled CTA kernels (tile.cu) for (16,128) and (32,256); launch_fused forwards there.
 cudaError_t launch_tiled(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s, long long* nblocks);
-// Tensor-core (tcgen05) unfolded forward at (32,256) (mma.cu); launch_tiled forwards there.
+// Tensor-core (tcgen05) unfolded forward / fixed-step PGD at (16,128), (32,256) (mma.cu);
+// launch_tiled forwards there.
 bool mma_supported(int K, int M, bool pgd);
-cudaError_t launch_mma(const FusedArgs& a, int K, int M, cudaStream_t s, long long* nblocks);
+cudaError_t launch_mma(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s, long long* nblocks);
 size_t general_smem_bytes(int K, int M);
 cudaError_t launch_general(const GeneralArgs& a, cudaStream_t s);
 cudaError_t launch_general64(const GeneralArgs64& a, cudaStream_t s);

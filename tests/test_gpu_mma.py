@@ -1,5 +1,5 @@
-"""The tcgen05 tensor-core path (csrc/mma.cu) of the unfolded forward at the
-BASELINE shapes (16, 128) and (32, 256): parity with the FP64 oracle at the
+"""The tcgen05 tensor-core path (csrc/mma.cu) of the unfolded forward and the
+fixed-step PGD at the BASELINE shapes (16, 128) and (32, 256): parity with the FP64 oracle at the
 north_star bars, agreement with the CUDA-core tile kernel (UFPGD_NO_MMA=1),
 every W0 mode, and exact equivariance under power-of-two channel scaling —
 the property the kernel's per-realization f16 range scaling must preserve
@@ -99,3 +99,49 @@ def test_mma_nonfinite_channel_isolated():
     ok = [i for i in range(8) if i not in (3, 5)]
     assert np.all(g["diverged_at"][ok] == -1)
     np.testing.assert_array_equal(g["W"][ok], clean["W"][ok])
+
+
+def run_pgd(H, lam, iters, c, mma=True, **kw):
+    old = os.environ.get("UFPGD_NO_MMA")
+    os.environ["UFPGD_NO_MMA"] = "0" if mma else "1"
+    try:
+        out = U.pgd_fixed(torch.from_numpy(np.ascontiguousarray(H)).cuda(), lam, iters, c,
+                          want_per_realization=True, **kw)
+        torch.cuda.synchronize()
+    finally:
+        if old is None:
+            os.environ.pop("UFPGD_NO_MMA", None)
+        else:
+            os.environ["UFPGD_NO_MMA"] = old
+    return {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
+
+
+@pytest.mark.parametrize("cfg,n,iters", [(4, 64, 400), (5, 128, 1000)])
+def test_mma_pgd_with_power_iteration(cfg, n, iters):
+    """Fixed-step PGD (pgd.cpp:178-268, W0 = H^*) on the tensor-core kernel: the
+    in-kernel 30-step power iteration against the oracle's, the iterate against
+    the FP64 oracle run at that step, and against the CUDA-core tile kernel."""
+    w = U.CONFIGS[cfg]
+    H = U.make_inputs(w, 3, n)
+    lam = 0.05
+    g = run_pgd(H, lam, iters, w.c, power_steps=30)
+    t = run_pgd(H, lam, iters, w.c, power_steps=30, mma=False)
+    Lo, st = O.power_iteration_batch_f32(H, 30)
+    assert np.all(st == 0)
+    assert np.max(np.abs(g["eta"] * Lo - 1.0)) <= 1e-5
+    ora = O.pgd_batch_f32(H, w.c, lam, 1.0 / Lo, iters, w0_mode=U.W0_CONJ_H)
+    rep = report(H, g["W"], ora, w.c, lam)
+    print(f"cfg{cfg} pgd-{iters}: rel max {rep['rel_max']:.2e} obj {rep['obj_max']:.2e} ties {rep['ties']}")
+    assert_parity(rep)
+    assert np.all(g["diverged_at"] == -1)
+    assert rel_fro(g["W"], t["W"].astype(np.complex128)).max() < 1e-4
+
+
+def test_mma_pgd_divergence_index_is_one_based():
+    """test_pgd.cpp:454-470 on the tensor-core kernel: eta = 1e6 diverges at an
+    iteration >= 1 (1-based)."""
+    w = U.CONFIGS[5]
+    H = U.make_inputs(w, 0, 4)
+    eta = torch.full((4,), 1e6, dtype=torch.float32, device="cuda")
+    g = run_pgd(H, 0.0, 50, w.c, eta=eta)
+    assert np.all(g["diverged_at"] >= 1)

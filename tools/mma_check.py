@@ -88,8 +88,8 @@ def timing(cfg=4, n=16384, reps=3):
 
 if __name__ == "__main__":
     what = sys.argv[1:] or ["one", "cfg4", "time"]
-    if what[0] == "phases":
-        what = ["phases-only"]
+    if what[0] in ("phases", "pgd"):
+        what = ["deferred"]
     if what[0] == "prof":  # one launch per config for ncu (-k regex:mma_kernel)
         for c in what[1:]:
             timing(int(c), 16384 if c == "4" else 65536, reps=1)
@@ -102,6 +102,23 @@ if __name__ == "__main__":
     if "time" in what:
         timing(4, 16384)
         timing(5, 65536)
+
+
+def pgd_timing(cfg, n=4096, iters=1000):
+    """Fixed-step PGD (in-kernel 30-step power iteration) at the config's shape:
+    tensor-core kernel vs the FFMA2 tile kernel."""
+    w = U.CONFIGS[cfg]
+    Hd = torch.empty((n, w.M, w.K), dtype=torch.complex64, device="cuda")
+    U.generate_channels_device(w.seed_h, w.seed_g, w.gain_db, 0, n, w.K, w.M, out=Hd)
+    for mma in (True, False):
+        os.environ["UFPGD_NO_MMA"] = "0" if mma else "1"
+        U.pgd_fixed(Hd, 0.05, 10, w.c); torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(); U.pgd_fixed(Hd, 0.05, iters, w.c); e.record(); torch.cuda.synchronize()
+        ms = s.elapsed_time(e)
+        fl = iters * (16 * w.K * w.K * w.M + 10 * w.K * w.M) * n
+        print(f"{'mma ' if mma else 'tile'} PGD-{iters} ({w.K},{w.M}) B={n}: {ms:.2f} ms  "
+              f"{fl / ms / 1e9:.1f} TFLOP/s (FP32-equivalent)", flush=True)
 
 
 def phase_probe(cfg):
@@ -125,3 +142,6 @@ def phase_probe(cfg):
 if __name__ == "__main__" and sys.argv[1:2] == ["phases"]:
     for c in sys.argv[2:]:
         phase_probe(int(c))
+if __name__ == "__main__" and sys.argv[1:2] == ["pgd"]:
+    for c in sys.argv[2:]:
+        pgd_timing(int(c))
