@@ -86,10 +86,11 @@ int ufpgd_gpu_device_count(int* count);
  *   stats[3] (double) {sum_b alpha*||W_b||_{2,1}, sum_b active_b, #diverged},
  *                     sums over non-diverged realizations, deterministic order.
  *
- * Kernels: the fused kernels for (4,16), (4,32), (4,64), (8,32), (8,64),
- * (8,128), (16,128), (32,256); any other (K, M) within 6x the flops of one of
- * them runs zero-padded on it (padded users / antennas stay exactly zero);
- * the rest run the general CTA-per-realization kernel.
+ * Kernels: the fused FFMA2 kernels for (4,16), (4,32), (4,64), (8,32), (8,64),
+ * (8,128); the tcgen05 tensor-core kernel (FP32-class 3-term f16 split, TMEM
+ * accumulators) for (16,128), (32,256); any other (K, M) within 6x the flops
+ * of one of them runs zero-padded on it (padded users / antennas stay exactly
+ * zero); the rest run the general CTA-per-realization kernel.
  */
 int ufpgd_gpu_unfolded_forward(const ufpgd_c64* H, int64_t B, int K, int M,
                                const double* lambda, const double* eta, int L,
