@@ -659,12 +659,18 @@ int pick_warps(int rpw, long long B) {
   return 1;
 }
 
+#ifndef UFPGD_PGD_MAXT
+#define UFPGD_PGD_MAXT 256
+#endif
+#ifndef UFPGD_PGD_MINB
+#define UFPGD_PGD_MINB 1
+#endif
 template <class S>
 cudaError_t launch_team(const FusedArgs& a, bool pgd, cudaStream_t s, long long* nblocks) {
   // The unfolded kernel takes the Team's launch bounds; the PGD kernel (power
   // iteration prologue, more live state) keeps 256 x 1 (no register cap).
-  auto kern = pgd ? fused_kernel<S, true, 256, 1> : fused_kernel<S, false, S::MAXT, S::MINB>;
-  const int maxt = pgd ? 256 : S::MAXT;
+  auto kern = pgd ? fused_kernel<S, true, UFPGD_PGD_MAXT, UFPGD_PGD_MINB> : fused_kernel<S, false, S::MAXT, S::MINB>;
+  const int maxt = pgd ? UFPGD_PGD_MAXT : S::MAXT;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kFusedMaxWarps * (S::SMEM_PER_WARP + S::WSMEM_PER_WARP));
   if (e != cudaSuccess) return e;
