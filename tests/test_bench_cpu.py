@@ -34,3 +34,31 @@ def test_cost_model_counts_performed_contractions():
     assert w.flops_per_realization() == (2 * L - 2) * 8 * K * K * M + 10 * K * M * L
     assert w.flops_per_realization(exact_w0=False) == 2 * L * 8 * K * K * M + 10 * K * M * L
     assert w.bytes_per_realization() == 16 * K * M
+
+
+def test_tensor_core_flop_model():
+    """Tensor-core flops of the tcgen05 kernel (csrc/mma.cu) per realization:
+    stage 1 M=4K, N=4K, K=M (skipped at a W0 = 0 layer 0), stage 2 per
+    128-antenna tile M=128, N=4K+2K, K=2K; ~3x the FP32-equivalent work (the
+    3-term f16 split) plus the stage-1 lo*lo block."""
+    sys.path.insert(0, ROOT)
+    import paper_2304_12745_b200 as U
+
+    for cfg in (4, 5):
+        w = U.CONFIGS[cfg]
+        K, M, L = w.K, w.M, w.L
+        s1 = 2 * (4 * K) * (4 * K) * M
+        s2 = (M // 128) * 2 * 128 * (6 * K) * (2 * K)
+        assert w.tensor_flops_per_realization() == (L - 1) * s1 + L * s2
+        assert 2.5 < w.tensor_flops_per_realization() / w.flops_per_realization() < 4.5
+    for cfg in (1, 2, 3):
+        assert U.CONFIGS[cfg].tensor_flops_per_realization() is None
+
+
+def test_measured_peaks_fallback():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    p = bench.measured_peaks()
+    assert p["hbm_gbs"] > 1000 and p["bf16_tflops"] > 500
+    assert p["source"] in ("MEASURED_PEAKS.json", "fallback")
