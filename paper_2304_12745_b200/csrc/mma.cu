@@ -58,15 +58,21 @@ struct MmaShape {
   static constexpr int OFF_HH = 0;                       // H hi  [R x M] f16, core layout hoff()
   static constexpr int OFF_HL = OFF_HH + R * M * 2;      // H lo
   static constexpr int OFF_W = OFF_HL + R * M * 2;       // [W_hi; W_lo] [Q x M] f16, woff()
+  // Bs builder chunk width: 4 values of an X' row per thread, or 2 when K^2/4
+  // chunks would leave threads idle (then a half-warp spans 16 rows, so the
+  // exchange rows are 2 words apart and Bs N-groups are padded by 64 bytes:
+  // both the 8-byte row reads and the 4-byte Bs stores are conflict-free).
+  static constexpr int CWD = (K * K / 4 >= NT) ? 4 : 2;
+  static constexpr int BSBO = 16 * R + (CWD == 2 ? 64 : 0);  // Bs N-group stride (descriptor SBO)
   static constexpr int OFF_BH = OFF_W + Q * M * 2;       // Bs hi [R x R] f16, boff()
-  static constexpr int OFF_BL = OFF_BH + R * R * 2;      // Bs lo
-  static constexpr int FSTR = R + 4;                     // fp32 exchange rows (floats), conflict-free LDS/STS.128
+  static constexpr int OFF_BL = OFF_BH + (R / 8) * BSBO; // Bs lo (continues Bs hi along N)
+  static constexpr int FSTR = R + (CWD == 4 ? 4 : 2);    // fp32 exchange rows (floats), conflict-free
   // F [R][FSTR] (hi rows of P) and G (lo rows) alias the W operand: they are
   // written after the stage-1 MMAs retire and read before W is rewritten.
   static constexpr int OFF_F = OFF_W;
   static constexpr int OFF_G = OFF_F + R * FSTR * 4;
   static_assert(2 * R * FSTR * 4 <= Q * M * 2, "");
-  static constexpr int OFF_BAR = OFF_BL + R * R * 2;     // mbarriers, TMEM slot, reductions
+  static constexpr int OFF_BAR = OFF_BL + (R / 8) * BSBO;  // mbarriers, TMEM slot, reductions
   static constexpr int OFF_NRM = OFF_BAR + 512;          // US > 1: partial column norms [US][M]
   static constexpr int SMEM = OFF_NRM + (US > 1 ? US * M * 4 : 0);
   // TMEM columns (fp32 accumulators)
@@ -94,7 +100,7 @@ struct MmaShape {
   }
   // Bs: element (kk, n), K-major (K = kk, N = n): LBO (K-group) 128, SBO (N-group) 16 R.
   static __device__ __forceinline__ int boff(int kk, int n) {
-    return (kk >> 3) * 128 + (n >> 3) * (16 * R) + (n & 7) * 16 + (kk & 7) * 2;
+    return (kk >> 3) * 128 + (n >> 3) * BSBO + (n & 7) * 16 + (kk & 7) * 2;
   }
 };
 
@@ -355,7 +361,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
   constexpr uint32_t IDESC1 = idesc_f16_amn<Q, 2 * R>();
   constexpr uint32_t IDESC2W = idesc_f16_amn<128, 2 * R>();
   constexpr uint32_t IDESC2 = idesc_f16_amn<128, R>();
-  static_assert(T::OFF_HL == T::OFF_HH + (R / 8) * 16 * M && T::OFF_BL == T::OFF_BH + (R / 8) * 16 * R,
+  static_assert(T::OFF_HL == T::OFF_HH + (R / 8) * 16 * M && T::OFF_BL == T::OFF_BH + (R / 8) * T::BSBO,
                 "lo operands continue the hi ones along N");
   float* F = reinterpret_cast<float*>(smem + T::OFF_F);
   float* G = reinterpret_cast<float*>(smem + T::OFF_G);
@@ -466,9 +472,14 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
           for (int i = 0; i < 16; ++i) a[i] *= kLoScale;  // lo rows: W_lo H_hi
         }
         if (lane < K) {
+          if constexpr (T::CWD == 4) {
 #pragma unroll
-          for (int i = 0; i < 16; i += 4)
-            *reinterpret_cast<float4*>(dst + cq + i) = make_float4(a[i], a[i + 1], a[i + 2], a[i + 3]);
+            for (int i = 0; i < 16; i += 4)
+              *reinterpret_cast<float4*>(dst + cq + i) = make_float4(a[i], a[i + 1], a[i + 2], a[i + 3]);
+          } else {  // rows 2 words apart: 8-byte stores keep a half-warp conflict-free
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) *reinterpret_cast<float2*>(dst + cq + i) = make_float2(a[i], a[i + 1]);
+          }
         }
       }
       __syncthreads();
@@ -478,11 +489,12 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     // 4-wide chunk of X' row k per thread
     // CWD-wide chunks of X' row k per thread (CWD = 4, or 2 when K / 4 chunks per
     // row would leave threads idle; 2-wide keeps a quarter-warp on one F row)
-    constexpr int CWD = (K * K / 4 >= T::NT) ? 4 : 2, NCH = K * K / CWD, CPR = K / CWD;
+    constexpr int CWD = T::CWD, NCH = K * K / CWD, CPR = K / CWD;
     using FV = typename std::conditional<CWD == 4, float4, float2>::type;
 #pragma unroll
     for (int ch = tid; ch < NCH; ch += T::NT) {
-      const int k = ch / CPR, c = (ch % CPR) * CWD;
+      // CWD 4: consecutive threads walk along a row; CWD 2: down the rows
+      const int k = CWD == 4 ? ch / CPR : ch % K, c = (CWD == 4 ? ch % CPR : ch / K) * CWD;
       float xr[CWD], xi[CWD];
 #pragma unroll
       for (int u = 0; u < CWD; ++u) xr[u] = xi[u] = 0.f;
@@ -551,7 +563,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
         for (int ks = 0; ks < R / 16; ++ks) {
           const uint64_t ah = sdesc(sb + T::OFF_HH + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
           const uint64_t al = sdesc(sb + T::OFF_HL + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
-          const uint64_t bh = sdesc(sb + T::OFF_BH + ks * 256, 128, 16 * R);  // N = 2R spans [Bs_hi | Bs_lo]
+          const uint64_t bh = sdesc(sb + T::OFF_BH + ks * 256, 128, T::BSBO);  // N = 2R spans [Bs_hi | Bs_lo]
           umma_f16(dm, ah, bh, IDESC2W, ks > 0);  // [main | corr] = H_hi [Bs_hi | Bs_lo]
           umma_f16(dc, al, bh, IDESC2, 1);        // corr += H_lo Bs_hi
         }
