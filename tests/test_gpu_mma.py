@@ -145,3 +145,25 @@ def test_mma_pgd_divergence_index_is_one_based():
     eta = torch.full((4,), 1e6, dtype=torch.float32, device="cuda")
     g = run_pgd(H, 0.0, 50, w.c, eta=eta)
     assert np.all(g["diverged_at"] >= 1)
+
+
+@pytest.mark.parametrize("K,M,lam_v", [(16, 128, 6.0), (32, 256, 9.0)])
+def test_mma_sparsity_zero_branch(K, M, lam_v):
+    """A large constant lambda (pgd_init-style layers from W0 = H^*) drives
+    antennas to exactly zero on the tensor-core path: the strict '>' prox
+    branch (pgd.cpp:237-244) in the power-of-two scaled domain, support equal
+    to the oracle's outside near-ties."""
+    L = 20
+    H = U.generate_channels(78, 0, 0.0, 0, 256, K, M)
+    lam = np.full(L, lam_v)
+    eta = np.full(L, 1.0 / U.mp_bound(K, M))
+    c = np.full(K, np.sqrt(10.0))
+    g = run(H, lam, eta, c, w0_mode=U.W0_CONJ_H)
+    ora = O.forward_batch_f32(H, c, lam, eta, w0_mode=U.W0_CONJ_H)
+    rep = report(H, g["W"], ora, c, lam_v)
+    clean = ora["tie_margin"] >= 1e-4
+    assert clean.sum() > 200
+    assert rep["rel"][clean].max() <= 1e-4
+    assert rep["support_mismatch"] == 0
+    assert ora["active"].mean() < M - 8  # the zero branch is exercised
+    assert np.array_equal(g["active"][clean], ora["active"][clean])
