@@ -1,10 +1,11 @@
-// Tensor-core (tcgen05 / TMEM) kernel for the unfolded forward at
-// (K, M) = (32, 256) — BASELINE config 4, the "larger M x K x K complex
-// contractions" north_star reserves the tensor cores for. One CTA (8 warps,
-// thread = antenna) owns a realization for all layers (unfolded.cpp:112-146):
+// Tensor-core (tcgen05 / TMEM) kernel for the unfolded forward and the
+// fixed-step PGD at (K, M) = (32, 256) and (16, 128) — BASELINE configs 4 and
+// 5, the "larger M x K x K complex contractions" north_star reserves the
+// tensor cores for. One CTA (thread = antenna) owns a realization for all
+// layers / iterations (unfolded.cpp:112-146, pgd.cpp:226-244):
 //
-//   stage 1  X  = W H^T           tcgen05.mma  M=128 N=128 K=256
-//   stage 2  G  = (-eta X') H^*   tcgen05.mma  M=128 N=128 + N=64, K=64, per 128-antenna tile
+//   stage 1  X  = W H^T           tcgen05.mma  M=4K N=4K K=M, split-K by 128-antenna tile
+//   stage 2  G  = (-eta X') H^*   tcgen05.mma  M=128 N=4K + N=2K, K=2K, per 128-antenna tile
 //   prox     per-antenna group soft threshold on V = W + G, in registers
 //
 // Precision: FP32 products are split into f16 pairs, x = hi + 2^-11 lo
@@ -19,7 +20,7 @@
 //
 // Real forms (rows r = (part, k), part 0 = Re, 1 = Im, r in [0, 2K)):
 //   stage 1: D1[q][(p', k')] = sum_m Wop[q][m] Hop[(p', k')][m], q = (hilo, p, k)
-//            (A = [W_hi; W_lo] 128 x M, MN-major; B = H_hi or H_lo, K-major)
+//            (A = [W_hi; W_lo] 4K x M, MN-major; B = [H_hi | H_lo], K-major)
 //            X_r = P[(0,k),(0,k')] - P[(1,k),(1,k')], X_i = P[(0,k),(1,k')] + P[(1,k),(0,k')]
 //   stage 2: D2[m][(p, k)] = sum_(p', k') Hop[(p', k')][m] Bs[(p', k')][(p, k)]
 //            (A = H as M x 2K MN-major — the same shared-memory bytes as
@@ -30,7 +31,6 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
-
 #include <type_traits>
 
 #include <cuda_fp16.h>
