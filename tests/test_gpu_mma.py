@@ -167,3 +167,23 @@ def test_mma_sparsity_zero_branch(K, M, lam_v):
     assert rep["support_mismatch"] == 0
     assert ora["active"].mean() < M - 8  # the zero branch is exercised
     assert np.array_equal(g["active"][clean], ora["active"][clean])
+
+
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_mma_host_path_and_position_invariance(cfg):
+    """The tensor-core kernel through the pipelined host-buffer entry point
+    (ufpgd_gpu_unfolded_forward_host) equals the device path bit for bit, and a
+    realization's W does not depend on its batch position or batch size
+    (B = 1, 3, ragged) — one CTA per realization, fixed summation order."""
+    w = U.CONFIGS[cfg]
+    n = 2048 if cfg == 4 else 8192  # several 16 MiB host-pipeline chunks
+    H = U.make_inputs(w, 5, n)
+    lam, eta = w.layer_params()
+    d = run(H, lam, eta, w.c)
+    h = U.unfolded_forward_host(H, lam, eta, w.c, w0_mode=w.w0_mode)
+    np.testing.assert_array_equal(h["W"], d["W"])
+    assert int(h["stats"][2]) == 0
+    for idx in ([0], [7, 1000, 3], list(range(n - 37, n))):
+        sub = run(np.ascontiguousarray(H[idx]), lam, eta, w.c)
+        np.testing.assert_array_equal(sub["W"], d["W"][idx])
+        np.testing.assert_array_equal(sub["l21"], d["l21"][idx])
