@@ -40,20 +40,18 @@
 namespace ufpgd_gpu_impl {
 namespace {
 
-// Shape of the tensor-core kernel: US threads per antenna (NT = US M; thread
-// tid owns antenna tid % M and users [h K/US, (h+1) K/US), h = tid / M), 2K
+// Shape of the tensor-core kernel: one thread per antenna (NT = M), 2K
 // real-form rows r = (part, k), Q = 4K operand rows q = (hilo, part, k) for
 // stage 1 (MMA M = Q: 128 at K = 32, 64 at K = 16), M / 128 stage-2 tiles.
-template <int K_, int M_, int MINB_, int US_ = 1>
+template <int K_, int M_, int MINB_>
 struct MmaShape {
-  static constexpr int K = K_, M = M_, US = US_, NT = US_ * M_, MINB = MINB_;
-  static constexpr int KH = K / US;   // users per thread
+  static constexpr int K = K_, M = M_, NT = M_, MINB = MINB_;
   static constexpr int R = 2 * K;     // real-form rows (part, k)
   static constexpr int Q = 2 * R;     // stage-1 A rows (hilo, part, k) = stage-1 MMA M
   static constexpr int NTILE = M / 128;
   static constexpr int NW = NT / 32;
   static_assert(Q == 64 || Q == 128, "stage-1 MMA M must be 64 or 128");
-  static_assert(M % 128 == 0 && NW <= 16 && K % 16 == 0 && (US == 1 || US == 2) && KH % 16 == 0, "");
+  static_assert(M % 128 == 0 && NW <= 8 && K % 16 == 0, "");
   // shared-memory byte offsets (all 1024-aligned)
   static constexpr int OFF_HH = 0;                       // H hi  [R x M] f16, core layout hoff()
   static constexpr int OFF_HL = OFF_HH + R * M * 2;      // H lo
@@ -73,8 +71,7 @@ struct MmaShape {
   static constexpr int OFF_G = OFF_F + R * FSTR * 4;
   static_assert(2 * R * FSTR * 4 <= Q * M * 2, "");
   static constexpr int OFF_BAR = OFF_BL + (R / 8) * BSBO;  // mbarriers, TMEM slot, reductions
-  static constexpr int OFF_NRM = OFF_BAR + 512;          // US > 1: partial column norms [US][M]
-  static constexpr int SMEM = OFF_NRM + (US > 1 ? US * M * 4 : 0);
+  static constexpr int SMEM = OFF_BAR + 512;
   // TMEM columns (fp32 accumulators)
   // D1 part t: [X-part with H_hi | with H_lo] (2R) over antenna tile t (stage 1 is
   // split-K by tile so each tile's antennas start their MMAs as soon as their own
@@ -178,7 +175,7 @@ __device__ __forceinline__ uint16_t f16_bits(__half h) { return *reinterpret_cas
 constexpr float kLoScale = 1.f / 2048.f;
 
 // Fixed-step power iteration on H^T H^* (pgd.cpp:146-162 with the BASELINE
-// 30-step rule), FP32 on the unscaled H, one thread per antenna (US = 1):
+// 30-step rule), FP32 on the unscaled H, one thread per antenna:
 // u = H^* v reduced over the CTA (shuffles, then per-warp partials in `scr`),
 // w_m = sum_k H(k, m) u_k in-thread, Rayleigh quotient Re(v^H w) of the last step.
 template <class T>
@@ -256,7 +253,7 @@ __device__ float cta_power(const float4 (&hv)[T::K / 2], const float2* v0, int s
 template <class T, bool PGD>
 __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_constant__ FusedArgs p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int K = T::K, M = T::M, R = T::R, Q = T::Q, NW = T::NW, KH = T::KH, US = T::US;
+  constexpr int K = T::K, M = T::M, R = T::R, Q = T::Q, NW = T::NW;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long rid = blockIdx.x;
   const uint32_t sb = smem_u32(smem);
@@ -265,7 +262,6 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + T::OFF_BAR + 48);
   float* red = reinterpret_cast<float*>(smem + T::OFF_BAR + 64);           // [2][16]
   long long* fbs = reinterpret_cast<long long*>(smem + T::OFF_BAR + 192);  // [16]
-  float* nrm = reinterpret_cast<float*>(smem + T::OFF_NRM);
 
   if (tid == 0) {
 #pragma unroll
@@ -279,18 +275,18 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
 
-  // ---- H of antenna m, users [k0, k0 + KH): registers, max |.| over the realization ----
-  const int m = tid % M, hh = tid / M, k0 = hh * KH;
-  float4 hv[KH / 2];  // hv[j] = (Re H(k0+2j, m), Im H(k0+2j, m), Re H(k0+2j+1, m), Im H(k0+2j+1, m))
+  // ---- H row of antenna m = tid: registers, max |.| over the realization ----
+  const int m = tid;
+  float4 hv[K / 2];  // hv[j] = (Re H(2j, m), Im H(2j, m), Re H(2j+1, m), Im H(2j+1, m))
   {
-    const float4* hg = reinterpret_cast<const float4*>(p.H + (rid * M + m) * K + k0);
+    const float4* hg = reinterpret_cast<const float4*>(p.H + (rid * M + m) * K);
 #pragma unroll
-    for (int j = 0; j < KH / 2; ++j) hv[j] = ldg_stream(hg + j);
+    for (int j = 0; j < K / 2; ++j) hv[j] = ldg_stream(hg + j);
   }
   float amax = 0.f;
   bool bad = false;  // fmaxf drops NaN: a non-finite channel keeps g = 1 (and diverges at layer 0)
 #pragma unroll
-  for (int j = 0; j < KH / 2; ++j) {
+  for (int j = 0; j < K / 2; ++j) {
     const float a = fmaxf(fmaxf(fabsf(hv[j].x), fabsf(hv[j].y)), fmaxf(fabsf(hv[j].z), fabsf(hv[j].w)));
     amax = fmaxf(amax, a);
     bad |= !(fabsf(hv[j].x) + fabsf(hv[j].y) + fabsf(hv[j].z) + fabsf(hv[j].w) <= FLT_MAX);
@@ -319,9 +315,9 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
 
   // ---- stage H (hi / lo f16) in the shared core layout -------------------------
 #pragma unroll
-  for (int j = 0; j < KH / 2; ++j) {
+  for (int j = 0; j < K / 2; ++j) {
     const float vals[4] = {hv[j].x * g, hv[j].y * g, hv[j].z * g, hv[j].w * g};
-    const int kk = k0 + 2 * j;
+    const int kk = 2 * j;
     const int rows[4] = {kk, K + kk, kk + 1, K + kk + 1};  // Re k, Im k, Re k+1, Im k+1
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -333,20 +329,20 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
   }
   fence_async_smem();  // H is read by the tensor cores (async proxy)
 
-  // ---- W0 (scaled: W_s = W / g) in registers: wr[k], wi[k], users k0 + k ----
-  float wr[KH], wi[KH];
+  // ---- W0 (scaled: W_s = W / g) in registers: wr[k], wi[k] for antenna m ------
+  float wr[K], wi[K];
   if (p.w0_mode == UFPGD_W0_CONJ_H) {
 #pragma unroll
-    for (int j = 0; j < KH / 2; ++j) {
+    for (int j = 0; j < K / 2; ++j) {
       wr[2 * j] = hv[j].x * ginv;
       wi[2 * j] = -hv[j].y * ginv;
       wr[2 * j + 1] = hv[j].z * ginv;
       wi[2 * j + 1] = -hv[j].w * ginv;
     }
   } else if (p.w0_mode == UFPGD_W0_GIVEN) {
-    const float4* wg0 = reinterpret_cast<const float4*>(p.W0 + (rid * M + m) * K + k0);
+    const float4* wg0 = reinterpret_cast<const float4*>(p.W0 + (rid * M + m) * K);
 #pragma unroll
-    for (int j = 0; j < KH / 2; ++j) {
+    for (int j = 0; j < K / 2; ++j) {
       const float4 v = wg0[j];
       wr[2 * j] = v.x * ginv;
       wi[2 * j] = v.y * ginv;
@@ -355,7 +351,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     }
   } else {
 #pragma unroll
-    for (int k = 0; k < KH; ++k) wr[k] = wi[k] = 0.f;
+    for (int k = 0; k < K; ++k) wr[k] = wi[k] = 0.f;
   }
 
   constexpr uint32_t IDESC1 = idesc_f16_amn<Q, 2 * R>();
@@ -386,7 +382,6 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
 #endif
   float eta_b = 0.f, thr_b = 0.f;  // PGD: the realization's fixed step 1/L and threshold lambda/L
   if constexpr (PGD) {
-    static_assert(US == 1, "PGD power iteration assumes one thread per antenna");
     if (p.eta_in) {
       eta_b = p.eta_in[rid];
     } else {
@@ -401,12 +396,12 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     const float ts = (PGD ? thr_b : p.thr[l]) * ginv;       // threshold in the scaled domain
     const float fstep = -(PGD ? eta_b : p.eta[l]) * g2inv;  // -eta / g^2 folded into Bs
     if (!xzero) {
-      // W operand rows q = (hilo, part, k), k in the thread's user range
+      // W operand rows q = (hilo, part, k) from the thread's antenna column
 #pragma unroll
-      for (int pg = 0; pg < 2 * (KH / 8); ++pg) {  // 8 rows (part, k .. k+7)
-        const int part = pg / (KH / 8), kg = pg % (KH / 8);
+      for (int pg = 0; pg < 2 * (K / 8); ++pg) {  // 8 rows (part, k .. k+7)
+        const int part = pg / (K / 8), kg = pg % (K / 8);
         const float* src = (part == 0 ? wr : wi) + 8 * kg;
-        const int q0 = part * K + k0 + 8 * kg;
+        const int q0 = part * K + 8 * kg;
         uint32_t h[4], lo[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) split2(src[2 * u], src[2 * u + 1], h[u], lo[u]);
@@ -419,7 +414,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
       if (T::NTILE > 1) named_bar(1 + tile, T::NT / T::NTILE);
       else __syncthreads();
       TSTAMP(1)
-      if (tid == tile * 128) {  // US = 1: thread 128 t; US = 2: the hh = 0 thread of antenna 128 t
+      if (tid == tile * 128) {  // the tile group's first thread
         tc_fence_after();
         constexpr int KST = 128 / 16;  // K-steps per antenna tile
 #pragma unroll 1
@@ -583,10 +578,10 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
       for (int part = 0; part < 2; ++part) {
         float* w = part == 0 ? wr : wi;
 #pragma unroll
-        for (int j0 = 0; j0 < KH; j0 += 16) {
+        for (int j0 = 0; j0 < K; j0 += 16) {
           float a[16], b[16];
-          tmem_ld16(cm + part * K + k0 + j0, a);
-          tmem_ld16(cc + part * K + k0 + j0, b);
+          tmem_ld16(cm + part * K + j0, a);
+          tmem_ld16(cc + part * K + j0, b);
           tmem_wait<16>(a);
           tmem_wait<16>(b);
 #pragma unroll
@@ -598,24 +593,17 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     // prox_l21 on the antenna column (strict '>', pgd.cpp:237-244 / unfolded.cpp:135-143)
     float s2 = 0.f;
 #pragma unroll
-    for (int k = 0; k < KH; ++k) s2 = fmaf(wr[k], wr[k], fmaf(wi[k], wi[k], s2));
-    if constexpr (US > 1) {  // the antenna's users are split over US threads: combine in a fixed order
-      nrm[hh * M + m] = s2;
-      __syncthreads();
-      s2 = 0.f;
-#pragma unroll
-      for (int u = 0; u < US; ++u) s2 += nrm[u * M + m];
-    }
+    for (int k = 0; k < K; ++k) s2 = fmaf(wr[k], wr[k], fmaf(wi[k], wi[k], s2));
     nonfinite |= !(s2 * (g * g) <= FLT_MAX);
     const bool on = s2 > ts * ts;
     const float r = rsqrt_ftz(fmaxf(s2, FLT_MIN));
     const float scale = on ? fmaf(-ts, r, 1.f) : 0.f;
 #pragma unroll
-    for (int k = 0; k < KH; ++k) {
+    for (int k = 0; k < K; ++k) {
       wr[k] *= scale;
       wi[k] *= scale;
     }
-    if (l + 1 == p.L && on && hh == 0) {
+    if (l + 1 == p.L && on) {
       l21 += g * fmaf(s2, r, -ts);
       act += 1;
     }
@@ -625,9 +613,9 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
 
   // ---- W out (unscaled), per-realization reductions ---------------------------
   {
-    float4* wg = reinterpret_cast<float4*>(p.W + (rid * M + m) * K + k0);
+    float4* wg = reinterpret_cast<float4*>(p.W + (rid * M + m) * K);
 #pragma unroll
-    for (int j = 0; j < KH / 2; ++j)
+    for (int j = 0; j < K / 2; ++j)
       stg_stream(wg + j, make_float4(wr[2 * j] * g, wi[2 * j] * g, wr[2 * j + 1] * g, wi[2 * j + 1] * g));
 #ifdef UFPGD_MMA_TIMING
     if (probe) {
@@ -672,17 +660,11 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
   }
 }
 
-#ifndef UFPGD_MMA32_US
-#define UFPGD_MMA32_US 1
-#endif
-#ifndef UFPGD_MMA16_US
-#define UFPGD_MMA16_US 1
-#endif
-using Mma_32_256 = MmaShape<32, 256, 1, UFPGD_MMA32_US>;
+using Mma_32_256 = MmaShape<32, 256, 1>;
 #ifndef UFPGD_MMA16_MINB
 #define UFPGD_MMA16_MINB 4
 #endif
-using Mma_16_128 = MmaShape<16, 128, UFPGD_MMA16_MINB, UFPGD_MMA16_US>;
+using Mma_16_128 = MmaShape<16, 128, UFPGD_MMA16_MINB>;
 
 template <class T>
 cudaError_t launch_mma_t(const FusedArgs& a, bool pgd, cudaStream_t s, long long* nblocks) {
@@ -701,7 +683,6 @@ cudaError_t launch_mma_t(const FusedArgs& a, bool pgd, cudaStream_t s, long long
 // selects the CUDA-core tile kernel for A/B runs.
 bool mma_supported(int K, int M, bool pgd) {
   if (!((K == 32 && M == 256) || (K == 16 && M == 128))) return false;
-  if (pgd && (K == 32 ? Mma_32_256::US : Mma_16_128::US) != 1) return false;
   const char* off = std::getenv("UFPGD_NO_MMA");
   return !(off && off[0] == '1');
 }
