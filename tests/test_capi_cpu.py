@@ -3,8 +3,10 @@ every symbol include/ufpgd_gpu.h declares, and its host-side input generator
 (the harness half of SURVEY §8d) is bit-identical to the oracle's restatement
 of rng.cpp / channel.cpp. No kernel is launched here."""
 import math
+import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -100,3 +102,16 @@ def test_compute_entry_points_fail_loudly_without_a_device():
         pytest.skip("a GPU is present")
     with pytest.raises(ValueError):
         U.unfolded_forward(torch.zeros((1, 64, 8), dtype=torch.complex64), [0.1], [0.005], np.ones(8))
+
+
+def test_missing_library_fails_loudly():
+    """No CPU fallback: with the CUDA library absent the package raises on first
+    use instead of computing anything on the host."""
+    code = ("import paper_2304_12745_b200 as U\n"
+            "try:\n    U.abi_version()\nexcept ImportError as e:\n"
+            "    assert 'no CPU fallback' in str(e); print('raised')\n")
+    env = dict(os.environ, UFPGD_LIB="/nonexistent/libufpgd_gpu.so")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-1000:]
+    assert r.stdout.strip() == "raised"
