@@ -2,7 +2,7 @@
 every BASELINE config, on bounded seeded samples (development aid; bench.py
 times config 2 itself). Prints one line per config."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import paper_2304_12745_b200 as U
 from oracle import oracle as O

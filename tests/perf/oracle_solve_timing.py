@@ -1,7 +1,7 @@
 """oracle_solve at scale timing: FP64 device path vs the
 FP64 oracle on the host cores (development aid)."""
 import math, os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import paper_2304_12745_b200 as U
 from oracle import oracle as O

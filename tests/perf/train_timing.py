@@ -1,8 +1,8 @@
 """Training-loop timing (development aid): ufpgd::train on the device via
 build/train_dump vs the oracle's restated loop on the host cores, same data."""
 import math, os, subprocess, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 import numpy as np
 import paper_2304_12745_b200 as U
 from oracle import oracle as O
