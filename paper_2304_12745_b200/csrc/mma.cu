@@ -52,7 +52,7 @@ struct MmaShape {
   static constexpr int NW = NT / 32;
   static_assert(Q == 64 || Q == 128, "stage-1 MMA M must be 64 or 128");
   static_assert(M % 128 == 0 && NW <= 8 && K % 16 == 0, "");
-  // shared-memory byte offsets (all 1024-aligned)
+  // shared-memory byte offsets (16-byte aligned, as the no-swizzle layouts need)
   static constexpr int OFF_HH = 0;                       // H hi  [R x M] f16, core layout hoff()
   static constexpr int OFF_HL = OFF_HH + R * M * 2;      // H lo
   static constexpr int OFF_W = OFF_HL + R * M * 2;       // [W_hi; W_lo] [Q x M] f16, woff()
@@ -95,7 +95,7 @@ struct MmaShape {
   static __device__ __forceinline__ int woff(int q, int m) {
     return (m >> 3) * (16 * Q) + (q >> 3) * 128 + (m & 7) * 16 + (q & 7) * 2;
   }
-  // Bs: element (kk, n), K-major (K = kk, N = n): LBO (K-group) 128, SBO (N-group) 16 R.
+  // Bs: element (kk, n), K-major (K = kk, N = n): LBO (K-group) 128, SBO (N-group) BSBO.
   static __device__ __forceinline__ int boff(int kk, int n) {
     return (kk >> 3) * 128 + (n >> 3) * BSBO + (n & 7) * 16 + (kk & 7) * 2;
   }
