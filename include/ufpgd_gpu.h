@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define UFPGD_GPU_ABI_VERSION 1
+#define UFPGD_GPU_ABI_VERSION 2
 
 typedef struct {
   float re, im;
@@ -66,6 +66,28 @@ enum ufpgd_w0_mode {
 
 int ufpgd_gpu_abi_version(void);
 const char* ufpgd_gpu_last_error(void);
+
+/*
+ * Process-wide tuning / A-B options of the library. They are set only through
+ * this call (never read from the environment), take effect at the next launch
+ * and default to the measured-best choice. No reference counterpart: the
+ * reference has one CPU code path.
+ */
+enum ufpgd_option {
+  UFPGD_OPT_TENSOR_CORES = 0,   /* 1 (default): tcgen05 kernel at (16,128), (32,256); 0: FFMA2 tile kernel */
+  UFPGD_OPT_FUSED_WARPS = 1,    /* 0 (default): warps per fused-kernel block chosen per launch; 1..8: forced */
+  UFPGD_OPT_FP64_TEAM = 2,      /* 1 (default): warp-per-realization FP64 PGD at (8,64), (4,32); 0: general kernel */
+  UFPGD_OPT_ZERO_PAD = 3,       /* 1 (default): unsupported shapes run zero-padded on a fused shape; 0: general */
+  UFPGD_OPT_PAD_SUB_BYTES = 4,  /* padded-path sub-batch size in bytes of padded H (default 1 GiB) */
+  UFPGD_OPT_HOST_PIPE = 5,      /* host-buffer pipeline: 0 (default) phased, 1 depth-first streams */
+  UFPGD_OPT_HOST_CHUNK_BYTES = 6, /* host-buffer pipeline chunk in bytes of H (default 16 MiB) */
+  UFPGD_OPT_HOST_TIMELINE = 7,  /* 1: per-chunk event timeline of the host pipeline on stderr */
+  UFPGD_OPT_COUNT = 8
+};
+/* Returns UFPGD_EINVAL_PARAM for an unknown option or out-of-range value. */
+int ufpgd_gpu_set_option(int option, int64_t value);
+/* Current value, or INT64_MIN for an unknown option. */
+int64_t ufpgd_gpu_get_option(int option);
 int ufpgd_gpu_device_count(int* count);
 
 /*
@@ -216,20 +238,36 @@ int ufpgd_gpu_pgd_fixed_host(const ufpgd_c64* H, int64_t B, int K, int M, int po
                              float* eta_out, double* stats, double alpha, int device);
 
 /*
- * Single-process multi-GPU: shard the batch contiguously over devices
- * 0..ngpus-1 (one host thread and stream per device) and reduce the three
- * summary statistics with one ncclAllReduce over an NCCL communicator built by
- * ufpgd_gpu_init (ncclCommInitAll). Host buffers, synchronous.
- * ufpgd_gpu_shutdown destroys the communicators and releases the per-device
- * workspaces of the host-buffer entry points and the scratch pool of the
- * zero-padded forward (they are re-created on demand).
+ * Single-process multi-GPU — replaces the reference's parallel_for over
+ * channels (parallel.cpp:25-59, parallel.hpp:12-18) with devices
+ * 0..ngpus-1 of this process and one ncclAllReduce of the three summary
+ * statistics over the communicators built by ufpgd_gpu_init
+ * (ncclCommInitAll). ufpgd_gpu_shutdown destroys the communicators and
+ * releases the per-device workspaces of the host-buffer entry points and the
+ * scratch pool of the zero-padded forward (they are re-created on demand).
+ *
+ * _sharded: host buffers, synchronous. Contiguous shards [g B/G, (g+1) B/G),
+ * one host thread per device driving its pipelined host path; W0 (host,
+ * [B][M][K]) for w0_mode = GIVEN. Returns UFPGD_EDIVERGED when any
+ * realization diverged (per-realization indices in diverged_at).
+ *
+ * _sharded_device: every device's shard already resident (H[g], B[g]
+ * realizations on device g; W0[g], W[g], diverged_at[g] likewise), outputs on
+ * the same devices. stats[g] (device, 3 doubles) receives the GLOBAL sums
+ * after the in-place all-reduce — no host round trip. Asynchronous on
+ * streams[g] (NULL: the legacy default stream), like the single-device entry.
  */
 int ufpgd_gpu_init(int ngpus);
 int ufpgd_gpu_shutdown(void);
 int ufpgd_gpu_unfolded_forward_sharded(const ufpgd_c64* H, int64_t B, int K, int M,
                                        const double* lambda, const double* eta, int L,
-                                       const double* c, int w0_mode, ufpgd_c64* W,
+                                       const double* c, int w0_mode, const ufpgd_c64* W0, ufpgd_c64* W,
                                        int32_t* diverged_at, double* stats, double alpha);
+int ufpgd_gpu_unfolded_forward_sharded_device(const ufpgd_c64* const* H, const int64_t* B, int K, int M,
+                                              const double* lambda, const double* eta, int L, const double* c,
+                                              int w0_mode, const ufpgd_c64* const* W0, ufpgd_c64* const* W,
+                                              int32_t* const* diverged_at, double* const* stats, double alpha,
+                                              const ufpgd_stream_t* streams);
 
 /*
  * Training-step gradients — the per-sample body of

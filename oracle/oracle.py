@@ -54,6 +54,8 @@ def lib():
             "ora_rng_draw": (i, [u64, u64, i, i, i, P, P]),
             "ora_generate_channel": (i, [u64, u64, i, i, i, P]),
             "ora_power_v0": (i, [i, P]),
+            "ora_generate_channels_batch_f32": (i, [u64, u64, d, i64, i64, i, i, P, i]),
+            "ora_layer_params": (i, [u64, i, i, i, P, P]),
             "ora_prox_l21": (i, [P, i, i, d, P]),
             "ora_grad_f": (i, [P, P, P, i, i, P]),
             "ora_pgd_step": (i, [P, P, P, i, i, d, d, P]),
@@ -713,6 +715,25 @@ def pgd_batch_f32(H: np.ndarray, c: np.ndarray, lambda_: float, eta: np.ndarray,
     if rc != ORA_OK:
         raise ValueError(f"ora_pgd_batch_f32 failed: {rc}")
     return dict(W=W, diverged_at=div, iterations=its, l21=l21, active=act, tie_margin=tie)
+
+
+def generate_channels_batch_f32(seed_h: int, seed_g: int, gain_range_db: float, first: int, B: int, K: int,
+                                M: int, threads: int = 0) -> np.ndarray:
+    """The BASELINE workloads' seeded channels as complex64
+    [B][M][K]: channel.cpp:7-16 draws with log-uniform user gains."""
+    H = np.empty((B, M, K), dtype=np.complex64)
+    rc = lib().ora_generate_channels_batch_f32(seed_h, seed_g, float(gain_range_db), first, B, K, M, _p(H), threads)
+    if rc != ORA_OK:
+        raise ValueError("ora_generate_channels_batch_f32 failed")
+    return H
+
+
+def layer_params(seed_p: int, L: int, K: int, M: int):
+    """Raw seeded (lambda_l, mu_l) of SURVEY §8d (before project_params)."""
+    lam, eta = np.empty(L), np.empty(L)
+    if lib().ora_layer_params(seed_p, L, K, M, _p(lam), _p(eta)) != ORA_OK:
+        raise ValueError("ora_layer_params failed")
+    return lam, eta
 
 
 def power_iteration_batch_f32(H: np.ndarray, steps: int = 30, threads: int = 0):

@@ -480,6 +480,50 @@ int ora_generate_channel(std::uint64_t seed, std::uint64_t stream, int use_strea
   return ORA_OK;
 }
 
+// The BASELINE workloads' inputs, for the reference arm of
+// bench.py so that it touches nothing of the product library: realization
+// first+b is generate_channel(Rng::stream(seed_h, first+b)) (channel.cpp:7-16)
+// with row k scaled in FP64 by 10^(-u_k R / 20), u_k drawn from
+// Rng::stream(seed_g, first+b), then rounded once to complex64 [B][M][K].
+int ora_generate_channels_batch_f32(std::uint64_t seed_h, std::uint64_t seed_g, double gain_range_db,
+                                    std::int64_t first, std::int64_t B, int K, int M, float* H, int threads) {
+  if (B < 0 || K < 1 || M < K || !(gain_range_db >= 0.0)) return ORA_EINVAL;
+  const std::size_t n = static_cast<std::size_t>(K) * M;
+  parallel_for(static_cast<std::size_t>(B), [&](std::size_t b) {
+    const std::uint64_t idx = static_cast<std::uint64_t>(first) + b;
+    std::vector<double> gain(K, 1.0);
+    if (gain_range_db > 0.0) {
+      Rng g = Rng::stream(seed_g, idx);
+      for (int k = 0; k < K; ++k) gain[k] = std::pow(10.0, -g.uniform() * gain_range_db / 20.0);
+    }
+    Rng r = Rng::stream(seed_h, idx);
+    float* h = H + 2 * n * b;
+    for (int k = 0; k < K; ++k)
+      for (int m = 0; m < M; ++m) {
+        const cd z = r.complex_gaussian();
+        h[2 * (static_cast<std::size_t>(m) * K + k)] = static_cast<float>(z.real() * gain[k]);
+        h[2 * (static_cast<std::size_t>(m) * K + k) + 1] = static_cast<float>(z.imag() * gain[k]);
+      }
+  }, threads);
+  return ORA_OK;
+}
+
+// Seeded layer parameters of the BASELINE configs, pack order (lambda_0,
+// mu_0, lambda_1, ...) from Rng::stream(seed_p, 0): lambda = 0.01 + 0.09 u,
+// mu = (0.5 + u) / mp_bound(K, M) — raw, before project_params. No FMA
+// contraction (-march=x86-64-v3 would fuse 0.01 + 0.09 u into one rounding).
+__attribute__((optimize("fp-contract=off"))) int ora_layer_params(std::uint64_t seed_p, int L, int K, int M, double* lambda, double* eta) {
+  if (L < 0 || K < 1 || M < 1) return ORA_EINVAL;
+  const double edge = std::sqrt(static_cast<double>(K)) + std::sqrt(static_cast<double>(M));
+  const double mp = edge * edge;
+  Rng r = Rng::stream(seed_p, 0);
+  for (int l = 0; l < L; ++l) {
+    lambda[l] = 0.01 + 0.09 * r.uniform();
+    eta[l] = (0.5 + r.uniform()) / mp;
+  }
+  return ORA_OK;
+}
+
 int ora_power_v0(int M, double* v0) {
   if (M < 1) return ORA_EINVAL;
   power_v0(M, as_c(v0));

@@ -22,10 +22,14 @@ from .capi import (  # noqa: F401
     W0_GIVEN,
     W0_ZERO,
     abi_version,
+    get_option,
+    options,
+    set_option,
     fp32_peak,
     init_multi_gpu,
     shutdown_multi_gpu,
     unfolded_forward_sharded,
+    unfolded_forward_sharded_device,
     generate_channels,
     generate_channels_device,
     layer_params,

@@ -62,6 +62,8 @@ def lib():
         i, d, i64, u64, P = C.c_int, C.c_double, C.c_int64, C.c_uint64, C.c_void_p
         sigs = {
             "ufpgd_gpu_abi_version": (i, []),
+            "ufpgd_gpu_set_option": (i, [i, i64]),
+            "ufpgd_gpu_get_option": (i64, [i]),
             "ufpgd_gpu_last_error": (C.c_char_p, []),
             "ufpgd_gpu_device_count": (i, [P]),
             "ufpgd_gpu_unfolded_forward": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, P, P, P, d, i, P]),
@@ -84,7 +86,8 @@ def lib():
             "ufpgd_gpu_unfolded_backward64": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, i, P]),
             "ufpgd_gpu_init": (i, [i]),
             "ufpgd_gpu_shutdown": (i, []),
-            "ufpgd_gpu_unfolded_forward_sharded": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, d]),
+            "ufpgd_gpu_unfolded_forward_sharded": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, P, d]),
+            "ufpgd_gpu_unfolded_forward_sharded_device": (i, [P, P, i, i, P, P, i, P, i, P, P, P, P, d, P]),
             "ufpgd_gpu_lipschitz_exact": (i, [P, i64, i, i, P, P, i, P]),
             "ufpgd_power_v0_f64": (i, [i, P]),
             "ufpgd_generate_channels": (i, [u64, u64, d, i64, i64, i, i, P, i]),
@@ -102,6 +105,44 @@ def lib():
 
 def abi_version() -> int:
     return lib().ufpgd_gpu_abi_version()
+
+
+# ufpgd_gpu_set_option ids (include/ufpgd_gpu.h): explicit, process-wide
+# tuning / A-B switches; the library never reads them from the environment.
+OPTIONS = {"tensor_cores": 0, "fused_warps": 1, "fp64_team": 2, "zero_pad": 3, "pad_sub_bytes": 4,
+           "host_pipe": 5, "host_chunk_bytes": 6, "host_timeline": 7}
+
+
+def set_option(name: str, value: int) -> None:
+    if name not in OPTIONS:
+        raise ValueError(f"unknown option {name!r}")
+    _check(lib().ufpgd_gpu_set_option(OPTIONS[name], int(value)))
+
+
+def get_option(name: str) -> int:
+    if name not in OPTIONS:
+        raise ValueError(f"unknown option {name!r}")
+    return int(lib().ufpgd_gpu_get_option(OPTIONS[name]))
+
+
+class options:
+    """Context manager: ``with options(tensor_cores=0): ...`` sets library
+    options for the block and restores the previous values."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.old[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            set_option(k, v)
+        return False
 
 
 def _check(rc: int, diverged=None, index_base: int = 0):
@@ -134,11 +175,17 @@ def _f64(a) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(-1))
 
 
-def _stream_ptr(stream) -> Optional[int]:
+def _stream_ptr(stream, device=None) -> Optional[int]:
+    """The launch stream: ``stream`` or the current stream OF THE TENSOR'S
+    DEVICE (the C ABI launches on that device; another device's stream handle
+    would be rejected as an invalid resource)."""
     import torch
 
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        if device is not None and stream.device != device:
+            raise ValueError(f"stream is on {stream.device}, the batch on {device}")
+        return stream.cuda_stream
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 def _check_batch(H):
@@ -149,6 +196,37 @@ def _check_batch(H):
         raise ValueError("H must be a contiguous CUDA complex64 tensor [B, M, K]")
     B, M, K = H.shape
     return B, K, M
+
+
+def _check_like(t, H, name: str):
+    """A device operand the kernels index like H (W0, out): same shape,
+    dtype, device and contiguity, else the reference's shape error
+    (unfolded.cpp:96-99, pgd.cpp:184-187) instead of an out-of-bounds access."""
+    import torch
+
+    if t is None:
+        return
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.device == H.device and t.dtype == H.dtype
+            and tuple(t.shape) == tuple(H.shape) and t.is_contiguous()):
+        raise ValueError(f"{name} shape mismatch: need a contiguous {H.dtype} tensor {tuple(H.shape)} on {H.device}")
+
+
+def _check_host_like(a, H, name: str):
+    """Host operand (W0, out) of the host-buffer entry points: C-contiguous
+    complex64 numpy array of H's shape."""
+    if a is None:
+        return
+    if not (isinstance(a, np.ndarray) and a.dtype == np.complex64 and a.shape == H.shape and a.flags.c_contiguous
+            and (name != "out" or a.flags.writeable)):
+        raise ValueError(f"{name} shape mismatch: need a C-contiguous complex64 array {H.shape}")
+
+
+def _check_w0(w0_mode: int, W0, H, host: bool = False):
+    if w0_mode not in (W0_ZERO, W0_CONJ_H, W0_GIVEN):
+        raise ValueError(f"w0_mode must be 0, 1 or 2 (got {w0_mode})")
+    if w0_mode == W0_GIVEN and W0 is None:
+        raise ValueError("w0_mode = W0_GIVEN needs W0")
+    (_check_host_like if host else _check_like)(W0, H, "W0")
 
 
 def unfolded_forward(H, lambda_, eta, c, *, w0_mode: int = W0_ZERO, W0=None, alpha: float = 1.0,
@@ -167,6 +245,8 @@ def unfolded_forward(H, lambda_, eta, c, *, w0_mode: int = W0_ZERO, W0=None, alp
     lam, et, cc = _f64(lambda_), _f64(eta), _f64(c)
     if lam.size != et.size:
         raise ValueError("lambda and eta must have one entry per layer")
+    _check_w0(w0_mode, W0, H)
+    _check_like(out, H, "out")
     dev = H.device
     W = out if out is not None else torch.empty_like(H)
     div = torch.empty(B, dtype=torch.int32, device=dev)
@@ -175,7 +255,7 @@ def unfolded_forward(H, lambda_, eta, c, *, w0_mode: int = W0_ZERO, W0=None, alp
     stats = torch.empty(3, dtype=torch.float64, device=dev) if want_stats else None
     rc = lib().ufpgd_gpu_unfolded_forward(
         _ptr(H), B, K, M, _ptr(lam), _ptr(et), lam.size, _ptr(cc), w0_mode, _ptr(W0), _ptr(W), _ptr(div),
-        _ptr(l21), _ptr(act), _ptr(stats), float(alpha), dev.index or 0, _stream_ptr(stream))
+        _ptr(l21), _ptr(act), _ptr(stats), float(alpha), dev.index or 0, _stream_ptr(stream, dev))
     _check(rc)
     return dict(W=W, diverged_at=div, l21=l21, active=act, stats=stats)
 
@@ -187,8 +267,10 @@ def power_iteration(H, steps: int = 30, v0=None, stream=None):
     B, K, M = _check_batch(H)
     Lout = torch.empty(B, dtype=torch.float32, device=H.device)
     v = None if v0 is None else np.ascontiguousarray(v0, dtype=np.complex64)
+    if v is not None and v.shape != (M,):
+        raise ValueError(f"v0 must have M = {M} entries")
     rc = lib().ufpgd_gpu_power_iteration(_ptr(H), B, K, M, _ptr(v), steps, _ptr(Lout), H.device.index or 0,
-                                         _stream_ptr(stream))
+                                         _stream_ptr(stream, H.device))
     _check(rc)
     return Lout
 
@@ -202,6 +284,10 @@ def pgd_fixed(H, lambda_: float, iters: int, c, *, eta=None, power_steps: int = 
 
     B, K, M = _check_batch(H)
     cc = _f64(c)
+    _check_w0(w0_mode, W0, H)
+    if eta is not None and not (isinstance(eta, torch.Tensor) and eta.is_cuda and eta.device == H.device
+                                and eta.dtype == torch.float32 and tuple(eta.shape) == (B,) and eta.is_contiguous()):
+        raise ValueError(f"eta must be a contiguous CUDA float32 tensor [{B}] on {H.device}")
     dev = H.device
     W = torch.empty_like(H)
     div = torch.empty(B, dtype=torch.int32, device=dev)
@@ -212,7 +298,7 @@ def pgd_fixed(H, lambda_: float, iters: int, c, *, eta=None, power_steps: int = 
     rc = lib().ufpgd_gpu_pgd_fixed(_ptr(H), B, K, M, _ptr(eta), power_steps, float(lambda_), int(iters),
                                    _ptr(cc), w0_mode, _ptr(W0), _ptr(W), _ptr(div), _ptr(l21), _ptr(act),
                                    _ptr(eta_out), _ptr(stats), float(alpha), dev.index or 0,
-                                   _stream_ptr(stream))
+                                   _stream_ptr(stream, dev))
     _check(rc)
     return dict(W=W, diverged_at=div, eta=eta_out, l21=l21, active=act, stats=stats)
 
@@ -226,6 +312,7 @@ def layers_general(H, eta, thr, c, *, w0_mode: int = W0_CONJ_H, W0=None, mode: i
 
     B, K, M = _check_batch(H)
     et, th, cc = _f64(eta), _f64(thr), _f64(c)
+    _check_w0(w0_mode, W0, H)
     L = 1 if mode == 1 else et.size
     dev = H.device
     W = torch.empty_like(H)
@@ -238,7 +325,7 @@ def layers_general(H, eta, thr, c, *, w0_mode: int = W0_CONJ_H, W0=None, mode: i
     rc = lib().ufpgd_gpu_layers_general(
         _ptr(H), B, K, M, _ptr(et), _ptr(th), L, _ptr(cc), w0_mode, _ptr(W0), mode, float(residual_tol),
         index_base, _ptr(W), _ptr(div), _ptr(its), _ptr(itr), _ptr(tv), _ptr(tn), _ptr(ts),
-        dev.index or 0, _stream_ptr(stream))
+        dev.index or 0, _stream_ptr(stream, dev))
     _check(rc)
     return dict(W=W, diverged_at=div, iterations=its, iterates=itr, tape_v=tv, tape_norms=tn,
                 tape_shrink=ts)
@@ -253,6 +340,8 @@ def unfolded_forward_host(H: np.ndarray, lambda_, eta, c, *, w0_mode: int = W0_Z
         raise ValueError("H must be a C-contiguous complex64 array [B, M, K]")
     B, M, K = H.shape
     lam, et, cc = _f64(lambda_), _f64(eta), _f64(c)
+    _check_w0(w0_mode, W0, H, host=True)
+    _check_host_like(out, H, "out")
     W = out if out is not None else np.empty_like(H)
     div = np.empty(B, dtype=np.int32)
     stats = np.zeros(3)
@@ -273,6 +362,7 @@ def pgd_fixed_host(H: np.ndarray, lambda_: float, iters: int, c, *, power_steps:
         raise ValueError("H must be a C-contiguous complex64 array [B, M, K]")
     B, M, K = H.shape
     cc = _f64(c)
+    _check_w0(w0_mode, W0, H, host=True)
     W = np.empty_like(H)
     div = np.empty(B, dtype=np.int32)
     eta = np.empty(B, dtype=np.float32)
@@ -298,7 +388,7 @@ def lipschitz_exact(H, stream=None):
     Lout = torch.empty(B, dtype=torch.float64, device=H.device)
     st = torch.empty(B, dtype=torch.int32, device=H.device)
     _check(lib().ufpgd_gpu_lipschitz_exact(_ptr(H), B, K, M, _ptr(Lout), _ptr(st), H.device.index or 0,
-                                           _stream_ptr(stream)))
+                                           _stream_ptr(stream, H.device)))
     return Lout, st
 
 
@@ -309,13 +399,12 @@ def metrics(H, W, c, *, sigma_nu: float = 1.0, alpha: float = 1.0, want_zf: bool
     import torch
 
     B, K, M = _check_batch(H)
-    if W.shape != H.shape or W.dtype != H.dtype or not W.is_cuda:
-        raise ValueError("W must match H")
+    _check_like(W, H, "W")
     cc = _f64(c)
     out = torch.empty((B, 6 + K), dtype=torch.float64, device=H.device)
     zf = torch.empty_like(H) if want_zf else None
     _check(lib().ufpgd_gpu_metrics(_ptr(H), _ptr(W), B, K, M, _ptr(cc), float(sigma_nu), float(alpha), _ptr(out),
-                                   _ptr(zf), H.device.index or 0, _stream_ptr(stream)))
+                                   _ptr(zf), H.device.index or 0, _stream_ptr(stream, H.device)))
     return dict(out=out, zf=zf)
 
 
@@ -328,13 +417,14 @@ def unfolded_grad(H, lambda_, eta, c, *, w0_mode: int = W0_CONJ_H, loss_kind: in
 
     B, K, M = _check_batch(H)
     lam, et, cc = _f64(lambda_), _f64(eta), _f64(c)
+    _check_like(labels, H, "labels")
     L = lam.size
     loss = torch.empty(B, dtype=torch.float64, device=H.device)
     grads = torch.empty((B, 2 * L), dtype=torch.float64, device=H.device)
     mean = torch.empty(1 + 2 * L, dtype=torch.float64, device=H.device)
     _check(lib().ufpgd_gpu_unfolded_grad(_ptr(H), B, K, M, _ptr(lam), _ptr(et), L, _ptr(cc), w0_mode, loss_kind,
                                          float(lambda_cost), _ptr(labels), _ptr(loss), _ptr(grads), _ptr(mean),
-                                         H.device.index or 0, _stream_ptr(stream)))
+                                         H.device.index or 0, _stream_ptr(stream, H.device)))
     return dict(loss=loss, grads=grads, mean=mean)
 
 
@@ -406,7 +496,7 @@ def oracle_solve(H, c, lambda_: float, *, max_iters: int = 100000, residual_tol:
     st = torch.empty(B, dtype=torch.int32, device=H.device)
     _check(lib().ufpgd_gpu_oracle_solve(_ptr(H), B, K, M, _ptr(_f64(c)), float(lambda_), int(max_iters),
                                         float(residual_tol), _ptr(W), _ptr(eta), _ptr(its), _ptr(st),
-                                        H.device.index or 0, _stream_ptr(stream)))
+                                        H.device.index or 0, _stream_ptr(stream, H.device)))
     return dict(W=W, eta=eta, iterations=its, status=st)
 
 
@@ -426,23 +516,69 @@ def shutdown_multi_gpu():
     _check(lib().ufpgd_gpu_shutdown())
 
 
-def unfolded_forward_sharded(H: np.ndarray, lambda_, eta, c, *, w0_mode: int = W0_ZERO, alpha: float = 1.0,
-                             raise_on_divergence: bool = True):
+def unfolded_forward_sharded(H: np.ndarray, lambda_, eta, c, *, w0_mode: int = W0_ZERO, W0=None,
+                             alpha: float = 1.0, raise_on_divergence: bool = True):
     """Single-process multi-GPU forward over the devices given to
-    init_multi_gpu: contiguous shards, one NCCL all-reduce of the statistics."""
+    init_multi_gpu, from host buffers: contiguous shards, one NCCL all-reduce
+    of the statistics."""
     H = np.asarray(H)
     if H.dtype != np.complex64 or H.ndim != 3 or not H.flags.c_contiguous:
         raise ValueError("H must be a C-contiguous complex64 array [B, M, K]")
     B, M, K = H.shape
     lam, et, cc = _f64(lambda_), _f64(eta), _f64(c)
+    _check_w0(w0_mode, W0, H, host=True)
     W = np.empty_like(H)
     div = np.empty(B, dtype=np.int32)
     stats = np.zeros(3)
     rc = lib().ufpgd_gpu_unfolded_forward_sharded(_ptr(H), B, K, M, _ptr(lam), _ptr(et), lam.size, _ptr(cc),
-                                                  w0_mode, _ptr(W), _ptr(div), _ptr(stats), float(alpha))
+                                                  w0_mode, _ptr(W0), _ptr(W), _ptr(div), _ptr(stats), float(alpha))
     if rc == EDIVERGED and not raise_on_divergence:
         rc = OK
     _check(rc, div)
+    return dict(W=W, diverged_at=div, stats=stats)
+
+
+def unfolded_forward_sharded_device(shards, lambda_, eta, c, *, w0_mode: int = W0_ZERO, W0=None,
+                                    alpha: float = 1.0, streams=None):
+    """Single-process multi-GPU forward over device-resident shards: shards[g]
+    is a CUDA complex64 tensor [B_g, M, K] on device g (g < the count given to
+    init_multi_gpu); W0 likewise for W0_GIVEN. Asynchronous on streams[g] (the
+    current stream of each device by default). Returns dict of per-device
+    lists W, diverged_at, stats — every stats[g] holds the global sums after
+    the in-place NCCL all-reduce."""
+    import torch
+
+    G = len(shards)
+    if G == 0:
+        raise ValueError("need one shard per device")
+    K = M = None
+    for g, t in enumerate(shards):
+        B, K_, M_ = _check_batch(t)
+        if t.device.index != g:
+            raise ValueError(f"shard {g} must live on cuda:{g}")
+        if K is None:
+            K, M = K_, M_
+        elif (K_, M_) != (K, M):
+            raise ValueError("all shards need the same (K, M)")
+    if W0 is not None:
+        if len(W0) != G:
+            raise ValueError("W0 needs one tensor per shard")
+        for g in range(G):
+            _check_like(W0[g], shards[g], "W0")
+    if w0_mode == W0_GIVEN and W0 is None:
+        raise ValueError("w0_mode = W0_GIVEN needs W0")
+    lam, et, cc = _f64(lambda_), _f64(eta), _f64(c)
+    W = [torch.empty_like(t) for t in shards]
+    div = [torch.empty(t.shape[0], dtype=torch.int32, device=t.device) for t in shards]
+    stats = [torch.empty(3, dtype=torch.float64, device=t.device) for t in shards]
+    arr = lambda xs: (C.c_void_p * G)(*[_ptr(x) for x in xs])  # noqa: E731
+    Bs = (C.c_int64 * G)(*[t.shape[0] for t in shards])
+    st = (C.c_void_p * G)(*[_stream_ptr(None if streams is None else streams[g], shards[g].device)
+                            for g in range(G)])
+    rc = lib().ufpgd_gpu_unfolded_forward_sharded_device(
+        arr(shards), Bs, K, M, _ptr(lam), _ptr(et), lam.size, _ptr(cc), w0_mode,
+        None if W0 is None else arr(W0), arr(W), arr(div), arr(stats), float(alpha), st)
+    _check(rc)
     return dict(W=W, diverged_at=div, stats=stats)
 
 
@@ -471,7 +607,7 @@ def generate_channels_device(seed_h: int, seed_g: int, gain_range_db: float, fir
     if out is not None and not (H.is_cuda and H.dtype == dt and tuple(H.shape) == (B, M, K) and H.is_contiguous()):
         raise ValueError("out must be a contiguous CUDA tensor [B, M, K] of the requested dtype")
     rc = lib().ufpgd_gpu_generate_channels(seed_h, seed_g, float(gain_range_db), first_index, B, K, M, _ptr(H),
-                                           int(dt == torch.complex128), H.device.index or 0, _stream_ptr(stream))
+                                           int(dt == torch.complex128), H.device.index or 0, _stream_ptr(stream, H.device))
     _check(rc)
     return H
 
@@ -491,7 +627,7 @@ def unfolded_backward64(H, lambda_, eta, c, dcost_dw, *, w0_mode: int = W0_CONJ_
     grads = torch.empty((B, 2 * lam.size), dtype=torch.float64, device=H.device)
     _check(lib().ufpgd_gpu_unfolded_backward64(_ptr(H), B, K, M, _ptr(lam), _ptr(et), lam.size, _ptr(cc), w0_mode,
                                                _ptr(W0), _ptr(dcost_dw), _ptr(grads), H.device.index or 0,
-                                               _stream_ptr(stream)))
+                                               _stream_ptr(stream, H.device)))
     return grads
 
 

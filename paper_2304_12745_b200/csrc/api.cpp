@@ -779,7 +779,7 @@ BatchResult forward_batch_multi_gpu(const UnfoldedNetwork& net, const std::compl
   const RealVector c = cfg.constraint_diag();
   const int rc = ufpgd_gpu_unfolded_forward_sharded(
       reinterpret_cast<const ufpgd_c64*>(channels), B, cfg.K, cfg.M, lam.data(), eta.data(),
-      static_cast<int>(lam.size()), c.data(), UFPGD_W0_CONJ_H, reinterpret_cast<ufpgd_c64*>(r.precoders.data()),
+      static_cast<int>(lam.size()), c.data(), UFPGD_W0_CONJ_H, nullptr, reinterpret_cast<ufpgd_c64*>(r.precoders.data()),
       r.diverged_at.data(), stats, cfg.alpha);
   if (rc != UFPGD_OK && rc != UFPGD_EDIVERGED) raise(rc);
   r.consumed_power_sum = stats[0];

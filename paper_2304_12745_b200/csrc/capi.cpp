@@ -5,6 +5,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -18,6 +19,24 @@
 #include "ufpgd_internal.h"
 
 using namespace ufpgd_gpu_impl;
+
+// ---- library options (ufpgd_gpu_set_option) -----------------------------------
+namespace {
+std::atomic<int64_t> g_options[UFPGD_OPT_COUNT] = {
+    1,           // UFPGD_OPT_TENSOR_CORES
+    0,           // UFPGD_OPT_FUSED_WARPS (auto)
+    1,           // UFPGD_OPT_FP64_TEAM
+    1,           // UFPGD_OPT_ZERO_PAD
+    1ll << 30,   // UFPGD_OPT_PAD_SUB_BYTES
+    0,           // UFPGD_OPT_HOST_PIPE (phased)
+    16ll << 20,  // UFPGD_OPT_HOST_CHUNK_BYTES
+    0,           // UFPGD_OPT_HOST_TIMELINE
+};
+}  // namespace
+
+namespace ufpgd_gpu_impl {
+int64_t option(int id) { return g_options[id].load(std::memory_order_relaxed); }
+}  // namespace ufpgd_gpu_impl
 
 namespace {
 
@@ -47,6 +66,17 @@ struct DeviceGuard {
     ok = cudaSetDevice(dev) == cudaSuccess;
   }
   ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Saves the caller's current device and restores it on scope exit.
+struct DeviceRestore {
+  int prev = -1;
+  DeviceRestore() {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  }
+  ~DeviceRestore() {
     if (prev >= 0) cudaSetDevice(prev);
   }
 };
@@ -108,12 +138,30 @@ cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
       props.location.id = dev;
       e = cudaMemPoolCreate(&g_pool[dev], &props);
       if (e != cudaSuccess) return e;
-      unsigned long long keep = ~0ULL;
+      // Keep up to 1 GiB mapped across calls (re-mapping the scratch of every
+      // padded call made it 2x slower); memory above that goes back to the
+      // device at the next synchronisation, so other users of HBM get it back.
+      unsigned long long keep = 1ull << 30;
       cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &keep);
     }
   }
   return cudaMallocFromPoolAsync(p, bytes, g_pool[dev], s);
 }
+
+}  // namespace
+
+namespace ufpgd_gpu_impl {
+// Stream-ordered scratch that stays mapped across calls (the private pool
+// above); during stream capture the graph's own allocator is used instead.
+cudaError_t scratch_alloc_async(void** p, size_t bytes, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+    return cudaMallocAsync(p, bytes, s);
+  return scratch_alloc(p, bytes, s);
+}
+}  // namespace ufpgd_gpu_impl
+
+namespace {
 
 void release_pool(int dev) {
   std::lock_guard<std::mutex> lock(g_pool_mu);
@@ -124,13 +172,10 @@ void release_pool(int dev) {
   }
 }
 
-long long pad_sub_bytes() {
-  const char* v = std::getenv("UFPGD_PAD_SUB_MB");  // tests: force several sub-batches
-  return (v ? std::max(1LL, std::atoll(v)) : 1024LL) << 20;
-}
+long long pad_sub_bytes() { return option(UFPGD_OPT_PAD_SUB_BYTES); }
 
 bool padded_shape(int K, int M, int* Kp, int* Mp) {
-  if (std::getenv("UFPGD_NO_PAD")) return false;
+  if (option(UFPGD_OPT_ZERO_PAD) == 0) return false;
   static const int shapes[][2] = {{4, 16}, {4, 32}, {4, 64}, {8, 32}, {8, 64}, {8, 128}, {16, 128}, {32, 256}};
   double best = 6.0 * K * K * M;
   bool found = false;
@@ -306,6 +351,63 @@ bool load_nccl() {
          g_nccl.CommDestroy;
 }
 
+// In-place sum of a 3-double statistics buffer per device over the
+// communicators of ufpgd_gpu_init (caller holds g_nccl_mu). Leaves the
+// caller's current device unchanged.
+int allreduce_stats(double* const* dstats, const cudaStream_t* streams, int G) {
+  DeviceRestore keep;
+  g_nccl.GroupStart();
+  ncclResult_t first = 0;
+  for (int gi = 0; gi < G; ++gi) {
+    cudaSetDevice(gi);
+    ncclResult_t r = g_nccl.AllReduce(dstats[gi], dstats[gi], 3, kNcclDouble, kNcclSum, g_comms[gi], streams[gi]);
+    if (r != 0 && first == 0) first = r;
+  }
+  ncclResult_t end = g_nccl.GroupEnd();
+  if (first == 0) first = end;
+  if (first != 0)
+    return fail(UFPGD_ENCCL, std::string("ncclAllReduce: ") + (g_nccl.GetErrorString ? g_nccl.GetErrorString(first) : "?"));
+  return UFPGD_OK;
+}
+
+// Per-device streams and 3-double statistics buffers of one sharded call,
+// released on every exit path; the caller's current device is restored.
+struct ShardSet {
+  int G;
+  bool ok = true;
+  std::vector<cudaStream_t> streams;
+  std::vector<double*> dstats;
+  explicit ShardSet(int g) : G(g), streams(g, nullptr), dstats(g, nullptr) {
+    DeviceRestore keep;
+    for (int gi = 0; gi < G && ok; ++gi) {
+      cudaSetDevice(gi);
+      ok = cudaStreamCreateWithFlags(&streams[gi], cudaStreamNonBlocking) == cudaSuccess &&
+           cudaMalloc(&dstats[gi], 3 * sizeof(double)) == cudaSuccess;
+    }
+  }
+  ~ShardSet() {
+    DeviceRestore keep;
+    for (int gi = 0; gi < G; ++gi) {
+      cudaSetDevice(gi);
+      if (streams[gi]) cudaStreamSynchronize(streams[gi]);
+      if (dstats[gi]) cudaFree(dstats[gi]);
+      if (streams[gi]) cudaStreamDestroy(streams[gi]);
+    }
+  }
+  int allreduce() { return allreduce_stats(dstats.data(), streams.data(), G); }
+  int sync_and_read(double* out) {
+    DeviceRestore keep;
+    for (int gi = 0; gi < G; ++gi) {
+      cudaSetDevice(gi);
+      if (cudaStreamSynchronize(streams[gi]) != cudaSuccess) return fail(UFPGD_ECUDA, "sharded stream sync");
+    }
+    cudaSetDevice(0);
+    if (cudaMemcpy(out, dstats[0], 3 * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return fail(UFPGD_ECUDA, "statistics read");
+    return UFPGD_OK;
+  }
+};
+
 // Per-device workspace of the host-buffer path: NS streams and grow-only
 // device buffers, kept across calls so an end-to-end call costs only its
 // copies and kernels. Host calls on one device are serialised by its mutex.
@@ -340,12 +442,8 @@ cudaError_t ensure(void*& p, size_t& cap, size_t need) {
   return e;
 }
 
-// Pipeline chunk size in bytes of H (UFPGD_HOST_CHUNK_MB overrides, for tuning).
-long long host_chunk_bytes(long long default_mb) {
-  long long mb = default_mb;
-  if (const char* v = std::getenv("UFPGD_HOST_CHUNK_MB")) mb = std::max(1LL, std::atoll(v));
-  return mb << 20;
-}
+// Pipeline chunk size in bytes of H (UFPGD_OPT_HOST_CHUNK_BYTES).
+long long host_chunk_bytes() { return option(UFPGD_OPT_HOST_CHUNK_BYTES); }
 
 // Releases a device's host-path workspace (ufpgd_gpu_shutdown).
 void release_workspace(HostWorkspace& ws) {
@@ -438,12 +536,11 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
   // with an H2D: PCIe then splits evenly between the directions (~48 GB/s
   // each), whereas a D2H started mid-way through an H2D takes the larger share
   // and slows the H2D stream that paces the pipeline (tools/pipe_probe2.py:
-  // 88.8 vs 81.9 GB/s total). UFPGD_HOST_PIPE=streams selects the earlier
+  // 88.8 vs 81.9 GB/s total). UFPGD_OPT_HOST_PIPE = 1 selects the earlier
   // depth-first pipeline over four streams, for A/B runs.
-  const char* pipe_env = std::getenv("UFPGD_HOST_PIPE");
-  const bool phased = !(pipe_env && std::strcmp(pipe_env, "streams") == 0);
-  // UFPGD_HOST_TIMELINE=1: per-chunk event timeline on stderr (tuning aid)
-  const bool timeline = std::getenv("UFPGD_HOST_TIMELINE") != nullptr;
+  const bool phased = option(UFPGD_OPT_HOST_PIPE) == 0;
+  // UFPGD_OPT_HOST_TIMELINE = 1: per-chunk event timeline on stderr (tuning aid)
+  const bool timeline = option(UFPGD_OPT_HOST_TIMELINE) != 0;
   std::vector<cudaEvent_t> tev(timeline ? 4 * nchunks : 0);
   for (cudaEvent_t& ev : tev) cudaEventCreate(&ev);
   // Buffer set i = chunk % NS; events: 0 = copy-in done, 1 = kernel done,
@@ -577,6 +674,29 @@ extern "C" {
 
 int ufpgd_gpu_abi_version(void) { return UFPGD_GPU_ABI_VERSION; }
 
+int ufpgd_gpu_set_option(int option, int64_t value) {
+  bool ok = false;
+  switch (option) {
+    case UFPGD_OPT_TENSOR_CORES:
+    case UFPGD_OPT_FP64_TEAM:
+    case UFPGD_OPT_ZERO_PAD:
+    case UFPGD_OPT_HOST_PIPE:
+    case UFPGD_OPT_HOST_TIMELINE: ok = value == 0 || value == 1; break;
+    case UFPGD_OPT_FUSED_WARPS: ok = value >= 0 && value <= 8; break;
+    case UFPGD_OPT_PAD_SUB_BYTES:
+    case UFPGD_OPT_HOST_CHUNK_BYTES: ok = value >= (1ll << 20) && value <= (1ll << 40); break;
+    default: return fail(UFPGD_EINVAL_PARAM, "unknown option " + std::to_string(option));
+  }
+  if (!ok) return fail(UFPGD_EINVAL_PARAM, "option " + std::to_string(option) + ": value out of range");
+  g_options[option].store(value, std::memory_order_relaxed);
+  return UFPGD_OK;
+}
+
+int64_t ufpgd_gpu_get_option(int option) {
+  if (option < 0 || option >= UFPGD_OPT_COUNT) return INT64_MIN;
+  return g_options[option].load(std::memory_order_relaxed);
+}
+
 const char* ufpgd_gpu_last_error(void) { return g_last_error.c_str(); }
 
 int ufpgd_gpu_device_count(int* count) {
@@ -606,7 +726,7 @@ int ufpgd_gpu_unfolded_forward(const ufpgd_c64* H, int64_t B, int K, int M, cons
   const bool fused = fused_supported(K, M) && L >= 1;
   const long long np = partial_count(B, K, M, fused);
   double* partials = nullptr;
-  if (stats) UFPGD_CUDA(cudaMallocAsync(&partials, sizeof(double) * 3 * np, s));
+  if (stats) UFPGD_CUDA(scratch_alloc_async(reinterpret_cast<void**>(&partials), sizeof(double) * 3 * np, s));
   long long used = 0;
   rc = enqueue_unfolded(reinterpret_cast<const float2*>(H), B, K, M, lambda, eta, L, c, w0_mode,
                         reinterpret_cast<const float2*>(W0), reinterpret_cast<float2*>(W),
@@ -795,7 +915,7 @@ int ufpgd_gpu_pgd_fixed(const ufpgd_c64* H, int64_t B, int K, int M, const float
   const long long np = partial_count(B, K, M, fused);
   long long used = B;
   double* partials = nullptr;
-  if (stats) UFPGD_CUDA(cudaMallocAsync(&partials, sizeof(double) * 3 * np, s));
+  if (stats) UFPGD_CUDA(scratch_alloc_async(reinterpret_cast<void**>(&partials), sizeof(double) * 3 * np, s));
   rc = enqueue_pgd(reinterpret_cast<const float2*>(H), B, K, M, eta_in, power_steps, lambda, iters, c, w0_mode,
                    reinterpret_cast<const float2*>(W0), reinterpret_cast<float2*>(W), diverged_at, l21, active,
                    eta_out, partials, alpha, device, s, &used);
@@ -1013,7 +1133,7 @@ int ufpgd_gpu_unfolded_forward_host(const ufpgd_c64* H, int64_t B, int K, int M,
   if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
   const bool fused = fused_supported(K, M) && L >= 1;
   // 16 MiB of H per chunk: short pipeline fill, chunks still fill the GPU.
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, host_chunk_bytes(16) / (8ll * K * M)));
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, host_chunk_bytes() / (8ll * K * M)));
   const long long ppc = partial_count(chunk, K, M, fused);
   return host_pipeline(
       device, H, B, K, M, w0_mode == UFPGD_W0_GIVEN ? W0 : nullptr, W, diverged_at, nullptr, ppc, chunk, stats,
@@ -1229,59 +1349,88 @@ int ufpgd_gpu_shutdown(void) {
 
 int ufpgd_gpu_unfolded_forward_sharded(const ufpgd_c64* H, int64_t B, int K, int M,
                                        const double* lambda, const double* eta, int L,
-                                       const double* c, int w0_mode, ufpgd_c64* W,
+                                       const double* c, int w0_mode, const ufpgd_c64* W0, ufpgd_c64* W,
                                        int32_t* diverged_at, double* stats, double alpha) {
   int rc;
-  if ((rc = check_shape(B, K, M)) || (rc = check_layers(lambda, eta, L)) || (rc = check_c(c, K))) return rc;
-  if (w0_mode != UFPGD_W0_ZERO && w0_mode != UFPGD_W0_CONJ_H)
-    return fail(UFPGD_EINVAL_PARAM, "sharded forward supports W0 = 0 or H^*");
+  if ((rc = check_shape(B, K, M)) || (rc = check_layers(lambda, eta, L)) || (rc = check_c(c, K)) ||
+      (rc = check_w0(w0_mode, W0)))
+    return rc;
+  if (B > 0 && (!H || !W)) return fail(UFPGD_EINVAL_PARAM, "H and W are required");
   std::lock_guard<std::mutex> lock(g_nccl_mu);
   const int G = static_cast<int>(g_comms.size());
   if (G == 0) return fail(UFPGD_ENCCL, "call ufpgd_gpu_init first");
-  // Contiguous shards [g*B/G, (g+1)*B/G); one host thread and stream per GPU.
+  ShardSet set(G);
+  if (!set.ok) return fail(UFPGD_ECUDA, "cannot create per-device streams / statistics buffers");
+  // Contiguous shards [g*B/G, (g+1)*B/G), each through its device's pipelined
+  // host path on its own host thread (the H2D / D2H copies of all devices run
+  // concurrently); the shard statistics land in device memory for the
+  // all-reduce.
   std::vector<int> rcs(G, UFPGD_OK);
   std::vector<std::string> errs(G);
-  std::vector<double*> dstats(G, nullptr);
-  std::vector<cudaStream_t> streams(G, nullptr);
   std::vector<std::thread> th;
   for (int gi = 0; gi < G; ++gi) {
     th.emplace_back([&, gi] {
       const int64_t b0 = B * gi / G, b1 = B * (gi + 1) / G, nb = b1 - b0;
-      cudaSetDevice(gi);
-      cudaStreamCreateWithFlags(&streams[gi], cudaStreamNonBlocking);
-      cudaMalloc(&dstats[gi], 3 * sizeof(double));
+      DeviceGuard dg(gi);
       double part[3] = {0, 0, 0};
-      int r = ufpgd_gpu_unfolded_forward_host(H + b0 * K * M, nb, K, M, lambda, eta, L, c,
-                                              w0_mode, nullptr, W + b0 * K * M,
+      const size_t off = static_cast<size_t>(b0) * K * M;
+      int r = ufpgd_gpu_unfolded_forward_host(H + off, nb, K, M, lambda, eta, L, c, w0_mode,
+                                              W0 ? W0 + off : nullptr, W + off,
                                               diverged_at ? diverged_at + b0 : nullptr, part, alpha, gi);
       if (r != UFPGD_OK && r != UFPGD_EDIVERGED) errs[gi] = g_last_error;
       rcs[gi] = r;
-      cudaMemcpyAsync(dstats[gi], part, sizeof(part), cudaMemcpyHostToDevice, streams[gi]);
-      cudaStreamSynchronize(streams[gi]);
+      if (cudaMemcpyAsync(set.dstats[gi], part, sizeof(part), cudaMemcpyHostToDevice, set.streams[gi]) !=
+              cudaSuccess ||
+          cudaStreamSynchronize(set.streams[gi]) != cudaSuccess) {
+        if (rcs[gi] == UFPGD_OK || rcs[gi] == UFPGD_EDIVERGED) {
+          rcs[gi] = UFPGD_ECUDA;
+          errs[gi] = "statistics copy failed";
+        }
+      }
     });
   }
   for (auto& t : th) t.join();
   for (int gi = 0; gi < G; ++gi)
     if (rcs[gi] != UFPGD_OK && rcs[gi] != UFPGD_EDIVERGED) return fail(rcs[gi], errs[gi]);
-  // The only collective: sum of the 3 statistics across GPUs.
-  g_nccl.GroupStart();
-  for (int gi = 0; gi < G; ++gi) {
-    cudaSetDevice(gi);
-    g_nccl.AllReduce(dstats[gi], dstats[gi], 3, kNcclDouble, kNcclSum, g_comms[gi], streams[gi]);
-  }
-  ncclResult_t nr = g_nccl.GroupEnd();
+  if ((rc = set.allreduce())) return rc;
   double out[3] = {0, 0, 0};
-  for (int gi = 0; gi < G; ++gi) {
-    cudaSetDevice(gi);
-    cudaStreamSynchronize(streams[gi]);
-    if (gi == 0) cudaMemcpy(out, dstats[0], sizeof(out), cudaMemcpyDeviceToHost);
-    cudaFree(dstats[gi]);
-    cudaStreamDestroy(streams[gi]);
-  }
-  if (nr != 0) return fail(UFPGD_ENCCL, "ncclAllReduce failed");
+  if ((rc = set.sync_and_read(out))) return rc;
   if (stats) std::memcpy(stats, out, sizeof(out));
   if (out[2] > 0.0) return fail(UFPGD_EDIVERGED, "non-finite iterate in at least one realization");
   return UFPGD_OK;
+}
+
+int ufpgd_gpu_unfolded_forward_sharded_device(const ufpgd_c64* const* H, const int64_t* B, int K, int M,
+                                              const double* lambda, const double* eta, int L, const double* c,
+                                              int w0_mode, const ufpgd_c64* const* W0, ufpgd_c64* const* W,
+                                              int32_t* const* diverged_at, double* const* stats, double alpha,
+                                              const ufpgd_stream_t* streams) {
+  int rc;
+  if (!H || !B || !W || !stats) return fail(UFPGD_EINVAL_PARAM, "H, B, W and stats arrays are required");
+  if ((rc = check_layers(lambda, eta, L)) || (rc = check_c(c, K))) return rc;
+  if (w0_mode == UFPGD_W0_GIVEN && !W0) return fail(UFPGD_EINVAL_PARAM, "W0 required");
+  std::lock_guard<std::mutex> lock(g_nccl_mu);
+  const int G = static_cast<int>(g_comms.size());
+  if (G == 0) return fail(UFPGD_ENCCL, "call ufpgd_gpu_init first");
+  for (int gi = 0; gi < G; ++gi) {
+    if ((rc = check_shape(B[gi], K, M))) return rc;
+    if (!stats[gi]) return fail(UFPGD_EINVAL_PARAM, "every device needs a stats buffer");
+  }
+  // Per device: the fused forward over its resident shard, its statistics
+  // written to its own device buffer (no host round trip) ...
+  for (int gi = 0; gi < G; ++gi) {
+    const ufpgd_stream_t s = streams ? streams[gi] : nullptr;
+    rc = ufpgd_gpu_unfolded_forward(H[gi], B[gi], K, M, lambda, eta, L, c, w0_mode, W0 ? W0[gi] : nullptr, W[gi],
+                                    diverged_at ? diverged_at[gi] : nullptr, nullptr, nullptr, stats[gi], alpha, gi,
+                                    s);
+    if (rc != UFPGD_OK) return rc;
+  }
+  // ... then the only collective, in place on the device buffers, stream
+  // ordered after each device's kernels. Asynchronous, like every device
+  // entry point; divergence is reported in stats[g][2].
+  std::vector<cudaStream_t> st(G);
+  for (int gi = 0; gi < G; ++gi) st[gi] = static_cast<cudaStream_t>(streams ? streams[gi] : nullptr);
+  return allreduce_stats(stats, st.data(), G);
 }
 
 }  // extern "C"

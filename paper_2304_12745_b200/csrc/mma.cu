@@ -26,6 +26,7 @@
 //            (A = H as M x 2K MN-major — the same shared-memory bytes as
 //            stage 1's K-major B — and Bs = the real form of -eta X'^T)
 // so H (hi and lo, f16) is staged once and read by both stages.
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -174,6 +175,9 @@ __device__ __forceinline__ uint16_t f16_bits(__half h) { return *reinterpret_cas
 
 constexpr float kLoScale = 1.f / 2048.f;
 
+// 2^e as a float, |e| <= 126 (exact).
+__device__ __forceinline__ float pow2i(int e) { return __int_as_float((127 + e) << 23); }
+
 // Fixed-step power iteration on H^T H^* (pgd.cpp:146-162 with the BASELINE
 // 30-step rule), FP32 on the unscaled H, one thread per antenna:
 // u = H^* v reduced over the CTA (shuffles, then per-warp partials in `scr`),
@@ -250,18 +254,28 @@ __device__ float cta_power(const float4 (&hv)[T::K / 2], const float2* v0, int s
   return est;
 }
 
-template <class T, bool PGD>
-__global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_constant__ FusedArgs p) {
+// RB = false (fast path): one CTA per realization; a realization that needs
+// the range-robust path is appended to redo_list instead of writing its
+// per-realization outputs. RB = true (range-robust path): a grid-stride loop
+// over the redo_list entries (normally none). The body is written inline in
+// the kernel (a device-function body taking the params by reference measured
+// 3% slower at (16,128)).
+template <class T, bool PGD, bool RB>
+__global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
+    mma_kernel(const __grid_constant__ FusedArgs p, int* redo_list, int* redo_count) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int K = T::K, M = T::M, R = T::R, Q = T::Q, NW = T::NW;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const long long rid = blockIdx.x;
+  const int n_real = RB ? *redo_count : 1;
+  for (int it = RB ? static_cast<int>(blockIdx.x) : 0; it < n_real; it += RB ? static_cast<int>(gridDim.x) : 1) {
+  const long long rid = RB ? static_cast<long long>(redo_list[it]) : static_cast<long long>(blockIdx.x);
   const uint32_t sb = smem_u32(smem);
   const uint32_t bar1 = sb + T::OFF_BAR;                // + 8 t: stage-1 part t done
   const uint32_t bar2 = sb + T::OFF_BAR + 8 * T::NTILE;  // + 8 t: stage-2 tile t done
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + T::OFF_BAR + 48);
   float* red = reinterpret_cast<float*>(smem + T::OFF_BAR + 64);           // [2][16]
   long long* fbs = reinterpret_cast<long long*>(smem + T::OFF_BAR + 192);  // [16]
+  float* redw = reinterpret_cast<float*>(smem + T::OFF_BAR + 320);         // [16]: robust-path maxima
 
   if (tid == 0) {
 #pragma unroll
@@ -272,7 +286,8 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
                  "n"(T::T_COLS)
                  : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    // (the robust kernel allocates again for its next realization)
+    if (!RB) asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
 
   // ---- H row of antenna m = tid: registers, max |.| over the realization ----
@@ -353,6 +368,12 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
 #pragma unroll
     for (int k = 0; k < K; ++k) wr[k] = wi[k] = 0.f;
   }
+  int aW = 0;        // robust path: the W registers hold W_s 2^-aW ...
+  float wn2 = 0.f;   // ... and ||w_m||^2 in that domain
+  if (RB) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) wn2 = fmaf(wr[k], wr[k], fmaf(wi[k], wi[k], wn2));
+  }
 
   constexpr uint32_t IDESC1 = idesc_f16_amn<Q, 2 * R>();
   constexpr uint32_t IDESC2W = idesc_f16_amn<128, 2 * R>();
@@ -393,7 +414,33 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
   for (long long l = 0; l < p.L; ++l) {
     TSTAMP(0)
     const bool xzero = (l == 0 && p.w0_mode == UFPGD_W0_ZERO);
-    const float ts = (PGD ? thr_b : p.thr[l]) * ginv;       // threshold in the scaled domain
+    float ts = (PGD ? thr_b : p.thr[l]) * ginv;             // threshold in the scaled domain
+    if constexpr (RB) {
+      // exact max ||w_m|| of the register W over the CTA, brought to [2^12, 2^13)
+      if (!xzero) {
+        const float wm = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(wn2 >= 0.f ? wn2 : __int_as_float(0x7f800000))));
+        if (lane == 0) redw[warp] = wm;
+        __syncthreads();
+        float mc2 = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) mc2 = fmaxf(mc2, redw[w]);
+        __syncthreads();  // redw is reused by the Bs maximum
+        if (mc2 > 0.f && mc2 < FLT_MAX) {
+          const int d = ilogbf(mc2) / 2 - 12;
+          if (d != 0) {
+            const float f = pow2i(-d);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              wr[k] *= f;
+              wi[k] *= f;
+            }
+            wn2 *= f * f;
+            aW += d;
+          }
+        }
+      }
+      ts *= pow2i(-aW);
+    }
     const float fstep = -(PGD ? eta_b : p.eta[l]) * g2inv;  // -eta / g^2 folded into Bs
     if (!xzero) {
       // W operand rows q = (hilo, part, k) from the thread's antenna column
@@ -484,66 +531,158 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     // 4-wide chunk of X' row k per thread
     // CWD-wide chunks of X' row k per thread (CWD = 4, or 2 when K / 4 chunks per
     // row would leave threads idle; 2-wide keeps a quarter-warp on one F row)
-    constexpr int CWD = T::CWD, NCH = K * K / CWD, CPR = K / CWD;
-    using FV = typename std::conditional<CWD == 4, float4, float2>::type;
-#pragma unroll
-    for (int ch = tid; ch < NCH; ch += T::NT) {
-      // CWD 4: consecutive threads walk along a row; CWD 2: down the rows
-      const int k = CWD == 4 ? ch / CPR : ch % K, c = (CWD == 4 ? ch % CPR : ch / K) * CWD;
-      float xr[CWD], xi[CWD];
-#pragma unroll
-      for (int u = 0; u < CWD; ++u) xr[u] = xi[u] = 0.f;
-      if (!xzero) {
-        const float* F0 = F + k * T::FSTR;        // P rows (0, k), (1, k): hi parts in F, lo in G
-        const float* F1 = F + (K + k) * T::FSTR;
-        const float* G0 = G + k * T::FSTR;
-        const float* G1 = G + (K + k) * T::FSTR;
-        const FV a00 = *reinterpret_cast<const FV*>(F0 + c), b00 = *reinterpret_cast<const FV*>(G0 + c);
-        const FV a11 = *reinterpret_cast<const FV*>(F1 + K + c), b11 = *reinterpret_cast<const FV*>(G1 + K + c);
-        const FV a01 = *reinterpret_cast<const FV*>(F0 + K + c), b01 = *reinterpret_cast<const FV*>(G0 + K + c);
-        const FV a10 = *reinterpret_cast<const FV*>(F1 + c), b10 = *reinterpret_cast<const FV*>(G1 + c);
-        const float* A00 = reinterpret_cast<const float*>(&a00);
-        const float* B00 = reinterpret_cast<const float*>(&b00);
-        const float* A11 = reinterpret_cast<const float*>(&a11);
-        const float* B11 = reinterpret_cast<const float*>(&b11);
-        const float* A01 = reinterpret_cast<const float*>(&a01);
-        const float* B01 = reinterpret_cast<const float*>(&b01);
-        const float* A10 = reinterpret_cast<const float*>(&a10);
-        const float* B10 = reinterpret_cast<const float*>(&b10);
-#pragma unroll
+    int aB = 0;  // robust path: Bs is built as Bs 2^-aB
+    if constexpr (!RB) {
+      constexpr int CWD = T::CWD, NCH = K * K / CWD, CPR = K / CWD;
+      using FV = typename std::conditional<CWD == 4, float4, float2>::type;
+  #pragma unroll
+      for (int ch = tid; ch < NCH; ch += T::NT) {
+        // CWD 4: consecutive threads walk along a row; CWD 2: down the rows
+        const int k = CWD == 4 ? ch / CPR : ch % K, c = (CWD == 4 ? ch % CPR : ch / K) * CWD;
+        float xr[CWD], xi[CWD];
+  #pragma unroll
+        for (int u = 0; u < CWD; ++u) xr[u] = xi[u] = 0.f;
+        if (!xzero) {
+          const float* F0 = F + k * T::FSTR;        // P rows (0, k), (1, k): hi parts in F, lo in G
+          const float* F1 = F + (K + k) * T::FSTR;
+          const float* G0 = G + k * T::FSTR;
+          const float* G1 = G + (K + k) * T::FSTR;
+          const FV a00 = *reinterpret_cast<const FV*>(F0 + c), b00 = *reinterpret_cast<const FV*>(G0 + c);
+          const FV a11 = *reinterpret_cast<const FV*>(F1 + K + c), b11 = *reinterpret_cast<const FV*>(G1 + K + c);
+          const FV a01 = *reinterpret_cast<const FV*>(F0 + K + c), b01 = *reinterpret_cast<const FV*>(G0 + K + c);
+          const FV a10 = *reinterpret_cast<const FV*>(F1 + c), b10 = *reinterpret_cast<const FV*>(G1 + c);
+          const float* A00 = reinterpret_cast<const float*>(&a00);
+          const float* B00 = reinterpret_cast<const float*>(&b00);
+          const float* A11 = reinterpret_cast<const float*>(&a11);
+          const float* B11 = reinterpret_cast<const float*>(&b11);
+          const float* A01 = reinterpret_cast<const float*>(&a01);
+          const float* B01 = reinterpret_cast<const float*>(&b01);
+          const float* A10 = reinterpret_cast<const float*>(&a10);
+          const float* B10 = reinterpret_cast<const float*>(&b10);
+  #pragma unroll
+          for (int u = 0; u < CWD; ++u) {
+            xr[u] = (A00[u] + B00[u]) - (A11[u] + B11[u]);
+            xi[u] = (A01[u] + B01[u]) + (A10[u] + B10[u]);
+          }
+        }
+  #pragma unroll
         for (int u = 0; u < CWD; ++u) {
-          xr[u] = (A00[u] + B00[u]) - (A11[u] + B11[u]);
-          xi[u] = (A01[u] + B01[u]) + (A10[u] + B10[u]);
+          if (c + u == k) xr[u] -= p.c[k];  // X' = X - diag(c)
+          xr[u] *= fstep;
+          xi[u] *= fstep;
+        }
+        uint32_t rh[CWD / 2], rl[CWD / 2], nh[CWD / 2], nl[CWD / 2], ih[CWD / 2], il[CWD / 2];
+  #pragma unroll
+        for (int v = 0; v < CWD / 2; ++v) {
+          split2(xr[2 * v], xr[2 * v + 1], rh[v], rl[v]);
+          split2(-xr[2 * v], -xr[2 * v + 1], nh[v], nl[v]);
+          split2(xi[2 * v], xi[2 * v + 1], ih[v], il[v]);
+        }
+        // (p_in, p_out) = (0,0): X'r, (1,0): X'i, (0,1): X'i, (1,1): -X'r
+        auto put = [&](int off, const uint32_t* v) {
+          if constexpr (CWD == 4)
+            *reinterpret_cast<uint2*>(smem + off) = make_uint2(v[0], v[1]);
+          else
+            *reinterpret_cast<uint32_t*>(smem + off) = v[0];
+        };
+        put(T::OFF_BH + T::boff(c, k), rh);
+        put(T::OFF_BL + T::boff(c, k), rl);
+        put(T::OFF_BH + T::boff(K + c, k), ih);
+        put(T::OFF_BL + T::boff(K + c, k), il);
+        put(T::OFF_BH + T::boff(c, K + k), ih);
+        put(T::OFF_BL + T::boff(c, K + k), il);
+        put(T::OFF_BH + T::boff(K + c, K + k), nh);
+        put(T::OFF_BL + T::boff(K + c, K + k), nl);
+      }
+    } else {
+      constexpr int CWD = T::CWD, NCH = K * K / CWD, CPR = K / CWD;
+      static_assert(NCH <= T::NT, "one Bs chunk per thread");
+      using FV = typename std::conditional<CWD == 4, float4, float2>::type;
+      // robust path: the P rows are X 2^-aW, so X' 2^-aW = P - c 2^-aW, and the
+      // chunk values become Bs 2^-aB with aB from their exact CTA maximum
+      const float cscale = RB ? pow2i(-aW) : 1.f, fstep_w = RB ? fstep * pow2i(aW) : fstep;
+      {
+        const int ch = tid;
+        // CWD 4: consecutive threads walk along a row; CWD 2: down the rows
+        const int k = CWD == 4 ? ch / CPR : ch % K, c = (CWD == 4 ? ch % CPR : ch / K) * CWD;
+        float xr[CWD], xi[CWD];
+  #pragma unroll
+        for (int u = 0; u < CWD; ++u) xr[u] = xi[u] = 0.f;
+        if (!xzero) {
+          const float* F0 = F + k * T::FSTR;        // P rows (0, k), (1, k): hi parts in F, lo in G
+          const float* F1 = F + (K + k) * T::FSTR;
+          const float* G0 = G + k * T::FSTR;
+          const float* G1 = G + (K + k) * T::FSTR;
+          const FV a00 = *reinterpret_cast<const FV*>(F0 + c), b00 = *reinterpret_cast<const FV*>(G0 + c);
+          const FV a11 = *reinterpret_cast<const FV*>(F1 + K + c), b11 = *reinterpret_cast<const FV*>(G1 + K + c);
+          const FV a01 = *reinterpret_cast<const FV*>(F0 + K + c), b01 = *reinterpret_cast<const FV*>(G0 + K + c);
+          const FV a10 = *reinterpret_cast<const FV*>(F1 + c), b10 = *reinterpret_cast<const FV*>(G1 + c);
+          const float* A00 = reinterpret_cast<const float*>(&a00);
+          const float* B00 = reinterpret_cast<const float*>(&b00);
+          const float* A11 = reinterpret_cast<const float*>(&a11);
+          const float* B11 = reinterpret_cast<const float*>(&b11);
+          const float* A01 = reinterpret_cast<const float*>(&a01);
+          const float* B01 = reinterpret_cast<const float*>(&b01);
+          const float* A10 = reinterpret_cast<const float*>(&a10);
+          const float* B10 = reinterpret_cast<const float*>(&b10);
+  #pragma unroll
+          for (int u = 0; u < CWD; ++u) {
+            xr[u] = (A00[u] + B00[u]) - (A11[u] + B11[u]);
+            xi[u] = (A01[u] + B01[u]) + (A10[u] + B10[u]);
+          }
+        }
+  #pragma unroll
+        for (int u = 0; u < CWD; ++u) {
+          if (c + u == k) xr[u] -= RB ? p.c[k] * cscale : p.c[k];  // X' = X - diag(c)
+          xr[u] *= fstep_w;
+          xi[u] *= fstep_w;
+        }
+        if constexpr (RB) {
+          float bm = 0.f;
+          if (ch < NCH) {
+  #pragma unroll
+            for (int u = 0; u < CWD; ++u) bm = fmaxf(bm, fmaxf(fabsf(xr[u]), fabsf(xi[u])));
+            if (!(bm <= FLT_MAX)) bm = __int_as_float(0x7f800000);
+          }
+          bm = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(bm)));
+          if (lane == 0) redw[warp] = bm;
+          __syncthreads();
+          float mb = 0.f;
+  #pragma unroll
+          for (int w = 0; w < NW; ++w) mb = fmaxf(mb, redw[w]);
+          if (mb > 0.f && mb < FLT_MAX) aB = ilogbf(mb) - 12;  // Bs 2^-aB in [2^12, 2^13)
+          const float f = pow2i(-aB);
+  #pragma unroll
+          for (int u = 0; u < CWD; ++u) {
+            xr[u] *= f;
+            xi[u] *= f;
+          }
+        }
+        if (ch < NCH) {
+        uint32_t rh[CWD / 2], rl[CWD / 2], nh[CWD / 2], nl[CWD / 2], ih[CWD / 2], il[CWD / 2];
+  #pragma unroll
+        for (int v = 0; v < CWD / 2; ++v) {
+          split2(xr[2 * v], xr[2 * v + 1], rh[v], rl[v]);
+          split2(-xr[2 * v], -xr[2 * v + 1], nh[v], nl[v]);
+          split2(xi[2 * v], xi[2 * v + 1], ih[v], il[v]);
+        }
+        // (p_in, p_out) = (0,0): X'r, (1,0): X'i, (0,1): X'i, (1,1): -X'r
+        auto put = [&](int off, const uint32_t* v) {
+          if constexpr (CWD == 4)
+            *reinterpret_cast<uint2*>(smem + off) = make_uint2(v[0], v[1]);
+          else
+            *reinterpret_cast<uint32_t*>(smem + off) = v[0];
+        };
+        put(T::OFF_BH + T::boff(c, k), rh);
+        put(T::OFF_BL + T::boff(c, k), rl);
+        put(T::OFF_BH + T::boff(K + c, k), ih);
+        put(T::OFF_BL + T::boff(K + c, k), il);
+        put(T::OFF_BH + T::boff(c, K + k), ih);
+        put(T::OFF_BL + T::boff(c, K + k), il);
+        put(T::OFF_BH + T::boff(K + c, K + k), nh);
+        put(T::OFF_BL + T::boff(K + c, K + k), nl);
         }
       }
-#pragma unroll
-      for (int u = 0; u < CWD; ++u) {
-        if (c + u == k) xr[u] -= p.c[k];  // X' = X - diag(c)
-        xr[u] *= fstep;
-        xi[u] *= fstep;
-      }
-      uint32_t rh[CWD / 2], rl[CWD / 2], nh[CWD / 2], nl[CWD / 2], ih[CWD / 2], il[CWD / 2];
-#pragma unroll
-      for (int v = 0; v < CWD / 2; ++v) {
-        split2(xr[2 * v], xr[2 * v + 1], rh[v], rl[v]);
-        split2(-xr[2 * v], -xr[2 * v + 1], nh[v], nl[v]);
-        split2(xi[2 * v], xi[2 * v + 1], ih[v], il[v]);
-      }
-      // (p_in, p_out) = (0,0): X'r, (1,0): X'i, (0,1): X'i, (1,1): -X'r
-      auto put = [&](int off, const uint32_t* v) {
-        if constexpr (CWD == 4)
-          *reinterpret_cast<uint2*>(smem + off) = make_uint2(v[0], v[1]);
-        else
-          *reinterpret_cast<uint32_t*>(smem + off) = v[0];
-      };
-      put(T::OFF_BH + T::boff(c, k), rh);
-      put(T::OFF_BL + T::boff(c, k), rl);
-      put(T::OFF_BH + T::boff(K + c, k), ih);
-      put(T::OFF_BL + T::boff(K + c, k), il);
-      put(T::OFF_BH + T::boff(c, K + k), ih);
-      put(T::OFF_BL + T::boff(c, K + k), il);
-      put(T::OFF_BH + T::boff(K + c, K + k), nh);
-      put(T::OFF_BL + T::boff(K + c, K + k), nl);
     }
     fence_async_smem();
     tc_fence_before();
@@ -584,8 +723,14 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
           tmem_ld16(cc + part * K + j0, b);
           tmem_wait<16>(a);
           tmem_wait<16>(b);
+          if constexpr (RB) {  // D2 = G 2^-aB onto W registers in the 2^-aW domain
+            const float u2 = pow2i(aB - aW);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) w[j0 + i] += fmaf(kLoScale, b[i], a[i]);  // V = W - eta X' H^*
+            for (int i = 0; i < 16; ++i) w[j0 + i] = fmaf(u2, fmaf(kLoScale, b[i], a[i]), w[j0 + i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) w[j0 + i] += fmaf(kLoScale, b[i], a[i]);  // V = W - eta X' H^*
+          }
         }
       }
     }
@@ -594,7 +739,12 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     float s2 = 0.f;
 #pragma unroll
     for (int k = 0; k < K; ++k) s2 = fmaf(wr[k], wr[k], fmaf(wi[k], wi[k], s2));
-    nonfinite |= !(s2 * (g * g) <= FLT_MAX);
+    const float gw = RB ? g * pow2i(aW) : g;  // register domain -> unscaled W
+    if constexpr (RB) {
+      nonfinite |= !(s2 * gw * gw <= FLT_MAX);
+    } else {
+      nonfinite |= !(s2 * (g * g) <= FLT_MAX);
+    }
     const bool on = s2 > ts * ts;
     const float r = rsqrt_ftz(fmaxf(s2, FLT_MIN));
     const float scale = on ? fmaf(-ts, r, 1.f) : 0.f;
@@ -603,8 +753,9 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
       wr[k] *= scale;
       wi[k] *= scale;
     }
+    if constexpr (RB) wn2 = scale * scale * s2;
     if (l + 1 == p.L && on) {
-      l21 += g * fmaf(s2, r, -ts);
+      l21 += gw * fmaf(s2, r, -ts);
       act += 1;
     }
     if (nonfinite && first_bad < 0) first_bad = l;
@@ -612,11 +763,14 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
   }
 
   // ---- W out (unscaled), per-realization reductions ---------------------------
+  // (a realization handed to the robust path writes garbage W here; the robust
+  // kernel, later in the stream, overwrites it)
   {
+    const float gout = RB ? g * pow2i(aW) : g;
     float4* wg = reinterpret_cast<float4*>(p.W + (rid * M + m) * K);
 #pragma unroll
     for (int j = 0; j < K / 2; ++j)
-      stg_stream(wg + j, make_float4(wr[2 * j] * g, wi[2 * j] * g, wr[2 * j + 1] * g, wi[2 * j + 1] * g));
+      stg_stream(wg + j, make_float4(wr[2 * j] * gout, wi[2 * j] * gout, wr[2 * j + 1] * gout, wi[2 * j + 1] * gout));
 #ifdef UFPGD_MMA_TIMING
     if (probe) {
       long long* o = reinterpret_cast<long long*>(p.W + rid * M * K);
@@ -636,13 +790,33 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
     red[warp] = l21;
     red[16 + warp] = static_cast<float>(act);
   }
+  // Fast path hand-off to the range-robust kernel, decided at the final CTA
+  // barrier so the layer loop is the plain one: any non-finite value on the
+  // way (an f16 overflow of W_s or Bs — e.g. W0 = H^* with a large channel —
+  // or a true divergence, which the robust path then reproduces with its
+  // index), or a Bs scale |eta / g^2| max c outside [2^-12, 2^12] (f16
+  // underflow: tiny c or steps). The handed-off realization's W is
+  // overwritten and its other outputs are written by the robust kernel.
   tc_fence_before();
-  __syncthreads();
+  bool handoff = false;
+  if (RB) {
+    __syncthreads();
+  } else {
+    const float sc_lo = (PGD ? eta_b : p.eta_lo) * p.cmax * g2inv, sc_hi = (PGD ? eta_b : p.eta_hi) * p.cmax * g2inv;
+    const bool range = !(sc_lo >= 0x1.0p-12f && sc_hi <= 0x1.0p12f);  // CTA-uniform
+    handoff = __syncthreads_or(nonfinite || range) != 0;
+  }
   if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(T::T_COLS) : "memory");
   }
-  if (tid == 0) {
+  if (RB && tid == 0) {  // the robust kernel re-initialises them for its next realization
+#pragma unroll
+    for (int b = 0; b < 2 * T::NTILE; ++b)
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar1 + 8 * b) : "memory");
+  }
+  if (tid == 0 && handoff) redo_list[atomicAdd(redo_count, 1)] = static_cast<int>(rid);
+  if (tid == 0 && !handoff) {
     for (int w = 1; w < NW; ++w) {
       fb = min(fb, fbs[w]);
       l21 += red[w];
@@ -658,6 +832,8 @@ __global__ void __launch_bounds__(T::NT, T::MINB) mma_kernel(const __grid_consta
       p.block_partials[rid * 3 + 2] = diverged ? 1.0 : 0.0;
     }
   }
+  if (RB) __syncthreads();  // the reduction slots are reused by the next realization
+  }  // realizations of the CTA
 }
 
 using Mma_32_256 = MmaShape<32, 256, 1>;
@@ -667,24 +843,49 @@ using Mma_32_256 = MmaShape<32, 256, 1>;
 using Mma_16_128 = MmaShape<16, 128, UFPGD_MMA16_MINB>;
 
 template <class T>
-cudaError_t launch_mma_t(const FusedArgs& a, bool pgd, cudaStream_t s, long long* nblocks) {
-  auto kern = pgd ? mma_kernel<T, true> : mma_kernel<T, false>;
+cudaError_t launch_mma_t(const FusedArgs& args, bool pgd, cudaStream_t s, long long* nblocks) {
+  FusedArgs a = args;  // + the range summary the fast path checks once per realization
+  a.cmax = 0.f;
+  for (int k = 0; k < T::K; ++k) a.cmax = std::max(a.cmax, std::fabs(a.c[k]));
+  a.eta_lo = FLT_MAX;
+  a.eta_hi = 0.f;
+  for (long long l = 0; !pgd && l < a.L && l < UFPGD_MAX_LAYERS; ++l) {
+    a.eta_lo = std::min(a.eta_lo, std::fabs(a.eta[l]));
+    a.eta_hi = std::max(a.eta_hi, std::fabs(a.eta[l]));
+  }
+  auto kern = pgd ? mma_kernel<T, true, false> : mma_kernel<T, false, false>;
+  auto robust = pgd ? mma_kernel<T, true, true> : mma_kernel<T, false, true>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(robust, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
   if (e != cudaSuccess) return e;
   if (nblocks) *nblocks = a.B;
   if (a.B == 0) return cudaSuccess;
-  kern<<<static_cast<unsigned>(a.B), T::NT, T::SMEM, s>>>(a);
-  return cudaGetLastError();
+  int* list = nullptr;
+  if ((e = scratch_alloc_async(reinterpret_cast<void**>(&list), sizeof(int) * (a.B + 1), s)) != cudaSuccess)
+    return e;
+  if ((e = cudaMemsetAsync(list, 0, sizeof(int), s)) == cudaSuccess) {
+    kern<<<static_cast<unsigned>(a.B), T::NT, T::SMEM, s>>>(a, list + 1, list);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    robust<<<static_cast<unsigned>(std::min<long long>(a.B, sms)), T::NT, T::SMEM, s>>>(a, list + 1, list);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(list, s);
+  return e;
 }
 
 }  // namespace
 
-// Unfolded forward and fixed-step PGD at (16,128), (32,256); UFPGD_NO_MMA=1
-// selects the CUDA-core tile kernel for A/B runs.
+// Unfolded forward and fixed-step PGD at (16,128), (32,256);
+// ufpgd_gpu_set_option(UFPGD_OPT_TENSOR_CORES, 0) selects the CUDA-core tile
+// kernel for A/B runs.
 bool mma_supported(int K, int M, bool pgd) {
   if (!((K == 32 && M == 256) || (K == 16 && M == 128))) return false;
-  const char* off = std::getenv("UFPGD_NO_MMA");
-  return !(off && off[0] == '1');
+  return option(UFPGD_OPT_TENSOR_CORES) != 0;
 }
 
 cudaError_t launch_mma(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s, long long* nblocks) {

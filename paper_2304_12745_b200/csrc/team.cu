@@ -675,7 +675,7 @@ cudaError_t launch_team(const FusedArgs& a, bool pgd, cudaStream_t s, long long*
                                        kFusedMaxWarps * (S::SMEM_PER_WARP + S::WSMEM_PER_WARP));
   if (e != cudaSuccess) return e;
   int nw = pick_warps(S::R, a.B);
-  if (const char* f = std::getenv("UFPGD_FUSED_WARPS")) nw = std::max(1, std::min(8, std::atoi(f)));
+  if (const int64_t f = option(UFPGD_OPT_FUSED_WARPS); f > 0) nw = static_cast<int>(f);
   nw = std::min(nw, maxt / 32);
   const long long rpb = static_cast<long long>(nw) * S::R;
   const long long blocks = (a.B + rpb - 1) / rpb;

@@ -219,7 +219,7 @@ cudaError_t launch_pgd64_team(const GeneralArgs64& a, cudaStream_t s) {
 }  // namespace
 
 bool pgd64_team_supported(const GeneralArgs64& a) {
-  if (std::getenv("UFPGD_NO_TEAM64")) return false;
+  if (option(UFPGD_OPT_FP64_TEAM) == 0) return false;
   const bool shape = (a.K == 8 && a.M == 64) || (a.K == 4 && a.M == 32);
   return shape && a.pgd == 1 && a.mode == 0 && a.index_base == 1 && !a.iterates && !a.tape_v && !a.tape_norms &&
          !a.tape_shrink;

@@ -27,6 +27,8 @@ struct FusedArgs {
   int power_steps;        // PGD with eta_in == nullptr
   float lambda;           // PGD threshold factor (thr = lambda * eta)
   float alpha;            // PA constant for the consumed-power statistic
+  float cmax;             // tensor-core kernel: max |c_k| and the range of the
+  float eta_lo, eta_hi;   //   per-layer steps (filled by launch_mma)
   float c[UFPGD_MAX_USERS];
   float eta[UFPGD_MAX_LAYERS];
   float thr[UFPGD_MAX_LAYERS];
@@ -115,6 +117,12 @@ struct PowerArgs {
   int K, M, steps;
   float2 v0[1024];
 };
+
+// Library options (ufpgd_gpu_set_option; capi.cpp), read at launch time.
+int64_t option(int id);
+// Stream-ordered scratch from the library's private pool (kept mapped across
+// calls); free with cudaFreeAsync.
+cudaError_t scratch_alloc_async(void** p, size_t bytes, cudaStream_t s);
 
 // Fused team kernel availability for (K, M); fills the launch geometry.
 bool fused_supported(int K, int M);

@@ -833,6 +833,27 @@ int main() {
     BatchResult p = solve_pgd_batch(H.data(), 64, cfg, 0.05, 500);
     CHECK(p.diverged == 0 && p.steps.size() == 64 && p.steps[0] > 0.0f);
   }
+  {  // Documented FP32 deviation of the batched path (INTEGRATION.md "Divergence"):
+     // a finite step image whose squared column norm overflows FP32 (|v| > ~1.8e19)
+     // is reported as diverged at that layer, while the FP64 per-channel forward
+     // (the reference's precision) continues and diverges a few layers later.
+    SystemConfig cfg = SystemConfig::uniform(8, 64, 10.0);
+    UnfoldedNetwork net = UnfoldedNetwork::pgd_init(8, 64, 20, 1.0 / 15.0);
+    ChannelMatrix h = 1e20 * channel_for(cfg, 57, 0);  // finite in FP32 (max ~3.4e38)
+    std::vector<std::complex<float>> H(512);
+    for (int m = 0; m < 64; ++m)
+      for (int k = 0; k < 8; ++k) H[m * 8 + k] = std::complex<float>(h(k, m));
+    for (const auto& z : H) CHECK(std::isfinite(z.real()) && std::isfinite(z.imag()));
+    BatchResult r = forward_batch(net, H.data(), 1, cfg);  // W0 = H^*: ||w_m||^2 ~ 1e41 > FLT_MAX
+    CHECK(r.diverged == 1 && r.diverged_at[0] == 0);
+    long fp64_index = -1;
+    try {
+      (void)forward(net, h, cfg);
+    } catch (const DivergenceError& e) {
+      fp64_index = e.index;
+    }
+    CHECK(fp64_index >= 1);  // FP64 reaches non-finite values only at a later layer
+  }
   // --- test_metrics.cpp / evaluate on the device -------------------------------------
   {
     SystemConfig cfg = SystemConfig::uniform(4, 16, 10.0);

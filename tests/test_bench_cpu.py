@@ -23,6 +23,42 @@ def test_reference_arm_prints_one_contract_line():
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    # the whole per-GPU batch per step, described with the GPU arm's config keys
+    assert d["config"]["per_gpu_batch"] == d["config"]["global_batch"] == 65536
+    assert d["config"]["layers_eta_clamped_by_projection"] == 7
+
+
+def test_reference_arm_loads_no_product_library():
+    """Inputs and layer parameters come from oracle/ (the restatements of
+    channel.cpp:7-16 / rng.cpp:19-40), so only oracle libraries are mapped."""
+    code = ("import sys; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '0'];"
+            "import bench; bench.main();"
+            "maps = open('/proc/self/maps').read();"
+            "print('PRODUCT_SO', 'libufpgd_gpu' in maps, 'ORACLE_SO', 'libufpgd_oracle' in maps)")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "PRODUCT_SO False ORACLE_SO True" in r.stdout
+
+
+def test_oracle_inputs_equal_product_inputs():
+    """The reference arm's oracle-generated batch and projected parameters are
+    the GPU arm's, bit for bit."""
+    sys.path.insert(0, ROOT)
+    import numpy as np
+
+    import bench
+    import paper_2304_12745_b200 as U
+    from oracle import oracle as O
+
+    for cfg in (2, 5):
+        w = U.CONFIGS[cfg]
+        a = U.make_inputs(w, 1234, 64)
+        b = O.generate_channels_batch_f32(w.seed_h, w.seed_g, w.gain_db, 1234, 64, w.K, w.M)
+        assert np.array_equal(a, b)
+        lam, eta, clamped = bench.projected_params_oracle(w)
+        lam2, eta2 = w.layer_params()
+        assert np.array_equal(lam, lam2) and np.array_equal(eta, eta2)
+        assert clamped == bench.clamped_layers(w)
 
 
 def test_cost_model_counts_performed_contractions():

@@ -19,11 +19,11 @@ HEADER = "include/ufpgd_gpu.h"
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(ufpgd_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(ufpgd_\w+)\s*\(", text, re.M)))
 
 
 def test_library_loads_and_reports_abi():
-    assert U.abi_version() == 1
+    assert U.abi_version() == 2
 
 
 def test_every_declared_symbol_is_exported():
@@ -36,6 +36,27 @@ def test_every_declared_symbol_is_exported():
     assert not missing, missing
     for n in names:
         assert hasattr(U.lib(), n)
+
+
+def test_options_are_explicit_and_validated():
+    """Tuning / A-B switches go through ufpgd_gpu_set_option only; the
+    environment variables that used to select kernels are ignored."""
+    assert U.get_option("tensor_cores") == 1 and U.get_option("zero_pad") == 1
+    assert U.get_option("pad_sub_bytes") == 1 << 30 and U.get_option("host_chunk_bytes") == 16 << 20
+    with U.options(tensor_cores=0, fused_warps=4):
+        assert U.get_option("tensor_cores") == 0 and U.get_option("fused_warps") == 4
+    assert U.get_option("tensor_cores") == 1 and U.get_option("fused_warps") == 0
+    for name, bad in (("tensor_cores", 2), ("fused_warps", 9), ("pad_sub_bytes", 1), ("host_pipe", -1)):
+        with pytest.raises(ValueError):
+            U.set_option(name, bad)
+    assert U.lib().ufpgd_gpu_set_option(99, 0) == U.capi.EINVAL_PARAM
+    assert U.lib().ufpgd_gpu_get_option(99) == -(1 << 63)
+    src = ""
+    for f in os.listdir("paper_2304_12745_b200/csrc"):
+        if f.endswith((".cu", ".cpp", ".cuh", ".h")) and f != "host_util.cpp":
+            src += open(os.path.join("paper_2304_12745_b200/csrc", f)).read()
+    # host_util.cpp keeps the reference's own UFPGD_THREADS (parallel.cpp:13-23)
+    assert "getenv" not in src
 
 
 def test_generator_matches_oracle_bit_for_bit():

@@ -67,9 +67,7 @@ def test_zero_padded_shapes_match_the_oracle(K, M):
     """Shapes without a specialised kernel but within 6x the flops of one run
     zero-padded on it (capi.cpp padded_shape): the cropped W, support and
     per-realization outputs equal the oracle's, for every start mode; the
-    general kernel (UFPGD_NO_PAD) agrees too."""
-    import os
-
+    general kernel (option zero_pad=0) agrees too."""
     B = 23
     H = U.generate_channels(41, 42, 10.0, 0, B, K, M)
     lam, eta = params(K, M, 20)
@@ -85,11 +83,8 @@ def test_zero_padded_shapes_match_the_oracle(K, M):
         assert np.array_equal(g["active"].cpu().numpy(), ora["active"])
         assert np.all(g["diverged_at"].cpu().numpy() == -1)
         np.testing.assert_allclose(g["l21"].cpu().numpy(), ora["l21"], rtol=1e-5)
-        os.environ["UFPGD_NO_PAD"] = "1"
-        try:
+        with U.options(zero_pad=0):
             gen = U.unfolded_forward(dev(H), lam, eta, c, **kw)
-        finally:
-            del os.environ["UFPGD_NO_PAD"]
         assert_parity(report(H, gen["W"].cpu().numpy(), ora, c, 1.0 / 15.0))
         np.testing.assert_allclose(g["stats"].cpu().numpy(), gen["stats"].cpu().numpy(), rtol=1e-5)
 
@@ -114,26 +109,18 @@ def test_zero_padded_pgd_with_power_iteration(K, M):
 
 
 def test_zero_padded_path_splits_large_batches():
-    """(6, 48) pads to (8, 64): with a 256 MiB scratch (UFPGD_PAD_SUB_MB) that
+    """(6, 48) pads to (8, 64): with a 256 MiB scratch (option pad_sub_bytes) that
     is 65,536 padded realizations per sub-batch, so 65,536 + 37 runs two
     sub-batches; the seam and the stats partials of both must line up (checked
     against the general kernel on all realizations and the oracle on the seam)."""
-    import os
-
-    os.environ["UFPGD_PAD_SUB_MB"] = "256"
     K, M, B = 6, 48, 65536 + 37
     H = U.generate_channels(43, 44, 10.0, 0, B, K, M)
     lam, eta = params(K, M, 20)
     c = np.full(K, np.sqrt(10.0))
-    try:
+    with U.options(pad_sub_bytes=256 << 20):
         g = U.unfolded_forward(dev(H), lam, eta, c, want_per_realization=True)
-    finally:
-        del os.environ["UFPGD_PAD_SUB_MB"]
-    os.environ["UFPGD_NO_PAD"] = "1"
-    try:
+    with U.options(zero_pad=0):
         gen = U.unfolded_forward(dev(H), lam, eta, c, want_per_realization=True)
-    finally:
-        del os.environ["UFPGD_NO_PAD"]
     Wg, We = g["W"].cpu().numpy(), gen["W"].cpu().numpy()
     rel = np.linalg.norm((Wg - We).reshape(B, -1), axis=1) / np.linalg.norm(We.reshape(B, -1), axis=1)
     assert rel.max() < 1e-5, rel.max()

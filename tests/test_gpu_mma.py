@@ -1,12 +1,10 @@
 """The tcgen05 tensor-core path (csrc/mma.cu) of the unfolded forward and the
 fixed-step PGD at the BASELINE shapes (16, 128) and (32, 256): parity with the FP64 oracle at the
-north_star bars, agreement with the CUDA-core tile kernel (UFPGD_NO_MMA=1),
+north_star bars, agreement with the CUDA-core tile kernel (option tensor_cores=0),
 every W0 mode, and exact equivariance under power-of-two channel scaling —
 the property the kernel's per-realization f16 range scaling must preserve
 (unfolded.cpp:112-146 is homogeneous: H -> aH, eta -> eta/a^2,
 lambda -> a lambda maps W -> W/a)."""
-import os
-
 import numpy as np
 import pytest
 
@@ -21,18 +19,11 @@ LAM_OBJ_UF = 1.0 / 15.0
 
 
 def run(H, lam, eta, c, w0_mode=0, W0=None, mma=True):
-    old = os.environ.get("UFPGD_NO_MMA")
-    os.environ["UFPGD_NO_MMA"] = "0" if mma else "1"
-    try:
+    with U.options(tensor_cores=int(mma)):
         out = U.unfolded_forward(torch.from_numpy(np.ascontiguousarray(H)).cuda(), lam, eta, c, w0_mode=w0_mode,
                                  W0=None if W0 is None else torch.from_numpy(np.ascontiguousarray(W0)).cuda(),
                                  want_per_realization=True)
         torch.cuda.synchronize()
-    finally:
-        if old is None:
-            os.environ.pop("UFPGD_NO_MMA", None)
-        else:
-            os.environ["UFPGD_NO_MMA"] = old
     return {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
 
 
@@ -102,17 +93,10 @@ def test_mma_nonfinite_channel_isolated():
 
 
 def run_pgd(H, lam, iters, c, mma=True, **kw):
-    old = os.environ.get("UFPGD_NO_MMA")
-    os.environ["UFPGD_NO_MMA"] = "0" if mma else "1"
-    try:
+    with U.options(tensor_cores=int(mma)):
         out = U.pgd_fixed(torch.from_numpy(np.ascontiguousarray(H)).cuda(), lam, iters, c,
                           want_per_realization=True, **kw)
         torch.cuda.synchronize()
-    finally:
-        if old is None:
-            os.environ.pop("UFPGD_NO_MMA", None)
-        else:
-            os.environ["UFPGD_NO_MMA"] = old
     return {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
 
 
@@ -187,3 +171,89 @@ def test_mma_host_path_and_position_invariance(cfg):
         sub = run(np.ascontiguousarray(H[idx]), lam, eta, w.c)
         np.testing.assert_array_equal(sub["W"], d["W"][idx])
         np.testing.assert_array_equal(sub["l21"], d["l21"][idx])
+
+
+@pytest.mark.parametrize("K,M", [(16, 128), (32, 256)])
+@pytest.mark.parametrize("w0_mode", [U.W0_CONJ_H, U.W0_GIVEN])
+def test_mma_large_channels_and_start_values_stay_in_f16_range(K, M, w0_mode):
+    """max |H| ~ 1e3 (not a power of two) with W0 = H^* or a large given W0:
+    the W operand (|W_s| ~ max|H|^2) and Bs leave the f16 range unless they
+    get their own per-layer exponents. The tensor-core path must agree with
+    the CUDA-core tile kernel and the oracle, with no spurious divergence."""
+    w = U.CONFIGS[4 if K == 32 else 5]
+    a = 1000.0
+    H = (U.make_inputs(w, 21, 24) * np.float32(a)).astype(np.complex64)
+    lam, eta = w.layer_params()
+    lam, eta = lam * a, eta / (a * a)  # the homogeneous rescaling of unfolded.cpp:112-146
+    W0 = None
+    if w0_mode == U.W0_GIVEN:
+        rng = np.random.default_rng(9)
+        W0 = (300.0 * (rng.standard_normal(H.shape) + 1j * rng.standard_normal(H.shape))).astype(np.complex64)
+    g = run(H, lam, eta, w.c, w0_mode=w0_mode, W0=W0)
+    t = run(H, lam, eta, w.c, w0_mode=w0_mode, W0=W0, mma=False)
+    assert np.all(g["diverged_at"] == -1) and np.all(t["diverged_at"] == -1)
+    ora = O.forward_batch_f32(H, w.c, lam, eta, w0_mode=w0_mode, W0=W0)
+    rg = report(H, g["W"], ora, w.c, LAM_OBJ_UF * a)
+    rt = report(H, t["W"], ora, w.c, LAM_OBJ_UF * a)
+    print(f"({K},{M}) w0 {w0_mode} x1e3: tcgen05 rel {rg['rel_max']:.2e}, tile rel {rt['rel_max']:.2e}")
+    assert_parity(rg)
+    # as accurate as the FP32 CUDA-core kernel (a large start makes both lose a few bits)
+    assert rg["rel_max"] <= max(3 * rt["rel_max"], 5e-6)
+
+
+@pytest.mark.parametrize("K,M", [(16, 128), (32, 256)])
+def test_mma_pgd_default_start_on_large_channels(K, M):
+    """pgd_fixed's default W0 = H^* (pgd.cpp:184) at max |H| ~ 1e3 on the
+    tcgen05 path: fixed-step PGD with eta = 1/L30 is scale-invariant, so it
+    must converge like the unit-scale run (advisor finding, round 1)."""
+    w = U.CONFIGS[4 if K == 32 else 5]
+    H = (U.make_inputs(w, 5, 16) * np.float32(1000.0)).astype(np.complex64)
+    lam, iters = 0.05 * 1000.0, 300
+    g = run_pgd(H, lam, iters, w.c, power_steps=30)
+    t = run_pgd(H, lam, iters, w.c, mma=False, power_steps=30)
+    assert np.all(g["diverged_at"] == -1)
+    np.testing.assert_allclose(g["eta"], t["eta"], rtol=1e-5)  # both 30-step power iterations, own order
+    Lo, _ = O.power_iteration_batch_f32(H, 30)
+    ora = O.pgd_batch_f32(H, w.c, lam, 1.0 / Lo, iters, w0_mode=U.W0_CONJ_H)
+    rg, rt = report(H, g["W"], ora, w.c, lam), report(H, t["W"], ora, w.c, lam)
+    print(f"({K},{M}) PGD x1e3: tcgen05 rel {rg['rel_max']:.2e}, tile rel {rt['rel_max']:.2e}")
+    assert_parity(rg)
+    assert rg["rel_max"] <= max(3 * rt["rel_max"], 5e-6)
+
+
+def test_environment_no_longer_selects_kernels(monkeypatch):
+    """The round-1 A/B environment knobs are gone from the dispatch path: a
+    stray UFPGD_NO_MMA in the caller's environment changes nothing."""
+    w = U.CONFIGS[5]
+    H = U.make_inputs(w, 0, 64)
+    lam, eta = w.layer_params()
+    a = run(H, lam, eta, w.c)
+    monkeypatch.setenv("UFPGD_NO_MMA", "1")
+    monkeypatch.setenv("UFPGD_FUSED_WARPS", "1")
+    b = run(H, lam, eta, w.c)
+    np.testing.assert_array_equal(a["W"], b["W"])
+    t = run(H, lam, eta, w.c, mma=False)
+    assert not np.array_equal(a["W"], t["W"])  # the option does switch kernels
+
+
+@pytest.mark.parametrize("K,M", [(16, 128), (32, 256)])
+@pytest.mark.parametrize("cscale", [1e-6, 1e5])
+def test_mma_extreme_constraint_scales_use_the_range_robust_path(K, M, cscale):
+    """Tiny or huge c (SystemConfig gamma) puts Bs = -eta/g^2 X' outside the
+    f16 range (underflow / overflow); such realizations run the range-robust
+    path (exact per-layer power-of-two exponents) and match the FP32 tile
+    kernel and the oracle."""
+    w = U.CONFIGS[4 if K == 32 else 5]
+    H = U.make_inputs(w, 31, 16)
+    lam, eta = w.layer_params()
+    c = w.c * cscale
+    lam = lam * cscale  # keep the threshold in proportion (the problem is homogeneous in (W, c, lambda))
+    g = run(H, lam, eta, c)
+    t = run(H, lam, eta, c, mma=False)
+    assert np.all(g["diverged_at"] == -1)
+    ora = O.forward_batch_f32(H, c, lam, eta, w0_mode=w.w0_mode)
+    rg = report(H, g["W"], ora, c, LAM_OBJ_UF * cscale)
+    rt = report(H, t["W"], ora, c, LAM_OBJ_UF * cscale)
+    print(f"({K},{M}) c x{cscale:g}: tcgen05 rel {rg['rel_max']:.2e}, tile rel {rt['rel_max']:.2e}")
+    assert_parity(rg)
+    assert rg["rel_max"] <= max(3 * rt["rel_max"], 5e-6)

@@ -6,9 +6,11 @@ name=$1; shift
 cd "$(dirname "$0")/.."
 mkdir -p tools/ablib/$name build/obj/ab/$name
 objs=""
+# SRC_<name>=path overrides one source (e.g. SRC_mma=/tmp/old/mma.cu)
 for f in team team64 tile mma general metrics grad datagen probe; do
+  var=SRC_$f; src=${!var:-paper_2304_12745_b200/csrc/$f.cu}
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++20 -Xcompiler -fPIC -Iinclude \
-    -Ipaper_2304_12745_b200/csrc "$@" -Xptxas -v -c paper_2304_12745_b200/csrc/$f.cu \
+    -Ipaper_2304_12745_b200/csrc "$@" -Xptxas -v -c $src \
     -o build/obj/ab/$name/$f.o 2> build/obj/ab/$name/$f.log &
   objs="$objs build/obj/ab/$name/$f.o"
 done

@@ -4,6 +4,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2304_12745_b200 as U
 
+if os.environ.get("UFPGD_HOST_CHUNK_MB"):  # tuning sweep input of this probe (tools/e2e_ab.sh)
+    U.set_option("host_chunk_bytes", int(os.environ["UFPGD_HOST_CHUNK_MB"]) << 20)
+if os.environ.get("UFPGD_E2E_PIPE"):  # 1: the depth-first streams pipeline (A/B)
+    U.set_option("host_pipe", int(os.environ["UFPGD_E2E_PIPE"]))
 w = U.CONFIGS[2]
 H = torch.from_numpy(U.make_inputs(w)).pin_memory()
 W = torch.empty_like(H).pin_memory()

@@ -5,5 +5,5 @@ w = U.CONFIGS[2]
 H = torch.from_numpy(U.make_inputs(w)).pin_memory(); W = torch.empty_like(H).pin_memory()
 lam, eta = w.layer_params()
 for _ in range(2): U.unfolded_forward_host(H.numpy(), lam, eta, w.c, out=W.numpy())
-os.environ["UFPGD_HOST_TIMELINE"] = "1"
+U.set_option("host_timeline", 1)
 U.unfolded_forward_host(H.numpy(), lam, eta, w.c, out=W.numpy())

@@ -9,7 +9,7 @@ import paper_2304_12745_b200 as U
 
 
 def run(H, lam, eta, c, w0_mode=0, W0=None, mma=True):
-    os.environ["UFPGD_NO_MMA"] = "0" if mma else "1"
+    U.set_option("tensor_cores", int(mma))
     Hd = torch.from_numpy(H).cuda()
     W0d = torch.from_numpy(W0).cuda() if W0 is not None else None
     out = U.unfolded_forward(Hd, lam, eta, c, w0_mode=w0_mode, W0=W0d, want_per_realization=True)
@@ -73,7 +73,7 @@ def timing(cfg=4, n=16384, reps=3):
     lam, eta = w.layer_params()
     W = torch.empty_like(Hd)
     for mma in (True, False):
-        os.environ["UFPGD_NO_MMA"] = "0" if mma else "1"
+        U.set_option("tensor_cores", int(mma))
         U.unfolded_forward(Hd, lam, eta, w.c, out=W); torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
@@ -110,7 +110,7 @@ def pgd_timing(cfg, n=4096, iters=1000):
     Hd = torch.empty((n, w.M, w.K), dtype=torch.complex64, device="cuda")
     U.generate_channels_device(w.seed_h, w.seed_g, w.gain_db, 0, n, w.K, w.M, out=Hd)
     for mma in (True, False):
-        os.environ["UFPGD_NO_MMA"] = "0" if mma else "1"
+        U.set_option("tensor_cores", int(mma))
         U.pgd_fixed(Hd, 0.05, 10, w.c); torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(); U.pgd_fixed(Hd, 0.05, iters, w.c); e.record(); torch.cuda.synchronize()

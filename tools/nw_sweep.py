@@ -12,7 +12,7 @@ for cfg, sizes in ((2, (8192, 16384, 32768, 65536, 262144)), (1, (1024, 16384, 6
         lam, eta = w.layer_params()
         row = []
         for nw in (1, 2, 4, 8):
-            os.environ["UFPGD_FUSED_WARPS"] = str(nw)
+            U.set_option("fused_warps", nw)
             for _ in range(3): U.unfolded_forward(H, lam, eta, w.c, out=W)
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             best = 1e9
@@ -22,5 +22,5 @@ for cfg, sizes in ((2, (8192, 16384, 32768, 65536, 262144)), (1, (1024, 16384, 6
                 for _ in range(reps): U.unfolded_forward(H, lam, eta, w.c, out=W)
                 e.record(); torch.cuda.synchronize(); best = min(best, s.elapsed_time(e) / reps)
             row.append(f"nw={nw}: {best*1e3:8.1f} us")
-        del os.environ["UFPGD_FUSED_WARPS"]
+        U.set_option("fused_warps", 0)
         print(f"cfg{cfg} B={n:7d}  " + "  ".join(row), flush=True)

@@ -14,7 +14,7 @@ for K, M in [(3, 10), (6, 48), (5, 40), (7, 64), (8, 50), (12, 100), (24, 200)]:
     res = {}
     for mode in ("pad", "general"):
         if mode == "general":
-            os.environ["UFPGD_NO_PAD"] = "1"
+            U.set_option("zero_pad", 0)
         run = lambda: U.unfolded_forward(H, lam, eta, c, w0_mode=U.W0_ZERO, out=W)
         run(); torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -23,7 +23,7 @@ for K, M in [(3, 10), (6, 48), (5, 40), (7, 64), (8, 50), (12, 100), (24, 200)]:
             run()
         b.record(); torch.cuda.synchronize()
         res[mode] = a.elapsed_time(b) / 5
-        os.environ.pop("UFPGD_NO_PAD", None)
+        U.set_option("zero_pad", 1)
     fl = 20 * (16 * K * K * M + 10 * K * M) * B
     print(f"({K:2d},{M:3d})  padded {res['pad']:8.3f} ms ({fl / res['pad'] / 1e9:5.1f} useful TFLOP/s)   "
           f"general {res['general']:8.3f} ms ({fl / res['general'] / 1e9:5.1f})   x{res['general'] / res['pad']:.2f}", flush=True)
