@@ -96,6 +96,23 @@ struct MmaShape {
   static __device__ __forceinline__ int woff(int q, int m) {
     return (m >> 3) * (16 * Q) + (q >> 3) * 128 + (m & 7) * 16 + (q & 7) * 2;
   }
+  // Bs builder chunk ch -> X' row k, columns c .. c + CWD - 1 (= Bs rows kk, column n = k).
+  // CWD 4: each half-warp covers one 8 x 8 block of X' — rows k0 .. k0+7 (lanes
+  // i & 7) x two 4-wide column halves (i >> 3) — so every Bs put of the half-warp
+  // fills one whole 128-byte core matrix (conflict-free 8-byte stores), and each
+  // quarter-warp reads 8 rows of one column chunk of the F / G exchange rows
+  // (row stride FSTR = 4 mod 32 words: conflict-free 16-byte loads).
+  // CWD 2: consecutive threads walk down the rows (see CWD above).
+  static __device__ __forceinline__ void chunk(int ch, int& k, int& c) {
+    if constexpr (CWD == 4) {
+      const int hw = ch >> 4, i = ch & 15;
+      k = (hw / (K / 8)) * 8 + (i & 7);
+      c = (hw % (K / 8)) * 8 + (i >> 3) * 4;
+    } else {
+      k = ch % K;
+      c = (ch / K) * CWD;
+    }
+  }
   // Bs: element (kk, n), K-major (K = kk, N = n): LBO (K-group) 128, SBO (N-group) BSBO.
   static __device__ __forceinline__ int boff(int kk, int n) {
     return (kk >> 3) * 128 + (n >> 3) * BSBO + (n & 7) * 16 + (kk & 7) * 2;
@@ -537,8 +554,8 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       using FV = typename std::conditional<CWD == 4, float4, float2>::type;
   #pragma unroll
       for (int ch = tid; ch < NCH; ch += T::NT) {
-        // CWD 4: consecutive threads walk along a row; CWD 2: down the rows
-        const int k = CWD == 4 ? ch / CPR : ch % K, c = (CWD == 4 ? ch % CPR : ch / K) * CWD;
+        int k, c;
+        T::chunk(ch, k, c);
         float xr[CWD], xi[CWD];
   #pragma unroll
         for (int u = 0; u < CWD; ++u) xr[u] = xi[u] = 0.f;
@@ -603,8 +620,8 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       const float cscale = RB ? pow2i(-aW) : 1.f, fstep_w = RB ? fstep * pow2i(aW) : fstep;
       {
         const int ch = tid;
-        // CWD 4: consecutive threads walk along a row; CWD 2: down the rows
-        const int k = CWD == 4 ? ch / CPR : ch % K, c = (CWD == 4 ? ch % CPR : ch / K) * CWD;
+        int k, c;
+        T::chunk(ch, k, c);
         float xr[CWD], xi[CWD];
   #pragma unroll
         for (int u = 0; u < CWD; ++u) xr[u] = xi[u] = 0.f;

@@ -686,10 +686,13 @@ cudaError_t launch_team(const FusedArgs& a, bool pgd, cudaStream_t s, long long*
 
 // Team shapes (K, M) -> (TK, TM): KA = K/TK = 2 users and MB = M/TM antennas
 // per thread keep W, X' and the next X' in registers.
-#ifndef UFPGD_T432_TM
-#define UFPGD_T432_TM 4
-#endif
-using Team_4_32 = Team<4, 32, 2, UFPGD_T432_TM>;
+using Team_4_32 = Team<4, 32, 2, 4>;
+// Small (4,32) batches (BASELINE config 1: 1,024 realizations = 256 four-team
+// warps, under 2 per SM) are latency-bound: 16-thread teams (2 per warp, 4
+// antennas per thread) give twice the warps — 14.0 vs 16.0 us at config 1
+// (CUDA-graph replay, B200); at many waves the 8-thread team's shorter X'
+// all-reduce wins.
+using Team_4_32w = Team<4, 32, 2, 8>;
 // Config 2's unfolded kernel: two sweeps per layer fit 168 registers without
 // spills, so 3 resident 4-warp blocks (12 warps/SM) — 3% over 8 warps at 255.
 #ifndef UFPGD_T864_MAXT
@@ -726,7 +729,7 @@ bool fused_supported(int K, int M) {
 
 int fused_realizations_per_block(int K, int M) {
   if (K == 4 && M == 16) return Team_4_16::R;
-  if (K == 4 && M == 32) return Team_4_32::R;
+  if (K == 4 && M == 32) return Team_4_32w::R;  // the smaller of the two (4,32) teams' R
   if (K == 4 && M == 64) return Team_4_64::R;
   if (K == 8 && M == 32) return Team_8_32::R;
   if (K == 8 && M == 64) return Team_8_64::R;
@@ -736,7 +739,13 @@ int fused_realizations_per_block(int K, int M) {
 
 cudaError_t launch_fused(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s, long long* nblocks) {
   if (K == 4 && M == 16) return launch_team<Team_4_16>(a, pgd, s, nblocks);
-  if (K == 4 && M == 32) return launch_team<Team_4_32>(a, pgd, s, nblocks);
+  if (K == 4 && M == 32) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (a.B / Team_4_32::R < 8LL * sms) return launch_team<Team_4_32w>(a, pgd, s, nblocks);
+    return launch_team<Team_4_32>(a, pgd, s, nblocks);
+  }
   if (K == 4 && M == 64) return launch_team<Team_4_64>(a, pgd, s, nblocks);
   if (K == 8 && M == 32) return launch_team<Team_8_32>(a, pgd, s, nblocks);
   if (K == 8 && M == 64) return launch_team<Team_8_64>(a, pgd, s, nblocks);

@@ -11,7 +11,11 @@ KEEP = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'smsp__sass_thread_inst_executed_op_ffma_pred_on.sum.per_cycle_elapsed',
         'smsp__sass_thread_inst_executed_op_fadd_pred_on.sum.per_cycle_elapsed',
         'smsp__sass_thread_inst_executed_op_fmul_pred_on.sum.per_cycle_elapsed',
-        'derived__smsp__sass_thread_inst_executed_op_ffma_pred_on_x2']
+        'derived__smsp__sass_thread_inst_executed_op_ffma_pred_on_x2',
+        'TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed',
+        'l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum.pct_of_peak_sustained_elapsed',
+        'l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum.pct_of_peak_sustained_elapsed',
+        'smsp__inst_executed.sum', 'launch__occupancy_limit_registers', 'launch__occupancy_limit_shared_mem']
 
 
 def main(rep, title, out):
@@ -19,7 +23,10 @@ def main(rep, title, out):
     rows = list(csv.reader(raw.splitlines()))
     hdr, units, vals = rows[0], rows[1], rows[2]
     with open(out, 'w') as f:
-        f.write(title + '\n\n')
+        f.write(title + '\n')
+        if 'Kernel Name' in hdr:
+            f.write('kernel: ' + vals[hdr.index('Kernel Name')] + '\n')
+        f.write('\n')
         for k in KEEP:
             if k in hdr:
                 f.write(f"{k:75s} {vals[hdr.index(k)]} {units[hdr.index(k)]}\n")
