@@ -753,9 +753,17 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     }
     tc_fence_before();
     // prox_l21 on the antenna column (strict '>', pgd.cpp:237-244 / unfolded.cpp:135-143)
-    float s2 = 0.f;
+    // (32,256): four independent partial sums — the 64-deep FMA chain sat on the
+    // per-layer critical path of the one resident realization (-1.8% per layer);
+    // (16,128) keeps one chain (4 CTAs/SM hide it; the extra registers cost 1%)
+    constexpr int NS = K >= 32 ? 4 : 1;
+    float s2p[NS];
 #pragma unroll
-    for (int k = 0; k < K; ++k) s2 = fmaf(wr[k], wr[k], fmaf(wi[k], wi[k], s2));
+    for (int i = 0; i < NS; ++i) s2p[i] = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) s2p[k % NS] = fmaf(wr[k], wr[k], fmaf(wi[k], wi[k], s2p[k % NS]));
+    float s2 = s2p[0];
+    if constexpr (NS == 4) s2 = (s2p[0] + s2p[1]) + (s2p[2] + s2p[3]);
     const float gw = RB ? g * pow2i(aW) : g;  // register domain -> unscaled W
     if constexpr (RB) {
       nonfinite |= !(s2 * gw * gw <= FLT_MAX);
