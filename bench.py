@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-other-configs", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="N > 1: eager steps instead of a CUDA graph")
+    ap.add_argument("--graph", action="store_true", help="capture the step in a CUDA graph at N = 1 as well")
     return ap.parse_args()
 
 
@@ -404,7 +405,7 @@ def run_ours(args, world, rank, local):
         Hd = H_host.to(dev, non_blocking=False)
     Wd = torch.empty_like(Hd)
     stream = torch.cuda.current_stream(dev)
-    use_graph = world > 1 and not args.no_graph
+    use_graph = (world > 1 or args.graph) and not args.no_graph
     step, graph, step_mode = make_step(U, torch, sharding, w, Hd, Wd, lam, eta, world, use_graph)
 
     for _ in range(max(3, args.warmup)):
