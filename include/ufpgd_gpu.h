@@ -231,6 +231,22 @@ int ufpgd_gpu_unfolded_forward_host(const ufpgd_c64* H, int64_t B, int K, int M,
                                     ufpgd_c64* W, int32_t* diverged_at, double* stats,
                                     double alpha, int device);
 
+/*
+ * Asynchronous form of ufpgd_gpu_unfolded_forward_host, for streams of batches:
+ * enqueues the batch's H2D copies, kernels, D2H copies and statistics on the
+ * device's host pipeline and returns at once with a ticket; the pipeline of the
+ * next call starts while this one drains, so back-to-back calls keep both PCIe
+ * directions busy (no per-call fill / drain). H, W0 and W must stay valid (and
+ * should be pinned) until ufpgd_gpu_host_wait(ticket), which also writes
+ * diverged_at and stats and returns UFPGD_EDIVERGED like the synchronous call.
+ * At most 3 calls per device may be in flight (UFPGD_ENOTSUP beyond).
+ */
+int ufpgd_gpu_unfolded_forward_host_async(const ufpgd_c64* H, int64_t B, int K, int M, const double* lambda,
+                                          const double* eta, int L, const double* c, int w0_mode,
+                                          const ufpgd_c64* W0, ufpgd_c64* W, int32_t* diverged_at, double* stats,
+                                          double alpha, int device, int64_t* ticket);
+int ufpgd_gpu_host_wait(int64_t ticket);
+
 /* Same for plain PGD with the in-kernel 1/L step (config 3 end to end). */
 int ufpgd_gpu_pgd_fixed_host(const ufpgd_c64* H, int64_t B, int K, int M, int power_steps,
                              double lambda, int64_t iters, const double* c, int w0_mode,

@@ -46,6 +46,7 @@ from .capi import (  # noqa: F401
     power_v0,
     unfolded_forward,
     unfolded_forward_host,
+    unfolded_forward_host_async,
     unfolded_grad,
     unfolded_backward64,
     ufpd_header,

@@ -71,6 +71,8 @@ def lib():
             "ufpgd_gpu_pgd_fixed": (i, [P, i64, i, i, P, i, d, i64, P, i, P, P, P, P, P, P, P, d, i, P]),
             "ufpgd_gpu_layers_general": (i, [P, i64, i, i, P, P, i, P, i, P, i, d, i, P, P, P, P, P, P, P, i, P]),
             "ufpgd_gpu_unfolded_forward_host": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, P, d, i]),
+            "ufpgd_gpu_unfolded_forward_host_async": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, P, d, i, P]),
+            "ufpgd_gpu_host_wait": (i, [i64]),
             "ufpgd_gpu_pgd_fixed_host": (i, [P, i64, i, i, i, d, i64, P, i, P, P, P, P, P, d, i]),
             "ufpgd_gpu_fp32_peak": (i, [i, P, P]),
             "ufpgd_dataset_last_error": (C.c_char_p, []),
@@ -352,6 +354,48 @@ def unfolded_forward_host(H: np.ndarray, lambda_, eta, c, *, w0_mode: int = W0_Z
         rc = OK
     _check(rc, div)
     return dict(W=W, diverged_at=div, stats=stats)
+
+
+class HostCall:
+    """An enqueued host-buffer call (unfolded_forward_host_async): ``wait()``
+    blocks until its W, diverged_at and stats are in the host buffers and
+    raises DivergenceError like the synchronous call (unless told not to).
+    Keeps its buffers alive until then."""
+
+    def __init__(self, ticket, W, div, stats, keep):
+        self.ticket, self.W, self.diverged_at, self.stats, self._keep = ticket, W, div, stats, keep
+        self._done = False
+
+    def wait(self, raise_on_divergence: bool = True):
+        if not self._done:
+            rc = lib().ufpgd_gpu_host_wait(self.ticket)
+            self._done = True
+            if rc == EDIVERGED and not raise_on_divergence:
+                rc = OK
+            _check(rc, self.diverged_at)
+        return dict(W=self.W, diverged_at=self.diverged_at, stats=self.stats)
+
+
+def unfolded_forward_host_async(H: np.ndarray, lambda_, eta, c, *, w0_mode: int = W0_ZERO, W0=None,
+                                alpha: float = 1.0, out: Optional[np.ndarray] = None, device: int = 0) -> HostCall:
+    """Enqueue-only host-buffer forward: back-to-back calls overlap one batch's
+    copy-out with the next batch's copy-in (H, W0 and out should be pinned)."""
+    H = np.asarray(H)
+    if H.dtype != np.complex64 or H.ndim != 3 or not H.flags.c_contiguous:
+        raise ValueError("H must be a C-contiguous complex64 array [B, M, K]")
+    B, M, K = H.shape
+    lam, et, cc = _f64(lambda_), _f64(eta), _f64(c)
+    _check_w0(w0_mode, W0, H, host=True)
+    _check_host_like(out, H, "out")
+    W = out if out is not None else np.empty_like(H)
+    div = np.empty(B, dtype=np.int32)
+    stats = np.zeros(3)
+    ticket = C.c_int64(-1)
+    rc = lib().ufpgd_gpu_unfolded_forward_host_async(_ptr(H), B, K, M, _ptr(lam), _ptr(et), lam.size, _ptr(cc),
+                                                     w0_mode, _ptr(W0), _ptr(W), _ptr(div), _ptr(stats),
+                                                     float(alpha), device, C.byref(ticket))
+    _check(rc)
+    return HostCall(ticket.value, W, div, stats, (H, W0))
 
 
 def pgd_fixed_host(H: np.ndarray, lambda_: float, iters: int, c, *, power_steps: int = 30,

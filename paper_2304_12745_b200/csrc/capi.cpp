@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -408,27 +409,44 @@ struct ShardSet {
   }
 };
 
-// Per-device workspace of the host-buffer path: NS streams and grow-only
-// device buffers, kept across calls so an end-to-end call costs only its
-// copies and kernels. Host calls on one device are serialised by its mutex.
+// Per-device workspace of the host-buffer path: NS chunk buffer sets, the
+// pipeline streams and NC call slots, kept across calls so an end-to-end call
+// costs only its copies and kernels. Enqueues on one device are serialised by
+// its mutex; up to NC calls may be in flight (ufpgd_gpu_unfolded_forward_host_async).
 struct HostWorkspace {
   std::mutex mu;
+  std::condition_variable slot_free;  // signalled by host_finish
   bool init = false;
-  static constexpr int NS = 4;
+  static constexpr int NS = 4;  // chunk buffer sets
+  static constexpr int NC = 3;  // host calls in flight
   cudaStream_t st[NS] = {};
   // phased pipeline: copy-in, two kernel and copy-out streams, chained per
-  // buffer set by events
+  // buffer set by events (across calls too: set i's previous use may belong to
+  // the previous call)
   cudaStream_t sx[4] = {};
   cudaEvent_t ev[NS][3] = {};
   void* buf[NS][5] = {};
   size_t cap[NS][5] = {};
-  double* partials = nullptr;
-  size_t partials_cap = 0;
-  double* dstats = nullptr;
-  // pinned staging of the small per-realization outputs: a D2H copy into
-  // pageable memory would block the host thread and serialise the pipeline
-  void* pinned = nullptr;
-  size_t pinned_cap = 0;
+  bool set_used[NS] = {};
+  int next_set = 0;
+  uint64_t chunk_seq = 0;
+  // one in-flight call: its statistics partials (device), final statistics,
+  // and pinned staging of the small per-realization outputs (a D2H copy into
+  // pageable memory would block the host thread and serialise the pipeline)
+  struct Call {
+    bool busy = false;
+    uint32_t gen = 0;
+    cudaEvent_t done = nullptr;
+    double* partials = nullptr;
+    size_t partials_cap = 0;
+    double* dstats = nullptr;
+    void* pinned = nullptr;
+    size_t pinned_cap = 0;
+    int32_t* user_div = nullptr;
+    float* user_eta = nullptr;
+    double* user_stats = nullptr;
+    int64_t B = 0;
+  } calls[NC];
 };
 HostWorkspace g_ws[64];
 
@@ -449,6 +467,8 @@ long long host_chunk_bytes() { return option(UFPGD_OPT_HOST_CHUNK_BYTES); }
 void release_workspace(HostWorkspace& ws) {
   std::lock_guard<std::mutex> lock(ws.mu);
   if (!ws.init) return;
+  for (cudaStream_t x : ws.sx)
+    if (x) cudaStreamSynchronize(x);
   for (int i = 0; i < HostWorkspace::NS; ++i) {
     cudaStreamSynchronize(ws.st[i]);
     for (int q = 0; q < 5; ++q) {
@@ -462,42 +482,97 @@ void release_workspace(HostWorkspace& ws) {
       if (ws.ev[i][q]) cudaEventDestroy(ws.ev[i][q]);
       ws.ev[i][q] = nullptr;
     }
+    ws.set_used[i] = false;
   }
   for (cudaStream_t& x : ws.sx) {
-    if (x) {
-      cudaStreamSynchronize(x);
-      cudaStreamDestroy(x);
-    }
+    if (x) cudaStreamDestroy(x);
     x = nullptr;
   }
-  if (ws.partials) cudaFree(ws.partials);
-  if (ws.dstats) cudaFree(ws.dstats);
-  if (ws.pinned) cudaFreeHost(ws.pinned);
-  ws.partials = nullptr;
-  ws.dstats = nullptr;
-  ws.pinned = nullptr;
-  ws.partials_cap = ws.pinned_cap = 0;
+  for (auto& c : ws.calls) {
+    if (c.done) cudaEventDestroy(c.done);
+    if (c.partials) cudaFree(c.partials);
+    if (c.dstats) cudaFree(c.dstats);
+    if (c.pinned) cudaFreeHost(c.pinned);
+    const uint32_t gen = c.gen + 1;
+    c = HostWorkspace::Call{};
+    c.gen = gen;  // outstanding tickets of this device become invalid
+  }
+  ws.next_set = 0;
   ws.init = false;
 }
 
-// Chunked host pipeline shared by the unfolded and PGD host entry points.
+// Host-call tickets: device (8 bits), slot (8 bits), generation (16 bits).
+int64_t make_ticket(int device, int slot, uint32_t gen) {
+  return (static_cast<int64_t>(gen & 0xFFFF) << 16) | (static_cast<int64_t>(slot) << 8) | device;
+}
+
+// Waits for an enqueued host call, copies its small outputs to the caller's
+// pointers and frees its slot. Returns UFPGD_EDIVERGED when a realization diverged.
+int host_finish(int64_t ticket) {
+  const int device = static_cast<int>(ticket & 0xFF), slot = static_cast<int>((ticket >> 8) & 0xFF);
+  const uint32_t gen = static_cast<uint32_t>((ticket >> 16) & 0xFFFF);
+  if (ticket < 0 || device >= 64 || slot >= HostWorkspace::NC) return fail(UFPGD_EINVAL_PARAM, "bad host-call ticket");
+  HostWorkspace& ws = g_ws[device];
+  HostWorkspace::Call* c = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(ws.mu);
+    c = &ws.calls[slot];
+    if (!c->busy || (c->gen & 0xFFFF) != gen) return fail(UFPGD_EINVAL_PARAM, "host-call ticket already completed");
+  }
+  cudaError_t e = cudaEventSynchronize(c->done);
+  double host_stats[3] = {0.0, 0.0, 0.0};
+  if (e == cudaSuccess) {
+    const char* base = static_cast<const char*>(c->pinned);
+    std::memcpy(host_stats, base, sizeof(host_stats));
+    size_t off = 64;
+    if (c->user_div) std::memcpy(c->user_div, base + off, sizeof(int32_t) * c->B);
+    if (c->user_div) off += sizeof(int32_t) * c->B;
+    if (c->user_eta) std::memcpy(c->user_eta, base + off, sizeof(float) * c->B);
+    if (c->user_stats) std::memcpy(c->user_stats, host_stats, sizeof(host_stats));
+  }
+  {
+    std::lock_guard<std::mutex> lock(ws.mu);
+    c->busy = false;
+    ++c->gen;
+  }
+  ws.slot_free.notify_all();
+  if (e != cudaSuccess) return cuda_fail(e, "host pipeline");
+  if (host_stats[2] > 0.0) return fail(UFPGD_EDIVERGED, "non-finite iterate in at least one realization");
+  return UFPGD_OK;
+}
+
+// Chunked host pipeline shared by the unfolded and PGD host entry points:
+// enqueues every chunk's H2D, kernel and D2H plus the statistics finalisation,
+// and returns a ticket for host_finish (the call itself does not wait).
 // `run` enqueues the kernel for one chunk on stream s given device buffers.
+// block_for_slot: the synchronous entry points wait for a free call slot
+// (concurrent callers on one device); the asynchronous one reports UFPGD_ENOTSUP.
 template <class Run>
-int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const ufpgd_c64* W0,
-                  ufpgd_c64* W, int32_t* diverged_at, float* eta_out, long long parts_per_chunk_max,
-                  int64_t chunk, double* stats, Run run) {
+int host_enqueue(int device, const ufpgd_c64* H, int64_t B, int K, int M, const ufpgd_c64* W0, ufpgd_c64* W,
+                 int32_t* diverged_at, float* eta_out, long long parts_per_chunk_max, int64_t chunk, double* stats,
+                 Run run, int64_t* ticket, bool block_for_slot) {
   if (device < 0 || device >= 64) return fail(UFPGD_EINVAL_PARAM, "device out of range");
   HostWorkspace& ws = g_ws[device];
-  std::lock_guard<std::mutex> lock(ws.mu);
+  std::unique_lock<std::mutex> lock(ws.mu);
   constexpr int NS = HostWorkspace::NS;
   if (!ws.init) {
     for (int i = 0; i < NS; ++i) UFPGD_CUDA(cudaStreamCreateWithFlags(&ws.st[i], cudaStreamNonBlocking));
     for (cudaStream_t& x : ws.sx) UFPGD_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
     for (int i = 0; i < NS; ++i)
       for (int q = 0; q < 3; ++q) UFPGD_CUDA(cudaEventCreateWithFlags(&ws.ev[i][q], cudaEventDisableTiming));
-    UFPGD_CUDA(cudaMalloc(&ws.dstats, sizeof(double) * 3));
+    for (auto& c : ws.calls) UFPGD_CUDA(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming));
     ws.init = true;
   }
+  int slot = -1;
+  for (;;) {
+    for (int i = 0; i < HostWorkspace::NC && slot < 0; ++i)
+      if (!ws.calls[i].busy) slot = i;
+    if (slot >= 0) break;
+    if (!block_for_slot)
+      return fail(UFPGD_ENOTSUP, "too many host calls in flight on this device (wait for one first)");
+    ws.slot_free.wait(lock);
+  }
+  HostWorkspace::Call& call = ws.calls[slot];
   const size_t per = static_cast<size_t>(K) * M * sizeof(float2);
   // Chunk boundaries (a geometric ramp of the first / last chunks was measured
   // and is no faster with the phased pipeline: the copy-out stream paces it).
@@ -508,26 +583,35 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
   const size_t need[5] = {per * chunk, per * chunk, W0 ? per * chunk : 0, sizeof(int32_t) * chunk,
                           eta_out ? sizeof(float) * chunk : 0};
   cudaError_t e = cudaSuccess;
+  // a buffer set being regrown may still be in use by an earlier call
+  bool regrow = false;
+  for (int i = 0; i < NS; ++i)
+    for (int q = 0; q < 5; ++q) regrow |= need[q] > ws.cap[i][q];
+  if (regrow) {
+    for (cudaStream_t x : ws.sx) cudaStreamSynchronize(x);
+    for (cudaStream_t x : ws.st) cudaStreamSynchronize(x);
+  }
   for (int i = 0; i < NS && e == cudaSuccess; ++i)
     for (int q = 0; q < 5 && e == cudaSuccess; ++q) e = ensure(ws.buf[i][q], ws.cap[i][q], need[q]);
   if (e == cudaSuccess) {
-    void* pp = ws.partials;
-    e = ensure(pp, ws.partials_cap, sizeof(double) * 3 * std::max<long long>(1, parts_per_chunk_max * nchunks));
-    ws.partials = static_cast<double*>(pp);
+    void* pp = call.partials;
+    e = ensure(pp, call.partials_cap, sizeof(double) * 3 * std::max<long long>(1, parts_per_chunk_max * nchunks));
+    call.partials = static_cast<double*>(pp);
   }
-  const size_t small_need = (diverged_at ? sizeof(int32_t) * B : 0) + (eta_out ? sizeof(float) * B : 0) + 64;
-  if (e == cudaSuccess && small_need > ws.pinned_cap) {
-    if (ws.pinned) cudaFreeHost(ws.pinned);
-    ws.pinned = nullptr;
-    ws.pinned_cap = 0;
-    e = cudaHostAlloc(&ws.pinned, small_need, cudaHostAllocDefault);
-    if (e == cudaSuccess) ws.pinned_cap = small_need;
+  if (e == cudaSuccess && !call.dstats) e = cudaMalloc(&call.dstats, sizeof(double) * 3);
+  const size_t small_need = 64 + (diverged_at ? sizeof(int32_t) * B : 0) + (eta_out ? sizeof(float) * B : 0);
+  if (e == cudaSuccess && small_need > call.pinned_cap) {
+    if (call.pinned) cudaFreeHost(call.pinned);
+    call.pinned = nullptr;
+    call.pinned_cap = 0;
+    e = cudaHostAlloc(&call.pinned, small_need, cudaHostAllocDefault);
+    if (e == cudaSuccess) call.pinned_cap = small_need;
   }
   if (e != cudaSuccess) return cuda_fail(e, "host pipeline allocation");
-  int32_t* div_stage = diverged_at ? static_cast<int32_t*>(ws.pinned) : nullptr;
-  float* eta_stage = eta_out ? reinterpret_cast<float*>(static_cast<char*>(ws.pinned) +
-                                                        (diverged_at ? sizeof(int32_t) * B : 0))
-                             : nullptr;
+  char* pin = static_cast<char*>(call.pinned);
+  double* stats_stage = reinterpret_cast<double*>(pin);
+  int32_t* div_stage = diverged_at ? reinterpret_cast<int32_t*>(pin + 64) : nullptr;
+  float* eta_stage = eta_out ? reinterpret_cast<float*>(pin + 64 + (diverged_at ? sizeof(int32_t) * B : 0)) : nullptr;
   int rc = UFPGD_OK;
   std::vector<long long> part_off(nchunks + 1, 0);
   // Default pipeline ("phased"): one copy-in stream, two kernel streams, one
@@ -543,16 +627,26 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
   const bool timeline = option(UFPGD_OPT_HOST_TIMELINE) != 0;
   std::vector<cudaEvent_t> tev(timeline ? 4 * nchunks : 0);
   for (cudaEvent_t& ev : tev) cudaEventCreate(&ev);
-  // Buffer set i = chunk % NS; events: 0 = copy-in done, 1 = kernel done,
-  // 2 = copy-out done. Copy-in of chunk k reuses the H buffer of chunk k - NS
-  // (waits for its kernel); the kernel reuses its W buffer (waits for its
-  // copy-out).
+  // Chunk ci uses buffer set set_of[ci] (a rotation that continues across
+  // calls); events: 0 = copy-in done, 1 = kernel done, 2 = copy-out done. The
+  // copy-in reuses the set's H buffer (waits for its previous kernel); the
+  // kernel reuses its W buffer (waits for its previous copy-out).
+  std::vector<int> set_of(nchunks);
+  for (int64_t ci = 0; ci < nchunks; ++ci) set_of[ci] = (ws.next_set + static_cast<int>(ci % NS)) % NS;
   cudaStream_t sin = ws.sx[0], sout = ws.sx[3];
+  if (phased)  // an earlier depth-first (A/B) call may still use the buffer sets
+    for (int i = 1; i < NS; ++i) {
+      cudaEvent_t j;
+      cudaEventCreateWithFlags(&j, cudaEventDisableTiming);
+      cudaEventRecord(j, ws.st[i]);
+      for (cudaStream_t x : ws.sx) cudaStreamWaitEvent(x, j, 0);
+      cudaEventDestroy(j);
+    }
   auto copy_out = [&](int64_t cj) -> int {
-    const int j = static_cast<int>(cj % NS);
+    const int j = set_of[cj];
     const int64_t b0 = cs[cj], nb = cs[cj + 1] - b0;
     cudaStreamWaitEvent(sout, ws.ev[j][1], 0);
-    if (cj + 1 < nchunks) cudaStreamWaitEvent(sout, ws.ev[(cj + 1) % NS][0], 0);
+    if (cj + 1 < nchunks) cudaStreamWaitEvent(sout, ws.ev[set_of[cj + 1]][0], 0);
     cudaError_t x = cudaMemcpyAsync(W + b0 * K * M, ws.buf[j][1], per * nb, cudaMemcpyDeviceToHost, sout);
     if (x == cudaSuccess && diverged_at)
       x = cudaMemcpyAsync(div_stage + b0, ws.buf[j][3], sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, sout);
@@ -564,15 +658,15 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
     return UFPGD_OK;
   };
   for (int64_t ci = 0; ci < nchunks && rc == UFPGD_OK && phased; ++ci) {
-    const int i = static_cast<int>(ci % NS);
+    const int i = set_of[ci];
     const int64_t b0 = cs[ci], nb = cs[ci + 1] - b0;
-    cudaStream_t sk = ws.sx[1 + (ci & 1)];
+    cudaStream_t sk = ws.sx[1 + ((ws.chunk_seq + ci) & 1)];
     float2* dh = static_cast<float2*>(ws.buf[i][0]);
     float2* dw = static_cast<float2*>(ws.buf[i][1]);
     float2* dw0 = static_cast<float2*>(ws.buf[i][2]);
     int32_t* ddiv = static_cast<int32_t*>(ws.buf[i][3]);
     float* deta = static_cast<float*>(ws.buf[i][4]);
-    if (ci >= NS) cudaStreamWaitEvent(sin, ws.ev[i][1], 0);
+    if (ws.set_used[i]) cudaStreamWaitEvent(sin, ws.ev[i][1], 0);
     if (timeline) cudaEventRecord(tev[4 * ci], sin);
     e = cudaMemcpyAsync(dh, H + b0 * K * M, per * nb, cudaMemcpyHostToDevice, sin);
     if (e == cudaSuccess && W0) e = cudaMemcpyAsync(dw0, W0 + b0 * K * M, per * nb, cudaMemcpyHostToDevice, sin);
@@ -583,30 +677,34 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
     cudaEventRecord(ws.ev[i][0], sin);
     if (timeline) cudaEventRecord(tev[4 * ci + 1], sin);
     cudaStreamWaitEvent(sk, ws.ev[i][0], 0);
-    if (ci >= NS) cudaStreamWaitEvent(sk, ws.ev[i][2], 0);
+    if (ws.set_used[i]) cudaStreamWaitEvent(sk, ws.ev[i][2], 0);
     long long np = 0;
-    rc = run(dh, nb, W0 ? dw0 : nullptr, dw, ddiv, eta_out ? deta : nullptr, ws.partials + 3 * part_off[ci], &np, sk);
+    rc = run(dh, nb, W0 ? dw0 : nullptr, dw, ddiv, eta_out ? deta : nullptr, call.partials + 3 * part_off[ci], &np, sk);
     if (rc != UFPGD_OK) break;
     part_off[ci + 1] = part_off[ci] + np;
     cudaEventRecord(ws.ev[i][1], sk);
+    ws.set_used[i] = true;
     if (timeline) cudaEventRecord(tev[4 * ci + 2], sk);
     if (ci >= 1) rc = copy_out(ci - 1);
   }
   if (phased && rc == UFPGD_OK && nchunks > 0) rc = copy_out(nchunks - 1);
   if (phased) {
-    // join the pipeline streams into st[1..NS-1] so the common tail below sees them
-    for (int x = 0; x < 4; ++x) {
-      cudaEvent_t j;
-      cudaEventCreateWithFlags(&j, cudaEventDisableTiming);
-      cudaEventRecord(j, ws.sx[x]);
-      cudaStreamWaitEvent(ws.st[1 + x % (NS - 1)], j, 0);
-      cudaEventDestroy(j);
-    }
+    ws.next_set = (ws.next_set + static_cast<int>(nchunks % NS)) % NS;
+    ws.chunk_seq += static_cast<uint64_t>(nchunks);
   }
   for (int64_t ci = 0; ci < nchunks && rc == UFPGD_OK && !phased; ++ci) {
+    // depth-first A/B pipeline (UFPGD_OPT_HOST_PIPE = 1): each chunk's copies
+    // and kernel on one of the NS streams; it joins the call's tail below
     const int i = static_cast<int>(ci % NS);
     const int64_t b0 = cs[ci], nb = cs[ci + 1] - b0;
     cudaStream_t s = ws.st[i];
+    for (cudaStream_t x : ws.sx) {  // the phased streams may hold an earlier call's use of set i
+      cudaEvent_t j;
+      cudaEventCreateWithFlags(&j, cudaEventDisableTiming);
+      cudaEventRecord(j, x);
+      cudaStreamWaitEvent(s, j, 0);
+      cudaEventDestroy(j);
+    }
     float2* dh = static_cast<float2*>(ws.buf[i][0]);
     float2* dw = static_cast<float2*>(ws.buf[i][1]);
     float2* dw0 = static_cast<float2*>(ws.buf[i][2]);
@@ -621,7 +719,7 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
       break;
     }
     long long np = 0;
-    rc = run(dh, nb, W0 ? dw0 : nullptr, dw, ddiv, eta_out ? deta : nullptr, ws.partials + 3 * part_off[ci], &np, s);
+    rc = run(dh, nb, W0 ? dw0 : nullptr, dw, ddiv, eta_out ? deta : nullptr, call.partials + 3 * part_off[ci], &np, s);
     if (rc != UFPGD_OK) break;
     part_off[ci + 1] = part_off[ci] + np;
     if (timeline) cudaEventRecord(tev[4 * ci + 2], s);
@@ -633,8 +731,32 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
     if (e != cudaSuccess) rc = cuda_fail(e, "D2H");
     if (timeline) cudaEventRecord(tev[4 * ci + 3], s);
   }
+  // the call's tail on st[0]: after every stream that carried its chunks, the
+  // statistics finalisation and their copy into the pinned slot, then `done`
+  for (cudaStream_t x : ws.sx) {
+    cudaEvent_t j;
+    cudaEventCreateWithFlags(&j, cudaEventDisableTiming);
+    cudaEventRecord(j, x);
+    cudaStreamWaitEvent(ws.st[0], j, 0);
+    cudaEventDestroy(j);
+  }
+  if (!phased)
+    for (int i = 1; i < NS; ++i) {
+      cudaEvent_t j;
+      cudaEventCreateWithFlags(&j, cudaEventDisableTiming);
+      cudaEventRecord(j, ws.st[i]);
+      cudaStreamWaitEvent(ws.st[0], j, 0);
+      cudaEventDestroy(j);
+    }
+  if (rc == UFPGD_OK) {
+    e = launch_stats_finalize(call.partials, part_off[nchunks], call.dstats, ws.st[0]);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(stats_stage, call.dstats, sizeof(double) * 3, cudaMemcpyDeviceToHost, ws.st[0]);
+    if (e == cudaSuccess) e = cudaEventRecord(call.done, ws.st[0]);
+    if (e != cudaSuccess) rc = cuda_fail(e, "host pipeline finalize");
+  }
   if (timeline) {
-    for (int i = 0; i < NS; ++i) cudaStreamSynchronize(ws.st[i]);
+    cudaStreamSynchronize(ws.st[0]);
     for (int64_t ci = 0; ci < nchunks; ++ci) {
       float t[4];
       for (int q = 0; q < 4; ++q) cudaEventElapsedTime(&t[q], tev[0], tev[4 * ci + q]);
@@ -643,29 +765,30 @@ int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const
     }
     for (cudaEvent_t ev : tev) cudaEventDestroy(ev);
   }
-  double host_stats[3] = {0.0, 0.0, 0.0};
-  if (rc == UFPGD_OK) {
-    for (int i = 1; i < NS; ++i) {
-      cudaEvent_t ev;
-      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-      cudaEventRecord(ev, ws.st[i]);
-      cudaStreamWaitEvent(ws.st[0], ev, 0);
-      cudaEventDestroy(ev);
-    }
-    e = launch_stats_finalize(ws.partials, part_off[nchunks], ws.dstats, ws.st[0]);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(host_stats, ws.dstats, sizeof(host_stats), cudaMemcpyDeviceToHost, ws.st[0]);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ws.st[0]);
-    if (e != cudaSuccess) rc = cuda_fail(e, "host pipeline finalize");
+  if (rc != UFPGD_OK) {  // leave no work behind that still writes into the caller's buffers
+    for (cudaStream_t x : ws.sx) cudaStreamSynchronize(x);
+    for (int i = 0; i < NS; ++i) cudaStreamSynchronize(ws.st[i]);
+    return rc;
   }
-  for (int i = 0; i < NS; ++i) cudaStreamSynchronize(ws.st[i]);
-  for (cudaStream_t x : ws.sx) cudaStreamSynchronize(x);
-  if (rc != UFPGD_OK) return rc;
-  if (diverged_at) std::memcpy(diverged_at, div_stage, sizeof(int32_t) * B);
-  if (eta_out) std::memcpy(eta_out, eta_stage, sizeof(float) * B);
-  if (stats) std::memcpy(stats, host_stats, sizeof(host_stats));
-  if (host_stats[2] > 0.0) return fail(UFPGD_EDIVERGED, "non-finite iterate in at least one realization");
+  call.busy = true;
+  call.user_div = diverged_at;
+  call.user_eta = eta_out;
+  call.user_stats = stats;
+  call.B = B;
+  *ticket = make_ticket(device, slot, call.gen);
   return UFPGD_OK;
+}
+
+// Synchronous form: enqueue, then wait.
+template <class Run>
+int host_pipeline(int device, const ufpgd_c64* H, int64_t B, int K, int M, const ufpgd_c64* W0, ufpgd_c64* W,
+                  int32_t* diverged_at, float* eta_out, long long parts_per_chunk_max, int64_t chunk, double* stats,
+                  Run run) {
+  int64_t ticket = -1;
+  const int rc = host_enqueue(device, H, B, K, M, W0, W, diverged_at, eta_out, parts_per_chunk_max, chunk, stats,
+                              run, &ticket, true);
+  if (rc != UFPGD_OK) return rc;
+  return host_finish(ticket);
 }
 
 }  // namespace
@@ -1119,10 +1242,10 @@ int ufpgd_gpu_oracle_solve(const double* H, int64_t B, int K, int M, const doubl
   return rc;
 }
 
-int ufpgd_gpu_unfolded_forward_host(const ufpgd_c64* H, int64_t B, int K, int M,
-                                    const double* lambda, const double* eta, int L, const double* c,
-                                    int w0_mode, const ufpgd_c64* W0, ufpgd_c64* W,
-                                    int32_t* diverged_at, double* stats, double alpha, int device) {
+namespace {
+int unfolded_host(const ufpgd_c64* H, int64_t B, int K, int M, const double* lambda, const double* eta, int L,
+                  const double* c, int w0_mode, const ufpgd_c64* W0, ufpgd_c64* W, int32_t* diverged_at,
+                  double* stats, double alpha, int device, int64_t* ticket) {
   int rc;
   if ((rc = check_shape(B, K, M)) || (rc = check_layers(lambda, eta, L)) || (rc = check_c(c, K)) ||
       (rc = check_w0(w0_mode, W0)))
@@ -1135,14 +1258,35 @@ int ufpgd_gpu_unfolded_forward_host(const ufpgd_c64* H, int64_t B, int K, int M,
   // 16 MiB of H per chunk: short pipeline fill, chunks still fill the GPU.
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(B, host_chunk_bytes() / (8ll * K * M)));
   const long long ppc = partial_count(chunk, K, M, fused);
-  return host_pipeline(
-      device, H, B, K, M, w0_mode == UFPGD_W0_GIVEN ? W0 : nullptr, W, diverged_at, nullptr, ppc, chunk, stats,
-      [&](float2* h, int64_t nb, float2* w0, float2* w, int32_t* div, float*, double* parts,
-          long long* np, cudaStream_t s) {
-        return enqueue_unfolded(h, nb, K, M, lambda, eta, L, c, w0_mode, w0, w, div, nullptr, nullptr,
-                                parts, alpha, s, np);
-      });
+  auto run = [&](float2* h, int64_t nb, float2* w0, float2* w, int32_t* div, float*, double* parts, long long* np,
+                 cudaStream_t s) {
+    return enqueue_unfolded(h, nb, K, M, lambda, eta, L, c, w0_mode, w0, w, div, nullptr, nullptr, parts, alpha, s,
+                            np);
+  };
+  const ufpgd_c64* w0 = w0_mode == UFPGD_W0_GIVEN ? W0 : nullptr;
+  if (ticket)
+    return host_enqueue(device, H, B, K, M, w0, W, diverged_at, nullptr, ppc, chunk, stats, run, ticket, false);
+  return host_pipeline(device, H, B, K, M, w0, W, diverged_at, nullptr, ppc, chunk, stats, run);
 }
+}  // namespace
+
+int ufpgd_gpu_unfolded_forward_host(const ufpgd_c64* H, int64_t B, int K, int M,
+                                    const double* lambda, const double* eta, int L, const double* c,
+                                    int w0_mode, const ufpgd_c64* W0, ufpgd_c64* W,
+                                    int32_t* diverged_at, double* stats, double alpha, int device) {
+  return unfolded_host(H, B, K, M, lambda, eta, L, c, w0_mode, W0, W, diverged_at, stats, alpha, device, nullptr);
+}
+
+int ufpgd_gpu_unfolded_forward_host_async(const ufpgd_c64* H, int64_t B, int K, int M, const double* lambda,
+                                          const double* eta, int L, const double* c, int w0_mode,
+                                          const ufpgd_c64* W0, ufpgd_c64* W, int32_t* diverged_at, double* stats,
+                                          double alpha, int device, int64_t* ticket) {
+  if (!ticket) return fail(UFPGD_EINVAL_PARAM, "ticket is required");
+  *ticket = -1;
+  return unfolded_host(H, B, K, M, lambda, eta, L, c, w0_mode, W0, W, diverged_at, stats, alpha, device, ticket);
+}
+
+int ufpgd_gpu_host_wait(int64_t ticket) { return host_finish(ticket); }
 
 int ufpgd_gpu_pgd_fixed_host(const ufpgd_c64* H, int64_t B, int K, int M, int power_steps,
                              double lambda, int64_t iters, const double* c, int w0_mode,
