@@ -893,10 +893,16 @@ cudaError_t launch_mma_t(const FusedArgs& args, bool pgd, cudaStream_t s, long l
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) {
-    int dev = 0, sms = 148;
+    // one wave of the robust instance: enough CTAs for a batch that is handed
+    // off entirely (e.g. every channel far outside the f16 range), and a few
+    // hundred CTAs that read a zero count and exit in the usual case
+    int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    robust<<<static_cast<unsigned>(std::min<long long>(a.B, sms)), T::NT, T::SMEM, s>>>(a, list + 1, list);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, robust, T::NT, T::SMEM) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    const long long grid = std::min<long long>(a.B, static_cast<long long>(sms) * per_sm);
+    robust<<<static_cast<unsigned>(grid), T::NT, T::SMEM, s>>>(a, list + 1, list);
     e = cudaGetLastError();
   }
   cudaFreeAsync(list, s);

@@ -257,3 +257,21 @@ def test_mma_extreme_constraint_scales_use_the_range_robust_path(K, M, cscale):
     print(f"({K},{M}) c x{cscale:g}: tcgen05 rel {rg['rel_max']:.2e}, tile rel {rt['rel_max']:.2e}")
     assert_parity(rg)
     assert rg["rel_max"] <= max(3 * rt["rel_max"], 5e-6)
+
+
+def test_mma_whole_batch_handed_to_the_range_robust_path():
+    """Every realization of a config-5-shaped batch out of the fast path's
+    range (W0 = H^* at max |H| ~ 1e3): the robust instance processes the whole
+    batch (one wave of CTAs looping over the redo list) and matches the
+    CUDA-core tile kernel; the statistics cover every realization."""
+    w = U.CONFIGS[5]
+    a = 1000.0
+    H = (U.make_inputs(w, 3, 4096) * np.float32(a)).astype(np.complex64)
+    lam, eta = w.layer_params()
+    lam, eta = lam * a, eta / (a * a)
+    g = run(H, lam, eta, w.c, w0_mode=U.W0_CONJ_H)
+    t = run(H, lam, eta, w.c, w0_mode=U.W0_CONJ_H, mma=False)
+    assert np.all(g["diverged_at"] == -1)
+    assert np.array_equal(g["active"], t["active"])
+    assert rel_fro(g["W"], t["W"].astype(np.complex128)).max() < 5e-5
+    assert g["stats"][1] == g["active"].sum()
