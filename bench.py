@@ -554,7 +554,9 @@ def run_ours(args, world, rank, local):
                             "for one step later)" + ("" if ne == B else f"; {ne} realizations of the shard per step"),
                     "synchronous_value": e2e_sync,
                     "synchronous_path": "ufpgd_gpu_unfolded_forward_host, one blocking call per step"},
-            "gpu_launches": 2 * args.steps,
+            # per step: the forward kernel (+ the tcgen05 path's range-robust
+            # instance, which exits at once when nothing is handed off) and stats_finalize
+            "gpu_launches": (3 if w.config == 5 else 2) * args.steps,
             "clocks": clocks.report(),
             "stats": sharding.summarize(stats, total),
             "other_configs": others,
