@@ -319,8 +319,10 @@ __global__ void __launch_bounds__(128) lipschitz_exact_kernel(const double2* __r
 }
 
 // Deterministic sum of per-block partials [n][3] -> stats[3].
-__global__ void __launch_bounds__(256) stats_finalize_kernel(const double* __restrict__ part, long long n,
-                                                             double* __restrict__ stats) {
+// Small partial counts (config 1, config 2: up to 16 Ki): one 256-thread block,
+// thread-strided triples, fixed tree.
+__global__ void __launch_bounds__(256) stats_finalize_small_kernel(const double* __restrict__ part, long long n,
+                                                                   double* __restrict__ stats) {
   __shared__ double acc[3][256];
   double s[3] = {0.0, 0.0, 0.0};
   for (long long i = threadIdx.x; i < n; i += 256)
@@ -336,6 +338,45 @@ __global__ void __launch_bounds__(256) stats_finalize_kernel(const double* __res
     __syncthreads();
   }
   if (threadIdx.x < 3) stats[threadIdx.x] = acc[threadIdx.x][0];
+}
+
+// Deterministic sum of n partial triples (block partials of the fused kernels)
+// over the range [i0, i1): the triples are read as one coalesced stream of
+// doubles (thread t takes doubles t, t + T, ...; double e belongs to column
+// e % 3), each thread keeps one sum per column in a fixed order, then a fixed
+// shared-memory tree combines the threads. Grid-wide: block b sums its range
+// into out[3 b]; a single block (out = stats) finishes.
+template <int kFinT>
+__global__ void __launch_bounds__(kFinT) stats_finalize_kernel(const double* __restrict__ part, long long n,
+                                                               long long per_block, double* __restrict__ out) {
+  static_assert(kFinT % 3 == 1, "column bookkeeping: thread t's next double is in column (c + 1) % 3");
+  __shared__ double acc[3][kFinT];
+  const long long i0 = static_cast<long long>(blockIdx.x) * per_block;
+  const long long i1 = min(n, i0 + per_block);
+  double s[3] = {0.0, 0.0, 0.0};
+  if (i1 > i0) {
+    const double* p = part + 3 * i0;
+    const long long nd = 3 * (i1 - i0);
+    int c = static_cast<int>(threadIdx.x % 3);  // column of double threadIdx.x + j kFinT (kFinT % 3 == 1)
+#pragma unroll 4
+    for (long long e = threadIdx.x; e < nd; e += kFinT) {
+      const double v = p[e];
+      s[0] += c == 0 ? v : 0.0;
+      s[1] += c == 1 ? v : 0.0;
+      s[2] += c == 2 ? v : 0.0;
+      c = c == 2 ? 0 : c + 1;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 3; ++q) acc[q][threadIdx.x] = s[q];
+  __syncthreads();
+  for (int w = kFinT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) acc[q][threadIdx.x] += acc[q][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x < 3) out[3 * blockIdx.x + threadIdx.x] = acc[threadIdx.x][0];
 }
 
 }  // namespace
@@ -387,8 +428,34 @@ cudaError_t launch_lipschitz_exact(const double2* H, long long B, int K, int M, 
 }
 
 cudaError_t launch_stats_finalize(const double* partials, long long n, double* stats, cudaStream_t s) {
-  stats_finalize_kernel<<<1, 256, 0, s>>>(partials, n, stats);
-  return cudaGetLastError();
+  // Up to 64 Ki partials (config 2: 8,192 blocks): one block. Beyond (the
+  // tcgen05 kernel writes one triple per realization: 2^20 at config 5), a
+  // first pass of up to 296 blocks over contiguous ranges, then one block over
+  // their sums — the order of every addition is fixed, so the result is
+  // deterministic and independent of scheduling.
+  // Small n: the 256-thread strided kernel (its latency is lowest at config 1).
+  constexpr long long kOneBlock = 1LL << 16;
+  if (n <= 16384) {
+    stats_finalize_small_kernel<<<1, 256, 0, s>>>(partials, n, stats);
+    return cudaGetLastError();
+  }
+  if (n <= kOneBlock) {
+    stats_finalize_kernel<1024><<<1, 1024, 0, s>>>(partials, n, n, stats);
+    return cudaGetLastError();
+  }
+  const long long G = std::min<long long>(296, (n + kOneBlock / 8 - 1) / (kOneBlock / 8));
+  const long long per = (n + G - 1) / G;
+  double* mid = nullptr;
+  cudaError_t e = scratch_alloc_async(reinterpret_cast<void**>(&mid), sizeof(double) * 3 * G, s);
+  if (e != cudaSuccess) return e;
+  stats_finalize_kernel<1024><<<static_cast<unsigned>(G), 1024, 0, s>>>(partials, n, per, mid);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    stats_finalize_kernel<256><<<1, 256, 0, s>>>(mid, G, G, stats);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(mid, s);
+  return e;
 }
 
 }  // namespace ufpgd_gpu_impl
