@@ -531,10 +531,18 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         }
         if (quad < 2) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) a[i] = fmaf(kLoScale, b[i], a[i]);  // hi rows: W_hi H_hi + W_hi H_lo
+          for (int i = 0; i < 16; i += 2) {  // hi rows: W_hi H_hi + W_hi H_lo (packed FP32x2)
+            const float2 t = ffma2(kLoScale, make_float2(b[i], b[i + 1]), make_float2(a[i], a[i + 1]));
+            a[i] = t.x;
+            a[i + 1] = t.y;
+          }
         } else {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) a[i] *= kLoScale;  // lo rows: W_lo H_hi
+          for (int i = 0; i < 16; i += 2) {  // lo rows: W_lo H_hi
+            const float2 t = fmul2(kLoScale, make_float2(a[i], a[i + 1]));
+            a[i] = t.x;
+            a[i + 1] = t.y;
+          }
         }
         if (lane < K) {
           if constexpr (T::CWD == 4) {
@@ -752,7 +760,12 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
             for (int i = 0; i < 16; ++i) w[j0 + i] = fmaf(u2, fmaf(kLoScale, b[i], a[i]), w[j0 + i]);
           } else {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) w[j0 + i] += fmaf(kLoScale, b[i], a[i]);  // V = W - eta X' H^*
+            for (int i = 0; i < 16; i += 2) {  // V = W - eta X' H^* (packed FP32x2)
+              const float2 t = fadd2(make_float2(w[j0 + i], w[j0 + i + 1]),
+                                     ffma2(kLoScale, make_float2(b[i], b[i + 1]), make_float2(a[i], a[i + 1])));
+              w[j0 + i] = t.x;
+              w[j0 + i + 1] = t.y;
+            }
           }
         }
       }
@@ -762,14 +775,18 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     // (32,256): four independent partial sums — the 64-deep FMA chain sat on the
     // per-layer critical path of the one resident realization (-1.8% per layer);
     // (16,128) keeps one chain (4 CTAs/SM hide it; the extra registers cost 1%)
-    constexpr int NS = K >= 32 ? 4 : 1;
-    float s2p[NS];
+    // packed FP32x2: one pair of partial sums per chain, NS chains
+    constexpr int NS = K >= 32 ? 2 : 1;
+    float2 s2p[NS];
 #pragma unroll
-    for (int i = 0; i < NS; ++i) s2p[i] = 0.f;
+    for (int i = 0; i < NS; ++i) s2p[i] = zero2();
 #pragma unroll
-    for (int k = 0; k < K; ++k) s2p[k % NS] = fmaf(wr[k], wr[k], fmaf(wi[k], wi[k], s2p[k % NS]));
-    float s2 = s2p[0];
-    if constexpr (NS == 4) s2 = (s2p[0] + s2p[1]) + (s2p[2] + s2p[3]);
+    for (int k = 0; k < K; k += 2) {
+      const float2 r2 = make_float2(wr[k], wr[k + 1]), i2 = make_float2(wi[k], wi[k + 1]);
+      s2p[(k / 2) % NS] = __ffma2_rn(r2, r2, __ffma2_rn(i2, i2, s2p[(k / 2) % NS]));
+    }
+    float s2 = s2p[0].x + s2p[0].y;
+    if constexpr (NS == 2) s2 = (s2p[0].x + s2p[0].y) + (s2p[1].x + s2p[1].y);
     const float gw = RB ? g * pow2i(aW) : g;  // register domain -> unscaled W
     if constexpr (RB) {
       nonfinite |= !(s2 * gw * gw <= FLT_MAX);
@@ -780,9 +797,12 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     const float r = rsqrt_ftz(fmaxf(s2, FLT_MIN));
     const float scale = on ? fmaf(-ts, r, 1.f) : 0.f;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      wr[k] *= scale;
-      wi[k] *= scale;
+    for (int k = 0; k < K; k += 2) {
+      const float2 r2 = fmul2(scale, make_float2(wr[k], wr[k + 1])), i2 = fmul2(scale, make_float2(wi[k], wi[k + 1]));
+      wr[k] = r2.x;
+      wr[k + 1] = r2.y;
+      wi[k] = i2.x;
+      wi[k + 1] = i2.y;
     }
     if constexpr (RB) wn2 = scale * scale * s2;
     if (l + 1 == p.L && on) {
