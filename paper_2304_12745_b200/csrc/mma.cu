@@ -591,9 +591,15 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
           const float* A10 = reinterpret_cast<const float*>(&a10);
           const float* B10 = reinterpret_cast<const float*>(&b10);
   #pragma unroll
-          for (int u = 0; u < CWD; ++u) {
-            xr[u] = (A00[u] + B00[u]) - (A11[u] + B11[u]);
-            xi[u] = (A01[u] + B01[u]) + (A10[u] + B10[u]);
+          for (int u = 0; u < CWD; u += 2) {  // packed FP32x2
+            const float2 r2 = fadd2(fadd2(make_float2(A00[u], A00[u + 1]), make_float2(B00[u], B00[u + 1])),
+                                    make_float2(-(A11[u] + B11[u]), -(A11[u + 1] + B11[u + 1])));
+            const float2 i2 = fadd2(fadd2(make_float2(A01[u], A01[u + 1]), make_float2(B01[u], B01[u + 1])),
+                                    fadd2(make_float2(A10[u], A10[u + 1]), make_float2(B10[u], B10[u + 1])));
+            xr[u] = r2.x;
+            xr[u + 1] = r2.y;
+            xi[u] = i2.x;
+            xi[u + 1] = i2.y;
           }
         }
   #pragma unroll
@@ -606,7 +612,8 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   #pragma unroll
         for (int v = 0; v < CWD / 2; ++v) {
           split2(xr[2 * v], xr[2 * v + 1], rh[v], rl[v]);
-          split2(-xr[2 * v], -xr[2 * v + 1], nh[v], nl[v]);
+          nh[v] = rh[v] ^ 0x80008000u;  // split of -X'r: f16 negation is exact
+          nl[v] = rl[v] ^ 0x80008000u;
           split2(xi[2 * v], xi[2 * v + 1], ih[v], il[v]);
         }
         // (p_in, p_out) = (0,0): X'r, (1,0): X'i, (0,1): X'i, (1,1): -X'r
@@ -657,9 +664,15 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
           const float* A10 = reinterpret_cast<const float*>(&a10);
           const float* B10 = reinterpret_cast<const float*>(&b10);
   #pragma unroll
-          for (int u = 0; u < CWD; ++u) {
-            xr[u] = (A00[u] + B00[u]) - (A11[u] + B11[u]);
-            xi[u] = (A01[u] + B01[u]) + (A10[u] + B10[u]);
+          for (int u = 0; u < CWD; u += 2) {  // packed FP32x2
+            const float2 r2 = fadd2(fadd2(make_float2(A00[u], A00[u + 1]), make_float2(B00[u], B00[u + 1])),
+                                    make_float2(-(A11[u] + B11[u]), -(A11[u + 1] + B11[u + 1])));
+            const float2 i2 = fadd2(fadd2(make_float2(A01[u], A01[u + 1]), make_float2(B01[u], B01[u + 1])),
+                                    fadd2(make_float2(A10[u], A10[u + 1]), make_float2(B10[u], B10[u + 1])));
+            xr[u] = r2.x;
+            xr[u + 1] = r2.y;
+            xi[u] = i2.x;
+            xi[u + 1] = i2.y;
           }
         }
   #pragma unroll
@@ -694,7 +707,8 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   #pragma unroll
         for (int v = 0; v < CWD / 2; ++v) {
           split2(xr[2 * v], xr[2 * v + 1], rh[v], rl[v]);
-          split2(-xr[2 * v], -xr[2 * v + 1], nh[v], nl[v]);
+          nh[v] = rh[v] ^ 0x80008000u;  // split of -X'r: f16 negation is exact
+          nl[v] = rl[v] ^ 0x80008000u;
           split2(xi[2 * v], xi[2 * v + 1], ih[v], il[v]);
         }
         // (p_in, p_out) = (0,0): X'r, (1,0): X'i, (0,1): X'i, (1,1): -X'r
