@@ -149,18 +149,39 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
+// UNROLL 4: four try_waits per round of the guard counter, each followed only
+// by its exit branch — the spin loop's own instructions take issue slots (at
+// (32,256), one CTA per SM: -2% per launch); UNROLL 1 measured better at
+// (16,128), where 4 CTAs share the SM.
+template <int UNROLL>
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t ok = 0;
-  // 32-bit down-counter: the spin loop's own instructions take issue slots
-  // from the other CTAs of the SM (the 64-bit counter cost ~4% of them)
-  for (uint32_t spin = 1u << 28;; --spin) {
-    asm volatile(
-        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
+  static_assert(UNROLL == 1 || UNROLL == 4, "");
+  for (uint32_t round = UNROLL == 4 ? (1u << 26) : (1u << 28);; --round) {
+    uint32_t ok;
+    if constexpr (UNROLL == 4) {
+      asm volatile(
+          "{\n.reg .pred p;\n"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+          "@p bra.uni MBW_DONE;\n"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+          "@p bra.uni MBW_DONE;\n"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+          "@p bra.uni MBW_DONE;\n"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+          "MBW_DONE:\n"
+          "selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(ok)
+          : "r"(bar), "r"(parity)
+          : "memory");
+    } else {
+      asm volatile(
+          "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(ok)
+          : "r"(bar), "r"(parity)
+          : "memory");
+    }
     if (ok) return;
-    if (spin == 0) __trap();  // never hang the GPU on a lost arrive
+    if (round == 0) __trap();  // never hang the GPU on a lost arrive
   }
 }
 __device__ __forceinline__ void named_bar(int id, int n) {
@@ -503,7 +524,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       constexpr int CW = R * 4 / NW;
       const int quad = warp & 3, c0 = (warp >> 2) * CW, part = quad & 1;
 #pragma unroll
-      for (int t = 0; t < T::NTILE; ++t) mbar_wait(bar1 + 8 * t, ph1);
+      for (int t = 0; t < T::NTILE; ++t) mbar_wait<(T::K >= 32 ? 4 : 1)>(bar1 + 8 * t, ph1);
       ph1 ^= 1;
       TSTAMP(3)
       tc_fence_after();
@@ -750,7 +771,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       }
     }
     TSTAMP(6)
-    mbar_wait(bar2 + 8 * tile, ph2);
+    mbar_wait<(T::K >= 32 ? 4 : 1)>(bar2 + 8 * tile, ph2);
     ph2 ^= 1;
     TSTAMP(7)
     tc_fence_after();
