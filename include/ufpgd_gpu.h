@@ -161,6 +161,22 @@ int ufpgd_gpu_pgd_fixed(const ufpgd_c64* H, int64_t B, int K, int M, const float
                         double alpha, int device, ufpgd_stream_t stream);
 
 /*
+ * solve_pgd over B channels with solve_pgd's early stop — replaces
+ * ufpgd::solve_pgd (pgd.hpp:102-110, pgd.cpp:178-268) with residual_tol > 0
+ * (pgd.cpp:246-260): each realization stops after the first iteration whose
+ * relative iterate change ||W_next - W||_F / max(||W||_F, 1e-12) is below
+ * residual_tol; iterations[B] (device, nullable) receives the count taken
+ * (result.iterations). residual_tol = 0 runs max_iters (= ufpgd_gpu_pgd_fixed).
+ * K <= 8 shapes run the fused FFMA2 kernel with per-realization early exit; the
+ * others the general kernel. Steps as for ufpgd_gpu_pgd_fixed.
+ */
+int ufpgd_gpu_solve_pgd_batch(const ufpgd_c64* H, int64_t B, int K, int M, const float* eta_in, int power_steps,
+                              double lambda, int64_t max_iters, double residual_tol, const double* c, int w0_mode,
+                              const ufpgd_c64* W0, ufpgd_c64* W, int32_t* diverged_at, int64_t* iterations,
+                              float* l21, int32_t* active, float* eta_out, double* stats, double alpha, int device,
+                              ufpgd_stream_t stream);
+
+/*
  * General layer sweep on any (K <= 64, M) shape — the per-realization
  * building blocks of pgd.hpp:41-72 (grad_f, prox_l21, pgd_step) and the taped
  * forward (ForwardOptions::with_tape / with_iterates, unfolded.hpp:40-62).

@@ -69,6 +69,7 @@ def lib():
             "ufpgd_gpu_unfolded_forward": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, P, P, P, d, i, P]),
             "ufpgd_gpu_power_iteration": (i, [P, i64, i, i, P, i, P, i, P]),
             "ufpgd_gpu_pgd_fixed": (i, [P, i64, i, i, P, i, d, i64, P, i, P, P, P, P, P, P, P, d, i, P]),
+            "ufpgd_gpu_solve_pgd_batch": (i, [P, i64, i, i, P, i, d, i64, d, P, i, P, P, P, P, P, P, P, P, d, i, P]),
             "ufpgd_gpu_layers_general": (i, [P, i64, i, i, P, P, i, P, i, P, i, d, i, P, P, P, P, P, P, P, i, P]),
             "ufpgd_gpu_unfolded_forward_host": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, P, d, i]),
             "ufpgd_gpu_unfolded_forward_host_async": (i, [P, i64, i, i, P, P, i, P, i, P, P, P, P, d, i, P]),
@@ -279,9 +280,11 @@ def power_iteration(H, steps: int = 30, v0=None, stream=None):
 
 def pgd_fixed(H, lambda_: float, iters: int, c, *, eta=None, power_steps: int = 30,
               w0_mode: int = W0_CONJ_H, W0=None, alpha: float = 1.0, want_per_realization=False,
-              stream=None):
-    """Batched ufpgd::solve_pgd at a fixed step (pgd.cpp:178-268, trace off,
-    residual_tol 0). ``eta`` (device float32 [B]) or the in-kernel 1/L."""
+              residual_tol: float = 0.0, stream=None):
+    """Batched ufpgd::solve_pgd at a fixed step (pgd.cpp:178-268, trace off):
+    ``iters`` iterations, or fewer per realization with ``residual_tol`` > 0
+    (relative iterate change, pgd.cpp:246-260; ``iterations`` then holds the
+    counts). ``eta`` (device float32 [B]) or the in-kernel 1/L."""
     import torch
 
     B, K, M = _check_batch(H)
@@ -297,12 +300,13 @@ def pgd_fixed(H, lambda_: float, iters: int, c, *, eta=None, power_steps: int = 
     l21 = torch.empty(B, dtype=torch.float32, device=dev) if want_per_realization else None
     act = torch.empty(B, dtype=torch.int32, device=dev) if want_per_realization else None
     stats = torch.empty(3, dtype=torch.float64, device=dev)
-    rc = lib().ufpgd_gpu_pgd_fixed(_ptr(H), B, K, M, _ptr(eta), power_steps, float(lambda_), int(iters),
-                                   _ptr(cc), w0_mode, _ptr(W0), _ptr(W), _ptr(div), _ptr(l21), _ptr(act),
-                                   _ptr(eta_out), _ptr(stats), float(alpha), dev.index or 0,
-                                   _stream_ptr(stream, dev))
+    its = torch.empty(B, dtype=torch.int64, device=dev) if (want_per_realization or residual_tol > 0) else None
+    rc = lib().ufpgd_gpu_solve_pgd_batch(_ptr(H), B, K, M, _ptr(eta), power_steps, float(lambda_), int(iters),
+                                         float(residual_tol), _ptr(cc), w0_mode, _ptr(W0), _ptr(W), _ptr(div),
+                                         _ptr(its), _ptr(l21), _ptr(act), _ptr(eta_out), _ptr(stats), float(alpha),
+                                         dev.index or 0, _stream_ptr(stream, dev))
     _check(rc)
-    return dict(W=W, diverged_at=div, eta=eta_out, l21=l21, active=act, stats=stats)
+    return dict(W=W, diverged_at=div, eta=eta_out, l21=l21, active=act, stats=stats, iterations=its)
 
 
 def layers_general(H, eta, thr, c, *, w0_mode: int = W0_CONJ_H, W0=None, mode: int = 0,

@@ -918,8 +918,11 @@ namespace {
 int enqueue_pgd(const float2* H, int64_t B, int K, int M, const float* eta_in, int power_steps, double lambda,
                 int64_t iters, const double* c, int w0_mode, const float2* W0, float2* W, int32_t* diverged_at,
                 float* l21, int32_t* active, float* eta_out, double* partials, double alpha, int device,
-                cudaStream_t s, long long* nparts) {
-  const bool fused = fused_supported(K, M) && iters >= 1;
+                cudaStream_t s, long long* nparts, double residual_tol = 0.0, int64_t* iterations = nullptr) {
+  // residual_tol > 0 (solve_pgd's early stop): the FFMA2 team kernels (K <= 8)
+  // or the general kernel; the tensor-core and tile kernels run fixed counts
+  const bool resid = residual_tol > 0.0;
+  const bool fused = fused_supported(K, M) && iters >= 1 && (!resid || K <= 8);
   int rc = UFPGD_OK, Kp = 0, Mp = 0;
   long long used = B;
   std::vector<ufpgd_c64> v0(M);
@@ -941,11 +944,17 @@ int enqueue_pgd(const float2* H, int64_t B, int K, int M, const float* eta_in, i
     a.power_steps = power_steps;
     a.lambda = static_cast<float>(lambda);
     a.alpha = static_cast<float>(alpha);
+    a.residual_tol = static_cast<float>(residual_tol);
+    a.iterations = iterations;
     for (int k = 0; k < K; ++k) a.c[k] = static_cast<float>(c[k]);
     std::memcpy(a.v0, v0.data(), sizeof(float2) * M);
     cudaError_t e = launch_fused(a, true, K, M, s, &used);
     if (e != cudaSuccess) rc = cuda_fail(e, "fused PGD kernel");
-  } else if (iters >= 1 && padded_shape(K, M, &Kp, &Mp)) {
+    if (e == cudaSuccess && !resid && iterations) {  // fixed count: every realization ran `iters`
+      e = launch_fill_i64(iterations, B, iters, s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "iterations fill");
+    }
+  } else if (!resid && iters >= 1 && padded_shape(K, M, &Kp, &Mp)) {
     // zero-padded on a fused shape; the power-iteration start vector is padded
     // with zeros too, so the padded antennas stay 0 in every step
     rc = run_padded(H, w0_mode == UFPGD_W0_GIVEN ? W0 : nullptr, W, B, K, M, Kp, Mp, partials, s, &used,
@@ -972,6 +981,10 @@ int enqueue_pgd(const float2* H, int64_t B, int K, int M, const float* eta_in, i
                       cudaError_t e = launch_fused(a, true, Kp, Mp, s, np);
                       return e == cudaSuccess ? UFPGD_OK : cuda_fail(e, "zero-padded fused PGD kernel");
                     });
+    if (rc == UFPGD_OK && iterations) {
+      cudaError_t e = launch_fill_i64(iterations, B, iters, s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "iterations fill");
+    }
   } else {
     if (!general_fits(K, M)) rc = fail(UFPGD_ENOTSUP, "(K, M) too large for the general kernel");
     float* lip = nullptr;
@@ -1001,6 +1014,8 @@ int enqueue_pgd(const float2* H, int64_t B, int K, int M, const float* eta_in, i
       gA.lambda = static_cast<float>(lambda);
       gA.index_base = 1;
       gA.alpha = static_cast<float>(alpha);
+      gA.residual_tol = static_cast<float>(residual_tol);
+      gA.iterations = iterations;
       for (int k = 0; k < K; ++k) gA.c[k] = static_cast<float>(c[k]);
       cudaError_t e = launch_general(gA, s);
       if (e != cudaSuccess) rc = cuda_fail(e, "general PGD kernel");
@@ -1015,15 +1030,16 @@ int enqueue_pgd(const float2* H, int64_t B, int K, int M, const float* eta_in, i
 
 extern "C" {
 
-int ufpgd_gpu_pgd_fixed(const ufpgd_c64* H, int64_t B, int K, int M, const float* eta_in,
-                        int power_steps, double lambda, int64_t iters, const double* c, int w0_mode,
-                        const ufpgd_c64* W0, ufpgd_c64* W, int32_t* diverged_at, float* l21,
-                        int32_t* active, float* eta_out, double* stats, double alpha, int device,
-                        ufpgd_stream_t stream) {
+int ufpgd_gpu_solve_pgd_batch(const ufpgd_c64* H, int64_t B, int K, int M, const float* eta_in, int power_steps,
+                              double lambda, int64_t max_iters, double residual_tol, const double* c, int w0_mode,
+                              const ufpgd_c64* W0, ufpgd_c64* W, int32_t* diverged_at, int64_t* iterations,
+                              float* l21, int32_t* active, float* eta_out, double* stats, double alpha, int device,
+                              ufpgd_stream_t stream) {
   int rc;
   if ((rc = check_shape(B, K, M)) || (rc = check_c(c, K)) || (rc = check_w0(w0_mode, W0))) return rc;
   if (!(lambda >= 0.0) || !std::isfinite(lambda)) return fail(UFPGD_EINVAL_PARAM, "PgdParams: lambda must be >= 0");
-  if (iters < 0) return fail(UFPGD_EINVAL_PARAM, "PgdParams: max_iters must be >= 0");
+  if (max_iters < 0) return fail(UFPGD_EINVAL_PARAM, "PgdParams: max_iters must be >= 0");
+  if (!(residual_tol >= 0.0)) return fail(UFPGD_EINVAL_PARAM, "PgdParams: residual_tol must be >= 0");
   if (!eta_in && power_steps < 1) return fail(UFPGD_EINVAL_PARAM, "need eta_in or power_steps >= 1");
   if (!(alpha > 0.0)) return fail(UFPGD_EINVAL_PARAM, "alpha must be > 0");
   if (B > 0 && (!H || !W)) return fail(UFPGD_EINVAL_PARAM, "H and W are required");
@@ -1034,16 +1050,25 @@ int ufpgd_gpu_pgd_fixed(const ufpgd_c64* H, int64_t B, int K, int M, const float
     if (stats) UFPGD_CUDA(cudaMemsetAsync(stats, 0, 3 * sizeof(double), s));
     return UFPGD_OK;
   }
-  const bool fused = fused_supported(K, M) && iters >= 1;
+  const bool fused = fused_supported(K, M) && max_iters >= 1;
   const long long np = partial_count(B, K, M, fused);
   long long used = B;
   double* partials = nullptr;
   if (stats) UFPGD_CUDA(scratch_alloc_async(reinterpret_cast<void**>(&partials), sizeof(double) * 3 * np, s));
-  rc = enqueue_pgd(reinterpret_cast<const float2*>(H), B, K, M, eta_in, power_steps, lambda, iters, c, w0_mode,
+  rc = enqueue_pgd(reinterpret_cast<const float2*>(H), B, K, M, eta_in, power_steps, lambda, max_iters, c, w0_mode,
                    reinterpret_cast<const float2*>(W0), reinterpret_cast<float2*>(W), diverged_at, l21, active,
-                   eta_out, partials, alpha, device, s, &used);
+                   eta_out, partials, alpha, device, s, &used, residual_tol, iterations);
   int rc2 = finish_stats(partials, rc == UFPGD_OK ? used : 0, stats, s);
   return rc != UFPGD_OK ? rc : rc2;
+}
+
+int ufpgd_gpu_pgd_fixed(const ufpgd_c64* H, int64_t B, int K, int M, const float* eta_in,
+                        int power_steps, double lambda, int64_t iters, const double* c, int w0_mode,
+                        const ufpgd_c64* W0, ufpgd_c64* W, int32_t* diverged_at, float* l21,
+                        int32_t* active, float* eta_out, double* stats, double alpha, int device,
+                        ufpgd_stream_t stream) {
+  return ufpgd_gpu_solve_pgd_batch(H, B, K, M, eta_in, power_steps, lambda, iters, 0.0, c, w0_mode, W0, W,
+                                   diverged_at, nullptr, l21, active, eta_out, stats, alpha, device, stream);
 }
 
 int ufpgd_gpu_layers_general(const ufpgd_c64* H, int64_t B, int K, int M, const double* eta,

@@ -427,6 +427,18 @@ cudaError_t launch_lipschitz_exact(const double2* H, long long B, int K, int M, 
   return cudaGetLastError();
 }
 
+namespace {
+__global__ void fill_i64_kernel(int64_t* p, long long n, int64_t v) {
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) p[i] = v;
+}
+}  // namespace
+
+cudaError_t launch_fill_i64(int64_t* p, long long n, int64_t value, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  fill_i64_kernel<<<static_cast<unsigned>(std::min<long long>((n + 255) / 256, 1024)), 256, 0, s>>>(p, n, value);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stats_finalize(const double* partials, long long n, double* stats, cudaStream_t s) {
   // Up to 64 Ki partials (config 2: 8,192 blocks): one block. Beyond (the
   // tcgen05 kernel writes one triple per realization: 2^20 at config 5), a

@@ -233,11 +233,14 @@ __device__ __forceinline__ void team_stage1(const WS& w, XAcc<S>& x, const float
 // at W (no merge adds) — measured fastest at 3 warps per scheduler, against
 // 2- and 4-chain splits.
 
-template <class S, bool STAGE1, bool STATS, class WS>
+// RESID: also accumulate sum |W_new - W|^2 and sum |W|^2 over the thread's
+// entries (user pairs packed) into dd / ss — solve_pgd's relative iterate
+// change (pgd.cpp:246-260).
+template <class S, bool STAGE1, bool STATS, class WS, bool RESID = false>
 __device__ __forceinline__ void team_layer(WS& w, XAcc<S>& x,
                                            const float* hs, int a, int b, float eta, float thr,
                                            const float2 (&cdiag)[S::P], bool& nonfinite, float& l21,
-                                           int& act) {
+                                           int& act, float2* dd = nullptr, float2* ss = nullptr) {
   constexpr int AB = 2;
   static_assert(S::MB % AB == 0, "antennas are processed in pairs");
   XAcc<S> xn;
@@ -257,6 +260,7 @@ __device__ __forceinline__ void team_layer(WS& w, XAcc<S>& x,
   for (int i0 = 0; i0 < S::MB; i0 += AB) {
     float2 h[AB][S::K];
     float2 vr[AB][S::P], vi[AB][S::P];
+    float2 wor[AB][S::P], woi[AB][S::P];  // RESID: the W entries before the update
     float2 s2p[AB];
 #pragma unroll
     for (int u = 0; u < AB; ++u) {
@@ -268,6 +272,10 @@ __device__ __forceinline__ void team_layer(WS& w, XAcc<S>& x,
       for (int p = 0; p < S::P; ++p) {
         float2 gr, gi;
         w.ld(i, p, gr, gi);
+        if (RESID) {
+          wor[u][p] = gr;
+          woi[u][p] = gi;
+        }
 #pragma unroll
         for (int j = 0; j < S::K; ++j) {
           gr = ffma2(h[u][j].x, x.re[p][j], gr);
@@ -306,6 +314,12 @@ __device__ __forceinline__ void team_layer(WS& w, XAcc<S>& x,
         nwr[p] = fmul2(scale, vr[u][p]);
         nwi[p] = fmul2(scale, vi[u][p]);
         w.st(i, p, nwr[p], nwi[p]);
+        if (RESID) {
+          const float2 dr = __ffma2_rn(make_float2(-1.f, -1.f), wor[u][p], nwr[p]);
+          const float2 di = __ffma2_rn(make_float2(-1.f, -1.f), woi[u][p], nwi[p]);
+          *dd = __ffma2_rn(dr, dr, __ffma2_rn(di, di, *dd));
+          *ss = __ffma2_rn(wor[u][p], wor[u][p], __ffma2_rn(woi[u][p], woi[u][p], *ss));
+        }
       }
       if (STATS) {
         if (a == 0 && on) {
@@ -449,7 +463,11 @@ __device__ __forceinline__ typename std::conditional<S::WSMEM, WSm<S>, WReg<S>>:
   }
 }
 
-template <class S, bool PGD, int MAXT, int MINB>
+// RESID (PGD only): solve_pgd's residual_tol early stop per realization; a
+// realization that met it keeps its W (steps 0 from then on: exactly the
+// identity) while the other team of its warp runs on, and the warp leaves the
+// loop when both have stopped.
+template <class S, bool PGD, int MAXT, int MINB, bool RESID = false>
 __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant__ FusedArgs p) {
   extern __shared__ __align__(16) float smem[];
   __shared__ double red[kFusedMaxWarps][3];
@@ -559,7 +577,41 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
     if (nonfinite) first_bad = 0;
     l0 = 1;
   }
-  for (long long l = l0; l + 1 < L; ++l) {
+  if constexpr (RESID) {
+    static_assert(PGD, "residual_tol is a solve_pgd option");
+    const float tol2 = p.residual_tol * p.residual_tol;
+    bool stopped = false;
+    long long taken = 0;
+    float eta_r = eta_b, thr_r = thr_b;
+    for (long long l = 0; l < L; ++l) {
+      float2 dd = zero2(), ss = zero2();
+      float l21_l = 0.f;
+      int act_l = 0;
+      team_layer<S, false, true, decltype(w), true>(w, x, hs, a, b, eta_r, thr_r, cdiag, nonfinite, l21_l, act_l,
+                                                    &dd, &ss);
+      if (nonfinite && first_bad < 0) first_bad = l;
+      float2 ds = make_float2(dd.x + dd.y, ss.x + ss.y);
+#pragma unroll
+      for (int off = 1; off < S::T; off <<= 1)
+        ds = fadd2(ds, make_float2(__shfl_xor_sync(kFull, ds.x, off), __shfl_xor_sync(kFull, ds.y, off)));
+      if (!stopped) {
+        taken = l + 1;
+        l21 = l21_l;
+        act = act_l;
+        // ||W_new - W|| / max(||W||, 1e-12) < tol, in squares (pgd.cpp:246-260)
+        if (ds.x < tol2 * fmaxf(ds.y, 1e-24f)) {
+          stopped = true;
+          eta_r = 0.f;  // from now on V = W and the prox is the identity: W stays
+          thr_r = 0.f;
+        }
+      }
+      if (__all_sync(kFull, stopped)) break;
+      __syncwarp();
+      team_stage1<S, true>(w, x, hs, a, b, cdiag);
+    }
+    if (valid && tl == 0 && p.iterations) p.iterations[rid] = taken;
+  }
+  for (long long l = l0; !RESID && l + 1 < L; ++l) {
     const float eta = PGD ? eta_b : p.eta[l];
     const float thr = PGD ? thr_b : p.thr[l];
     if constexpr (S::TWO_SWEEP) {
@@ -571,7 +623,7 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
     }
     if (nonfinite && first_bad < 0) first_bad = l;
   }
-  if (L >= 1 && L > l0) {
+  if (!RESID && L >= 1 && L > l0) {
     const float eta = PGD ? eta_b : p.eta[L - 1];
     const float thr = PGD ? thr_b : p.thr[L - 1];
     team_layer<S, false, true>(w, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
@@ -669,7 +721,9 @@ template <class S>
 cudaError_t launch_team(const FusedArgs& a, bool pgd, cudaStream_t s, long long* nblocks) {
   // The unfolded kernel takes the Team's launch bounds; the PGD kernel (power
   // iteration prologue, more live state) keeps 256 x 1 (no register cap).
-  auto kern = pgd ? fused_kernel<S, true, UFPGD_PGD_MAXT, UFPGD_PGD_MINB> : fused_kernel<S, false, S::MAXT, S::MINB>;
+  auto kern = pgd ? (a.residual_tol > 0.f ? fused_kernel<S, true, UFPGD_PGD_MAXT, UFPGD_PGD_MINB, true>
+                                          : fused_kernel<S, true, UFPGD_PGD_MAXT, UFPGD_PGD_MINB>)
+                  : fused_kernel<S, false, S::MAXT, S::MINB>;
   const int maxt = pgd ? UFPGD_PGD_MAXT : S::MAXT;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kFusedMaxWarps * (S::SMEM_PER_WARP + S::WSMEM_PER_WARP));

@@ -27,6 +27,8 @@ struct FusedArgs {
   int power_steps;        // PGD with eta_in == nullptr
   float lambda;           // PGD threshold factor (thr = lambda * eta)
   float alpha;            // PA constant for the consumed-power statistic
+  float residual_tol;     // PGD: relative iterate-change stop (0 = run all iterations; team kernels)
+  int64_t* iterations;    // PGD with residual_tol: iterations taken per realization (nullable)
   float cmax;             // tensor-core kernel: max |c_k| and the range of the
   float eta_lo, eta_hi;   //   per-layer steps (filled by launch_mma)
   float c[UFPGD_MAX_USERS];
@@ -160,6 +162,7 @@ cudaError_t launch_convert(const void* src, void* dst, long long B, int K, int M
 cudaError_t launch_repack_c64(const float2* src, int Ms, int Ks, float2* dst, int Md, int Kd, long long B,
                               cudaStream_t s);
 cudaError_t measure_fp32_peak(double* tflops, double* sm_ghz);
+cudaError_t launch_fill_i64(int64_t* p, long long n, int64_t value, cudaStream_t s);
 cudaError_t launch_stats_finalize(const double* partials, long long n, double* stats,
                                   cudaStream_t s);
 

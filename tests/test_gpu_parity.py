@@ -236,3 +236,31 @@ def test_general_kernel_helpers_match_oracle():
     ref = O.prox_l21(w.astype(np.complex64).astype(complex), 1.5)
     assert np.linalg.norm(prox - ref) <= 1e-6 * np.linalg.norm(ref)
     assert np.array_equal(np.all(prox == 0, axis=0), np.all(ref == 0, axis=0))
+
+
+@pytest.mark.parametrize("K,M", [(8, 64), (4, 32), (16, 128)])
+def test_pgd_residual_tol_early_stop_matches_oracle(K, M):
+    """solve_pgd with residual_tol > 0 (pgd.cpp:246-260): every realization stops
+    after the first iteration whose relative iterate change is below the
+    tolerance. (8,64) / (4,32) run the fused team kernel with per-realization
+    early exit, (16,128) the general kernel. Iteration counts within a few of
+    the FP64 oracle's (the change is compared in FP32), W within the bar."""
+    B, iters, lam, tol = 96, 6000, 0.05, 1e-4
+    H = U.generate_channels(321, 0, 10.0, 0, B, K, M)
+    c = np.full(K, math.sqrt(10.0))
+    out = U.pgd_fixed(dev(H), lam, iters, c, power_steps=30, residual_tol=tol, want_per_realization=True)
+    torch.cuda.synchronize()
+    its = out["iterations"].cpu().numpy()
+    eta = out["eta"].cpu().numpy().astype(np.float64)
+    ora = O.pgd_batch_f32(H, c, lam, eta, iters, residual_tol=tol, w0_mode=U.W0_CONJ_H)
+    d = np.abs(its - ora["iterations"])
+    print(f"({K},{M}) residual_tol {tol:g}: iterations {its.min()}..{its.max()} (oracle {ora['iterations'].min()}.."
+          f"{ora['iterations'].max()}), max |diff| {d.max()}")
+    assert np.all(its < iters) and np.all(its >= 1)
+    assert np.median(d) <= 2 and d.max() <= max(10, 0.02 * ora["iterations"].max())
+    rep = report(H, out["W"].cpu().numpy(), ora, c, lam)
+    assert rep["rel_max"] <= 1e-3  # a stop a few iterations apart at this tolerance
+    assert np.all(out["diverged_at"].cpu().numpy() == -1)
+    # residual_tol = 0 reports the fixed count
+    fixed = U.pgd_fixed(dev(H[:8]), lam, 50, c, power_steps=30, want_per_realization=True)
+    assert np.all(fixed["iterations"].cpu().numpy() == 50)
