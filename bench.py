@@ -356,8 +356,11 @@ def make_step(U, torch, sharding, w, Hd, Wd, lam, eta, world, use_graph):
 
     if not use_graph:
         return eager, None, "eager"
+    import torch.distributed as dist
+
     ref = eager()["stats"].clone()
     torch.cuda.synchronize()
+    g, gout, err = None, None, None
     try:
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
@@ -366,20 +369,28 @@ def make_step(U, torch, sharding, w, Hd, Wd, lam, eta, world, use_graph):
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
+        with torch.cuda.graph(g):  # records (does not run) the forward and the all-reduce
             gout = eager()
-        g.replay()
+    except Exception as e:
+        g, err = None, f"{type(e).__name__}: {e}"
         torch.cuda.synchronize()
-        if not torch.equal(gout["stats"], ref):
-            raise RuntimeError("graph replay statistics differ from the eager step")
+    # every rank must take the same path before any replay runs a collective
+    if world > 1:
+        ok = torch.tensor([1 if g is not None else 0], dtype=torch.int32, device=Hd.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0 and g is not None:
+            g, err = None, "another rank's graph capture failed"
+    if g is None:
+        return eager, None, f"eager (graph capture failed: {err})"
+    g.replay()  # one step: one all-reduce on every rank, whichever way it is checked below
+    torch.cuda.synchronize()
+    if not torch.equal(gout["stats"], ref):
+        return eager, None, "eager (graph replay statistics differ from the eager step)"
 
-        def replay(ev=None):
-            g.replay()
-            return gout
-        return replay, g, "cuda_graph"
-    except Exception as e:  # keep benchmarking on the eager step, say why
-        torch.cuda.synchronize()
-        return eager, None, f"eager (graph capture failed: {type(e).__name__}: {e})"
+    def replay(ev=None):
+        g.replay()
+        return gout
+    return replay, g, "cuda_graph"
 
 
 def run_ours(args, world, rank, local):
