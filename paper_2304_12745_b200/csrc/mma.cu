@@ -187,6 +187,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 // 16 consecutive TMEM columns of this warp's 32 lanes -> 16 registers per thread.
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   asm volatile(
@@ -754,21 +757,30 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     tc_fence_before();
     __syncthreads();
     TSTAMP(5)
-    if (tid == 0) {
+    // Each antenna tile's stage-2 MMAs are issued by the tile group's first
+    // thread, tile 1 after tile 0's are queued (warp 0 -> warp 4 named barrier):
+    // an MMA issue holds the issuing warp ~60 clocks, so one thread issuing both
+    // tiles kept warp 0 — and with it tile 0's epilogue — out of the drain until
+    // tile 1's MMAs were nearly done.
+    static_assert(T::NTILE <= 2, "");
+    if (T::NTILE > 1 && warp == 4) named_bar(3, 64);
+    if ((tid & 127) == 0) {
       tc_fence_after();
-#pragma unroll 1
-      for (int t = 0; t < T::NTILE; ++t) {
-        const uint32_t dm = tmem + T::T_D2 + t * 2 * R, dc = dm + R;
+      const int t = tile;
+      const uint32_t dm = tmem + T::T_D2 + t * 2 * R, dc = dm + R;
 #pragma unroll
-        for (int ks = 0; ks < R / 16; ++ks) {
-          const uint64_t ah = sdesc(sb + T::OFF_HH + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
-          const uint64_t al = sdesc(sb + T::OFF_HL + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
-          const uint64_t bh = sdesc(sb + T::OFF_BH + ks * 256, 128, T::BSBO);  // N = 2R spans [Bs_hi | Bs_lo]
-          umma_f16(dm, ah, bh, IDESC2W, ks > 0);  // [main | corr] = H_hi [Bs_hi | Bs_lo]
-          umma_f16(dc, al, bh, IDESC2, 1);        // corr += H_lo Bs_hi
-        }
-        umma_commit(bar2 + 8 * t);  // each tile's epilogue starts as soon as its MMAs retire
+      for (int ks = 0; ks < R / 16; ++ks) {
+        const uint64_t ah = sdesc(sb + T::OFF_HH + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
+        const uint64_t al = sdesc(sb + T::OFF_HL + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
+        const uint64_t bh = sdesc(sb + T::OFF_BH + ks * 256, 128, T::BSBO);  // N = 2R spans [Bs_hi | Bs_lo]
+        umma_f16(dm, ah, bh, IDESC2W, ks > 0);  // [main | corr] = H_hi [Bs_hi | Bs_lo]
+        umma_f16(dc, al, bh, IDESC2, 1);        // corr += H_lo Bs_hi
       }
+      umma_commit(bar2 + 8 * t);  // each tile's epilogue starts as soon as its MMAs retire
+    }
+    if (T::NTILE > 1 && warp == 0) {
+      __syncwarp();
+      named_bar_arrive(3, 64);
     }
     TSTAMP(6)
     mbar_wait<(T::K >= 32 ? 4 : 1)>(bar2 + 8 * tile, ph2);
