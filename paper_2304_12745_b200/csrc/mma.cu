@@ -133,15 +133,23 @@ template <int MM, int NN>
 __device__ __forceinline__ constexpr uint32_t idesc_f16_amn() {
   return (1u << 4) | (1u << 15) | (static_cast<uint32_t>(NN >> 3) << 17) | (static_cast<uint32_t>(MM >> 4) << 24);
 }
+// MMA issue and commit, executed by a whole warp with warp-uniform operands;
+// one lane (elect.sync) issues. Issued from a single thread inside a
+// thread-divergent branch, ptxas moved every descriptor through R2UR and an
+// ELECT loop: ~48 clocks per MMA, against back-to-back UTCHMMAs from uniform
+// registers here (tools/probe/stage_probe.cu: 4 MMAs issued in 40 clocks instead
+// of 284, and an 8-MMA chain done at 618 instead of 680 clocks).
 __device__ __forceinline__ void umma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-               : "memory");
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(bar)
+      : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -313,6 +321,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int K = T::K, M = T::M, R = T::R, Q = T::Q, NW = T::NW;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wu = __shfl_sync(kFull, warp, 0);  // warp index the compiler knows is warp-uniform
   const int n_real = RB ? *redo_count : 1;
   for (int it = RB ? static_cast<int>(blockIdx.x) : 0; it < n_real; it += RB ? static_cast<int>(gridDim.x) : 1) {
   const long long rid = RB ? static_cast<long long>(redo_list[it]) : static_cast<long long>(blockIdx.x);
@@ -508,17 +517,18 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       if (T::NTILE > 1) named_bar(1 + tile, T::NT / T::NTILE);
       else __syncthreads();
       TSTAMP(1)
-      if (tid == tile * 128) {  // the tile group's first thread
+      if (wu == tile * 4) {  // the tile group's first warp
+        const int tu = wu >> 2;  // = tile, warp-uniform: the descriptors stay in uniform registers
         tc_fence_after();
         constexpr int KST = 128 / 16;  // K-steps per antenna tile
-#pragma unroll 1
-        for (int ks = tile * KST; ks < (tile + 1) * KST; ++ks) {
+        const uint32_t sw = sb + T::OFF_W + tu * KST * 2 * 16 * Q, sh = sb + T::OFF_HH + tu * KST * 256;
+#pragma unroll
+        for (int i = 0; i < KST; ++i) {
           // B = [H_hi | H_lo] (N = 2R: OFF_HL continues OFF_HH's N-group stride)
-          const uint64_t a = sdesc(sb + T::OFF_W + ks * 2 * 16 * Q, 16 * Q, 128);
-          umma_f16(tmem + tile * 2 * R + T::T_D1A, a, sdesc(sb + T::OFF_HH + ks * 256, 128, 16 * M), IDESC1,
-                   ks > tile * KST);
+          umma_f16(tmem + tu * 2 * R + T::T_D1A, sdesc(sw + i * 2 * 16 * Q, 16 * Q, 128),
+                   sdesc(sh + i * 256, 128, 16 * M), IDESC1, i > 0);
         }
-        umma_commit(bar1 + 8 * tile);
+        umma_commit(bar1 + 8 * tu);
       }
       TSTAMP(2)
       // D1 rows q = (hilo, part, k): TMEM lane quadrant hilo * 2 + part, lane k
@@ -758,15 +768,15 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     __syncthreads();
     TSTAMP(5)
     // Each antenna tile's stage-2 MMAs are issued by the tile group's first
-    // thread, tile 1 after tile 0's are queued (warp 0 -> warp 4 named barrier):
-    // an MMA issue holds the issuing warp ~60 clocks, so one thread issuing both
-    // tiles kept warp 0 — and with it tile 0's epilogue — out of the drain until
-    // tile 1's MMAs were nearly done.
+    // warp, tile 1 after tile 0's are queued (warp 0 -> warp 4 named barrier):
+    // issuing blocks while the MMA queue is full, so one warp issuing both tiles
+    // kept warp 0 — and with it tile 0's epilogue — out of the drain until tile
+    // 1's MMAs were nearly done.
     static_assert(T::NTILE <= 2, "");
     if (T::NTILE > 1 && warp == 4) named_bar(3, 64);
-    if ((tid & 127) == 0) {
+    if ((wu & 3) == 0) {  // the tile group's first warp
       tc_fence_after();
-      const int t = tile;
+      const int t = wu >> 2;  // = tile, warp-uniform
       const uint32_t dm = tmem + T::T_D2 + t * 2 * R, dc = dm + R;
 #pragma unroll
       for (int ks = 0; ks < R / 16; ++ks) {

@@ -34,6 +34,16 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(id), "r"(acc));
 }
+// warp-wide issue: every lane executes, one elected lane issues (descriptors warp-uniform)
+__device__ __forceinline__ void mma_w(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void commit_w(uint32_t bar) {
+  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -70,7 +80,33 @@ __global__ void __launch_bounds__(128, 1) probe(int reps, unsigned long long* ou
   const uint32_t tmem = slot, sb = su32(sm), b0 = su32(&bar[0]), b1 = su32(&bar[1]);
   unsigned long long a0 = 0, a1 = 0, a2 = 0;
   uint32_t ph = 0;
-  if (tid == 0) {
+  const int wu = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  if (SEQ >= 200 && wu == 0) {
+    for (int r = 0; r < reps; ++r) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const unsigned long long t0 = clock64();
+      constexpr int n = (SEQ - 200) / 10;
+      for (int i = 0; i < n; ++i)
+        mma_w(tmem, sdesc(sb + OFF_W + i * 2 * 16 * Q, 16 * Q, 128), sdesc(sb + OFF_HH + i * 256, 128, 16 * M), idesc<Q, 2 * R>(), i > 0);
+      commit_w(b0);
+      commit_w(b1);
+      const unsigned long long ti = clock64();
+      wait(b0, ph);
+      const unsigned long long tw0 = clock64();
+      wait(b1, ph);
+      const unsigned long long tw1 = clock64();
+      ph ^= 1;
+      a0 += ti - t0;
+      a1 += tw0 - t0;
+      a2 += tw1 - t0;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+      out[0] = a0;
+      out[1] = a1;
+      out[2] = a2;
+    }
+  }
+  if (SEQ < 200 && tid == 0) {
     for (int r = 0; r < reps; ++r) {
       asm volatile("tcgen05.fence::after_thread_sync;");
       const unsigned long long t0 = clock64();
@@ -81,6 +117,17 @@ __global__ void __launch_bounds__(128, 1) probe(int reps, unsigned long long* ou
                 idesc<Q, 2 * R>(), ks > t * 8);
           commit(t ? b1 : b0);
         }
+      } else if (SEQ >= 100) {  // SEQ 100 + 10 n + big: n MMAs, tiny (M=64, N=8) or M=128 N=128
+        constexpr int n = (SEQ - 100) / 10;
+        constexpr bool big = (SEQ % 10) != 0;
+        for (int i = 0; i < n; ++i) {
+          if (big)
+            mma(tmem, sdesc(sb + OFF_W + i * 2 * 16 * Q, 16 * Q, 128), sdesc(sb + OFF_HH + i * 256, 128, 16 * M), idesc<Q, 2 * R>(), i > 0);
+          else
+            mma(tmem, sdesc(sb + OFF_W + i * 2 * 16 * Q, 16 * Q, 128), sdesc(sb + OFF_HH + i * 256, 128, 16 * M), idesc<64, 8>(), i > 0);
+        }
+        commit(b0);
+        commit(b1);
       } else if (SEQ == 4) {
         mma(tmem, sdesc(sb + OFF_W, 16 * Q, 128), sdesc(sb + OFF_HH, 128, 16 * M), idesc<Q, 2 * R>(), 0);
         commit(b0);
@@ -146,6 +193,18 @@ void run(const char* name) {
 
 int main() {
   run<4>("lat");
+  run<110>("1 tiny");
+  run<120>("2 tiny");
+  run<140>("4 tiny");
+  run<180>("8 tiny");
+  run<111>("1 big");
+  run<121>("2 big");
+  run<141>("4 big");
+  run<181>("8 big");
+  run<210>("w 1 big");
+  run<220>("w 2 big");
+  run<240>("w 4 big");
+  run<280>("w 8 big");
   run<0>("s1");
   run<1>("s2-int");
   run<2>("s2-grp");
