@@ -81,7 +81,33 @@ __global__ void __launch_bounds__(128, 1) probe(int reps, unsigned long long* ou
   unsigned long long a0 = 0, a1 = 0, a2 = 0;
   uint32_t ph = 0;
   const int wu = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  if (SEQ >= 200 && wu == 0) {
+  if (SEQ >= 300 && wu == 0) {
+    for (int r = 0; r < reps; ++r) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const unsigned long long t0 = clock64();
+      constexpr int n = 2 * ((SEQ - 300) / 10), v = SEQ % 10;
+      constexpr uint32_t ID = v == 0 ? idesc<64, 64>() : v == 1 ? idesc<128, 64>() : v == 2 ? idesc<64, 32>() : v == 3 ? idesc<128, 32>() : idesc<64, 128>();
+      for (int i = 0; i < n; ++i)
+        mma_w(tmem, sdesc(sb + OFF_W + i * 2 * 16 * Q, 16 * Q, 128), sdesc(sb + OFF_HH + i * 256, 128, 16 * M), ID, i > 0);
+      commit_w(b0);
+      commit_w(b1);
+      const unsigned long long ti = clock64();
+      wait(b0, ph);
+      const unsigned long long tw0 = clock64();
+      wait(b1, ph);
+      const unsigned long long tw1 = clock64();
+      ph ^= 1;
+      a0 += ti - t0;
+      a1 += tw0 - t0;
+      a2 += tw1 - t0;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+      out[0] = a0;
+      out[1] = a1;
+      out[2] = a2;
+    }
+  }
+  if (SEQ >= 200 && SEQ < 300 && wu == 0) {
     for (int r = 0; r < reps; ++r) {
       asm volatile("tcgen05.fence::after_thread_sync;");
       const unsigned long long t0 = clock64();
@@ -205,6 +231,11 @@ int main() {
   run<220>("w 2 big");
   run<240>("w 4 big");
   run<280>("w 8 big");
+  run<380>("16 M64N64");
+  run<381>("16 M128N64");
+  run<382>("16 M64N32");
+  run<383>("16 M128N32");
+  run<384>("16 M64N128");
   run<0>("s1");
   run<1>("s2-int");
   run<2>("s2-grp");
