@@ -123,28 +123,49 @@ struct MmaShape {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-// tcgen05 shared-memory matrix descriptor, SWIZZLE_NONE, version 1 (sm_100).
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
-         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
-}
 // Instruction descriptor, kind::f16: f16 A/B, f32 D, A MN-major, B K-major.
 template <int MM, int NN>
 __device__ __forceinline__ constexpr uint32_t idesc_f16_amn() {
   return (1u << 4) | (1u << 15) | (static_cast<uint32_t>(NN >> 3) << 17) | (static_cast<uint32_t>(MM >> 4) << 24);
 }
-// MMA issue and commit, executed by a whole warp with warp-uniform operands;
-// one lane (elect.sync) issues. Issued from a single thread inside a
-// thread-divergent branch, ptxas moved every descriptor through R2UR and an
-// ELECT loop: ~48 clocks per MMA, against back-to-back UTCHMMAs from uniform
-// registers here (tools/probe/stage_probe.cu: 4 MMAs issued in 40 clocks instead
-// of 284, and an 8-MMA chain done at 618 instead of 680 clocks).
+// MMA issue, executed by a whole warp with warp-uniform operands; one lane
+// (elect.sync) issues. Issued from a single thread inside a thread-divergent
+// branch, ptxas moved every descriptor through R2UR and an ELECT loop: ~48
+// clocks per MMA, against back-to-back UTCHMMAs from uniform registers here
+// (tools/probe/stage_probe.cu: 4 MMAs issued in 40 clocks instead of 284, and an
+// 8-MMA chain done at 618 instead of 680 clocks).
 __device__ __forceinline__ void umma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// tcgen05 shared-memory matrix descriptor, SWIZZLE_NONE, version 1 (sm_100).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+// umma_f16w: the descriptors passed as their two 32-bit words (used at
+// (16,128); at (32,256) ptxas already keeps umma_f16's 64-bit descriptors in
+// uniform registers across the layer loop, and the split form measured 1%
+// slower there — it routed them through R2UR): the low word (start address
+// >> 4 | LBO >> 4 << 16) is a per-layer base plus a compile-time K-step offset (the 14-bit address field
+// never carries into LBO: shared addresses are < 256 KB), the high word (SBO >> 4,
+// version bit 46) a constant — one uniform add per descriptor instead of the
+// shifts and masks recomputed for each MMA (~70 uniform instructions between the
+// barrier and the first stage-1 MMA at (16,128), on the per-layer critical path).
+__device__ __forceinline__ void umma_f16w(uint32_t d, uint32_t alo, uint32_t ahi, uint32_t blo, uint32_t bhi,
+                                          uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\n.reg .b64 da, db;\nmov.b64 da, {%1, %2};\nmov.b64 db, {%3, %4};\n"
+      "elect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %6, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n}\n" ::"r"(d),
+      "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ uint32_t sdesc_lo(uint32_t saddr, uint32_t lbo) {
+  return ((saddr >> 4) & 0x3FFFu) | (((lbo >> 4) & 0x3FFFu) << 16);
+}
+__host__ __device__ constexpr uint32_t sdesc_hi(uint32_t sbo) { return ((sbo >> 4) & 0x3FFFu) | (1u << 14); }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile(
       "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
@@ -522,11 +543,16 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         tc_fence_after();
         constexpr int KST = 128 / 16;  // K-steps per antenna tile
         const uint32_t sw = sb + T::OFF_W + tu * KST * 2 * 16 * Q, sh = sb + T::OFF_HH + tu * KST * 256;
+        const uint32_t alo = sdesc_lo(sw, 16 * Q), blo = sdesc_lo(sh, 128);
 #pragma unroll
         for (int i = 0; i < KST; ++i) {
           // B = [H_hi | H_lo] (N = 2R: OFF_HL continues OFF_HH's N-group stride)
-          umma_f16(tmem + tu * 2 * R + T::T_D1A, sdesc(sw + i * 2 * 16 * Q, 16 * Q, 128),
-                   sdesc(sh + i * 256, 128, 16 * M), IDESC1, i > 0);
+          if constexpr (T::NTILE == 1)
+            umma_f16w(tmem + tu * 2 * R + T::T_D1A, alo + i * (2 * 16 * Q >> 4), sdesc_hi(128), blo + i * (256 >> 4),
+                      sdesc_hi(16 * M), IDESC1, i > 0);
+          else
+            umma_f16(tmem + tu * 2 * R + T::T_D1A, sdesc(sw + i * 2 * 16 * Q, 16 * Q, 128),
+                     sdesc(sh + i * 256, 128, 16 * M), IDESC1, i > 0);
         }
         umma_commit(bar1 + 8 * tu);
       }
@@ -778,13 +804,23 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       tc_fence_after();
       const int t = wu >> 2;  // = tile, warp-uniform
       const uint32_t dm = tmem + T::T_D2 + t * 2 * R, dc = dm + R;
+      const uint32_t ahlo = sdesc_lo(sb + T::OFF_HH + t * 16 * 128, 16 * M);
+      const uint32_t bhlo = sdesc_lo(sb + T::OFF_BH, 128);
+      constexpr uint32_t HLO = (T::OFF_HL - T::OFF_HH) >> 4;
 #pragma unroll
       for (int ks = 0; ks < R / 16; ++ks) {
-        const uint64_t ah = sdesc(sb + T::OFF_HH + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
-        const uint64_t al = sdesc(sb + T::OFF_HL + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
-        const uint64_t bh = sdesc(sb + T::OFF_BH + ks * 256, 128, T::BSBO);  // N = 2R spans [Bs_hi | Bs_lo]
-        umma_f16(dm, ah, bh, IDESC2W, ks > 0);  // [main | corr] = H_hi [Bs_hi | Bs_lo]
-        umma_f16(dc, al, bh, IDESC2, 1);        // corr += H_lo Bs_hi
+        // [main | corr] = H_hi [Bs_hi | Bs_lo] (N = 2R spans both), then corr += H_lo Bs_hi
+        if constexpr (T::NTILE == 1) {
+          const uint32_t ah = ahlo + ks * (2 * 16 * M >> 4), bh = bhlo + ks * (256 >> 4);
+          umma_f16w(dm, ah, sdesc_hi(128), bh, sdesc_hi(T::BSBO), IDESC2W, ks > 0);
+          umma_f16w(dc, ah + HLO, sdesc_hi(128), bh, sdesc_hi(T::BSBO), IDESC2, 1);
+        } else {
+          const uint64_t ah = sdesc(sb + T::OFF_HH + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
+          const uint64_t al = sdesc(sb + T::OFF_HL + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
+          const uint64_t bh = sdesc(sb + T::OFF_BH + ks * 256, 128, T::BSBO);
+          umma_f16(dm, ah, bh, IDESC2W, ks > 0);
+          umma_f16(dc, al, bh, IDESC2, 1);
+        }
       }
       umma_commit(bar2 + 8 * t);  // each tile's epilogue starts as soon as its MMAs retire
     }
