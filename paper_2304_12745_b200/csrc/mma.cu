@@ -58,14 +58,12 @@ struct MmaShape {
   static constexpr int OFF_HL = OFF_HH + R * M * 2;      // H lo
   static constexpr int OFF_W = OFF_HL + R * M * 2;       // [W_hi; W_lo] [Q x M] f16, woff()
   // Bs builder chunk width: 4 values of an X' row per thread, or 2 when K^2/4
-  // chunks would leave threads idle (then a half-warp spans 16 rows, so the
-  // exchange rows are 2 words apart and Bs N-groups are padded by 64 bytes:
-  // both the 8-byte row reads and the 4-byte Bs stores are conflict-free).
+  // chunks would leave threads idle (chunk() maps either conflict-free).
   static constexpr int CWD = (K * K / 4 >= NT) ? 4 : 2;
-  static constexpr int BSBO = 16 * R + (CWD == 2 ? 64 : 0);  // Bs N-group stride (descriptor SBO)
+  static constexpr int BSBO = 16 * R;                    // Bs N-group stride (descriptor SBO)
   static constexpr int OFF_BH = OFF_W + Q * M * 2;       // Bs hi [R x R] f16, boff()
   static constexpr int OFF_BL = OFF_BH + (R / 8) * BSBO; // Bs lo (continues Bs hi along N)
-  static constexpr int FSTR = R + (CWD == 4 ? 4 : 2);    // fp32 exchange rows (floats), conflict-free
+  static constexpr int FSTR = R + 4;  // fp32 exchange rows (floats): 4 mod 32 words, see chunk()
   // F [R][FSTR] (hi rows of P) and G (lo rows) alias the W operand: they are
   // written after the stage-1 MMAs retire and read before W is rewritten.
   static constexpr int OFF_F = OFF_W;
@@ -80,7 +78,12 @@ struct MmaShape {
   // tile t's threads drain D2 part t (E2) before issuing D1 part t, and D1 is
   // drained (E1) behind a CTA barrier before the stage-2 MMAs.
   static constexpr uint32_t T_D1A = 0, T_D1B = R, T_D2 = 0;
-  static constexpr uint32_t T_USED = 2 * NTILE * R;
+  // Stage 2's A operand (H hi / lo, K-major f16 pairs: R / 2 columns each per
+  // tile) lives in TMEM from the prologue on, so the stage-2 MMAs read only
+  // Bs from shared memory: shared-memory bandwidth (LSU traffic plus the MMAs'
+  // operand reads) is what the (16,128) kernel runs out of first.
+  static constexpr uint32_t T_HA = 2 * NTILE * R;
+  static constexpr uint32_t T_USED = T_HA + NTILE * R;
   static constexpr uint32_t T_COLS = T_USED <= 32 ? 32 : T_USED <= 64 ? 64 : T_USED <= 128 ? 128 : T_USED <= 256 ? 256 : 512;
   static_assert(T_USED <= 512, "");
 
@@ -102,15 +105,22 @@ struct MmaShape {
   // fills one whole 128-byte core matrix (conflict-free 8-byte stores), and each
   // quarter-warp reads 8 rows of one column chunk of the F / G exchange rows
   // (row stride FSTR = 4 mod 32 words: conflict-free 16-byte loads).
-  // CWD 2: consecutive threads walk down the rows (see CWD above).
+  // CWD 2: each warp covers one 8 x 8 block of X' — rows k0 .. k0+7 (lanes
+  // i & 7) x four 2-wide column chunks (i >> 3) — so every 4-byte Bs put of the
+  // warp fills one whole core matrix, and each half-warp's 8-byte F / G loads
+  // cover 8 rows x 4 consecutive words (FSTR = 4 mod 32): both conflict-free
+  // (the earlier row-major walk had 2-way conflicting Bs stores — ~64 excess
+  // wavefronts per realization-layer at (16,128)).
+  // The stage-1 drain stores 16-byte row pieces, conflict-free at this FSTR.
   static __device__ __forceinline__ void chunk(int ch, int& k, int& c) {
     if constexpr (CWD == 4) {
       const int hw = ch >> 4, i = ch & 15;
       k = (hw / (K / 8)) * 8 + (i & 7);
       c = (hw % (K / 8)) * 8 + (i >> 3) * 4;
     } else {
-      k = ch % K;
-      c = (ch / K) * CWD;
+      const int w = ch >> 5, i = ch & 31;
+      k = (w / (K / 8)) * 8 + (i & 7);
+      c = (w % (K / 8)) * 8 + (i >> 3) * 2;
     }
   }
   // Bs: element (kk, n), K-major (K = kk, N = n): LBO (K-group) 128, SBO (N-group) BSBO.
@@ -127,6 +137,11 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 template <int MM, int NN>
 __device__ __forceinline__ constexpr uint32_t idesc_f16_amn() {
   return (1u << 4) | (1u << 15) | (static_cast<uint32_t>(NN >> 3) << 17) | (static_cast<uint32_t>(MM >> 4) << 24);
+}
+// The same with A K-major (A from TMEM).
+template <int MM, int NN>
+__device__ __forceinline__ constexpr uint32_t idesc_f16_ak() {
+  return (1u << 4) | (static_cast<uint32_t>(NN >> 3) << 17) | (static_cast<uint32_t>(MM >> 4) << 24);
 }
 // MMA issue, executed by a whole warp with warp-uniform operands; one lane
 // (elect.sync) issues. Issued from a single thread inside a thread-divergent
@@ -161,6 +176,21 @@ __device__ __forceinline__ void umma_f16w(uint32_t d, uint32_t alo, uint32_t ahi
       "elect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %6, 0;\n"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n}\n" ::"r"(d),
       "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(acc));
+}
+// A from TMEM (K-major, [a_tmem]), B from a shared-memory descriptor.
+__device__ __forceinline__ void umma_f16_ta(uint32_t d, uint32_t a, uint32_t blo, uint32_t bhi, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\n.reg .b64 db;\nmov.b64 db, {%2, %3};\n"
+      "elect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %5, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], db, %4, p;\n}\n" ::"r"(d),
+      "r"(a), "r"(blo), "r"(bhi), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_f16_ta(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ uint32_t sdesc_lo(uint32_t saddr, uint32_t lbo) {
   return ((saddr >> 4) & 0x3FFFu) | (((lbo >> 4) & 0x3FFFu) << 16);
@@ -226,6 +256,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
       : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
         "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
       : "r"(taddr));
+}
+// 16 registers per thread -> 16 consecutive TMEM columns of this warp's 32 lanes.
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
 }
 // Waits for this thread's tcgen05.ld results; the laundering asm keeps every
 // use of v after the wait.
@@ -420,6 +458,27 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     }
   }
   fence_async_smem();  // H is read by the tensor cores (async proxy)
+  // Stage 2's A operand in TMEM: antenna m's row (K-major, r = part K + k) in
+  // TMEM lane m % 128 of its tile's H columns — the same f16 values (same
+  // rounding) as the shared copy stage 1 reads. Ordered before the first
+  // stage-2 MMA by tcgen05.wait::st and the fenced CTA barriers of layer 0.
+  {
+    const uint32_t th = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + T::T_HA + (m >> 7) * R;
+#pragma unroll
+    for (int half = 0; half < R / 32; ++half) {  // 16 columns = 32 rows r per store
+      uint32_t hh[16], hl[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const int r = half * 32 + 2 * c;  // rows r, r + 1: one part, users k, k + 1 (K even)
+        const int part = r / K, k = r % K;
+        const float4 hq = hv[k / 2];
+        split2((part == 0 ? hq.x : hq.y) * g, (part == 0 ? hq.z : hq.w) * g, hh[c], hl[c]);
+      }
+      tmem_st16(th + half * 16, hh);
+      tmem_st16(th + R / 2 + half * 16, hl);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
 
   // ---- W0 (scaled: W_s = W / g) in registers: wr[k], wi[k] for antenna m ------
   float wr[K], wi[K];
@@ -453,8 +512,8 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   }
 
   constexpr uint32_t IDESC1 = idesc_f16_amn<Q, 2 * R>();
-  constexpr uint32_t IDESC2W = idesc_f16_amn<128, 2 * R>();
-  constexpr uint32_t IDESC2 = idesc_f16_amn<128, R>();
+  constexpr uint32_t IDESC2W = idesc_f16_ak<128, 2 * R>();  // A = H from TMEM (K-major)
+  constexpr uint32_t IDESC2 = idesc_f16_ak<128, R>();
   static_assert(T::OFF_HL == T::OFF_HH + (R / 8) * 16 * M && T::OFF_BL == T::OFF_BH + (R / 8) * T::BSBO,
                 "lo operands continue the hi ones along N");
   float* F = reinterpret_cast<float*>(smem + T::OFF_F);
@@ -605,14 +664,9 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
           }
         }
         if (lane < K) {
-          if constexpr (T::CWD == 4) {
 #pragma unroll
-            for (int i = 0; i < 16; i += 4)
-              *reinterpret_cast<float4*>(dst + cq + i) = make_float4(a[i], a[i + 1], a[i + 2], a[i + 3]);
-          } else {  // rows 2 words apart: 8-byte stores keep a half-warp conflict-free
-#pragma unroll
-            for (int i = 0; i < 16; i += 2) *reinterpret_cast<float2*>(dst + cq + i) = make_float2(a[i], a[i + 1]);
-          }
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(dst + cq + i) = make_float4(a[i], a[i + 1], a[i + 2], a[i + 3]);
         }
       }
       __syncthreads();
@@ -804,22 +858,20 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       tc_fence_after();
       const int t = wu >> 2;  // = tile, warp-uniform
       const uint32_t dm = tmem + T::T_D2 + t * 2 * R, dc = dm + R;
-      const uint32_t ahlo = sdesc_lo(sb + T::OFF_HH + t * 16 * 128, 16 * M);
+      const uint32_t ta = tmem + T::T_HA + t * R;  // H_hi columns; H_lo at + R / 2
       const uint32_t bhlo = sdesc_lo(sb + T::OFF_BH, 128);
-      constexpr uint32_t HLO = (T::OFF_HL - T::OFF_HH) >> 4;
 #pragma unroll
       for (int ks = 0; ks < R / 16; ++ks) {
-        // [main | corr] = H_hi [Bs_hi | Bs_lo] (N = 2R spans both), then corr += H_lo Bs_hi
+        // [main | corr] = H_hi [Bs_hi | Bs_lo] (N = 2R spans both), then corr += H_lo Bs_hi;
+        // a K16 step of A is 8 TMEM columns (f16 pairs)
         if constexpr (T::NTILE == 1) {
-          const uint32_t ah = ahlo + ks * (2 * 16 * M >> 4), bh = bhlo + ks * (256 >> 4);
-          umma_f16w(dm, ah, sdesc_hi(128), bh, sdesc_hi(T::BSBO), IDESC2W, ks > 0);
-          umma_f16w(dc, ah + HLO, sdesc_hi(128), bh, sdesc_hi(T::BSBO), IDESC2, 1);
+          const uint32_t bh = bhlo + ks * (256 >> 4);
+          umma_f16_ta(dm, ta + ks * 8, bh, sdesc_hi(T::BSBO), IDESC2W, ks > 0);
+          umma_f16_ta(dc, ta + R / 2 + ks * 8, bh, sdesc_hi(T::BSBO), IDESC2, 1);
         } else {
-          const uint64_t ah = sdesc(sb + T::OFF_HH + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
-          const uint64_t al = sdesc(sb + T::OFF_HL + t * 16 * 128 + ks * 2 * 16 * M, 16 * M, 128);
           const uint64_t bh = sdesc(sb + T::OFF_BH + ks * 256, 128, T::BSBO);
-          umma_f16(dm, ah, bh, IDESC2W, ks > 0);
-          umma_f16(dc, al, bh, IDESC2, 1);
+          umma_f16_ta(dm, ta + ks * 8, bh, IDESC2W, ks > 0);
+          umma_f16_ta(dc, ta + R / 2 + ks * 8, bh, IDESC2, 1);
         }
       }
       umma_commit(bar2 + 8 * t);  // each tile's epilogue starts as soon as its MMAs retire
