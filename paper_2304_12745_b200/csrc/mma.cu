@@ -413,6 +413,23 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
 #pragma unroll
     for (int j = 0; j < K / 2; ++j) hv[j] = ldg_stream(hg + j);
   }
+  // The shared-memory H staging works on items (user pair j, group of 8
+  // antennas G) instead of the thread's own antenna: 8 antennas of one row r
+  // fill one 16-byte core-matrix row, so each item writes 16-byte rows
+  // (STS.128) where the thread-per-antenna layout needed 2-byte stores that
+  // four antenna groups of a warp sent to the same banks (~770 excess
+  // wavefronts per realization at (16,128)). Its loads re-read H (L2 hits)
+  // and are issued before the CTA barrier.
+  constexpr int NJ = K / 2, NIT = NJ * (M / 8) / T::NT;
+  static_assert(NJ * (M / 8) % T::NT == 0 && NJ % 8 == 0, "");
+  float4 hs[NIT][8];  // hs[q][i] = (Re, Im) of H(2j, 8G + i), H(2j + 1, 8G + i)
+#pragma unroll
+  for (int q = 0; q < NIT; ++q) {
+    const int it = tid + q * T::NT, j = it % NJ, G = it / NJ;
+    const float4* hg = reinterpret_cast<const float4*>(p.H + (rid * M + 8 * G) * K) + j;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) hs[q][i] = __ldg(hg + i * (K / 2));
+  }
   float amax = 0.f;
   bool bad = false;  // fmaxf drops NaN: a non-finite channel keeps g = 1 (and diverges at layer 0)
 #pragma unroll
@@ -444,17 +461,31 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   const float ginv = 1.f / g;  // exact (power of two)
 
   // ---- stage H (hi / lo f16) in the shared core layout -------------------------
+  // Item (j, G) writes rows Re 2j, Re 2j+1, Im 2j, Im 2j+1 over antennas 8G..8G+7.
+  // Rows 2j and 2j + 1 go out in swapped order for j & 4, so the 8 lanes of a
+  // quarter-warp (j = 8n .. 8n+7) hit the 8 distinct 16-byte rows of a core
+  // matrix pair: conflict-free.
 #pragma unroll
-  for (int j = 0; j < K / 2; ++j) {
-    const float vals[4] = {hv[j].x * g, hv[j].y * g, hv[j].z * g, hv[j].w * g};
-    const int kk = 2 * j;
-    const int rows[4] = {kk, K + kk, kk + 1, K + kk + 1};  // Re k, Im k, Re k+1, Im k+1
+  for (int q = 0; q < NIT; ++q) {
+    const int it = tid + q * T::NT, j = it % NJ, G = it / NJ;
+    const bool swp = (j >> 2) & 1;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const __half h = __float2half_rn(vals[u]);
-      const __half l = __float2half_rn((vals[u] - __half2float(h)) * 2048.f);
-      *reinterpret_cast<uint16_t*>(smem + T::OFF_HH + T::hoff(rows[u], m)) = f16_bits(h);
-      *reinterpret_cast<uint16_t*>(smem + T::OFF_HL + T::hoff(rows[u], m)) = f16_bits(l);
+    for (int s = 0; s < 2; ++s) {      // user 2j + (s ^ swp)
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        uint32_t hh[4], hl[4];
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+          const float4 a = hs[q][i], b = hs[q][i + 1];
+          const bool up = (s == 1) != swp;  // user 2j + 1
+          const float va = part == 0 ? (up ? a.z : a.x) : (up ? a.w : a.y);
+          const float vb = part == 0 ? (up ? b.z : b.x) : (up ? b.w : b.y);
+          split2(va * g, vb * g, hh[i / 2], hl[i / 2]);
+        }
+        const int r = part * K + 2 * j + ((s == 1) != swp ? 1 : 0);
+        *reinterpret_cast<uint4*>(smem + T::OFF_HH + T::hoff(r, 8 * G)) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
+        *reinterpret_cast<uint4*>(smem + T::OFF_HL + T::hoff(r, 8 * G)) = make_uint4(hl[0], hl[1], hl[2], hl[3]);
+      }
     }
   }
   fence_async_smem();  // H is read by the tensor cores (async proxy)
