@@ -405,6 +405,16 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     if (!RB) asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
 
+  // The realization that will most likely take this CTA slot next (blocks are
+  // dispatched in order, one wave = prefetch_ahead CTAs) gets its H pulled into
+  // L2 now, so its prologue loads hit L2 instead of waiting on HBM: with one
+  // CTA per SM at (32,256) nothing else overlaps a prologue (the launch's
+  // L-independent cost was ~15% of config 4 before).
+  if (!RB && tid == 0 && p.prefetch_ahead > 0 && rid + p.prefetch_ahead < p.B) {
+    const float2* nh = p.H + (rid + p.prefetch_ahead) * M * K;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nh), "r"(static_cast<uint32_t>(M * K * 8))
+                 : "memory");
+  }
   // ---- H row of antenna m = tid: registers, max |.| over the realization ----
   const int m = tid;
   float4 hv[K / 2];  // hv[j] = (Re H(2j, m), Im H(2j, m), Re H(2j+1, m), Im H(2j+1, m))
@@ -1087,6 +1097,16 @@ cudaError_t launch_mma_t(const FusedArgs& args, bool pgd, cudaStream_t s, long l
   if (e != cudaSuccess) return e;
   if (nblocks) *nblocks = a.B;
   if (a.B == 0) return cudaSuccess;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  {
+    int fast_per_sm = 1;  // one wave of the fast kernel = the L2 prefetch distance
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fast_per_sm, kern, T::NT, T::SMEM) != cudaSuccess ||
+        fast_per_sm < 1)
+      fast_per_sm = 1;
+    a.prefetch_ahead = static_cast<long long>(sms) * fast_per_sm;
+  }
   int* list = nullptr;
   if ((e = scratch_alloc_async(reinterpret_cast<void**>(&list), sizeof(int) * (a.B + 1), s)) != cudaSuccess)
     return e;
@@ -1098,9 +1118,7 @@ cudaError_t launch_mma_t(const FusedArgs& args, bool pgd, cudaStream_t s, long l
     // one wave of the robust instance: enough CTAs for a batch that is handed
     // off entirely (e.g. every channel far outside the f16 range), and a few
     // hundred CTAs that read a zero count and exit in the usual case
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int per_sm = 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, robust, T::NT, T::SMEM) != cudaSuccess || per_sm < 1)
       per_sm = 1;
     const long long grid = std::min<long long>(a.B, static_cast<long long>(sms) * per_sm);

@@ -31,6 +31,7 @@ struct FusedArgs {
   int64_t* iterations;    // PGD with residual_tol: iterations taken per realization (nullable)
   float cmax;             // tensor-core kernel: max |c_k| and the range of the
   float eta_lo, eta_hi;   //   per-layer steps (filled by launch_mma)
+  long long prefetch_ahead;  // tensor-core kernel: L2 prefetch distance in realizations (0: none)
   float c[UFPGD_MAX_USERS];
   float eta[UFPGD_MAX_LAYERS];
   float thr[UFPGD_MAX_LAYERS];
