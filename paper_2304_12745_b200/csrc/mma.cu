@@ -63,7 +63,8 @@ struct MmaShape {
   static constexpr int BSBO = 16 * R;                    // Bs N-group stride (descriptor SBO)
   static constexpr int OFF_BH = OFF_W + Q * M * 2;       // Bs hi [R x R] f16, boff()
   static constexpr int OFF_BL = OFF_BH + (R / 8) * BSBO; // Bs lo (continues Bs hi along N)
-  static constexpr int FSTR = R + 4;  // fp32 exchange rows (floats): 4 mod 32 words, see chunk()
+  // fp32 exchange rows (floats): 4 mod 32 words at CWD 4, 8 mod 32 at CWD 2 (see chunk())
+  static constexpr int FSTR = R + (CWD == 4 ? 4 : 8);
   // F [R][FSTR] (hi rows of P) and G (lo rows) alias the W operand: they are
   // written after the stage-1 MMAs retire and read before W is rewritten.
   static constexpr int OFF_F = OFF_W;
@@ -105,13 +106,13 @@ struct MmaShape {
   // fills one whole 128-byte core matrix (conflict-free 8-byte stores), and each
   // quarter-warp reads 8 rows of one column chunk of the F / G exchange rows
   // (row stride FSTR = 4 mod 32 words: conflict-free 16-byte loads).
-  // CWD 2: each warp covers one 8 x 8 block of X' — rows k0 .. k0+7 (lanes
-  // i & 7) x four 2-wide column chunks (i >> 3) — so every 4-byte Bs put of the
-  // warp fills one whole core matrix, and each half-warp's 8-byte F / G loads
-  // cover 8 rows x 4 consecutive words (FSTR = 4 mod 32): both conflict-free
-  // (the earlier row-major walk had 2-way conflicting Bs stores — ~64 excess
-  // wavefronts per realization-layer at (16,128)).
-  // The stage-1 drain stores 16-byte row pieces, conflict-free at this FSTR.
+  // CWD 2 (the (16,128) shape, whose M = 64 stage-1 drain reads TMEM with the
+  // 16x256b shape: thread i holds rows i / 4 and i / 4 + 8, column pairs
+  // 2 (i % 4)): each warp covers one 8 x 8 block of X' — rows (i & 3) +
+  // 4 (i >> 4) x four 2-wide column chunks ((i >> 2) & 3) — so every 4-byte Bs
+  // put of the warp fills one whole core matrix, and each half-warp's 8-byte
+  // F / G loads cover 4 rows x 8 consecutive words (FSTR = 8 mod 32), as do the
+  // drain's 8-byte stores: all conflict-free.
   static __device__ __forceinline__ void chunk(int ch, int& k, int& c) {
     if constexpr (CWD == 4) {
       const int hw = ch >> 4, i = ch & 15;
@@ -119,8 +120,8 @@ struct MmaShape {
       c = (hw % (K / 8)) * 8 + (i >> 3) * 4;
     } else {
       const int w = ch >> 5, i = ch & 31;
-      k = (w / (K / 8)) * 8 + (i & 7);
-      c = (w % (K / 8)) * 8 + (i >> 3) * 2;
+      k = (w / (K / 8)) * 8 + (i & 3) + 4 * (i >> 4);
+      c = (w % (K / 8)) * 8 + ((i >> 2) & 3) * 2;
     }
   }
   // Bs: element (kk, n), K-major (K = kk, N = n): LBO (K-group) 128, SBO (N-group) BSBO.
@@ -257,6 +258,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
         "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
       : "r"(taddr));
 }
+// 16 lanes x 32 columns (from the 16-lane group at taddr): thread i gets rows
+// i / 4 (v[4 j], v[4 j + 1]) and i / 4 + 8 (v[4 j + 2], v[4 j + 3]) at columns
+// 8 j + 2 (i % 4) + {0, 1}, j = 0..3 (layout measured: tools/probe/tmem_layout.cu).
+__device__ __forceinline__ void tmem_ld16x256(uint32_t taddr, float* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
+        "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+      : "r"(taddr));
+}
 // 16 registers per thread -> 16 consecutive TMEM columns of this warp's 32 lanes.
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
   asm volatile(
@@ -384,6 +395,13 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   const int n_real = RB ? *redo_count : 1;
   for (int it = RB ? static_cast<int>(blockIdx.x) : 0; it < n_real; it += RB ? static_cast<int>(gridDim.x) : 1) {
   const long long rid = RB ? static_cast<long long>(redo_list[it]) : static_cast<long long>(blockIdx.x);
+#ifdef UFPGD_MMA_TIMING
+  long long pst[7];  // prologue / epilogue stamps of the probe CTA (see tst below)
+#define PSTAMP(i) pst[i] = clock64();
+  PSTAMP(0)
+#else
+#define PSTAMP(i)
+#endif
   const uint32_t sb = smem_u32(smem);
   const uint32_t bar1 = sb + T::OFF_BAR;                // + 8 t: stage-1 part t done
   const uint32_t bar2 = sb + T::OFF_BAR + 8 * T::NTILE;  // + 8 t: stage-2 tile t done
@@ -458,6 +476,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  PSTAMP(1)
   const uint32_t tmem = *tslot;
   float gmax = 0.f, gbad = 0.f;
 #pragma unroll
@@ -499,6 +518,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     }
   }
   fence_async_smem();  // H is read by the tensor cores (async proxy)
+  PSTAMP(2)
   // Stage 2's A operand in TMEM: antenna m's row (K-major, r = part K + k) in
   // TMEM lane m % 128 of its tile's H columns — the same f16 values (same
   // rounding) as the shared copy stage 1 reads. Ordered before the first
@@ -520,6 +540,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
+  PSTAMP(3)
 
   // ---- W0 (scaled: W_s = W / g) in registers: wr[k], wi[k] for antenna m ------
   float wr[K], wi[K];
@@ -588,6 +609,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     thr_b = p.lambda * eta_b;
     if (p.eta_out && tid == 0) p.eta_out[rid] = eta_b;
   }
+  PSTAMP(4)
   for (long long l = 0; l < p.L; ++l) {
     TSTAMP(0)
     const bool xzero = (l == 0 && p.w0_mode == UFPGD_W0_ZERO);
@@ -667,6 +689,32 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       ph1 ^= 1;
       TSTAMP(3)
       tc_fence_after();
+      if constexpr (Q == 64) {
+        // M = 64 accumulator: rows in lanes 0..15 of each quadrant. The 16x256b
+        // shape loads just those 16 lanes (thread i: rows i / 4, i / 4 + 8,
+        // column pairs 8 j + 2 (i % 4)), so no lane loads or combines the 16
+        // unused lanes of the 32x32b shape (half the LDTM and FP32x2 work).
+        static_assert(T::NTILE == 1 && CW == 2 * R / 2 && T::CWD == 2, "");
+        float a[16], b[16];
+        tmem_ld16x256(tmem + lrow + T::T_D1A, a);
+        if (quad < 2) tmem_ld16x256(tmem + lrow + T::T_D1B, b);
+        tmem_wait<16>(a);
+        if (quad < 2) tmem_wait<16>(b);
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const float2 t = quad < 2 ? ffma2(kLoScale, make_float2(b[i], b[i + 1]), make_float2(a[i], a[i + 1]))
+                                    : fmul2(kLoScale, make_float2(a[i], a[i + 1]));
+          a[i] = t.x;
+          a[i + 1] = t.y;
+        }
+        const int kr = lane >> 2, cp = 2 * (lane & 3);
+        float* d0 = (quad < 2 ? F : G) + (part * K + kr) * T::FSTR + cp;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          *reinterpret_cast<float2*>(d0 + 8 * j) = make_float2(a[4 * j], a[4 * j + 1]);
+          *reinterpret_cast<float2*>(d0 + 8 * T::FSTR + 8 * j) = make_float2(a[4 * j + 2], a[4 * j + 3]);
+        }
+      } else {
       float* dst = (quad < 2 ? F : G) + (part * K + lane) * T::FSTR + c0;
 #pragma unroll
       for (int cq = 0; cq < CW; cq += 16) {
@@ -709,6 +757,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
           for (int i = 0; i < 16; i += 4)
             *reinterpret_cast<float4*>(dst + cq + i) = make_float4(a[i], a[i + 1], a[i + 2], a[i + 3]);
         }
+      }
       }
       __syncthreads();
     }
@@ -999,6 +1048,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     TSTAMP(8)
   }
 
+  PSTAMP(5)
   // ---- W out (unscaled), per-realization reductions ---------------------------
   // (a realization handed to the robust path writes garbage W here; the robust
   // kernel, later in the stream, overwrites it)
@@ -1009,9 +1059,11 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     for (int j = 0; j < K / 2; ++j)
       stg_stream(wg + j, make_float4(wr[2 * j] * gout, wi[2 * j] * gout, wr[2 * j + 1] * gout, wi[2 * j + 1] * gout));
 #ifdef UFPGD_MMA_TIMING
+    PSTAMP(6)
     if (probe) {
       long long* o = reinterpret_cast<long long*>(p.W + rid * M * K);
       for (int i = 0; i < 9; ++i) o[i] = tst[i];
+      for (int i = 0; i < 7; ++i) o[9 + i] = pst[i];
     }
 #endif
   }
