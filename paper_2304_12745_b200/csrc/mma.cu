@@ -285,15 +285,21 @@ __device__ __forceinline__ void tmem_wait(float* v) {
   for (int i = 0; i < N; ++i) asm volatile("" : "+f"(v[i]));
 }
 // f16 pair split of (a, b): hi = f16(x), lo = f16((x - hi) * 2^11).
-// The residual and its 2^11 scaling run as packed FP32x2 (FADD2, FMUL2): one
-// instruction each for the pair (the f16 splits were ~24% of the (16,128)
-// kernel's instructions).
+// The residual hi - x comes from the mixed-precision add (add.f32.f16: one
+// FHADD reading the f16 half in place, so hi is never converted back to FP32 —
+// 5 instructions per pair instead of 6; the f16 splits were ~24% of the
+// (16,128) kernel's instructions), scaled by -2^11 as one packed FMUL2. Both
+// steps are exact (x - hi is representable), so the bits are those of the
+// FP32 residual.
 __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(a, b);
-  const float2 hf = __half22float2(h);
-  const float2 r = __fmul2_rn(__fadd2_rn(make_float2(a, b), make_float2(-hf.x, -hf.y)), make_float2(2048.f, 2048.f));
+  const uint32_t hb = *reinterpret_cast<const uint32_t*>(&h);
+  float d0, d1;
+  asm("add.rn.f32.f16 %0, %1, %2;" : "=f"(d0) : "h"(static_cast<unsigned short>(hb & 0xffffu)), "f"(-a));
+  asm("add.rn.f32.f16 %0, %1, %2;" : "=f"(d1) : "h"(static_cast<unsigned short>(hb >> 16)), "f"(-b));
+  const float2 r = __fmul2_rn(make_float2(d0, d1), make_float2(-2048.f, -2048.f));
   const __half2 l = __floats2half2_rn(r.x, r.y);
-  hi = *reinterpret_cast<const uint32_t*>(&h);
+  hi = hb;
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 __device__ __forceinline__ uint16_t f16_bits(__half h) { return *reinterpret_cast<const uint16_t*>(&h); }
