@@ -73,11 +73,12 @@ struct MmaShape {
   static constexpr int OFF_BAR = OFF_BL + (R / 8) * BSBO;  // mbarriers, TMEM slot, reductions
   static constexpr int SMEM = OFF_BAR + 512;
   // TMEM columns (fp32 accumulators)
-  // D1 part t: [X-part with H_hi | with H_lo] (2R) over antenna tile t (stage 1 is
-  // split-K by tile so each tile's antennas start their MMAs as soon as their own
-  // W operand is written); D2 per tile t: [main | corr]. Both at column 2R t:
-  // tile t's threads drain D2 part t (E2) before issuing D1 part t, and D1 is
-  // drained (E1) behind a CTA barrier before the stage-2 MMAs.
+  // D1: [X-part with H_hi | with H_lo] (2R columns; each antenna tile's K-steps
+  // are issued as soon as that tile's W operand is written, tile 1's after tile
+  // 0's); D2 per tile t: [main | corr] at column 2R t. D1 overlaps D2 tile 0:
+  // tile 0's threads drain D2 tile 0 before its stage-1 MMAs are issued (tile
+  // 1's wait for tile 0's issue), and D1 is drained behind a CTA barrier
+  // before the stage-2 MMAs.
   static constexpr uint32_t T_D1A = 0, T_D1B = R, T_D2 = 0;
   // Stage 2's A operand (H hi / lo, K-major f16 pairs: R / 2 columns each per
   // tile) lives in TMEM from the prologue on, so the stage-2 MMAs read only
@@ -666,6 +667,13 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       if (T::NTILE > 1) named_bar(1 + tile, T::NT / T::NTILE);
       else __syncthreads();
       TSTAMP(1)
+      // (32,256): both tiles accumulate into one D1 (columns [0, 2R)); tile 1's
+      // first warp issues after tile 0's MMAs are queued (warp 0 -> warp 4
+      // named barrier, tcgen05 fences around it), so the tensor pipe runs them
+      // in order and the drain reads one accumulator instead of summing two
+      // split-K parts (half its TMEM loads). Tile 1's MMAs also overwrite D2
+      // tile 0's columns only after tile 0's group has drained them.
+      if (T::NTILE > 1 && warp == 4) named_bar(4, 64);
       if (wu == tile * 4) {  // the tile group's first warp
         const int tu = wu >> 2;  // = tile, warp-uniform: the descriptors stay in uniform registers
         tc_fence_after();
@@ -679,15 +687,20 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
             umma_f16w(tmem + tu * 2 * R + T::T_D1A, alo + i * (2 * 16 * Q >> 4), sdesc_hi(128), blo + i * (256 >> 4),
                       sdesc_hi(16 * M), IDESC1, i > 0);
           else
-            umma_f16(tmem + tu * 2 * R + T::T_D1A, sdesc(sw + i * 2 * 16 * Q, 16 * Q, 128),
-                     sdesc(sh + i * 256, 128, 16 * M), IDESC1, i > 0);
+            umma_f16(tmem + T::T_D1A, sdesc(sw + i * 2 * 16 * Q, 16 * Q, 128), sdesc(sh + i * 256, 128, 16 * M),
+                     IDESC1, tu > 0 || i > 0);
         }
         umma_commit(bar1 + 8 * tu);
       }
+      if (T::NTILE > 1 && warp == 0) {
+        tc_fence_before();
+        __syncwarp();
+        named_bar_arrive(4, 64);
+      }
       TSTAMP(2)
       // D1 rows q = (hilo, part, k): TMEM lane quadrant hilo * 2 + part, lane k
-      // (M = 128: lanes 32 q4 + k; M = 64: lanes 32 q4 + k for k < 16), summed
-      // over the tile parts. Warp w reads quadrant w % 4, columns [w / 4 * CW, + CW).
+      // (M = 128: lanes 32 q4 + k; M = 64: lanes 32 q4 + k for k < 16).
+      // Warp w reads quadrant w % 4, columns [w / 4 * CW, + CW).
       constexpr int CW = R * 4 / NW;
       const int quad = warp & 3, c0 = (warp >> 2) * CW, part = quad & 1;
 #pragma unroll
@@ -729,20 +742,6 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         if (quad < 2) tmem_ld16(tmem + lrow + T::T_D1B + c0 + cq, b);
         tmem_wait<16>(a);
         if (quad < 2) tmem_wait<16>(b);
-#pragma unroll
-        for (int t = 1; t < T::NTILE; ++t) {  // the other antenna tiles' partial sums, in tile order
-          float a2[16], b2[16];
-          tmem_ld16(tmem + lrow + t * 2 * R + T::T_D1A + c0 + cq, a2);
-          if (quad < 2) tmem_ld16(tmem + lrow + t * 2 * R + T::T_D1B + c0 + cq, b2);
-          tmem_wait<16>(a2);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) a[i] += a2[i];
-          if (quad < 2) {
-            tmem_wait<16>(b2);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) b[i] += b2[i];
-          }
-        }
         if (quad < 2) {
 #pragma unroll
           for (int i = 0; i < 16; i += 2) {  // hi rows: W_hi H_hi + W_hi H_lo (packed FP32x2)
