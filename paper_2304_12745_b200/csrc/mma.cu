@@ -44,9 +44,19 @@ namespace {
 // Shape of the tensor-core kernel: one thread per antenna (NT = M), 2K
 // real-form rows r = (part, k), Q = 4K operand rows q = (hilo, part, k) for
 // stage 1 (MMA M = Q: 128 at K = 32, 64 at K = 16), M / 128 stage-2 tiles.
-template <int K_, int M_, int MINB_>
+// PAIR: the (16,128) frame holds two (8,64) realizations block-diagonally
+// (BASELINE config 2's shape): H_pair = diag(H_a, H_b), so X, X' H^* and the
+// per-antenna prox never mix the blocks. Thread m works on antenna m % 64 of
+// realization m / 64 and holds only its realization's 8 users; the
+// off-diagonal operand blocks (W rows of the other users at its antenna, Bs)
+// are zeros written once, so the split, drain, Bs build and prox do half the
+// (16,128) kernel's work for the same MMAs.
+template <int K_, int M_, int MINB_, bool PAIR_ = false>
 struct MmaShape {
   static constexpr int K = K_, M = M_, NT = M_, MINB = MINB_;
+  static constexpr bool PAIR = PAIR_;
+  static constexpr int KX = PAIR ? K_ / 2 : K_, MX = PAIR ? M_ / 2 : M_;  // per-realization users, antennas
+  static_assert(!PAIR || (K_ == 16 && M_ == 128), "pairs of (8,64) realizations in the (16,128) frame");
   static constexpr int R = 2 * K;     // real-form rows (part, k)
   static constexpr int Q = 2 * R;     // stage-1 A rows (hilo, part, k) = stage-1 MMA M
   static constexpr int NTILE = M / 128;
@@ -66,11 +76,13 @@ struct MmaShape {
   // fp32 exchange rows (floats): 4 mod 32 words at CWD 4, 8 mod 32 at CWD 2 (see chunk())
   static constexpr int FSTR = R + (CWD == 4 ? 4 : 8);
   // F [R][FSTR] (hi rows of P) and G (lo rows) alias the W operand: they are
-  // written after the stage-1 MMAs retire and read before W is rewritten.
-  static constexpr int OFF_F = OFF_W;
+  // written after the stage-1 MMAs retire and read before W is rewritten (PAIR:
+  // their own region, as the W operand's zero rows are written only once).
+  static constexpr int OFF_X = OFF_BL + (R / 8) * BSBO;
+  static constexpr int OFF_F = PAIR ? OFF_X : OFF_W;
   static constexpr int OFF_G = OFF_F + R * FSTR * 4;
   static_assert(2 * R * FSTR * 4 <= Q * M * 2, "");
-  static constexpr int OFF_BAR = OFF_BL + (R / 8) * BSBO;  // mbarriers, TMEM slot, reductions
+  static constexpr int OFF_BAR = PAIR ? OFF_X + 2 * R * FSTR * 4 : OFF_X;  // mbarriers, TMEM slot, reductions
   static constexpr int SMEM = OFF_BAR + 512;
   // TMEM columns (fp32 accumulators)
   // D1: [X-part with H_hi | with H_lo] (2R columns; each antenna tile's K-steps
@@ -269,6 +281,12 @@ __device__ __forceinline__ void tmem_ld16x256(uint32_t taddr, float* v) {
         "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
       : "r"(taddr));
 }
+// 8 consecutive TMEM columns of this warp's 32 lanes -> 8 registers per thread.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "r"(taddr));
+}
 // 16 registers per thread -> 16 consecutive TMEM columns of this warp's 32 lanes.
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
   asm volatile(
@@ -402,6 +420,12 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   const int n_real = RB ? *redo_count : 1;
   for (int it = RB ? static_cast<int>(blockIdx.x) : 0; it < n_real; it += RB ? static_cast<int>(gridDim.x) : 1) {
   const long long rid = RB ? static_cast<long long>(redo_list[it]) : static_cast<long long>(blockIdx.x);
+  // the thread's realization (PAIR: 2 rid + tid / 64) and its antenna there
+  constexpr int KT = T::KX;  // users per thread
+  const int hx = T::PAIR ? tid / T::MX : 0;
+  const long long rx = T::PAIR ? 2 * rid + hx : rid;
+  const bool xvalid = !T::PAIR || rx < p.B;  // PAIR: an odd batch's last CTA has one realization
+  const int ml = T::PAIR ? tid % T::MX : tid;
 #ifdef UFPGD_MMA_TIMING
   long long pst[7];  // prologue / epilogue stamps of the probe CTA (see tst below)
 #define PSTAMP(i) pst[i] = clock64();
@@ -435,18 +459,23 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   // L2 now, so its prologue loads hit L2 instead of waiting on HBM: with one
   // CTA per SM at (32,256) nothing else overlaps a prologue (the launch's
   // L-independent cost was ~15% of config 4 before).
-  if (!RB && tid == 0 && p.prefetch_ahead > 0 && rid + p.prefetch_ahead < p.B) {
-    const float2* nh = p.H + (rid + p.prefetch_ahead) * M * K;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nh), "r"(static_cast<uint32_t>(M * K * 8))
-                 : "memory");
+  if (!RB && tid == 0 && p.prefetch_ahead > 0) {
+    constexpr int RPC = T::PAIR ? 2 : 1;  // realizations per CTA
+    const long long r0 = (rid + p.prefetch_ahead) * RPC, nr = min(static_cast<long long>(RPC), p.B - r0);
+    if (nr > 0) {
+      const float2* nh = p.H + r0 * T::MX * T::KX;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nh),
+                   "r"(static_cast<uint32_t>(nr * T::MX * T::KX * 8))
+                   : "memory");
+    }
   }
   // ---- H row of antenna m = tid: registers, max |.| over the realization ----
   const int m = tid;
-  float4 hv[K / 2];  // hv[j] = (Re H(2j, m), Im H(2j, m), Re H(2j+1, m), Im H(2j+1, m))
+  float4 hv[KT / 2];  // hv[j] = (Re H(2j, m), Im H(2j, m), Re H(2j+1, m), Im H(2j+1, m)) of the thread's realization
   {
-    const float4* hg = reinterpret_cast<const float4*>(p.H + (rid * M + m) * K);
+    const float4* hg = reinterpret_cast<const float4*>(p.H + (rx * T::MX + ml) * KT);
 #pragma unroll
-    for (int j = 0; j < K / 2; ++j) hv[j] = ldg_stream(hg + j);
+    for (int j = 0; j < KT / 2; ++j) hv[j] = xvalid ? ldg_stream(hg + j) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   // The shared-memory H staging works on items (user pair j, group of 8
   // antennas G) instead of the thread's own antenna: 8 antennas of one row r
@@ -461,14 +490,24 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
 #pragma unroll
   for (int q = 0; q < NIT; ++q) {
     const int it = tid + q * T::NT, j = it % NJ, G = it / NJ;
-    const float4* hg = reinterpret_cast<const float4*>(p.H + (rid * M + 8 * G) * K) + j;
+    if constexpr (T::PAIR) {
+      // frame user pair j, antenna group G: realization G / 8 (= hx here); the
+      // off-diagonal blocks (j / 4 != G / 8) are zeros
+      const bool diag = (j / (T::KX / 2)) == (G / (T::MX / 8));
+      const float4* hg = reinterpret_cast<const float4*>(p.H + (rx * T::MX + 8 * (G % (T::MX / 8))) * KT) +
+                         j % (T::KX / 2);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) hs[q][i] = __ldg(hg + i * (K / 2));
+      for (int i = 0; i < 8; ++i) hs[q][i] = diag && xvalid ? __ldg(hg + i * (KT / 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      const float4* hg = reinterpret_cast<const float4*>(p.H + (rid * M + 8 * G) * K) + j;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) hs[q][i] = __ldg(hg + i * (K / 2));
+    }
   }
   float amax = 0.f;
   bool bad = false;  // fmaxf drops NaN: a non-finite channel keeps g = 1 (and diverges at layer 0)
 #pragma unroll
-  for (int j = 0; j < K / 2; ++j) {
+  for (int j = 0; j < KT / 2; ++j) {
     const float a = fmaxf(fmaxf(fabsf(hv[j].x), fabsf(hv[j].y)), fmaxf(fabsf(hv[j].z), fabsf(hv[j].w)));
     amax = fmaxf(amax, a);
     bad |= !(fabsf(hv[j].x) + fabsf(hv[j].y) + fabsf(hv[j].z) + fabsf(hv[j].w) <= FLT_MAX);
@@ -485,11 +524,12 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   tc_fence_after();
   PSTAMP(1)
   const uint32_t tmem = *tslot;
-  float gmax = 0.f, gbad = 0.f;
+  float gmax = 0.f, gbad = 0.f;  // over the thread's realization (PAIR: its half of the warps)
+  constexpr int NWX = T::PAIR ? NW / 2 : NW;
 #pragma unroll
-  for (int w = 0; w < NW; ++w) {
-    gmax = fmaxf(gmax, red[w]);
-    gbad = fmaxf(gbad, red[16 + w]);
+  for (int w = 0; w < NWX; ++w) {
+    gmax = fmaxf(gmax, red[hx * NWX + w]);
+    gbad = fmaxf(gbad, red[16 + hx * NWX + w]);
   }
   // g = 2^-e with gmax in [2^e, 2^(e+1)): g * gmax in [1, 2). Exact scaling.
   float g = 1.f;
@@ -539,7 +579,9 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       for (int c = 0; c < 16; ++c) {
         const int r = half * 32 + 2 * c;  // rows r, r + 1: one part, users k, k + 1 (K even)
         const int part = r / K, k = r % K;
-        const float4 hq = hv[k / 2];
+        // PAIR: the other realization's users at this antenna are zeros
+        const bool own = !T::PAIR || k / T::KX == hx;
+        const float4 hq = own ? hv[(k % T::KX) / 2] : make_float4(0.f, 0.f, 0.f, 0.f);
         split2((part == 0 ? hq.x : hq.y) * g, (part == 0 ? hq.z : hq.w) * g, hh[c], hl[c]);
       }
       tmem_st16(th + half * 16, hh);
@@ -550,20 +592,20 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   PSTAMP(3)
 
   // ---- W0 (scaled: W_s = W / g) in registers: wr[k], wi[k] for antenna m ------
-  float wr[K], wi[K];
+  float wr[KT], wi[KT];
   if (p.w0_mode == UFPGD_W0_CONJ_H) {
 #pragma unroll
-    for (int j = 0; j < K / 2; ++j) {
+    for (int j = 0; j < KT / 2; ++j) {
       wr[2 * j] = hv[j].x * ginv;
       wi[2 * j] = -hv[j].y * ginv;
       wr[2 * j + 1] = hv[j].z * ginv;
       wi[2 * j + 1] = -hv[j].w * ginv;
     }
   } else if (p.w0_mode == UFPGD_W0_GIVEN) {
-    const float4* wg0 = reinterpret_cast<const float4*>(p.W0 + (rid * M + m) * K);
+    const float4* wg0 = reinterpret_cast<const float4*>(p.W0 + (rx * T::MX + ml) * KT);
 #pragma unroll
-    for (int j = 0; j < K / 2; ++j) {
-      const float4 v = wg0[j];
+    for (int j = 0; j < KT / 2; ++j) {
+      const float4 v = xvalid ? wg0[j] : make_float4(0.f, 0.f, 0.f, 0.f);
       wr[2 * j] = v.x * ginv;
       wi[2 * j] = v.y * ginv;
       wr[2 * j + 1] = v.z * ginv;
@@ -571,13 +613,31 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     }
   } else {
 #pragma unroll
-    for (int k = 0; k < K; ++k) wr[k] = wi[k] = 0.f;
+    for (int k = 0; k < KT; ++k) wr[k] = wi[k] = 0.f;
   }
   int aW = 0;        // robust path: the W registers hold W_s 2^-aW ...
   float wn2 = 0.f;   // ... and ||w_m||^2 in that domain
   if (RB) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) wn2 = fmaf(wr[k], wr[k], fmaf(wi[k], wi[k], wn2));
+    for (int k = 0; k < KT; ++k) wn2 = fmaf(wr[k], wr[k], fmaf(wi[k], wi[k], wn2));
+  }
+  if constexpr (T::PAIR) {
+    // the off-diagonal zeros, written once: the W operand rows of the other
+    // realization's users at this antenna, and the whole Bs (its diagonal
+    // blocks are rewritten every layer); ordered before the first MMAs by the
+    // fenced barriers of layer 0
+#pragma unroll
+    for (int hl = 0; hl < 2; ++hl)
+#pragma unroll
+      for (int part = 0; part < 2; ++part)
+        *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(hl * R + part * K + T::KX * (1 - hx), m)) =
+            make_uint4(0u, 0u, 0u, 0u);
+    constexpr int BSB = 2 * (R / 8) * T::BSBO;  // Bs hi + lo bytes
+    static_assert(BSB % (16 * T::NT) == 0, "");
+#pragma unroll
+    for (int i = 0; i < BSB / (16 * T::NT); ++i)
+      *reinterpret_cast<uint4*>(smem + T::OFF_BH + 16 * (tid + i * T::NT)) = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();  // before layer 0's Bs build writes the diagonal blocks (no split barrier at W0 = 0)
   }
 
   constexpr uint32_t IDESC1 = idesc_f16_amn<Q, 2 * R>();
@@ -629,7 +689,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         __syncthreads();
         float mc2 = 0.f;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) mc2 = fmaxf(mc2, redw[w]);
+        for (int w = hx * NWX; w < (hx + 1) * NWX; ++w) mc2 = fmaxf(mc2, redw[w]);  // PAIR: own realization
         __syncthreads();  // redw is reused by the Bs maximum
         if (mc2 > 0.f && mc2 < FLT_MAX) {
           const int d = ilogbf(mc2) / 2 - 12;
@@ -651,10 +711,10 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     if (!xzero) {
       // W operand rows q = (hilo, part, k) from the thread's antenna column
 #pragma unroll
-      for (int pg = 0; pg < 2 * (K / 8); ++pg) {  // 8 rows (part, k .. k+7)
-        const int part = pg / (K / 8), kg = pg % (K / 8);
+      for (int pg = 0; pg < 2 * (KT / 8); ++pg) {  // 8 rows (part, k .. k+7)
+        const int part = pg / (KT / 8), kg = pg % (KT / 8);
         const float* src = (part == 0 ? wr : wi) + 8 * kg;
-        const int q0 = part * K + 8 * kg;
+        const int q0 = part * K + 8 * kg + (T::PAIR ? T::KX * hx : 0);
         uint32_t h[4], lo[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) split2(src[2 * u], src[2 * u + 1], h[u], lo[u]);
@@ -719,8 +779,11 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         if (quad < 2) tmem_ld16x256(tmem + lrow + T::T_D1B, b);
         tmem_wait<16>(a);
         if (quad < 2) tmem_wait<16>(b);
+        // PAIR: only the diagonal blocks of X are needed — row kr (realization
+        // a) with column blocks j = 0, 2, row kr + 8 (b) with j = 1, 3
 #pragma unroll
         for (int i = 0; i < 16; i += 2) {
+          if (T::PAIR && i != 0 && i != 6 && i != 8 && i != 14) continue;
           const float2 t = quad < 2 ? ffma2(kLoScale, make_float2(b[i], b[i + 1]), make_float2(a[i], a[i + 1]))
                                     : fmul2(kLoScale, make_float2(a[i], a[i + 1]));
           a[i] = t.x;
@@ -730,8 +793,10 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         float* d0 = (quad < 2 ? F : G) + (part * K + kr) * T::FSTR + cp;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          *reinterpret_cast<float2*>(d0 + 8 * j) = make_float2(a[4 * j], a[4 * j + 1]);
-          *reinterpret_cast<float2*>(d0 + 8 * T::FSTR + 8 * j) = make_float2(a[4 * j + 2], a[4 * j + 3]);
+          if (!T::PAIR || j % 2 == 0)
+            *reinterpret_cast<float2*>(d0 + 8 * j) = make_float2(a[4 * j], a[4 * j + 1]);
+          if (!T::PAIR || j % 2 == 1)
+            *reinterpret_cast<float2*>(d0 + 8 * T::FSTR + 8 * j) = make_float2(a[4 * j + 2], a[4 * j + 3]);
         }
       } else {
       float* dst = (quad < 2 ? F : G) + (part * K + lane) * T::FSTR + c0;
@@ -779,6 +844,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       for (int ch = tid; ch < NCH; ch += T::NT) {
         int k, c;
         T::chunk(ch, k, c);
+        if (T::PAIR && k / T::KX != c / T::KX) continue;  // off-diagonal block: static zeros (warp-uniform)
         float xr[CWD], xi[CWD];
   #pragma unroll
         for (int u = 0; u < CWD; ++u) xr[u] = xi[u] = 0.f;
@@ -852,10 +918,11 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         const int ch = tid;
         int k, c;
         T::chunk(ch, k, c);
+        const bool live = !T::PAIR || k / T::KX == c / T::KX;  // PAIR: off-diagonal blocks stay zero
         float xr[CWD], xi[CWD];
   #pragma unroll
         for (int u = 0; u < CWD; ++u) xr[u] = xi[u] = 0.f;
-        if (!xzero) {
+        if (!xzero && live) {
           const float* F0 = F + k * T::FSTR;        // P rows (0, k), (1, k): hi parts in F, lo in G
           const float* F1 = F + (K + k) * T::FSTR;
           const float* G0 = G + k * T::FSTR;
@@ -902,7 +969,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
           __syncthreads();
           float mb = 0.f;
   #pragma unroll
-          for (int w = 0; w < NW; ++w) mb = fmaxf(mb, redw[w]);
+          for (int w = hx * NWX; w < (hx + 1) * NWX; ++w) mb = fmaxf(mb, redw[w]);  // PAIR: its block's warps
           if (mb > 0.f && mb < FLT_MAX) aB = ilogbf(mb) - 12;  // Bs 2^-aB in [2^12, 2^13)
           const float f = pow2i(-aB);
   #pragma unroll
@@ -911,7 +978,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
             xi[u] *= f;
           }
         }
-        if (ch < NCH) {
+        if (ch < NCH && live) {
         uint32_t rh[CWD / 2], rl[CWD / 2], nh[CWD / 2], nl[CWD / 2], ih[CWD / 2], il[CWD / 2];
   #pragma unroll
         for (int v = 0; v < CWD / 2; ++v) {
@@ -984,6 +1051,30 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       // antenna m: TMEM lane m % 128 (warp quadrant warp % 4), tile m / 128
       const uint32_t cm = tmem + lrow + T::T_D2 + tile * 2 * R;
       const uint32_t cc = cm + R;
+      if constexpr (T::PAIR) {  // the thread's 8 users only
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+          float* w = part == 0 ? wr : wi;
+          float a[8], b[8];
+          tmem_ld8(cm + part * K + T::KX * hx, a);
+          tmem_ld8(cc + part * K + T::KX * hx, b);
+          tmem_wait<8>(a);
+          tmem_wait<8>(b);
+          if constexpr (RB) {
+            const float u2 = pow2i(aB - aW);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = fmaf(u2, fmaf(kLoScale, b[i], a[i]), w[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) {
+              const float2 t = fadd2(make_float2(w[i], w[i + 1]),
+                                     ffma2(kLoScale, make_float2(b[i], b[i + 1]), make_float2(a[i], a[i + 1])));
+              w[i] = t.x;
+              w[i + 1] = t.y;
+            }
+          }
+        }
+      } else {
 #pragma unroll
       for (int part = 0; part < 2; ++part) {
         float* w = part == 0 ? wr : wi;
@@ -1009,6 +1100,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
           }
         }
       }
+      }
     }
     tc_fence_before();
     // prox_l21 on the antenna column (strict '>', pgd.cpp:237-244 / unfolded.cpp:135-143)
@@ -1021,7 +1113,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
 #pragma unroll
     for (int i = 0; i < NS; ++i) s2p[i] = zero2();
 #pragma unroll
-    for (int k = 0; k < K; k += 2) {
+    for (int k = 0; k < KT; k += 2) {
       const float2 r2 = make_float2(wr[k], wr[k + 1]), i2 = make_float2(wi[k], wi[k + 1]);
       s2p[(k / 2) % NS] = __ffma2_rn(r2, r2, __ffma2_rn(i2, i2, s2p[(k / 2) % NS]));
     }
@@ -1037,7 +1129,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     const float r = rsqrt_ftz(fmaxf(s2, FLT_MIN));
     const float scale = on ? fmaf(-ts, r, 1.f) : 0.f;
 #pragma unroll
-    for (int k = 0; k < K; k += 2) {
+    for (int k = 0; k < KT; k += 2) {
       const float2 r2 = fmul2(scale, make_float2(wr[k], wr[k + 1])), i2 = fmul2(scale, make_float2(wi[k], wi[k + 1]));
       wr[k] = r2.x;
       wr[k + 1] = r2.y;
@@ -1059,10 +1151,12 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   // kernel, later in the stream, overwrites it)
   {
     const float gout = RB ? g * pow2i(aW) : g;
-    float4* wg = reinterpret_cast<float4*>(p.W + (rid * M + m) * K);
+    float4* wg = reinterpret_cast<float4*>(p.W + (rx * T::MX + ml) * KT);
+    if (xvalid) {
 #pragma unroll
-    for (int j = 0; j < K / 2; ++j)
-      stg_stream(wg + j, make_float4(wr[2 * j] * gout, wi[2 * j] * gout, wr[2 * j + 1] * gout, wi[2 * j + 1] * gout));
+      for (int j = 0; j < KT / 2; ++j)
+        stg_stream(wg + j, make_float4(wr[2 * j] * gout, wi[2 * j] * gout, wr[2 * j + 1] * gout, wi[2 * j + 1] * gout));
+    }
 #ifdef UFPGD_MMA_TIMING
     PSTAMP(6)
     if (probe) {
@@ -1097,7 +1191,9 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     __syncthreads();
   } else {
     const float sc_lo = (PGD ? eta_b : p.eta_lo) * p.cmax * g2inv, sc_hi = (PGD ? eta_b : p.eta_hi) * p.cmax * g2inv;
-    const bool range = !(sc_lo >= 0x1.0p-12f && sc_hi <= 0x1.0p12f);  // CTA-uniform
+    // (uniform per realization; an odd batch's phantom second realization —
+    // zero channel, g = 1 — must not send its real partner to the robust path)
+    const bool range = xvalid && !(sc_lo >= 0x1.0p-12f && sc_hi <= 0x1.0p12f);
     handoff = __syncthreads_or(nonfinite || range) != 0;
   }
   if (warp == 0) {
@@ -1110,20 +1206,21 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar1 + 8 * b) : "memory");
   }
   if (tid == 0 && handoff) redo_list[atomicAdd(redo_count, 1)] = static_cast<int>(rid);
-  if (tid == 0 && !handoff) {
-    for (int w = 1; w < NW; ++w) {
+  // each realization's first thread (PAIR: threads 0 and 64) combines its warps
+  if (tid == hx * NWX * 32 && !handoff && xvalid) {
+    for (int w = hx * NWX + 1; w < (hx + 1) * NWX; ++w) {
       fb = min(fb, fbs[w]);
       l21 += red[w];
       act += static_cast<int>(red[16 + w]);
     }
     const bool diverged = fb != LLONG_MAX;
-    if (p.diverged_at) p.diverged_at[rid] = diverged ? static_cast<int32_t>(fb + (PGD ? 1 : 0)) : -1;
-    if (p.l21) p.l21[rid] = diverged ? __int_as_float(0x7fc00000) : l21;
-    if (p.active) p.active[rid] = diverged ? -1 : act;
+    if (p.diverged_at) p.diverged_at[rx] = diverged ? static_cast<int32_t>(fb + (PGD ? 1 : 0)) : -1;
+    if (p.l21) p.l21[rx] = diverged ? __int_as_float(0x7fc00000) : l21;
+    if (p.active) p.active[rx] = diverged ? -1 : act;
     if (p.block_partials) {
-      p.block_partials[rid * 3 + 0] = diverged ? 0.0 : static_cast<double>(p.alpha) * l21;
-      p.block_partials[rid * 3 + 1] = diverged ? 0.0 : static_cast<double>(act);
-      p.block_partials[rid * 3 + 2] = diverged ? 1.0 : 0.0;
+      p.block_partials[rx * 3 + 0] = diverged ? 0.0 : static_cast<double>(p.alpha) * l21;
+      p.block_partials[rx * 3 + 1] = diverged ? 0.0 : static_cast<double>(act);
+      p.block_partials[rx * 3 + 2] = diverged ? 1.0 : 0.0;
     }
   }
   if (RB) __syncthreads();  // the reduction slots are reused by the next realization
@@ -1135,10 +1232,15 @@ using Mma_32_256 = MmaShape<32, 256, 1>;
 #define UFPGD_MMA16_MINB 4
 #endif
 using Mma_16_128 = MmaShape<16, 128, UFPGD_MMA16_MINB>;
+using Mma_8_64x2 = MmaShape<16, 128, UFPGD_MMA16_MINB, true>;
 
 template <class T>
 cudaError_t launch_mma_t(const FusedArgs& args, bool pgd, cudaStream_t s, long long* nblocks) {
   FusedArgs a = args;  // + the range summary the fast path checks once per realization
+  if constexpr (T::PAIR) {
+    if (pgd) return cudaErrorInvalidValue;  // PGD at (8,64) runs on the FFMA2 team kernel
+    for (int k = T::KX; k < T::K; ++k) a.c[k] = a.c[k - T::KX];  // c of the pair frame: [c; c]
+  }
   a.cmax = 0.f;
   for (int k = 0; k < T::K; ++k) a.cmax = std::max(a.cmax, std::fabs(a.c[k]));
   a.eta_lo = FLT_MAX;
@@ -1147,8 +1249,15 @@ cudaError_t launch_mma_t(const FusedArgs& args, bool pgd, cudaStream_t s, long l
     a.eta_lo = std::min(a.eta_lo, std::fabs(a.eta[l]));
     a.eta_hi = std::max(a.eta_hi, std::fabs(a.eta[l]));
   }
-  auto kern = pgd ? mma_kernel<T, true, false> : mma_kernel<T, false, false>;
-  auto robust = pgd ? mma_kernel<T, true, true> : mma_kernel<T, false, true>;
+  void (*kern)(FusedArgs, int*, int*) = mma_kernel<T, false, false>;
+  void (*robust)(FusedArgs, int*, int*) = mma_kernel<T, false, true>;
+  if constexpr (!T::PAIR) {
+    if (pgd) {
+      kern = mma_kernel<T, true, false>;
+      robust = mma_kernel<T, true, true>;
+    }
+  }
+  const long long ncta = T::PAIR ? (a.B + 1) / 2 : a.B;  // CTAs (PAIR: two realizations each)
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(robust, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
   if (e != cudaSuccess) return e;
@@ -1165,10 +1274,10 @@ cudaError_t launch_mma_t(const FusedArgs& args, bool pgd, cudaStream_t s, long l
     a.prefetch_ahead = static_cast<long long>(sms) * fast_per_sm;
   }
   int* list = nullptr;
-  if ((e = scratch_alloc_async(reinterpret_cast<void**>(&list), sizeof(int) * (a.B + 1), s)) != cudaSuccess)
+  if ((e = scratch_alloc_async(reinterpret_cast<void**>(&list), sizeof(int) * (ncta + 1), s)) != cudaSuccess)
     return e;
   if ((e = cudaMemsetAsync(list, 0, sizeof(int), s)) == cudaSuccess) {
-    kern<<<static_cast<unsigned>(a.B), T::NT, T::SMEM, s>>>(a, list + 1, list);
+    kern<<<static_cast<unsigned>(ncta), T::NT, T::SMEM, s>>>(a, list + 1, list);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) {
@@ -1178,7 +1287,7 @@ cudaError_t launch_mma_t(const FusedArgs& args, bool pgd, cudaStream_t s, long l
     int per_sm = 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, robust, T::NT, T::SMEM) != cudaSuccess || per_sm < 1)
       per_sm = 1;
-    const long long grid = std::min<long long>(a.B, static_cast<long long>(sms) * per_sm);
+    const long long grid = std::min<long long>(ncta, static_cast<long long>(sms) * per_sm);
     robust<<<static_cast<unsigned>(grid), T::NT, T::SMEM, s>>>(a, list + 1, list);
     e = cudaGetLastError();
   }
@@ -1191,14 +1300,17 @@ cudaError_t launch_mma_t(const FusedArgs& args, bool pgd, cudaStream_t s, long l
 // Unfolded forward and fixed-step PGD at (16,128), (32,256);
 // ufpgd_gpu_set_option(UFPGD_OPT_TENSOR_CORES, 0) selects the CUDA-core tile
 // kernel for A/B runs.
+// (8,64) (BASELINE config 2, unfolded forward only): realization pairs in the
+// (16,128) frame; the fixed-step PGD there stays on the FFMA2 team kernel.
 bool mma_supported(int K, int M, bool pgd) {
-  if (!((K == 32 && M == 256) || (K == 16 && M == 128))) return false;
+  if (!((K == 32 && M == 256) || (K == 16 && M == 128) || (K == 8 && M == 64 && !pgd))) return false;
   return option(UFPGD_OPT_TENSOR_CORES) != 0;
 }
 
 cudaError_t launch_mma(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s, long long* nblocks) {
   if (K == 32 && M == 256) return launch_mma_t<Mma_32_256>(a, pgd, s, nblocks);
   if (K == 16 && M == 128) return launch_mma_t<Mma_16_128>(a, pgd, s, nblocks);
+  if (K == 8 && M == 64) return launch_mma_t<Mma_8_64x2>(a, pgd, s, nblocks);
   return cudaErrorInvalidValue;
 }
 

@@ -786,7 +786,7 @@ int fused_realizations_per_block(int K, int M) {
   if (K == 4 && M == 32) return Team_4_32w::R;  // the smaller of the two (4,32) teams' R
   if (K == 4 && M == 64) return Team_4_64::R;
   if (K == 8 && M == 32) return Team_8_32::R;
-  if (K == 8 && M == 64) return Team_8_64::R;
+  if (K == 8 && M == 64) return 1;  // the tcgen05 pair kernel writes one partial per realization
   if (K == 8 && M == 128) return Team_8_128::R;
   return 1;  // tile kernels: one realization per block
 }
@@ -802,7 +802,10 @@ cudaError_t launch_fused(const FusedArgs& a, bool pgd, int K, int M, cudaStream_
   }
   if (K == 4 && M == 64) return launch_team<Team_4_64>(a, pgd, s, nblocks);
   if (K == 8 && M == 32) return launch_team<Team_8_32>(a, pgd, s, nblocks);
-  if (K == 8 && M == 64) return launch_team<Team_8_64>(a, pgd, s, nblocks);
+  if (K == 8 && M == 64) {
+    if (mma_supported(K, M, pgd)) return launch_mma(a, pgd, K, M, s, nblocks);  // mma.cu: realization pairs
+    return launch_team<Team_8_64>(a, pgd, s, nblocks);
+  }
   if (K == 8 && M == 128) return launch_team<Team_8_128>(a, pgd, s, nblocks);
   return launch_tiled(a, pgd, K, M, s, nblocks);  // tile.cu: (16,128), (32,256)
 }

@@ -1,0 +1,40 @@
+"""Config 2 on the tcgen05 realization-pair kernel vs the FFMA2 team kernel
+(ufpgd_gpu_set_option(UFPGD_OPT_TENSOR_CORES, 0)): CUDA-graph timing, outputs
+compared (development aid)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2304_12745_b200 as U
+
+w = U.CONFIGS[2]
+B = int(sys.argv[1]) if len(sys.argv) > 1 else w.B
+H = U.generate_channels_device(w.seed_h, w.seed_g, w.gain_db, 0, B, w.K, w.M)
+lam, eta = w.layer_params()
+
+
+def timeit(fn, reps=20):
+    fn(); torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    best = 1e9
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            g.replay()
+        b.record(); torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b) / reps)
+    return best
+
+
+res = {}
+for tc in (1, 0):
+    U.set_option("tensor_cores", tc)
+    W = torch.empty_like(H)
+    t = timeit(lambda: U.unfolded_forward(H, lam, eta, w.c, out=W))
+    res[tc] = (t, W.clone())
+    print(f"tensor cores {tc}: {t:.3f} ms ({B / t / 1e3:.2f} M/s)", flush=True)
+U.set_option("tensor_cores", 1)
+d = (res[1][1] - res[0][1]).abs().flatten(1).norm(dim=1) / res[0][1].abs().flatten(1).norm(dim=1).clamp_min(1e-30)
+print(f"pair vs team: W rel diff max {d.max().item():.2e} median {d.median().item():.2e}; ratio {res[1][0] / res[0][0]:.3f}")
