@@ -531,8 +531,22 @@ def run_ours(args, world, rank, local):
         cfg = config_dict(w, world, B, total, scaling)
         cfg["layers_eta_clamped_by_projection"] = clamped_layers(w)
         cfg["step"] = step_mode
-        kname = ("mma_kernel<MmaShape<16,128>> (tcgen05)" if w.config == 5
-                 else "fused_kernel<Team<8,64,4,4>> (+stats_finalize)")
+        tensor_path = U.get_option("tensor_cores") != 0 and w.tensor_flops_per_realization() is not None
+        if w.config == 5:
+            kname = "mma_kernel<MmaShape<16,128>> (tcgen05)"
+        elif tensor_path:
+            kname = "mma_kernel<MmaShape<16,128,PAIR>> (tcgen05, (8,64) realization pairs) (+stats_finalize)"
+        else:
+            kname = "fused_kernel<Team<8,64,4,4>> (+stats_finalize)"
+        tensor = None
+        if tensor_path:
+            tfl = w.tensor_flops_per_realization() * B
+            tensor = {"achieved": tfl / (kern_ms * 1e-3) / 1e12, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                      "frac": tfl / (kern_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+                      "flops_per_launch": tfl, "peak_source": peaks["source"] + " bf16_tflops",
+                      "note": "f16 tensor-core work the kernel issues (3-term split: ~3x the FP32-equivalent "
+                              "contractions, block-diagonal pairs: 2x more); the CUDA-core epilogues between "
+                              "the MMAs, not the tensor pipe, set the rate"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_total / args.steps, "higher_is_better": True,
@@ -552,7 +566,12 @@ def run_ours(args, world, rank, local):
                                       "X' = -diag(c) makes the second a per-entry scaling)"},
                 "probe_peak": {"tflops": probe_tflops, "sm_ghz": probe_ghz,
                                "frac": achieved / probe_tflops,
-                               "note": "live FFMA2 outer-product probe (the kernel's instruction form)"},
+                               "note": "live FFMA2 outer-product probe (the FFMA2 team kernel's instruction form)"},
+                "executed_on": ("tensor cores (tcgen05.mma kind::f16, TMEM accumulators, 3-term f16 split) + "
+                                "CUDA-core epilogues: frac counts SURVEY 8d's FP32-equivalent work against the "
+                                "nominal FP32 FMA peak (the north_star's roofline) and can exceed the FFMA2 probe"
+                                if tensor_path else "CUDA cores (FFMA2)"),
+                "tensor": tensor,
                 "hbm": {"achieved_GBps": hbm_bytes / (kern_ms * 1e-3) / 1e9, "peak_GBps": peaks["hbm_gbs"],
                         "frac": hbm_bytes / (kern_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                         "bytes_per_launch": hbm_bytes, "peak_source": peaks["source"] + " hbm_gbs"},
@@ -567,7 +586,7 @@ def run_ours(args, world, rank, local):
                     "synchronous_path": "ufpgd_gpu_unfolded_forward_host, one blocking call per step"},
             # per step: the forward kernel (+ the tcgen05 path's range-robust
             # instance, which exits at once when nothing is handed off) and stats_finalize
-            "gpu_launches": (3 if w.config == 5 else 2) * args.steps,
+            "gpu_launches": (3 if (w.config == 5 or tensor_path) else 2) * args.steps,
             "clocks": clocks.report(),
             "stats": sharding.summarize(stats, total),
             "other_configs": others,
