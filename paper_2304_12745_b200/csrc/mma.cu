@@ -332,11 +332,12 @@ __device__ __forceinline__ float pow2i(int e) { return __int_as_float((127 + e) 
 // 30-step rule), FP32 on the unscaled H, one thread per antenna:
 // u = H^* v reduced over the CTA (shuffles, then per-warp partials in `scr`),
 // w_m = sum_k H(k, m) u_k in-thread, Rayleigh quotient Re(v^H w) of the last step.
+// PAIR: each realization over its own half of the CTA (its users, its warps).
 template <class T>
-__device__ float cta_power(const float4 (&hv)[T::K / 2], const float2* v0, int steps, float* scr, float* red,
-                           int warp, int lane) {
-  constexpr int K = T::K, NW = T::NW;
-  const int m = threadIdx.x;
+__device__ float cta_power(const float4 (&hv)[T::KX / 2], const float2* v0, int steps, float* scr, float* red,
+                           int warp, int lane, int hx) {
+  constexpr int K = T::KX, NWX = T::PAIR ? T::NW / 2 : T::NW;
+  const int m = threadIdx.x % T::MX;  // the antenna within the thread's realization
   float2 v = v0[m];
   float est = 0.f;
   bool zero = false;
@@ -361,7 +362,7 @@ __device__ float cta_power(const float4 (&hv)[T::K / 2], const float2* v0, int s
     for (int i = 0; i < 2 * K; ++i) {
       float a = 0.f;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) a += scr[w * 2 * K + i];
+      for (int w = hx * NWX; w < (hx + 1) * NWX; ++w) a += scr[w * 2 * K + i];
       u[i] = a;
     }
     float2 wm = make_float2(0.f, 0.f);
@@ -385,7 +386,7 @@ __device__ float cta_power(const float4 (&hv)[T::K / 2], const float2* v0, int s
     dot = 0.f;
     wn2 = 0.f;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
+    for (int w = hx * NWX; w < (hx + 1) * NWX; ++w) {
       dot += red[w];
       wn2 += red[16 + w];
     }
@@ -669,12 +670,13 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   float eta_b = 0.f, thr_b = 0.f;  // PGD: the realization's fixed step 1/L and threshold lambda/L
   if constexpr (PGD) {
     if (p.eta_in) {
-      eta_b = p.eta_in[rid];
+      eta_b = xvalid ? p.eta_in[rx] : 1.f;
     } else {
-      eta_b = 1.f / cta_power<T>(hv, p.v0, p.power_steps, F, red, warp, lane);  // F: free before stage 1
+      eta_b = 1.f / cta_power<T>(hv, p.v0, p.power_steps, F, red, warp, lane, hx);  // F: free before stage 1
+      if (!xvalid) eta_b = 1.f;  // phantom partner (zero channel: L = 0)
     }
     thr_b = p.lambda * eta_b;
-    if (p.eta_out && tid == 0) p.eta_out[rid] = eta_b;
+    if (p.eta_out && tid == hx * (T::NT / (T::PAIR ? 2 : 1)) && xvalid) p.eta_out[rx] = eta_b;
   }
   PSTAMP(4)
   for (long long l = 0; l < p.L; ++l) {
@@ -1238,7 +1240,7 @@ template <class T>
 cudaError_t launch_mma_t(const FusedArgs& args, bool pgd, cudaStream_t s, long long* nblocks) {
   FusedArgs a = args;  // + the range summary the fast path checks once per realization
   if constexpr (T::PAIR) {
-    if (pgd) return cudaErrorInvalidValue;  // PGD at (8,64) runs on the FFMA2 team kernel
+    if (pgd && a.residual_tol > 0.f) return cudaErrorInvalidValue;  // early stop: FFMA2 team kernel
     for (int k = T::KX; k < T::K; ++k) a.c[k] = a.c[k - T::KX];  // c of the pair frame: [c; c]
   }
   a.cmax = 0.f;
@@ -1249,14 +1251,8 @@ cudaError_t launch_mma_t(const FusedArgs& args, bool pgd, cudaStream_t s, long l
     a.eta_lo = std::min(a.eta_lo, std::fabs(a.eta[l]));
     a.eta_hi = std::max(a.eta_hi, std::fabs(a.eta[l]));
   }
-  void (*kern)(FusedArgs, int*, int*) = mma_kernel<T, false, false>;
-  void (*robust)(FusedArgs, int*, int*) = mma_kernel<T, false, true>;
-  if constexpr (!T::PAIR) {
-    if (pgd) {
-      kern = mma_kernel<T, true, false>;
-      robust = mma_kernel<T, true, true>;
-    }
-  }
+  auto kern = pgd ? mma_kernel<T, true, false> : mma_kernel<T, false, false>;
+  auto robust = pgd ? mma_kernel<T, true, true> : mma_kernel<T, false, true>;
   const long long ncta = T::PAIR ? (a.B + 1) / 2 : a.B;  // CTAs (PAIR: two realizations each)
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(robust, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
@@ -1300,10 +1296,11 @@ cudaError_t launch_mma_t(const FusedArgs& args, bool pgd, cudaStream_t s, long l
 // Unfolded forward and fixed-step PGD at (16,128), (32,256);
 // ufpgd_gpu_set_option(UFPGD_OPT_TENSOR_CORES, 0) selects the CUDA-core tile
 // kernel for A/B runs.
-// (8,64) (BASELINE config 2, unfolded forward only): realization pairs in the
-// (16,128) frame; the fixed-step PGD there stays on the FFMA2 team kernel.
+// (8,64) (BASELINE configs 2 and 3): realization pairs in the (16,128) frame
+// (solve_pgd's residual_tol early stop stays on the FFMA2 team kernel).
 bool mma_supported(int K, int M, bool pgd) {
-  if (!((K == 32 && M == 256) || (K == 16 && M == 128) || (K == 8 && M == 64 && !pgd))) return false;
+  (void)pgd;
+  if (!((K == 32 && M == 256) || (K == 16 && M == 128) || (K == 8 && M == 64))) return false;
   return option(UFPGD_OPT_TENSOR_CORES) != 0;
 }
 

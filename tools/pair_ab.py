@@ -38,3 +38,17 @@ for tc in (1, 0):
 U.set_option("tensor_cores", 1)
 d = (res[1][1] - res[0][1]).abs().flatten(1).norm(dim=1) / res[0][1].abs().flatten(1).norm(dim=1).clamp_min(1e-30)
 print(f"pair vs team: W rel diff max {d.max().item():.2e} median {d.median().item():.2e}; ratio {res[1][0] / res[0][0]:.3f}")
+
+if len(sys.argv) > 2 and sys.argv[2] == "pgd":  # config 3: PGD-5000 (+ in-kernel 30-step power iteration)
+    w3 = U.CONFIGS[3]
+    H3 = U.generate_channels_device(w3.seed_h, w3.seed_g, w3.gain_db, 0, w3.B, w3.K, w3.M)
+    r3 = {}
+    for tc in (1, 0):
+        U.set_option("tensor_cores", tc)
+        t = timeit(lambda: U.pgd_fixed(H3, w3.lambda_pgd, w3.L, w3.c), reps=2)
+        r3[tc] = (t, U.pgd_fixed(H3, w3.lambda_pgd, w3.L, w3.c)["W"].clone())
+        print(f"cfg3 tensor cores {tc}: {t:.3f} ms", flush=True)
+    U.set_option("tensor_cores", 1)
+    d = (r3[1][1] - r3[0][1]).abs().flatten(1).norm(dim=1) / r3[0][1].abs().flatten(1).norm(dim=1).clamp_min(1e-30)
+    print(f"cfg3 pair vs team: W rel diff max {d.max().item():.2e} median {d.median().item():.2e}; "
+          f"ratio {r3[1][0] / r3[0][0]:.3f}")
