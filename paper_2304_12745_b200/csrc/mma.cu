@@ -642,6 +642,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   }
 
   constexpr uint32_t IDESC1 = idesc_f16_amn<Q, 2 * R>();
+  constexpr uint32_t IDESC1P = idesc_f16_amn<Q, R>();  // PAIR: per-realization N = 32
   constexpr uint32_t IDESC2W = idesc_f16_ak<128, 2 * R>();  // A = H from TMEM (K-major)
   constexpr uint32_t IDESC2 = idesc_f16_ak<128, R>();
   static_assert(T::OFF_HL == T::OFF_HH + (R / 8) * 16 * M && T::OFF_BL == T::OFF_BH + (R / 8) * T::BSBO,
@@ -742,6 +743,21 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         constexpr int KST = 128 / 16;  // K-steps per antenna tile
         const uint32_t sw = sb + T::OFF_W + tu * KST * 2 * 16 * Q, sh = sb + T::OFF_HH + tu * KST * 256;
         const uint32_t alo = sdesc_lo(sw, 16 * Q), blo = sdesc_lo(sh, 128);
+        if constexpr (T::PAIR) {
+          // one chain per realization over its own 64 antennas (K-steps 4x ..
+          // 4x + 3) and its own N = 32 H columns — every other 8-row N-group
+          // of [H_hi | H_lo] (SBO doubled) — into D1 columns [32 x, 32 x + 32):
+          // [hi p0 | hi p1 | lo p0 | lo p1] of its 8 users. The block-diagonal
+          // frame's zero blocks (half the stage-1 MACs and of its H reads) are
+          // never multiplied.
+          constexpr int KX4 = T::MX / 16;  // K-steps per realization
+#pragma unroll
+          for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int i = 0; i < KX4; ++i)
+              umma_f16w(tmem + T::T_D1A + 32 * x, alo + (x * KX4 + i) * (2 * 16 * Q >> 4), sdesc_hi(128),
+                        blo + (x * KX4 + i) * (256 >> 4) + x * (16 * M >> 4), sdesc_hi(2 * 16 * M), IDESC1P, i > 0);
+        } else {
 #pragma unroll
         for (int i = 0; i < KST; ++i) {
           // B = [H_hi | H_lo] (N = 2R: OFF_HL continues OFF_HH's N-group stride)
@@ -751,6 +767,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
           else
             umma_f16(tmem + T::T_D1A, sdesc(sw + i * 2 * 16 * Q, 16 * Q, 128), sdesc(sh + i * 256, 128, 16 * M),
                      IDESC1, tu > 0 || i > 0);
+        }
         }
         umma_commit(bar1 + 8 * tu);
       }
@@ -776,29 +793,54 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         // column pairs 8 j + 2 (i % 4)), so no lane loads or combines the 16
         // unused lanes of the 32x32b shape (half the LDTM and FP32x2 work).
         static_assert(T::NTILE == 1 && CW == 2 * R / 2 && T::CWD == 2, "");
+        const int kr = lane >> 2, cp = 2 * (lane & 3);
+        float* d0 = (quad < 2 ? F : G) + (part * K + kr) * T::FSTR + cp;
         float a[16], b[16];
+        if constexpr (T::PAIR) {
+          // D1 columns [32 x, +32) hold realization x's [hi p0 | hi p1 | lo p0 |
+          // lo p1]: row kr (a) lives in the first load's blocks, row kr + 8 (b)
+          // in the second's (their other rows are the frame's zeros). F / G get
+          // the same entries as the full-frame layout: (row kr, columns cp, K + cp),
+          // (row kr + 8, columns 8 + cp, K + 8 + cp).
+          tmem_ld16x256(tmem + lrow + T::T_D1A, a);
+          tmem_ld16x256(tmem + lrow + T::T_D1A + 32, b);
+          tmem_wait<16>(a);
+          tmem_wait<16>(b);
+          float2 v[4];  // (row kr: p'0, p'1), (row kr + 8: p'0, p'1)
+          const float2 h0 = make_float2(a[0], a[1]), h1 = make_float2(a[4], a[5]);
+          const float2 h2 = make_float2(b[2], b[3]), h3 = make_float2(b[6], b[7]);
+          if (quad < 2) {  // hi W rows: W_hi H_hi + 2^-11 W_hi H_lo
+            v[0] = ffma2(kLoScale, make_float2(a[8], a[9]), h0);
+            v[1] = ffma2(kLoScale, make_float2(a[12], a[13]), h1);
+            v[2] = ffma2(kLoScale, make_float2(b[10], b[11]), h2);
+            v[3] = ffma2(kLoScale, make_float2(b[14], b[15]), h3);
+          } else {         // lo W rows: 2^-11 W_lo H_hi
+            v[0] = fmul2(kLoScale, h0);
+            v[1] = fmul2(kLoScale, h1);
+            v[2] = fmul2(kLoScale, h2);
+            v[3] = fmul2(kLoScale, h3);
+          }
+          *reinterpret_cast<float2*>(d0) = v[0];
+          *reinterpret_cast<float2*>(d0 + K) = v[1];
+          *reinterpret_cast<float2*>(d0 + 8 * T::FSTR + 8) = v[2];
+          *reinterpret_cast<float2*>(d0 + 8 * T::FSTR + K + 8) = v[3];
+        } else {
         tmem_ld16x256(tmem + lrow + T::T_D1A, a);
         if (quad < 2) tmem_ld16x256(tmem + lrow + T::T_D1B, b);
         tmem_wait<16>(a);
         if (quad < 2) tmem_wait<16>(b);
-        // PAIR: only the diagonal blocks of X are needed — row kr (realization
-        // a) with column blocks j = 0, 2, row kr + 8 (b) with j = 1, 3
 #pragma unroll
         for (int i = 0; i < 16; i += 2) {
-          if (T::PAIR && i != 0 && i != 6 && i != 8 && i != 14) continue;
           const float2 t = quad < 2 ? ffma2(kLoScale, make_float2(b[i], b[i + 1]), make_float2(a[i], a[i + 1]))
                                     : fmul2(kLoScale, make_float2(a[i], a[i + 1]));
           a[i] = t.x;
           a[i + 1] = t.y;
         }
-        const int kr = lane >> 2, cp = 2 * (lane & 3);
-        float* d0 = (quad < 2 ? F : G) + (part * K + kr) * T::FSTR + cp;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          if (!T::PAIR || j % 2 == 0)
-            *reinterpret_cast<float2*>(d0 + 8 * j) = make_float2(a[4 * j], a[4 * j + 1]);
-          if (!T::PAIR || j % 2 == 1)
-            *reinterpret_cast<float2*>(d0 + 8 * T::FSTR + 8 * j) = make_float2(a[4 * j + 2], a[4 * j + 3]);
+          *reinterpret_cast<float2*>(d0 + 8 * j) = make_float2(a[4 * j], a[4 * j + 1]);
+          *reinterpret_cast<float2*>(d0 + 8 * T::FSTR + 8 * j) = make_float2(a[4 * j + 2], a[4 * j + 3]);
+        }
         }
       } else {
       float* dst = (quad < 2 ? F : G) + (part * K + lane) * T::FSTR + c0;
