@@ -141,6 +141,23 @@ struct MmaShape {
   static __device__ __forceinline__ int boff(int kk, int n) {
     return (kk >> 3) * 128 + (n >> 3) * BSBO + (n & 7) * 16 + (kk & 7) * 2;
   }
+  // PAIR: stage 2 runs one K-step per realization x (the TMEM A operand's
+  // K order is r' = (x, part, k_local)), so Bs is one tile per realization:
+  // [16 K-rows (p_in, k'_local) x 32 N-columns ((p_out, k_local) hi | lo)],
+  // K-major, N-group stride BSBOP, tile x at x * BST, lo after the 2 hi N-groups.
+  static constexpr int BSBOP = 2 * 128, BST = 4 * BSBOP;
+  static __device__ __forceinline__ int boffp(int kk, int n) {
+    return (kk >> 3) * 128 + (n >> 3) * BSBOP + (n & 7) * 16 + (kk & 7) * 2;
+  }
+  // Byte offset from OFF_BH of the (p_in, p_out) Bs entry of X'(k, c .. c+CWD-1)
+  // (frame users k, c), and of its lo part from its hi part.
+  static __device__ __forceinline__ int bpos(int pin, int pout, int k, int c) {
+    if constexpr (PAIR)
+      return (k / KX) * BST + boffp(pin * KX + c % KX, pout * KX + k % KX);
+    else
+      return boff(pin * K + c, pout * K + k);
+  }
+  static constexpr int BLO = PAIR ? 2 * BSBOP : (R / 8) * BSBO;
 };
 
 // ---- PTX wrappers -------------------------------------------------------------
@@ -579,8 +596,10 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         const int r = half * 32 + 2 * c;  // rows r, r + 1: one part, users k, k + 1 (K even)
-        const int part = r / K, k = r % K;
-        // PAIR: the other realization's users at this antenna are zeros
+        // PAIR: K order r' = (x, part, k_local), one K-step per realization; the
+        // other realization's users at this antenna are zeros
+        const int part = T::PAIR ? (r % 16) / 8 : r / K;
+        const int k = T::PAIR ? (r / 16) * T::KX + r % 8 : r % K;
         const bool own = !T::PAIR || k / T::KX == hx;
         const float4 hq = own ? hv[(k % T::KX) / 2] : make_float4(0.f, 0.f, 0.f, 0.f);
         split2((part == 0 ? hq.x : hq.y) * g, (part == 0 ? hq.z : hq.w) * g, hh[c], hl[c]);
@@ -622,29 +641,15 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
 #pragma unroll
     for (int k = 0; k < KT; ++k) wn2 = fmaf(wr[k], wr[k], fmaf(wi[k], wi[k], wn2));
   }
-  if constexpr (T::PAIR) {
-    // the off-diagonal zeros, written once: the W operand rows of the other
-    // realization's users at this antenna, and the whole Bs (its diagonal
-    // blocks are rewritten every layer); ordered before the first MMAs by the
-    // fenced barriers of layer 0
-#pragma unroll
-    for (int hl = 0; hl < 2; ++hl)
-#pragma unroll
-      for (int part = 0; part < 2; ++part)
-        *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(hl * R + part * K + T::KX * (1 - hx), m)) =
-            make_uint4(0u, 0u, 0u, 0u);
-    constexpr int BSB = 2 * (R / 8) * T::BSBO;  // Bs hi + lo bytes
-    static_assert(BSB % (16 * T::NT) == 0, "");
-#pragma unroll
-    for (int i = 0; i < BSB / (16 * T::NT); ++i)
-      *reinterpret_cast<uint4*>(smem + T::OFF_BH + 16 * (tid + i * T::NT)) = make_uint4(0u, 0u, 0u, 0u);
-    __syncthreads();  // before layer 0's Bs build writes the diagonal blocks (no split barrier at W0 = 0)
-  }
+  // (PAIR: no zero blocks to write — each realization's stage-1 chain and
+  // stage-2 K-step read only its own operand rows and Bs tile, and the drains
+  // read only its own D1 / D2 columns)
 
   constexpr uint32_t IDESC1 = idesc_f16_amn<Q, 2 * R>();
   constexpr uint32_t IDESC1P = idesc_f16_amn<Q, R>();  // PAIR: per-realization N = 32
   constexpr uint32_t IDESC2W = idesc_f16_ak<128, 2 * R>();  // A = H from TMEM (K-major)
   constexpr uint32_t IDESC2 = idesc_f16_ak<128, R>();
+  constexpr uint32_t IDESC2PW = idesc_f16_ak<128, 32>(), IDESC2P = idesc_f16_ak<128, 16>();  // PAIR
   static_assert(T::OFF_HL == T::OFF_HH + (R / 8) * 16 * M && T::OFF_BL == T::OFF_BH + (R / 8) * T::BSBO,
                 "lo operands continue the hi ones along N");
   float* F = reinterpret_cast<float*>(smem + T::OFF_F);
@@ -942,14 +947,14 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
           else
             *reinterpret_cast<uint32_t*>(smem + off) = v[0];
         };
-        put(T::OFF_BH + T::boff(c, k), rh);
-        put(T::OFF_BL + T::boff(c, k), rl);
-        put(T::OFF_BH + T::boff(K + c, k), ih);
-        put(T::OFF_BL + T::boff(K + c, k), il);
-        put(T::OFF_BH + T::boff(c, K + k), ih);
-        put(T::OFF_BL + T::boff(c, K + k), il);
-        put(T::OFF_BH + T::boff(K + c, K + k), nh);
-        put(T::OFF_BL + T::boff(K + c, K + k), nl);
+        put(T::OFF_BH + T::bpos(0, 0, k, c), rh);
+        put(T::OFF_BH + T::BLO + T::bpos(0, 0, k, c), rl);
+        put(T::OFF_BH + T::bpos(1, 0, k, c), ih);
+        put(T::OFF_BH + T::BLO + T::bpos(1, 0, k, c), il);
+        put(T::OFF_BH + T::bpos(0, 1, k, c), ih);
+        put(T::OFF_BH + T::BLO + T::bpos(0, 1, k, c), il);
+        put(T::OFF_BH + T::bpos(1, 1, k, c), nh);
+        put(T::OFF_BH + T::BLO + T::bpos(1, 1, k, c), nl);
       }
     } else {
       constexpr int CWD = T::CWD, NCH = K * K / CWD, CPR = K / CWD;
@@ -1038,14 +1043,14 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
           else
             *reinterpret_cast<uint32_t*>(smem + off) = v[0];
         };
-        put(T::OFF_BH + T::boff(c, k), rh);
-        put(T::OFF_BL + T::boff(c, k), rl);
-        put(T::OFF_BH + T::boff(K + c, k), ih);
-        put(T::OFF_BL + T::boff(K + c, k), il);
-        put(T::OFF_BH + T::boff(c, K + k), ih);
-        put(T::OFF_BL + T::boff(c, K + k), il);
-        put(T::OFF_BH + T::boff(K + c, K + k), nh);
-        put(T::OFF_BL + T::boff(K + c, K + k), nl);
+        put(T::OFF_BH + T::bpos(0, 0, k, c), rh);
+        put(T::OFF_BH + T::BLO + T::bpos(0, 0, k, c), rl);
+        put(T::OFF_BH + T::bpos(1, 0, k, c), ih);
+        put(T::OFF_BH + T::BLO + T::bpos(1, 0, k, c), il);
+        put(T::OFF_BH + T::bpos(0, 1, k, c), ih);
+        put(T::OFF_BH + T::BLO + T::bpos(0, 1, k, c), il);
+        put(T::OFF_BH + T::bpos(1, 1, k, c), nh);
+        put(T::OFF_BH + T::BLO + T::bpos(1, 1, k, c), nl);
         }
       }
     }
@@ -1066,6 +1071,16 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       const uint32_t dm = tmem + T::T_D2 + t * 2 * R, dc = dm + R;
       const uint32_t ta = tmem + T::T_HA + t * R;  // H_hi columns; H_lo at + R / 2
       const uint32_t bhlo = sdesc_lo(sb + T::OFF_BH, 128);
+      if constexpr (T::PAIR) {
+        // realization x: its K-step of A (8 TMEM columns of H hi / lo) against its
+        // Bs tile, into D2 columns [32 x, +32) = [main hh | main hl + corr]
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          const uint32_t bx = bhlo + x * (T::BST >> 4);
+          umma_f16_ta(dm + 32 * x, ta + x * 8, bx, sdesc_hi(T::BSBOP), IDESC2PW, 0);
+          umma_f16_ta(dm + 32 * x + 16, ta + R / 2 + x * 8, bx, sdesc_hi(T::BSBOP), IDESC2P, 1);
+        }
+      } else
 #pragma unroll
       for (int ks = 0; ks < R / 16; ++ks) {
         // [main | corr] = H_hi [Bs_hi | Bs_lo] (N = 2R spans both), then corr += H_lo Bs_hi;
@@ -1100,8 +1115,8 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         for (int part = 0; part < 2; ++part) {
           float* w = part == 0 ? wr : wi;
           float a[8], b[8];
-          tmem_ld8(cm + part * K + T::KX * hx, a);
-          tmem_ld8(cc + part * K + T::KX * hx, b);
+          tmem_ld8(cm + 32 * hx + 8 * part, a);       // D2 [main hh | main hl + corr] of realization hx
+          tmem_ld8(cm + 32 * hx + 16 + 8 * part, b);
           tmem_wait<8>(a);
           tmem_wait<8>(b);
           if constexpr (RB) {
