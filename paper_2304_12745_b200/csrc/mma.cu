@@ -47,10 +47,11 @@ namespace {
 // PAIR: the (16,128) frame holds two (8,64) realizations block-diagonally
 // (BASELINE config 2's shape): H_pair = diag(H_a, H_b), so X, X' H^* and the
 // per-antenna prox never mix the blocks. Thread m works on antenna m % 64 of
-// realization m / 64 and holds only its realization's 8 users; the
-// off-diagonal operand blocks (W rows of the other users at its antenna, Bs)
-// are zeros written once, so the split, drain, Bs build and prox do half the
-// (16,128) kernel's work for the same MMAs.
+// realization m / 64 and holds only its realization's 8 users. Each
+// realization's MMAs touch only its own operand blocks (stage 1: one N = 32
+// chain over its antennas and H rows; stage 2: one K-step against its own Bs
+// tile), and the split, drains, Bs build and prox cover only its 8 users: the
+// frame's off-diagonal blocks are never staged, multiplied or read.
 template <int K_, int M_, int MINB_, bool PAIR_ = false>
 struct MmaShape {
   static constexpr int K = K_, M = M_, NT = M_, MINB = MINB_;
@@ -76,13 +77,11 @@ struct MmaShape {
   // fp32 exchange rows (floats): 4 mod 32 words at CWD 4, 8 mod 32 at CWD 2 (see chunk())
   static constexpr int FSTR = R + (CWD == 4 ? 4 : 8);
   // F [R][FSTR] (hi rows of P) and G (lo rows) alias the W operand: they are
-  // written after the stage-1 MMAs retire and read before W is rewritten (PAIR:
-  // their own region, as the W operand's zero rows are written only once).
-  static constexpr int OFF_X = OFF_BL + (R / 8) * BSBO;
-  static constexpr int OFF_F = PAIR ? OFF_X : OFF_W;
+  // written after the stage-1 MMAs retire and read before W is rewritten.
+  static constexpr int OFF_F = OFF_W;
   static constexpr int OFF_G = OFF_F + R * FSTR * 4;
   static_assert(2 * R * FSTR * 4 <= Q * M * 2, "");
-  static constexpr int OFF_BAR = PAIR ? OFF_X + 2 * R * FSTR * 4 : OFF_X;  // mbarriers, TMEM slot, reductions
+  static constexpr int OFF_BAR = OFF_BL + (R / 8) * BSBO;  // mbarriers, TMEM slot, reductions
   static constexpr int SMEM = OFF_BAR + 512;
   // TMEM columns (fp32 accumulators)
   // D1: [X-part with H_hi | with H_lo] (2R columns; each antenna tile's K-steps
@@ -304,6 +303,12 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
                : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
                : "r"(taddr));
 }
+// 8 registers per thread -> 8 consecutive TMEM columns of this warp's 32 lanes.
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
 // 16 registers per thread -> 16 consecutive TMEM columns of this warp's 32 lanes.
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
   asm volatile(
@@ -510,7 +515,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     const int it = tid + q * T::NT, j = it % NJ, G = it / NJ;
     if constexpr (T::PAIR) {
       // frame user pair j, antenna group G: realization G / 8 (= hx here); the
-      // off-diagonal blocks (j / 4 != G / 8) are zeros
+      // off-diagonal items (j / 4 != G / 8) are never read by stage 1: skipped
       const bool diag = (j / (T::KX / 2)) == (G / (T::MX / 8));
       const float4* hg = reinterpret_cast<const float4*>(p.H + (rx * T::MX + 8 * (G % (T::MX / 8))) * KT) +
                          j % (T::KX / 2);
@@ -562,6 +567,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
 #pragma unroll
   for (int q = 0; q < NIT; ++q) {
     const int it = tid + q * T::NT, j = it % NJ, G = it / NJ;
+    if (T::PAIR && (j / (T::KX / 2)) != (G / (T::MX / 8))) continue;  // (warp-uniform)
     const bool swp = (j >> 2) & 1;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {      // user 2j + (s ^ swp)
@@ -588,7 +594,22 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   // TMEM lane m % 128 of its tile's H columns — the same f16 values (same
   // rounding) as the shared copy stage 1 reads. Ordered before the first
   // stage-2 MMA by tcgen05.wait::st and the fenced CTA barriers of layer 0.
-  {
+  if constexpr (T::PAIR) {
+    // K order r' = (x, part, k_local): the thread's realization fills K-step hx
+    // (8 columns of hi, 8 of lo); the other K-step's columns of its lane only
+    // feed D2 rows no thread reads
+    const uint32_t th = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + T::T_HA + 8 * hx;
+    uint32_t hh[8], hl[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {  // columns (part, users 2 c' .. 2 c' + 1), c' = c % 4
+      const int part = c / 4, kl = 2 * (c % 4);
+      const float4 hq = hv[kl / 2];
+      split2((part == 0 ? hq.x : hq.y) * g, (part == 0 ? hq.z : hq.w) * g, hh[c], hl[c]);
+    }
+    tmem_st8(th, hh);
+    tmem_st8(th + R / 2, hl);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  } else {
     const uint32_t th = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + T::T_HA + (m >> 7) * R;
 #pragma unroll
     for (int half = 0; half < R / 32; ++half) {  // 16 columns = 32 rows r per store
@@ -596,12 +617,8 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         const int r = half * 32 + 2 * c;  // rows r, r + 1: one part, users k, k + 1 (K even)
-        // PAIR: K order r' = (x, part, k_local), one K-step per realization; the
-        // other realization's users at this antenna are zeros
-        const int part = T::PAIR ? (r % 16) / 8 : r / K;
-        const int k = T::PAIR ? (r / 16) * T::KX + r % 8 : r % K;
-        const bool own = !T::PAIR || k / T::KX == hx;
-        const float4 hq = own ? hv[(k % T::KX) / 2] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const int part = r / K, k = r % K;
+        const float4 hq = hv[k / 2];
         split2((part == 0 ? hq.x : hq.y) * g, (part == 0 ? hq.z : hq.w) * g, hh[c], hl[c]);
       }
       tmem_st16(th + half * 16, hh);
@@ -641,9 +658,6 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
 #pragma unroll
     for (int k = 0; k < KT; ++k) wn2 = fmaf(wr[k], wr[k], fmaf(wi[k], wi[k], wn2));
   }
-  // (PAIR: no zero blocks to write — each realization's stage-1 chain and
-  // stage-2 K-step read only its own operand rows and Bs tile, and the drains
-  // read only its own D1 / D2 columns)
 
   constexpr uint32_t IDESC1 = idesc_f16_amn<Q, 2 * R>();
   constexpr uint32_t IDESC1P = idesc_f16_amn<Q, R>();  // PAIR: per-realization N = 32
@@ -893,7 +907,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       for (int ch = tid; ch < NCH; ch += T::NT) {
         int k, c;
         T::chunk(ch, k, c);
-        if (T::PAIR && k / T::KX != c / T::KX) continue;  // off-diagonal block: static zeros (warp-uniform)
+        if (T::PAIR && k / T::KX != c / T::KX) continue;  // off-diagonal: no Bs tile (warp-uniform)
         float xr[CWD], xi[CWD];
   #pragma unroll
         for (int u = 0; u < CWD; ++u) xr[u] = xi[u] = 0.f;
@@ -967,7 +981,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         const int ch = tid;
         int k, c;
         T::chunk(ch, k, c);
-        const bool live = !T::PAIR || k / T::KX == c / T::KX;  // PAIR: off-diagonal blocks stay zero
+        const bool live = !T::PAIR || k / T::KX == c / T::KX;  // PAIR: off-diagonal blocks have no Bs tile
         float xr[CWD], xi[CWD];
   #pragma unroll
         for (int u = 0; u < CWD; ++u) xr[u] = xi[u] = 0.f;
@@ -1291,7 +1305,10 @@ using Mma_32_256 = MmaShape<32, 256, 1>;
 #define UFPGD_MMA16_MINB 4
 #endif
 using Mma_16_128 = MmaShape<16, 128, UFPGD_MMA16_MINB>;
-using Mma_8_64x2 = MmaShape<16, 128, UFPGD_MMA16_MINB, true>;
+#ifndef UFPGD_PAIR_MINB
+#define UFPGD_PAIR_MINB UFPGD_MMA16_MINB
+#endif
+using Mma_8_64x2 = MmaShape<16, 128, UFPGD_PAIR_MINB, true>;
 
 template <class T>
 cudaError_t launch_mma_t(const FusedArgs& args, bool pgd, cudaStream_t s, long long* nblocks) {
