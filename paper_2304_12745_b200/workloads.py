@@ -88,8 +88,8 @@ class Workload:
 
     def tensor_flops_per_realization(self):
         """Tensor-core flops the tcgen05 kernel (csrc/mma.cu) issues per
-        realization at (16,128) / (32,256) unfolded — and at (8,64), half a
-        (16,128) frame's (two realizations per frame) — None elsewhere: stage 1
+        realization at (16,128) / (32,256) unfolded — and at (8,64), where two
+        realizations share a (16,128) frame with their own MMAs — None elsewhere: stage 1
         2 Q (2R) M per layer (Q = 4K rows [W_hi; W_lo], N = [H_hi | H_lo]),
         skipped at a W0 = 0 layer 0; stage 2 (M/128) 2*128 (2R R + R R) per
         layer (H_hi [Bs_hi | Bs_lo] + H_lo Bs_hi), R = 2K. The 3-term f16
@@ -97,14 +97,16 @@ class Workload:
         if self.kind != "unfolded" or (self.K, self.M) not in ((8, 64), (16, 128), (32, 256)):
             return None
         K, M, L = self.K, self.M, self.L
-        pair = (K, M) == (8, 64)  # realization pairs in the (16,128) frame: half a frame's MMAs each
-        if pair:
-            K, M = 16, 128
+        n1 = L - 1 if self.w0_mode == capi.W0_ZERO else L
+        if (K, M) == (8, 64):
+            # realization pairs in the (16,128) frame, each with its own MMAs:
+            # stage 1 one M = 64 (the pair's [W_hi; W_lo] rows), N = 32, K = 64
+            # chain; stage 2 one K = 16 step, M = 128, N = 32 + 16
+            return n1 * 2.0 * 64 * 32 * 64 + L * 2.0 * 128 * 48 * 16
         R, Q = 2 * K, 4 * K
         s1 = 2.0 * Q * (2 * R) * M
         s2 = (M // 128) * 2.0 * 128 * 3 * R * R
-        n1 = L - 1 if self.w0_mode == capi.W0_ZERO else L
-        return (n1 * s1 + L * s2) / (2 if pair else 1)
+        return n1 * s1 + L * s2
 
     def bytes_per_realization(self) -> float:
         return 16.0 * self.K * self.M  # H in + W out, complex64
