@@ -78,10 +78,13 @@ struct MmaShape {
   static constexpr int FSTR = R + (CWD == 4 ? 4 : 8);
   // F [R][FSTR] (hi rows of P) and G (lo rows) alias the W operand: they are
   // written after the stage-1 MMAs retire and read before W is rewritten.
-  static constexpr int OFF_F = OFF_W;
+  // PAIR: their own region after the two 1 KB Bs tiles, since the W operand
+  // keeps the zeros of the other realization's users at each antenna (see the
+  // shared accumulators below); 45.6 KB in all, so 5 CTAs fit an SM.
+  static constexpr int OFF_F = PAIR ? OFF_BH + 2 * 4 * 2 * 128 : OFF_W;
   static constexpr int OFF_G = OFF_F + R * FSTR * 4;
   static_assert(2 * R * FSTR * 4 <= Q * M * 2, "");
-  static constexpr int OFF_BAR = OFF_BL + (R / 8) * BSBO;  // mbarriers, TMEM slot, reductions
+  static constexpr int OFF_BAR = PAIR ? OFF_G + R * FSTR * 4 : OFF_BL + (R / 8) * BSBO;  // mbarriers, TMEM slot, reductions
   static constexpr int SMEM = OFF_BAR + 512;
   // TMEM columns (fp32 accumulators)
   // D1: [X-part with H_hi | with H_lo] (2R columns; each antenna tile's K-steps
@@ -99,6 +102,14 @@ struct MmaShape {
   static constexpr uint32_t T_USED = T_HA + NTILE * R;
   static constexpr uint32_t T_COLS = T_USED <= 32 ? 32 : T_USED <= 64 ? 64 : T_USED <= 128 ? 128 : T_USED <= 256 ? 256 : 512;
   static_assert(T_USED <= 512, "");
+  // PAIR, fast path ("shared"): both realizations' stage-1 chains accumulate
+  // into one 32-column D1 and both stage-2 K-steps into one 32-column D2 — the
+  // other realization's terms are exact zeros (zero W-operand entries, zero
+  // TMEM A columns) — so a CTA needs 64 TMEM columns and 5 CTAs fit an SM.
+  // Exact only while both realizations stay finite (0 * Inf = NaN): a pair
+  // with a non-finite value is handed to the range-robust instance, which
+  // keeps separate columns per realization (D1 / D2 at 32 x, A at T_HA).
+  static constexpr uint32_t T_HA_SH = 32, T_COLS_SH = 64;
 
   // Canonical no-swizzle layouts: 8 x 16-byte core matrices (128 contiguous bytes).
   // H: element (r, m); core (r / 8, m / 8); inside: row r % 8 (16 B), m % 8 (2 B).
@@ -445,6 +456,8 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   const long long rid = RB ? static_cast<long long>(redo_list[it]) : static_cast<long long>(blockIdx.x);
   // the thread's realization (PAIR: 2 rid + tid / 64) and its antenna there
   constexpr int KT = T::KX;  // users per thread
+  constexpr bool SH = T::PAIR && !RB;  // pair with shared accumulators (see MmaShape)
+  constexpr uint32_t THA = SH ? T::T_HA_SH : T::T_HA, TCOLS = SH ? T::T_COLS_SH : T::T_COLS;
   const int hx = T::PAIR ? tid / T::MX : 0;
   const long long rx = T::PAIR ? 2 * rid + hx : rid;
   const bool xvalid = !T::PAIR || rx < p.B;  // PAIR: an odd batch's last CTA has one realization
@@ -471,7 +484,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                 "n"(T::T_COLS)
+                 "n"(TCOLS)
                  : "memory");
     // (the robust kernel allocates again for its next realization)
     if (!RB) asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -596,18 +609,23 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   // stage-2 MMA by tcgen05.wait::st and the fenced CTA barriers of layer 0.
   if constexpr (T::PAIR) {
     // K order r' = (x, part, k_local): the thread's realization fills K-step hx
-    // (8 columns of hi, 8 of lo); the other K-step's columns of its lane only
-    // feed D2 rows no thread reads
-    const uint32_t th = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + T::T_HA + 8 * hx;
-    uint32_t hh[8], hl[8];
+    // (8 columns of hi, 8 of lo), the other K-step is zeros (both K-steps
+    // accumulate into one D2)
+    const uint32_t th = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + THA;
+    uint32_t hh[16], hl[16];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {  // columns (part, users 2 c' .. 2 c' + 1), c' = c % 4
       const int part = c / 4, kl = 2 * (c % 4);
       const float4 hq = hv[kl / 2];
-      split2((part == 0 ? hq.x : hq.y) * g, (part == 0 ? hq.z : hq.w) * g, hh[c], hl[c]);
+      uint32_t h, l;
+      split2((part == 0 ? hq.x : hq.y) * g, (part == 0 ? hq.z : hq.w) * g, h, l);
+      hh[c] = hx == 0 ? h : 0u;
+      hh[8 + c] = hx == 1 ? h : 0u;
+      hl[c] = hx == 0 ? l : 0u;
+      hl[8 + c] = hx == 1 ? l : 0u;
     }
-    tmem_st8(th, hh);
-    tmem_st8(th + R / 2, hl);
+    tmem_st16(th, hh);
+    tmem_st16(th + R / 2, hl);
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   } else {
     const uint32_t th = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + T::T_HA + (m >> 7) * R;
@@ -651,6 +669,19 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   } else {
 #pragma unroll
     for (int k = 0; k < KT; ++k) wr[k] = wi[k] = 0.f;
+  }
+  if constexpr (T::PAIR) {
+    // zeros of the other realization's users at this antenna in the W operand,
+    // written once (the split only rewrites the thread's own rows, F / G have
+    // their own region): the other realization's stage-1 chain accumulates
+    // exactly 0 onto this realization's D1 rows. Ordered before the first
+    // stage-1 MMA by the split's fence and barrier.
+#pragma unroll
+    for (int hl = 0; hl < 2; ++hl)
+#pragma unroll
+      for (int part = 0; part < 2; ++part)
+        *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(hl * R + part * K + T::KX * (1 - hx), m)) =
+            make_uint4(0u, 0u, 0u, 0u);
   }
   int aW = 0;        // robust path: the W registers hold W_s 2^-aW ...
   float wn2 = 0.f;   // ... and ||w_m||^2 in that domain
@@ -765,17 +796,19 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         if constexpr (T::PAIR) {
           // one chain per realization over its own 64 antennas (K-steps 4x ..
           // 4x + 3) and its own N = 32 H columns — every other 8-row N-group
-          // of [H_hi | H_lo] (SBO doubled) — into D1 columns [32 x, 32 x + 32):
-          // [hi p0 | hi p1 | lo p0 | lo p1] of its 8 users. The block-diagonal
-          // frame's zero blocks (half the stage-1 MACs and of its H reads) are
-          // never multiplied.
+          // of [H_hi | H_lo] (SBO doubled) — both into D1 columns [0, 32):
+          // [hi p0 | hi p1 | lo p0 | lo p1] of the row's realization's 8 users
+          // (the other chain adds the exact zeros of the W operand's
+          // off-diagonal entries). The frame's zero blocks (half the stage-1
+          // MACs and of its H reads) are never multiplied.
           constexpr int KX4 = T::MX / 16;  // K-steps per realization
 #pragma unroll
           for (int x = 0; x < 2; ++x)
 #pragma unroll
             for (int i = 0; i < KX4; ++i)
-              umma_f16w(tmem + T::T_D1A + 32 * x, alo + (x * KX4 + i) * (2 * 16 * Q >> 4), sdesc_hi(128),
-                        blo + (x * KX4 + i) * (256 >> 4) + x * (16 * M >> 4), sdesc_hi(2 * 16 * M), IDESC1P, i > 0);
+              umma_f16w(tmem + T::T_D1A + (SH ? 0 : 32 * x), alo + (x * KX4 + i) * (2 * 16 * Q >> 4), sdesc_hi(128),
+                        blo + (x * KX4 + i) * (256 >> 4) + x * (16 * M >> 4), sdesc_hi(2 * 16 * M), IDESC1P,
+                        (SH && x > 0) || i > 0);
         } else {
 #pragma unroll
         for (int i = 0; i < KST; ++i) {
@@ -816,23 +849,25 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         float* d0 = (quad < 2 ? F : G) + (part * K + kr) * T::FSTR + cp;
         float a[16], b[16];
         if constexpr (T::PAIR) {
-          // D1 columns [32 x, +32) hold realization x's [hi p0 | hi p1 | lo p0 |
-          // lo p1]: row kr (a) lives in the first load's blocks, row kr + 8 (b)
-          // in the second's (their other rows are the frame's zeros). F / G get
+          // D1 columns [0, 32) hold each row's realization's [hi p0 | hi p1 |
+          // lo p0 | lo p1]: one 16x256b load carries row kr (a) and kr + 8 (b). F / G get
           // the same entries as the full-frame layout: (row kr, columns cp, K + cp),
           // (row kr + 8, columns 8 + cp, K + 8 + cp).
+          // (robust instance: realization x's columns at 32 x — row kr from the
+          // first load, row kr + 8 from the second)
           tmem_ld16x256(tmem + lrow + T::T_D1A, a);
-          tmem_ld16x256(tmem + lrow + T::T_D1A + 32, b);
+          if (!SH) tmem_ld16x256(tmem + lrow + T::T_D1A + 32, b);
           tmem_wait<16>(a);
-          tmem_wait<16>(b);
+          if (!SH) tmem_wait<16>(b);
+          const float* bb = SH ? a : b;
           float2 v[4];  // (row kr: p'0, p'1), (row kr + 8: p'0, p'1)
           const float2 h0 = make_float2(a[0], a[1]), h1 = make_float2(a[4], a[5]);
-          const float2 h2 = make_float2(b[2], b[3]), h3 = make_float2(b[6], b[7]);
+          const float2 h2 = make_float2(bb[2], bb[3]), h3 = make_float2(bb[6], bb[7]);
           if (quad < 2) {  // hi W rows: W_hi H_hi + 2^-11 W_hi H_lo
             v[0] = ffma2(kLoScale, make_float2(a[8], a[9]), h0);
             v[1] = ffma2(kLoScale, make_float2(a[12], a[13]), h1);
-            v[2] = ffma2(kLoScale, make_float2(b[10], b[11]), h2);
-            v[3] = ffma2(kLoScale, make_float2(b[14], b[15]), h3);
+            v[2] = ffma2(kLoScale, make_float2(bb[10], bb[11]), h2);
+            v[3] = ffma2(kLoScale, make_float2(bb[14], bb[15]), h3);
           } else {         // lo W rows: 2^-11 W_lo H_hi
             v[0] = fmul2(kLoScale, h0);
             v[1] = fmul2(kLoScale, h1);
@@ -1083,16 +1118,18 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       tc_fence_after();
       const int t = wu >> 2;  // = tile, warp-uniform
       const uint32_t dm = tmem + T::T_D2 + t * 2 * R, dc = dm + R;
-      const uint32_t ta = tmem + T::T_HA + t * R;  // H_hi columns; H_lo at + R / 2
+      const uint32_t ta = tmem + THA + t * R;  // H_hi columns; H_lo at + R / 2
       const uint32_t bhlo = sdesc_lo(sb + T::OFF_BH, 128);
       if constexpr (T::PAIR) {
-        // realization x: its K-step of A (8 TMEM columns of H hi / lo) against its
-        // Bs tile, into D2 columns [32 x, +32) = [main hh | main hl + corr]
+        // realization x: its K-step of A (8 TMEM columns of H hi / lo; zeros in
+        // the other realization's lanes) against its Bs tile, both into D2
+        // columns [0, 32) = [main hh | main hl + corr]
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
           const uint32_t bx = bhlo + x * (T::BST >> 4);
-          umma_f16_ta(dm + 32 * x, ta + x * 8, bx, sdesc_hi(T::BSBOP), IDESC2PW, 0);
-          umma_f16_ta(dm + 32 * x + 16, ta + R / 2 + x * 8, bx, sdesc_hi(T::BSBOP), IDESC2P, 1);
+          const uint32_t dx = dm + (SH ? 0 : 32 * x);
+          umma_f16_ta(dx, ta + x * 8, bx, sdesc_hi(T::BSBOP), IDESC2PW, SH && x > 0);
+          umma_f16_ta(dx + 16, ta + R / 2 + x * 8, bx, sdesc_hi(T::BSBOP), IDESC2P, 1);
         }
       } else
 #pragma unroll
@@ -1129,8 +1166,9 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         for (int part = 0; part < 2; ++part) {
           float* w = part == 0 ? wr : wi;
           float a[8], b[8];
-          tmem_ld8(cm + 32 * hx + 8 * part, a);       // D2 [main hh | main hl + corr] of realization hx
-          tmem_ld8(cm + 32 * hx + 16 + 8 * part, b);
+          const uint32_t cx = cm + (SH ? 0 : 32 * hx);  // D2 [main hh | main hl + corr]
+          tmem_ld8(cx + 8 * part, a);
+          tmem_ld8(cx + 16 + 8 * part, b);
           tmem_wait<8>(a);
           tmem_wait<8>(b);
           if constexpr (RB) {
@@ -1271,7 +1309,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   }
   if (warp == 0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(T::T_COLS) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS) : "memory");
   }
   if (RB && tid == 0) {  // the robust kernel re-initialises them for its next realization
 #pragma unroll
@@ -1306,7 +1344,7 @@ using Mma_32_256 = MmaShape<32, 256, 1>;
 #endif
 using Mma_16_128 = MmaShape<16, 128, UFPGD_MMA16_MINB>;
 #ifndef UFPGD_PAIR_MINB
-#define UFPGD_PAIR_MINB UFPGD_MMA16_MINB
+#define UFPGD_PAIR_MINB 5
 #endif
 using Mma_8_64x2 = MmaShape<16, 128, UFPGD_PAIR_MINB, true>;
 
