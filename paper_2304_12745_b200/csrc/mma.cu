@@ -67,7 +67,9 @@ struct MmaShape {
   // shared-memory byte offsets (16-byte aligned, as the no-swizzle layouts need)
   static constexpr int OFF_HH = 0;                       // H hi  [R x M] f16, core layout hoff()
   static constexpr int OFF_HL = OFF_HH + R * M * 2;      // H lo
-  static constexpr int OFF_W = OFF_HL + R * M * 2;       // [W_hi; W_lo] [Q x M] f16, woff()
+  // PAIR: H is only staged per realization (hoffp(): 8 KB instead of 16), so
+  // the W operand follows right after it
+  static constexpr int OFF_W = PAIR ? OFF_HH + 2 * 4 * 8 * 128 : OFF_HL + R * M * 2;  // [W_hi; W_lo] [Q x M] f16, woff()
   // Bs builder chunk width: 4 values of an X' row per thread, or 2 when K^2/4
   // chunks would leave threads idle (chunk() maps either conflict-free).
   static constexpr int CWD = (K * K / 4 >= NT) ? 4 : 2;
@@ -117,6 +119,12 @@ struct MmaShape {
   //   stage 2 A (MN-major, MN = m, K = r): LBO (K-group) 16 M, SBO (MN-group) 128
   static __device__ __forceinline__ int hoff(int r, int m) {
     return (r >> 3) * (16 * M) + (m >> 3) * 128 + (r & 7) * 16 + (m & 7) * 2;
+  }
+  // PAIR: realization x's stage-1 B operand alone, K-major: N-groups g = (hilo,
+  // part) of its 8 users (rows kl), K-groups of 8 of its 64 antennas (ml):
+  // LBO 128, SBO 1024 — the [hi p0 | hi p1 | lo p0 | lo p1] order of its chain.
+  static __device__ __forceinline__ int hoffp(int x, int g, int kl, int ml) {
+    return x * 4096 + g * 1024 + (ml >> 3) * 128 + kl * 16 + (ml & 7) * 2;
   }
   // W operand: element (q, m), MN-major (MN = q, K = m): core (q / 8, m / 8);
   // inside: row m % 8 (16 B), q % 8 (2 B). LBO (K-group) 16 Q, SBO 128.
@@ -580,7 +588,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
 #pragma unroll
   for (int q = 0; q < NIT; ++q) {
     const int it = tid + q * T::NT, j = it % NJ, G = it / NJ;
-    if (T::PAIR && (j / (T::KX / 2)) != (G / (T::MX / 8))) continue;  // (warp-uniform)
+    if (T::PAIR && (j / (T::KX / 2)) != (G / (T::MX / 8))) continue;  // off-diagonal item: not staged
     const bool swp = (j >> 2) & 1;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {      // user 2j + (s ^ swp)
@@ -596,8 +604,15 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
           split2(va * g, vb * g, hh[i / 2], hl[i / 2]);
         }
         const int r = part * K + 2 * j + ((s == 1) != swp ? 1 : 0);
-        *reinterpret_cast<uint4*>(smem + T::OFF_HH + T::hoff(r, 8 * G)) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
-        *reinterpret_cast<uint4*>(smem + T::OFF_HL + T::hoff(r, 8 * G)) = make_uint4(hl[0], hl[1], hl[2], hl[3]);
+        if constexpr (T::PAIR) {
+          const int x = G / (T::MX / 8), kl = r % T::KX, ml = 8 * (G % (T::MX / 8));
+          *reinterpret_cast<uint4*>(smem + T::OFF_HH + T::hoffp(x, part, kl, ml)) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
+          *reinterpret_cast<uint4*>(smem + T::OFF_HH + T::hoffp(x, 2 + part, kl, ml)) =
+              make_uint4(hl[0], hl[1], hl[2], hl[3]);
+        } else {
+          *reinterpret_cast<uint4*>(smem + T::OFF_HH + T::hoff(r, 8 * G)) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
+          *reinterpret_cast<uint4*>(smem + T::OFF_HL + T::hoff(r, 8 * G)) = make_uint4(hl[0], hl[1], hl[2], hl[3]);
+        }
       }
     }
   }
@@ -795,8 +810,8 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         const uint32_t alo = sdesc_lo(sw, 16 * Q), blo = sdesc_lo(sh, 128);
         if constexpr (T::PAIR) {
           // one chain per realization over its own 64 antennas (K-steps 4x ..
-          // 4x + 3) and its own N = 32 H columns — every other 8-row N-group
-          // of [H_hi | H_lo] (SBO doubled) — both into D1 columns [0, 32):
+          // 4x + 3) and its own N = 32 H columns (its hoffp() tile) — both
+          // into D1 columns [0, 32):
           // [hi p0 | hi p1 | lo p0 | lo p1] of the row's realization's 8 users
           // (the other chain adds the exact zeros of the W operand's
           // off-diagonal entries). The frame's zero blocks (half the stage-1
@@ -807,8 +822,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
 #pragma unroll
             for (int i = 0; i < KX4; ++i)
               umma_f16w(tmem + T::T_D1A + (SH ? 0 : 32 * x), alo + (x * KX4 + i) * (2 * 16 * Q >> 4), sdesc_hi(128),
-                        blo + (x * KX4 + i) * (256 >> 4) + x * (16 * M >> 4), sdesc_hi(2 * 16 * M), IDESC1P,
-                        (SH && x > 0) || i > 0);
+                        blo + (x * 4096 + i * 256 >> 4), sdesc_hi(1024), IDESC1P, (SH && x > 0) || i > 0);
         } else {
 #pragma unroll
         for (int i = 0; i < KST; ++i) {
@@ -1344,7 +1358,7 @@ using Mma_32_256 = MmaShape<32, 256, 1>;
 #endif
 using Mma_16_128 = MmaShape<16, 128, UFPGD_MMA16_MINB>;
 #ifndef UFPGD_PAIR_MINB
-#define UFPGD_PAIR_MINB 5
+#define UFPGD_PAIR_MINB 6
 #endif
 using Mma_8_64x2 = MmaShape<16, 128, UFPGD_PAIR_MINB, true>;
 
