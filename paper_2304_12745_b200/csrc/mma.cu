@@ -84,9 +84,21 @@ struct MmaShape {
   // keeps the zeros of the other realization's users at each antenna (see the
   // shared accumulators below); 45.6 KB in all, so 5 CTAs fit an SM.
   static constexpr int OFF_F = PAIR ? OFF_BH + 2 * 4 * 2 * 128 : OFF_W;
-  static constexpr int OFF_G = OFF_F + R * FSTR * 4;
+  // PAIR: only the diagonal 8 x 8 blocks of P are exchanged — rows (part, k)
+  // with the 16 columns (part', k' of k's realization), 16 floats per row,
+  // 8-word halves swapped on rows (row >> 1) odd (fx()): conflict-free for the
+  // drain's stores and the Bs build's loads, 4 KB for F and G together.
+  static constexpr int FROW = PAIR ? 16 : FSTR;  // floats per exchange row
+  static constexpr int OFF_G = OFF_F + R * FROW * 4;
   static_assert(2 * R * FSTR * 4 <= Q * M * 2, "");
-  static constexpr int OFF_BAR = PAIR ? OFF_G + R * FSTR * 4 : OFF_BL + (R / 8) * BSBO;  // mbarriers, TMEM slot, reductions
+  static constexpr int OFF_BAR = PAIR ? OFF_G + R * FROW * 4 : OFF_BL + (R / 8) * BSBO;  // mbarriers, TMEM slot, reductions
+  // exchange-row index of P(row, col): row = (part, k), col = (part', k'), frame indices
+  static __device__ __forceinline__ int fx(int row, int col) {
+    if constexpr (PAIR)
+      return row * 16 + (((col / K) * 8 + col % 8) ^ (((row >> 1) & 1) << 3));
+    else
+      return row * FSTR + col;
+  }
   static constexpr int SMEM = OFF_BAR + 512;
   // TMEM columns (fp32 accumulators)
   // D1: [X-part with H_hi | with H_lo] (2R columns; each antenna tile's K-steps
@@ -860,7 +872,9 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         // unused lanes of the 32x32b shape (half the LDTM and FP32x2 work).
         static_assert(T::NTILE == 1 && CW == 2 * R / 2 && T::CWD == 2, "");
         const int kr = lane >> 2, cp = 2 * (lane & 3);
-        float* d0 = (quad < 2 ? F : G) + (part * K + kr) * T::FSTR + cp;
+        float* const FG = quad < 2 ? F : G;
+        const int r0 = part * K + kr;
+        float* d0 = FG + r0 * T::FSTR + cp;
         float a[16], b[16];
         if constexpr (T::PAIR) {
           // D1 columns [0, 32) hold each row's realization's [hi p0 | hi p1 |
@@ -888,10 +902,10 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
             v[2] = fmul2(kLoScale, h2);
             v[3] = fmul2(kLoScale, h3);
           }
-          *reinterpret_cast<float2*>(d0) = v[0];
-          *reinterpret_cast<float2*>(d0 + K) = v[1];
-          *reinterpret_cast<float2*>(d0 + 8 * T::FSTR + 8) = v[2];
-          *reinterpret_cast<float2*>(d0 + 8 * T::FSTR + K + 8) = v[3];
+          *reinterpret_cast<float2*>(FG + T::fx(r0, cp)) = v[0];
+          *reinterpret_cast<float2*>(FG + T::fx(r0, K + cp)) = v[1];
+          *reinterpret_cast<float2*>(FG + T::fx(r0 + 8, 8 + cp)) = v[2];
+          *reinterpret_cast<float2*>(FG + T::fx(r0 + 8, K + 8 + cp)) = v[3];
         } else {
         tmem_ld16x256(tmem + lrow + T::T_D1A, a);
         if (quad < 2) tmem_ld16x256(tmem + lrow + T::T_D1B, b);
@@ -961,14 +975,12 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   #pragma unroll
         for (int u = 0; u < CWD; ++u) xr[u] = xi[u] = 0.f;
         if (!xzero) {
-          const float* F0 = F + k * T::FSTR;        // P rows (0, k), (1, k): hi parts in F, lo in G
-          const float* F1 = F + (K + k) * T::FSTR;
-          const float* G0 = G + k * T::FSTR;
-          const float* G1 = G + (K + k) * T::FSTR;
-          const FV a00 = *reinterpret_cast<const FV*>(F0 + c), b00 = *reinterpret_cast<const FV*>(G0 + c);
-          const FV a11 = *reinterpret_cast<const FV*>(F1 + K + c), b11 = *reinterpret_cast<const FV*>(G1 + K + c);
-          const FV a01 = *reinterpret_cast<const FV*>(F0 + K + c), b01 = *reinterpret_cast<const FV*>(G0 + K + c);
-          const FV a10 = *reinterpret_cast<const FV*>(F1 + c), b10 = *reinterpret_cast<const FV*>(G1 + c);
+          // P rows (0, k), (1, k): hi parts in F, lo in G
+          const int i00 = T::fx(k, c), i11 = T::fx(K + k, K + c), i01 = T::fx(k, K + c), i10 = T::fx(K + k, c);
+          const FV a00 = *reinterpret_cast<const FV*>(F + i00), b00 = *reinterpret_cast<const FV*>(G + i00);
+          const FV a11 = *reinterpret_cast<const FV*>(F + i11), b11 = *reinterpret_cast<const FV*>(G + i11);
+          const FV a01 = *reinterpret_cast<const FV*>(F + i01), b01 = *reinterpret_cast<const FV*>(G + i01);
+          const FV a10 = *reinterpret_cast<const FV*>(F + i10), b10 = *reinterpret_cast<const FV*>(G + i10);
           const float* A00 = reinterpret_cast<const float*>(&a00);
           const float* B00 = reinterpret_cast<const float*>(&b00);
           const float* A11 = reinterpret_cast<const float*>(&a11);
@@ -1035,14 +1047,12 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   #pragma unroll
         for (int u = 0; u < CWD; ++u) xr[u] = xi[u] = 0.f;
         if (!xzero && live) {
-          const float* F0 = F + k * T::FSTR;        // P rows (0, k), (1, k): hi parts in F, lo in G
-          const float* F1 = F + (K + k) * T::FSTR;
-          const float* G0 = G + k * T::FSTR;
-          const float* G1 = G + (K + k) * T::FSTR;
-          const FV a00 = *reinterpret_cast<const FV*>(F0 + c), b00 = *reinterpret_cast<const FV*>(G0 + c);
-          const FV a11 = *reinterpret_cast<const FV*>(F1 + K + c), b11 = *reinterpret_cast<const FV*>(G1 + K + c);
-          const FV a01 = *reinterpret_cast<const FV*>(F0 + K + c), b01 = *reinterpret_cast<const FV*>(G0 + K + c);
-          const FV a10 = *reinterpret_cast<const FV*>(F1 + c), b10 = *reinterpret_cast<const FV*>(G1 + c);
+          // P rows (0, k), (1, k): hi parts in F, lo in G
+          const int i00 = T::fx(k, c), i11 = T::fx(K + k, K + c), i01 = T::fx(k, K + c), i10 = T::fx(K + k, c);
+          const FV a00 = *reinterpret_cast<const FV*>(F + i00), b00 = *reinterpret_cast<const FV*>(G + i00);
+          const FV a11 = *reinterpret_cast<const FV*>(F + i11), b11 = *reinterpret_cast<const FV*>(G + i11);
+          const FV a01 = *reinterpret_cast<const FV*>(F + i01), b01 = *reinterpret_cast<const FV*>(G + i01);
+          const FV a10 = *reinterpret_cast<const FV*>(F + i10), b10 = *reinterpret_cast<const FV*>(G + i10);
           const float* A00 = reinterpret_cast<const float*>(&a00);
           const float* B00 = reinterpret_cast<const float*>(&b00);
           const float* A11 = reinterpret_cast<const float*>(&a11);
@@ -1358,7 +1368,7 @@ using Mma_32_256 = MmaShape<32, 256, 1>;
 #endif
 using Mma_16_128 = MmaShape<16, 128, UFPGD_MMA16_MINB>;
 #ifndef UFPGD_PAIR_MINB
-#define UFPGD_PAIR_MINB 6
+#define UFPGD_PAIR_MINB 7
 #endif
 using Mma_8_64x2 = MmaShape<16, 128, UFPGD_PAIR_MINB, true>;
 
