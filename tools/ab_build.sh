@@ -4,7 +4,7 @@
 set -e
 name=$1; shift
 cd "$(dirname "$0")/.."
-mkdir -p tools/ablib/$name build/obj/ab/$name
+rm -rf build/obj/ab/$name; mkdir -p tools/ablib/$name build/obj/ab/$name
 objs=""
 # SRC_<name>=path overrides one source (e.g. SRC_mma=/tmp/old/mma.cu)
 for f in team team64 tile mma general metrics grad datagen probe; do
