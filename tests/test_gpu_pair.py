@@ -143,3 +143,67 @@ def test_pair_position_invariance():
         sub = run(np.ascontiguousarray(H[idx]), lam, eta, W2.c)
         np.testing.assert_array_equal(sub["W"], d["W"][idx])
         np.testing.assert_array_equal(sub["l21"], d["l21"][idx])
+
+
+# ---- fixed-step PGD (BASELINE config 3's shape) on the pair kernel -----------
+
+def run_pgd(H, lam, iters, c, mma=True, **kw):
+    with U.options(tensor_cores=int(mma)):
+        out = U.pgd_fixed(torch.from_numpy(np.ascontiguousarray(H)).cuda(), lam, iters, c,
+                          want_per_realization=True, **kw)
+        torch.cuda.synchronize()
+    return {k: (v.cpu().numpy() if v is not None else None) for k, v in out.items()}
+
+
+W3 = U.CONFIGS[3]
+
+
+@pytest.mark.parametrize("n", [1, 3, 130])
+def test_pair_pgd_power_iteration_and_parity(n):
+    """pgd.cpp:178-268 with the BASELINE 30-step 1/L rule: each realization of
+    a pair runs its own power iteration over its half of the CTA (L30 against
+    the oracle's), then PGD against the FP64 oracle at that step and against
+    the FFMA2 team kernel; odd n leaves a phantom partner in the last CTA."""
+    H = U.make_inputs(W3, 4, n)
+    iters = 600
+    g = run_pgd(H, W3.lambda_pgd, iters, W3.c, power_steps=30)
+    t = run_pgd(H, W3.lambda_pgd, iters, W3.c, power_steps=30, mma=False)
+    Lo, st = O.power_iteration_batch_f32(H, 30)
+    assert np.all(st == 0)
+    assert np.max(np.abs(g["eta"] * Lo - 1.0)) <= 1e-5
+    np.testing.assert_allclose(g["eta"], t["eta"], rtol=1e-5)
+    ora = O.pgd_batch_f32(H, W3.c, W3.lambda_pgd, 1.0 / Lo, iters, w0_mode=U.W0_CONJ_H)
+    rep = report(H, g["W"], ora, W3.c, W3.lambda_pgd)
+    print(f"pair pgd n={n}: rel max {rep['rel_max']:.2e} obj {rep['obj_max']:.2e} ties {rep['ties']}")
+    assert_parity(rep)
+    assert np.all(g["diverged_at"] == -1)
+
+
+def test_pair_pgd_given_steps_and_start():
+    """eta given per realization (pgd.cpp's fixed step) and a given W0: the
+    pair kernel reads both per realization."""
+    H = U.make_inputs(W3, 6, 33)
+    Lo, _ = O.power_iteration_batch_f32(H, 30)
+    eta = torch.from_numpy((0.9 / Lo).astype(np.float32)).cuda()
+    rng = np.random.default_rng(5)
+    W0 = (0.02 * (rng.standard_normal(H.shape) + 1j * rng.standard_normal(H.shape))).astype(np.complex64)
+    g = run_pgd(H, W3.lambda_pgd, 300, W3.c, eta=eta, w0_mode=U.W0_GIVEN,
+                W0=torch.from_numpy(W0).cuda())
+    np.testing.assert_array_equal(g["eta"], eta.cpu().numpy())
+    ora = O.pgd_batch_f32(H, W3.c, W3.lambda_pgd, 0.9 / Lo, 300, w0_mode=U.W0_GIVEN, W0=W0)
+    assert_parity(report(H, g["W"], ora, W3.c, W3.lambda_pgd))
+
+
+def test_pair_pgd_divergence_is_per_realization():
+    """test_pgd.cpp:454-470: eta = 1e6 diverges (1-based iteration index); the
+    partner with a sane step in the same pair converges as if alone."""
+    H = U.make_inputs(W3, 0, 4)
+    Lo, _ = O.power_iteration_batch_f32(H, 30)
+    steps = (1.0 / Lo).astype(np.float32)
+    steps[1] = 1e6  # pair (0, 1): realization 1 diverges
+    g = run_pgd(H, 0.05, 200, W3.c, eta=torch.from_numpy(steps).cuda())
+    alone = run_pgd(np.ascontiguousarray(H[[0, 2, 3]]), 0.05, 200, W3.c,
+                    eta=torch.from_numpy(np.ascontiguousarray(steps[[0, 2, 3]])).cuda())
+    assert g["diverged_at"][1] >= 1
+    assert np.all(g["diverged_at"][[0, 2, 3]] == -1)
+    assert rel_fro(g["W"][[0, 2, 3]], alone["W"].astype(np.complex128)).max() < 5e-6
