@@ -530,8 +530,13 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   float4 hv[KT / 2];  // hv[j] = (Re H(2j, m), Im H(2j, m), Re H(2j+1, m), Im H(2j+1, m)) of the thread's realization
   {
     const float4* hg = reinterpret_cast<const float4*>(p.H + (rx * T::MX + ml) * KT);
+    // (16,128) and pairs: L1-allocating loads, so the staging items' re-read of
+    // the same lines below hits L1 (config 5 -1.5%, config 2 -0.7%); at (32,256)
+    // the 144 KB of shared memory leaves too little L1 (+0.4%): streaming loads
+    constexpr bool L1 = T::K < 32;
 #pragma unroll
-    for (int j = 0; j < KT / 2; ++j) hv[j] = xvalid ? ldg_stream(hg + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < KT / 2; ++j)
+      hv[j] = xvalid ? (L1 ? __ldg(hg + j) : ldg_stream(hg + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   // The shared-memory H staging works on items (user pair j, group of 8
   // antennas G) instead of the thread's own antenna: 8 antennas of one row r
