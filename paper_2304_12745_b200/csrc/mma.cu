@@ -562,7 +562,8 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     } else {
       const float4* hg = reinterpret_cast<const float4*>(p.H + (rid * M + 8 * G) * K) + j;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) hs[q][i] = __ldg(hg + i * (K / 2));
+      for (int i = 0; i < 8; ++i)  // (32,256): streaming, as the row loads (-0.3%)
+        hs[q][i] = T::K < 32 ? __ldg(hg + i * (K / 2)) : ldg_stream(hg + i * (K / 2));
     }
   }
   float amax = 0.f;
