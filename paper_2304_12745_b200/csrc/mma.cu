@@ -1,11 +1,14 @@
 // Tensor-core (tcgen05 / TMEM) kernel for the unfolded forward and the
 // fixed-step PGD at (K, M) = (32, 256) and (16, 128) — BASELINE configs 4 and
 // 5, the "larger M x K x K complex contractions" north_star reserves the
-// tensor cores for. One CTA (thread = antenna) owns a realization for all
-// layers / iterations (unfolded.cpp:112-146, pgd.cpp:226-244):
+// tensor cores for — and at (8, 64) (configs 2 and 3) as pairs of
+// realizations in the (16, 128) frame (MmaShape PAIR). One CTA (thread =
+// antenna) owns a realization (a pair) for all layers / iterations
+// (unfolded.cpp:112-146, pgd.cpp:226-244):
 //
-//   stage 1  X  = W H^T           tcgen05.mma  M=4K N=4K K=M, split-K by 128-antenna tile
-//   stage 2  G  = (-eta X') H^*   tcgen05.mma  M=128 N=4K + N=2K, K=2K, per 128-antenna tile
+//   stage 1  X  = W H^T           tcgen05.mma  M=4K N=4K K=M, by 128-antenna tile into one accumulator
+//   stage 2  G  = (-eta X') H^*   tcgen05.mma  M=128 N=4K + N=2K, K=2K, per 128-antenna tile,
+//                                              A = H from TMEM
 //   prox     per-antenna group soft threshold on V = W + G, in registers
 //
 // Precision: FP32 products are split into f16 pairs, x = hi + 2^-11 lo
@@ -15,17 +18,20 @@
 // numpy emulation of the whole 20-layer forward at config 4 gives 1.5e-7
 // W relative error against the FP64 oracle vs 1.4e-7 for plain FP32). Each
 // realization is scaled by an exact power of two g (max |g H| in [1, 2)) so
-// the f16 range is never approached: X is invariant (W_s = W / g), the step
-// becomes eta / g^2 and the threshold thr / g.
+// the f16 range of H is never approached: X is invariant (W_s = W / g), the
+// step becomes eta / g^2 and the threshold thr / g; realizations whose W or Bs
+// operands would still leave the f16 range go to a range-robust instance.
 //
 // Real forms (rows r = (part, k), part 0 = Re, 1 = Im, r in [0, 2K)):
 //   stage 1: D1[q][(p', k')] = sum_m Wop[q][m] Hop[(p', k')][m], q = (hilo, p, k)
 //            (A = [W_hi; W_lo] 4K x M, MN-major; B = [H_hi | H_lo], K-major)
 //            X_r = P[(0,k),(0,k')] - P[(1,k),(1,k')], X_i = P[(0,k),(1,k')] + P[(1,k),(0,k')]
 //   stage 2: D2[m][(p, k)] = sum_(p', k') Hop[(p', k')][m] Bs[(p', k')][(p, k)]
-//            (A = H as M x 2K MN-major — the same shared-memory bytes as
-//            stage 1's K-major B — and Bs = the real form of -eta X'^T)
-// so H (hi and lo, f16) is staged once and read by both stages.
+//            (A = H as M x 2K, K-major f16 pairs in TMEM, staged once per
+//            realization from the thread's own H row; Bs = the real form of
+//            -eta X'^T in shared memory)
+// so H (hi and lo, f16) is staged once, in shared memory for stage 1 and in
+// TMEM for stage 2.
 #include <algorithm>
 #include <cfloat>
 #include <climits>
