@@ -470,9 +470,12 @@ __device__ float cta_power(const float4 (&hv)[T::KX / 2], const float2* v0, int 
 // over the redo_list entries (normally none). The body is written inline in
 // the kernel (a device-function body taking the params by reference measured
 // 3% slower at (16,128)).
-template <class T, bool PGD, bool RB>
+// RESID (PGD pairs only): solve_pgd's residual_tol early stop per realization
+// (pgd.cpp:246-260; see the layer loop).
+template <class T, bool PGD, bool RB, bool RESID = false>
 __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     mma_kernel(const __grid_constant__ FusedArgs p, int* redo_list, int* redo_count) {
+  static_assert(!RESID || (PGD && T::PAIR), "the early stop is built for the (8,64) PGD pairs");
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int K = T::K, M = T::M, R = T::R, Q = T::Q, NW = T::NW;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -502,6 +505,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   float* red = reinterpret_cast<float*>(smem + T::OFF_BAR + 64);           // [2][16]
   long long* fbs = reinterpret_cast<long long*>(smem + T::OFF_BAR + 192);  // [16]
   float* redw = reinterpret_cast<float*>(smem + T::OFF_BAR + 320);         // [16]: robust-path maxima
+  float* rsd = reinterpret_cast<float*>(smem + T::OFF_BAR + 384);          // [NW][2]: early-stop partials
 
   if (tid == 0) {
 #pragma unroll
@@ -769,6 +773,22 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     if (p.eta_out && tid == hx * (T::NT / (T::PAIR ? 2 : 1)) && xvalid) p.eta_out[rx] = eta_b;
   }
   PSTAMP(4)
+  // RESID: a realization whose relative iterate change ||W_new - W|| / max(||W||,
+  // 1e-12) fell below residual_tol after iteration l stops there (taken = l + 1;
+  // its statistics are those of that iteration): from then on its step and
+  // threshold are 0, so every further iteration is exactly the identity while
+  // its partner runs on, and the CTA leaves once both have stopped. The
+  // per-warp sums of |dW|^2 and |W|^2 of iteration l are read after the next
+  // iteration's split barrier (no extra barrier per iteration); "stopped after
+  // l" is just "the criterion held at l", since a stopped realization's dW is 0.
+  bool stopped = false;
+  long long taken = 0;
+  float l21_prev = 0.f, l21_keep = 0.f;
+  int act_prev = 0, act_keep = 0;
+  const float tol2 = RESID ? p.residual_tol * p.residual_tol : 0.f;
+  float wor[RESID ? KT : 1], woi[RESID ? KT : 1];  // W before the iteration's update
+  (void)wor;
+  (void)woi;
   for (long long l = 0; l < p.L; ++l) {
     TSTAMP(0)
     const bool xzero = (l == 0 && p.w0_mode == UFPGD_W0_ZERO);
@@ -799,7 +819,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       }
       ts *= pow2i(-aW);
     }
-    const float fstep = -(PGD ? eta_b : p.eta[l]) * g2inv;  // -eta / g^2 folded into Bs
+    float fstep = -(PGD ? eta_b : p.eta[l]) * g2inv;  // -eta / g^2 folded into Bs
     if (!xzero) {
       // W operand rows q = (hilo, part, k) from the thread's antenna column
 #pragma unroll
@@ -819,6 +839,27 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       if (T::NTILE > 1) named_bar(1 + tile, T::NT / T::NTILE);
       else __syncthreads();
       TSTAMP(1)
+      if constexpr (RESID) {
+        if (l > 0) {
+          bool crit[2];
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            const float dd = rsd[4 * x] + rsd[4 * x + 2], ss = rsd[4 * x + 1] + rsd[4 * x + 3];
+            crit[x] = dd < tol2 * fmaxf(ss, 1e-24f);
+          }
+          if (!stopped) {
+            taken = l;
+            l21_keep = l21_prev;
+            act_keep = act_prev;
+            stopped = crit[hx];
+          }
+          if (crit[0] && crit[1]) break;  // CTA-uniform: both realizations have stopped
+        }
+        if (stopped) {
+          fstep = 0.f;
+          ts = 0.f;
+        }
+      }
       // (32,256): both tiles accumulate into one D1 (columns [0, 2R)); tile 1's
       // first warp issues after tile 0's MMAs are queued (warp 0 -> warp 4
       // named barrier, tcgen05 fences around it), so the tensor pipe runs them
@@ -1197,6 +1238,13 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       // antenna m: TMEM lane m % 128 (warp quadrant warp % 4), tile m / 128
       const uint32_t cm = tmem + lrow + T::T_D2 + tile * 2 * R;
       const uint32_t cc = cm + R;
+      if constexpr (RESID) {
+#pragma unroll
+        for (int k = 0; k < KT; ++k) {
+          wor[k] = wr[k];
+          woi[k] = wi[k];
+        }
+      }
       if constexpr (T::PAIR) {  // the thread's 8 users only
 #pragma unroll
         for (int part = 0; part < 2; ++part) {
@@ -1284,12 +1332,39 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       wi[k + 1] = i2.y;
     }
     if constexpr (RB) wn2 = scale * scale * s2;
-    if (l + 1 == p.L && on) {
+    if constexpr (RESID) {
+      l21_prev = on ? gw * fmaf(s2, r, -ts) : 0.f;
+      act_prev = on ? 1 : 0;
+      float2 dsum = zero2();  // (|dW|^2, |W|^2) of this thread's entries, in the register domain
+#pragma unroll
+      for (int k = 0; k < KT; ++k) {
+        const float dr = wr[k] - wor[k], di = wi[k] - woi[k];
+        dsum = __ffma2_rn(make_float2(dr, wor[k]), make_float2(dr, wor[k]), dsum);
+        dsum = __ffma2_rn(make_float2(di, woi[k]), make_float2(di, woi[k]), dsum);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+        dsum = fadd2(dsum, make_float2(__shfl_xor_sync(kFull, dsum.x, off), __shfl_xor_sync(kFull, dsum.y, off)));
+      if (lane == 0) {
+        rsd[2 * warp] = dsum.x;
+        rsd[2 * warp + 1] = dsum.y;
+      }
+    } else if (l + 1 == p.L && on) {
       l21 += gw * fmaf(s2, r, -ts);
       act += 1;
     }
     if (nonfinite && first_bad < 0) first_bad = l;
     TSTAMP(8)
+  }
+  if constexpr (RESID) {
+    __syncthreads();  // the last iteration's partials
+    if (!stopped) {  // ran to max_iters, or stopped at the last iteration (same outputs)
+      taken = p.L;
+      l21_keep = l21_prev;
+      act_keep = act_prev;
+    }
+    l21 = l21_keep;
+    act = act_keep;
   }
 
   PSTAMP(5)
@@ -1364,6 +1439,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     if (p.diverged_at) p.diverged_at[rx] = diverged ? static_cast<int32_t>(fb + (PGD ? 1 : 0)) : -1;
     if (p.l21) p.l21[rx] = diverged ? __int_as_float(0x7fc00000) : l21;
     if (p.active) p.active[rx] = diverged ? -1 : act;
+    if (RESID && p.iterations) p.iterations[rx] = taken;
     if (p.block_partials) {
       p.block_partials[rx * 3 + 0] = diverged ? 0.0 : static_cast<double>(p.alpha) * l21;
       p.block_partials[rx * 3 + 1] = diverged ? 0.0 : static_cast<double>(act);
@@ -1388,8 +1464,9 @@ template <class T>
 cudaError_t launch_mma_t(const FusedArgs& args, bool pgd, cudaStream_t s, long long* nblocks) {
   FusedArgs a = args;  // + the range summary the fast path checks once per realization
   if constexpr (T::PAIR) {
-    if (pgd && a.residual_tol > 0.f) return cudaErrorInvalidValue;  // early stop: FFMA2 team kernel
     for (int k = T::KX; k < T::K; ++k) a.c[k] = a.c[k - T::KX];  // c of the pair frame: [c; c]
+  } else if (a.residual_tol > 0.f) {
+    return cudaErrorInvalidValue;  // the early stop is built for the (8,64) pairs
   }
   a.cmax = 0.f;
   for (int k = 0; k < T::K; ++k) a.cmax = std::max(a.cmax, std::fabs(a.c[k]));
@@ -1401,6 +1478,12 @@ cudaError_t launch_mma_t(const FusedArgs& args, bool pgd, cudaStream_t s, long l
   }
   auto kern = pgd ? mma_kernel<T, true, false> : mma_kernel<T, false, false>;
   auto robust = pgd ? mma_kernel<T, true, true> : mma_kernel<T, false, true>;
+  if constexpr (T::PAIR) {
+    if (pgd && a.residual_tol > 0.f) {
+      kern = mma_kernel<T, true, false, true>;
+      robust = mma_kernel<T, true, true, true>;
+    }
+  }
   const long long ncta = T::PAIR ? (a.B + 1) / 2 : a.B;  // CTAs (PAIR: two realizations each)
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(robust, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);

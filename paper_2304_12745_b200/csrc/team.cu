@@ -803,8 +803,7 @@ cudaError_t launch_fused(const FusedArgs& a, bool pgd, int K, int M, cudaStream_
   if (K == 4 && M == 64) return launch_team<Team_4_64>(a, pgd, s, nblocks);
   if (K == 8 && M == 32) return launch_team<Team_8_32>(a, pgd, s, nblocks);
   if (K == 8 && M == 64) {
-    if (mma_supported(K, M, pgd) && !(pgd && a.residual_tol > 0.f))
-      return launch_mma(a, pgd, K, M, s, nblocks);  // mma.cu: realization pairs
+    if (mma_supported(K, M, pgd)) return launch_mma(a, pgd, K, M, s, nblocks);  // mma.cu: realization pairs
     return launch_team<Team_8_64>(a, pgd, s, nblocks);
   }
   if (K == 8 && M == 128) return launch_team<Team_8_128>(a, pgd, s, nblocks);

@@ -52,3 +52,17 @@ if len(sys.argv) > 2 and sys.argv[2] == "pgd":  # config 3: PGD-5000 (+ in-kerne
     d = (r3[1][1] - r3[0][1]).abs().flatten(1).norm(dim=1) / r3[0][1].abs().flatten(1).norm(dim=1).clamp_min(1e-30)
     print(f"cfg3 pair vs team: W rel diff max {d.max().item():.2e} median {d.median().item():.2e}; "
           f"ratio {r3[1][0] / r3[0][0]:.3f}")
+
+if len(sys.argv) > 2 and sys.argv[2] == "tol":  # config 3's data with solve_pgd's residual_tol = 1e-4
+    w3 = U.CONFIGS[3]
+    H3 = U.generate_channels_device(w3.seed_h, w3.seed_g, w3.gain_db, 0, w3.B, w3.K, w3.M)
+    r3 = {}
+    for tc in (1, 0):
+        U.set_option("tensor_cores", tc)
+        t = timeit(lambda: U.pgd_fixed(H3, w3.lambda_pgd, w3.L, w3.c, residual_tol=1e-4), reps=2)
+        o = U.pgd_fixed(H3, w3.lambda_pgd, w3.L, w3.c, residual_tol=1e-4)
+        r3[tc] = (t, o["W"].clone(), o["iterations"].cpu().numpy())
+        print(f"cfg3 tol 1e-4 tensor cores {tc}: {t:.3f} ms, mean iterations {r3[tc][2].mean():.0f}", flush=True)
+    U.set_option("tensor_cores", 1)
+    import numpy as np
+    print(f"iterations |pair - team| max {np.abs(r3[1][2] - r3[0][2]).max()}, ratio {r3[1][0] / r3[0][0]:.3f}")
