@@ -188,6 +188,12 @@ int ufpgd_gpu_solve_pgd_batch(const ufpgd_c64* H, int64_t B, int K, int M, const
  * Optional tapes (device, NULL skips): iterates[(L+1)][B][M][K],
  * tape_v[L][B][M][K] (step images), tape_norms / tape_shrink [L][B][M].
  * diverged_at: 0-based layer (index_base = 0) or 1-based iteration (1).
+ * Mode 0 with index_base 0, no residual_tol and L >= 1 runs on the fused
+ * kernels: with tapes on the team kernel's taped instance for the K <= 8
+ * shapes ((4,16), (4,32), (4,64), (8,32), (8,64), (8,128); tapes written from
+ * the registers of the layer sweep), without tapes on the unfolded forward's
+ * kernel for every fused shape. The rest runs the general kernel (exact FP32
+ * sqrt / division in the prox).
  */
 int ufpgd_gpu_layers_general(const ufpgd_c64* H, int64_t B, int K, int M, const double* eta,
                              const double* thr, int L, const double* c, int w0_mode,

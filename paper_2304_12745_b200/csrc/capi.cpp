@@ -1090,6 +1090,39 @@ int ufpgd_gpu_layers_general(const ufpgd_c64* H, int64_t B, int K, int M, const 
   DeviceGuard g(device);
   if (!g.ok) return fail(UFPGD_ECUDA, "cannot select device");
   if (B == 0) return UFPGD_OK;
+  const bool taped = iterates || tape_v || tape_norms || tape_shrink;
+  if (mode == 0 && residual_tol == 0.0 && index_base == 0 && L >= 1 &&
+      (taped ? fused_taped_supported(K, M) : fused_supported(K, M))) {
+    // the layer sweep on the fused kernels: same raw (eta, thr) per layer,
+    // layer-indexed divergence, iterations = L. With tapes: the team kernel's
+    // taped instance (K <= 8); without: the unfolded forward's own kernel
+    // for the shape (tcgen05 / tiled / team, as ufpgd_gpu_unfolded_forward).
+    FusedArgs f{};
+    f.H = reinterpret_cast<const float2*>(H);
+    f.W = reinterpret_cast<float2*>(W);
+    f.W0 = reinterpret_cast<const float2*>(W0);
+    f.diverged_at = diverged_at;
+    f.iterations = iterations;
+    f.iterates = reinterpret_cast<float2*>(iterates);
+    f.tape_v = reinterpret_cast<float2*>(tape_v);
+    f.tape_norms = tape_norms;
+    f.tape_shrink = tape_shrink;
+    f.B = B;
+    f.L = L;
+    f.w0_mode = w0_mode;
+    f.alpha = 1.f;
+    for (int k = 0; k < K; ++k) f.c[k] = static_cast<float>(c[k]);
+    for (int l = 0; l < L; ++l) {
+      f.eta[l] = static_cast<float>(eta[l]);
+      f.thr[l] = static_cast<float>(thr[l]);
+    }
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    long long nb = 0;
+    cudaError_t e = taped ? launch_fused_taped(f, K, M, s) : launch_fused(f, false, K, M, s, &nb);
+    if (e == cudaSuccess && !taped && iterations) e = launch_fill_i64(iterations, B, L, s);
+    if (e != cudaSuccess) return cuda_fail(e, "fused layer sweep");
+    return UFPGD_OK;
+  }
   if (!general_fits(K, M)) return fail(UFPGD_ENOTSUP, "(K, M) too large for the general kernel");
   GeneralArgs a{};
   a.H = reinterpret_cast<const float2*>(H);

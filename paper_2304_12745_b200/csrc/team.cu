@@ -233,14 +233,39 @@ __device__ __forceinline__ void team_stage1(const WS& w, XAcc<S>& x, const float
 // at W (no merge adds) — measured fastest at 3 warps per scheduler, against
 // 2- and 4-chain splits.
 
+// Tape rows of one layer of one realization (ForwardOptions::with_tape /
+// with_iterates, unfolded.cpp:127-143): step image V, column norms and shrink
+// factors of layer l, and iterate l + 1. Null members are not written (absent
+// tape, padding team).
+struct TapeRow {
+  float2* v;
+  float* nrm;
+  float* shr;
+  float2* it;
+};
+
+template <class S>
+__device__ __forceinline__ TapeRow tape_row(const FusedArgs& p, long long l, long long rid, bool valid) {
+  if (!valid) return TapeRow{nullptr, nullptr, nullptr, nullptr};
+  const long long o = l * p.B + rid;
+  return TapeRow{p.tape_v ? p.tape_v + o * (S::M * S::K) : nullptr, p.tape_norms ? p.tape_norms + o * S::M : nullptr,
+                 p.tape_shrink ? p.tape_shrink + o * S::M : nullptr,
+                 p.iterates ? p.iterates + (o + p.B) * (S::M * S::K) : nullptr};
+}
+
 // RESID: also accumulate sum |W_new - W|^2 and sum |W|^2 over the thread's
 // entries (user pairs packed) into dd / ss — solve_pgd's relative iterate
 // change (pgd.cpp:246-260).
-template <class S, bool STAGE1, bool STATS, class WS, bool RESID = false>
+// TAPE: also store the layer's tape rows (tr): V and the new W as 16-byte
+// user-pair units (the team's TK threads cover an antenna's K entries, so a
+// warp's stores are contiguous), the column norm sqrt(s) and the shrink factor
+// actually applied (0 when the column is cut).
+template <class S, bool STAGE1, bool STATS, class WS, bool RESID = false, bool TAPE = false>
 __device__ __forceinline__ void team_layer(WS& w, XAcc<S>& x,
                                            const float* hs, int a, int b, float eta, float thr,
                                            const float2 (&cdiag)[S::P], bool& nonfinite, float& l21,
-                                           int& act, float2* dd = nullptr, float2* ss = nullptr) {
+                                           int& act, float2* dd = nullptr, float2* ss = nullptr,
+                                           TapeRow tr = TapeRow{nullptr, nullptr, nullptr, nullptr}) {
   constexpr int AB = 2;
   static_assert(S::MB % AB == 0, "antennas are processed in pairs");
   XAcc<S> xn;
@@ -319,6 +344,21 @@ __device__ __forceinline__ void team_layer(WS& w, XAcc<S>& x,
           const float2 di = __ffma2_rn(make_float2(-1.f, -1.f), woi[u][p], nwi[p]);
           *dd = __ffma2_rn(dr, dr, __ffma2_rn(di, di, *dd));
           *ss = __ffma2_rn(wor[u][p], wor[u][p], __ffma2_rn(woi[u][p], woi[u][p], *ss));
+        }
+      }
+      if (TAPE) {
+        const int m = i * S::TM + b, ko = m * S::K + a * S::KA;
+#pragma unroll
+        for (int p = 0; p < S::P; ++p) {
+          if (tr.v)
+            stg_stream(reinterpret_cast<float4*>(tr.v + ko + 2 * p),
+                       make_float4(vr[u][p].x, vi[u][p].x, vr[u][p].y, vi[u][p].y));
+          if (tr.it)
+            stg_stream(reinterpret_cast<float4*>(tr.it + ko + 2 * p), make_float4(nwr[p].x, nwi[p].x, nwr[p].y, nwi[p].y));
+        }
+        if (a == 0) {
+          if (tr.nrm) tr.nrm[m] = sqrtf(s[u]);
+          if (tr.shr) tr.shr[m] = scale;
         }
       }
       if (STATS) {
@@ -467,7 +507,9 @@ __device__ __forceinline__ typename std::conditional<S::WSMEM, WSm<S>, WReg<S>>:
 // realization that met it keeps its W (steps 0 from then on: exactly the
 // identity) while the other team of its warp runs on, and the warp leaves the
 // loop when both have stopped.
-template <class S, bool PGD, int MAXT, int MINB, bool RESID = false>
+// TAPE (unfolded only): every layer from layer 0 through team_layer (no
+// layer-0 shortcut), with its tape rows, iterate 0 = W0 and iterations = L.
+template <class S, bool PGD, int MAXT, int MINB, bool RESID = false, bool TAPE = false>
 __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant__ FusedArgs p) {
   extern __shared__ __align__(16) float smem[];
   __shared__ double red[kFusedMaxWarps][3];
@@ -560,7 +602,22 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
   int act = 0;
   const long long L = p.L;
   long long l0 = 0;
-  if (!PGD && p.w0_mode == UFPGD_W0_ZERO && L >= 1) {
+  if constexpr (TAPE) {
+    static_assert(!PGD && !RESID, "tapes are a forward option");
+    if (valid && p.iterates) {
+      float2* it = p.iterates + rid * (S::M * S::K);
+#pragma unroll
+      for (int i = 0; i < S::MB; ++i)
+#pragma unroll
+        for (int q = 0; q < S::P; ++q) {
+          float2 wr, wi;
+          w.ld(i, q, wr, wi);
+          stg_stream(reinterpret_cast<float4*>(it + (i * S::TM + b) * S::K + a * S::KA + 2 * q),
+                     make_float4(wr.x, wi.x, wr.y, wi.y));
+        }
+    }
+  }
+  if (!PGD && !TAPE && p.w0_mode == UFPGD_W0_ZERO && L >= 1) {
     static_assert(S::MB % 2 == 0, "layer-0 path pairs antennas");
     float2 ceta[S::P];
 #pragma unroll
@@ -615,20 +672,24 @@ __global__ void __launch_bounds__(MAXT, MINB) fused_kernel(const __grid_constant
     const float eta = PGD ? eta_b : p.eta[l];
     const float thr = PGD ? thr_b : p.thr[l];
     if constexpr (S::TWO_SWEEP) {
-      team_layer<S, false, false>(w, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
+      team_layer<S, false, false, WS, false, TAPE>(w, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act, nullptr,
+                                                   nullptr, TAPE ? tape_row<S>(p, l, rid, valid) : TapeRow{});
       __syncwarp();  // scheduling fence: the next X' is built only after every prox
       team_stage1<S, true>(w, x, hs, a, b, cdiag);
     } else {
-      team_layer<S, true, false>(w, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
+      team_layer<S, true, false, WS, false, TAPE>(w, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act, nullptr,
+                                                  nullptr, TAPE ? tape_row<S>(p, l, rid, valid) : TapeRow{});
     }
     if (nonfinite && first_bad < 0) first_bad = l;
   }
   if (!RESID && L >= 1 && L > l0) {
     const float eta = PGD ? eta_b : p.eta[L - 1];
     const float thr = PGD ? thr_b : p.thr[L - 1];
-    team_layer<S, false, true>(w, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act);
+    team_layer<S, false, true, WS, false, TAPE>(w, x, hs, a, b, eta, thr, cdiag, nonfinite, l21, act, nullptr, nullptr,
+                                                TAPE ? tape_row<S>(p, L - 1, rid, valid) : TapeRow{});
     if (nonfinite && first_bad < 0) first_bad = L - 1;
   }
+  if (TAPE && valid && tl == 0 && p.iterations) p.iterations[rid] = L;  // layers_general's step count
 
   // Team-wide first divergence (min over the team, -1 = none).
   long long fb = first_bad < 0 ? LLONG_MAX : first_bad;
@@ -718,12 +779,12 @@ int pick_warps(int rpw, long long B) {
 #define UFPGD_PGD_MINB 1
 #endif
 template <class S>
-cudaError_t launch_team(const FusedArgs& a, bool pgd, cudaStream_t s, long long* nblocks) {
+cudaError_t launch_team(const FusedArgs& a, bool pgd, cudaStream_t s, long long* nblocks, bool taped = false) {
   // The unfolded kernel takes the Team's launch bounds; the PGD kernel (power
   // iteration prologue, more live state) keeps 256 x 1 (no register cap).
   auto kern = pgd ? (a.residual_tol > 0.f ? fused_kernel<S, true, UFPGD_PGD_MAXT, UFPGD_PGD_MINB, true>
                                           : fused_kernel<S, true, UFPGD_PGD_MAXT, UFPGD_PGD_MINB>)
-                  : fused_kernel<S, false, S::MAXT, S::MINB>;
+                  : taped ? fused_kernel<S, false, S::MAXT, S::MINB, false, true> : fused_kernel<S, false, S::MAXT, S::MINB>;
   const int maxt = pgd ? UFPGD_PGD_MAXT : S::MAXT;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kFusedMaxWarps * (S::SMEM_PER_WARP + S::WSMEM_PER_WARP));
@@ -772,6 +833,27 @@ using Team_8_32 = Team<8, 32, 4, 4>;
 using Team_8_128 = Team<8, 128, 4, 8, 128, 3>;
 
 }  // namespace
+
+bool fused_taped_supported(int K, int M) {
+  return (K == 4 && (M == 16 || M == 32 || M == 64)) || (K == 8 && (M == 32 || M == 64 || M == 128));
+}
+
+cudaError_t launch_fused_taped(const FusedArgs& a, int K, int M, cudaStream_t s) {
+  constexpr bool t = true;  // the taped instance
+  if (K == 4 && M == 16) return launch_team<Team_4_16>(a, false, s, nullptr, t);
+  if (K == 4 && M == 32) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (a.B / Team_4_32::R < 8LL * sms) return launch_team<Team_4_32w>(a, false, s, nullptr, t);
+    return launch_team<Team_4_32>(a, false, s, nullptr, t);
+  }
+  if (K == 4 && M == 64) return launch_team<Team_4_64>(a, false, s, nullptr, t);
+  if (K == 8 && M == 32) return launch_team<Team_8_32>(a, false, s, nullptr, t);
+  if (K == 8 && M == 64) return launch_team<Team_8_64>(a, false, s, nullptr, t);
+  if (K == 8 && M == 128) return launch_team<Team_8_128>(a, false, s, nullptr, t);
+  return cudaErrorInvalidValue;
+}
 
 bool fused_supported(int K, int M) {
   return (K == 4 && (M == 16 || M == 32 || M == 64)) || (K == 8 && (M == 32 || M == 64 || M == 128)) ||

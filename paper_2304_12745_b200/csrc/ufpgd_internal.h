@@ -32,6 +32,12 @@ struct FusedArgs {
   float cmax;             // tensor-core kernel: max |c_k| and the range of the
   float eta_lo, eta_hi;   //   per-layer steps (filled by launch_mma)
   long long prefetch_ahead;  // tensor-core kernel: L2 prefetch distance in realizations (0: none)
+  // taped team kernel (launch_fused_taped; nullable): iterates[(L+1)][B][M][K],
+  // step images tape_v[L][B][M][K], column norms / shrink factors [L][B][M]
+  float2* iterates;
+  float2* tape_v;
+  float* tape_norms;
+  float* tape_shrink;
   float c[UFPGD_MAX_USERS];
   float eta[UFPGD_MAX_LAYERS];
   float thr[UFPGD_MAX_LAYERS];
@@ -133,6 +139,10 @@ int fused_realizations_per_block(int K, int M);
 // *nblocks receives the grid size (= number of block partials written).
 cudaError_t launch_fused(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s,
                          long long* nblocks);
+// Unfolded layers with tapes / iterates (ForwardOptions, unfolded.hpp:40-62) on
+// the fused team kernel, for the K <= 8 team shapes; raw per-layer eta / thr.
+bool fused_taped_supported(int K, int M);
+cudaError_t launch_fused_taped(const FusedArgs& a, int K, int M, cudaStream_t s);
 // Tiled CTA kernels (tile.cu) for (16,128) and (32,256); launch_fused forwards there.
 cudaError_t launch_tiled(const FusedArgs& a, bool pgd, int K, int M, cudaStream_t s, long long* nblocks);
 // Tensor-core (tcgen05) unfolded forward / fixed-step PGD at (16,128), (32,256) (mma.cu);
