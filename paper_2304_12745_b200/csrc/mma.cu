@@ -58,10 +58,21 @@ namespace {
 // chain over its antennas and H rows; stage 2: one K-step against its own Bs
 // tile), and the split, drains, Bs build and prox cover only its 8 users: the
 // frame's off-diagonal blocks are never staged, multiplied or read.
+#ifndef UFPGD_MMA_DBS
+#define UFPGD_MMA_DBS 1  // 0: the F / G shared-memory exchange between the stage-1 drain and the Bs build (A/B)
+#endif
 template <int K_, int M_, int MINB_, bool PAIR_ = false>
 struct MmaShape {
   static constexpr int K = K_, M = M_, NT = M_, MINB = MINB_;
   static constexpr bool PAIR = PAIR_;
+  // DBS ("direct Bs", the M = 64 stage-1 shapes): the stage-1 operand rows are
+  // ordered q = (k / 4, part, hilo, k % 4), so TMEM lane quadrant w holds all
+  // 16 rows of users 4w .. 4w+3 and the 16x256b drain gives thread i rows
+  // i / 4 = (hilo, k % 4) of part 0 and part 1 together: the thread forms its
+  // hi- or lo-row share of X(k, .) in registers, adds its partner's (lane ^ 16:
+  // one shuffle per value) and splits / stores its Bs chunk at once. No F / G
+  // exchange through shared memory and one CTA barrier less per layer.
+  static constexpr bool DBS = (4 * K_ == 64) && UFPGD_MMA_DBS;
   static constexpr int KX = PAIR ? K_ / 2 : K_, MX = PAIR ? M_ / 2 : M_;  // per-realization users, antennas
   static_assert(!PAIR || (K_ == 16 && M_ == 128), "pairs of (8,64) realizations in the (16,128) frame");
   static constexpr int R = 2 * K;     // real-form rows (part, k)
@@ -79,7 +90,12 @@ struct MmaShape {
   // Bs builder chunk width: 4 values of an X' row per thread, or 2 when K^2/4
   // chunks would leave threads idle (chunk() maps either conflict-free).
   static constexpr int CWD = (K * K / 4 >= NT) ? 4 : 2;
-  static constexpr int BSBO = 16 * R;                    // Bs N-group stride (descriptor SBO)
+  // Bs K-group stride (descriptor LBO). DBS: 192 — the two half-warps of a
+  // put write K-groups that differ by one, and 128 + 64 bytes apart they land
+  // in different bank halves (conflict-free 4-byte stores).
+  static constexpr int BLBO = DBS ? 192 : 128;
+  static constexpr int BSBO = (R / 8) * BLBO;            // Bs N-group stride (descriptor SBO)
+  static constexpr int BSBOP = 2 * BLBO, BST = 4 * BSBOP;  // PAIR: per-realization Bs tiles (boffp())
   static constexpr int OFF_BH = OFF_W + Q * M * 2;       // Bs hi [R x R] f16, boff()
   static constexpr int OFF_BL = OFF_BH + (R / 8) * BSBO; // Bs lo (continues Bs hi along N)
   // fp32 exchange rows (floats): 4 mod 32 words at CWD 4, 8 mod 32 at CWD 2 (see chunk())
@@ -89,7 +105,7 @@ struct MmaShape {
   // PAIR: their own region after the two 1 KB Bs tiles, since the W operand
   // keeps the zeros of the other realization's users at each antenna (see the
   // shared accumulators below); 45.6 KB in all, so 5 CTAs fit an SM.
-  static constexpr int OFF_F = PAIR ? OFF_BH + 2 * 4 * 2 * 128 : OFF_W;
+  static constexpr int OFF_F = PAIR ? OFF_BH + 2 * BST : OFF_W;
   // PAIR: only the diagonal 8 x 8 blocks of P are exchanged — rows (part, k)
   // with the 16 columns (part', k' of k's realization), 16 floats per row,
   // 8-word halves swapped on rows (row >> 1) odd (fx()): conflict-free for the
@@ -97,7 +113,9 @@ struct MmaShape {
   static constexpr int FROW = PAIR ? 16 : FSTR;  // floats per exchange row
   static constexpr int OFF_G = OFF_F + R * FROW * 4;
   static_assert(2 * R * FSTR * 4 <= Q * M * 2, "");
-  static constexpr int OFF_BAR = PAIR ? OFF_G + R * FROW * 4 : OFF_BL + (R / 8) * BSBO;  // mbarriers, TMEM slot, reductions
+  // (PAIR with DBS: F is only the power iteration's 256-byte scratch)
+  static constexpr int OFF_BAR = PAIR ? (DBS ? OFF_F + 256 : OFF_G + R * FROW * 4)
+                                      : OFF_BL + (R / 8) * BSBO;  // mbarriers, TMEM slot, reductions
   // exchange-row index of P(row, col): row = (part, k), col = (part', k'), frame indices
   static __device__ __forceinline__ int fx(int row, int col) {
     if constexpr (PAIR)
@@ -149,6 +167,13 @@ struct MmaShape {
   static __device__ __forceinline__ int woff(int q, int m) {
     return (m >> 3) * (16 * Q) + (q >> 3) * 128 + (m & 7) * 16 + (q & 7) * 2;
   }
+  // Stage-1 operand row of (hilo, part, frame user k).
+  static __device__ __forceinline__ int qrow(int hl, int part, int k) {
+    if constexpr (DBS)
+      return (k >> 2) * 16 + part * 8 + hl * 4 + (k & 3);
+    else
+      return hl * R + part * K + k;
+  }
   // Bs builder chunk ch -> X' row k, columns c .. c + CWD - 1 (= Bs rows kk, column n = k).
   // CWD 4: each half-warp covers one 8 x 8 block of X' — rows k0 .. k0+7 (lanes
   // i & 7) x two 4-wide column halves (i >> 3) — so every Bs put of the half-warp
@@ -175,15 +200,14 @@ struct MmaShape {
   }
   // Bs: element (kk, n), K-major (K = kk, N = n): LBO (K-group) 128, SBO (N-group) BSBO.
   static __device__ __forceinline__ int boff(int kk, int n) {
-    return (kk >> 3) * 128 + (n >> 3) * BSBO + (n & 7) * 16 + (kk & 7) * 2;
+    return (kk >> 3) * BLBO + (n >> 3) * BSBO + (n & 7) * 16 + (kk & 7) * 2;
   }
   // PAIR: stage 2 runs one K-step per realization x (the TMEM A operand's
   // K order is r' = (x, part, k_local)), so Bs is one tile per realization:
   // [16 K-rows (p_in, k'_local) x 32 N-columns ((p_out, k_local) hi | lo)],
   // K-major, N-group stride BSBOP, tile x at x * BST, lo after the 2 hi N-groups.
-  static constexpr int BSBOP = 2 * 128, BST = 4 * BSBOP;
   static __device__ __forceinline__ int boffp(int kk, int n) {
-    return (kk >> 3) * 128 + (n >> 3) * BSBOP + (n & 7) * 16 + (kk & 7) * 2;
+    return (kk >> 3) * BLBO + (n >> 3) * BSBOP + (n & 7) * 16 + (kk & 7) * 2;
   }
   // Byte offset from OFF_BH of the (p_in, p_out) Bs entry of X'(k, c .. c+CWD-1)
   // (frame users k, c), and of its lo part from its hi part.
@@ -719,11 +743,15 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     // their own region): the other realization's stage-1 chain accumulates
     // exactly 0 onto this realization's D1 rows. Ordered before the first
     // stage-1 MMA by the split's fence and barrier.
+    // (8-row chunks: DBS (quadrant, part) of the other realization's two
+    // quadrants, else (hilo, part) of its 8 users)
 #pragma unroll
     for (int hl = 0; hl < 2; ++hl)
 #pragma unroll
       for (int part = 0; part < 2; ++part)
-        *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(hl * R + part * K + T::KX * (1 - hx), m)) =
+        *reinterpret_cast<uint4*>(smem + T::OFF_W +
+                                  T::woff(T::DBS ? T::qrow(0, part, T::KX * (1 - hx) + 4 * hl)
+                                                 : T::qrow(hl, part, T::KX * (1 - hx)), m)) =
             make_uint4(0u, 0u, 0u, 0u);
   }
   int aW = 0;        // robust path: the W registers hold W_s 2^-aW ...
@@ -820,6 +848,12 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       ts *= pow2i(-aW);
     }
     float fstep = -(PGD ? eta_b : p.eta[l]) * g2inv;  // -eta / g^2 folded into Bs
+    // DBS: the thread's Bs chunk of X, straight from the stage-1 drain. Lane i
+    // of warp w: X row k = 4w + (i / 4) % 4, hl = i / 16. Full frame: columns
+    // c = 2 (i % 4) + 8 hl, dx = (Xr(k,c), Xr(k,c+1), Xi(k,c), Xi(k,c+1)).
+    // PAIR: columns c = 2 (i % 4) of k's realization, dx[0..1] = Xr (hl 0) or
+    // Xi (hl 1) of (k, c), (k, c+1).
+    float dx[4] = {0.f, 0.f, 0.f, 0.f};
     if (!xzero) {
       // W operand rows q = (hilo, part, k) from the thread's antenna column
 #pragma unroll
@@ -830,8 +864,17 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         uint32_t h[4], lo[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) split2(src[2 * u], src[2 * u + 1], h[u], lo[u]);
+        if constexpr (T::DBS) {
+          // 8-row chunk (quadrant k / 4, part) = [hi k..k+3 | lo k..k+3]
+          const int kf = 8 * kg + (T::PAIR ? T::KX * hx : 0);
+          *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(T::qrow(0, part, kf), m)) =
+              make_uint4(h[0], h[1], lo[0], lo[1]);
+          *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(T::qrow(0, part, kf + 4), m)) =
+              make_uint4(h[2], h[3], lo[2], lo[3]);
+        } else {
         *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(q0, m)) = make_uint4(h[0], h[1], h[2], h[3]);
         *reinterpret_cast<uint4*>(smem + T::OFF_W + T::woff(R + q0, m)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
       }
       fence_async_smem();
       tc_fence_before();
@@ -929,7 +972,56 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         const int r0 = part * K + kr;
         float* d0 = FG + r0 * T::FSTR + cp;
         float a[16], b[16];
-        if constexpr (T::PAIR) {
+        if constexpr (T::DBS) {
+          // Thread i holds rows (hl, k % 4) = i / 4 of part 0 (a[4j], a[4j+1]) and
+          // part 1 (a[4j+2], a[4j+3]) at columns 8 j + 2 (i % 4) + {0, 1}.
+          // Row value = A + 2^-11 B on a hi row (B: the product with H_lo),
+          // 2^-11 A on a lo row; X is linear in the rows, so the part / p'
+          // combinations are formed on A and B first:
+          //   Xr = P[(0,k),(0,k')] - P[(1,k),(1,k')], Xi = P[(0,k),(1,k')] + P[(1,k),(0,k')]
+          const bool lo_row = lane >= 16;
+          const float sa = lo_row ? kLoScale : 1.f, sb = lo_row ? 0.f : kLoScale;
+          auto pr = [](const float* v, int i) { return make_float2(v[i], v[i + 1]); };
+          if constexpr (T::PAIR) {
+            // 32 columns [hi p'0 | hi p'1 | lo p'0 | lo p'1] of the 8 users k'
+            // of the warp's realization (robust instance: at 32 x)
+            tmem_ld16x256(tmem + lrow + T::T_D1A + (SH ? 0 : 32 * (warp >> 1)), a);
+            tmem_wait<16>(a);
+            const float2 ar = ffma2(-1.f, pr(a, 6), pr(a, 0)), ai = fadd2(pr(a, 4), pr(a, 2));
+            const float2 br = ffma2(-1.f, pr(a, 14), pr(a, 8)), bi = fadd2(pr(a, 12), pr(a, 10));
+            const float2 xr = ffma2(sb, br, fmul2(sa, ar)), xi = ffma2(sb, bi, fmul2(sa, ai));
+            // the hi-row lane takes Xr, the lo-row lane Xi: each sends the other its share
+            const float2 give = lo_row ? xr : xi, keep = lo_row ? xi : xr;
+            const float2 got = make_float2(__shfl_xor_sync(kFull, give.x, 16), __shfl_xor_sync(kFull, give.y, 16));
+            const float2 t = fadd2(keep, got);
+            dx[0] = t.x;
+            dx[1] = t.y;
+          } else {
+            // columns [H_hi: p'0 (16 users) | p'1] in D1A, the same with H_lo in D1B;
+            // j = 0, 1: p'0 at k' = 2 (i % 4) + {0, 1} and 8 more, j = 2, 3: p'1
+            tmem_ld16x256(tmem + lrow + T::T_D1A, a);
+            tmem_ld16x256(tmem + lrow + T::T_D1B, b);
+            tmem_wait<16>(a);
+            tmem_wait<16>(b);
+            float2 xr[2], xi[2];  // column chunks c = 2 (i % 4) and 8 more
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const float2 ar = ffma2(-1.f, pr(a, 10 + 4 * h), pr(a, 4 * h)), ai = fadd2(pr(a, 8 + 4 * h), pr(a, 2 + 4 * h));
+              const float2 br = ffma2(-1.f, pr(b, 10 + 4 * h), pr(b, 4 * h)), bi = fadd2(pr(b, 8 + 4 * h), pr(b, 2 + 4 * h));
+              xr[h] = ffma2(sb, br, fmul2(sa, ar));
+              xi[h] = ffma2(sb, bi, fmul2(sa, ai));
+            }
+            // the hi-row lane takes chunk 0, the lo-row lane chunk 1
+            const float2 gr = lo_row ? xr[0] : xr[1], gi = lo_row ? xi[0] : xi[1];
+            const float2 kr = lo_row ? xr[1] : xr[0], ki = lo_row ? xi[1] : xi[0];
+            const float2 tr = fadd2(kr, make_float2(__shfl_xor_sync(kFull, gr.x, 16), __shfl_xor_sync(kFull, gr.y, 16)));
+            const float2 ti = fadd2(ki, make_float2(__shfl_xor_sync(kFull, gi.x, 16), __shfl_xor_sync(kFull, gi.y, 16)));
+            dx[0] = tr.x;
+            dx[1] = tr.y;
+            dx[2] = ti.x;
+            dx[3] = ti.y;
+          }
+        } else if constexpr (T::PAIR) {
           // D1 columns [0, 32) hold each row's realization's [hi p0 | hi p1 |
           // lo p0 | lo p1]: one 16x256b load carries row kr (a) and kr + 8 (b). F / G get
           // the same entries as the full-frame layout: (row kr, columns cp, K + cp),
@@ -1008,7 +1100,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         }
       }
       }
-      __syncthreads();
+      if constexpr (!T::DBS) __syncthreads();  // F / G complete (DBS: the chunk is in registers)
     }
     TSTAMP(4)
     // Bs[(p_in, k')][(p_out, k)] = -eta/g^2 * { X'r, X'i ; X'i, -X'r }(k, k'), one
@@ -1016,7 +1108,65 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
     // CWD-wide chunks of X' row k per thread (CWD = 4, or 2 when K / 4 chunks per
     // row would leave threads idle; 2-wide keeps a quarter-warp on one F row)
     int aB = 0;  // robust path: Bs is built as Bs 2^-aB
-    if constexpr (!RB) {
+    if constexpr (T::DBS) {
+      // The thread's chunk of X is in dx (see above): X' = X - diag(c), times
+      // -eta / g^2, split and stored. Robust path: the P rows are X 2^-aW, so
+      // X' 2^-aW = P - c 2^-aW, and the chunk values become Bs 2^-aB with aB
+      // from their exact CTA maximum (PAIR: over the realization's two warps).
+      constexpr int NV = T::PAIR ? 2 : 4;
+      const bool lo_row = lane >= 16;
+      const int k = 4 * warp + ((lane >> 2) & 3);
+      const int c = T::PAIR ? T::KX * (warp >> 1) + 2 * (lane & 3) : 2 * (lane & 3) + (lo_row ? 8 : 0);
+      const float cscale = RB ? pow2i(-aW) : 1.f, fstep_w = RB ? fstep * pow2i(aW) : fstep;
+      if (!T::PAIR || !lo_row) {  // the Xr values
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (c + u == k) dx[u] -= RB ? p.c[k] * cscale : p.c[k];
+      }
+#pragma unroll
+      for (int u = 0; u < NV; ++u) dx[u] *= fstep_w;
+      if constexpr (RB) {
+        float bm = 0.f;
+#pragma unroll
+        for (int u = 0; u < NV; ++u) bm = fmaxf(bm, fabsf(dx[u]));
+        if (!(bm <= FLT_MAX)) bm = __int_as_float(0x7f800000);
+        bm = __uint_as_float(__reduce_max_sync(kFull, __float_as_uint(bm)));
+        if (lane == 0) redw[warp] = bm;
+        __syncthreads();
+        float mb = 0.f;
+#pragma unroll
+        for (int w = hx * NWX; w < (hx + 1) * NWX; ++w) mb = fmaxf(mb, redw[w]);  // PAIR: its block's warps
+        if (mb > 0.f && mb < FLT_MAX) aB = ilogbf(mb) - 12;  // Bs 2^-aB in [2^12, 2^13)
+        const float f = pow2i(-aB);
+#pragma unroll
+        for (int u = 0; u < NV; ++u) dx[u] *= f;
+      }
+      auto put = [&](int off, uint32_t v) { *reinterpret_cast<uint32_t*>(smem + off) = v; };
+      // (p_in, p_out) = (0,0): X'r, (1,0): X'i, (0,1): X'i, (1,1): -X'r (f16 negation is exact)
+      if constexpr (T::PAIR) {
+        uint32_t vh, vl;
+        split2(dx[0], dx[1], vh, vl);
+        const uint32_t neg = lo_row ? 0u : 0x80008000u;
+        const int o1 = T::OFF_BH + (lo_row ? T::bpos(1, 0, k, c) : T::bpos(0, 0, k, c));
+        const int o2 = T::OFF_BH + (lo_row ? T::bpos(0, 1, k, c) : T::bpos(1, 1, k, c));
+        put(o1, vh);
+        put(o1 + T::BLO, vl);
+        put(o2, vh ^ neg);
+        put(o2 + T::BLO, vl ^ neg);
+      } else {
+        uint32_t rh, rl, ih, il;
+        split2(dx[0], dx[1], rh, rl);
+        split2(dx[2], dx[3], ih, il);
+        put(T::OFF_BH + T::bpos(0, 0, k, c), rh);
+        put(T::OFF_BH + T::BLO + T::bpos(0, 0, k, c), rl);
+        put(T::OFF_BH + T::bpos(1, 0, k, c), ih);
+        put(T::OFF_BH + T::BLO + T::bpos(1, 0, k, c), il);
+        put(T::OFF_BH + T::bpos(0, 1, k, c), ih);
+        put(T::OFF_BH + T::BLO + T::bpos(0, 1, k, c), il);
+        put(T::OFF_BH + T::bpos(1, 1, k, c), rh ^ 0x80008000u);
+        put(T::OFF_BH + T::BLO + T::bpos(1, 1, k, c), rl ^ 0x80008000u);
+      }
+    } else if constexpr (!RB) {
       constexpr int CWD = T::CWD, NCH = K * K / CWD, CPR = K / CWD;
       using FV = typename std::conditional<CWD == 4, float4, float2>::type;
   #pragma unroll
@@ -1196,7 +1346,7 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       const int t = wu >> 2;  // = tile, warp-uniform
       const uint32_t dm = tmem + T::T_D2 + t * 2 * R, dc = dm + R;
       const uint32_t ta = tmem + THA + t * R;  // H_hi columns; H_lo at + R / 2
-      const uint32_t bhlo = sdesc_lo(sb + T::OFF_BH, 128);
+      const uint32_t bhlo = sdesc_lo(sb + T::OFF_BH, T::BLBO);
       if constexpr (T::PAIR) {
         // realization x: its K-step of A (8 TMEM columns of H hi / lo; zeros in
         // the other realization's lanes) against its Bs tile, both into D2
@@ -1214,11 +1364,11 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         // [main | corr] = H_hi [Bs_hi | Bs_lo] (N = 2R spans both), then corr += H_lo Bs_hi;
         // a K16 step of A is 8 TMEM columns (f16 pairs)
         if constexpr (T::NTILE == 1) {
-          const uint32_t bh = bhlo + ks * (256 >> 4);
+          const uint32_t bh = bhlo + ks * (2 * T::BLBO >> 4);
           umma_f16_ta(dm, ta + ks * 8, bh, sdesc_hi(T::BSBO), IDESC2W, ks > 0);
           umma_f16_ta(dc, ta + R / 2 + ks * 8, bh, sdesc_hi(T::BSBO), IDESC2, 1);
         } else {
-          const uint64_t bh = sdesc(sb + T::OFF_BH + ks * 256, 128, T::BSBO);
+          const uint64_t bh = sdesc(sb + T::OFF_BH + ks * 2 * T::BLBO, T::BLBO, T::BSBO);
           umma_f16_ta(dm, ta + ks * 8, bh, IDESC2W, ks > 0);
           umma_f16_ta(dc, ta + R / 2 + ks * 8, bh, IDESC2, 1);
         }
