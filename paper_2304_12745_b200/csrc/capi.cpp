@@ -446,7 +446,9 @@ struct HostWorkspace {
     float* user_eta = nullptr;
     double* user_stats = nullptr;
     int64_t B = 0;
+    std::vector<cudaEvent_t> tev;  // UFPGD_OPT_HOST_TIMELINE = 2: printed by host_finish
   } calls[NC];
+  cudaEvent_t tbase = nullptr;     // ... relative to the first such call's start
 };
 HostWorkspace g_ws[64];
 
@@ -520,6 +522,18 @@ int host_finish(int64_t ticket) {
     if (!c->busy || (c->gen & 0xFFFF) != gen) return fail(UFPGD_EINVAL_PARAM, "host-call ticket already completed");
   }
   cudaError_t e = cudaEventSynchronize(c->done);
+  if (!c->tev.empty()) {  // deferred timeline (tuning aid): no synchronisation inside the enqueue
+    const size_t nchunks = c->tev.size() / 4;
+    for (size_t ci = 0; ci < nchunks; ++ci) {
+      float t[4];
+      for (int q = 0; q < 4; ++q) cudaEventElapsedTime(&t[q], ws.tbase, c->tev[4 * ci + q]);
+      std::fprintf(stderr, "slot %d chunk %3zu  h2d %7.3f-%7.3f  kernel -%7.3f  d2h -%7.3f ms\n", slot, ci, t[0], t[1],
+                   t[2], t[3]);
+    }
+    for (cudaEvent_t ev : c->tev)
+      if (ev != ws.tbase) cudaEventDestroy(ev);
+    c->tev.clear();
+  }
   double host_stats[3] = {0.0, 0.0, 0.0};
   if (e == cudaSuccess) {
     const char* base = static_cast<const char*>(c->pinned);
@@ -598,7 +612,6 @@ int host_enqueue(int device, const ufpgd_c64* H, int64_t B, int K, int M, const 
     e = ensure(pp, call.partials_cap, sizeof(double) * 3 * std::max<long long>(1, parts_per_chunk_max * nchunks));
     call.partials = static_cast<double*>(pp);
   }
-  if (e == cudaSuccess && !call.dstats) e = cudaMalloc(&call.dstats, sizeof(double) * 3);
   const size_t small_need = 64 + (diverged_at ? sizeof(int32_t) * B : 0) + (eta_out ? sizeof(float) * B : 0);
   if (e == cudaSuccess && small_need > call.pinned_cap) {
     if (call.pinned) cudaFreeHost(call.pinned);
@@ -624,7 +637,10 @@ int host_enqueue(int device, const ufpgd_c64* H, int64_t B, int K, int M, const 
   // depth-first pipeline over four streams, for A/B runs.
   const bool phased = option(UFPGD_OPT_HOST_PIPE) == 0;
   // UFPGD_OPT_HOST_TIMELINE = 1: per-chunk event timeline on stderr (tuning aid)
+  // (= 2: deferred — printed by host_finish against the first call's start, so
+  // the overlap of streamed calls shows)
   const bool timeline = option(UFPGD_OPT_HOST_TIMELINE) != 0;
+  const bool timeline_deferred = option(UFPGD_OPT_HOST_TIMELINE) == 2;
   std::vector<cudaEvent_t> tev(timeline ? 4 * nchunks : 0);
   for (cudaEvent_t& ev : tev) cudaEventCreate(&ev);
   // Chunk ci uses buffer set set_of[ci] (a rotation that continues across
@@ -749,13 +765,20 @@ int host_enqueue(int device, const ufpgd_c64* H, int64_t B, int K, int M, const 
       cudaEventDestroy(j);
     }
   if (rc == UFPGD_OK) {
-    e = launch_stats_finalize(call.partials, part_off[nchunks], call.dstats, ws.st[0]);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(stats_stage, call.dstats, sizeof(double) * 3, cudaMemcpyDeviceToHost, ws.st[0]);
+    // The finalisation kernel stores the three statistics straight into the
+    // pinned slot (UVA: pinned host memory is device-addressable). A 24-byte
+    // cudaMemcpyAsync here would sit in a copy-engine queue until this call's
+    // last chunk is done, and the next streamed call's H2D copies queue up
+    // behind it on the same engine: measured as every third streamed call
+    // running ~7 ms instead of 5.6 (tools/e2e_periods.py, host_timeline2.py).
+    e = launch_stats_finalize(call.partials, part_off[nchunks], stats_stage, ws.st[0]);
     if (e == cudaSuccess) e = cudaEventRecord(call.done, ws.st[0]);
     if (e != cudaSuccess) rc = cuda_fail(e, "host pipeline finalize");
   }
-  if (timeline) {
+  if (timeline_deferred && rc == UFPGD_OK) {
+    if (!ws.tbase && !tev.empty()) ws.tbase = tev[0];
+    call.tev = std::move(tev);
+  } else if (timeline) {
     cudaStreamSynchronize(ws.st[0]);
     for (int64_t ci = 0; ci < nchunks; ++ci) {
       float t[4];
@@ -803,8 +826,8 @@ int ufpgd_gpu_set_option(int option, int64_t value) {
     case UFPGD_OPT_TENSOR_CORES:
     case UFPGD_OPT_FP64_TEAM:
     case UFPGD_OPT_ZERO_PAD:
-    case UFPGD_OPT_HOST_PIPE:
-    case UFPGD_OPT_HOST_TIMELINE: ok = value == 0 || value == 1; break;
+    case UFPGD_OPT_HOST_PIPE: ok = value == 0 || value == 1; break;
+    case UFPGD_OPT_HOST_TIMELINE: ok = value >= 0 && value <= 2; break;
     case UFPGD_OPT_FUSED_WARPS: ok = value >= 0 && value <= 8; break;
     case UFPGD_OPT_PAD_SUB_BYTES:
     case UFPGD_OPT_HOST_CHUNK_BYTES: ok = value >= (1ll << 20) && value <= (1ll << 40); break;

@@ -105,7 +105,9 @@ struct MmaShape {
   // PAIR: their own region after the two 1 KB Bs tiles, since the W operand
   // keeps the zeros of the other realization's users at each antenna (see the
   // shared accumulators below); 45.6 KB in all, so 5 CTAs fit an SM.
-  static constexpr int OFF_F = PAIR ? OFF_BH + 2 * BST : OFF_W;
+  // (PAIR with DBS: F is only the power iteration's 256-byte scratch and
+  // aliases the Bs tiles, which are first written in the layer loop)
+  static constexpr int OFF_F = PAIR ? (DBS ? OFF_BH : OFF_BH + 2 * BST) : OFF_W;
   // PAIR: only the diagonal 8 x 8 blocks of P are exchanged — rows (part, k)
   // with the 16 columns (part', k' of k's realization), 16 floats per row,
   // 8-word halves swapped on rows (row >> 1) odd (fx()): conflict-free for the
@@ -113,8 +115,7 @@ struct MmaShape {
   static constexpr int FROW = PAIR ? 16 : FSTR;  // floats per exchange row
   static constexpr int OFF_G = OFF_F + R * FROW * 4;
   static_assert(2 * R * FSTR * 4 <= Q * M * 2, "");
-  // (PAIR with DBS: F is only the power iteration's 256-byte scratch)
-  static constexpr int OFF_BAR = PAIR ? (DBS ? OFF_F + 256 : OFF_G + R * FROW * 4)
+  static constexpr int OFF_BAR = PAIR ? (DBS ? OFF_BH + 2 * BST : OFF_G + R * FROW * 4)
                                       : OFF_BL + (R / 8) * BSBO;  // mbarriers, TMEM slot, reductions
   // exchange-row index of P(row, col): row = (part, k), col = (part', k'), frame indices
   static __device__ __forceinline__ int fx(int row, int col) {
