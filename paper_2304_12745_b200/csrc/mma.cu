@@ -818,6 +818,22 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   float wor[RESID ? KT : 1], woi[RESID ? KT : 1];  // W before the iteration's update
   (void)wor;
   (void)woi;
+#ifndef UFPGD_MMA_CDIAG
+#define UFPGD_MMA_CDIAG 1  // 0: the diagonal test and c[k] load inside the layer loop (A/B)
+#endif
+  // DBS fast path: the thread's share of diag(c) in its Bs chunk (see the Bs
+  // build), fixed for the realization: c[k] where chunk column c + u is the
+  // row's own user k (and the chunk holds Xr), else 0.
+  float cdg[2] = {0.f, 0.f};
+  if constexpr (T::DBS && !RB && UFPGD_MMA_CDIAG) {
+    const int k = 4 * warp + ((lane >> 2) & 3);
+    const int c = T::PAIR ? T::KX * (warp >> 1) + 2 * (lane & 3) : 2 * (lane & 3) + (lane >= 16 ? 8 : 0);
+    if (!T::PAIR || lane < 16) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (c + u == k) cdg[u] = p.c[k];
+    }
+  }
   for (long long l = 0; l < p.L; ++l) {
     TSTAMP(0)
     const bool xzero = (l == 0 && p.w0_mode == UFPGD_W0_ZERO);
@@ -1119,7 +1135,10 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
       const int k = 4 * warp + ((lane >> 2) & 3);
       const int c = T::PAIR ? T::KX * (warp >> 1) + 2 * (lane & 3) : 2 * (lane & 3) + (lo_row ? 8 : 0);
       const float cscale = RB ? pow2i(-aW) : 1.f, fstep_w = RB ? fstep * pow2i(aW) : fstep;
-      if (!T::PAIR || !lo_row) {  // the Xr values
+      if constexpr (!RB && UFPGD_MMA_CDIAG) {
+        dx[0] -= cdg[0];  // x - 0 is exact: the same values as the in-loop test
+        dx[1] -= cdg[1];
+      } else if (!T::PAIR || !lo_row) {  // the Xr values
 #pragma unroll
         for (int u = 0; u < 2; ++u)
           if (c + u == k) dx[u] -= RB ? p.c[k] * cscale : p.c[k];

@@ -80,3 +80,34 @@ def test_async_divergence_is_reported_at_wait():
         call.wait()
     assert ei.value.index == 0
     assert list(call.diverged_at) == [-1, 0, -1]
+
+
+def test_streamed_calls_report_divergence_per_chunk_and_statistics():
+    """diverged_at and the statistics reach the host by direct stores into the
+    call's pinned stage (no copy-engine op): diverging realizations in several
+    pipeline chunks of back-to-back streamed calls must come out exactly as on
+    the device path, and a clean call in between must not see them."""
+    w = U.CONFIGS[2]
+    lam, eta = w.layer_params()
+    B = 3 * 4096 + 77  # four 16 MiB chunks at (8,64)
+    clean = U.make_inputs(w, 0, B)
+    bad = clean.copy()
+    idx = [5, 4095, 4096, 9000, B - 1]
+    for i in idx:
+        bad[i, 0, 0] = np.complex64(complex(float("nan"), 0.0))
+    clean, bad = _pinned(clean), _pinned(bad)
+    dev_div = U.unfolded_forward(torch.from_numpy(bad).cuda(), lam, eta, w.c)["diverged_at"].cpu().numpy()
+    assert sorted(np.nonzero(dev_div >= 0)[0].tolist()) == idx
+    ref = U.unfolded_forward_host(bad, lam, eta, w.c, raise_on_divergence=False)
+    assert np.array_equal(ref["diverged_at"], dev_div) and ref["stats"][2] == len(idx)
+    calls = [U.unfolded_forward_host_async(h, lam, eta, w.c) for h in (bad, clean, bad)]
+    for k, c in enumerate(calls):
+        if k == 1:
+            r = c.wait()
+            assert (r["diverged_at"] == -1).all() and r["stats"][2] == 0.0
+            continue
+        with pytest.raises(U.DivergenceError) as ei:
+            c.wait()
+        assert ei.value.index == 0  # the layer of the first non-finite iterate (NaN channel: layer 0)
+        assert np.array_equal(np.asarray(c.diverged_at), dev_div)
+        assert np.array_equal(np.asarray(c.stats), np.asarray(ref["stats"]), equal_nan=True)
