@@ -825,15 +825,32 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   // build), fixed for the realization: c[k] where chunk column c + u is the
   // row's own user k (and the chunk holds Xr), else 0.
   float cdg[2] = {0.f, 0.f};
-  if constexpr (T::DBS && !RB && UFPGD_MMA_CDIAG) {
+  // ... and the byte offsets of its Bs puts (PAIR: the hi-row lane stores the
+  // (0,0) and (1,1) entries, the lo-row lane (1,0) and (0,1); full frame: the
+  // other three entries are compile-time offsets from (0,0)).
+  // Kept in registers across the layers where measured faster: the full frame
+  // (config 5: 3.429 -> 3.397 ms per 65,536) and the PGD pairs (config 3:
+  // 14.2 -> 13.65 ms); the unfolded pairs at their 72-register cap recompute
+  // them per layer (0.965 vs 0.997 ms hoisted).
+  constexpr bool HOIST_BO = UFPGD_MMA_CDIAG && (!T::PAIR || PGD);
+  int bo1 = 0, bo2 = 0;
+  if constexpr (T::DBS && UFPGD_MMA_CDIAG) {
     const int k = 4 * warp + ((lane >> 2) & 3);
     const int c = T::PAIR ? T::KX * (warp >> 1) + 2 * (lane & 3) : 2 * (lane & 3) + (lane >= 16 ? 8 : 0);
-    if (!T::PAIR || lane < 16) {
+    if (!RB && (!T::PAIR || lane < 16)) {
 #pragma unroll
       for (int u = 0; u < 2; ++u)
         if (c + u == k) cdg[u] = p.c[k];
     }
+    if constexpr (HOIST_BO && T::PAIR) {
+      bo1 = T::OFF_BH + (lane >= 16 ? T::bpos(1, 0, k, c) : T::bpos(0, 0, k, c));
+      bo2 = T::OFF_BH + (lane >= 16 ? T::bpos(0, 1, k, c) : T::bpos(1, 1, k, c));
+    } else if constexpr (HOIST_BO) {
+      bo1 = T::OFF_BH + T::bpos(0, 0, k, c);
+    }
   }
+  (void)bo1;
+  (void)bo2;
   for (long long l = 0; l < p.L; ++l) {
     TSTAMP(0)
     const bool xzero = (l == 0 && p.w0_mode == UFPGD_W0_ZERO);
@@ -1167,8 +1184,8 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         uint32_t vh, vl;
         split2(dx[0], dx[1], vh, vl);
         const uint32_t neg = lo_row ? 0u : 0x80008000u;
-        const int o1 = T::OFF_BH + (lo_row ? T::bpos(1, 0, k, c) : T::bpos(0, 0, k, c));
-        const int o2 = T::OFF_BH + (lo_row ? T::bpos(0, 1, k, c) : T::bpos(1, 1, k, c));
+        const int o1 = HOIST_BO ? bo1 : T::OFF_BH + (lo_row ? T::bpos(1, 0, k, c) : T::bpos(0, 0, k, c));
+        const int o2 = HOIST_BO ? bo2 : T::OFF_BH + (lo_row ? T::bpos(0, 1, k, c) : T::bpos(1, 1, k, c));
         put(o1, vh);
         put(o1 + T::BLO, vl);
         put(o2, vh ^ neg);
@@ -1177,14 +1194,17 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         uint32_t rh, rl, ih, il;
         split2(dx[0], dx[1], rh, rl);
         split2(dx[2], dx[3], ih, il);
-        put(T::OFF_BH + T::bpos(0, 0, k, c), rh);
-        put(T::OFF_BH + T::BLO + T::bpos(0, 0, k, c), rl);
-        put(T::OFF_BH + T::bpos(1, 0, k, c), ih);
-        put(T::OFF_BH + T::BLO + T::bpos(1, 0, k, c), il);
-        put(T::OFF_BH + T::bpos(0, 1, k, c), ih);
-        put(T::OFF_BH + T::BLO + T::bpos(0, 1, k, c), il);
-        put(T::OFF_BH + T::bpos(1, 1, k, c), rh ^ 0x80008000u);
-        put(T::OFF_BH + T::BLO + T::bpos(1, 1, k, c), rl ^ 0x80008000u);
+        // bpos(pin, pout, k, c) = bpos(0, 0, k, c) + pin (K / 8) BLBO + pout (K / 8) BSBO
+        constexpr int DI = (K / 8) * T::BLBO, DO = (K / 8) * T::BSBO;
+        const int o0 = HOIST_BO ? bo1 : T::OFF_BH + T::bpos(0, 0, k, c);
+        put(o0, rh);
+        put(o0 + T::BLO, rl);
+        put(o0 + DI, ih);
+        put(o0 + DI + T::BLO, il);
+        put(o0 + DO, ih);
+        put(o0 + DO + T::BLO, il);
+        put(o0 + DI + DO, rh ^ 0x80008000u);
+        put(o0 + DI + DO + T::BLO, rl ^ 0x80008000u);
       }
     } else if constexpr (!RB) {
       constexpr int CWD = T::CWD, NCH = K * K / CWD, CPR = K / CWD;
