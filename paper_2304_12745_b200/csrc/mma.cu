@@ -851,6 +851,20 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
   }
   (void)bo1;
   (void)bo2;
+#ifndef UFPGD_MMA_CDQ
+#define UFPGD_MMA_CDQ 1  // 0: (32,256) tests c + u == k and loads c[k] in every layer (A/B)
+#endif
+  // The exchange-path Bs build with one chunk per thread ((32,256)): the same
+  // share of diag(c) for the thread's 4-wide chunk of X' row k.
+  constexpr bool CDQ = UFPGD_MMA_CDQ && !T::DBS && !RB && !T::PAIR && (K * K / T::CWD == T::NT);
+  float cdq[CDQ ? T::CWD : 1];
+  if constexpr (CDQ) {
+    int k, c;
+    T::chunk(tid, k, c);
+#pragma unroll
+    for (int u = 0; u < T::CWD; ++u) cdq[u] = (c + u == k) ? p.c[k] : 0.f;
+  }
+  (void)cdq;
   for (long long l = 0; l < p.L; ++l) {
     TSTAMP(0)
     const bool xzero = (l == 0 && p.w0_mode == UFPGD_W0_ZERO);
@@ -1246,7 +1260,11 @@ __global__ void __launch_bounds__(T::NT, RB ? 1 : T::MINB)
         }
   #pragma unroll
         for (int u = 0; u < CWD; ++u) {
-          if (c + u == k) xr[u] -= p.c[k];  // X' = X - diag(c)
+          if constexpr (CDQ) {
+            xr[u] -= cdq[u];  // X' = X - diag(c): the thread's share, set before the loop
+          } else {
+            if (c + u == k) xr[u] -= p.c[k];
+          }
           xr[u] *= fstep;
           xi[u] *= fstep;
         }
