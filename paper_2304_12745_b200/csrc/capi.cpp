@@ -617,6 +617,9 @@ int host_enqueue(int device, const ufpgd_c64* H, int64_t B, int K, int M, const 
     if (call.pinned) cudaFreeHost(call.pinned);
     call.pinned = nullptr;
     call.pinned_cap = 0;
+    // (default flags: under unified addressing every cudaHostAlloc allocation is
+    // portable and device-addressable at its host address — the kernels store
+    // diverged_at and the statistics into it)
     e = cudaHostAlloc(&call.pinned, small_need, cudaHostAllocDefault);
     if (e == cudaSuccess) call.pinned_cap = small_need;
   }
